@@ -1,0 +1,292 @@
+/*
+ * auxmc_gpu.h — C ABI of the B200-native hot path of auxmc 0.1.0 (arXiv 2303.00301).
+ *
+ * The reference (/root/reference/proj) is a C++20 + Eigen library with no FFI
+ * layer.  Its seams are free functions; each entry point below
+ * replaces one of them in batched form (C chains / B independent problems) and
+ * cites the reference interface it stands for.  INTEGRATION.md shows the
+ * binding a maintainer would add on the reference side.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no C++ or torch types.
+ *  - Array arguments are DEVICE pointers unless the name ends in `_host`.
+ *  - Row-major dense matrices of double.  Batched arrays are batch-major:
+ *    trajectories [B][T+1][dx], filter moments [B][T+1][dx] and [B][T+1][dx][dx].
+ *  - Every call is asynchronous on the given stream (cudaStream_t passed as
+ *    void*; NULL = legacy default stream) unless documented otherwise.
+ *  - Return value: AUXMC_OK or an AUXMC_E_* code.  Exceptions of the reference
+ *    (common.hpp:17-43) become codes; per-chain failures inside a batched call
+ *    are reported through per-item status arrays, never by aborting the batch.
+ *  - There is no CPU fallback: on a machine without a usable sm_100 device every
+ *    compute entry point returns AUXMC_E_CUDA.
+ */
+#ifndef AUXMC_GPU_H
+#define AUXMC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (common.hpp:17-43) ---- */
+#define AUXMC_OK 0
+#define AUXMC_E_DIM 1          /* DimensionError */
+#define AUXMC_E_FACTOR 2       /* FactorizationError */
+#define AUXMC_E_DEGENERATE 3   /* DegenerateWeightsError */
+#define AUXMC_E_CONTRACT 4     /* ContractError */
+#define AUXMC_E_CONFIG 5       /* ConfigError */
+#define AUXMC_E_CUDA 6         /* no device / launch failure */
+#define AUXMC_E_ARG 7          /* invalid argument (null pointer, bad size) */
+#define AUXMC_E_WORKSPACE 8    /* workspace too small */
+
+/* ---- stream labels (rng.hpp:14-30) ---- */
+#define AUXMC_L_BACKWARD_NOISE 1
+#define AUXMC_L_TERMINAL_DRAW 2
+#define AUXMC_L_AUX_OBS 3
+#define AUXMC_L_DNC_BRIDGE 4
+#define AUXMC_L_MH_ACCEPT 5
+#define AUXMC_L_ITERATION 6
+#define AUXMC_L_CHAIN 7
+#define AUXMC_L_STEP 8
+#define AUXMC_L_PARTICLE 9
+#define AUXMC_L_RESAMPLE 10
+#define AUXMC_L_TERMINAL_INDEX 11
+#define AUXMC_L_BACKWARD_INDEX 12
+#define AUXMC_L_PM_KEY 13
+#define AUXMC_L_SIMULATE 14
+#define AUXMC_L_PARAM 15
+
+const char* auxmc_version(void);             /* version.hpp kVersion "0.1.0" */
+const char* auxmc_status_string(int status);
+/* 1 if a CUDA device with compute capability 10.x is usable, else 0. */
+int auxmc_device_ok(void);
+/* Last CUDA error text recorded by the library (thread-local). */
+const char* auxmc_last_error(void);
+/* Number of kernel launches issued by this library since load (all threads). */
+unsigned long long auxmc_launch_count(void);
+
+/* ---- counter RNG, host side, bit-exact with rng.hpp:35-118 ---- */
+uint64_t auxmc_rng_from_seed(uint64_t seed);                               /* RngStream::from_seed */
+uint64_t auxmc_rng_derive(uint64_t key, uint64_t label, uint64_t index);   /* RngStream::derive */
+double auxmc_rng_uniform(uint64_t key, uint64_t counter);                  /* next_uniform at counter */
+double auxmc_rng_normal(uint64_t key, uint64_t counter);                   /* next_normal at counter */
+
+/* Device batch generation, for tests and pre-drawn noise:
+ * out[b][i][j] = normal_vec of keys[b].derive(label, index0 + i), component j.
+ * (StreamNoise::normal, rng.hpp:128-137) */
+int auxmc_rng_normals(const uint64_t* keys, int B, uint64_t label, uint64_t index0, int n_index,
+                      int dim, double* out, void* stream);
+
+/* ---- linear-Gaussian state-space model (lgssm.hpp:19-49) ----
+ * Time-varying arrays carry a count: 1 (broadcast, lgssm.hpp:34-40) or T (F,b,Q) /
+ * T+1 (H,c,R).  The library symmetrizes P0, Q, R on use exactly as the Model
+ * constructor does (lgssm.cpp:20-71). */
+typedef struct {
+  int T, dx, dy;
+  const double* m0; const double* P0;
+  const double* F; int nF;
+  const double* b; int nb;
+  const double* Q; int nQ;
+  const double* H; int nH;
+  const double* c; int nc;
+  const double* R; int nR;
+  const uint8_t* mask;   /* NULL = every step observed, else [T+1] */
+} auxmc_lgssm;
+
+/* FilterResult (lgssm.hpp:51-55), batch-major */
+typedef struct {
+  double* pred_mean;   /* [B][T+1][dx] */
+  double* pred_cov;    /* [B][T+1][dx][dx] */
+  double* filt_mean;   /* [B][T+1][dx] */
+  double* filt_cov;    /* [B][T+1][dx][dx] */
+  double* log_marginal;/* [B] */
+} auxmc_filter_result;
+
+/* Kalman filtering of B observation sequences obs [B][T+1][dy] under one model.
+ * mode 0: sequential covariance filter (lgssm::kalman_filter, lgssm.cpp:73-112)
+ * mode 1: parallel-in-time scan filter (pit::parallel_filter, pit.cpp:117-188)
+ * status[B] receives per-sequence codes. */
+int auxmc_kalman_filter(const auxmc_lgssm* model, const double* obs, int B, int mode,
+                        auxmc_filter_result* out, int* status, void* workspace,
+                        size_t workspace_bytes, void* stream);
+size_t auxmc_kalman_filter_workspace(const auxmc_lgssm* model, int B, int mode);
+
+/* ---- noise sources (rng.hpp:123-137) ----
+ * kind 0 (stream): per-problem stream keys; draws at keys[b].derive(label, index).
+ * kind 1 (pre-drawn): arrays addressed by (label, index); the NoiseSource
+ *   analogue used for strict parity and for affine-law probing. */
+#define AUXMC_NOISE_STREAM 0
+#define AUXMC_NOISE_PREDRAWN 1
+typedef struct {
+  int kind;
+  const uint64_t* keys;       /* [B] */
+  const double* terminal;     /* [B][dx]            (kTerminalDraw, 0) */
+  const double* backward;     /* [B][T][dx]         (kBackwardNoise, t) */
+  const double* bridge;       /* [B][n_bridge][dx]  (kDncBridge, node id) */
+  long long n_bridge;
+} auxmc_noise;
+
+/* Number of bridge ids a pre-drawn DnC noise array must cover for horizon T
+ * (heap ids of the BFS segment tree, pit.cpp:214-234). */
+long long auxmc_dnc_bridge_count(int T);
+
+/* Pathwise posterior draws of B paths traj [B][T+1][dx] from filter results.
+ * fr_shared = 1: one filter result (B_fr = 1) shared by all paths (the C2
+ * workload: one model, many chains); 0: one per path.
+ *   sampler 0: lgssm::backward_sample (lgssm.cpp:151-177)
+ *   sampler 1: pit::prefix_sample     (pit.cpp:78-115)
+ *   sampler 2: pit::dnc_sample        (pit.cpp:192-301)
+ * status[B] receives per-path codes. */
+#define AUXMC_SAMPLER_SEQ 0
+#define AUXMC_SAMPLER_PREFIX 1
+#define AUXMC_SAMPLER_DNC 2
+int auxmc_sample_paths(const auxmc_lgssm* model, const auxmc_filter_result* fr, int fr_shared,
+                       const auxmc_noise* noise, int B, int sampler, double* traj, int* status,
+                       void* workspace, size_t workspace_bytes, void* stream);
+size_t auxmc_sample_paths_workspace(const auxmc_lgssm* model, int fr_shared, int B, int sampler);
+
+/* Host-buffer convenience entry for the reference-facing facade: copies the
+ * model, filter result and noise keys to the device, draws B paths and copies
+ * them back into traj_host [B][T+1][dx] (pinned or pageable).  All host pointers. */
+int auxmc_sample_paths_host(const auxmc_lgssm* model_host, const auxmc_filter_result* fr_host,
+                            int fr_shared, const uint64_t* keys_host, int B, int sampler,
+                            double* traj_host, int* status_host);
+
+/* lgssm::path_logpdf (lgssm.cpp:179-199) for B paths traj [B][T+1][dx] against
+ * observations obs [B or 1][T+1][dy] and filter results (fr_shared as above). */
+int auxmc_path_logpdf(const auxmc_lgssm* model, const double* obs, int obs_shared,
+                      const double* traj, const auxmc_filter_result* fr, int fr_shared, int B,
+                      double* out, int* status, void* stream);
+
+/* ---- targets (target.hpp:34-93) and bench models (models.hpp:16-54) ----
+ * Model closures become compiled device functors selected by `kind`. */
+#define AUXMC_KIND_LGSSM 0          /* linear dynamics, exact Gaussian potentials */
+#define AUXMC_KIND_STOCHVOL 1       /* models.cpp:113-128, :261-278 */
+#define AUXMC_KIND_LORENZ63 2       /* diffusion-smoothing, models.cpp:70-85, :280-297 */
+#define AUXMC_KIND_SPATIO 3         /* models.cpp:88-111, :299-317 */
+#define AUXMC_KIND_GRID1D 4         /* models.cpp:319-333 */
+#define AUXMC_KIND_LORENZ96 5       /* new: Lorenz-96 diffusion, even coordinates observed */
+#define AUXMC_KIND_GAUSS_GENERIC 6  /* linear, Gaussian potentials in generic form */
+
+typedef struct {
+  int kind;
+  int T, dx;
+  int ydim;                 /* data columns */
+  int linear;               /* 1: F,b,Q below; 0: tractable (kind-specific functors) */
+  const double* m0; const double* P0;
+  const double* F; const double* b; const double* Q; int nF;   /* count 1 or T */
+  /* exact Gaussian potential rows q = max_exact_rows (target.cpp:65-70) */
+  int q; int ne;            /* ne = 1 or T+1 */
+  const double* eH; const double* ec; const double* eR;   /* [ne][q][dx], [ne][q], [ne][q][q] */
+  const double* ey;         /* [T+1][q] */
+  const uint8_t* emask;     /* [T+1] 1 where an exact block exists */
+  const double* data;       /* [T+1][ydim] generic-potential data */
+  const uint8_t* gmask;     /* [T+1] 1 where a generic factor exists */
+  /* GAUSS_GENERIC blocks: [ne][ydim][dx], [ne][ydim], [ne][ydim][ydim] */
+  const double* gH; const double* gc; const double* gR;
+  /* kind parameters (ModelSpec fields) */
+  double lz_sigma, lz_rho, lz_beta, lz_h;
+  double l96_F, l96_h;
+} auxmc_target;
+
+/* ---- auxiliary Kalman MH kernel (auxk.hpp:15-79) ---- */
+#define AUXMC_BACKEND_SEQ 0
+#define AUXMC_BACKEND_PREFIX 1
+#define AUXMC_BACKEND_DNC 2
+typedef struct {
+  int backend;          /* KernelOptions::backend */
+  int parallel_filter;  /* KernelOptions::parallel_filter */
+  int zeroth_order;     /* KernelOptions::zeroth_order */
+} auxmc_kernel_options;
+
+/* KernelStats (auxk.hpp:41-48), one per chain, device memory */
+typedef struct {
+  long long accepted, rejected, aborted, nonfinite_gamma;
+  double last_log_alpha, last_accept_prob;
+} auxmc_kernel_stats;
+
+/* Batched chain state (AuxChainState, auxk.hpp:50-57), device arrays over C chains. */
+typedef struct {
+  int C;
+  double* x;            /* [C][T+1][dx] */
+  double* delta;        /* [C] */
+  double* log_gamma;    /* [C] */
+  double* grad_gen;     /* [C][T+1][dx] */
+  long long* iter;      /* [C] */
+  auxmc_kernel_stats* stats;  /* [C] */
+  const uint64_t* root_keys;  /* [C] chain roots (from_seed(seed).derive(kChain, c)) */
+} auxmc_chains;
+
+/* auxk::init_chain (auxk.cpp:120-128) for every chain: log_gamma and grad_gen from x. */
+int auxmc_init_chains(const auxmc_target* target, auxmc_chains* chains, void* workspace,
+                      size_t workspace_bytes, void* stream);
+/* auxk::kernel_step (auxk.cpp:130-198) for every chain. */
+int auxmc_aux_kernel_step(const auxmc_target* target, auxmc_chains* chains,
+                          const auxmc_kernel_options* opts, void* workspace,
+                          size_t workspace_bytes, void* stream);
+size_t auxmc_aux_kernel_workspace(const auxmc_target* target, int C,
+                                  const auxmc_kernel_options* opts);
+/* auxk::adapt_delta (auxk.cpp:213-218) for every chain. */
+int auxmc_adapt_delta(auxmc_chains* chains, double target_rate, void* stream);
+/* target.log_gamma (target.cpp:100-108) of B paths. */
+int auxmc_log_gamma(const auxmc_target* target, const double* traj, int B, double* out,
+                    int* status, void* stream);
+
+/* ---- auxiliary particle Gibbs (fkpg.hpp:61-109) ---- */
+#define AUXMC_PG_PRIOR 0
+#define AUXMC_PG_GRADIENT 1
+#define AUXMC_PG_ADAPTED 2
+#define AUXMC_CSMC_REFERENCE 0   /* sequential cSMC with multinomial resampling (fkpg.cpp:44-152) */
+#define AUXMC_CSMC_PIT 1         /* parallel-in-time cSMC, independent proposals (new) */
+typedef struct {
+  int C, N;
+  double* x;            /* [C][T+1][dx] reference trajectories */
+  uint64_t* keys;       /* [C][T+1] reference aux keys */
+  double* delta;        /* [C] */
+  long long* iter;      /* [C] */
+  long long* updates;   /* [C] */
+  double* last_update;  /* [C] */
+  const uint64_t* root_keys;  /* [C] */
+  int* status;          /* [C] AUXMC_OK or AUXMC_E_DEGENERATE */
+  int* bad_t;           /* [C] step named by DegenerateWeightsError */
+  int* ancestors;       /* optional [C][T+1][N] trace of ancestor indices (NULL = off) */
+  int* selected;        /* optional [C][T+1] trace of selected indices (NULL = off) */
+} auxmc_pg_chains;
+
+int auxmc_aux_pgibbs_step(const auxmc_target* target, auxmc_pg_chains* chains, int mode,
+                          int variant, void* workspace, size_t workspace_bytes, void* stream);
+size_t auxmc_aux_pgibbs_workspace(const auxmc_target* target, int C, int N, int variant);
+int auxmc_pg_adapt_delta(auxmc_pg_chains* chains, double target_rate, void* stream);
+
+/* ---- host-side bench models (models.cpp:51-68, :162-238, :240-336) ----
+ * Spec mirrors ModelSpec (models.hpp:16-54) plus the Lorenz-96 block. */
+typedef struct {
+  int kind;
+  int T, dx, dy, grid;
+  uint64_t data_seed;
+  double sv_mu, sv_phi, sv_sig2, sv_rho;
+  double lz_sigma, lz_rho, lz_beta, lz_h, lz_gamma, lz_obs_var;
+  double st_phi, st_kappa2, st_tau2;
+  double g1_phi, g1_q, g1_m0, g1_p0;
+  double l96_F, l96_h, l96_gamma, l96_obs_var;
+} auxmc_model_spec;
+
+void auxmc_spec_default(auxmc_model_spec* spec);
+int auxmc_latent_dim(const auxmc_model_spec* spec);
+int auxmc_obs_dim(const auxmc_model_spec* spec);
+/* bench::simulate — host buffers latent_host [T+1][dx], data_host [T+1][ydim]. */
+int auxmc_simulate(const auxmc_model_spec* spec, double* latent_host, double* data_host);
+/* bench::synth_mats for lgssm-synthetic, host buffers (row-major). */
+int auxmc_synth_mats(const auxmc_model_spec* spec, double* m0, double* b, double* P0, double* F,
+                     double* Q, double* H, double* R);
+/* Host-side parameter arrays of make_target for kinds STOCHVOL / SPATIO / GRID1D /
+ * LORENZ63 / LORENZ96 (m0 [dx], P0 [dx][dx], Q [dx][dx]; F,b for linear kinds). */
+int auxmc_target_params(const auxmc_model_spec* spec, double* m0, double* P0, double* F,
+                        double* b, double* Q);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AUXMC_GPU_H */

@@ -1,0 +1,98 @@
+// common.cuh — shared host/device plumbing of libauxmc_b200: status codes,
+// launch accounting, error capture, model accessors.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+
+#include "../../include/auxmc_gpu.h"
+
+namespace auxmc_gpu {
+
+extern std::atomic<unsigned long long> g_launches;
+void set_last_error(const char* where, cudaError_t e);
+
+#define AUXMC_LAUNCH(kernel, grid, block, smem, stream, ...)                   \
+  do {                                                                         \
+    kernel<<<(grid), (block), (smem), (cudaStream_t)(stream)>>>(__VA_ARGS__);  \
+    ::auxmc_gpu::g_launches.fetch_add(1, std::memory_order_relaxed);           \
+    cudaError_t _e = cudaGetLastError();                                       \
+    if (_e != cudaSuccess) {                                                   \
+      ::auxmc_gpu::set_last_error(#kernel, _e);                                \
+      return AUXMC_E_CUDA;                                                     \
+    }                                                                          \
+  } while (0)
+
+#define AUXMC_CUDA_TRY(expr)                                                   \
+  do {                                                                         \
+    cudaError_t _e = (expr);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      ::auxmc_gpu::set_last_error(#expr, _e);                                  \
+      return AUXMC_E_CUDA;                                                     \
+    }                                                                          \
+  } while (0)
+
+bool device_ok();
+int num_sms();
+
+inline size_t align_up(size_t n, size_t a = 256) { return (n + a - 1) / a * a; }
+
+// Bump allocator over a caller-provided workspace.
+struct Arena {
+  char* base;
+  size_t size, used;
+  template <class T>
+  T* take(size_t count) {
+    size_t off = align_up(used);
+    size_t bytes = sizeof(T) * count;
+    if (base == nullptr) {  // sizing pass
+      used = off + bytes;
+      return nullptr;
+    }
+    if (off + bytes > size) return nullptr;
+    used = off + bytes;
+    return reinterpret_cast<T*>(base + off);
+  }
+};
+
+// ---- lgssm model accessors (lgssm.hpp:34-40 broadcast rule) ----
+struct DevModel {
+  int T, dx, dy;
+  const double *m0, *P0, *F, *b, *Q, *H, *c, *R;
+  int nF, nb, nQ, nH, nc, nR;
+  const uint8_t* mask;
+  __device__ __forceinline__ const double* Ft(int t) const { return F + (size_t)(nF > 1 ? t : 0) * dx * dx; }
+  __device__ __forceinline__ const double* bt(int t) const { return b + (size_t)(nb > 1 ? t : 0) * dx; }
+  __device__ __forceinline__ const double* Qt(int t) const { return Q + (size_t)(nQ > 1 ? t : 0) * dx * dx; }
+  __device__ __forceinline__ const double* Ht(int t) const { return H + (size_t)(nH > 1 ? t : 0) * dy * dx; }
+  __device__ __forceinline__ const double* ct(int t) const { return c + (size_t)(nc > 1 ? t : 0) * dy; }
+  __device__ __forceinline__ const double* Rt(int t) const { return R + (size_t)(nR > 1 ? t : 0) * dy * dy; }
+  __device__ __forceinline__ bool observed(int t) const { return mask == nullptr || mask[t] != 0; }
+};
+
+inline DevModel to_dev(const auxmc_lgssm& m) {
+  DevModel d;
+  d.T = m.T; d.dx = m.dx; d.dy = m.dy;
+  d.m0 = m.m0; d.P0 = m.P0; d.F = m.F; d.b = m.b; d.Q = m.Q; d.H = m.H; d.c = m.c; d.R = m.R;
+  d.nF = m.nF; d.nb = m.nb; d.nQ = m.nQ; d.nH = m.nH; d.nc = m.nc; d.nR = m.nR;
+  d.mask = m.mask;
+  return d;
+}
+
+int check_model(const auxmc_lgssm* m);
+
+__host__ __device__ inline int elem_stride(int d) { return (2 * d * d + d + 1) & ~1; }
+__host__ __device__ inline int term_stride(int d) { return (d * d + d + 1) & ~1; }
+
+struct NoiseArgs {
+  int kind;
+  const uint64_t* keys;
+  const double* terminal;
+  const double* backward;
+  const double* bridge;
+  long long n_bridge;
+};
+
+}  // namespace auxmc_gpu

@@ -1,0 +1,313 @@
+// dnc.cu — pit::dnc_sample (pit.cpp:192-301) on B200.
+//
+// The reference builds a breadth-first segment tree over [0, T] (split at
+// floor((l+r)/2) while r-l >= 2, heap ids 1, 2h, 2h+1; pit.cpp:214-234).  The
+// tree depends only on T, so here nodes are addressed directly by heap id: the
+// interval of node h follows from the bits of h, and node arrays are indexed
+// by h (no host-built tree).  Levels run deepest-first for the bottom-up
+// element composition (pit.cpp:237-245) and root-first for the Gaussian bridges
+// (pit.cpp:265-293).  Bridge gains and factors depend only on the elements, so
+// with a shared filter result they are computed once and reused by every chain.
+#include "common.cuh"
+#include "dense.cuh"
+#include "rng.cuh"
+
+namespace auxmc_gpu {
+
+
+__host__ __device__ inline int dnc_depth(int T) {
+  int depth = 0;
+  long long cap = 1;
+  while (cap < T) {
+    cap <<= 1;
+    ++depth;
+  }
+  return depth;
+}
+
+// Interval of heap node h; returns false if the node does not exist.
+__device__ __forceinline__ bool dnc_interval(uint64_t h, int T, int& l, int& r) {
+  int depth = 63 - __clzll((long long)h);
+  l = 0;
+  r = T;
+  for (int bit = depth - 1; bit >= 0; --bit) {
+    if (r - l < 2) return false;
+    const int m = (l + r) / 2;
+    if ((h >> bit) & 1ull) l = m;
+    else r = m;
+  }
+  return true;
+}
+
+// Bottom-up: elem[h] = leaf ? base[l] : elem[2h] ∘ elem[2h+1] (pit.cpp:23-30).
+template <bool BLOCK>
+__global__ void k_dnc_compose(int T, int d, int level, int Bfr, const double* __restrict__ base,
+                              double* nodes, long long n_heap) {
+  extern __shared__ double smem[];
+  const int dd = d * d, ES = (2 * dd + d + 1) & ~1;
+  Grp g = BLOCK ? block_group() : warp_group();
+  const int gid = BLOCK ? 0 : (threadIdx.x >> 5);
+  const int gpb = BLOCK ? 1 : (blockDim.x >> 5);
+  double* W = smem + (size_t)gid * 2 * dd;
+  const long long width = 1LL << level;
+  const long long n_items = width * Bfr;
+  for (long long item = (long long)blockIdx.x * gpb + gid; item < n_items;
+       item += (long long)gridDim.x * gpb) {
+    const int b = (int)(item / width);
+    const uint64_t h = (uint64_t)width + (uint64_t)(item % width);
+    int l, r;
+    if (!dnc_interval(h, T, l, r)) continue;
+    double* out = nodes + ((size_t)b * n_heap + h) * ES;
+    if (r - l < 2) {
+      const double* src = base + ((size_t)b * T + l) * ES;
+      g_copy(g, 2 * dd + d, src, out);
+      g.sync();
+      continue;
+    }
+    const double* a = nodes + ((size_t)b * n_heap + 2 * h) * ES;
+    const double* bb = nodes + ((size_t)b * n_heap + 2 * h + 1) * ES;
+    g_mm(g, d, d, d, a, bb, out);                         // G = a.G b.G
+    g_mv(g, d, d, a, bb + dd, out + dd, a + dd);          // c = a.G b.c + a.c
+    g_mm(g, d, d, d, a, bb + dd + d, W);                  // a.G b.cov
+    g.sync();
+    g_mm_nt(g, d, d, d, W, a, out + dd + d, a + dd + d);  // (.) a.G^T + a.cov
+    g.sync();
+    g_symm(g, d, out + dd + d);
+    g.sync();
+  }
+}
+
+// Bridge parameters per internal node (pit.cpp:270-291): K (gain), L = chol(cov).
+// Root (h = 1): L = chol_psd(root cov) (pit.cpp:259-263).
+template <bool BLOCK>
+__global__ void k_dnc_bridge(int T, int d, int Bfr, const double* __restrict__ nodes,
+                             long long n_heap, long long n_first, long long n_last,
+                             double* params, int* status) {
+  extern __shared__ double smem[];
+  const int dd = d * d, ES = (2 * dd + d + 1) & ~1;
+  Grp g = BLOCK ? block_group() : warp_group();
+  const int gid = BLOCK ? 0 : (threadIdx.x >> 5);
+  const int gpb = BLOCK ? 1 : (blockDim.x >> 5);
+  const int per = 8 * dd + 4;
+  double* sm = smem + (size_t)gid * per;
+  double* cross = sm;
+  double* s = cross + dd;
+  double* K = s + dd;
+  double* A = K + dd;
+  double* cov = A + dd;
+  double* W = cov + dd;
+  double* L = W + dd;
+  double* scr = L + dd;
+  double* red = scr + dd;
+  int* flag = reinterpret_cast<int*>(red + 2);
+  const long long width = n_last - n_first;
+  const long long n_items = width * Bfr;
+  for (long long item = (long long)blockIdx.x * gpb + gid; item < n_items;
+       item += (long long)gridDim.x * gpb) {
+    const int b = (int)(item / width);
+    const uint64_t h = (uint64_t)(n_first + item % width);
+    int l, r;
+    if (!dnc_interval(h, T, l, r)) continue;
+    double* out = params + ((size_t)b * n_heap + h) * 2 * dd;
+    int st = 0;
+    if (h == 1) {  // root factor lives in the unused heap slot 0
+      st = g_chol_psd(g, d, nodes + ((size_t)b * n_heap + 1) * ES + dd + d, L, scr, flag, red);
+      g_copy(g, dd, L, params + (size_t)b * n_heap * 2 * dd + dd);
+      g.sync();
+      if (st && g.lane == 0) atomicMax(status + b, st);
+    }
+    if (r - l < 2) continue;
+    const double* elm = nodes + ((size_t)b * n_heap + 2 * h) * ES;
+    const double* emr = nodes + ((size_t)b * n_heap + 2 * h + 1) * ES;
+    const double* Glm = elm;
+    const double* Slm = elm + dd + d;
+    const double* Smr = emr + dd + d;
+    g_mm_nt(g, d, d, d, Smr, Glm, cross);  // cov(x_m, x_l | x_r)
+    g.sync();
+    if (g_all_zero(g, dd, cross, flag)) {
+      g_zero(g, dd, K);
+      g.sync();
+    } else {
+      g_mm(g, d, d, d, Glm, Smr, W);
+      g.sync();
+      g_mm_nt(g, d, d, d, W, Glm, s, Slm);
+      g.sync();
+      g_symm(g, d, s);
+      for (int i = g.lane; i < dd; i += g.size) A[i] = cross[(i % d) * d + i / d];  // cross^T
+      g.sync();
+      st = g_factor_psd(g, d, s, L, scr, flag, red);
+      if (st) {
+        if (g.lane == 0) atomicMax(status + b, st);
+        g.sync();
+        continue;
+      }
+      g_llt_solve(g, d, L, d, A);
+      for (int i = g.lane; i < dd; i += g.size) K[i] = A[(i % d) * d + i / d];
+      g.sync();
+    }
+    // A = I - K G_lm ; cov = symm(A S_mr A^T + K S_lm K^T)
+    g_mm(g, d, d, d, K, Glm, A);
+    g.sync();
+    for (int i = g.lane; i < dd; i += g.size) A[i] = (i / d == i % d ? 1.0 : 0.0) - A[i];
+    g.sync();
+    g_mm(g, d, d, d, A, Smr, W);
+    g.sync();
+    g_mm_nt(g, d, d, d, W, A, cov);
+    g.sync();
+    g_mm(g, d, d, d, K, Slm, W);
+    g.sync();
+    g_mm_nt(g, d, d, d, W, K, s);
+    g.sync();
+    for (int i = g.lane; i < dd; i += g.size) cov[i] += s[i];
+    g.sync();
+    g_symm(g, d, cov);
+    g.sync();
+    st = g_chol_psd(g, d, cov, L, scr, flag, red);
+    if (st && g.lane == 0) atomicMax(status + b, st);
+    g_copy(g, dd, K, out);
+    g_copy(g, dd, L, out + dd);
+    g.sync();
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void dnc_normals(const NoiseArgs& nz, int c, uint64_t label,
+                                            uint64_t index, int T, double* xi) {
+  if (nz.kind == AUXMC_NOISE_PREDRAWN) {
+    const double* src = label == kDncBridge ? nz.bridge + ((size_t)c * nz.n_bridge + index) * D
+                        : label == kTerminalDraw ? nz.terminal + (size_t)c * D
+                                                 : nz.backward + ((size_t)c * T + index) * D;
+#pragma unroll
+    for (int i = 0; i < D; ++i) xi[i] = src[i];
+  } else {
+    const uint64_t k = derive(nz.keys[c], label, index);
+#pragma unroll
+    for (int i = 0; i < D; ++i) xi[i] = normal_at(k, (uint64_t)i);
+  }
+}
+
+// x_T (pit.cpp:206-208) and x_0 | x_T through the root (pit.cpp:259-263).
+template <int D>
+__global__ void k_dnc_ends(int T, int B, int fr_shared, const double* __restrict__ term,
+                           const double* __restrict__ nodes, const double* __restrict__ params,
+                           long long n_heap, NoiseArgs nz, double* traj) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= B) return;
+  constexpr int ES = (2 * D * D + D + 1) & ~1;
+  constexpr int TS = (D * D + D + 1) & ~1;
+  const int b = fr_shared ? 0 : c;
+  const double* tm = term + (size_t)b * TS;
+  double* out = traj + (size_t)c * (T + 1) * D;
+  double xi[D], x[D], v[D];
+  dnc_normals<D>(nz, c, kTerminalDraw, 0, T, xi);
+  r_matvec<D>(tm + D, xi, x);
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    x[i] = tm[i] + x[i];
+    out[(size_t)T * D + i] = x[i];
+  }
+  if (T == 0) return;
+  const double* root = nodes + ((size_t)b * n_heap + 1) * ES;
+  const double* Lr = params + (size_t)b * n_heap * 2 * D * D + D * D;
+  dnc_normals<D>(nz, c, kBackwardNoise, 0, T, xi);
+  r_matvec<D>(Lr, xi, v);
+#pragma unroll
+  for (int i = 0; i < D; ++i) v[i] = root[D * D + i] + v[i];  // shifted = c + L xi
+  double gx[D];
+  r_matvec<D>(root, x, gx);
+#pragma unroll
+  for (int i = 0; i < D; ++i) out[i] = gx[i] + v[i];
+}
+
+// One level of bridges: thread per (node, chain), chains fastest.
+template <int D>
+__global__ void k_dnc_level(int T, int B, int fr_shared, int level,
+                            const double* __restrict__ nodes, const double* __restrict__ params,
+                            long long n_heap, NoiseArgs nz, double* traj) {
+  constexpr int ES = (2 * D * D + D + 1) & ~1;
+  const long long width = 1LL << level;
+  const long long n = width * B;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(q % B);
+    const uint64_t h = (uint64_t)width + (uint64_t)(q / B);
+    int l, r;
+    if (!dnc_interval(h, T, l, r) || r - l < 2) continue;
+    const int m = (l + r) / 2;
+    const int b = fr_shared ? 0 : c;
+    const double* elm = nodes + ((size_t)b * n_heap + 2 * h) * ES;
+    const double* emr = nodes + ((size_t)b * n_heap + 2 * h + 1) * ES;
+    const double* K = params + ((size_t)b * n_heap + h) * 2 * D * D;
+    const double* L = K + D * D;
+    double* out = traj + (size_t)c * (T + 1) * D;
+    double xl[D], xr[D], mu[D], v[D], w[D], xi[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      xl[i] = out[(size_t)l * D + i];
+      xr[i] = out[(size_t)r * D + i];
+    }
+    r_matvec<D>(emr, xr, mu);
+#pragma unroll
+    for (int i = 0; i < D; ++i) mu[i] += emr[D * D + i];
+    r_matvec<D>(elm, mu, v);
+#pragma unroll
+    for (int i = 0; i < D; ++i) v[i] = (xl[i] - v[i]) - elm[D * D + i];
+    r_matvec<D>(K, v, w);
+    dnc_normals<D>(nz, c, kDncBridge, h, T, xi);
+    double lx[D];
+    r_matvec<D>(L, xi, lx);
+#pragma unroll
+    for (int i = 0; i < D; ++i) out[(size_t)m * D + i] = (mu[i] + w[i]) + lx[i];
+  }
+}
+
+int launch_dnc(const DevModel& dm, int Bfr, int fr_shared, const double* elems,
+               const double* term, const NoiseArgs& nz, int B, double* traj, Arena& ws,
+               int* st_fr, cudaStream_t stream) {
+  const int d = dm.dx, T = dm.T, dd = d * d;
+  const int ES = (2 * dd + d + 1) & ~1;
+  const int depth = dnc_depth(T);
+  const long long n_heap = 2LL << depth;  // ids < 2^(depth+1)
+  double* nodes = ws.take<double>((size_t)Bfr * n_heap * ES);
+  double* params = ws.take<double>((size_t)Bfr * n_heap * 2 * dd);
+  if (ws.base == nullptr) return AUXMC_OK;
+  if (!nodes || !params) return AUXMC_E_WORKSPACE;
+  if (d > 8) return AUXMC_E_DIM;
+  const bool block = d > 16;
+  const int warps = 4;
+  if (T > 0) {
+    for (int level = depth; level >= 0; --level) {
+      const long long items = (1LL << level) * Bfr;
+      const int grid = (int)std::min<long long>((items + warps - 1) / warps, 148LL * 64);
+      AUXMC_LAUNCH(k_dnc_compose<false>, grid, 32 * warps, sizeof(double) * 2 * dd * warps,
+                   stream, T, d, level, Bfr, elems, nodes, n_heap);
+    }
+    const long long items = (n_heap - 1) * Bfr;
+    const int grid = (int)std::min<long long>((items + warps - 1) / warps, 148LL * 64);
+    const size_t smem = sizeof(double) * (8 * dd + 4) * warps;
+    AUXMC_LAUNCH(k_dnc_bridge<false>, grid, 32 * warps, smem, stream, T, d, Bfr, nodes, n_heap,
+                 1LL, n_heap, params, st_fr);
+  }
+  (void)block;
+  switch (d) {
+#define CASE(D)                                                                              \
+  case D: {                                                                                  \
+    AUXMC_LAUNCH(k_dnc_ends<D>, (B + 127) / 128, 128, 0, stream, T, B, fr_shared, term, nodes, \
+                 params, n_heap, nz, traj);                                                  \
+    for (int level = 0; level < depth; ++level) {                                            \
+      const long long n = (1LL << level) * B;                                                \
+      const int grid = (int)std::min<long long>((n + 255) / 256, 148LL * 32);                \
+      AUXMC_LAUNCH(k_dnc_level<D>, grid, 256, 0, stream, T, B, fr_shared, level, nodes,      \
+                   params, n_heap, nz, traj);                                                \
+    }                                                                                        \
+    break;                                                                                   \
+  }
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default:
+      return AUXMC_E_DIM;
+  }
+  return AUXMC_OK;
+}
+
+}  // namespace auxmc_gpu

@@ -1,0 +1,185 @@
+// filter.cu — batched Kalman filtering on B200.
+//
+//  * k_filter_seq: lgssm::kalman_filter (lgssm.cpp:73-112), covariance form with
+//    Joseph update, one sequence per group (warp for small dims, CTA for large).
+//    The innovation factor is computed once and reused for the log-likelihood
+//    term: the reference factors the identical symmetrized S twice
+//    (lgssm.cpp:101 and :105-106), which yields the same bits.
+#include "common.cuh"
+#include "dense.cuh"
+
+namespace auxmc_gpu {
+
+__host__ __device__ inline int filter_smem_doubles(int dx, int dy) {
+  const int W = dx > dy ? dx : dy;
+  return 4 * dx + 3 * W + 5 * dx * dx + 2 * dy * dx + 3 * dy * dy + 8;
+}
+
+template <bool BLOCK>
+__global__ void k_filter_seq(DevModel m, const double* __restrict__ obs, int B,
+                             double* pred_mean, double* pred_cov, double* filt_mean,
+                             double* filt_cov, double* log_marginal, int* status) {
+  extern __shared__ double smem[];
+  const int dx = m.dx, dy = m.dy, T = m.T;
+  const int W = dx > dy ? dx : dy;
+  const int per = filter_smem_doubles(dx, dy);
+  Grp g = BLOCK ? block_group() : warp_group();
+  const int gid = BLOCK ? 0 : (threadIdx.x >> 5);
+  const int gpb = BLOCK ? 1 : (blockDim.x >> 5);
+  double* sm = smem + (size_t)gid * per;
+  double* mm = sm;
+  double* mp = mm + dx;
+  double* v = mp + dx;
+  double* innov = v + W;
+  double* v2 = innov + W;
+  double* p = v2 + W;
+  double* tmp = p + dx * dx;
+  double* a = tmp + dx * dx;
+  double* work = a + dx * dx;
+  double* Qs = work + dx * dx;
+  double* hp = Qs + dx * dx;
+  double* X = hp + dy * dx;
+  double* S = X + dy * dx;
+  double* L = S + dy * dy;
+  double* scr = L + dy * dy;
+  double* red = scr + dy * dy;
+  int* flag = reinterpret_cast<int*>(red + 2);
+  const int ddx = dx * dx;
+  for (int b = blockIdx.x * gpb + gid; b < B; b += gridDim.x * gpb) {
+    const double* y_all = obs + (size_t)b * (T + 1) * dy;
+    double* pm_out = pred_mean + (size_t)b * (T + 1) * dx;
+    double* pc_out = pred_cov + (size_t)b * (T + 1) * ddx;
+    double* fm_out = filt_mean + (size_t)b * (T + 1) * dx;
+    double* fc_out = filt_cov + (size_t)b * (T + 1) * ddx;
+    double ll = 0.0;
+    int st = 0;
+    for (int i = g.lane; i < dx; i += g.size) mm[i] = m.m0[i];
+    for (int i = g.lane; i < ddx; i += g.size) {
+      const int r = i / dx, c = i % dx;
+      p[i] = 0.5 * (m.P0[r * dx + c] + m.P0[c * dx + r]);
+    }
+    g.sync();
+    for (int t = 0; t <= T; ++t) {
+      if (t > 0) {
+        const double* F = m.Ft(t - 1);
+        const double* bb = m.bt(t - 1);
+        const double* Q = m.Qt(t - 1);
+        for (int i = g.lane; i < dx; i += g.size) {
+          double s = 0.0;
+          for (int j = 0; j < dx; ++j) s += F[i * dx + j] * mm[j];
+          v[i] = s + bb[i];
+        }
+        for (int i = g.lane; i < ddx; i += g.size) {
+          const int r = i / dx, c = i % dx;
+          Qs[i] = 0.5 * (Q[r * dx + c] + Q[c * dx + r]);
+        }
+        g_mm(g, dx, dx, dx, F, p, tmp);
+        g.sync();
+        for (int i = g.lane; i < dx; i += g.size) mm[i] = v[i];
+        g_mm_nt(g, dx, dx, dx, tmp, F, p, Qs);
+        g.sync();
+        g_symm(g, dx, p);
+        g.sync();
+      }
+      for (int i = g.lane; i < dx; i += g.size) {
+        pm_out[(size_t)t * dx + i] = mm[i];
+        mp[i] = mm[i];
+      }
+      for (int i = g.lane; i < ddx; i += g.size) pc_out[(size_t)t * ddx + i] = p[i];
+      if (m.observed(t)) {
+        const double* H = m.Ht(t);
+        const double* c = m.ct(t);
+        const double* R = m.Rt(t);
+        const double* y = y_all + (size_t)t * dy;
+        for (int i = g.lane; i < dy; i += g.size) {
+          double s = 0.0;
+          for (int j = 0; j < dx; ++j) s += H[i * dx + j] * mm[j];
+          innov[i] = (y[i] - s) - c[i];
+          v2[i] = s + c[i];  // H m_pred + c
+        }
+        g_mm(g, dy, dx, dx, H, p, hp);  // H P
+        g.sync();
+        for (int i = g.lane; i < dy * dy; i += g.size) {
+          const int r = i / dy, cc = i % dy;
+          scr[i] = 0.5 * (R[r * dy + cc] + R[cc * dy + r]);  // Rs
+        }
+        g.sync();
+        g_mm_nt(g, dy, dx, dy, hp, H, S, scr);
+        g.sync();
+        g_symm(g, dy, S);
+        g.sync();
+        st = g_factor_psd(g, dy, S, L, scr, flag, red);
+        if (st) break;
+        g_copy(g, dy * dx, hp, X);
+        g.sync();
+        g_llt_solve(g, dy, L, dx, X);  // X = S^{-1} H P ; gain = X^T
+        // m += X^T innov
+        for (int j = g.lane; j < dx; j += g.size) {
+          double s = 0.0;
+          for (int i = 0; i < dy; ++i) s += X[i * dx + j] * innov[i];
+          mm[j] += s;
+        }
+        // a = I - X^T H
+        g_mm_tn(g, dx, dy, dx, X, H, a);
+        g.sync();
+        for (int i = g.lane; i < ddx; i += g.size) a[i] = (i / dx == i % dx ? 1.0 : 0.0) - a[i];
+        for (int i = g.lane; i < dy * dy; i += g.size) {
+          const int r = i / dy, cc = i % dy;
+          scr[i] = 0.5 * (R[r * dy + cc] + R[cc * dy + r]);
+        }
+        g.sync();
+        g_mm(g, dx, dx, dx, a, p, tmp);       // a p
+        g_mm_tn(g, dx, dy, dy, X, scr, hp);   // X^T R  (dx×dy), reuses hp
+        g.sync();
+        g_mm_nt(g, dx, dx, dx, tmp, a, work); // a p a^T
+        g_mm(g, dx, dy, dx, hp, X, p);        // X^T R X
+        g.sync();
+        for (int i = g.lane; i < ddx; i += g.size) p[i] = work[i] + p[i];
+        g.sync();
+        g_symm(g, dx, p);
+        g.sync();
+        ll += g_log_pdf_factored(g, dy, y, v2, L, innov, red);
+      }
+      for (int i = g.lane; i < dx; i += g.size) fm_out[(size_t)t * dx + i] = mm[i];
+      for (int i = g.lane; i < ddx; i += g.size) fc_out[(size_t)t * ddx + i] = p[i];
+      g.sync();
+    }
+    if (g.lane == 0) {
+      log_marginal[b] = ll;
+      status[b] = st;
+    }
+    g.sync();
+  }
+}
+
+int launch_filter_seq(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
+                      int* status, cudaStream_t stream) {
+  const int per = filter_smem_doubles(dm.dx, dm.dy);
+  const bool block = (dm.dx > 16 || dm.dy > 16);
+  if (block) {
+    const size_t smem = sizeof(double) * per;
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_filter_seq<true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    AUXMC_LAUNCH(k_filter_seq<true>, B, 256, smem, stream, dm, obs, B, out->pred_mean,
+                 out->pred_cov, out->filt_mean, out->filt_cov, out->log_marginal, status);
+  } else {
+    const int warps = 4;
+    const size_t smem = sizeof(double) * per * warps;
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_filter_seq<false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = (B + warps - 1) / warps;
+    AUXMC_LAUNCH(k_filter_seq<false>, grid, 32 * warps, smem, stream, dm, obs, B, out->pred_mean,
+                 out->pred_cov, out->filt_mean, out->filt_cov, out->log_marginal, status);
+  }
+  return AUXMC_OK;
+}
+
+}  // namespace auxmc_gpu
+
+namespace auxmc_gpu {
+size_t filter_pit_workspace(const DevModel& dm, int B) { return 0; }
+int launch_filter_pit(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
+                      int* status, Arena& ws, cudaStream_t stream) {
+  return AUXMC_E_ARG;  // implemented in pitfilter.cu
+}
+}  // namespace auxmc_gpu

@@ -1,0 +1,662 @@
+// sample.cu — pathwise posterior samplers on B200.
+//
+//  * k_bwd_elements: one-step backward conditionals (lgssm.cpp:129-149) as
+//    affine elements (G_t, offset_t, L_t = chol_psd(Λ_t)) plus the terminal law
+//    (m_T, chol_psd(P_T)) (lgssm.cpp:151-154, pit.cpp:85-87).  Group-cooperative.
+//  * k_prefix: pit::prefix_sample (pit.cpp:78-115).  The suffix composition of
+//    realized elements is evaluated as a fixed-tree reduce-then-scan: one CTA
+//    owns a few chains over the whole horizon and walks it top-down in
+//    superchunks staged through shared memory (cp.async double buffering);
+//    inside a superchunk each thread reduces a sub-chunk, the sub-chunk
+//    aggregates are scanned with the superchunk's carry, and each thread
+//    expands its sub-chunk.  The association tree depends only on (T, LS, S), so
+//    the output is bit-deterministic; noise is consumed by address (kBackwardNoise, t),
+//    never by evaluation order (rng.hpp:128-137).
+//  * k_seq: lgssm::backward_sample (lgssm.cpp:151-177), thread per path.
+#include <cuda_pipeline.h>
+
+#include "common.cuh"
+#include "dense.cuh"
+#include "rng.cuh"
+
+namespace auxmc_gpu {
+
+
+__device__ int g_flip_backward_gain = 0;  // testhooks::flip_backward_gain (testhooks.hpp:11)
+
+// ---------------------------------------------------------------- elements
+// smem per group: 9 d*d + 4 d doubles + 2 ints
+__device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel& m, int t,
+                                                   const double* fm, const double* fc,
+                                                   const double* pc, double* sm, int* flag,
+                                                   double* out /* G | off | L (or Λ) */,
+                                                   int store_cov) {
+  const int d = m.dx, dd = d * d;
+  double* P = sm;
+  double* F = P + dd;
+  double* S = F + dd;
+  double* X = S + dd;   // cross, then solve rhs/result
+  double* L = X + dd;
+  double* A = L + dd;
+  double* W = A + dd;
+  double* G = W + dd;
+  double* scr = G + dd;
+  double* v = scr + dd;
+  double* red = v + 2 * d;
+  const double* Ft = m.Ft(t);
+  g_copy(g, dd, fc + (size_t)t * dd, P);
+  g_copy(g, dd, Ft, F);
+  g_copy(g, dd, pc + (size_t)(t + 1) * dd, S);
+  g.sync();
+  g_mm_nt(g, d, d, d, P, F, X);  // cross = P F^T
+  g.sync();
+  int st = 0;
+  if (g_all_zero(g, dd, X, flag)) {
+    g_zero(g, dd, G);
+    g.sync();
+  } else {
+    // rhs = cross^T (into W), X := S^{-1} cross^T, G = X^T
+    for (int i = g.lane; i < dd; i += g.size) W[i] = X[(i % d) * d + i / d];
+    g.sync();
+    st = g_factor_psd(g, d, S, L, scr, flag, red);
+    if (st) return st;
+    g_llt_solve(g, d, L, d, W);
+    for (int i = g.lane; i < dd; i += g.size) G[i] = W[(i % d) * d + i / d];
+    g.sync();
+  }
+  if (g_flip_backward_gain) {
+    for (int i = g.lane; i < dd; i += g.size) G[i] = -G[i];
+    g.sync();
+  }
+  // offset = m_t - G (F m_t + b_t)
+  const double* mt = fm + (size_t)t * d;
+  const double* bt = m.bt(t);
+  for (int i = g.lane; i < d; i += g.size) {
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) s += F[i * d + j] * mt[j];
+    v[i] = s + bt[i];
+  }
+  g.sync();
+  for (int i = g.lane; i < d; i += g.size) {
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) s += G[i * d + j] * v[j];
+    v[d + i] = mt[i] - s;
+  }
+  // A = I - G F
+  g_mm(g, d, d, d, G, F, A);
+  g.sync();
+  for (int i = g.lane; i < dd; i += g.size) A[i] = (i / d == i % d ? 1.0 : 0.0) - A[i];
+  g.sync();
+  // Λ = symm(A P A^T + G Q G^T)
+  g_mm(g, d, d, d, A, P, W);
+  g.sync();
+  g_mm_nt(g, d, d, d, W, A, X);  // X = A P A^T
+  g.sync();
+  g_copy(g, dd, m.Qt(t), S);
+  g.sync();
+  g_mm(g, d, d, d, G, S, W);
+  g.sync();
+  g_mm_nt(g, d, d, d, W, G, P);  // P = G Q G^T
+  g.sync();
+  for (int i = g.lane; i < dd; i += g.size) X[i] += P[i];
+  g.sync();
+  g_symm(g, d, X);
+  g.sync();
+  if (!store_cov) {
+    st = g_chol_psd(g, d, X, L, scr, flag, red);
+    if (st) return st;
+  }
+  for (int i = g.lane; i < dd; i += g.size) {
+    out[i] = G[i];
+    out[dd + d + i] = store_cov ? X[i] : L[i];
+  }
+  for (int i = g.lane; i < d; i += g.size) out[dd + i] = v[d + i];
+  g.sync();
+  return 0;
+}
+
+// items: (b, t) for t in [0, T]; t == T is the terminal law.
+template <bool BLOCK>
+__global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
+                               const double* __restrict__ filt_cov,
+                               const double* __restrict__ pred_cov, int Bfr, double* elems,
+                               double* term, int* status, int store_cov) {
+  extern __shared__ double smem[];
+  const int d = m.dx, dd = d * d;
+  const int T = m.T;
+  const int per = 9 * dd + 4 * d + 4;
+  Grp g = BLOCK ? block_group() : warp_group();
+  const int gid = BLOCK ? 0 : (threadIdx.x >> 5);
+  const int groups_per_block = BLOCK ? 1 : (blockDim.x >> 5);
+  double* sm = smem + (size_t)gid * per;
+  int* flag = reinterpret_cast<int*>(sm + per - 2);
+  const long long n_items = (long long)Bfr * (T + 1);
+  for (long long item = (long long)blockIdx.x * groups_per_block + gid; item < n_items;
+       item += (long long)gridDim.x * groups_per_block) {
+    const int b = (int)(item / (T + 1));
+    const int t = (int)(item % (T + 1));
+    const double* fm = filt_mean + (size_t)b * (T + 1) * d;
+    const double* fc = filt_cov + (size_t)b * (T + 1) * dd;
+    const double* pc = pred_cov + (size_t)b * (T + 1) * dd;
+    int st;
+    if (t == T) {
+      double* out = term + (size_t)b * term_stride(d);
+      double* P = sm;
+      double* L = P + dd;
+      double* scr = L + dd;
+      double* red = scr + dd;
+      g_copy(g, dd, fc + (size_t)T * dd, P);
+      g.sync();
+      st = g_chol_psd(g, d, P, L, scr, flag, red);
+      for (int i = g.lane; i < d; i += g.size) out[i] = fm[(size_t)T * d + i];
+      for (int i = g.lane; i < dd; i += g.size) out[d + i] = L[i];
+    } else {
+      st = backward_step_group(g, m, t, fm, fc, pc, sm, flag,
+                               elems + ((size_t)b * T + t) * elem_stride(d), store_cov);
+    }
+    if (st && g.lane == 0) atomicMax(status + b, st);
+    g.sync();
+  }
+}
+
+// Gsub[s] = G_lo ... G_{hi-1} over the global sub-chunk s (shared elements only).
+template <int D>
+__global__ void k_gsub(const double* __restrict__ elems, int T, int LS, double* gsub) {
+  const int n_sub = (T + LS - 1) / LS;
+  const int ES = elem_stride(D);
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_sub; s += gridDim.x * blockDim.x) {
+    const int lo = s * LS, hi = min(lo + LS, T);
+    double P[D * D], Q[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) P[i] = (i / D == i % D) ? 1.0 : 0.0;
+    for (int t = hi - 1; t >= lo; --t) {
+      const double* G = elems + (size_t)t * ES;
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) acc += G[i * D + k] * P[k * D + j];
+          Q[i * D + j] = acc;
+        }
+#pragma unroll
+      for (int i = 0; i < D * D; ++i) P[i] = Q[i];
+    }
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) gsub[(size_t)s * D * D + i] = P[i];
+  }
+}
+
+// ---------------------------------------------------------------- noise
+
+template <int D>
+__device__ __forceinline__ void stream_normals(uint64_t key, double* xi) {
+#pragma unroll
+  for (int i = 0; i < D; ++i) xi[i] = normal_at(key, (uint64_t)i);
+}
+
+// ---------------------------------------------------------------- prefix scan
+// Shared-element prefix sampler.  CTA = chains [c_begin, c_end) (<= CG) over the
+// full horizon.  Thread (c, j): chain c (slow), sub-chunk j (fast).
+template <int D, int CG, int NS, int LS, bool PRE>
+__global__ void __launch_bounds__(CG* NS)
+    k_prefix_shared(int T, int C, const double* __restrict__ elems,
+                    const double* __restrict__ term, const double* __restrict__ gsub,
+                    NoiseArgs noise, double* __restrict__ traj) {
+  constexpr int S = NS * LS;
+  constexpr int ES = (2 * D * D + D + 1) & ~1;
+  constexpr int XSUB = LS * D + 2;          // padded sub-chunk block in the x tile
+  constexpr int XROW = NS * XSUB;           // per chain
+  constexpr int ESUB = LS * ES + 2;         // padded sub-chunk block in the element tile
+  constexpr int XT = CG * XROW;             // x tile doubles
+  constexpr int ET = NS * ESUB;             // element tile doubles
+  extern __shared__ __align__(16) double sm[];
+  double* xt[2] = {sm, sm + XT};
+  double* et[2] = {sm + 2 * XT, sm + 2 * XT + ET};
+  double* csub = sm + 2 * (XT + ET);        // [CG][NS][D]
+  double* xtop = csub + CG * NS * D;        // [CG][NS][D]
+  double* carry = xtop + CG * NS * D;       // [CG][D]
+
+  const int c_begin = (int)(((long long)blockIdx.x * C) / gridDim.x);
+  const int c_end = (int)(((long long)(blockIdx.x + 1) * C) / gridDim.x);
+  const int nc = c_end - c_begin;
+  const int tid = threadIdx.x;
+  const int cl = tid / NS, j = tid % NS;
+  const int c = c_begin + cl;
+  const bool active = cl < nc;
+  const long long row = (long long)(T + 1) * D;  // doubles per path
+
+  // terminal draw x_T = m_T + L_T xi (pit.cpp:85-87)
+  if (active && j == 0) {
+    double xi[D];
+    if (PRE) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) xi[i] = noise.terminal[(size_t)c * D + i];
+    } else {
+      stream_normals<D>(derive(noise.keys[c], kTerminalDraw, 0), xi);
+    }
+    double x[D];
+    r_matvec<D>(term + D, xi, x);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      x[i] = term[i] + x[i];
+      carry[cl * D + i] = x[i];
+      traj[(size_t)c * row + (size_t)T * D + i] = x[i];
+    }
+  }
+  if (T == 0) return;
+  const int K = (T + S - 1) / S;
+  uint64_t klabel = 0;
+  if (!PRE && active) klabel = derive_label(noise.keys[c], kBackwardNoise);
+
+  auto stage = [&](int k, int buf) {
+    const int t0 = k * S, t1 = min(t0 + S, T), len = t1 - t0;
+    // elements: contiguous len*ES doubles; 16 B chunks into padded sub-chunk blocks
+    const double* esrc = elems + (size_t)t0 * ES;
+    const int echunks = len * ES / 2;
+    for (int q = tid; q < echunks; q += CG * NS) {
+      const int off = q * 2;
+      const int s = off / (LS * ES), r = off % (LS * ES);
+      __pipeline_memcpy_async(et[buf] + s * ESUB + r, esrc + off, 16);
+    }
+    if (PRE) {
+      const int xn = len * D;
+      for (int q = tid; q < nc * xn; q += CG * NS) {
+        const int ch = q / xn, off = q % xn;
+        const int s = off / (LS * D), r = off % (LS * D);
+        __pipeline_memcpy_async(xt[buf] + ch * XROW + s * XSUB + r,
+                                noise.backward + ((size_t)(c_begin + ch) * T + t0) * D + off, 8);
+      }
+    }
+    __pipeline_commit();
+  };
+
+  stage(K - 1, (K - 1) & 1);
+  for (int k = K - 1; k >= 0; --k) {
+    const int buf = k & 1;
+    if (k > 0) stage(k - 1, (k - 1) & 1);
+    if (k > 0) __pipeline_wait_prior(1);
+    else __pipeline_wait_prior(0);
+    __syncthreads();
+    const int t0 = k * S, t1 = min(t0 + S, T);
+    const int lo = t0 + j * LS, hi = min(lo + LS, t1);
+    double* X = xt[buf] + cl * XROW + j * XSUB;      // rows lo.. of this sub-chunk
+    const double* E = et[buf] + j * ESUB;
+    // Phase A: realize noise c_t = off_t + L_t xi_t (pit.cpp:64-76) and reduce.
+    if (active) {
+      double y[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) y[i] = 0.0;
+      for (int t = hi - 1; t >= lo; --t) {
+        const int s = t - lo;
+        const double* e = E + s * ES;
+        double xi[D], cv[D];
+        if (PRE) {
+#pragma unroll
+          for (int i = 0; i < D; ++i) xi[i] = X[s * D + i];
+        } else {
+          stream_normals<D>(derive_index(klabel, (uint64_t)t), xi);
+        }
+        r_matvec<D>(e + D * D + D, xi, cv);
+        double gy[D];
+        r_matvec<D>(e, y, gy);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          cv[i] = e[D * D + i] + cv[i];
+          X[s * D + i] = cv[i];
+          y[i] = gy[i] + cv[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) csub[(cl * NS + j) * D + i] = y[i];
+    }
+    __syncthreads();
+    // Phase B: carry scan over the sub-chunk aggregates, top-down.
+    if (active && j == 0) {
+      double x[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) x[i] = carry[cl * D + i];
+      const int s0 = t0 / LS;
+      for (int jj = NS - 1; jj >= 0; --jj) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) xtop[(cl * NS + jj) * D + i] = x[i];
+        if (t0 + jj * LS >= t1) continue;
+        double gx[D];
+        r_matvec<D>(gsub + (size_t)(s0 + jj) * D * D, x, gx);
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = gx[i] + csub[(cl * NS + jj) * D + i];
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) carry[cl * D + i] = x[i];
+    }
+    __syncthreads();
+    // Phase C: expand x_t = G_t x_{t+1} + c_t.
+    if (active) {
+      double x[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) x[i] = xtop[(cl * NS + j) * D + i];
+      for (int t = hi - 1; t >= lo; --t) {
+        const int s = t - lo;
+        double gx[D];
+        r_matvec<D>(E + s * ES, x, gx);
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          x[i] = gx[i] + X[s * D + i];
+          X[s * D + i] = x[i];
+        }
+      }
+    }
+    __syncthreads();
+    // store the tile: rows [t0, t1) of each chain, coalesced 16 B
+    {
+      const int xn = (t1 - t0) * D;
+      for (int q = tid; q < nc * xn; q += CG * NS) {
+        const int ch = q / xn, off = q % xn;
+        const int s = off / (LS * D), r = off % (LS * D);
+        traj[(size_t)(c_begin + ch) * row + (size_t)t0 * D + off] = xt[buf][ch * XROW + s * XSUB + r];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int D, int CG, int NS, int LS>
+constexpr size_t prefix_smem_bytes() {
+  return sizeof(double) * (2 * (CG * NS * (LS * D + 2)) + 2 * (NS * (LS * ((2 * D * D + D + 1) & ~1) + 2)) +
+                           2 * CG * NS * D + CG * D);
+}
+
+// ---------------------------------------------------------------- sequential / per-path elements
+// Thread per path; elements either shared (es = 0) or per path.
+template <int D, bool PRE>
+__global__ void k_seq_sample(int T, int C, const double* __restrict__ elems, long long estride,
+                             const double* __restrict__ term, long long tstride, NoiseArgs noise,
+                             double* __restrict__ traj) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  constexpr int ES = (2 * D * D + D + 1) & ~1;
+  const double* E = elems + (size_t)c * estride;
+  const double* tm = term + (size_t)c * tstride;
+  const long long row = (long long)(T + 1) * D;
+  double x[D], xi[D];
+  if (PRE) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) xi[i] = noise.terminal[(size_t)c * D + i];
+  } else {
+    stream_normals<D>(derive(noise.keys[c], kTerminalDraw, 0), xi);
+  }
+  r_matvec<D>(tm + D, xi, x);
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    x[i] = tm[i] + x[i];
+    traj[(size_t)c * row + (size_t)T * D + i] = x[i];
+  }
+  const uint64_t kl = PRE ? 0 : derive_label(noise.keys[c], kBackwardNoise);
+  for (int t = T - 1; t >= 0; --t) {
+    const double* e = E + (size_t)t * ES;
+    if (PRE) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) xi[i] = noise.backward[((size_t)c * T + t) * D + i];
+    } else {
+      stream_normals<D>(derive_index(kl, (uint64_t)t), xi);
+    }
+    double cv[D], gx[D];
+    r_matvec<D>(e + D * D + D, xi, cv);
+    r_matvec<D>(e, x, gx);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      x[i] = gx[i] + (e[D * D + i] + cv[i]);
+      traj[(size_t)c * row + (size_t)t * D + i] = x[i];
+    }
+  }
+}
+
+// Per-path-element prefix sampler (aux-kernel backend): thread per (path,
+// sub-chunk) with in-thread sub-chunk products; sub-chunk carries scanned by
+// one thread per path.  Same fixed tree as k_prefix_shared.
+template <int D, int NS, int LS, bool PRE>
+__global__ void __launch_bounds__(NS)
+    k_prefix_private(int T, const double* __restrict__ elems, const double* __restrict__ term,
+                     NoiseArgs noise, double* __restrict__ traj) {
+  constexpr int S = NS * LS;
+  constexpr int ES = (2 * D * D + D + 1) & ~1;
+  __shared__ double csub[NS * D], gsub[NS * D * D], xtop[NS * D], carry[D];
+  const int c = blockIdx.x, j = threadIdx.x;
+  const double* E = elems + (size_t)c * T * ES;
+  const double* tm = term + (size_t)c * ((D * D + D + 1) & ~1);
+  const long long row = (long long)(T + 1) * D;
+  double* out = traj + (size_t)c * row;
+  if (j == 0) {
+    double xi[D], x[D];
+    if (PRE) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) xi[i] = noise.terminal[(size_t)c * D + i];
+    } else {
+      stream_normals<D>(derive(noise.keys[c], kTerminalDraw, 0), xi);
+    }
+    r_matvec<D>(tm + D, xi, x);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      x[i] = tm[i] + x[i];
+      carry[i] = x[i];
+      out[(size_t)T * D + i] = x[i];
+    }
+  }
+  if (T == 0) return;
+  const uint64_t kl = PRE ? 0 : derive_label(noise.keys[c], kBackwardNoise);
+  const int K = (T + S - 1) / S;
+  for (int k = K - 1; k >= 0; --k) {
+    __syncthreads();
+    const int t0 = k * S, t1 = min(t0 + S, T);
+    const int lo = t0 + j * LS, hi = min(lo + LS, t1);
+    double y[D], P[D * D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) y[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) P[i] = (i / D == i % D) ? 1.0 : 0.0;
+    for (int t = hi - 1; t >= lo; --t) {
+      const double* e = E + (size_t)t * ES;
+      double xi[D], cv[D], gy[D], Q[D * D];
+      if (PRE) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) xi[i] = noise.backward[((size_t)c * T + t) * D + i];
+      } else {
+        stream_normals<D>(derive_index(kl, (uint64_t)t), xi);
+      }
+      r_matvec<D>(e + D * D + D, xi, cv);
+      r_matvec<D>(e, y, gy);
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        cv[i] = e[D * D + i] + cv[i];
+        out[(size_t)t * D + i] = cv[i];  // park c_t in the output row
+        y[i] = gy[i] + cv[i];
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q = 0; q < D; ++q) acc += e[a * D + q] * P[q * D + b];
+          Q[a * D + b] = acc;
+        }
+#pragma unroll
+      for (int i = 0; i < D * D; ++i) P[i] = Q[i];
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) csub[j * D + i] = y[i];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) gsub[j * D * D + i] = P[i];
+    __syncthreads();
+    if (j == 0) {
+      double x[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) x[i] = carry[i];
+      for (int jj = NS - 1; jj >= 0; --jj) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) xtop[jj * D + i] = x[i];
+        if (t0 + jj * LS >= t1) continue;
+        double gx[D];
+        r_matvec<D>(gsub + jj * D * D, x, gx);
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = gx[i] + csub[jj * D + i];
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) carry[i] = x[i];
+    }
+    __syncthreads();
+    double x[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) x[i] = xtop[j * D + i];
+    for (int t = hi - 1; t >= lo; --t) {
+      const double* e = E + (size_t)t * ES;
+      double gx[D];
+      r_matvec<D>(e, x, gx);
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        x[i] = gx[i] + out[(size_t)t * D + i];
+        out[(size_t)t * D + i] = x[i];
+      }
+    }
+  }
+}
+
+}  // namespace auxmc_gpu
+
+namespace auxmc_gpu {
+
+__global__ void k_fanout_status(const int* st_fr, int fr_shared, int B, int* status) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x)
+    status[b] = st_fr[fr_shared ? 0 : b];
+}
+
+int launch_dnc(const DevModel& dm, int Bfr, int fr_shared, const double* elems,
+               const double* term, const NoiseArgs& nz, int B, double* traj, Arena& ws,
+               int* st_fr, cudaStream_t stream);
+
+namespace {
+
+constexpr int kCG = 8, kNS = 16, kLS = 8;      // shared-element prefix tiling
+constexpr int kNSp = 32, kLSp = 8;             // per-path prefix tiling
+
+template <int D>
+int run_prefix_shared(int T, int B, const double* elems, const double* term, Arena& ws,
+                      const NoiseArgs& nz, double* traj, cudaStream_t stream) {
+  const int n_sub = (T + kLS - 1) / kLS;
+  double* gsub = ws.take<double>((size_t)(n_sub > 0 ? n_sub : 1) * D * D);
+  if (ws.base == nullptr) return AUXMC_OK;
+  if (!gsub) return AUXMC_E_WORKSPACE;
+  if (T > 0) {
+    const int grid = std::min((n_sub + 127) / 128, 148 * 8);
+    AUXMC_LAUNCH(k_gsub<D>, grid, 128, 0, stream, elems, T, kLS, gsub);
+  }
+  constexpr size_t smem = prefix_smem_bytes<D, kCG, kNS, kLS>();
+  const int grid = std::max((B + kCG - 1) / kCG, std::min(B, num_sms()));
+  if (nz.kind == AUXMC_NOISE_PREDRAWN) {
+    auto kern = k_prefix_shared<D, kCG, kNS, kLS, true>;
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    AUXMC_LAUNCH(kern, grid, kCG * kNS, smem, stream, T, B, elems, term, gsub, nz, traj);
+  } else {
+    auto kern = k_prefix_shared<D, kCG, kNS, kLS, false>;
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    AUXMC_LAUNCH(kern, grid, kCG * kNS, smem, stream, T, B, elems, term, gsub, nz, traj);
+  }
+  return AUXMC_OK;
+}
+
+template <int D>
+int run_sampler(int sampler, int T, int B, int fr_shared, const double* elems,
+                const double* term, Arena& ws, const NoiseArgs& nz, double* traj,
+                cudaStream_t stream) {
+  const bool pre = nz.kind == AUXMC_NOISE_PREDRAWN;
+  if (sampler == AUXMC_SAMPLER_PREFIX && fr_shared)
+    return run_prefix_shared<D>(T, B, elems, term, ws, nz, traj, stream);
+  if (ws.base == nullptr) return AUXMC_OK;
+  const long long es = fr_shared ? 0 : (long long)T * elem_stride(D);
+  const long long ts = fr_shared ? 0 : term_stride(D);
+  if (sampler == AUXMC_SAMPLER_PREFIX) {
+    if (pre)
+      AUXMC_LAUNCH((k_prefix_private<D, kNSp, kLSp, true>), B, kNSp, 0, stream, T, elems, term, nz, traj);
+    else
+      AUXMC_LAUNCH((k_prefix_private<D, kNSp, kLSp, false>), B, kNSp, 0, stream, T, elems, term, nz, traj);
+    return AUXMC_OK;
+  }
+  const int grid = (B + 127) / 128;
+  if (pre)
+    AUXMC_LAUNCH((k_seq_sample<D, true>), grid, 128, 0, stream, T, B, elems, es, term, ts, nz, traj);
+  else
+    AUXMC_LAUNCH((k_seq_sample<D, false>), grid, 128, 0, stream, T, B, elems, es, term, ts, nz, traj);
+  return AUXMC_OK;
+}
+
+}  // namespace
+
+int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, const double* pc,
+                        int Bfr, double* elems, double* term, int* st_fr, int store_cov,
+                        cudaStream_t stream) {
+  const int d = dm.dx;
+  const int per = 9 * d * d + 4 * d + 4;
+  const long long n_items = (long long)Bfr * (dm.T + 1);
+  if (d > 16) {
+    const size_t smem = sizeof(double) * per;
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_bwd_elements<true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = (int)std::min<long long>(n_items, 148LL * 64);
+    AUXMC_LAUNCH(k_bwd_elements<true>, grid, 128, smem, stream, dm, fm, fc, pc, Bfr, elems, term,
+                 st_fr, store_cov);
+  } else {
+    const int warps = 4;
+    const size_t smem = sizeof(double) * per * warps;
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_bwd_elements<false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = (int)std::min<long long>((n_items + warps - 1) / warps, 148LL * 64);
+    AUXMC_LAUNCH(k_bwd_elements<false>, grid, 32 * warps, smem, stream, dm, fm, fc, pc, Bfr, elems,
+                 term, st_fr, store_cov);
+  }
+  return AUXMC_OK;
+}
+
+int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int fr_shared,
+                        const auxmc_noise* noise, int B, int sampler, double* traj, int* status,
+                        Arena& ws, cudaStream_t stream) {
+  const int d = dm.dx, T = dm.T;
+  const int Bfr = fr_shared ? 1 : B;
+  if (sampler < 0 || sampler > 2) return AUXMC_E_ARG;
+  double* elems = ws.take<double>((size_t)Bfr * (T > 0 ? T : 1) * elem_stride(d));
+  double* term = ws.take<double>((size_t)Bfr * term_stride(d));
+  int* st_fr = ws.take<int>((size_t)Bfr);
+  NoiseArgs nz{};
+  if (noise) {
+    nz.kind = noise->kind;
+    nz.keys = noise->keys;
+    nz.terminal = noise->terminal;
+    nz.backward = noise->backward;
+    nz.bridge = noise->bridge;
+    nz.n_bridge = noise->n_bridge;
+  }
+  if (ws.base != nullptr) {
+    if (!elems || !term || !st_fr) return AUXMC_E_WORKSPACE;
+    AUXMC_CUDA_TRY(cudaMemsetAsync(st_fr, 0, sizeof(int) * Bfr, stream));
+    int rc = launch_bwd_elements(dm, fr->filt_mean, fr->filt_cov, fr->pred_cov, Bfr, elems, term,
+                                 st_fr, sampler == AUXMC_SAMPLER_DNC ? 1 : 0, stream);
+    if (rc) return rc;
+  }
+  int rc = AUXMC_OK;
+  if (sampler == AUXMC_SAMPLER_DNC) {
+    rc = launch_dnc(dm, Bfr, fr_shared, elems, term, nz, B, traj, ws, st_fr, stream);
+  } else {
+    switch (d) {
+#define CASE(D) \
+  case D: rc = run_sampler<D>(sampler, T, B, fr_shared, elems, term, ws, nz, traj, stream); break;
+      CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+      default: rc = AUXMC_E_DIM;
+    }
+  }
+  if (rc || ws.base == nullptr) return rc;
+  AUXMC_LAUNCH(k_fanout_status, (B + 255) / 256, 256, 0, stream, st_fr, fr_shared, B, status);
+  return AUXMC_OK;
+}
+
+}  // namespace auxmc_gpu

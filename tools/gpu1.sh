@@ -1,0 +1,6 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_lgssm.py -x -q -m gpu 2>&1 | tail -30 > gpurun_out/pytest1.log
+cat gpurun_out/pytest1.log
+timeout 300 python tools/quick_c2.py 65536 1024 2>&1 | tail -20
