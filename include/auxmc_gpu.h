@@ -179,6 +179,7 @@ typedef struct {
   const double* F; const double* b; const double* Q; int nF;   /* count 1 or T */
   /* exact Gaussian potential rows q = max_exact_rows (target.cpp:65-70) */
   int q; int ne;            /* ne = 1 or T+1 */
+  int exact_tv;             /* 1 if the exact blocks differ across t (ne > 1, or emask mixed) */
   const double* eH; const double* ec; const double* eR;   /* [ne][q][dx], [ne][q], [ne][q][q] */
   const double* ey;         /* [T+1][q] */
   const uint8_t* emask;     /* [T+1] 1 where an exact block exists */

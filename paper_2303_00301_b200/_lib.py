@@ -46,7 +46,7 @@ class Target(C.Structure):
     _fields_ = [("kind", C.c_int), ("T", C.c_int), ("dx", C.c_int), ("ydim", C.c_int),
                 ("linear", C.c_int), ("m0", C.c_void_p), ("P0", C.c_void_p), ("F", C.c_void_p),
                 ("b", C.c_void_p), ("Q", C.c_void_p), ("nF", C.c_int), ("q", C.c_int),
-                ("ne", C.c_int), ("eH", C.c_void_p), ("ec", C.c_void_p), ("eR", C.c_void_p),
+                ("ne", C.c_int), ("exact_tv", C.c_int), ("eH", C.c_void_p), ("ec", C.c_void_p), ("eR", C.c_void_p),
                 ("ey", C.c_void_p), ("emask", C.c_void_p), ("data", C.c_void_p),
                 ("gmask", C.c_void_p), ("gH", C.c_void_p), ("gc", C.c_void_p),
                 ("gR", C.c_void_p), ("lz_sigma", C.c_double), ("lz_rho", C.c_double),

@@ -58,17 +58,21 @@ struct Arena {
 };
 
 // ---- lgssm model accessors (lgssm.hpp:34-40 broadcast rule) ----
+// One LGSSM, or a batch of LGSSMs sharing (T, dx, dy): each array has a
+// per-problem stride in doubles (0 = shared by the batch, the public API's
+// case; the auxiliary kernel uses per-chain F, b, R).
 struct DevModel {
   int T, dx, dy;
   const double *m0, *P0, *F, *b, *Q, *H, *c, *R;
   int nF, nb, nQ, nH, nc, nR;
+  long long sF, sb, sQ, sH, sc, sR;
   const uint8_t* mask;
-  __device__ __forceinline__ const double* Ft(int t) const { return F + (size_t)(nF > 1 ? t : 0) * dx * dx; }
-  __device__ __forceinline__ const double* bt(int t) const { return b + (size_t)(nb > 1 ? t : 0) * dx; }
-  __device__ __forceinline__ const double* Qt(int t) const { return Q + (size_t)(nQ > 1 ? t : 0) * dx * dx; }
-  __device__ __forceinline__ const double* Ht(int t) const { return H + (size_t)(nH > 1 ? t : 0) * dy * dx; }
-  __device__ __forceinline__ const double* ct(int t) const { return c + (size_t)(nc > 1 ? t : 0) * dy; }
-  __device__ __forceinline__ const double* Rt(int t) const { return R + (size_t)(nR > 1 ? t : 0) * dy * dy; }
+  __device__ __forceinline__ const double* Ft(int t, int k = 0) const { return F + (size_t)k * sF + (size_t)(nF > 1 ? t : 0) * dx * dx; }
+  __device__ __forceinline__ const double* bt(int t, int k = 0) const { return b + (size_t)k * sb + (size_t)(nb > 1 ? t : 0) * dx; }
+  __device__ __forceinline__ const double* Qt(int t, int k = 0) const { return Q + (size_t)k * sQ + (size_t)(nQ > 1 ? t : 0) * dx * dx; }
+  __device__ __forceinline__ const double* Ht(int t, int k = 0) const { return H + (size_t)k * sH + (size_t)(nH > 1 ? t : 0) * dy * dx; }
+  __device__ __forceinline__ const double* ct(int t, int k = 0) const { return c + (size_t)k * sc + (size_t)(nc > 1 ? t : 0) * dy; }
+  __device__ __forceinline__ const double* Rt(int t, int k = 0) const { return R + (size_t)k * sR + (size_t)(nR > 1 ? t : 0) * dy * dy; }
   __device__ __forceinline__ bool observed(int t) const { return mask == nullptr || mask[t] != 0; }
 };
 
@@ -77,6 +81,7 @@ inline DevModel to_dev(const auxmc_lgssm& m) {
   d.T = m.T; d.dx = m.dx; d.dy = m.dy;
   d.m0 = m.m0; d.P0 = m.P0; d.F = m.F; d.b = m.b; d.Q = m.Q; d.H = m.H; d.c = m.c; d.R = m.R;
   d.nF = m.nF; d.nb = m.nb; d.nQ = m.nQ; d.nH = m.nH; d.nc = m.nc; d.nR = m.nR;
+  d.sF = d.sb = d.sQ = d.sH = d.sc = d.sR = 0;
   d.mask = m.mask;
   return d;
 }

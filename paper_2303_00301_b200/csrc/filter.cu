@@ -61,9 +61,9 @@ __global__ void k_filter_seq(DevModel m, const double* __restrict__ obs, int B,
     g.sync();
     for (int t = 0; t <= T; ++t) {
       if (t > 0) {
-        const double* F = m.Ft(t - 1);
-        const double* bb = m.bt(t - 1);
-        const double* Q = m.Qt(t - 1);
+        const double* F = m.Ft(t - 1, b);
+        const double* bb = m.bt(t - 1, b);
+        const double* Q = m.Qt(t - 1, b);
         for (int i = g.lane; i < dx; i += g.size) {
           double s = 0.0;
           for (int j = 0; j < dx; ++j) s += F[i * dx + j] * mm[j];
@@ -87,9 +87,9 @@ __global__ void k_filter_seq(DevModel m, const double* __restrict__ obs, int B,
       }
       for (int i = g.lane; i < ddx; i += g.size) pc_out[(size_t)t * ddx + i] = p[i];
       if (m.observed(t)) {
-        const double* H = m.Ht(t);
-        const double* c = m.ct(t);
-        const double* R = m.Rt(t);
+        const double* H = m.Ht(t, b);
+        const double* c = m.ct(t, b);
+        const double* R = m.Rt(t, b);
         const double* y = y_all + (size_t)t * dy;
         for (int i = g.lane; i < dy; i += g.size) {
           double s = 0.0;

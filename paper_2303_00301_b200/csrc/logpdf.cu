@@ -10,11 +10,14 @@
 
 namespace auxmc_gpu {
 
-// Factor matrix j of a list: P0 (j = 0), Q_i (1..nQ), R_i (nQ+1..nQ+nR).
-__global__ void k_factor_list(DevModel m, double* Ls, double* logdet, int* status) {
+// Factor matrix j of a list: P0 (j = 0), then Q sets (nQb of nQ matrices),
+// then R sets (nRb of nR); a set per problem when that array is batch-strided.
+__global__ void k_factor_list(DevModel m, int nQb, int nRb, double* Ls, double* logdet,
+                              int* status) {
   extern __shared__ double smem[];
   const int dx = m.dx, dy = m.dy;
-  const int n_items = 1 + m.nQ + (dy > 0 ? m.nR : 0);
+  const int nq = nQb * m.nQ;
+  const int n_items = 1 + nq + (dy > 0 ? nRb * m.nR : 0);
   const int W = dx > dy ? dx : dy;
   Grp g = warp_group();
   const int gid = threadIdx.x >> 5, gpb = blockDim.x >> 5;
@@ -27,8 +30,15 @@ __global__ void k_factor_list(DevModel m, double* Ls, double* logdet, int* statu
     const double* src;
     int n;
     if (j == 0) { src = m.P0; n = dx; }
-    else if (j <= m.nQ) { src = m.Q + (size_t)(j - 1) * dx * dx; n = dx; }
-    else { src = m.R + (size_t)(j - 1 - m.nQ) * dy * dy; n = dy; }
+    else if (j <= nq) {
+      const int k = (j - 1) / m.nQ, i = (j - 1) % m.nQ;
+      src = m.Q + (size_t)k * m.sQ + (size_t)i * dx * dx;
+      n = dx;
+    } else {
+      const int k = (j - 1 - nq) / m.nR, i = (j - 1 - nq) % m.nR;
+      src = m.R + (size_t)k * m.sR + (size_t)i * dy * dy;
+      n = dy;
+    }
     for (int i = g.lane; i < n * n; i += g.size) {
       const int r = i / n, c = i % n;
       A[i] = (src[r * n + c] + src[c * n + r]) * 0.5;
@@ -48,7 +58,7 @@ __global__ void k_factor_list(DevModel m, double* Ls, double* logdet, int* statu
 }
 
 // term index k: 0 prior; 1..T transition t=k-1; T+1..2T+1 observation t=k-T-1.
-__global__ void k_path_terms(DevModel m, const double* __restrict__ obs, int obs_shared,
+__global__ void k_path_terms(DevModel m, const double* __restrict__ obs, long long obs_stride,
                              const double* __restrict__ traj, int B, const double* __restrict__ Ls,
                              const double* __restrict__ logdet, double* terms) {
   const int T = m.T, dx = m.dx, dy = m.dy;
@@ -71,14 +81,14 @@ __global__ void k_path_terms(DevModel m, const double* __restrict__ obs, int obs
     } else if (k <= T) {
       const int t = k - 1;
       nn = dx;
-      const double* F = m.Ft(t);
-      const double* bb = m.bt(t);
+      const double* F = m.Ft(t, b);
+      const double* bb = m.bt(t, b);
       for (int i = 0; i < dx; ++i) {
         double s = 0.0;
         for (int j = 0; j < dx; ++j) s += F[i * dx + j] * x[(size_t)t * dx + j];
         r[i] = x[(size_t)(t + 1) * dx + i] - (s + bb[i]);
       }
-      const int j = 1 + (m.nQ > 1 ? t : 0);
+      const int j = 1 + (m.sQ ? b * m.nQ : 0) + (m.nQ > 1 ? t : 0);
       L = Ls + (size_t)j * W * W;
       ld = logdet[j];
     } else {
@@ -88,15 +98,16 @@ __global__ void k_path_terms(DevModel m, const double* __restrict__ obs, int obs
         continue;
       }
       nn = dy;
-      const double* H = m.Ht(t);
-      const double* cc = m.ct(t);
-      const double* y = obs + (size_t)(obs_shared ? 0 : b) * (T + 1) * dy + (size_t)t * dy;
+      const double* H = m.Ht(t, b);
+      const double* cc = m.ct(t, b);
+      const double* y = obs + (size_t)b * obs_stride + (size_t)t * dy;
       for (int i = 0; i < dy; ++i) {
         double s = 0.0;
         for (int j = 0; j < dx; ++j) s += H[i * dx + j] * x[(size_t)t * dx + j];
         r[i] = y[i] - (s + cc[i]);
       }
-      const int j = 1 + m.nQ + (m.nR > 1 ? t : 0);
+      const int nq = (m.sQ ? B : 1) * m.nQ;
+      const int j = 1 + nq + (m.sR ? b * m.nR : 0) + (m.nR > 1 ? t : 0);
       L = Ls + (size_t)j * W * W;
       ld = logdet[j];
     }
@@ -128,6 +139,42 @@ __global__ void k_path_sum(int T, int B, const double* terms, const uint8_t* mas
 
 }  // namespace auxmc_gpu
 
+namespace auxmc_gpu {
+
+int launch_path_logpdf(const DevModel& dm, const double* obs, long long obs_stride,
+                       const double* traj, const double* log_marginal, int lm_shared, int B,
+                       double* out, int* status, cudaStream_t s) {
+  const int W = dm.dx > dm.dy ? dm.dx : dm.dy;
+  const int nQb = dm.sQ ? B : 1, nRb = dm.sR ? B : 1;
+  const int n_mats = 1 + nQb * dm.nQ + (dm.dy > 0 ? nRb * dm.nR : 0);
+  const int K = 2 * dm.T + 2;
+  double *Ls = nullptr, *logdet = nullptr, *terms = nullptr;
+  int* fst = nullptr;
+  AUXMC_CUDA_TRY(cudaMallocAsync(&Ls, sizeof(double) * n_mats * W * W, s));
+  AUXMC_CUDA_TRY(cudaMallocAsync(&logdet, sizeof(double) * n_mats, s));
+  AUXMC_CUDA_TRY(cudaMallocAsync(&terms, sizeof(double) * (size_t)B * K, s));
+  AUXMC_CUDA_TRY(cudaMallocAsync(&fst, sizeof(int), s));
+  AUXMC_CUDA_TRY(cudaMemsetAsync(fst, 0, sizeof(int), s));
+  const int warps = 4;
+  const size_t smem = sizeof(double) * (3 * W * W + 4) * warps;
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_factor_list, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  AUXMC_LAUNCH(k_factor_list, std::min((n_mats + warps - 1) / warps, 148 * 8), 32 * warps, smem,
+               s, dm, nQb, nRb, Ls, logdet, fst);
+  const long long n = (long long)B * K;
+  AUXMC_LAUNCH(k_path_terms, (int)std::min<long long>((n + 127) / 128, 148LL * 64), 128, 0, s, dm,
+               obs, obs_stride, traj, B, Ls, logdet, terms);
+  AUXMC_LAUNCH(k_path_sum, (B + 127) / 128, 128, 0, s, dm.T, B, terms, dm.mask, dm.dy,
+               log_marginal, lm_shared, fst, out, status);
+  cudaFreeAsync(Ls, s);
+  cudaFreeAsync(logdet, s);
+  cudaFreeAsync(terms, s);
+  cudaFreeAsync(fst, s);
+  return AUXMC_OK;
+}
+
+}  // namespace auxmc_gpu
+
 using namespace auxmc_gpu;
 
 extern "C" int auxmc_path_logpdf(const auxmc_lgssm* model, const double* obs, int obs_shared,
@@ -141,31 +188,6 @@ extern "C" int auxmc_path_logpdf(const auxmc_lgssm* model, const double* obs, in
     return AUXMC_E_ARG;
   if (B == 0) return AUXMC_OK;
   const DevModel dm = to_dev(*model);
-  const int W = dm.dx > dm.dy ? dm.dx : dm.dy;
-  const int n_mats = 1 + dm.nQ + (dm.dy > 0 ? dm.nR : 0);
-  const int K = 2 * dm.T + 2;
-  cudaStream_t s = (cudaStream_t)stream;
-  double *Ls = nullptr, *logdet = nullptr, *terms = nullptr;
-  int* fst = nullptr;
-  AUXMC_CUDA_TRY(cudaMallocAsync(&Ls, sizeof(double) * n_mats * W * W, s));
-  AUXMC_CUDA_TRY(cudaMallocAsync(&logdet, sizeof(double) * n_mats, s));
-  AUXMC_CUDA_TRY(cudaMallocAsync(&terms, sizeof(double) * (size_t)B * K, s));
-  AUXMC_CUDA_TRY(cudaMallocAsync(&fst, sizeof(int), s));
-  AUXMC_CUDA_TRY(cudaMemsetAsync(fst, 0, sizeof(int), s));
-  const int warps = 4;
-  const size_t smem = sizeof(double) * (3 * W * W + 4) * warps;
-  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_factor_list, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-  AUXMC_LAUNCH(k_factor_list, std::min((n_mats + warps - 1) / warps, 148 * 8), 32 * warps, smem,
-               s, dm, Ls, logdet, fst);
-  const long long n = (long long)B * K;
-  AUXMC_LAUNCH(k_path_terms, (int)std::min<long long>((n + 127) / 128, 148LL * 64), 128, 0, s, dm,
-               obs, obs_shared, traj, B, Ls, logdet, terms);
-  AUXMC_LAUNCH(k_path_sum, (B + 127) / 128, 128, 0, s, dm.T, B, terms, dm.mask, dm.dy,
-               fr->log_marginal, fr_shared, fst, out, status);
-  cudaFreeAsync(Ls, s);
-  cudaFreeAsync(logdet, s);
-  cudaFreeAsync(terms, s);
-  cudaFreeAsync(fst, s);
-  return AUXMC_OK;
+  return launch_path_logpdf(dm, obs, obs_shared ? 0 : (long long)(dm.T + 1) * dm.dy, traj,
+                            fr->log_marginal, fr_shared, B, out, status, (cudaStream_t)stream);
 }

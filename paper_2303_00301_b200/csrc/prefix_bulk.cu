@@ -1,0 +1,365 @@
+// prefix_bulk.cu — bulk-copy (1-D TMA) variant of the shared-element prefix
+// sampler (pit::prefix_sample, pit.cpp:78-115) for even state dimension.
+//
+// Same fixed reduce-then-scan tree family as prefix.cu, with all chain I/O done
+// by the TMA engine: per superchunk, one bulk copy stages the packed elements
+// and scan tables, one bulk copy per chain stages that chain's noise rows, and
+// one bulk store per chain writes its path rows from shared memory.  No thread
+// issues a global load or store in the steady state, so HBM sees full sectors
+// in both directions.
+//
+// Thread map (8 warps): lane = slot + 8 q, slot = chain of the CTA (<= 8),
+// sub-chunk j = 4 warp + q.  Sub-chunk carries are scanned in two levels:
+// Kogge-Stone over the 4 sub-chunks of a warp (shuffles, chain-independent
+// G-span tables), then a serial pass over the 8 warp aggregates per chain.
+#include "common.cuh"
+#include "dense.cuh"
+#include "rng.cuh"
+#include "tma.cuh"
+
+namespace auxmc_gpu {
+
+template <int D>
+struct BulkGeom {
+  static constexpr int LS = 16 / D;        // steps per sub-chunk (D = 2, 4)
+  static constexpr int NSUB = 32, WARPS = 8, SLOTS = 8;
+  static constexpr int S = NSUB * LS;      // steps per superchunk
+  static constexpr int LP = D * (D + 1) / 2;
+  static constexpr int ES = D * D + D + LP;
+  static constexpr int SUB = LS * ES + ((LS * ES) % 2 == 0 ? 1 : 0);  // odd: spreads a warp's blocks
+  static constexpr int EB = NSUB * SUB;
+  static constexpr int TAB = 3 * NSUB * D * D;  // Gsub | Gpair | Gin
+  static constexpr int TB = (EB + TAB + 1) & ~1;
+  static constexpr int ROW = S * D + 2;    // io row stride: slot stride = 4 banks
+  static constexpr int IOB = SLOTS * ROW;
+  static constexpr int STAGES = 2;         // in: (tables + noise) double-buffered
+  static constexpr int STG = TB + IOB;
+  static constexpr int CS = D + 2;         // per-(warp, slot) carry stride: conflict-free LDS.128
+  // + 2 out tiles (paths) so a bulk store drains while the next superchunk computes
+  static constexpr size_t SMEM =
+      sizeof(double) * (STAGES * STG + 2 * IOB + 2 * SLOTS * WARPS * CS + SLOTS * D) +
+      STAGES * sizeof(uint64_t);
+};
+
+template <int D>
+__device__ __forceinline__ void mat_mul(const double* A, const double* B, double* C) {
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < D; ++q) acc += A[a * D + q] * B[q * D + b];
+      C[a * D + b] = acc;
+    }
+}
+
+// elements + Gsub per (superchunk, sub-chunk)
+template <int D>
+__global__ void k_bulk_pack1(const double* __restrict__ elems, int T, double* tiles) {
+  using G = BulkGeom<D>;
+  const int n_sub = ((T + G::S - 1) / G::S) * G::NSUB;
+  const int ESg = elem_stride(D);
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_sub; s += gridDim.x * blockDim.x) {
+    const int k = s / G::NSUB, j = s % G::NSUB;
+    double* tile = tiles + (size_t)k * G::TB;
+    double* blk = tile + j * G::SUB;
+    const int lo = k * G::S + j * G::LS;
+    double P[D * D], Q[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) P[i] = (i / D == i % D) ? 1.0 : 0.0;
+    for (int q = G::LS - 1; q >= 0; --q) {
+      const int t = lo + q;
+      double* out = blk + q * G::ES;
+      if (t >= T) {
+        for (int i = 0; i < G::ES; ++i) out[i] = 0.0;
+        continue;
+      }
+      const double* e = elems + (size_t)t * ESg;
+#pragma unroll
+      for (int i = 0; i < D * D + D; ++i) out[i] = e[i];
+      int w = 0;
+#pragma unroll
+      for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c) out[D * D + D + w++] = e[D * D + D + r * D + c];
+      mat_mul<D>(e, P, Q);
+#pragma unroll
+      for (int i = 0; i < D * D; ++i) P[i] = Q[i];
+    }
+    blk[G::LS * G::ES] = 0.0;
+    double* gs = tile + G::EB + j * D * D;
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) gs[i] = P[i];
+    if (j == 0 && G::TB > G::EB + G::TAB) tile[G::TB - 1] = 0.0;
+  }
+}
+
+// Gpair_j = Gsub_j Gsub_{j+1} (j % 4 <= 2); Gin_j = Gsub_j ... Gsub_{4(j/4)+3}
+template <int D>
+__global__ void k_bulk_pack2(int T, double* tiles) {
+  using G = BulkGeom<D>;
+  const int n_sub = ((T + G::S - 1) / G::S) * G::NSUB;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_sub; s += gridDim.x * blockDim.x) {
+    const int k = s / G::NSUB, j = s % G::NSUB;
+    double* tile = tiles + (size_t)k * G::TB;
+    const double* gsub = tile + G::EB;
+    double* gpair = tile + G::EB + G::NSUB * D * D;
+    double* gin = gpair + G::NSUB * D * D;
+    const int gend = 4 * (j / 4) + 3;
+    double P[D * D], Q[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) P[i] = gsub[gend * D * D + i];
+    for (int jj = gend - 1; jj >= j; --jj) {
+      mat_mul<D>(gsub + jj * D * D, P, Q);
+#pragma unroll
+      for (int i = 0; i < D * D; ++i) P[i] = Q[i];
+    }
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) gin[j * D * D + i] = P[i];
+    if (j < gend) {
+      mat_mul<D>(gsub + j * D * D, gsub + (j + 1) * D * D, Q);
+#pragma unroll
+      for (int i = 0; i < D * D; ++i) gpair[j * D * D + i] = Q[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < D * D; ++i) gpair[j * D * D + i] = 0.0;
+    }
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void shfl_down_vec(const double* v, double* out, int delta) {
+#pragma unroll
+  for (int i = 0; i < D; ++i) out[i] = __shfl_down_sync(0xffffffffu, v[i], delta);
+}
+
+template <int D, bool PRE>
+__global__ void __launch_bounds__(BulkGeom<D>::WARPS * 32, 1)
+    k_prefix_bulk(int T, int C, const double* __restrict__ tiles, const double* __restrict__ term,
+                  NoiseArgs noise, double* __restrict__ traj) {
+  using G = BulkGeom<D>;
+  constexpr int LS = G::LS, ES = G::ES, S = G::S, NS = G::NSUB, W = G::WARPS;
+  extern __shared__ __align__(16) double sm[];
+  constexpr int CS = G::CS;
+  auto tile = [&](int b) { return sm + b * G::STG; };
+  auto xit = [&](int b) { return sm + b * G::STG + G::TB; };
+  auto xot = [&](int b) { return sm + G::STAGES * G::STG + b * G::IOB; };
+  double* cagg = sm + G::STAGES * G::STG + 2 * G::IOB;  // [W][SLOTS][CS]
+  double* xwtop = cagg + G::SLOTS * W * CS;    // [W][SLOTS][CS]
+  double* carry = xwtop + G::SLOTS * W * CS;   // [SLOTS][D]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(carry + G::SLOTS * D);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int slot = lane & 7, q = lane >> 3, j = warp * 4 + q;
+  const int c_begin = (int)(((long long)blockIdx.x * C) / gridDim.x);
+  const int c_end = (int)(((long long)(blockIdx.x + 1) * C) / gridDim.x);
+  const int nc = c_end - c_begin;
+  const int c = c_begin + slot;
+  const bool active = slot < nc;
+  const long long row = (long long)(T + 1) * D;
+
+  if (tid == 0) {
+    for (int b = 0; b < G::STAGES; ++b) mbar_init(&bar[b], 1);
+    mbar_fence_init();
+  }
+  if (active && j == 0) {  // x_T = m_T + L_T xi (pit.cpp:85-87)
+    double xi[D], x[D];
+    if (PRE) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) xi[i] = noise.terminal[(size_t)c * D + i];
+    } else {
+      const uint64_t k = derive(noise.keys[c], kTerminalDraw, 0);
+#pragma unroll
+      for (int i = 0; i < D; ++i) xi[i] = normal_at(k, (uint64_t)i);
+    }
+    r_matvec<D>(term + D, xi, x);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      x[i] = term[i] + x[i];
+      carry[slot * D + i] = x[i];
+      traj[(size_t)c * row + (size_t)T * D + i] = x[i];
+    }
+  }
+  __syncthreads();
+  if (T == 0) return;
+  const int K = (T + S - 1) / S;
+  auto issue = [&](int k) {
+    const int b = k % G::STAGES, t0 = k * S, len = min(S, T - t0);
+    const unsigned tb = G::TB * sizeof(double);
+    const unsigned xb = (unsigned)(len * D * sizeof(double));
+    mbar_expect_tx(&bar[b], tb + (PRE ? xb * nc : 0u));
+    bulk_g2s(tile(b), tiles + (size_t)k * G::TB, tb, &bar[b]);
+    if (PRE)
+      for (int ch = 0; ch < nc; ++ch)
+        bulk_g2s(xit(b) + ch * G::ROW, noise.backward + ((size_t)(c_begin + ch) * T + t0) * D, xb,
+                 &bar[b]);
+  };
+  if (tid == 0) issue(K - 1);
+  unsigned phase_bits = 0u;
+  uint64_t klabel = 0;
+  if (!PRE && active) klabel = derive_label(noise.keys[c], kBackwardNoise);
+
+  for (int k = K - 1; k >= 0; --k) {
+    const int buf = k % G::STAGES;
+    if (tid == 0 && k > 0) issue(k - 1);  // stage (k-1) % 2 was released by superchunk k+1
+    mbar_wait(&bar[buf], (phase_bits >> buf) & 1u);
+    phase_bits ^= 1u << buf;
+    const int t0 = k * S, t1 = min(t0 + S, T);
+    const int lo = t0 + j * LS;
+    const bool full = (t1 - t0) == S;
+    const double* E = tile(buf) + j * G::SUB;
+    const double* gsub = tile(buf) + G::EB;
+    const double* gpair = gsub + NS * D * D;
+    const double* gin = gpair + NS * D * D;
+    double* X = xit(buf) + slot * G::ROW + j * LS * D;
+    // Phase A: realize c_t = off_t + L_t xi_t and reduce the sub-chunk (zero carry)
+    double cs[LS * D], y[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) y[i] = 0.0;
+#pragma unroll
+    for (int s = LS - 1; s >= 0; --s) {
+      const int t = lo + s;
+      if (full || t < t1) {  // inactive slots compute on scratch rows; only live rows are stored
+        const double* e = E + s * ES;
+        double xi[D];
+        if (PRE) {
+#pragma unroll
+          for (int i = 0; i < D; i += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(X + s * D + i);
+            xi[i] = v.x;
+            xi[i + 1] = v.y;
+          }
+        } else {
+          const uint64_t key = derive_index(klabel, (uint64_t)t);
+#pragma unroll
+          for (int i = 0; i < D; ++i) xi[i] = normal_at(key, (uint64_t)i);
+        }
+        double gy[D];
+        r_matvec<D>(e, y, gy);
+        int w = 0;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          double acc = 0.0;
+#pragma unroll
+          for (int cc = 0; cc <= r; ++cc) acc += e[D * D + D + w++] * xi[cc];
+          const double cv = e[D * D + r] + acc;
+          cs[s * D + r] = cv;
+          y[r] = gy[r] + cv;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < D; ++r) cs[s * D + r] = 0.0;
+      }
+    }
+    // Kogge-Stone over the warp's 4 sub-chunks (suffix direction): y -> c over [j, group end)
+    {
+      double yn[D], gy[D];
+      shfl_down_vec<D>(y, yn, 8);
+      if (q < 3) {
+        r_matvec<D>(gsub + j * D * D, yn, gy);
+#pragma unroll
+        for (int i = 0; i < D; ++i) y[i] = gy[i] + y[i];
+      }
+      shfl_down_vec<D>(y, yn, 16);
+      if (q < 2) {
+        r_matvec<D>(gpair + j * D * D, yn, gy);
+#pragma unroll
+        for (int i = 0; i < D; ++i) y[i] = gy[i] + y[i];
+      }
+    }
+    if (q == 0) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) cagg[(warp * G::SLOTS + slot) * CS + i] = y[i];
+    }
+    if (tid == 0) bulk_wait_read<1>();  // the store of superchunk k+2 has left xot(k & 1)
+    __syncthreads();
+    // Phase B: serial pass over the 8 warp aggregates of each chain, top-down
+    if (warp == 0 && lane < 8 && active) {
+      double x[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) x[i] = carry[slot * D + i];
+      for (int w = W - 1; w >= 0; --w) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) xwtop[(w * G::SLOTS + slot) * CS + i] = x[i];
+        if (t0 + 4 * w * LS >= t1) continue;
+        double gx[D];
+        r_matvec<D>(gin + 4 * w * D * D, x, gx);
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = gx[i] + cagg[(w * G::SLOTS + slot) * CS + i];
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) carry[slot * D + i] = x[i];
+    }
+    __syncthreads();
+    // Phase C: x at the top of each sub-chunk, then expand x_t = G_t x_{t+1} + c_t
+    {
+      double xt[D], xb[D], xn[D], x[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) xt[i] = xwtop[(warp * G::SLOTS + slot) * CS + i];
+      r_matvec<D>(gin + j * D * D, xt, xb);
+#pragma unroll
+      for (int i = 0; i < D; ++i) xb[i] = xb[i] + y[i];
+      shfl_down_vec<D>(xb, xn, 8);
+#pragma unroll
+      for (int i = 0; i < D; ++i) x[i] = q < 3 ? xn[i] : xt[i];
+      double* XO = xot(k & 1) + slot * G::ROW + j * LS * D;
+#pragma unroll
+      for (int s = LS - 1; s >= 0; --s) {
+        const int t = lo + s;
+        if (full || t < t1) {
+          double gx[D];
+          r_matvec<D>(E + s * ES, x, gx);
+#pragma unroll
+          for (int i = 0; i < D; ++i) x[i] = gx[i] + cs[s * D + i];
+#pragma unroll
+          for (int i = 0; i < D; i += 2)
+            *reinterpret_cast<double2*>(XO + s * D + i) = make_double2(x[i], x[i + 1]);
+        }
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned xb = (unsigned)((t1 - t0) * D * sizeof(double));
+      for (int ch = 0; ch < nc; ++ch)
+        bulk_s2g(traj + (size_t)(c_begin + ch) * row + (size_t)t0 * D, xot(k & 1) + ch * G::ROW, xb);
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait<0>();
+}
+
+template <int D>
+int run_prefix_bulk(int T, int B, const double* elems, const double* term, Arena& ws,
+                    const NoiseArgs& nz, double* traj, cudaStream_t stream) {
+  using G = BulkGeom<D>;
+  const int K = T > 0 ? (T + G::S - 1) / G::S : 1;
+  double* tiles = ws.take<double>((size_t)K * G::TB);
+  if (ws.base == nullptr) return AUXMC_OK;
+  if (!tiles) return AUXMC_E_WORKSPACE;
+  if (T > 0) {
+    const int n_sub = K * G::NSUB;
+    const int grid = std::min((n_sub + 127) / 128, 148 * 16);
+    AUXMC_LAUNCH(k_bulk_pack1<D>, grid, 128, 0, stream, elems, T, tiles);
+    AUXMC_LAUNCH(k_bulk_pack2<D>, grid, 128, 0, stream, T, tiles);
+  }
+  const int grid = std::max((B + G::SLOTS - 1) / G::SLOTS, std::min(B, num_sms()));
+  if (nz.kind == AUXMC_NOISE_PREDRAWN) {
+    auto kern = k_prefix_bulk<D, true>;
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    AUXMC_LAUNCH(kern, grid, G::WARPS * 32, G::SMEM, stream, T, B, tiles, term, nz, traj);
+  } else {
+    auto kern = k_prefix_bulk<D, false>;
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    AUXMC_LAUNCH(kern, grid, G::WARPS * 32, G::SMEM, stream, T, B, tiles, term, nz, traj);
+  }
+  return AUXMC_OK;
+}
+
+template int run_prefix_bulk<2>(int, int, const double*, const double*, Arena&, const NoiseArgs&,
+                                double*, cudaStream_t);
+template int run_prefix_bulk<4>(int, int, const double*, const double*, Arena&, const NoiseArgs&,
+                                double*, cudaStream_t);
+
+}  // namespace auxmc_gpu

@@ -13,8 +13,6 @@
 //    the output is bit-deterministic; noise is consumed by address (kBackwardNoise, t),
 //    never by evaluation order (rng.hpp:128-137).
 //  * k_seq: lgssm::backward_sample (lgssm.cpp:151-177), thread per path.
-#include <cuda_pipeline.h>
-
 #include "common.cuh"
 #include "dense.cuh"
 #include "rng.cuh"
@@ -29,7 +27,7 @@ __device__ int g_flip_backward_gain = 0;  // testhooks::flip_backward_gain (test
 __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel& m, int t,
                                                    const double* fm, const double* fc,
                                                    const double* pc, double* sm, int* flag,
-                                                   double* out /* G | off | L (or Λ) */,
+                                                   double* out /* G | off | L (or Λ) */, int k,
                                                    int store_cov) {
   const int d = m.dx, dd = d * d;
   double* P = sm;
@@ -43,7 +41,7 @@ __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel&
   double* scr = G + dd;
   double* v = scr + dd;
   double* red = v + 2 * d;
-  const double* Ft = m.Ft(t);
+  const double* Ft = m.Ft(t, k);
   g_copy(g, dd, fc + (size_t)t * dd, P);
   g_copy(g, dd, Ft, F);
   g_copy(g, dd, pc + (size_t)(t + 1) * dd, S);
@@ -70,7 +68,7 @@ __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel&
   }
   // offset = m_t - G (F m_t + b_t)
   const double* mt = fm + (size_t)t * d;
-  const double* bt = m.bt(t);
+  const double* bt = m.bt(t, k);
   for (int i = g.lane; i < d; i += g.size) {
     double s = 0.0;
     for (int j = 0; j < d; ++j) s += F[i * d + j] * mt[j];
@@ -92,7 +90,7 @@ __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel&
   g.sync();
   g_mm_nt(g, d, d, d, W, A, X);  // X = A P A^T
   g.sync();
-  g_copy(g, dd, m.Qt(t), S);
+  g_copy(g, dd, m.Qt(t, k), S);
   g.sync();
   g_mm(g, d, d, d, G, S, W);
   g.sync();
@@ -152,39 +150,10 @@ __global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
       for (int i = g.lane; i < dd; i += g.size) out[d + i] = L[i];
     } else {
       st = backward_step_group(g, m, t, fm, fc, pc, sm, flag,
-                               elems + ((size_t)b * T + t) * elem_stride(d), store_cov);
+                               elems + ((size_t)b * T + t) * elem_stride(d), b, store_cov);
     }
     if (st && g.lane == 0) atomicMax(status + b, st);
     g.sync();
-  }
-}
-
-// Gsub[s] = G_lo ... G_{hi-1} over the global sub-chunk s (shared elements only).
-template <int D>
-__global__ void k_gsub(const double* __restrict__ elems, int T, int LS, double* gsub) {
-  const int n_sub = (T + LS - 1) / LS;
-  const int ES = elem_stride(D);
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_sub; s += gridDim.x * blockDim.x) {
-    const int lo = s * LS, hi = min(lo + LS, T);
-    double P[D * D], Q[D * D];
-#pragma unroll
-    for (int i = 0; i < D * D; ++i) P[i] = (i / D == i % D) ? 1.0 : 0.0;
-    for (int t = hi - 1; t >= lo; --t) {
-      const double* G = elems + (size_t)t * ES;
-#pragma unroll
-      for (int i = 0; i < D; ++i)
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < D; ++k) acc += G[i * D + k] * P[k * D + j];
-          Q[i * D + j] = acc;
-        }
-#pragma unroll
-      for (int i = 0; i < D * D; ++i) P[i] = Q[i];
-    }
-#pragma unroll
-    for (int i = 0; i < D * D; ++i) gsub[(size_t)s * D * D + i] = P[i];
   }
 }
 
@@ -194,177 +163,6 @@ template <int D>
 __device__ __forceinline__ void stream_normals(uint64_t key, double* xi) {
 #pragma unroll
   for (int i = 0; i < D; ++i) xi[i] = normal_at(key, (uint64_t)i);
-}
-
-// ---------------------------------------------------------------- prefix scan
-// Shared-element prefix sampler.  CTA = chains [c_begin, c_end) (<= CG) over the
-// full horizon.  Thread (c, j): chain c (slow), sub-chunk j (fast).
-template <int D, int CG, int NS, int LS, bool PRE>
-__global__ void __launch_bounds__(CG* NS)
-    k_prefix_shared(int T, int C, const double* __restrict__ elems,
-                    const double* __restrict__ term, const double* __restrict__ gsub,
-                    NoiseArgs noise, double* __restrict__ traj) {
-  constexpr int S = NS * LS;
-  constexpr int ES = (2 * D * D + D + 1) & ~1;
-  constexpr int XSUB = LS * D + 2;          // padded sub-chunk block in the x tile
-  constexpr int XROW = NS * XSUB;           // per chain
-  constexpr int ESUB = LS * ES + 2;         // padded sub-chunk block in the element tile
-  constexpr int XT = CG * XROW;             // x tile doubles
-  constexpr int ET = NS * ESUB;             // element tile doubles
-  extern __shared__ __align__(16) double sm[];
-  double* xt[2] = {sm, sm + XT};
-  double* et[2] = {sm + 2 * XT, sm + 2 * XT + ET};
-  double* csub = sm + 2 * (XT + ET);        // [CG][NS][D]
-  double* xtop = csub + CG * NS * D;        // [CG][NS][D]
-  double* carry = xtop + CG * NS * D;       // [CG][D]
-
-  const int c_begin = (int)(((long long)blockIdx.x * C) / gridDim.x);
-  const int c_end = (int)(((long long)(blockIdx.x + 1) * C) / gridDim.x);
-  const int nc = c_end - c_begin;
-  const int tid = threadIdx.x;
-  const int cl = tid / NS, j = tid % NS;
-  const int c = c_begin + cl;
-  const bool active = cl < nc;
-  const long long row = (long long)(T + 1) * D;  // doubles per path
-
-  // terminal draw x_T = m_T + L_T xi (pit.cpp:85-87)
-  if (active && j == 0) {
-    double xi[D];
-    if (PRE) {
-#pragma unroll
-      for (int i = 0; i < D; ++i) xi[i] = noise.terminal[(size_t)c * D + i];
-    } else {
-      stream_normals<D>(derive(noise.keys[c], kTerminalDraw, 0), xi);
-    }
-    double x[D];
-    r_matvec<D>(term + D, xi, x);
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      x[i] = term[i] + x[i];
-      carry[cl * D + i] = x[i];
-      traj[(size_t)c * row + (size_t)T * D + i] = x[i];
-    }
-  }
-  if (T == 0) return;
-  const int K = (T + S - 1) / S;
-  uint64_t klabel = 0;
-  if (!PRE && active) klabel = derive_label(noise.keys[c], kBackwardNoise);
-
-  auto stage = [&](int k, int buf) {
-    const int t0 = k * S, t1 = min(t0 + S, T), len = t1 - t0;
-    // elements: contiguous len*ES doubles; 16 B chunks into padded sub-chunk blocks
-    const double* esrc = elems + (size_t)t0 * ES;
-    const int echunks = len * ES / 2;
-    for (int q = tid; q < echunks; q += CG * NS) {
-      const int off = q * 2;
-      const int s = off / (LS * ES), r = off % (LS * ES);
-      __pipeline_memcpy_async(et[buf] + s * ESUB + r, esrc + off, 16);
-    }
-    if (PRE) {
-      const int xn = len * D;
-      for (int q = tid; q < nc * xn; q += CG * NS) {
-        const int ch = q / xn, off = q % xn;
-        const int s = off / (LS * D), r = off % (LS * D);
-        __pipeline_memcpy_async(xt[buf] + ch * XROW + s * XSUB + r,
-                                noise.backward + ((size_t)(c_begin + ch) * T + t0) * D + off, 8);
-      }
-    }
-    __pipeline_commit();
-  };
-
-  stage(K - 1, (K - 1) & 1);
-  for (int k = K - 1; k >= 0; --k) {
-    const int buf = k & 1;
-    if (k > 0) stage(k - 1, (k - 1) & 1);
-    if (k > 0) __pipeline_wait_prior(1);
-    else __pipeline_wait_prior(0);
-    __syncthreads();
-    const int t0 = k * S, t1 = min(t0 + S, T);
-    const int lo = t0 + j * LS, hi = min(lo + LS, t1);
-    double* X = xt[buf] + cl * XROW + j * XSUB;      // rows lo.. of this sub-chunk
-    const double* E = et[buf] + j * ESUB;
-    // Phase A: realize noise c_t = off_t + L_t xi_t (pit.cpp:64-76) and reduce.
-    if (active) {
-      double y[D];
-#pragma unroll
-      for (int i = 0; i < D; ++i) y[i] = 0.0;
-      for (int t = hi - 1; t >= lo; --t) {
-        const int s = t - lo;
-        const double* e = E + s * ES;
-        double xi[D], cv[D];
-        if (PRE) {
-#pragma unroll
-          for (int i = 0; i < D; ++i) xi[i] = X[s * D + i];
-        } else {
-          stream_normals<D>(derive_index(klabel, (uint64_t)t), xi);
-        }
-        r_matvec<D>(e + D * D + D, xi, cv);
-        double gy[D];
-        r_matvec<D>(e, y, gy);
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-          cv[i] = e[D * D + i] + cv[i];
-          X[s * D + i] = cv[i];
-          y[i] = gy[i] + cv[i];
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < D; ++i) csub[(cl * NS + j) * D + i] = y[i];
-    }
-    __syncthreads();
-    // Phase B: carry scan over the sub-chunk aggregates, top-down.
-    if (active && j == 0) {
-      double x[D];
-#pragma unroll
-      for (int i = 0; i < D; ++i) x[i] = carry[cl * D + i];
-      const int s0 = t0 / LS;
-      for (int jj = NS - 1; jj >= 0; --jj) {
-#pragma unroll
-        for (int i = 0; i < D; ++i) xtop[(cl * NS + jj) * D + i] = x[i];
-        if (t0 + jj * LS >= t1) continue;
-        double gx[D];
-        r_matvec<D>(gsub + (size_t)(s0 + jj) * D * D, x, gx);
-#pragma unroll
-        for (int i = 0; i < D; ++i) x[i] = gx[i] + csub[(cl * NS + jj) * D + i];
-      }
-#pragma unroll
-      for (int i = 0; i < D; ++i) carry[cl * D + i] = x[i];
-    }
-    __syncthreads();
-    // Phase C: expand x_t = G_t x_{t+1} + c_t.
-    if (active) {
-      double x[D];
-#pragma unroll
-      for (int i = 0; i < D; ++i) x[i] = xtop[(cl * NS + j) * D + i];
-      for (int t = hi - 1; t >= lo; --t) {
-        const int s = t - lo;
-        double gx[D];
-        r_matvec<D>(E + s * ES, x, gx);
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-          x[i] = gx[i] + X[s * D + i];
-          X[s * D + i] = x[i];
-        }
-      }
-    }
-    __syncthreads();
-    // store the tile: rows [t0, t1) of each chain, coalesced 16 B
-    {
-      const int xn = (t1 - t0) * D;
-      for (int q = tid; q < nc * xn; q += CG * NS) {
-        const int ch = q / xn, off = q % xn;
-        const int s = off / (LS * D), r = off % (LS * D);
-        traj[(size_t)(c_begin + ch) * row + (size_t)t0 * D + off] = xt[buf][ch * XROW + s * XSUB + r];
-      }
-    }
-    __syncthreads();
-  }
-}
-
-template <int D, int CG, int NS, int LS>
-constexpr size_t prefix_smem_bytes() {
-  return sizeof(double) * (2 * (CG * NS * (LS * D + 2)) + 2 * (NS * (LS * ((2 * D * D + D + 1) & ~1) + 2)) +
-                           2 * CG * NS * D + CG * D);
 }
 
 // ---------------------------------------------------------------- sequential / per-path elements
@@ -531,39 +329,15 @@ __global__ void k_fanout_status(const int* st_fr, int fr_shared, int B, int* sta
     status[b] = st_fr[fr_shared ? 0 : b];
 }
 
+int launch_prefix_shared(int d, int T, int B, const double* elems, const double* term, Arena& ws,
+                         const NoiseArgs& nz, double* traj, cudaStream_t stream);
 int launch_dnc(const DevModel& dm, int Bfr, int fr_shared, const double* elems,
                const double* term, const NoiseArgs& nz, int B, double* traj, Arena& ws,
                int* st_fr, cudaStream_t stream);
 
 namespace {
 
-constexpr int kCG = 8, kNS = 16, kLS = 8;      // shared-element prefix tiling
 constexpr int kNSp = 32, kLSp = 8;             // per-path prefix tiling
-
-template <int D>
-int run_prefix_shared(int T, int B, const double* elems, const double* term, Arena& ws,
-                      const NoiseArgs& nz, double* traj, cudaStream_t stream) {
-  const int n_sub = (T + kLS - 1) / kLS;
-  double* gsub = ws.take<double>((size_t)(n_sub > 0 ? n_sub : 1) * D * D);
-  if (ws.base == nullptr) return AUXMC_OK;
-  if (!gsub) return AUXMC_E_WORKSPACE;
-  if (T > 0) {
-    const int grid = std::min((n_sub + 127) / 128, 148 * 8);
-    AUXMC_LAUNCH(k_gsub<D>, grid, 128, 0, stream, elems, T, kLS, gsub);
-  }
-  constexpr size_t smem = prefix_smem_bytes<D, kCG, kNS, kLS>();
-  const int grid = std::max((B + kCG - 1) / kCG, std::min(B, num_sms()));
-  if (nz.kind == AUXMC_NOISE_PREDRAWN) {
-    auto kern = k_prefix_shared<D, kCG, kNS, kLS, true>;
-    AUXMC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    AUXMC_LAUNCH(kern, grid, kCG * kNS, smem, stream, T, B, elems, term, gsub, nz, traj);
-  } else {
-    auto kern = k_prefix_shared<D, kCG, kNS, kLS, false>;
-    AUXMC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    AUXMC_LAUNCH(kern, grid, kCG * kNS, smem, stream, T, B, elems, term, gsub, nz, traj);
-  }
-  return AUXMC_OK;
-}
 
 template <int D>
 int run_sampler(int sampler, int T, int B, int fr_shared, const double* elems,
@@ -571,7 +345,7 @@ int run_sampler(int sampler, int T, int B, int fr_shared, const double* elems,
                 cudaStream_t stream) {
   const bool pre = nz.kind == AUXMC_NOISE_PREDRAWN;
   if (sampler == AUXMC_SAMPLER_PREFIX && fr_shared)
-    return run_prefix_shared<D>(T, B, elems, term, ws, nz, traj, stream);
+    return launch_prefix_shared(D, T, B, elems, term, ws, nz, traj, stream);
   if (ws.base == nullptr) return AUXMC_OK;
   const long long es = fr_shared ? 0 : (long long)T * elem_stride(D);
   const long long ts = fr_shared ? 0 : term_stride(D);
