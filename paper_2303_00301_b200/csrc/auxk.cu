@@ -1,0 +1,765 @@
+// auxk.cu — auxiliary Kalman MH kernel (auxk.cpp:45-218) and the target density
+// (target.cpp:47-108) for batches of chains on B200.
+//
+// One kernel_step for C chains is a fixed sequence of batched launches:
+//   aux draws u (auxk.cpp:45-54)
+//   surrogate LGSSM at x (auxk.cpp:56-118): per-chain pseudo-observations z,
+//     linearized dynamics for tractable targets, per-chain R = diag(δ/2 I, R_e, I)
+//   Kalman filter -> pathwise proposal (seq / prefix / dnc backend)
+//   log q(x'|x) = path_logpdf(cur, x'), log γ(x'), ∇ log g(x')
+//   surrogate at x', reverse filter, log q(x|x')
+//   aux log-likelihoods, log α, accept with U(kMhAccept, 0) (auxk.cpp:173-193)
+// Chains never branch the launch sequence: failures (factorization, non-finite
+// γ or gradients, NaN log α) are per-chain status words resolved in the MH
+// kernel exactly in the reference's order (auxk.cpp:151-197).  Model closures
+// (target.hpp:25-38) are compiled device functors selected by target kind.
+#include <cmath>
+
+#include "common.cuh"
+#include "dense.cuh"
+#include "rng.cuh"
+
+namespace auxmc_gpu {
+
+int launch_filter_seq(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
+                      int* status, cudaStream_t stream);
+int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int fr_shared,
+                        const auxmc_noise* noise, int B, int sampler, double* traj, int* status,
+                        Arena& ws, cudaStream_t stream);
+int launch_path_logpdf(const DevModel& dm, const double* obs, long long obs_stride,
+                       const double* traj, const double* log_marginal, int lm_shared, int B,
+                       double* out, int* status, cudaStream_t s);
+
+struct DevTarget {
+  int kind, T, dx, ydim, linear;
+  const double *m0, *P0, *F, *b, *Q;
+  int nF, q, ne, exact_tv;
+  const double *eH, *ec, *eR, *ey;
+  const uint8_t* emask;
+  const double* data;
+  const uint8_t* gmask;
+  const double *gH, *gc, *gR;
+  double lz_sigma, lz_rho, lz_beta, lz_h, l96_F, l96_h;
+  __device__ __forceinline__ const double* Ft(int t) const { return F + (size_t)(nF > 1 ? t : 0) * dx * dx; }
+  __device__ __forceinline__ const double* bt(int t) const { return b + (size_t)(nF > 1 ? t : 0) * dx; }
+  __device__ __forceinline__ const double* Qt(int t) const { return Q + (size_t)(nF > 1 ? t : 0) * dx * dx; }
+  __device__ __forceinline__ const double* eHt(int t) const { return eH + (size_t)(ne > 1 ? t : 0) * q * dx; }
+  __device__ __forceinline__ const double* ect(int t) const { return ec + (size_t)(ne > 1 ? t : 0) * q; }
+  __device__ __forceinline__ const double* eRt(int t) const { return eR + (size_t)(ne > 1 ? t : 0) * q * q; }
+  __device__ __forceinline__ const double* gHt(int t) const { return gH + (size_t)(ne > 1 ? t : 0) * ydim * dx; }
+  __device__ __forceinline__ const double* gct(int t) const { return gc + (size_t)(ne > 1 ? t : 0) * ydim; }
+  __device__ __forceinline__ const double* gRt(int t) const { return gR + (size_t)(ne > 1 ? t : 0) * ydim * ydim; }
+};
+
+static DevTarget to_dev_target(const auxmc_target& t) {
+  DevTarget d;
+  d.kind = t.kind; d.T = t.T; d.dx = t.dx; d.ydim = t.ydim; d.linear = t.linear;
+  d.m0 = t.m0; d.P0 = t.P0; d.F = t.F; d.b = t.b; d.Q = t.Q; d.nF = t.nF;
+  d.q = t.q; d.ne = t.ne; d.exact_tv = t.exact_tv;
+  d.eH = t.eH; d.ec = t.ec; d.eR = t.eR; d.ey = t.ey; d.emask = t.emask;
+  d.data = t.data; d.gmask = t.gmask; d.gH = t.gH; d.gc = t.gc; d.gR = t.gR;
+  d.lz_sigma = t.lz_sigma; d.lz_rho = t.lz_rho; d.lz_beta = t.lz_beta; d.lz_h = t.lz_h;
+  d.l96_F = t.l96_F; d.l96_h = t.l96_h;
+  return d;
+}
+
+static int check_target(const auxmc_target* t) {
+  if (!t) return AUXMC_E_ARG;
+  if (t->T < 0 || t->dx < 1 || t->dx > 64 || t->q < 0 || t->dx + t->q > 64 || t->ydim < 0 ||
+      t->ydim > 64)
+    return AUXMC_E_DIM;
+  if (!t->m0 || !t->P0 || !t->Q || !t->emask || !t->gmask) return AUXMC_E_ARG;
+  if (t->linear && (!t->F || !t->b)) return AUXMC_E_ARG;
+  if (t->q > 0 && (!t->eH || !t->ec || !t->eR || !t->ey)) return AUXMC_E_ARG;
+  if (t->kind == AUXMC_KIND_GAUSS_GENERIC && (!t->gH || !t->gc || !t->gR || !t->data))
+    return AUXMC_E_ARG;
+  if ((t->kind == AUXMC_KIND_STOCHVOL || t->kind == AUXMC_KIND_SPATIO) && !t->data)
+    return AUXMC_E_ARG;
+  if (!t->linear && t->kind != AUXMC_KIND_LORENZ63 && t->kind != AUXMC_KIND_LORENZ96)
+    return AUXMC_E_CONFIG;
+  return AUXMC_OK;
+}
+
+// ---------------------------------------------------------------- functors
+// E[x_{t+1} | x_t = x]_i (target.cpp:47-49; models.cpp:283-297; Lorenz-96)
+__device__ double dyn_mean_i(const DevTarget& tg, int t, const double* x, int i) {
+  const int d = tg.dx;
+  if (tg.linear) {
+    const double* F = tg.Ft(t);
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) s += F[i * d + j] * x[j];
+    return s + tg.bt(t)[i];
+  }
+  if (tg.kind == AUXMC_KIND_LORENZ63) {
+    const double f = i == 0 ? tg.lz_sigma * (x[1] - x[0])
+                     : i == 1 ? x[0] * (tg.lz_rho - x[2]) - x[1]
+                              : x[0] * x[1] - tg.lz_beta * x[2];
+    return x[i] + tg.lz_h * f;
+  }
+  const double f = (x[(i + 1) % d] - x[(i + d - 2) % d]) * x[(i + d - 1) % d] - x[i] + tg.l96_F;
+  return x[i] + tg.l96_h * f;
+}
+
+// ∂ mean_i / ∂ x_j (target.cpp:51-53)
+__device__ double dyn_jac_ij(const DevTarget& tg, int t, const double* x, int i, int j) {
+  const int d = tg.dx;
+  if (tg.linear) return tg.Ft(t)[i * d + j];
+  double J;
+  if (tg.kind == AUXMC_KIND_LORENZ63) {
+    const double Jm[9] = {-tg.lz_sigma, tg.lz_sigma, 0.0, tg.lz_rho - x[2], -1.0, -x[0],
+                          x[1],         x[0],        -tg.lz_beta};
+    J = Jm[i * 3 + j];
+    return (i == j ? 1.0 : 0.0) + tg.lz_h * J;
+  }
+  const int ip1 = (i + 1) % d, im1 = (i + d - 1) % d, im2 = (i + d - 2) % d;
+  J = 0.0;
+  if (j == ip1) J += x[im1];
+  if (j == im2) J -= x[im1];
+  if (j == im1) J += x[ip1] - x[im2];
+  if (j == i) J -= 1.0;
+  return (i == j ? 1.0 : 0.0) + tg.l96_h * J;
+}
+
+// Mahalanobis term with a precomputed lower factor: -0.5 (n log 2π + |L^-1 r|^2) - logdet
+__device__ double gauss_term(int n, double* r, const double* L, double logdet) {
+  double sq = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double s = r[i];
+    for (int j = 0; j < i; ++j) s -= L[i * n + j] * r[j];
+    r[i] = s / L[i * n + i];
+    sq += r[i] * r[i];
+  }
+  return -0.5 * (n * kLog2Pi + sq) - logdet;
+}
+
+// generic factor log g_t(x) (models.cpp:261-317; testutil.hpp:112-140)
+__device__ double generic_log_g(const DevTarget& tg, int t, const double* x, const double* Lg,
+                                double ldg, double* r) {
+  const int d = tg.dx;
+  const double* y = tg.data + (size_t)t * tg.ydim;
+  switch (tg.kind) {
+    case AUXMC_KIND_STOCHVOL: {
+      double sx = 0.0, sy = 0.0;
+      for (int i = 0; i < d; ++i) sx += x[i];
+      for (int i = 0; i < d; ++i) sy += (y[i] * y[i]) * exp(-x[i]);
+      return -0.5 * (log(2.0 * 3.14159265358979323846) * d + sx + sy);
+    }
+    case AUXMC_KIND_SPATIO: {
+      double s = 0.0;
+      for (int j = 0; j < d; ++j) s += y[j] * x[j] - exp(x[j]) - lgamma(y[j] + 1.0);
+      return s;
+    }
+    case AUXMC_KIND_GRID1D:
+      return -x[0] * x[0] * x[0] * x[0];
+    case AUXMC_KIND_GAUSS_GENERIC: {
+      const int n = tg.ydim;
+      const double* H = tg.gHt(t);
+      const double* c = tg.gct(t);
+      for (int i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < d; ++j) s += H[i * d + j] * x[j];
+        r[i] = ((y[i] - c[i]) - s) - 0.0;
+      }
+      return gauss_term(n, r, Lg, ldg);
+    }
+  }
+  return 0.0;
+}
+
+__device__ void generic_grad(const DevTarget& tg, int t, const double* x, const double* Lg,
+                             double* r, double* g) {
+  const int d = tg.dx;
+  if (!tg.gmask[t]) {
+    for (int i = 0; i < d; ++i) g[i] = 0.0;
+    return;
+  }
+  const double* y = tg.data + (size_t)t * tg.ydim;
+  switch (tg.kind) {
+    case AUXMC_KIND_STOCHVOL:
+      for (int i = 0; i < d; ++i) g[i] = 0.5 * ((y[i] * y[i]) * exp(-x[i]) - 1.0);
+      return;
+    case AUXMC_KIND_SPATIO:
+      for (int i = 0; i < d; ++i) g[i] = y[i] - exp(x[i]);
+      return;
+    case AUXMC_KIND_GRID1D:
+      g[0] = -4.0 * x[0] * x[0] * x[0];
+      return;
+    case AUXMC_KIND_GAUSS_GENERIC: {
+      const int n = tg.ydim;
+      const double* H = tg.gHt(t);
+      const double* c = tg.gct(t);
+      for (int i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < d; ++j) s += H[i * d + j] * x[j];
+        r[i] = (y[i] - c[i]) - s;
+      }
+      for (int i = 0; i < n; ++i) {  // L L^T z = r
+        double s = r[i];
+        for (int j = 0; j < i; ++j) s -= Lg[i * n + j] * r[j];
+        r[i] = s / Lg[i * n + i];
+      }
+      for (int i = n - 1; i >= 0; --i) {
+        double s = r[i];
+        for (int j = i + 1; j < n; ++j) s -= Lg[j * n + i] * r[j];
+        r[i] = s / Lg[i * n + i];
+      }
+      for (int j = 0; j < d; ++j) {
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s += H[i * d + j] * r[i];
+        g[j] = s;
+      }
+      return;
+    }
+  }
+  for (int i = 0; i < d; ++i) g[i] = 0.0;
+}
+
+// ---------------------------------------------------------------- target factors
+// items: P0 | Q_i (nF) | eR_i (ne, if q > 0) | gR_i (ne, if generic Gaussian)
+struct FactorLayout {
+  int nQ, nE, nG, W;
+  __host__ __device__ int total() const { return 1 + nQ + nE + nG; }
+};
+
+static FactorLayout factor_layout(const DevTarget& tg) {
+  FactorLayout f;
+  f.nQ = tg.linear ? tg.nF : 1;
+  f.nE = tg.q > 0 ? tg.ne : 0;
+  f.nG = tg.kind == AUXMC_KIND_GAUSS_GENERIC ? tg.ne : 0;
+  int W = tg.dx;
+  if (tg.q > W) W = tg.q;
+  if (f.nG && tg.ydim > W) W = tg.ydim;
+  f.W = W;
+  return f;
+}
+
+__global__ void k_target_factors(DevTarget tg, FactorLayout fl, double* Ls, double* logdet,
+                                 int* status) {
+  extern __shared__ double smem[];
+  const int W = fl.W;
+  Grp g = warp_group();
+  const int gid = threadIdx.x >> 5, gpb = blockDim.x >> 5;
+  double* A = smem + (size_t)gid * (3 * W * W + 4);
+  double* L = A + W * W;
+  double* scr = L + W * W;
+  double* red = scr + W * W;
+  int* flag = reinterpret_cast<int*>(red + 2);
+  for (int j = blockIdx.x * gpb + gid; j < fl.total(); j += gridDim.x * gpb) {
+    const double* src;
+    int n;
+    if (j == 0) { src = tg.P0; n = tg.dx; }
+    else if (j <= fl.nQ) { src = tg.Q + (size_t)(j - 1) * tg.dx * tg.dx; n = tg.dx; }
+    else if (j <= fl.nQ + fl.nE) { src = tg.eR + (size_t)(j - 1 - fl.nQ) * tg.q * tg.q; n = tg.q; }
+    else { src = tg.gR + (size_t)(j - 1 - fl.nQ - fl.nE) * tg.ydim * tg.ydim; n = tg.ydim; }
+    for (int i = g.lane; i < n * n; i += g.size) {
+      const int r = i / n, c = i % n;
+      A[i] = (src[r * n + c] + src[c * n + r]) * 0.5;  // Gaussian ctor symmetrization
+    }
+    g.sync();
+    const int st = g_factor_psd(g, n, A, L, scr, flag, red);
+    double* out = Ls + (size_t)j * W * W;
+    for (int i = g.lane; i < n * n; i += g.size) out[i] = L[i];
+    if (g.lane == 0) {
+      double ld = 0.0;
+      for (int i = 0; i < n; ++i) ld += log(L[i * n + i]);
+      logdet[j] = ld;
+      if (st) atomicMax(status, st);
+    }
+    g.sync();
+  }
+}
+
+// log γ terms (target.cpp:100-108): k = 0 prior, 1..T dynamics, T+1.. potentials
+__global__ void k_gamma_terms(DevTarget tg, FactorLayout fl, int C, const double* __restrict__ traj,
+                              const double* __restrict__ Ls, const double* __restrict__ logdet,
+                              double* terms) {
+  const int T = tg.T, d = tg.dx, W = fl.W;
+  const int K = 2 * T + 2;
+  const long long n = (long long)C * K;
+  double r[64];
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(q / K), k = (int)(q % K);
+    const double* x = traj + (size_t)c * (T + 1) * d;
+    double v;
+    if (k == 0) {
+      for (int i = 0; i < d; ++i) r[i] = x[i] - tg.m0[i];
+      v = gauss_term(d, r, Ls, logdet[0]);
+    } else if (k <= T) {
+      const int t = k - 1;
+      for (int i = 0; i < d; ++i) r[i] = x[(size_t)(t + 1) * d + i] - dyn_mean_i(tg, t, x + (size_t)t * d, i);
+      const int jq = 1 + (fl.nQ > 1 ? t : 0);
+      v = gauss_term(d, r, Ls + (size_t)jq * W * W, logdet[jq]);
+    } else {
+      const int t = k - T - 1;
+      const double* xt = x + (size_t)t * d;
+      double lp = 0.0;
+      if (tg.q > 0 && tg.emask[t]) {
+        const double* H = tg.eHt(t);
+        const double* cc = tg.ect(t);
+        const double* y = tg.ey + (size_t)t * tg.q;
+        for (int i = 0; i < tg.q; ++i) {
+          double s = 0.0;
+          for (int j = 0; j < d; ++j) s += H[i * d + j] * xt[j];
+          r[i] = y[i] - (s + cc[i]);
+        }
+        const int je = 1 + fl.nQ + (tg.ne > 1 ? t : 0);
+        lp += gauss_term(tg.q, r, Ls + (size_t)je * W * W, logdet[je]);
+      }
+      if (tg.gmask[t]) {
+        const int jg = 1 + fl.nQ + fl.nE + (tg.ne > 1 ? t : 0);
+        lp += generic_log_g(tg, t, xt, fl.nG ? Ls + (size_t)jg * W * W : nullptr,
+                            fl.nG ? logdet[jg] : 0.0, r);
+      }
+      v = lp;
+    }
+    terms[q] = v;
+  }
+}
+
+__global__ void k_gamma_sum(int T, int C, const double* terms, const int* fst, double* out,
+                            int* status) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const int K = 2 * T + 2;
+  const double* tm = terms + (size_t)c * K;
+  double lg = tm[0];
+  for (int t = 0; t < T; ++t) lg += tm[1 + t];
+  for (int t = 0; t <= T; ++t) lg += tm[T + 1 + t];
+  out[c] = lg;
+  if (status) status[c] = *fst;
+}
+
+__global__ void k_grads(DevTarget tg, FactorLayout fl, int C, const double* __restrict__ traj,
+                        const double* __restrict__ Ls, double* grads, int* bad) {
+  const int T = tg.T, d = tg.dx;
+  const long long n = (long long)C * (T + 1);
+  double r[64], g[64];
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(q / (T + 1)), t = (int)(q % (T + 1));
+    const int jg = 1 + fl.nQ + fl.nE + (tg.ne > 1 ? t : 0);
+    generic_grad(tg, t, traj + (size_t)q * d, fl.nG ? Ls + (size_t)jg * fl.W * fl.W : nullptr, r, g);
+    bool ok = true;
+    for (int i = 0; i < d; ++i) {
+      grads[(size_t)q * d + i] = g[i];
+      ok = ok && isfinite(g[i]);
+    }
+    if (!ok && bad) atomicOr(bad + c, 1);
+  }
+}
+
+// ---------------------------------------------------------------- aux model
+__global__ void k_iter_keys(int C, const uint64_t* root, const long long* iter, uint64_t* it) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C) it[c] = derive(root[c], kIteration, (uint64_t)iter[c]);
+}
+
+// u_t = x_t + sqrt(δ/2) xi(kAuxObs, t) (auxk.cpp:45-54)
+__global__ void k_aux_obs(int C, int T, int d, const double* __restrict__ x,
+                          const double* __restrict__ delta, const uint64_t* __restrict__ it,
+                          double* u) {
+  const long long n = (long long)C * (T + 1) * d;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(q % d);
+    const long long ct = q / d;
+    const int t = (int)(ct % (T + 1)), c = (int)(ct / (T + 1));
+    const double sd = sqrt(delta[c] / 2.0);
+    u[q] = x[q] + sd * normal_at(derive(it[c], kAuxObs, (uint64_t)t), (uint64_t)i);
+  }
+}
+
+// Per-chain pseudo-observations and linearized dynamics (auxk.cpp:60-113)
+__global__ void k_build_aux(DevTarget tg, int C, int zeroth, const double* __restrict__ xs,
+                            const double* __restrict__ gs, const double* __restrict__ u,
+                            const double* __restrict__ delta, double* z, double* Fa, double* ba) {
+  const int T = tg.T, d = tg.dx, p = d + tg.q;
+  const long long n = (long long)C * (T + 1);
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(q / (T + 1)), t = (int)(q % (T + 1));
+    const double h = delta[c] / 2.0;
+    double* zt = z + (size_t)q * p;
+    for (int i = 0; i < d; ++i) {
+      double v = u[(size_t)q * d + i];
+      if (!zeroth) v += h * gs[(size_t)q * d + i];
+      zt[i] = v;
+    }
+    for (int k = 0; k < tg.q; ++k) zt[d + k] = tg.emask[t] ? tg.ey[(size_t)t * tg.q + k] : 0.0;
+    if (!tg.linear && t < T) {
+      const double* xt = xs + (size_t)q * d;
+      double* F = Fa + ((size_t)c * T + t) * d * d;
+      double* bb = ba + ((size_t)c * T + t) * d;
+      for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j) F[i * d + j] = dyn_jac_ij(tg, t, xt, i, j);
+      for (int i = 0; i < d; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < d; ++j) s += F[i * d + j] * xt[j];
+        bb[i] = dyn_mean_i(tg, t, xt, i) - s;
+      }
+    }
+  }
+}
+
+// H = [I; H_e; 0], c = [0; c_e; 0] (shared), R = diag(δ/2 I, R_e, I) per chain
+__global__ void k_build_HR(DevTarget tg, int C, int nH, const double* __restrict__ delta,
+                           double* H, double* cv, double* R) {
+  const int d = tg.dx, q = tg.q, p = d + q;
+  const long long nR = (long long)C * nH * p * p;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < nR;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx % p), i = (int)((idx / p) % p);
+    const int tt = (int)((idx / ((long long)p * p)) % nH);
+    const int c = (int)(idx / ((long long)p * p * nH));
+    const bool ex = q > 0 && tg.emask[tt];
+    double v;
+    if (i < d || j < d) v = (i == j) ? (i < d ? delta[c] / 2.0 : 1.0) : 0.0;
+    else v = ex ? tg.eRt(tt)[(i - d) * q + (j - d)] : (i == j ? 1.0 : 0.0);
+    R[idx] = v;
+    if (c == 0) {
+      if (j < d) {
+        double hv;
+        if (i < d) hv = (i == j) ? 1.0 : 0.0;
+        else hv = ex ? tg.eHt(tt)[(i - d) * d + j] : 0.0;
+        H[((size_t)tt * p + i) * d + j] = hv;
+      }
+      if (j == 0) cv[(size_t)tt * p + i] = (i >= d && ex) ? tg.ect(tt)[i - d] : 0.0;
+    }
+  }
+}
+
+__global__ void k_aux_lik_terms(int C, int T, int d, const double* __restrict__ u,
+                                const double* __restrict__ x, const double* __restrict__ delta,
+                                double* terms) {
+  const long long n = (long long)C * (T + 1);
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(q / (T + 1));
+    const double var = delta[c] / 2.0;
+    double sq = 0.0;
+    for (int i = 0; i < d; ++i) {
+      const double r = u[(size_t)q * d + i] - x[(size_t)q * d + i];
+      sq += r * r;
+    }
+    terms[q] = -0.5 * (d * (kLog2Pi + log(var)) + sq / var);  // gauss.cpp:59-62
+  }
+}
+
+__global__ void k_row_sum(int C, int n, const double* terms, double* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0.0;
+  for (int t = 0; t < n; ++t) s += terms[(size_t)c * n + t];
+  out[c] = s;
+}
+
+struct StepScalars {
+  double *logq_fwd, *logq_rev, *lg_prop, *aux_prop, *aux_x;
+  int *st_filt, *st_samp, *st_lqf, *st_lg, *bad, *st_filt_r, *st_lqr, *accept;
+};
+
+// auxk.cpp:130-197 decision logic, per chain
+__global__ void k_mh(int C, StepScalars s, const uint64_t* it, double* log_gamma, long long* iter,
+                     auxmc_kernel_stats* stats) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  auxmc_kernel_stats st = stats[c];
+  iter[c] += 1;
+  st.last_accept_prob = 0.0;
+  st.last_log_alpha = -INFINITY;
+  int acc = 0;
+  if (s.st_filt[c] || s.st_samp[c] || s.st_lqf[c] || s.st_lg[c]) {
+    ++st.aborted;
+    ++st.rejected;
+  } else if (!isfinite(s.lg_prop[c])) {
+    ++st.nonfinite_gamma;
+    ++st.rejected;
+  } else if (s.bad[c]) {
+    ++st.aborted;
+    ++st.rejected;
+  } else if (s.st_filt_r[c] || s.st_lqr[c]) {
+    ++st.aborted;
+    ++st.rejected;
+  } else {
+    const double la = (s.lg_prop[c] + s.aux_prop[c] + s.logq_rev[c]) -
+                      (log_gamma[c] + s.aux_x[c] + s.logq_fwd[c]);
+    if (isnan(la)) {
+      ++st.aborted;
+      ++st.rejected;
+    } else {
+      st.last_log_alpha = la;
+      st.last_accept_prob = la >= 0.0 ? 1.0 : exp(la);
+      const double uacc = uniform_at(derive(it[c], kMhAccept, 0), 0);
+      if (uacc < st.last_accept_prob) {
+        acc = 1;
+        log_gamma[c] = s.lg_prop[c];
+        ++st.accepted;
+      } else {
+        ++st.rejected;
+      }
+    }
+  }
+  s.accept[c] = acc;
+  stats[c] = st;
+}
+
+__global__ void k_accept_copy(int C, long long row, const int* accept, const double* prop,
+                              const double* gprop, double* x, double* grad) {
+  const long long n = (long long)C * row;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    if (accept[q / row]) {
+      x[q] = prop[q];
+      grad[q] = gprop[q];
+    }
+  }
+}
+
+// δ ← exp(log δ + n^{-0.6} (α̂ - target)), n = max(iter, 1) (auxk.cpp:213-218)
+__global__ void k_adapt(int C, const long long* iter, const auxmc_kernel_stats* stats,
+                        double target, double* delta) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double n = (double)(iter[c] > 1 ? iter[c] : 1);
+  delta[c] = exp(log(delta[c]) + pow(n, -0.6) * (stats[c].last_accept_prob - target));
+}
+
+static int grid_for(long long n, int block = 256) {
+  long long g = (n + block - 1) / block;
+  if (g > 148LL * 32) g = 148LL * 32;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// log γ of C paths into out[C] (+ status); needs factor workspace
+static int launch_log_gamma(const DevTarget& tg, int C, const double* traj, double* out,
+                            int* status, Arena& ws, cudaStream_t s) {
+  const FactorLayout fl = factor_layout(tg);
+  double* Ls = ws.take<double>((size_t)fl.total() * fl.W * fl.W);
+  double* logdet = ws.take<double>(fl.total());
+  double* terms = ws.take<double>((size_t)C * (2 * tg.T + 2));
+  int* fst = ws.take<int>(1);
+  if (ws.base == nullptr) return AUXMC_OK;
+  if (!Ls || !logdet || !terms || !fst) return AUXMC_E_WORKSPACE;
+  AUXMC_CUDA_TRY(cudaMemsetAsync(fst, 0, sizeof(int), s));
+  const int warps = factor_warps(fl.W);
+  const size_t smem = sizeof(double) * (3 * fl.W * fl.W + 4) * warps;
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_target_factors,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  AUXMC_LAUNCH(k_target_factors, (fl.total() + warps - 1) / warps, 32 * warps, smem, s, tg, fl, Ls,
+               logdet, fst);
+  AUXMC_LAUNCH(k_gamma_terms, grid_for((long long)C * (2 * tg.T + 2), 128), 128, 0, s, tg, fl, C,
+               traj, Ls, logdet, terms);
+  AUXMC_LAUNCH(k_gamma_sum, (C + 127) / 128, 128, 0, s, tg.T, C, terms, fst, out, status);
+  return AUXMC_OK;
+}
+
+static int launch_grads(const DevTarget& tg, int C, const double* traj, double* grads, int* bad,
+                        Arena& ws, cudaStream_t s) {
+  const FactorLayout fl = factor_layout(tg);
+  double* Ls = ws.take<double>((size_t)fl.total() * fl.W * fl.W);
+  double* logdet = ws.take<double>(fl.total());
+  int* fst = ws.take<int>(1);
+  if (ws.base == nullptr) return AUXMC_OK;
+  if (!Ls || !logdet || !fst) return AUXMC_E_WORKSPACE;
+  if (fl.nG) {
+    AUXMC_CUDA_TRY(cudaMemsetAsync(fst, 0, sizeof(int), s));
+    const int warps = factor_warps(fl.W);
+    const size_t smem = sizeof(double) * (3 * fl.W * fl.W + 4) * warps;
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_target_factors,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    AUXMC_LAUNCH(k_target_factors, (fl.total() + warps - 1) / warps, 32 * warps, smem, s, tg, fl,
+                 Ls, logdet, fst);
+  }
+  AUXMC_LAUNCH(k_grads, grid_for((long long)C * (tg.T + 1), 128), 128, 0, s, tg, fl, C, traj, Ls,
+               grads, bad);
+  return AUXMC_OK;
+}
+
+// One auxiliary Kalman step for all chains (auxk.cpp:130-198).
+static int aux_step(const DevTarget& tg, auxmc_chains* ch, const auxmc_kernel_options& o,
+                    Arena& ws, cudaStream_t s) {
+  const int C = ch->C, T = tg.T, d = tg.dx, p = d + tg.q;
+  const int nH = tg.exact_tv ? T + 1 : 1;
+  const size_t nx = (size_t)C * (T + 1) * d;
+  uint64_t* it = ws.take<uint64_t>(C);
+  double* u = ws.take<double>(nx);
+  double* prop = ws.take<double>(nx);
+  double* gprop = ws.take<double>(nx);
+  double* z = ws.take<double>((size_t)C * (T + 1) * p);
+  double* Fa = tg.linear ? nullptr : ws.take<double>((size_t)C * (T > 0 ? T : 1) * d * d);
+  double* ba = tg.linear ? nullptr : ws.take<double>((size_t)C * (T > 0 ? T : 1) * d);
+  double* H = ws.take<double>((size_t)nH * p * d);
+  double* cv = ws.take<double>((size_t)nH * p);
+  double* R = ws.take<double>((size_t)C * nH * p * p);
+  auxmc_filter_result fr;
+  fr.pred_mean = ws.take<double>(nx);
+  fr.filt_mean = ws.take<double>(nx);
+  fr.pred_cov = ws.take<double>(nx * d);
+  fr.filt_cov = ws.take<double>(nx * d);
+  fr.log_marginal = ws.take<double>(C);
+  StepScalars sc;
+  sc.logq_fwd = ws.take<double>(C);
+  sc.logq_rev = ws.take<double>(C);
+  sc.lg_prop = ws.take<double>(C);
+  sc.aux_prop = ws.take<double>(C);
+  sc.aux_x = ws.take<double>(C);
+  int* ints = ws.take<int>((size_t)C * 9);
+  double* terms = ws.take<double>((size_t)C * (T + 1));
+  auxmc_noise nz{};
+  nz.kind = AUXMC_NOISE_STREAM;
+  nz.keys = it;
+  DevModel dm;
+  dm.T = T; dm.dx = d; dm.dy = p;
+  dm.m0 = tg.m0; dm.P0 = tg.P0;
+  dm.F = tg.linear ? tg.F : Fa; dm.nF = tg.linear ? tg.nF : (T > 0 ? T : 1);
+  dm.sF = tg.linear ? 0 : (long long)(T > 0 ? T : 1) * d * d;
+  dm.b = tg.linear ? tg.b : ba; dm.nb = dm.nF;
+  dm.sb = tg.linear ? 0 : (long long)(T > 0 ? T : 1) * d;
+  dm.Q = tg.Q; dm.nQ = tg.linear ? tg.nF : 1; dm.sQ = 0;
+  dm.H = H; dm.nH = nH; dm.sH = 0;
+  dm.c = cv; dm.nc = nH; dm.sc = 0;
+  dm.R = R; dm.nR = nH; dm.sR = (long long)nH * p * p;
+  dm.mask = nullptr;
+  const int sampler = o.backend;
+  int rc;
+  // sub-arenas for the sampler, log γ and gradients (sizing pass included)
+  if (ws.base == nullptr) {
+    rc = launch_sample_paths(dm, &fr, 0, &nz, C, sampler, prop, nullptr, ws, s);
+    if (rc) return rc;
+    rc = launch_log_gamma(tg, C, prop, sc.lg_prop, nullptr, ws, s);
+    if (rc) return rc;
+    return launch_grads(tg, C, prop, gprop, nullptr, ws, s);
+  }
+  if (!it || !u || !prop || !gprop || !z || !H || !cv || !R || !fr.filt_cov || !ints || !terms ||
+      (!tg.linear && (!Fa || !ba)))
+    return AUXMC_E_WORKSPACE;
+  sc.st_filt = ints; sc.st_samp = ints + C; sc.st_lqf = ints + 2 * C; sc.st_lg = ints + 3 * C;
+  sc.bad = ints + 4 * C; sc.st_filt_r = ints + 5 * C; sc.st_lqr = ints + 6 * C;
+  sc.accept = ints + 7 * C;
+  AUXMC_CUDA_TRY(cudaMemsetAsync(ints, 0, sizeof(int) * C * 9, s));
+  const int cb = (C + 127) / 128;
+  AUXMC_LAUNCH(k_iter_keys, cb, 128, 0, s, C, ch->root_keys, ch->iter, it);
+  AUXMC_LAUNCH(k_aux_obs, grid_for((long long)nx), 256, 0, s, C, T, d, ch->x, ch->delta, it, u);
+  AUXMC_LAUNCH(k_build_HR, grid_for((long long)C * nH * p * p), 256, 0, s, tg, C, nH, ch->delta,
+               H, cv, R);
+  // forward: surrogate at x, filter, proposal, log q(x'|x)
+  AUXMC_LAUNCH(k_build_aux, grid_for((long long)C * (T + 1), 128), 128, 0, s, tg, C,
+               o.zeroth_order, ch->x, ch->grad_gen, u, ch->delta, z, Fa, ba);
+  rc = launch_filter_seq(dm, z, C, &fr, sc.st_filt, s);
+  if (rc) return rc;
+  rc = launch_sample_paths(dm, &fr, 0, &nz, C, sampler, prop, sc.st_samp, ws, s);
+  if (rc) return rc;
+  rc = launch_path_logpdf(dm, z, (long long)(T + 1) * p, prop, fr.log_marginal, 0, C, sc.logq_fwd,
+                          sc.st_lqf, s);
+  if (rc) return rc;
+  // log γ(x'), ∇ log g(x')
+  {
+    Arena sub = ws;
+    rc = launch_log_gamma(tg, C, prop, sc.lg_prop, sc.st_lg, sub, s);
+    if (rc) return rc;
+    Arena sub2 = ws;
+    rc = launch_grads(tg, C, prop, gprop, sc.bad, sub2, s);
+    if (rc) return rc;
+  }
+  // reverse: surrogate at x', filter, log q(x|x')
+  AUXMC_LAUNCH(k_build_aux, grid_for((long long)C * (T + 1), 128), 128, 0, s, tg, C,
+               o.zeroth_order, prop, gprop, u, ch->delta, z, Fa, ba);
+  rc = launch_filter_seq(dm, z, C, &fr, sc.st_filt_r, s);
+  if (rc) return rc;
+  rc = launch_path_logpdf(dm, z, (long long)(T + 1) * p, ch->x, fr.log_marginal, 0, C,
+                          sc.logq_rev, sc.st_lqr, s);
+  if (rc) return rc;
+  // aux log-likelihoods Σ_t log N(u_t; ·, δ/2 I)
+  AUXMC_LAUNCH(k_aux_lik_terms, grid_for((long long)C * (T + 1)), 256, 0, s, C, T, d, u, prop,
+               ch->delta, terms);
+  AUXMC_LAUNCH(k_row_sum, cb, 128, 0, s, C, T + 1, terms, sc.aux_prop);
+  AUXMC_LAUNCH(k_aux_lik_terms, grid_for((long long)C * (T + 1)), 256, 0, s, C, T, d, u, ch->x,
+               ch->delta, terms);
+  AUXMC_LAUNCH(k_row_sum, cb, 128, 0, s, C, T + 1, terms, sc.aux_x);
+  AUXMC_LAUNCH(k_mh, cb, 128, 0, s, C, sc, it, ch->log_gamma, ch->iter, ch->stats);
+  AUXMC_LAUNCH(k_accept_copy, grid_for((long long)nx), 256, 0, s, C, (long long)(T + 1) * d,
+               sc.accept, prop, gprop, ch->x, ch->grad_gen);
+  return AUXMC_OK;
+}
+
+}  // namespace auxmc_gpu
+
+using namespace auxmc_gpu;
+
+extern "C" {
+
+size_t auxmc_aux_kernel_workspace(const auxmc_target* target, int C,
+                                  const auxmc_kernel_options* opts) {
+  if (check_target(target) || C < 0 || !opts) return 0;
+  Arena ws{nullptr, 0, 0};
+  auxmc_chains ch{};
+  ch.C = C;
+  aux_step(to_dev_target(*target), &ch, *opts, ws, nullptr);
+  return ws.used + 4096;
+}
+
+int auxmc_aux_kernel_step(const auxmc_target* target, auxmc_chains* chains,
+                          const auxmc_kernel_options* opts, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  int st = check_target(target);
+  if (st) return st;
+  if (!chains || !opts || chains->C < 0 || !chains->x || !chains->delta || !chains->log_gamma ||
+      !chains->grad_gen || !chains->iter || !chains->stats || !chains->root_keys)
+    return AUXMC_E_ARG;
+  if (opts->backend < 0 || opts->backend > 2) return AUXMC_E_ARG;
+  if (opts->parallel_filter) return AUXMC_E_ARG;  // scan filter: see auxmc_kalman_filter mode 1
+  if (chains->C == 0) return AUXMC_OK;
+  if (!workspace) return AUXMC_E_WORKSPACE;
+  Arena ws{(char*)workspace, workspace_bytes, 0};
+  return aux_step(to_dev_target(*target), chains, *opts, ws, (cudaStream_t)stream);
+}
+
+int auxmc_init_chains(const auxmc_target* target, auxmc_chains* chains, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  int st = check_target(target);
+  if (st) return st;
+  if (!chains || !chains->x || !chains->log_gamma || !chains->grad_gen) return AUXMC_E_ARG;
+  if (chains->C == 0) return AUXMC_OK;
+  const DevTarget tg = to_dev_target(*target);
+  Arena sizing{nullptr, 0, 0};
+  launch_log_gamma(tg, chains->C, chains->x, chains->log_gamma, nullptr, sizing, nullptr);
+  launch_grads(tg, chains->C, chains->x, chains->grad_gen, nullptr, sizing, nullptr);
+  if (!workspace || workspace_bytes < sizing.used) return AUXMC_E_WORKSPACE;
+  Arena ws{(char*)workspace, workspace_bytes, 0};
+  st = launch_log_gamma(tg, chains->C, chains->x, chains->log_gamma, nullptr, ws, (cudaStream_t)stream);
+  if (st) return st;
+  Arena ws2{(char*)workspace, workspace_bytes, 0};
+  return launch_grads(tg, chains->C, chains->x, chains->grad_gen, nullptr, ws2, (cudaStream_t)stream);
+}
+
+int auxmc_adapt_delta(auxmc_chains* chains, double target_rate, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  if (!chains || !chains->delta || !chains->iter || !chains->stats) return AUXMC_E_ARG;
+  if (chains->C == 0) return AUXMC_OK;
+  AUXMC_LAUNCH(k_adapt, (chains->C + 127) / 128, 128, 0, stream, chains->C, chains->iter,
+               chains->stats, target_rate, chains->delta);
+  return AUXMC_OK;
+}
+
+int auxmc_log_gamma(const auxmc_target* target, const double* traj, int B, double* out,
+                    int* status, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  int st = check_target(target);
+  if (st) return st;
+  if (!traj || !out || B < 0) return AUXMC_E_ARG;
+  if (B == 0) return AUXMC_OK;
+  const DevTarget tg = to_dev_target(*target);
+  Arena sizing{nullptr, 0, 0};
+  launch_log_gamma(tg, B, traj, out, status, sizing, nullptr);
+  void* buf = nullptr;
+  AUXMC_CUDA_TRY(cudaMallocAsync(&buf, sizing.used + 1024, (cudaStream_t)stream));
+  Arena ws{(char*)buf, sizing.used + 1024, 0};
+  st = launch_log_gamma(tg, B, traj, out, status, ws, (cudaStream_t)stream);
+  cudaFreeAsync(buf, (cudaStream_t)stream);
+  return st;
+}
+
+}  // extern "C"

@@ -39,6 +39,14 @@ int num_sms();
 
 inline size_t align_up(size_t n, size_t a = 256) { return (n + a - 1) / a * a; }
 
+// Warps per CTA for warp-per-matrix factorization kernels (3 W×W tiles per warp).
+inline int factor_warps(int W) {
+  const size_t per = sizeof(double) * (3 * (size_t)W * W + 4);
+  size_t w = (200 * 1024) / per;
+  if (w > 4) w = 4;
+  return w < 1 ? 1 : (int)w;
+}
+
 // Bump allocator over a caller-provided workspace.
 struct Arena {
   char* base;

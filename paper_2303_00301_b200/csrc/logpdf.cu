@@ -155,7 +155,7 @@ int launch_path_logpdf(const DevModel& dm, const double* obs, long long obs_stri
   AUXMC_CUDA_TRY(cudaMallocAsync(&terms, sizeof(double) * (size_t)B * K, s));
   AUXMC_CUDA_TRY(cudaMallocAsync(&fst, sizeof(int), s));
   AUXMC_CUDA_TRY(cudaMemsetAsync(fst, 0, sizeof(int), s));
-  const int warps = 4;
+  const int warps = factor_warps(W);
   const size_t smem = sizeof(double) * (3 * W * W + 4) * warps;
   AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_factor_list, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));

@@ -210,6 +210,57 @@ __global__ void k_seq_sample(int T, int C, const double* __restrict__ elems, lon
   }
 }
 
+// Any state dimension (d <= 64): warp per path, lanes over rows.
+__global__ void k_seq_sample_warp(int T, int d, int C, const double* __restrict__ elems,
+                                  long long estride, const double* __restrict__ term,
+                                  long long tstride, NoiseArgs noise, double* __restrict__ traj) {
+  __shared__ double sx[4][2][64];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 4 + w;
+  if (c >= C) return;
+  const int ES = elem_stride(d), dd = d * d;
+  const double* E = elems + (size_t)c * estride;
+  const double* tm = term + (size_t)c * tstride;
+  const long long row = (long long)(T + 1) * d;
+  double* out = traj + (size_t)c * row;
+  double* xi = sx[w][0];
+  double* x = sx[w][1];
+  const bool pre = noise.kind == AUXMC_NOISE_PREDRAWN;
+  for (int i = lane; i < d; i += 32)
+    xi[i] = pre ? noise.terminal[(size_t)c * d + i]
+                : normal_at(derive(noise.keys[c], kTerminalDraw, 0), (uint64_t)i);
+  __syncwarp();
+  for (int i = lane; i < d; i += 32) {
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) s += tm[d + i * d + j] * xi[j];
+    x[i] = tm[i] + s;
+    out[(size_t)T * d + i] = x[i];
+  }
+  const uint64_t kl = pre ? 0 : derive_label(noise.keys[c], kBackwardNoise);
+  double xn[2];
+  for (int t = T - 1; t >= 0; --t) {
+    const double* e = E + (size_t)t * ES;
+    __syncwarp();
+    const uint64_t key = pre ? 0 : derive_index(kl, (uint64_t)t);
+    for (int i = lane; i < d; i += 32)
+      xi[i] = pre ? noise.backward[((size_t)c * T + t) * d + i] : normal_at(key, (uint64_t)i);
+    __syncwarp();
+    int r = 0;
+    for (int i = lane; i < d; i += 32, ++r) {
+      double cv = 0.0, gx = 0.0;
+      for (int j = 0; j < d; ++j) cv += e[dd + d + i * d + j] * xi[j];
+      for (int j = 0; j < d; ++j) gx += e[i * d + j] * x[j];
+      xn[r] = gx + (e[dd + i] + cv);
+    }
+    __syncwarp();
+    r = 0;
+    for (int i = lane; i < d; i += 32, ++r) {
+      x[i] = xn[r];
+      out[(size_t)t * d + i] = xn[r];
+    }
+  }
+}
+
 // Per-path-element prefix sampler (aux-kernel backend): thread per (path,
 // sub-chunk) with in-thread sub-chunk products; sub-chunk carries scanned by
 // one thread per path.  Same fixed tree as k_prefix_shared.
@@ -425,7 +476,15 @@ int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int f
   case D: rc = run_sampler<D>(sampler, T, B, fr_shared, elems, term, ws, nz, traj, stream); break;
       CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
-      default: rc = AUXMC_E_DIM;
+      default:
+        if (sampler != AUXMC_SAMPLER_SEQ || d > 64) {
+          rc = AUXMC_E_DIM;
+        } else if (ws.base != nullptr) {
+          const long long es = fr_shared ? 0 : (long long)T * elem_stride(d);
+          const long long ts = fr_shared ? 0 : term_stride(d);
+          AUXMC_LAUNCH(k_seq_sample_warp, (B + 3) / 4, 128, 0, stream, T, d, B, elems, es, term,
+                       ts, nz, traj);
+        }
     }
   }
   if (rc || ws.base == nullptr) return rc;
