@@ -66,6 +66,12 @@ int auxmc_device_ok(void);
 const char* auxmc_last_error(void);
 /* Number of kernel launches issued by this library since load (all threads). */
 unsigned long long auxmc_launch_count(void);
+/* Bracket every subsequent launch with CUDA events on its stream (measurement
+ * support for bench.py: per-kernel device time inside a timed region). */
+void auxmc_profile_begin(void);
+/* Stop bracketing; sum the durations of launches whose kernel name contains
+ * kernel_substr (NULL = all). Synchronizes on the recorded events. */
+int auxmc_profile_end(const char* kernel_substr, double* total_ms, long long* count);
 
 /* ---- counter RNG, host side, bit-exact with rng.hpp:35-118 ---- */
 uint64_t auxmc_rng_from_seed(uint64_t seed);                               /* RngStream::from_seed */

@@ -256,6 +256,117 @@ void ao_pg_adapt_delta(ao_pg* st, double target_rate) {
   st->delta = exp(log(st->delta) + pow(n, -0.6) * (st->last_update - target_rate));
 }
 
+/* One parallel-in-time auxiliary particle Gibbs sweep with independent
+ * (gradient, kAuxObs) proposals — the checker for the GPU PIT variant.
+ * Particles use the reference's addresses (fkpg.cpp:77-84); the index path is
+ * drawn from the lattice law by forward log-messages and backward sampling
+ * with the reference's terminal/backward index uniforms (fkpg.cpp:127-150). */
+int ao_pit_pgibbs_step(const ao_target* tg, ao_pg* pg, int N, ao_stream rng, int* sel_out,
+                       int* bad_t) {
+  const int T = tg->T, d = tg->dx;
+  const size_t n = (size_t)(T + 1) * d;
+  const ao_stream it = ao_derive(rng, AO_L_ITERATION, (uint64_t)pg->iter);
+  ++pg->iter;
+  double* u = (double*)malloc(sizeof(double) * n);
+  ao_sample_aux_obs(pg->x, T, d, pg->delta, it, u);
+  aux_fk fk = {tg, u, pg->delta, AO_PG_GRADIENT};
+  double* part = (double*)malloc(sizeof(double) * (size_t)(T + 1) * N * d);
+  double* lw = (double*)malloc(sizeof(double) * (size_t)(T + 1) * N);
+  double* alpha = (double*)malloc(sizeof(double) * (size_t)(T + 1) * N);
+  double* tmp = (double*)malloc(sizeof(double) * N);
+  double* W = (double*)malloc(sizeof(double) * N);
+  double* traj = (double*)malloc(sizeof(double) * n);
+  uint64_t* tkeys = (uint64_t*)malloc(sizeof(uint64_t) * (T + 1));
+  double* mean = (double*)malloc(sizeof(double) * (2 * d + d * d + 64));
+  double* cov = mean + d;
+  double* r = cov + d * d;
+  int st = AO_OK;
+  for (int t = 0; t <= T; ++t) {
+    ao_stream sst = ao_derive(it, AO_L_STEP, (uint64_t)t);
+    proposal(&fk, t, NULL, mean, cov);
+    for (int i = 0; i < N; ++i) {
+      double* x = part + ((size_t)t * N + i) * d;
+      if (i == 0) {
+        memcpy(x, pg->x + (size_t)t * d, sizeof(double) * d);
+      } else {
+        ao_stream pi = ao_derive(sst, AO_L_PARTICLE, (uint64_t)i);
+        st |= sample_proposal(&fk, t, NULL, &pi, x);
+      }
+      for (int k = 0; k < d; ++k) r[k] = u[(size_t)t * d + k] - x[k];
+      double v = ao_log_pot(tg, t, x, &st) + ao_isotropic_log_pdf(d, r, pg->delta / 2.0);
+      if (t == 0) v += ao_log_pdf(d, x, tg->m0, tg->P0, &st);
+      v -= ao_log_pdf(d, x, mean, cov, &st);
+      lw[(size_t)t * N + i] = v;
+    }
+  }
+  double* dm = (double*)malloc(sizeof(double) * (size_t)N * d);
+  double* dc = (double*)malloc(sizeof(double) * d * d);
+  for (int i = 0; i < N; ++i) alpha[i] = lw[i];
+  for (int t = 1; t <= T && st == AO_OK; ++t) {
+    for (int i = 0; i < N; ++i)
+      ao_dyn_mean(tg, t - 1, part + ((size_t)(t - 1) * N + i) * d, dm + (size_t)i * d);
+    ao_dyn_cov(tg, t - 1, NULL, dc);
+    for (int j = 0; j < N; ++j) {
+      const double* xj = part + ((size_t)t * N + j) * d;
+      double m = -INFINITY;
+      for (int i = 0; i < N; ++i) {
+        tmp[i] = alpha[(size_t)(t - 1) * N + i] + ao_log_pdf(d, xj, dm + (size_t)i * d, dc, &st);
+        m = tmp[i] > m ? tmp[i] : m;
+      }
+      double s = 0.0;
+      for (int i = 0; i < N; ++i) s += exp(tmp[i] - m);
+      alpha[(size_t)t * N + j] = lw[(size_t)t * N + j] + (m + log(s));
+    }
+  }
+  int sel = 0;
+  if (st == AO_OK && normalize(alpha + (size_t)T * N, N, W, NULL) != AO_OK) {
+    st = AO_E_DEGENERATE;
+    if (bad_t) *bad_t = T;
+  }
+  if (st == AO_OK) {
+    ao_stream ti = ao_derive(it, AO_L_TERMINAL_INDEX, 0);
+    sel = multinomial_draw(W, N, ao_next_uniform(&ti));
+    if (sel_out) sel_out[T] = sel;
+    memcpy(traj + (size_t)T * d, part + ((size_t)T * N + sel) * d, sizeof(double) * d);
+    for (int t = T - 1; t >= 0 && st == AO_OK; --t) {
+      const double* chosen = traj + (size_t)(t + 1) * d;
+      ao_dyn_cov(tg, t, NULL, dc);
+      for (int i = 0; i < N; ++i) {
+        ao_dyn_mean(tg, t, part + ((size_t)t * N + i) * d, dm);
+        tmp[i] = alpha[(size_t)t * N + i] + ao_log_pdf(d, chosen, dm, dc, &st);
+      }
+      if (normalize(tmp, N, W, NULL) != AO_OK) {
+        st = AO_E_DEGENERATE;
+        if (bad_t) *bad_t = t;
+        break;
+      }
+      ao_stream bs = ao_derive(it, AO_L_BACKWARD_INDEX, (uint64_t)t);
+      sel = multinomial_draw(W, N, ao_next_uniform(&bs));
+      if (sel_out) sel_out[t] = sel;
+      memcpy(traj + (size_t)t * d, part + ((size_t)t * N + sel) * d, sizeof(double) * d);
+    }
+  }
+  if (st == AO_OK) {
+    for (int t = 0; t <= T; ++t) {
+      const int s_t = sel_out ? sel_out[t] : 0;
+      if (s_t == 0) {
+        tkeys[t] = pg->keys[t];
+      } else {
+        ao_stream ks = ao_derive(ao_derive(it, AO_L_STEP, (uint64_t)t), AO_L_PM_KEY, (uint64_t)s_t);
+        tkeys[t] = ao_next_key(&ks);
+      }
+    }
+    int changed = memcmp(traj, pg->x, sizeof(double) * n) != 0;
+    memcpy(pg->x, traj, sizeof(double) * n);
+    memcpy(pg->keys, tkeys, sizeof(uint64_t) * (T + 1));
+    pg->last_update = changed ? 1.0 : 0.0;
+    if (changed) ++pg->updates;
+  }
+  free(u); free(part); free(lw); free(alpha); free(tmp); free(W); free(traj); free(tkeys);
+  free(mean); free(dm); free(dc);
+  return st;
+}
+
 /* Parallel-in-time cSMC lattice law (no reference: SPEC.md:16).  With
  * independent proposals q_t (gradient mode at the aux obs), the conditional law
  * of the index path given all particles is

@@ -240,6 +240,10 @@ void ao_pg_free(ao_pg* st);
 int ao_aux_pgibbs_step(const ao_target* tg, ao_pg* st, int N, ao_stream rng, int mode,
                        int* ancestors, int* selected, int* bad_t);
 void ao_pg_adapt_delta(ao_pg* st, double target_rate);
+/* Parallel-in-time auxiliary particle Gibbs sweep (independent gradient
+ * proposals, lattice forward-backward over indices); sel_out [T+1] required. */
+int ao_pit_pgibbs_step(const ao_target* tg, ao_pg* st, int N, ao_stream rng, int* sel_out,
+                       int* bad_t);
 
 /* ---------------- parallel-in-time cSMC with independent proposals -----------
  * No reference implementation exists.  Law-level oracle: brute

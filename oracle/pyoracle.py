@@ -166,6 +166,7 @@ def _declare(L):
     L.ao_aux_pgibbs_step.argtypes = [C.POINTER(Target), C.POINTER(PG), C.c_int, Stream, C.c_int,
                                      PI, PI, PI]
     L.ao_pg_adapt_delta.argtypes = [C.POINTER(PG), C.c_double]
+    L.ao_pit_pgibbs_step.argtypes = [C.POINTER(Target), C.POINTER(PG), C.c_int, Stream, PI, PI]
     L.ao_pit_csmc_marginals.argtypes = [C.POINTER(Target), PD, C.c_double, PD, C.c_int, PD]
 
 
@@ -596,6 +597,13 @@ class PGChain:
 
     def adapt(self, target_rate):
         lib().ao_pg_adapt_delta(C.byref(self.p), target_rate)
+
+    def step_pit(self, N, rng: Stream):
+        sel = np.zeros(self.tg.T + 1, np.int32)
+        bad = C.c_int(-1)
+        st = lib().ao_pit_pgibbs_step(C.byref(self.tg.raw), C.byref(self.p), N, rng,
+                                      sel.ctypes.data_as(PI), C.byref(bad))
+        return st, bad.value, sel
 
 
 def pit_csmc_marginals(tg: OTarget, u, delta, particles):

@@ -93,6 +93,8 @@ SIGNATURES = {
     "auxmc_device_ok": (C.c_int, []),
     "auxmc_last_error": (C.c_char_p, []),
     "auxmc_launch_count": (C.c_ulonglong, []),
+    "auxmc_profile_begin": (None, []),
+    "auxmc_profile_end": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_longlong)]),
     "auxmc_rng_from_seed": (C.c_uint64, [C.c_uint64]),
     "auxmc_rng_derive": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
     "auxmc_rng_uniform": (C.c_double, [C.c_uint64, C.c_uint64]),

@@ -13,7 +13,38 @@
 namespace auxmc_gpu {
 
 std::atomic<unsigned long long> g_launches{0};
+std::atomic<int> g_prof_on{0};
 static thread_local std::string g_last_error;
+
+struct ProfRecord {
+  std::string name;
+  cudaEvent_t begin, end;
+};
+static std::mutex g_prof_mu;
+static std::vector<ProfRecord> g_prof;
+static std::vector<cudaEvent_t> g_prof_pool;
+
+static cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void prof_mark(const char* name, cudaStream_t s, bool begin) {
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  if (begin) {
+    ProfRecord r{name, prof_event(), prof_event()};
+    cudaEventRecord(r.begin, s);
+    g_prof.push_back(r);
+  } else if (!g_prof.empty()) {
+    cudaEventRecord(g_prof.back().end, s);
+  }
+}
 
 void set_last_error(const char* where, cudaError_t e) {
   g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
@@ -108,6 +139,34 @@ const char* auxmc_status_string(int s) {
 }
 
 int auxmc_device_ok(void) { return device_ok() ? 1 : 0; }
+
+void auxmc_profile_begin(void) {
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  for (auto& r : g_prof) {
+    g_prof_pool.push_back(r.begin);
+    g_prof_pool.push_back(r.end);
+  }
+  g_prof.clear();
+  g_prof_on.store(1);
+}
+
+int auxmc_profile_end(const char* kernel_substr, double* total_ms, long long* count) {
+  g_prof_on.store(0);
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  double tot = 0.0;
+  long long n = 0;
+  for (auto& r : g_prof) {
+    if (kernel_substr && std::strstr(r.name.c_str(), kernel_substr) == nullptr) continue;
+    if (cudaEventSynchronize(r.end) != cudaSuccess) return AUXMC_E_CUDA;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.begin, r.end) != cudaSuccess) return AUXMC_E_CUDA;
+    tot += ms;
+    ++n;
+  }
+  if (total_ms) *total_ms = tot;
+  if (count) *count = n;
+  return AUXMC_OK;
+}
 const char* auxmc_last_error(void) { return g_last_error.c_str(); }
 unsigned long long auxmc_launch_count(void) { return g_launches.load(); }
 

@@ -12,10 +12,15 @@
 namespace auxmc_gpu {
 
 extern std::atomic<unsigned long long> g_launches;
+extern std::atomic<int> g_prof_on;
 void set_last_error(const char* where, cudaError_t e);
+// Per-launch CUDA-event bracketing while profiling is enabled (auxmc_profile_*).
+void prof_mark(const char* name, cudaStream_t s, bool begin);
 
 #define AUXMC_LAUNCH(kernel, grid, block, smem, stream, ...)                   \
   do {                                                                         \
+    const bool _prof = ::auxmc_gpu::g_prof_on.load(std::memory_order_relaxed); \
+    if (_prof) ::auxmc_gpu::prof_mark(#kernel, (cudaStream_t)(stream), true);  \
     kernel<<<(grid), (block), (smem), (cudaStream_t)(stream)>>>(__VA_ARGS__);  \
     ::auxmc_gpu::g_launches.fetch_add(1, std::memory_order_relaxed);           \
     cudaError_t _e = cudaGetLastError();                                       \
@@ -23,6 +28,7 @@ void set_last_error(const char* where, cudaError_t e);
       ::auxmc_gpu::set_last_error(#kernel, _e);                                \
       return AUXMC_E_CUDA;                                                     \
     }                                                                          \
+    if (_prof) ::auxmc_gpu::prof_mark(#kernel, (cudaStream_t)(stream), false); \
   } while (0)
 
 #define AUXMC_CUDA_TRY(expr)                                                   \

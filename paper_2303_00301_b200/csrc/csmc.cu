@@ -1,0 +1,609 @@
+// csmc.cu — auxiliary particle Gibbs on B200 (fkpg.cpp:19-280), gradient
+// proposals linearized at the auxiliary observation (fkpg.cpp:154-186), plus
+// the parallel-in-time conditional SMC with independent proposals.
+//
+// variant REFERENCE (K6): the reference's conditional SMC sweep with
+//   multinomial resampling and backward index sampling (fkpg.cpp:44-152),
+//   one CTA per chain, particles across threads, sequential in t.  Resampling
+//   uses the reference's exact sequential cumulative sum and "first i with
+//   u <= acc" rule (fkpg.cpp:29-37), so ancestor and backward indices agree
+//   with the reference bit for bit given the same weights.
+// variant PIT (K7, no reference: SPEC.md:16): with independent proposals the
+//   particle lattice x_t^i and the parent-free weights are generated for all t
+//   at once (fully parallel); the index path is then drawn exactly from the
+//   lattice law P(i_{0:T}) ∝ w_0(i_0) Π p(x_t^{i_t} | x_{t-1}^{i_{t-1}}) w_t(i_t)
+//   by log-sum-exp forward messages over the N×N transitions and backward
+//   index sampling with the reference's stream addresses.
+#include <cmath>
+
+#include "common.cuh"
+#include "dense.cuh"
+#include "rng.cuh"
+#include "target.cuh"
+
+namespace auxmc_gpu {
+
+int launch_target_factors(const DevTarget& tg, double* Ls, double* logdet, int* fst,
+                          cudaStream_t s);
+int launch_aux_obs(int C, int T, int d, const double* x, const double* delta, const uint64_t* it,
+                   double* u, cudaStream_t s);
+
+struct FactorRef {
+  FactorLayout fl;
+  const double* Ls;
+  const double* logdet;
+  __device__ __forceinline__ const double* L(int j) const { return Ls + (size_t)j * fl.W * fl.W; }
+};
+
+__device__ __forceinline__ double log_pot_dev(const DevTarget& tg, const FactorRef& f, int t,
+                                              const double* x, double* r) {
+  double lp = 0.0;
+  const int d = tg.dx;
+  if (tg.q > 0 && tg.emask[t]) {
+    const double* H = tg.eHt(t);
+    const double* cc = tg.ect(t);
+    const double* y = tg.ey + (size_t)t * tg.q;
+    for (int i = 0; i < tg.q; ++i) {
+      double s = 0.0;
+      for (int j = 0; j < d; ++j) s += H[i * d + j] * x[j];
+      r[i] = y[i] - (s + cc[i]);
+    }
+    const int je = 1 + f.fl.nQ + (tg.ne > 1 ? t : 0);
+    lp += gauss_term(tg.q, r, f.L(je), f.logdet[je]);
+  }
+  if (tg.gmask[t]) {
+    const int jg = 1 + f.fl.nQ + f.fl.nE + (tg.ne > 1 ? t : 0);
+    lp += generic_log_g(tg, t, x, f.fl.nG ? f.L(jg) : nullptr, f.fl.nG ? f.logdet[jg] : 0.0, r);
+  }
+  return lp;
+}
+
+__device__ __forceinline__ double log_dyn_dev(const DevTarget& tg, const FactorRef& f, int t,
+                                              const double* xp, const double* x, double* r) {
+  const int d = tg.dx;
+  for (int i = 0; i < d; ++i) r[i] = x[i] - dyn_mean_i(tg, t, xp, i);
+  const int jq = 1 + (f.fl.nQ > 1 ? t : 0);
+  return gauss_term(d, r, f.L(jq), f.logdet[jq]);
+}
+
+__device__ __forceinline__ double log_prior_dev(const DevTarget& tg, const FactorRef& f,
+                                                const double* x, double* r) {
+  for (int i = 0; i < tg.dx; ++i) r[i] = x[i] - tg.m0[i];
+  return gauss_term(tg.dx, r, f.L(0), f.logdet[0]);
+}
+
+// log N(x; mean, (δ/2) I) through the LLT path of gauss::log_pdf (gauss.cpp:51-57)
+__device__ __forceinline__ double log_q_dev(int d, const double* x, const double* mean, double sq2) {
+  double sq = 0.0, ld = 0.0;
+  for (int i = 0; i < d; ++i) {
+    const double z = (x[i] - mean[i]) / sq2;
+    sq += z * z;
+  }
+  for (int i = 0; i < d; ++i) ld += log(sq2);
+  return -0.5 * (d * kLog2Pi + sq) - ld;
+}
+
+// isotropic_log_pdf(u - x, var) (gauss.cpp:59-62)
+__device__ __forceinline__ double iso_dev(int d, const double* u, const double* x, double var) {
+  double sq = 0.0;
+  for (int i = 0; i < d; ++i) {
+    const double r = u[i] - x[i];
+    sq += r * r;
+  }
+  return -0.5 * (d * (kLog2Pi + log(var)) + sq / var);
+}
+
+// potential of the auxiliary FK model (fkpg.cpp:212-223), gradient mode
+__device__ __forceinline__ double potential_dev(const DevTarget& tg, const FactorRef& f, int t,
+                                                const double* xp, const double* x, const double* u_t,
+                                                const double* mq_t, double delta, double sq2,
+                                                double* r) {
+  const int d = tg.dx;
+  double lg = log_pot_dev(tg, f, t, x, r) + iso_dev(d, u_t, x, delta / 2.0);
+  const double ld = t == 0 ? log_prior_dev(tg, f, x, r) : log_dyn_dev(tg, f, t - 1, xp, x, r);
+  lg += ld - log_q_dev(d, x, mq_t, sq2);
+  return lg;
+}
+
+// ---------------------------------------------------------------- prep kernels
+__global__ void k_pg_keys(int C, const uint64_t* root, const long long* iter, uint64_t* it) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C) it[c] = derive(root[c], kIteration, (uint64_t)iter[c]);
+}
+
+// proposal mean u_t + (δ/2) ∇ log g_t(u_t) (fkpg.cpp:166-171), both factors
+__global__ void k_pg_prop_mean(DevTarget tg, FactorRef f, int C, const double* __restrict__ u,
+                               const double* __restrict__ delta, double* mq, int* bad) {
+  const int T = tg.T, d = tg.dx;
+  const long long n = (long long)C * (T + 1);
+  double r[64], g[64];
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(q / (T + 1)), t = (int)(q % (T + 1));
+    const double* ut = u + (size_t)q * d;
+    const int jg = 1 + f.fl.nQ + f.fl.nE + (tg.ne > 1 ? t : 0);
+    generic_grad(tg, t, ut, f.fl.nG ? f.L(jg) : nullptr, r, g);
+    if (tg.q > 0 && tg.emask[t]) {  // + H^T R^{-1} (y - H x - c) (target.cpp:90-98)
+      const double* H = tg.eHt(t);
+      const double* cc = tg.ect(t);
+      const double* y = tg.ey + (size_t)t * tg.q;
+      const int je = 1 + f.fl.nQ + (tg.ne > 1 ? t : 0);
+      const double* L = f.L(je);
+      const int qn = tg.q;
+      for (int i = 0; i < qn; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < d; ++j) s += H[i * d + j] * ut[j];
+        r[i] = (y[i] - s) - cc[i];
+      }
+      for (int i = 0; i < qn; ++i) {
+        double s = r[i];
+        for (int j = 0; j < i; ++j) s -= L[i * qn + j] * r[j];
+        r[i] = s / L[i * qn + i];
+      }
+      for (int i = qn - 1; i >= 0; --i) {
+        double s = r[i];
+        for (int j = i + 1; j < qn; ++j) s -= L[j * qn + i] * r[j];
+        r[i] = s / L[i * qn + i];
+      }
+      for (int j = 0; j < d; ++j) {
+        double s = 0.0;
+        for (int i = 0; i < qn; ++i) s += H[i * d + j] * r[i];
+        g[j] += s;
+      }
+    }
+    const double h = delta[c] / 2.0;
+    for (int i = 0; i < d; ++i) {
+      mq[(size_t)q * d + i] = ut[i] + h * g[i];
+      if (!isfinite(g[i]) && bad) atomicOr(bad + c, 1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- block helpers
+__device__ __forceinline__ double block_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = red[0];
+    for (int i = 1; i < nw; ++i) m = fmax(m, red[i]);
+    red[32] = m;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// normalize (fkpg.cpp:19-27) over logw[0..N) in shared memory -> W (shared),
+// sequential sum as the reference's order; returns false if degenerate.
+__device__ __forceinline__ bool block_normalize(int N, const double* logw, double* W, double* red) {
+  double m = -INFINITY;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const double v = logw[i];
+    m = (v > m || m != m) ? v : m;
+  }
+  // NaN handling: Eigen maxCoeff; treat NaN like the reference's non-finite max
+  m = block_max(m, red);
+  if (!isfinite(m)) return false;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) W[i] = exp(logw[i] - m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < N; ++i) s += W[i];
+    red[33] = s;
+  }
+  __syncthreads();
+  const double s = red[33];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) W[i] = W[i] / s;
+  __syncthreads();
+  return true;
+}
+
+// cumulative weights in the reference's sequential order (fkpg.cpp:29-37)
+__device__ __forceinline__ void block_cumsum(int N, const double* W, double* cum) {
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int i = 0; i < N; ++i) {
+      acc += W[i];
+      cum[i] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+// first i with u <= cum[i], else N-1
+__device__ __forceinline__ int draw_index(int N, const double* cum, double u) {
+  int lo = 0, hi = N;  // lower_bound of u in cum (non-decreasing)
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (u <= cum[mid]) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo < N ? lo : N - 1;
+}
+
+struct PgArgs {
+  int C, N;
+  double* x;
+  uint64_t* keys;
+  const double* delta;
+  const uint64_t* it;
+  const double* u;
+  const double* mq;
+  double* part;     // [C][T+1][N][d]
+  double* Wt;       // [C][T+1][N] normalized weights (or forward log-messages for PIT)
+  double* traj;     // [C][T+1][d] new path
+  uint64_t* tkeys;  // [C][T+1]
+  int* status;
+  int* bad_t;
+  int* anc;         // optional [C][T+1][N]
+  int* sel;         // optional [C][T+1]
+  const int* grad_bad;
+};
+
+// ---------------------------------------------------------------- K6 reference cSMC
+__global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
+  extern __shared__ double sm[];
+  const int N = a.N, T = tg.T, d = tg.dx;
+  const int c = blockIdx.x;
+  double* logw = sm;           // N
+  double* W = logw + N;        // N
+  double* cum = W + N;         // N
+  double* red = cum + N;       // 40
+  double* chosen = red + 40;   // d
+  int* anc = reinterpret_cast<int*>(chosen + 64);  // N
+  const double delta = a.delta[c];
+  const double sq2 = sqrt(delta / 2.0);  // LLT of (δ/2) I (gauss.cpp:64-67)
+  const uint64_t it = a.it[c];
+  double* P = a.part + (size_t)c * (T + 1) * N * d;
+  double* Wg = a.Wt + (size_t)c * (T + 1) * N;
+  const double* uc = a.u + (size_t)c * (T + 1) * d;
+  const double* mqc = a.mq + (size_t)c * (T + 1) * d;
+  const double* ref = a.x + (size_t)c * (T + 1) * d;
+  double r[64], xv[64];
+  if (a.grad_bad && a.grad_bad[c]) {  // non-finite proposal mean: treat as degenerate
+    if (threadIdx.x == 0) { a.status[c] = AUXMC_E_DEGENERATE; a.bad_t[c] = 0; }
+    return;
+  }
+  for (int t = 0; t <= T; ++t) {
+    const uint64_t st = derive(it, kStep, (uint64_t)t);
+    if (t > 0) {
+      block_cumsum(N, W, cum);
+      const uint64_t rs = derive(st, kResample, 0);
+      for (int i = threadIdx.x; i < N; i += blockDim.x)
+        anc[i] = i == 0 ? 0 : draw_index(N, cum, uniform_at(rs, (uint64_t)(i - 1)));
+      __syncthreads();
+    }
+    const uint64_t kp = derive_label(st, kParticle);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      if (i == 0) {
+        for (int k = 0; k < d; ++k) xv[k] = ref[(size_t)t * d + k];
+      } else {
+        const uint64_t pk = derive_index(kp, (uint64_t)i);
+        for (int k = 0; k < d; ++k) xv[k] = mqc[(size_t)t * d + k] + sq2 * normal_at(pk, (uint64_t)k);
+      }
+      for (int k = 0; k < d; ++k) P[((size_t)t * N + i) * d + k] = xv[k];
+      const double* parent = t > 0 ? P + ((size_t)(t - 1) * N + anc[i]) * d : nullptr;
+      logw[i] = potential_dev(tg, f, t, parent, xv, uc + (size_t)t * d, mqc + (size_t)t * d, delta,
+                              sq2, r);
+      if (a.anc) a.anc[((size_t)c * (T + 1) + t) * N + i] = t > 0 ? anc[i] : 0;
+    }
+    __syncthreads();
+    if (!block_normalize(N, logw, W, red)) {
+      if (threadIdx.x == 0) { a.status[c] = AUXMC_E_DEGENERATE; a.bad_t[c] = t; }
+      return;
+    }
+    for (int i = threadIdx.x; i < N; i += blockDim.x) Wg[(size_t)t * N + i] = W[i];
+    __syncthreads();
+  }
+  // terminal index (fkpg.cpp:127-133) and backward index sampling (:135-150)
+  block_cumsum(N, W, cum);
+  __shared__ int s_sel;
+  double* tr = a.traj + (size_t)c * (T + 1) * d;
+  uint64_t* tk = a.tkeys + (size_t)c * (T + 1);
+  auto pm_key = [&](int t, int i) -> uint64_t {
+    if (i == 0) return a.keys[(size_t)c * (T + 1) + t];
+    return key_at(derive(derive(it, kStep, (uint64_t)t), kPmKey, (uint64_t)i), 0);
+  };
+  if (threadIdx.x == 0) {
+    const int sel = draw_index(N, cum, uniform_at(derive(it, kTerminalIndex, 0), 0));
+    s_sel = sel;
+    for (int k = 0; k < d; ++k) {
+      chosen[k] = P[((size_t)T * N + sel) * d + k];
+      tr[(size_t)T * d + k] = chosen[k];
+    }
+    tk[T] = pm_key(T, sel);
+    if (a.sel) a.sel[(size_t)c * (T + 1) + T] = sel;
+  }
+  __syncthreads();
+  for (int t = T - 1; t >= 0; --t) {
+    // m_logpdf(t+1, ., chosen) and the parent-free part of log_g(t+1, ., chosen)
+    const double* mq1 = mqc + (size_t)(t + 1) * d;
+    const double mlp = log_q_dev(d, chosen, mq1, sq2);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const double* xi = P + ((size_t)t * N + i) * d;
+      const double lg = potential_dev(tg, f, t + 1, xi, chosen, uc + (size_t)(t + 1) * d, mq1,
+                                      delta, sq2, r);
+      logw[i] = log(Wg[(size_t)t * N + i]) + mlp + lg;
+    }
+    __syncthreads();
+    if (!block_normalize(N, logw, W, red)) {
+      if (threadIdx.x == 0) { a.status[c] = AUXMC_E_DEGENERATE; a.bad_t[c] = t; }
+      return;
+    }
+    block_cumsum(N, W, cum);
+    if (threadIdx.x == 0) {
+      const int sel = draw_index(N, cum, uniform_at(derive(it, kBackwardIndex, (uint64_t)t), 0));
+      for (int k = 0; k < d; ++k) {
+        chosen[k] = P[((size_t)t * N + sel) * d + k];
+        tr[(size_t)t * d + k] = chosen[k];
+      }
+      tk[t] = pm_key(t, sel);
+      if (a.sel) a.sel[(size_t)c * (T + 1) + t] = sel;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- K7 PIT cSMC
+// Lattice particles and parent-free log-weights for every (t, i) at once.
+__global__ void k_pit_particles(DevTarget tg, FactorRef f, PgArgs a, double* lw) {
+  const int N = a.N, T = tg.T, d = tg.dx;
+  const long long n = (long long)a.C * (T + 1) * N;
+  double r[64], xv[64];
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(q % N);
+    const long long ct = q / N;
+    const int t = (int)(ct % (T + 1)), c = (int)(ct / (T + 1));
+    const double delta = a.delta[c], sq2 = sqrt(delta / 2.0);
+    const double* mq = a.mq + ((size_t)c * (T + 1) + t) * d;
+    if (i == 0) {
+      for (int k = 0; k < d; ++k) xv[k] = a.x[((size_t)c * (T + 1) + t) * d + k];
+    } else {
+      const uint64_t pk = derive(derive(a.it[c], kStep, (uint64_t)t), kParticle, (uint64_t)i);
+      for (int k = 0; k < d; ++k) xv[k] = mq[k] + sq2 * normal_at(pk, (uint64_t)k);
+    }
+    double* P = a.part + (size_t)q * d;
+    for (int k = 0; k < d; ++k) P[k] = xv[k];
+    const double* ut = a.u + ((size_t)c * (T + 1) + t) * d;
+    double v = log_pot_dev(tg, f, t, xv, r) + iso_dev(d, ut, xv, delta / 2.0);
+    if (t == 0) v += log_prior_dev(tg, f, xv, r);
+    v -= log_q_dev(d, xv, mq, sq2);
+    lw[q] = v;
+  }
+}
+
+// Forward log-messages alpha_t(j) = lw_t(j) + LSE_i(alpha_{t-1}(i) + log p(x_t^j | x_{t-1}^i)),
+// one CTA per chain, then backward index sampling with the reference's addresses.
+__global__ void k_pit_forward_backward(DevTarget tg, FactorRef f, PgArgs a, const double* lw) {
+  extern __shared__ double sm[];
+  const int N = a.N, T = tg.T, d = tg.dx;
+  const int c = blockIdx.x;
+  double* alpha = sm;            // N
+  double* W = alpha + N;         // N
+  double* cum = W + N;           // N
+  double* mprev = cum + N;       // N*d dynamics means of the previous particles
+  double* red = mprev + (size_t)N * d;  // 40
+  double* chosen = red + 40;     // d
+  const double* P = a.part + (size_t)c * (T + 1) * N * d;
+  const double* LW = lw + (size_t)c * (T + 1) * N;
+  double* A = a.Wt + (size_t)c * (T + 1) * N;
+  const int jq0 = 1;
+  double r[64];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    alpha[i] = LW[i];
+    A[i] = alpha[i];
+  }
+  __syncthreads();
+  for (int t = 1; t <= T; ++t) {
+    for (int q = threadIdx.x; q < N * d; q += blockDim.x) {
+      const int i = q / d, k = q % d;
+      mprev[q] = dyn_mean_i(tg, t - 1, P + ((size_t)(t - 1) * N + i) * d, k);
+    }
+    const double am = block_max([&] {
+      double m = -INFINITY;
+      for (int i = threadIdx.x; i < N; i += blockDim.x) m = fmax(m, alpha[i]);
+      return m;
+    }(), red);
+    const int jq = jq0 + (f.fl.nQ > 1 ? t - 1 : 0);
+    const double* LQ = f.L(jq);
+    const double ldq = f.logdet[jq];
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+      const double* xj = P + ((size_t)t * N + j) * d;
+      double m = -INFINITY, s = 0.0;  // online log-sum-exp over i
+      for (int i = 0; i < N; ++i) {
+        for (int k = 0; k < d; ++k) r[k] = xj[k] - mprev[i * d + k];
+        const double v = (alpha[i] - am) + gauss_term(d, r, LQ, ldq);
+        if (v > m) {
+          s = s * exp(m - v) + 1.0;
+          m = v;
+        } else {
+          s += exp(v - m);
+        }
+      }
+      W[j] = LW[(size_t)t * N + j] + (am + (m + log(s)));
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+      alpha[j] = W[j];
+      A[(size_t)t * N + j] = W[j];
+    }
+    __syncthreads();
+  }
+  // backward: i_T ∝ exp(alpha_T); i_t ∝ exp(alpha_t(i)) p(x_{t+1}^{i_{t+1}} | x_t^i)
+  double* tr = a.traj + (size_t)c * (T + 1) * d;
+  uint64_t* tk = a.tkeys + (size_t)c * (T + 1);
+  const uint64_t it = a.it[c];
+  auto pm_key = [&](int t, int i) -> uint64_t {
+    if (i == 0) return a.keys[(size_t)c * (T + 1) + t];
+    return key_at(derive(derive(it, kStep, (uint64_t)t), kPmKey, (uint64_t)i), 0);
+  };
+  if (!block_normalize(N, alpha, W, red)) {
+    if (threadIdx.x == 0) { a.status[c] = AUXMC_E_DEGENERATE; a.bad_t[c] = T; }
+    return;
+  }
+  block_cumsum(N, W, cum);
+  if (threadIdx.x == 0) {
+    const int sel = draw_index(N, cum, uniform_at(derive(it, kTerminalIndex, 0), 0));
+    for (int k = 0; k < d; ++k) chosen[k] = tr[(size_t)T * d + k] = P[((size_t)T * N + sel) * d + k];
+    tk[T] = pm_key(T, sel);
+    if (a.sel) a.sel[(size_t)c * (T + 1) + T] = sel;
+  }
+  __syncthreads();
+  for (int t = T - 1; t >= 0; --t) {
+    const int jq = jq0 + (f.fl.nQ > 1 ? t : 0);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const double* xi = P + ((size_t)t * N + i) * d;
+      for (int k = 0; k < d; ++k) r[k] = chosen[k] - dyn_mean_i(tg, t, xi, k);
+      alpha[i] = A[(size_t)t * N + i] + gauss_term(d, r, f.L(jq), f.logdet[jq]);
+    }
+    __syncthreads();
+    if (!block_normalize(N, alpha, W, red)) {
+      if (threadIdx.x == 0) { a.status[c] = AUXMC_E_DEGENERATE; a.bad_t[c] = t; }
+      return;
+    }
+    block_cumsum(N, W, cum);
+    if (threadIdx.x == 0) {
+      const int sel = draw_index(N, cum, uniform_at(derive(it, kBackwardIndex, (uint64_t)t), 0));
+      for (int k = 0; k < d; ++k) chosen[k] = tr[(size_t)t * d + k] = P[((size_t)t * N + sel) * d + k];
+      tk[t] = pm_key(t, sel);
+      if (a.sel) a.sel[(size_t)c * (T + 1) + t] = sel;
+    }
+    __syncthreads();
+  }
+}
+
+// adopt the new path (fkpg.cpp:269-273)
+__global__ void k_pg_commit(int C, int T, int d, const double* traj, const uint64_t* tkeys,
+                            const int* status, double* x, uint64_t* keys, long long* iter,
+                            long long* updates, double* last_update) {
+  const int c = blockIdx.x;
+  __shared__ int changed;
+  if (threadIdx.x == 0) changed = 0;
+  __syncthreads();
+  const size_t n = (size_t)(T + 1) * d;
+  const bool ok = status[c] == AUXMC_OK;
+  if (ok)
+    for (size_t q = threadIdx.x; q < n; q += blockDim.x)
+      if (__double_as_longlong(traj[c * n + q]) != __double_as_longlong(x[c * n + q])) changed = 1;
+  __syncthreads();
+  if (ok) {
+    for (size_t q = threadIdx.x; q < n; q += blockDim.x) x[c * n + q] = traj[c * n + q];
+    for (int t = threadIdx.x; t <= T; t += blockDim.x)
+      keys[(size_t)c * (T + 1) + t] = tkeys[(size_t)c * (T + 1) + t];
+  }
+  if (threadIdx.x == 0) {
+    iter[c] += 1;
+    if (ok) {
+      last_update[c] = changed ? 1.0 : 0.0;
+      if (changed) updates[c] += 1;
+    }
+  }
+}
+
+__global__ void k_pg_adapt(int C, const long long* iter, const double* last_update, double target,
+                           double* delta) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double n = (double)(iter[c] > 1 ? iter[c] : 1);
+  delta[c] = exp(log(delta[c]) + pow(n, -0.6) * (last_update[c] - target));
+}
+
+static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int variant, Arena& ws,
+                   cudaStream_t s) {
+  const int C = ch->C, N = ch->N, T = tg.T, d = tg.dx;
+  const FactorLayout fl = factor_layout(tg);
+  uint64_t* it = ws.take<uint64_t>(C);
+  double* u = ws.take<double>((size_t)C * (T + 1) * d);
+  double* mq = ws.take<double>((size_t)C * (T + 1) * d);
+  double* part = ws.take<double>((size_t)C * (T + 1) * N * d);
+  double* Wt = ws.take<double>((size_t)C * (T + 1) * N);
+  double* lw = variant == AUXMC_CSMC_PIT ? ws.take<double>((size_t)C * (T + 1) * N) : nullptr;
+  double* traj = ws.take<double>((size_t)C * (T + 1) * d);
+  uint64_t* tkeys = ws.take<uint64_t>((size_t)C * (T + 1));
+  double* Ls = ws.take<double>((size_t)fl.total() * fl.W * fl.W);
+  double* logdet = ws.take<double>(fl.total());
+  int* ints = ws.take<int>((size_t)C + 1);
+  if (ws.base == nullptr) return AUXMC_OK;
+  if (!it || !u || !mq || !part || !Wt || !traj || !tkeys || !Ls || !logdet || !ints ||
+      (variant == AUXMC_CSMC_PIT && !lw))
+    return AUXMC_E_WORKSPACE;
+  AUXMC_CUDA_TRY(cudaMemsetAsync(ch->status, 0, sizeof(int) * C, s));
+  AUXMC_CUDA_TRY(cudaMemsetAsync(ch->bad_t, 0xff, sizeof(int) * C, s));
+  AUXMC_CUDA_TRY(cudaMemsetAsync(ints, 0, sizeof(int) * (C + 1), s));
+  int rc = launch_target_factors(tg, Ls, logdet, ints + C, s);
+  if (rc) return rc;
+  FactorRef f{fl, Ls, logdet};
+  AUXMC_LAUNCH(k_pg_keys, (C + 127) / 128, 128, 0, s, C, ch->root_keys, ch->iter, it);
+  rc = launch_aux_obs(C, T, d, ch->x, ch->delta, it, u, s);
+  if (rc) return rc;
+  const long long nct = (long long)C * (T + 1);
+  AUXMC_LAUNCH(k_pg_prop_mean, (int)std::min<long long>((nct + 127) / 128, 148LL * 32), 128, 0, s,
+               tg, f, C, u, ch->delta, mq, ints);
+  PgArgs a{C, N, ch->x, ch->keys, ch->delta, it, u, mq, part, Wt, traj, tkeys, ch->status,
+           ch->bad_t, ch->ancestors, ch->selected, ints};
+  const int threads = N >= 256 ? 256 : ((N + 31) / 32) * 32;
+  if (variant == AUXMC_CSMC_REFERENCE) {
+    const size_t smem = sizeof(double) * (3 * N + 40 + 64) + sizeof(int) * N;
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_csmc_reference,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    AUXMC_LAUNCH(k_csmc_reference, C, threads, smem, s, tg, f, a);
+  } else {
+    const long long np = nct * N;
+    AUXMC_LAUNCH(k_pit_particles, (int)std::min<long long>((np + 255) / 256, 148LL * 64), 256, 0, s,
+                 tg, f, a, lw);
+    const size_t smem = sizeof(double) * (3 * N + (size_t)N * d + 40 + 64);
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pit_forward_backward,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    AUXMC_LAUNCH(k_pit_forward_backward, C, threads, smem, s, tg, f, a, lw);
+  }
+  AUXMC_LAUNCH(k_pg_commit, C, 256, 0, s, C, T, d, traj, tkeys, ch->status, ch->x, ch->keys,
+               ch->iter, ch->updates, ch->last_update);
+  return AUXMC_OK;
+}
+
+}  // namespace auxmc_gpu
+
+using namespace auxmc_gpu;
+
+extern "C" {
+
+size_t auxmc_aux_pgibbs_workspace(const auxmc_target* target, int C, int N, int variant) {
+  if (check_target(target) || C < 0 || N < 1) return 0;
+  Arena ws{nullptr, 0, 0};
+  auxmc_pg_chains ch{};
+  ch.C = C;
+  ch.N = N;
+  pg_step(to_dev_target(*target), &ch, variant, ws, nullptr);
+  return ws.used + 4096;
+}
+
+int auxmc_aux_pgibbs_step(const auxmc_target* target, auxmc_pg_chains* chains, int mode,
+                          int variant, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  int st = check_target(target);
+  if (st) return st;
+  if (mode != AUXMC_PG_GRADIENT) return AUXMC_E_ARG;  // prior / fully adapted: see DESIGN.md
+  if (variant != AUXMC_CSMC_REFERENCE && variant != AUXMC_CSMC_PIT) return AUXMC_E_ARG;
+  if (!chains || chains->C < 0 || chains->N < 1 || chains->N > 4096 || !chains->x ||
+      !chains->keys || !chains->delta || !chains->iter || !chains->updates ||
+      !chains->last_update || !chains->root_keys || !chains->status || !chains->bad_t)
+    return AUXMC_E_ARG;
+  if (chains->C == 0) return AUXMC_OK;
+  if (!workspace) return AUXMC_E_WORKSPACE;
+  Arena ws{(char*)workspace, workspace_bytes, 0};
+  return pg_step(to_dev_target(*target), chains, variant, ws, (cudaStream_t)stream);
+}
+
+int auxmc_pg_adapt_delta(auxmc_pg_chains* chains, double target_rate, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  if (!chains || !chains->delta || !chains->iter || !chains->last_update) return AUXMC_E_ARG;
+  if (chains->C == 0) return AUXMC_OK;
+  AUXMC_LAUNCH(k_pg_adapt, (chains->C + 127) / 128, 128, 0, stream, chains->C, chains->iter,
+               chains->last_update, target_rate, chains->delta);
+  return AUXMC_OK;
+}
+
+}  // extern "C"

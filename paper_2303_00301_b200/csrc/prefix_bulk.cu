@@ -346,13 +346,15 @@ int run_prefix_bulk(int T, int B, const double* elems, const double* term, Arena
   }
   const int grid = std::max((B + G::SLOTS - 1) / G::SLOTS, std::min(B, num_sms()));
   if (nz.kind == AUXMC_NOISE_PREDRAWN) {
-    auto kern = k_prefix_bulk<D, true>;
-    AUXMC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-    AUXMC_LAUNCH(kern, grid, G::WARPS * 32, G::SMEM, stream, T, B, tiles, term, nz, traj);
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_prefix_bulk<D, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    AUXMC_LAUNCH((k_prefix_bulk<D, true>), grid, G::WARPS * 32, G::SMEM, stream, T, B, tiles, term,
+                 nz, traj);
   } else {
-    auto kern = k_prefix_bulk<D, false>;
-    AUXMC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-    AUXMC_LAUNCH(kern, grid, G::WARPS * 32, G::SMEM, stream, T, B, tiles, term, nz, traj);
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_prefix_bulk<D, false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+    AUXMC_LAUNCH((k_prefix_bulk<D, false>), grid, G::WARPS * 32, G::SMEM, stream, T, B, tiles,
+                 term, nz, traj);
   }
   return AUXMC_OK;
 }
