@@ -545,6 +545,24 @@ class AuxChain:
         lib().ao_adapt_delta(C.byref(self.c), target_rate)
 
 
+def aux_model_filter(tg: OTarget, x, u, delta, zeroth_order=False):
+    """build_aux_lgssm (auxk.cpp:56-118) then kalman_filter; returns (FilterResult, obs)."""
+    x, u = _f64(x), _f64(u)
+    m = LGSSM()
+    obs = C.POINTER(C.c_double)()
+    lib().ao_build_aux_lgssm.argtypes = [C.POINTER(Target), PD, PD, C.c_double, C.c_int, PD,
+                                         C.POINTER(LGSSM), C.POINTER(PD)]
+    _check(lib().ao_build_aux_lgssm(C.byref(tg.raw), _p(x), _p(u), delta, int(zeroth_order), None,
+                                    C.byref(m), C.byref(obs)), "build_aux_lgssm")
+    T, dy = m.T, m.dy
+    ob = np.ctypeslib.as_array(obs, shape=((T + 1) * dy,)).copy().reshape(T + 1, dy)
+    fr = FilterResult(T, m.dx)
+    raw = fr.raw()
+    _check(lib().ao_kalman_filter(C.byref(m), obs, C.byref(raw)), "kalman_filter")
+    fr.log_marginal = raw.log_marginal
+    return fr, ob
+
+
 def sample_aux_obs(x, delta, it: Stream):
     x = _f64(x)
     u = np.zeros_like(x)

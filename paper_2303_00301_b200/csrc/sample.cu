@@ -157,6 +157,153 @@ __global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
   }
 }
 
+// Register path of k_bwd_elements for small d: one thread per (b, t).
+template <int D>
+__global__ void k_bwd_elements_reg(DevModel m, const double* __restrict__ filt_mean,
+                                   const double* __restrict__ filt_cov,
+                                   const double* __restrict__ pred_cov, int Bfr, double* elems,
+                                   double* term, int* status, int store_cov) {
+  constexpr int DD = D * D;
+  const int T = m.T;
+  const long long n_items = (long long)Bfr * (T + 1);
+  for (long long item = (long long)blockIdx.x * blockDim.x + threadIdx.x; item < n_items;
+       item += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(item / (T + 1)), t = (int)(item % (T + 1));
+    const double* fm = filt_mean + (size_t)b * (T + 1) * D;
+    const double* fc = filt_cov + (size_t)b * (T + 1) * DD;
+    double P[DD], L[DD];
+#pragma unroll
+    for (int i = 0; i < DD; ++i) P[i] = fc[(size_t)t * DD + i];
+    int st = 0;
+    if (t == T) {  // terminal law (pit.cpp:85-87)
+      st = r_chol_psd<D>(P, L);
+      double* out = term + (size_t)b * term_stride(D);
+#pragma unroll
+      for (int i = 0; i < D; ++i) out[i] = fm[(size_t)T * D + i];
+#pragma unroll
+      for (int i = 0; i < DD; ++i) out[D + i] = L[i];
+    } else {  // backward_step (lgssm.cpp:129-149)
+      const double* Fp = m.Ft(t, b);
+      double F[DD], G[DD], X[DD], A[DD], W[DD];
+#pragma unroll
+      for (int i = 0; i < DD; ++i) F[i] = Fp[i];
+      bool zero = true;
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {  // X = cross^T = (P F^T)^T, X[j][i] = cross[i][j]
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) s += P[i * D + k] * F[j * D + k];
+          X[j * D + i] = s;
+          zero = zero && (s == 0.0);
+        }
+      if (zero) {
+#pragma unroll
+        for (int i = 0; i < DD; ++i) G[i] = 0.0;
+      } else {
+        double S[DD];
+        const double* Sp = pred_cov + ((size_t)b * (T + 1) + t + 1) * DD;
+#pragma unroll
+        for (int i = 0; i < DD; ++i) S[i] = Sp[i];
+        st = r_factor_psd<D>(S, L);
+        r_llt_solve<D, D>(L, X);
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+          for (int j = 0; j < D; ++j) G[i * D + j] = X[j * D + i];
+      }
+      if (g_flip_backward_gain) {
+#pragma unroll
+        for (int i = 0; i < DD; ++i) G[i] = -G[i];
+      }
+      const double* mt = fm + (size_t)t * D;
+      const double* bt = m.bt(t, b);
+      double v[D], off[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) s += F[i * D + j] * mt[j];
+        v[i] = s + bt[i];
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) s += G[i * D + j] * v[j];
+        off[i] = mt[i] - s;
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {  // A = I - G F
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) s += G[i * D + k] * F[k * D + j];
+          A[i * D + j] = (i == j ? 1.0 : 0.0) - s;
+        }
+      // Λ = symm(A P A^T + G Q G^T)
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) s += A[i * D + k] * P[k * D + j];
+          W[i * D + j] = s;
+        }
+      double Lam[DD];
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) s += W[i * D + k] * A[j * D + k];
+          Lam[i * D + j] = s;
+        }
+      const double* Qp = m.Qt(t, b);
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) s += G[i * D + k] * Qp[k * D + j];
+          W[i * D + j] = s;
+        }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) s += W[i * D + k] * G[j * D + k];
+          Lam[i * D + j] += s;
+        }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = i + 1; j < D; ++j) {
+          const double s = 0.5 * (Lam[i * D + j] + Lam[j * D + i]);
+          Lam[i * D + j] = s;
+          Lam[j * D + i] = s;
+        }
+      if (!store_cov && !st) st = r_chol_psd<D>(Lam, L);
+      double* out = elems + ((size_t)b * T + t) * elem_stride(D);
+#pragma unroll
+      for (int i = 0; i < DD; ++i) {
+        out[i] = G[i];
+        out[DD + D + i] = store_cov ? Lam[i] : L[i];
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i) out[DD + i] = off[i];
+    }
+    if (st) atomicMax(status + b, st);
+  }
+}
+
 // ---------------------------------------------------------------- noise
 
 template <int D>
@@ -423,7 +570,18 @@ int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, 
   const int d = dm.dx;
   const int per = 9 * d * d + 4 * d + 4;
   const long long n_items = (long long)Bfr * (dm.T + 1);
-  if (d > 16) {
+  if (d <= 4) {
+    const int grid = (int)std::min<long long>((n_items + 127) / 128, 148LL * 16);
+    switch (d) {
+#define CASE(D)                                                                                  \
+  case D:                                                                                        \
+    AUXMC_LAUNCH(k_bwd_elements_reg<D>, grid, 128, 0, stream, dm, fm, fc, pc, Bfr, elems, term, \
+                 st_fr, store_cov);                                                              \
+    break;
+      CASE(1) CASE(2) CASE(3) CASE(4)
+#undef CASE
+    }
+  } else if (d > 16) {
     const size_t smem = sizeof(double) * per;
     AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_bwd_elements<true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

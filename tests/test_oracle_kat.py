@@ -141,6 +141,65 @@ def test_filter_and_smoother_match_dense_oracle(oracle, seed):
         assert np.max(np.abs(sc[t] - cov[t * d:(t + 1) * d, t * d:(t + 1) * d])) < 1e-7
 
 
+def test_dense_oracle_two_step_scalar(oracle):
+    """test_lgssm.cpp:324-341: hand-conditioned two-step scalar case."""
+    p0, f, q, r, y1 = 1.0, 0.5, 0.3, 0.4, 0.8
+    m = scalar_model(oracle, 1, 0.0, p0, f, 0.0, q, 1.0, 0.0, r, np.array([0, 1], np.uint8))
+    mean, cov, _ = oracle.dense_oracle(m, np.array([[0.0], [y1]]))
+    joint = np.array([[p0, f * p0], [f * p0, f * f * p0 + q]])
+    s = joint[1, 1] + r
+    want_mean = np.array([joint[0, 1] / s * y1, joint[1, 1] / s * y1])
+    want_cov = joint - np.outer(joint[:, 1], joint[:, 1]) / s
+    assert np.max(np.abs(mean - want_mean)) < 1e-12
+    assert np.max(np.abs(cov - want_cov)) < 1e-12
+
+
+def test_backward_elements_limits(oracle):
+    """test_pit.cpp:58-84: uninformative future collapses to the filtered law;
+    deterministic copy dynamics give identity maps."""
+    T = 3
+    m = scalar_model(oracle, T, 0.2, 1.0, 0.9, 0.0, 1e12, 1.0, 0.0, 0.5)
+    fr = oracle.kalman_filter(m, np.array([[0.1], [-0.4], [0.3], [0.2]]))
+    for t in range(T):
+        G, off, cov = oracle.backward_step(m, fr, t)
+        assert abs(G[0, 0]) < 1e-9
+        assert abs(off[0] - fr.filt_mean[t, 0]) <= 1e-6 * abs(fr.filt_mean[t, 0]) + 1e-12
+        assert abs(cov[0, 0] - fr.filt_cov[t, 0, 0]) <= 1e-6 * fr.filt_cov[t, 0, 0]
+    T = 4
+    m = scalar_model(oracle, T, 0.0, 1.0, 1.0, 0.0, 0.0, 1.0, 0.0, 0.5)
+    fr = oracle.kalman_filter(m, np.zeros((T + 1, 1)))
+    for t in range(T):
+        G, off, cov = oracle.backward_step(m, fr, t)
+        assert abs(G[0, 0] - 1.0) < 1e-10 and abs(off[0]) < 1e-10 and abs(cov[0, 0]) < 1e-10
+
+
+def test_aux_model_scalar_conjugate_posterior(oracle):
+    """test_target_auxk.cpp:153-180: exact potential + aux row == conjugate update."""
+    m0, p0, r, y, uu, delta = 0.3, 1.2, 0.5, 0.9, -0.1, 0.8
+    m = scalar_model(oracle, 0, m0, p0, 1.0, 0.0, 1.0, 1.0, 0.0, r)
+    tg = oracle.target_from_lgssm(m, np.array([[y]]), generic=False)
+    fr, obs = oracle.aux_model_filter(tg, np.array([[0.2]]), np.array([[uu]]), delta)
+    prec = 1.0 / p0 + 1.0 / r + 2.0 / delta
+    mean = (m0 / p0 + y / r + 2.0 * uu / delta) / prec
+    assert abs(fr.filt_mean[0, 0] - mean) < 1e-10 * abs(mean)
+    assert abs(fr.filt_cov[0, 0, 0] - 1.0 / prec) < 1e-10 / prec
+
+
+def test_aux_model_potential_free_observes_noisy_copies(oracle):
+    """test_target_auxk.cpp:119-134: z = u, H = 1, R = δ/2 with no potentials."""
+    T = 3
+    m = scalar_model(oracle, T, 0.0, 1.0, 0.9, 0.0, 0.2, 1.0, 0.0, 1.0,
+                     np.zeros(T + 1, np.uint8))
+    tg = oracle.target_from_lgssm(m, np.zeros((T + 1, 1)), generic=False)
+    u = np.array([[0.1], [-0.2], [0.3], [0.0]])
+    fr, obs = oracle.aux_model_filter(tg, np.zeros((T + 1, 1)), u, 0.5)
+    assert np.array_equal(obs[:, :1], u)
+    # posterior of a 0.9-AR(1) observed through z = u with variance 0.25
+    want = oracle.kalman_filter(oracle.Model.homogeneous(T, [0.0], [[1.0]], [[0.9]], [0.0], [[0.2]],
+                                                         [[1.0]], [0.0], [[0.25]]), u)
+    assert np.max(np.abs(fr.filt_mean - want.filt_mean)) < 1e-12
+
+
 # ---------------------------------------------------------------- pit (test_pit.cpp)
 @pytest.mark.parametrize("seed", range(1, 11))
 def test_sampler_laws_equal_dense_posterior(oracle, seed):
