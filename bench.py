@@ -42,7 +42,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="c2", choices=["c2", "c1", "c3"])
+    p.add_argument("--config", default="c2", choices=["c2", "c1", "c3", "c4"])
     p.add_argument("--sampler", default="prefix", choices=["prefix", "dnc", "seq"])
     p.add_argument("--noise", default="predrawn", choices=["predrawn", "rng"])
     p.add_argument("--chains", type=int, default=0, help="chains per GPU (0 = config default)")

@@ -217,11 +217,14 @@ class AuxChains:
                                                  ws.numel(), torch.cuda.current_stream().cuda_stream),
                    "init_chains")
 
-    def kernel_step(self, backend=Backend.kSequential, zeroth_order=False, stream=None):
+    def kernel_step(self, backend=Backend.kSequential, zeroth_order=False, parallel_filter=False,
+                    stream=None):
+        """auxk::kernel_step (auxk.cpp:130-198) for every chain; KernelOptions fields
+        (auxk.hpp:34-39) as keyword arguments."""
         lib = _lib.load()
         tr, ch = self.target.raw(), self.raw()
-        o = _lib.KernelOptions(int(backend), 0, int(zeroth_order))
-        key = (int(backend), bool(zeroth_order))
+        o = _lib.KernelOptions(int(backend), int(parallel_filter), int(zeroth_order))
+        key = (int(backend), bool(zeroth_order), bool(parallel_filter))
         if self._ws_key != key:
             self._ws_bytes = lib.auxmc_aux_kernel_workspace(C.byref(tr), self.C, C.byref(o))
             self._ws_key = key

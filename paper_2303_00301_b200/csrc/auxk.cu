@@ -22,6 +22,8 @@
 
 namespace auxmc_gpu {
 
+int launch_filter_pit(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
+                      int* status, Arena& ws, cudaStream_t stream);
 int launch_filter_seq(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
                       int* status, cudaStream_t stream);
 int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int fr_shared,
@@ -423,6 +425,10 @@ static int aux_step(const DevTarget& tg, auxmc_chains* ch, const auxmc_kernel_op
   int rc;
   // sub-arenas for the sampler, log γ and gradients (sizing pass included)
   if (ws.base == nullptr) {
+    if (o.parallel_filter) {
+      rc = launch_filter_pit(dm, z, C, &fr, nullptr, ws, s);
+      if (rc) return rc;
+    }
     rc = launch_sample_paths(dm, &fr, 0, &nz, C, sampler, prop, nullptr, ws, s);
     if (rc) return rc;
     rc = launch_log_gamma(tg, C, prop, sc.lg_prop, nullptr, ws, s);
@@ -444,7 +450,15 @@ static int aux_step(const DevTarget& tg, auxmc_chains* ch, const auxmc_kernel_op
   // forward: surrogate at x, filter, proposal, log q(x'|x)
   AUXMC_LAUNCH(k_build_aux, grid_for((long long)C * (T + 1), 128), 128, 0, s, tg, C,
                o.zeroth_order, ch->x, ch->grad_gen, u, ch->delta, z, Fa, ba);
-  rc = launch_filter_seq(dm, z, C, &fr, sc.st_filt, s);
+  Arena pf_ws = ws;  // scan-filter scratch (sized in the sizing pass above)
+  auto filter = [&](int* st) {
+    if (o.parallel_filter) {
+      Arena sub = pf_ws;
+      return launch_filter_pit(dm, z, C, &fr, st, sub, s);
+    }
+    return launch_filter_seq(dm, z, C, &fr, st, s);
+  };
+  rc = filter(sc.st_filt);
   if (rc) return rc;
   rc = launch_sample_paths(dm, &fr, 0, &nz, C, sampler, prop, sc.st_samp, ws, s);
   if (rc) return rc;
@@ -463,7 +477,7 @@ static int aux_step(const DevTarget& tg, auxmc_chains* ch, const auxmc_kernel_op
   // reverse: surrogate at x', filter, log q(x|x')
   AUXMC_LAUNCH(k_build_aux, grid_for((long long)C * (T + 1), 128), 128, 0, s, tg, C,
                o.zeroth_order, prop, gprop, u, ch->delta, z, Fa, ba);
-  rc = launch_filter_seq(dm, z, C, &fr, sc.st_filt_r, s);
+  rc = filter(sc.st_filt_r);
   if (rc) return rc;
   rc = launch_path_logpdf(dm, z, (long long)(T + 1) * p, ch->x, fr.log_marginal, 0, C,
                           sc.logq_rev, sc.st_lqr, s);
@@ -528,7 +542,6 @@ int auxmc_aux_kernel_step(const auxmc_target* target, auxmc_chains* chains,
       !chains->grad_gen || !chains->iter || !chains->stats || !chains->root_keys)
     return AUXMC_E_ARG;
   if (opts->backend < 0 || opts->backend > 2) return AUXMC_E_ARG;
-  if (opts->parallel_filter) return AUXMC_E_ARG;  // scan filter: see auxmc_kalman_filter mode 1
   if (chains->C == 0) return AUXMC_OK;
   if (!workspace) return AUXMC_E_WORKSPACE;
   Arena ws{(char*)workspace, workspace_bytes, 0};

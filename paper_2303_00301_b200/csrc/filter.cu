@@ -176,10 +176,3 @@ int launch_filter_seq(const DevModel& dm, const double* obs, int B, auxmc_filter
 
 }  // namespace auxmc_gpu
 
-namespace auxmc_gpu {
-size_t filter_pit_workspace(const DevModel& dm, int B) { return 0; }
-int launch_filter_pit(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
-                      int* status, Arena& ws, cudaStream_t stream) {
-  return AUXMC_E_ARG;  // implemented in pitfilter.cu
-}
-}  // namespace auxmc_gpu

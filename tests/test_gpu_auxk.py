@@ -131,3 +131,23 @@ def test_log_gamma_and_grad_match_oracle(aux, oracle):
     got = gtg.log_gamma(paths).cpu().numpy()
     want = [otg.log_gamma(p) for p in paths]
     assert_close(got, want, 1e-10, "log_gamma")
+
+
+@pytest.mark.parametrize("backend", [0, 1])
+def test_parallel_filter_option(aux, oracle, backend):
+    """KernelOptions::parallel_filter (auxk.cpp:143-146): scan filter inside the step."""
+    auxk, bm = aux
+    so = oracle.spec("stochvol", T=30, dx=3, data_seed=11)
+    lat, data = oracle.simulate(so)
+    otg = oracle.make_target(so, data)
+    gtg = auxk.make_target(bm.ModelSpec(kind="stochvol", T=30, dx=3, data_seed=11), data)
+    ch = auxk.init_chains(gtg, lat, 1.0, 4, 3)
+    oc = [oracle.AuxChain(otg, lat, 1.0) for _ in range(3)]
+    root = oracle.from_seed(4)
+    for it in range(6):
+        ch.kernel_step(backend, parallel_filter=True)
+        for c, o in enumerate(oc):
+            o.step(oracle.derive(root, oracle.L_CHAIN, c), backend, 1)
+        assert np.array_equal(ch.accepted.cpu().numpy(), [o.c.stats.accepted for o in oc])
+    for c, o in enumerate(oc):
+        assert_close(ch.x[c].cpu().numpy(), o.x, 1e-8, "path")

@@ -206,3 +206,32 @@ def test_device_normals_match_stream(gpu, oracle):
             s = oracle.derive(base, 1, 5 + i)
             want = oracle.normal_vec(s, 4)
             assert np.all(np.abs(out[c, i] - want) <= 4e-16 * np.maximum(1, np.abs(want)))
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_parallel_filter_matches_oracle(gpu, oracle, case):
+    """pit::parallel_filter (pit.cpp:117-188): GPU blocked scan vs the oracle's
+    Sklansky scan and vs the sequential filter (test_pit.cpp:188-229)."""
+    lgssm, _, _ = gpu
+    m, obs = _oracle_case(oracle, *case)
+    seq = oracle.kalman_filter(m, obs)
+    par, _ = oracle.parallel_filter(m, obs)
+    fr = lgssm.parallel_filter(to_gpu_model(m), obs)
+    assert int(fr.status[0]) == 0
+    assert_close(fr.filt_mean[0].cpu(), par.filt_mean, 1e-8, "filt_mean vs oracle scan")
+    assert_close(fr.filt_cov[0].cpu(), par.filt_cov, 1e-8, "filt_cov vs oracle scan")
+    assert_close(fr.pred_cov[0].cpu(), par.pred_cov, 1e-8, "pred_cov vs oracle scan")
+    assert_close(fr.log_marginal[0].cpu(), par.log_marginal, 1e-9, "log_marginal")
+    assert_close(fr.filt_mean[0].cpu(), seq.filt_mean, 1e-6, "filt_mean vs sequential")
+
+
+def test_parallel_filter_batched_long(gpu, oracle):
+    lgssm, _, _ = gpu
+    s = oracle.spec("lgssm-synthetic", T=5000, dx=4, dy=1, data_seed=1)
+    lat, data = oracle.simulate(s)
+    m = oracle.synthetic_lgssm(s)
+    seq = oracle.kalman_filter(m, data)
+    fr = lgssm.parallel_filter(to_gpu_model(m), np.stack([data, data]))
+    for b in range(2):
+        assert_close(fr.filt_mean[b].cpu(), seq.filt_mean, 1e-8, "filt_mean")
+        assert_close(fr.log_marginal[b].cpu(), seq.log_marginal, 1e-9, "log_marginal")

@@ -1,0 +1,95 @@
+"""Secondary bench configurations (bench.py --config c1|c3|c4), one JSON line each.
+
+c1: auxiliary Kalman sampler, 1-D LGSSM, T = 1024, 1 chain, prefix backend
+    (BASELINE.json configs[0]); a step is one MCMC iteration.
+c3: Lorenz-96 d = 40 diffusion smoothing, auxiliary Kalman sampler, T = 4096,
+    256 chains, sequential backend (configs[2]).
+c4: stochastic volatility d = 3, auxiliary particle Gibbs, N = 256, T = 2^14
+    (configs[3]), parallel-in-time cSMC (--sampler dnc selects the reference cSMC).
+Units: chain-timesteps/s = chains * (T+1) * iterations / device seconds.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+
+METRIC = "chain-timesteps/sec (device-timed) at 1/2/4/8 B200; MCMC iters/sec; % HBM/FP64 roofline"
+FP64_PEAK_TFLOPS = 37.0  # datasheet placeholder (no measured DFMA peak in MEASURED_PEAKS.json)
+
+
+def run(args, rank, world, local):
+    import torch
+    from bench import Clocks, timed
+    from paper_2303_00301_b200 import _lib, auxk, bench_models as bm, fkpg
+    device = f"cuda:{local}"
+    torch.cuda.set_device(local)
+    lib = _lib.load()
+    cfg = args.config
+    if cfg == "c1":
+        T, C, d = args.T or 1024, args.chains or 1, 1
+        spec = bm.ModelSpec(kind="lgssm-synthetic", T=T, dx=1, dy=1, data_seed=1)
+        backend, delta = auxk.Backend.kPrefix, 1.0
+        flops_ct = 130.0  # F_pit, scan filter counted
+    elif cfg == "c3":
+        T, C, d = args.T or 4096, args.chains or 256, 40
+        spec = bm.ModelSpec(kind="lorenz96", T=T, dx=40, data_seed=3)
+        backend, delta = auxk.Backend.kSequential, 0.05
+        flops_ct = 2.14e6  # F_seq at d = 40, q = 20
+    else:
+        T, C, d = args.T or 16384, args.chains or 148, 3
+        spec = bm.ModelSpec(kind="stochvol", T=T, dx=3, data_seed=11)
+        delta = 1.0
+        N = 256
+        flops_ct = N * N * (3 * d * d + d + 20.0)
+    lat, data = bm.simulate(spec)
+    tg = auxk.make_target(spec, data, device=device)
+    x0 = torch.as_tensor(lat, device=device) if cfg != "c1" else \
+        torch.as_tensor(lat * 0 + tg.m0.cpu().numpy(), device=device)
+    if cfg == "c4":
+        variant = fkpg.Variant.kReference if args.sampler == "dnc" else fkpg.Variant.kPit
+        ch = fkpg.init_pg(tg, x0, delta, 1, C, N, first=rank * C)
+
+        def step():
+            ch.aux_pgibbs_step(variant)
+    else:
+        ch = auxk.init_chains(tg, x0, delta, 1, C, first=rank * C)
+
+        def step():
+            ch.kernel_step(backend)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    n0 = lib.auxmc_launch_count()
+    with Clocks(local) as clk:
+        ms = timed(step, args.steps, world)
+    launches = lib.auxmc_launch_count() - n0
+    ct = C * (T + 1) * args.steps * world
+    value = ct / (ms / 1e3)
+    tflops = flops_ct * ct / (ms / 1e3) / 1e12
+    if rank == 0:
+        extra = {}
+        if cfg != "c4":
+            extra["accept_rate"] = float(ch.accepted.sum()) / max(1, float(
+                (ch.accepted + ch.rejected).sum()))
+        else:
+            extra["update_rate"] = float(ch.updates.sum()) / max(1, float(ch.iter.sum()))
+        line = {
+            "metric": METRIC, "value": value, "unit": "chain-timesteps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": {"c1": "C1 aux-Kalman 1-D LGSSM prefix backend",
+                                    "c3": "C3 aux-Kalman Lorenz-96 d=40 sequential backend",
+                                    "c4": "C4 stochvol aux particle Gibbs N=256"}[cfg],
+                       "T": T, "chains_per_gpu": C, "mcmc_iters_per_sec": 1e3 * args.steps / ms,
+                       **extra},
+            "roofline": {"bound": "fp64" if cfg != "c1" else "latency",
+                         "achieved": tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": tflops / FP64_PEAK_TFLOPS, "traffic": None,
+                         "algorithmic_flops_per_chain_timestep": flops_ct,
+                         "peak_source": "datasheet placeholder (no measured FP64 peak)"},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
