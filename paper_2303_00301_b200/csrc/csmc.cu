@@ -377,6 +377,7 @@ __global__ void k_pit_particles(DevTarget tg, FactorRef f, PgArgs a, double* lw)
 
 // Forward log-messages alpha_t(j) = lw_t(j) + LSE_i(alpha_{t-1}(i) + log p(x_t^j | x_{t-1}^i)),
 // one CTA per chain, then backward index sampling with the reference's addresses.
+template <int DT>
 __global__ void k_pit_forward_backward(DevTarget tg, FactorRef f, PgArgs a, const double* lw) {
   extern __shared__ double sm[];
   const int N = a.N, T = tg.T, d = tg.dx;
@@ -413,14 +414,82 @@ __global__ void k_pit_forward_backward(DevTarget tg, FactorRef f, PgArgs a, cons
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
       const double* xj = P + ((size_t)t * N + j) * d;
       double m = -INFINITY, s = 0.0;  // online log-sum-exp over i
-      for (int i = 0; i < N; ++i) {
-        for (int k = 0; k < d; ++k) r[k] = xj[k] - mprev[i * d + k];
-        const double v = (alpha[i] - am) + gauss_term(d, r, LQ, ldq);
-        if (v > m) {
-          s = s * exp(m - v) + 1.0;
-          m = v;
-        } else {
-          s += exp(v - m);
+      if constexpr (DT > 0) {
+        // register path: x_t^j and the lower factor of Q held in registers
+        double xr[DT], Lr[DT * DT];
+#pragma unroll
+        for (int k = 0; k < DT; ++k) xr[k] = xj[k];
+#pragma unroll
+        for (int k = 0; k < DT * DT; ++k) Lr[k] = LQ[k];
+        // Every transition log-density is <= M = -0.5 d log 2π - log|L_Q| and
+        // alpha - am <= 0, so exp(v - M) never overflows: four independent
+        // accumulators give ILP without a running max.  If everything
+        // underflows (s == 0) the exact online log-sum-exp below takes over.
+        const double M = -0.5 * (DT * kLog2Pi) - ldq;
+        double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+        int i = 0;
+        for (; i + 4 <= N; i += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            double z[DT], sq = 0.0;
+#pragma unroll
+            for (int k = 0; k < DT; ++k) {
+              double acc = xr[k] - mprev[(i + u) * DT + k];
+#pragma unroll
+              for (int l = 0; l < k; ++l) acc -= Lr[k * DT + l] * z[l];
+              z[k] = acc / Lr[k * DT + k];
+              sq += z[k] * z[k];
+            }
+            const double v = (alpha[i + u] - am) + (-0.5 * (DT * kLog2Pi + sq) - ldq);
+            acc4[u] += exp(v - M);
+          }
+        }
+        for (; i < N; ++i) {
+          double z[DT], sq = 0.0;
+#pragma unroll
+          for (int k = 0; k < DT; ++k) {
+            double acc = xr[k] - mprev[i * DT + k];
+#pragma unroll
+            for (int l = 0; l < k; ++l) acc -= Lr[k * DT + l] * z[l];
+            z[k] = acc / Lr[k * DT + k];
+            sq += z[k] * z[k];
+          }
+          acc4[0] += exp((alpha[i] - am) + (-0.5 * (DT * kLog2Pi + sq) - ldq) - M);
+        }
+        s = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+        m = M;
+        if (!(s > 0.0)) {  // total underflow: exact online log-sum-exp
+          m = -INFINITY;
+          s = 0.0;
+          for (int i2 = 0; i2 < N; ++i2) {
+            double z[DT], sq = 0.0;
+#pragma unroll
+            for (int k = 0; k < DT; ++k) {
+              double acc = xr[k] - mprev[i2 * DT + k];
+#pragma unroll
+              for (int l = 0; l < k; ++l) acc -= Lr[k * DT + l] * z[l];
+              z[k] = acc / Lr[k * DT + k];
+              sq += z[k] * z[k];
+            }
+            const double v = (alpha[i2] - am) + (-0.5 * (DT * kLog2Pi + sq) - ldq);
+            if (v > m) {
+              s = s * exp(m - v) + 1.0;
+              m = v;
+            } else {
+              s += exp(v - m);
+            }
+          }
+        }
+      } else {
+        for (int i = 0; i < N; ++i) {
+          for (int k = 0; k < d; ++k) r[k] = xj[k] - mprev[i * d + k];
+          const double v = (alpha[i] - am) + gauss_term(d, r, LQ, ldq);
+          if (v > m) {
+            s = s * exp(m - v) + 1.0;
+            m = v;
+          } else {
+            s += exp(v - m);
+          }
         }
       }
       W[j] = LW[(size_t)t * N + j] + (am + (m + log(s)));
@@ -555,9 +624,21 @@ static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int variant, Arena&
     AUXMC_LAUNCH(k_pit_particles, (int)std::min<long long>((np + 255) / 256, 148LL * 64), 256, 0, s,
                  tg, f, a, lw);
     const size_t smem = sizeof(double) * (3 * N + (size_t)N * d + 40 + 64);
-    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pit_forward_backward,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    AUXMC_LAUNCH(k_pit_forward_backward, C, threads, smem, s, tg, f, a, lw);
+    switch (d) {
+#define PCASE(DT)                                                                        \
+  case DT:                                                                               \
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pit_forward_backward<DT>,                      \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                        (int)smem));                                     \
+    AUXMC_LAUNCH((k_pit_forward_backward<DT>), C, threads, smem, s, tg, f, a, lw);       \
+    break;
+      PCASE(1) PCASE(2) PCASE(3) PCASE(4) PCASE(5) PCASE(6) PCASE(7) PCASE(8)
+#undef PCASE
+      default:
+        AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pit_forward_backward<0>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AUXMC_LAUNCH((k_pit_forward_backward<0>), C, threads, smem, s, tg, f, a, lw);
+    }
   }
   AUXMC_LAUNCH(k_pg_commit, C, 256, 0, s, C, T, d, traj, tkeys, ch->status, ch->x, ch->keys,
                ch->iter, ch->updates, ch->last_update);

@@ -152,8 +152,239 @@ __global__ void k_filter_seq(DevModel m, const double* __restrict__ obs, int B,
   }
 }
 
+// Register path for small dims: one thread per sequence, state and covariance
+// in registers (D <= 6, observation rows <= DY).  Same operation order as the
+// group kernel (lgssm.cpp:73-112).
+template <int D, int DY>
+__global__ void k_filter_reg(DevModel m, const double* __restrict__ obs, int B, double* pred_mean,
+                             double* pred_cov, double* filt_mean, double* filt_cov,
+                             double* log_marginal, int* status) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int T = m.T, dy = m.dy;
+  constexpr int DD = D * D;
+  double mm[D], p[DD];
+#pragma unroll
+  for (int i = 0; i < D; ++i) mm[i] = m.m0[i];
+#pragma unroll
+  for (int i = 0; i < DD; ++i) p[i] = 0.5 * (m.P0[(i / D) * D + i % D] + m.P0[(i % D) * D + i / D]);
+  double ll = 0.0;
+  int st = 0;
+  const double* y_all = obs + (size_t)b * (T + 1) * dy;
+  for (int t = 0; t <= T && !st; ++t) {
+    if (t > 0) {
+      const double* F = m.Ft(t - 1, b);
+      const double* bb = m.bt(t - 1, b);
+      const double* Q = m.Qt(t - 1, b);
+      double Fr[DD], v[D], tmp[DD];
+#pragma unroll
+      for (int i = 0; i < DD; ++i) Fr[i] = F[i];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) s += Fr[i * D + j] * mm[j];
+        v[i] = s + bb[i];
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) s += Fr[i * D + k] * p[k * D + j];
+          tmp[i * D + j] = s;
+        }
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        mm[i] = v[i];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) s += tmp[i * D + k] * Fr[j * D + k];
+          p[i * D + j] = s + 0.5 * (Q[i * D + j] + Q[j * D + i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = i + 1; j < D; ++j) {
+          const double s = 0.5 * (p[i * D + j] + p[j * D + i]);
+          p[i * D + j] = s;
+          p[j * D + i] = s;
+        }
+    }
+    double* pmo = pred_mean + ((size_t)b * (T + 1) + t) * D;
+    double* pco = pred_cov + ((size_t)b * (T + 1) + t) * DD;
+#pragma unroll
+    for (int i = 0; i < D; ++i) pmo[i] = mm[i];
+#pragma unroll
+    for (int i = 0; i < DD; ++i) pco[i] = p[i];
+    if (dy > 0 && m.observed(t)) {
+      const double* H = m.Ht(t, b);
+      const double* c = m.ct(t, b);
+      const double* R = m.Rt(t, b);
+      const double* y = y_all + (size_t)t * dy;
+      double innov[DY], v2[DY], hp[DY * D], S[DY * DY], L[DY * DY], X[DY * D];
+      for (int i = 0; i < dy; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) s += H[i * D + j] * mm[j];
+        innov[i] = (y[i] - s) - c[i];
+        v2[i] = s + c[i];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double a = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) a += H[i * D + k] * p[k * D + j];
+          hp[i * D + j] = a;
+        }
+      }
+      for (int i = 0; i < dy; ++i)
+        for (int j = 0; j < dy; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) s += hp[i * D + k] * H[j * D + k];
+          S[i * dy + j] = s + 0.5 * (R[i * dy + j] + R[j * dy + i]);
+        }
+      for (int i = 0; i < dy; ++i)
+        for (int j = i + 1; j < dy; ++j) {
+          const double s = 0.5 * (S[i * dy + j] + S[j * dy + i]);
+          S[i * dy + j] = s;
+          S[j * dy + i] = s;
+        }
+      // factor_psd(S) (gauss.cpp:26-35)
+      bool ok = false;
+      for (int pass = 0; pass < 3 && !ok; ++pass) {
+        double jit = 0.0;
+        if (pass > 0) {
+          double tr = 0.0;
+          for (int i = 0; i < dy; ++i) tr += S[i * dy + i];
+          double sc = tr / dy;
+          if (sc <= 0.0) {
+            sc = 0.0;
+            for (int i = 0; i < dy * dy; ++i) sc = fabs(S[i]) > sc ? fabs(S[i]) : sc;
+          }
+          jit = (pass == 1 ? 1e-10 : 1e-8) * sc;
+        }
+        ok = true;
+        for (int k = 0; k < dy && ok; ++k) {
+          double x = S[k * dy + k] + (pass ? jit * 1.0 : 0.0);
+          for (int j = 0; j < k; ++j) x -= L[k * dy + j] * L[k * dy + j];
+          if (x <= 0.0) {
+            ok = false;
+            break;
+          }
+          x = sqrt(x);
+          L[k * dy + k] = x;
+          for (int i = k + 1; i < dy; ++i) {
+            double s = S[i * dy + k];
+            for (int j = 0; j < k; ++j) s -= L[i * dy + j] * L[k * dy + j];
+            L[i * dy + k] = s / x;
+          }
+          for (int j = k + 1; j < dy; ++j) L[k * dy + j] = 0.0;
+        }
+      }
+      if (!ok) {
+        st = AUXMC_E_FACTOR;
+        break;
+      }
+      // X = S^{-1} H P (dy×D)
+      for (int col = 0; col < D; ++col) {
+        for (int i = 0; i < dy; ++i) {
+          double s = hp[i * D + col];
+          for (int j = 0; j < i; ++j) s -= L[i * dy + j] * X[j * D + col];
+          X[i * D + col] = s / L[i * dy + i];
+        }
+        for (int i = dy - 1; i >= 0; --i) {
+          double s = X[i * D + col];
+          for (int j = i + 1; j < dy; ++j) s -= L[j * dy + i] * X[j * D + col];
+          X[i * D + col] = s / L[i * dy + i];
+        }
+      }
+      double a[DD], tmp[DD], gr[D * DY];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double s = 0.0;
+        for (int i = 0; i < dy; ++i) s += X[i * D + j] * innov[i];
+        mm[j] += s;
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double s = 0.0;
+          for (int k = 0; k < dy; ++k) s += X[k * D + i] * H[k * D + j];
+          a[i * D + j] = (i == j ? 1.0 : 0.0) - s;
+        }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) s += a[i * D + k] * p[k * D + j];
+          tmp[i * D + j] = s;
+        }
+      for (int i = 0; i < D; ++i)
+        for (int j = 0; j < dy; ++j) {
+          double s = 0.0;
+          for (int k = 0; k < dy; ++k) s += X[k * D + i] * (0.5 * (R[k * dy + j] + R[j * dy + k]));
+          gr[i * DY + j] = s;
+        }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double s = 0.0, s2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; ++k) s += tmp[i * D + k] * a[j * D + k];
+          for (int k = 0; k < dy; ++k) s2 += gr[i * DY + k] * X[k * D + j];
+          p[i * D + j] = s + s2;
+        }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = i + 1; j < D; ++j) {
+          const double s = 0.5 * (p[i * D + j] + p[j * D + i]);
+          p[i * D + j] = s;
+          p[j * D + i] = s;
+        }
+      // log N(y; H m_pred + c, S) with the same factor
+      double sq = 0.0, ld = 0.0, z[DY];
+      for (int i = 0; i < dy; ++i) {
+        double s = y[i] - v2[i];
+        for (int j = 0; j < i; ++j) s -= L[i * dy + j] * z[j];
+        z[i] = s / L[i * dy + i];
+        sq += z[i] * z[i];
+      }
+      for (int i = 0; i < dy; ++i) ld += log(L[i * dy + i]);
+      ll += -0.5 * (dy * kLog2Pi + sq) - ld;
+    }
+    double* fmo = filt_mean + ((size_t)b * (T + 1) + t) * D;
+    double* fco = filt_cov + ((size_t)b * (T + 1) + t) * DD;
+#pragma unroll
+    for (int i = 0; i < D; ++i) fmo[i] = mm[i];
+#pragma unroll
+    for (int i = 0; i < DD; ++i) fco[i] = p[i];
+  }
+  log_marginal[b] = ll;
+  status[b] = st;
+}
+
 int launch_filter_seq(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
                       int* status, cudaStream_t stream) {
+  if (dm.dy <= 8 && dm.dx <= 6) {
+    const int grid = (B + 63) / 64;
+#define FCASE(D)                                                                              \
+  case D:                                                                                     \
+    AUXMC_LAUNCH((k_filter_reg<D, 8>), grid, 64, 0, stream, dm, obs, B, out->pred_mean,       \
+                 out->pred_cov, out->filt_mean, out->filt_cov, out->log_marginal, status);    \
+    return AUXMC_OK;
+    switch (dm.dx) { FCASE(1) FCASE(2) FCASE(3) FCASE(4) FCASE(5) FCASE(6) }
+#undef FCASE
+  }
   const int per = filter_smem_doubles(dm.dx, dm.dy);
   const bool block = (dm.dx > 16 || dm.dy > 16);
   if (block) {

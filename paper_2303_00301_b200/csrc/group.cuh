@@ -1,0 +1,356 @@
+// group.cuh — group-cooperative dense FP64 routines on shared-memory matrices
+// (included by dense.cuh).  A group is one warp or one CTA (size a multiple of
+// 16); lanes are laid out as a 16-wide grid (tx = lane & 15, ty = lane >> 4) so
+// 2-D loops carry no integer division and a warp touches 16 consecutive
+// columns (conflict-free) of at most two rows (broadcast).  Every output element
+// is owned by one lane and accumulated in ascending index order, so results are
+// deterministic and independent of the group size.
+#pragma once
+
+namespace auxmc_gpu {
+
+struct Grp {
+  int lane, size;
+  bool block;
+  __device__ __forceinline__ void sync() const {
+    if (block) __syncthreads();
+    else __syncwarp();
+  }
+  __device__ __forceinline__ int tx() const { return lane & 15; }
+  __device__ __forceinline__ int ty() const { return lane >> 4; }
+  __device__ __forceinline__ int ny() const { return size >> 4; }
+};
+
+__device__ __forceinline__ Grp warp_group() { return Grp{int(threadIdx.x & 31), 32, false}; }
+__device__ __forceinline__ Grp block_group() { return Grp{int(threadIdx.x), int(blockDim.x), true}; }
+
+// ---------------------------------------------------------------- copies
+__device__ __forceinline__ void g_copy(const Grp& g, int n, const double* __restrict__ src,
+                                       double* __restrict__ dst) {
+  for (int i = g.lane; i < n; i += g.size) dst[i] = src[i];
+}
+__device__ __forceinline__ void g_zero(const Grp& g, int n, double* dst) {
+  for (int i = g.lane; i < n; i += g.size) dst[i] = 0.0;
+}
+__device__ __forceinline__ void g_eye(const Grp& g, int n, double* dst) {
+  for (int i = g.ty(); i < n; i += g.ny())
+    for (int j = g.tx(); j < n; j += 16) dst[i * n + j] = (i == j) ? 1.0 : 0.0;
+}
+
+// ---------------------------------------------------------------- FP64 tensor-core products
+// For CTA groups on d >= 16 matrices the element algebra is a real dense
+// contraction: 8×8 output tiles are accumulated with mma.sync m8n8k4 f64
+// (DMMA, one instruction per 256 FMAs instead of 32) — fragments gathered from
+// shared memory with bounds guards, so no padding is needed.
+// TA/TB: operand transposed in memory (A^T B, A B^T forms).
+template <bool TA, bool TB>
+__device__ __forceinline__ void g_mm_dmma(const Grp& g, int m, int k, int n, const double* A,
+                                          const double* B, double* C, const double* D) {
+  const int warp = g.lane >> 5, lane = g.lane & 31, nw = g.size >> 5;
+  const int gi = lane >> 2, ti = lane & 3;
+  const int mt = (m + 7) >> 3, nt = (n + 7) >> 3, kt = (k + 3) >> 2;
+  for (int tile = warp; tile < mt * nt; tile += nw) {
+    const int I = (tile / nt) * 8, J = (tile % nt) * 8;
+    double c0 = 0.0, c1 = 0.0;
+    const int ar = I + gi, bc = J + gi;
+    for (int K = 0; K < kt; ++K) {
+      const int kk = K * 4 + ti;
+      double a = 0.0, b = 0.0;
+      if (ar < m && kk < k) a = TA ? A[kk * m + ar] : A[ar * k + kk];
+      if (bc < n && kk < k) b = TB ? B[bc * k + kk] : B[kk * n + bc];
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c0), "+d"(c1)
+                   : "d"(a), "d"(b));
+    }
+    const int r = I + gi, cc = J + 2 * ti;
+    if (r < m) {
+      if (cc < n) C[r * n + cc] = D ? c0 + D[r * n + cc] : c0;
+      if (cc + 1 < n) C[r * n + cc + 1] = D ? c1 + D[r * n + cc + 1] : c1;
+    }
+  }
+}
+
+__device__ __forceinline__ bool use_dmma(const Grp& g, int m, int k, int n) {
+  return g.block && m >= 16 && n >= 16 && k >= 8;
+}
+
+// ---------------------------------------------------------------- products
+// Each lane owns outputs (i, j), (i + ny, j): two independent FMA chains.
+// C (m×n) = A (m×k) B (k×n) [+ D]
+__device__ __forceinline__ void g_mm(const Grp& g, int m, int k, int n, const double* A,
+                                     const double* B, double* C, const double* D = nullptr) {
+  if (use_dmma(g, m, k, n)) {
+    g_mm_dmma<false, false>(g, m, k, n, A, B, C, D);
+    return;
+  }
+  const int ny = g.ny();
+  for (int i = g.ty(); i < m; i += 2 * ny) {
+    const int i2 = i + ny;
+    const bool two = i2 < m;
+    for (int j = g.tx(); j < n; j += 16) {
+      double s = 0.0, s2 = 0.0;
+      for (int l = 0; l < k; ++l) {
+        const double b = B[l * n + j];
+        s += A[i * k + l] * b;
+        if (two) s2 += A[i2 * k + l] * b;
+      }
+      C[i * n + j] = D ? s + D[i * n + j] : s;
+      if (two) C[i2 * n + j] = D ? s2 + D[i2 * n + j] : s2;
+    }
+  }
+}
+// C (m×n) = A (m×k) B^T, B (n×k) [+ D]
+__device__ __forceinline__ void g_mm_nt(const Grp& g, int m, int k, int n, const double* A,
+                                        const double* B, double* C, const double* D = nullptr) {
+  if (use_dmma(g, m, k, n)) {
+    g_mm_dmma<false, true>(g, m, k, n, A, B, C, D);
+    return;
+  }
+  const int ny = g.ny();
+  for (int i = g.ty(); i < m; i += 2 * ny) {
+    const int i2 = i + ny;
+    const bool two = i2 < m;
+    for (int j = g.tx(); j < n; j += 16) {
+      double s = 0.0, s2 = 0.0;
+      for (int l = 0; l < k; ++l) {
+        const double b = B[j * k + l];
+        s += A[i * k + l] * b;
+        if (two) s2 += A[i2 * k + l] * b;
+      }
+      C[i * n + j] = D ? s + D[i * n + j] : s;
+      if (two) C[i2 * n + j] = D ? s2 + D[i2 * n + j] : s2;
+    }
+  }
+}
+// C (m×n) = A^T B, A (k×m), B (k×n) [+ D]
+__device__ __forceinline__ void g_mm_tn(const Grp& g, int m, int k, int n, const double* A,
+                                        const double* B, double* C, const double* D = nullptr) {
+  if (use_dmma(g, m, k, n)) {
+    g_mm_dmma<true, false>(g, m, k, n, A, B, C, D);
+    return;
+  }
+  const int ny = g.ny();
+  for (int i = g.ty(); i < m; i += 2 * ny) {
+    const int i2 = i + ny;
+    const bool two = i2 < m;
+    for (int j = g.tx(); j < n; j += 16) {
+      double s = 0.0, s2 = 0.0;
+      for (int l = 0; l < k; ++l) {
+        const double b = B[l * n + j];
+        s += A[l * m + i] * b;
+        if (two) s2 += A[l * m + i2] * b;
+      }
+      C[i * n + j] = D ? s + D[i * n + j] : s;
+      if (two) C[i2 * n + j] = D ? s2 + D[i2 * n + j] : s2;
+    }
+  }
+}
+// y (m) = A (m×n) x [+ add]
+__device__ __forceinline__ void g_mv(const Grp& g, int m, int n, const double* A, const double* x,
+                                     double* y, const double* add = nullptr) {
+  for (int i = g.lane; i < m; i += g.size) {
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s += A[i * n + j] * x[j];
+    y[i] = add ? s + add[i] : s;
+  }
+}
+// y (n) = A^T x, A (m×n)
+__device__ __forceinline__ void g_mtv(const Grp& g, int m, int n, const double* A,
+                                      const double* x, double* y) {
+  for (int j = g.lane; j < n; j += g.size) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += A[i * n + j] * x[i];
+    y[j] = s;
+  }
+}
+// in-place symm(A) = (A + A^T)/2 ; caller syncs before (A complete) and after
+__device__ __forceinline__ void g_symm(const Grp& g, int n, double* A) {
+  for (int i = g.ty(); i < n; i += g.ny())
+    for (int j = i + 1 + g.tx(); j < n; j += 16) {
+      const double v = 0.5 * (A[i * n + j] + A[j * n + i]);
+      A[i * n + j] = v;
+      A[j * n + i] = v;
+    }
+}
+// A := symm(A + B)  (both complete)
+__device__ __forceinline__ void g_add_symm(const Grp& g, int n, double* A, const double* B) {
+  for (int i = g.ty(); i < n; i += g.ny())
+    for (int j = i + g.tx(); j < n; j += 16) {
+      const double a = A[i * n + j] + B[i * n + j];
+      const double b = A[j * n + i] + B[j * n + i];
+      const double v = 0.5 * (a + b);
+      A[i * n + j] = v;
+      A[j * n + i] = v;
+    }
+}
+
+// group-wide boolean "all entries exactly zero"; flag in shared memory
+__device__ __forceinline__ bool g_all_zero(const Grp& g, int n, const double* A, int* flag) {
+  if (g.lane == 0) *flag = 1;
+  g.sync();
+  for (int i = g.lane; i < n; i += g.size)
+    if (A[i] != 0.0) *flag = 0;
+  g.sync();
+  const bool r = *flag != 0;
+  g.sync();
+  return r;
+}
+
+// ---------------------------------------------------------------- Cholesky
+// LLT of the lower triangle of A (n×n) into L; Eigen semantics: fail iff a
+// pivot x <= 0 (NaN passes).  Right-looking: the trailing update of column k is
+// spread over the group, so the serial depth is O(n) syncs.
+__device__ __forceinline__ bool g_llt(const Grp& g, int n, const double* A, double* L,
+                                      int* flag) {
+  for (int i = g.ty(); i < n; i += g.ny())
+    for (int j = g.tx(); j < n; j += 16) L[i * n + j] = j <= i ? A[i * n + j] : 0.0;
+  (void)flag;
+  g.sync();
+  for (int k = 0; k < n; ++k) {
+    // every lane reads the same (final) pivot, so the failure test is uniform
+    const double x = L[k * n + k];
+    if (x <= 0.0) {
+      g.sync();
+      return false;
+    }
+    const double piv = sqrt(x);
+    for (int i = k + 1 + g.lane; i < n; i += g.size) L[i * n + k] = L[i * n + k] / piv;
+    g.sync();
+    if (g.lane == 0) L[k * n + k] = piv;  // not read by the trailing update
+    for (int i = k + 1 + g.ty(); i < n; i += g.ny()) {
+      const double lik = L[i * n + k];
+      for (int j = k + 1 + g.tx(); j <= i; j += 16) L[i * n + j] -= lik * L[j * n + k];
+    }
+    g.sync();
+  }
+  return true;
+}
+
+// factor_psd (gauss.cpp:26-35): LLT, then + eps*s*I for eps in {1e-10, 1e-8}.
+// scratch: n*n doubles.  Returns 0 ok, 2 (AUXMC_E_FACTOR) on failure.
+__device__ __forceinline__ int g_factor_psd(const Grp& g, int n, const double* A, double* L,
+                                            double* scratch, int* flag, double* red) {
+  if (g_llt(g, n, A, L, flag)) return 0;
+  if (g.lane == 0) {  // jitter scale (gauss.cpp:20-24)
+    double tr = 0.0;
+    for (int i = 0; i < n; ++i) tr += A[i * n + i];
+    double s = tr / static_cast<double>(n);
+    if (s <= 0.0) {
+      double m = 0.0;
+      for (int i = 0; i < n * n; ++i) m = fabs(A[i]) > m ? fabs(A[i]) : m;
+      s = m;
+    }
+    *red = s;
+  }
+  g.sync();
+  const double s = *red;
+  const double eps[2] = {1e-10, 1e-8};
+  for (int e = 0; e < 2; ++e) {
+    for (int i = g.ty(); i < n; i += g.ny())
+      for (int j = g.tx(); j < n; j += 16)
+        scratch[i * n + j] = A[i * n + j] + (i == j ? (eps[e] * s) * 1.0 : 0.0);
+    g.sync();
+    if (g_llt(g, n, scratch, L, flag)) return 0;
+  }
+  return 2;
+}
+
+// chol_psd (gauss.cpp:45-49): exactly-zero matrix factors to zero.
+__device__ __forceinline__ int g_chol_psd(const Grp& g, int n, const double* A, double* L,
+                                          double* scratch, int* flag, double* red) {
+  if (g_all_zero(g, n * n, A, flag)) {
+    for (int i = g.lane; i < n * n; i += g.size) L[i] = 0.0;
+    g.sync();
+    return 0;
+  }
+  return g_factor_psd(g, n, A, L, scratch, flag, red);
+}
+
+// In-place solve L L^T X = B for X (B n×r), L lower.  One group sync per row.
+// Row i of the running right-hand side holds the solved x_i once step i starts:
+// the lane that applies the last update to row i+1 also divides it by L_{i+1,i+1},
+// so each x is divided exactly once (x_i = (b_i - Σ_j L_ij x_j) / L_ii in
+// ascending j, the reference's order) and there is one group sync per row.
+__device__ __forceinline__ void g_llt_solve(const Grp& g, int n, const double* L, int r,
+                                            double* B) {
+  const int ny = g.ny();
+  for (int c = g.lane; c < r; c += g.size) B[c] = B[c] / L[0];
+  g.sync();
+  for (int i = 0; i < n; ++i) {  // forward: L Y = B
+    for (int j = i + 1 + g.ty(); j < n; j += ny) {
+      const double lji = L[j * n + i];
+      const bool last = j == i + 1;
+      const double ljj = L[j * n + j];
+      for (int c = g.tx(); c < r; c += 16) {
+        const double v = B[j * r + c] - lji * B[i * r + c];
+        B[j * r + c] = last ? v / ljj : v;
+      }
+    }
+    g.sync();
+  }
+  for (int c = g.lane; c < r; c += g.size)
+    B[(n - 1) * r + c] = B[(n - 1) * r + c] / L[(n - 1) * n + (n - 1)];
+  g.sync();
+  for (int i = n - 1; i >= 0; --i) {  // backward: L^T X = Y
+    for (int j = g.ty(); j < i; j += ny) {
+      const double lij = L[i * n + j];
+      const bool last = j == i - 1;
+      const double ljj = L[j * n + j];
+      for (int c = g.tx(); c < r; c += 16) {
+        const double v = B[j * r + c] - lij * B[i * r + c];
+        B[j * r + c] = last ? v / ljj : v;
+      }
+    }
+    g.sync();
+  }
+}
+
+// In-place forward substitution L z = r (vector), same scheme.
+__device__ __forceinline__ void g_lower_solve_vec(const Grp& g, int n, const double* L, double* r) {
+  if (g.lane == 0) r[0] = r[0] / L[0];
+  g.sync();
+  for (int i = 0; i < n; ++i) {
+    for (int j = i + 1 + g.lane; j < n; j += g.size) {
+      const double v = r[j] - L[j * n + i] * r[i];
+      r[j] = j == i + 1 ? v / L[j * n + j] : v;
+    }
+    g.sync();
+  }
+}
+
+// group sum of v[0..n) into *out (lane 0 sequential for determinism)
+__device__ __forceinline__ double g_sum_seq(const Grp& g, int n, const double* v, double* out) {
+  if (g.lane == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += v[i];
+    *out = s;
+  }
+  g.sync();
+  const double r = *out;
+  g.sync();
+  return r;
+}
+
+constexpr double kLog2Pi = 1.8378770664093454835606594728112;
+
+// log N(x; mean, cov) (gauss.cpp:51-57) given the LLT factor L of symm(cov).
+// work: n doubles.  Returns value on all lanes.
+__device__ __forceinline__ double g_log_pdf_factored(const Grp& g, int n, const double* x,
+                                                     const double* mean, const double* L,
+                                                     double* work, double* red) {
+  for (int i = g.lane; i < n; i += g.size) work[i] = x[i] - mean[i];
+  g.sync();
+  g_lower_solve_vec(g, n, L, work);
+  if (g.lane == 0) {
+    double sq = 0.0, ld = 0.0;
+    for (int i = 0; i < n; ++i) sq += work[i] * work[i];
+    for (int i = 0; i < n; ++i) ld += log(L[i * n + i]);
+    *red = -0.5 * (n * kLog2Pi + sq) - ld;
+  }
+  g.sync();
+  const double v = *red;
+  g.sync();
+  return v;
+}
+
+}  // namespace auxmc_gpu

@@ -54,8 +54,12 @@ def run(args, rank, world, local):
     else:
         ch = auxk.init_chains(tg, x0, delta, 1, C, first=rank * C)
 
+        # C1 is one short chain: the scan filter (KernelOptions::parallel_filter)
+        # parallelizes the horizon; C3 has 256 chains and uses the sequential filter.
+        pf = cfg == "c1"
+
         def step():
-            ch.kernel_step(backend)
+            ch.kernel_step(backend, parallel_filter=pf)
 
     for _ in range(max(args.warmup, 1)):
         step()

@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest14.log 2>&1; tail -3 gpurun_out/pytest14.log
+for c in "c3 --T 512" "c1" "c4 --T 2048 --chains 1"; do
+  timeout 900 python bench.py --config $c --steps 3 --warmup 2 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', d['value'], d['ms_per_step'], 'ms')"
+done
+C3="python bench.py --config c3 --T 256 --steps 1 --warmup 1"
+$C3 > gpurun_out/c3_plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/c3_launches5.csv $C3 > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/c3_launches5.csv 2>&1 | head -12
