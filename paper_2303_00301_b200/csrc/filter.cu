@@ -12,9 +12,12 @@ namespace auxmc_gpu {
 
 __host__ __device__ inline int filter_smem_doubles(int dx, int dy) {
   const int W = dx > dy ? dx : dy;
-  return 4 * dx + 3 * W + 5 * dx * dx + 2 * dy * dx + 3 * dy * dy + 8;
+  return 4 * dx + 3 * W + 4 * dx * dx + 3 * dy * dx + 3 * dy * dy + 8;
 }
 
+// Per step the model blocks F, Q, H, R are staged into shared memory with
+// coalesced loads (the symmetrizations then run on shared memory), so every
+// product reads shared operands only.
 template <bool BLOCK>
 __global__ void k_filter_seq(DevModel m, const double* __restrict__ obs, int B,
                              double* pred_mean, double* pred_cov, double* filt_mean,
@@ -33,16 +36,20 @@ __global__ void k_filter_seq(DevModel m, const double* __restrict__ obs, int B,
   double* innov = v + W;
   double* v2 = innov + W;
   double* p = v2 + W;
-  double* tmp = p + dx * dx;
-  double* a = tmp + dx * dx;
-  double* work = a + dx * dx;
-  double* Qs = work + dx * dx;
-  double* hp = Qs + dx * dx;
+  double* tmp = p + dx * dx;   // tmp, a, work contiguous: also the factor scratch
+  double* a = tmp + dx * dx;   // F during the prediction
+  double* work = a + dx * dx;  // Qs during the prediction
+  double* Hs = work + dx * dx;
+  double* hp = Hs + dy * dx;
   double* X = hp + dy * dx;
   double* S = X + dy * dx;
-  double* L = S + dy * dy;
-  double* scr = L + dy * dy;
+  double* L = S + dy * dy;     // raw R while staging
+  double* scr = L + dy * dy;   // Rs
   double* red = scr + dy * dy;
+  // factor scratch: dy*dy doubles (warp groups: jitter matrix) or the inverted
+  // diagonal blocks (CTA groups, dy >= 16); tmp..work when it fits, else Rs
+  const bool fits = dy * dy <= 3 * dx * dx && dinv_doubles(dy) <= dx * dx;
+  double* fscr = fits ? tmp : scr;
   int* flag = reinterpret_cast<int*>(red + 2);
   const int ddx = dx * dx;
   for (int b = blockIdx.x * gpb + gid; b < B; b += gridDim.x * gpb) {
@@ -54,29 +61,26 @@ __global__ void k_filter_seq(DevModel m, const double* __restrict__ obs, int B,
     double ll = 0.0;
     int st = 0;
     for (int i = g.lane; i < dx; i += g.size) mm[i] = m.m0[i];
-    for (int i = g.lane; i < ddx; i += g.size) {
-      const int r = i / dx, c = i % dx;
-      p[i] = 0.5 * (m.P0[r * dx + c] + m.P0[c * dx + r]);
-    }
+    g_copy(g, ddx, m.P0, p);
+    g.sync();
+    g_symm(g, dx, p);
     g.sync();
     for (int t = 0; t <= T; ++t) {
       if (t > 0) {
-        const double* F = m.Ft(t - 1, b);
+        g_copy(g, ddx, m.Ft(t - 1, b), a);
+        g_copy(g, ddx, m.Qt(t - 1, b), work);
+        g.sync();
         const double* bb = m.bt(t - 1, b);
-        const double* Q = m.Qt(t - 1, b);
         for (int i = g.lane; i < dx; i += g.size) {
           double s = 0.0;
-          for (int j = 0; j < dx; ++j) s += F[i * dx + j] * mm[j];
+          for (int j = 0; j < dx; ++j) s += a[i * dx + j] * mm[j];
           v[i] = s + bb[i];
         }
-        for (int i = g.lane; i < ddx; i += g.size) {
-          const int r = i / dx, c = i % dx;
-          Qs[i] = 0.5 * (Q[r * dx + c] + Q[c * dx + r]);
-        }
-        g_mm(g, dx, dx, dx, F, p, tmp);
+        g_symm(g, dx, work);
+        g_mm(g, dx, dx, dx, a, p, tmp);
         g.sync();
         for (int i = g.lane; i < dx; i += g.size) mm[i] = v[i];
-        g_mm_nt(g, dx, dx, dx, tmp, F, p, Qs);
+        g_mm_nt(g, dx, dx, dx, tmp, a, p, work);
         g.sync();
         g_symm(g, dx, p);
         g.sync();
@@ -87,47 +91,74 @@ __global__ void k_filter_seq(DevModel m, const double* __restrict__ obs, int B,
       }
       for (int i = g.lane; i < ddx; i += g.size) pc_out[(size_t)t * ddx + i] = p[i];
       if (m.observed(t)) {
-        const double* H = m.Ht(t, b);
         const double* c = m.ct(t, b);
-        const double* R = m.Rt(t, b);
         const double* y = y_all + (size_t)t * dy;
+        g_copy(g, dy * dx, m.Ht(t, b), Hs);
+        g_copy(g, dy * dy, m.Rt(t, b), L);
+        g.sync();
         for (int i = g.lane; i < dy; i += g.size) {
           double s = 0.0;
-          for (int j = 0; j < dx; ++j) s += H[i * dx + j] * mm[j];
+          for (int j = 0; j < dx; ++j) s += Hs[i * dx + j] * mm[j];
           innov[i] = (y[i] - s) - c[i];
           v2[i] = s + c[i];  // H m_pred + c
         }
-        g_mm(g, dy, dx, dx, H, p, hp);  // H P
+        g_mm(g, dy, dx, dx, Hs, p, hp);  // H P
+        for (int i = g.ty(); i < dy; i += g.ny())  // Rs = symm(R)
+          for (int j = g.tx(); j < dy; j += 16)
+            scr[i * dy + j] = 0.5 * (L[i * dy + j] + L[j * dy + i]);
         g.sync();
-        for (int i = g.lane; i < dy * dy; i += g.size) {
-          const int r = i / dy, cc = i % dy;
-          scr[i] = 0.5 * (R[r * dy + cc] + R[cc * dy + r]);  // Rs
-        }
-        g.sync();
-        g_mm_nt(g, dy, dx, dy, hp, H, S, scr);
+        g_mm_nt(g, dy, dx, dy, hp, Hs, S, scr);
         g.sync();
         g_symm(g, dy, S);
         g.sync();
-        st = g_factor_psd(g, dy, S, L, scr, flag, red);
+        st = g_factor_psd(g, dy, S, L, fscr, flag, red);
         if (st) break;
+        const bool blk = use_blocked(g, dy) && g.size > 32;
+        const double* dinv = blk ? fscr : nullptr;  // inverted diagonal blocks of L
         g_copy(g, dy * dx, hp, X);
         g.sync();
-        g_llt_solve(g, dy, L, dx, X);  // X = S^{-1} H P ; gain = X^T
-        // m += X^T innov
-        for (int j = g.lane; j < dx; j += g.size) {
-          double s = 0.0;
-          for (int i = 0; i < dy; ++i) s += X[i * dx + j] * innov[i];
-          mm[j] += s;
+        g_llt_solve(g, dy, L, dx, X, dinv);  // X = S^{-1} H P ; gain = X^T
+        if (blk) {
+          // warp 0: log-likelihood term (serial triangular solve); the other
+          // warps meanwhile update the mean and form a = I - X^T H.
+          if (g.lane < 32) {
+            ll += w_log_pdf_factored(g.lane, dy, y, v2, L, dinv, v);
+          } else {
+            const Grp gw = warps_group(1, g.size / 32 - 1, 1);
+            for (int j = gw.lane; j < dx; j += gw.size) {
+              double s = 0.0;
+              for (int i = 0; i < dy; ++i) s += X[i * dx + j] * innov[i];
+              mm[j] += s;
+            }
+            g_mm_tn(gw, dx, dy, dx, X, Hs, a);
+            gw.sync();
+            for (int i = gw.ty(); i < dx; i += gw.ny())
+              for (int j = gw.tx(); j < dx; j += 16)
+                a[i * dx + j] = (i == j ? 1.0 : 0.0) - a[i * dx + j];
+          }
+          g.sync();
+        } else {
+          // m += X^T innov
+          for (int j = g.lane; j < dx; j += g.size) {
+            double s = 0.0;
+            for (int i = 0; i < dy; ++i) s += X[i * dx + j] * innov[i];
+            mm[j] += s;
+          }
+          // a = I - X^T H
+          g_mm_tn(g, dx, dy, dx, X, Hs, a);
+          g.sync();
+          for (int i = g.ty(); i < dx; i += g.ny())
+            for (int j = g.tx(); j < dx; j += 16) a[i * dx + j] = (i == j ? 1.0 : 0.0) - a[i * dx + j];
+          g.sync();
         }
-        // a = I - X^T H
-        g_mm_tn(g, dx, dy, dx, X, H, a);
-        g.sync();
-        for (int i = g.lane; i < ddx; i += g.size) a[i] = (i / dx == i % dx ? 1.0 : 0.0) - a[i];
-        for (int i = g.lane; i < dy * dy; i += g.size) {
-          const int r = i / dy, cc = i % dy;
-          scr[i] = 0.5 * (R[r * dy + cc] + R[cc * dy + r]);
+        if (fscr == scr) {  // factor scratch overlapped Rs: restage it
+          g_copy(g, dy * dy, m.Rt(t, b), S);
+          g.sync();
+          for (int i = g.ty(); i < dy; i += g.ny())
+            for (int j = g.tx(); j < dy; j += 16)
+              scr[i * dy + j] = 0.5 * (S[i * dy + j] + S[j * dy + i]);
+          g.sync();
         }
-        g.sync();
         g_mm(g, dx, dx, dx, a, p, tmp);       // a p
         g_mm_tn(g, dx, dy, dy, X, scr, hp);   // X^T R  (dx×dy), reuses hp
         g.sync();
@@ -138,7 +169,7 @@ __global__ void k_filter_seq(DevModel m, const double* __restrict__ obs, int B,
         g.sync();
         g_symm(g, dx, p);
         g.sync();
-        ll += g_log_pdf_factored(g, dy, y, v2, L, innov, red);
+        if (!blk) ll += g_log_pdf_factored(g, dy, y, v2, L, innov, red);
       }
       for (int i = g.lane; i < dx; i += g.size) fm_out[(size_t)t * dx + i] = mm[i];
       for (int i = g.lane; i < ddx; i += g.size) fc_out[(size_t)t * ddx + i] = p[i];

@@ -12,17 +12,25 @@ namespace auxmc_gpu {
 struct Grp {
   int lane, size;
   bool block;
+  int bar;  // CTA groups: 0 = whole CTA (__syncthreads), > 0 = named barrier of `size` threads
   __device__ __forceinline__ void sync() const {
-    if (block) __syncthreads();
-    else __syncwarp();
+    if (!block) __syncwarp();
+    else if (bar == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(size) : "memory");
   }
   __device__ __forceinline__ int tx() const { return lane & 15; }
   __device__ __forceinline__ int ty() const { return lane >> 4; }
   __device__ __forceinline__ int ny() const { return size >> 4; }
 };
 
-__device__ __forceinline__ Grp warp_group() { return Grp{int(threadIdx.x & 31), 32, false}; }
-__device__ __forceinline__ Grp block_group() { return Grp{int(threadIdx.x), int(blockDim.x), true}; }
+__device__ __forceinline__ Grp warp_group() { return Grp{int(threadIdx.x & 31), 32, false, 0}; }
+__device__ __forceinline__ Grp block_group() {
+  return Grp{int(threadIdx.x), int(blockDim.x), true, 0};
+}
+// warps [first, first + count) of the CTA as a group synchronized by named barrier `bar`
+__device__ __forceinline__ Grp warps_group(int first, int count, int bar) {
+  return Grp{int(threadIdx.x) - 32 * first, 32 * count, true, bar};
+}
 
 // ---------------------------------------------------------------- copies
 __device__ __forceinline__ void g_copy(const Grp& g, int n, const double* __restrict__ src,
@@ -196,6 +204,207 @@ __device__ __forceinline__ bool g_all_zero(const Grp& g, int n, const double* A,
   return r;
 }
 
+// ---------------------------------------------------------------- blocked (CTA, n >= 16)
+// Blocked factor/solves with 8-wide panels.  The diagonal 8×8 blocks are
+// factored and inverted by one warp; every other step (panel solve, trailing
+// SYRK, triangular solves) is an 8×8-tile DMMA product, so the serial depth is
+// O(n/8) group syncs and the O(n^3) work runs on the FP64 tensor cores.  The
+// inverted diagonal blocks (dinv: ceil(n/8) row-major 8×8 blocks, 64*ceil(n/8)
+// doubles) are kept for the triangular solves that follow a factorization.
+constexpr int kNB = 8;
+
+__host__ __device__ constexpr int dinv_doubles(int n) { return 64 * ((n + 7) / 8); }
+
+// C (m×n, ldc) = op(A) op(B)  or  C -= op(A) op(B)  (sub); A(i,l) = TA ? A[l*lda+i] :
+// A[i*lda+l], B(l,j) = TB ? B[j*ldb+l] : B[l*ldb+j]; lower: only j <= i is written
+// (and tiles above the diagonal skipped).  For sub the accumulator starts at C
+// and the A fragment is negated (one fused chain C - Σ a b).  A tile loads its
+// whole k-range before it stores, so C may alias the rows of A when n <= 8, or
+// the columns of B when m <= 8.
+template <bool TA, bool TB>
+__device__ __forceinline__ void g_dmma(const Grp& g, int m, int k, int n, const double* A, int lda,
+                                       const double* B, int ldb, double* C, int ldc, bool sub,
+                                       bool lower) {
+  const int warp = g.lane >> 5, lane = g.lane & 31, nw = g.size >> 5;
+  const int gi = lane >> 2, ti = lane & 3;
+  const int mt = (m + 7) >> 3, nt = (n + 7) >> 3, kt = (k + 3) >> 2;
+  for (int tile = warp; tile < mt * nt; tile += nw) {
+    const int It = tile / nt, Jt = tile - It * nt;
+    if (lower && Jt > It) continue;
+    const int I = It * 8, J = Jt * 8;
+    const int r = I + gi, cc = J + 2 * ti;
+    double c0 = 0.0, c1 = 0.0;
+    if (sub) {
+      if (r < m && cc < n) c0 = C[r * ldc + cc];
+      if (r < m && cc + 1 < n) c1 = C[r * ldc + cc + 1];
+    }
+    const int ar = I + gi, bc = J + gi;
+    for (int K = 0; K < kt; ++K) {
+      const int kk = K * 4 + ti;
+      double a = 0.0, b = 0.0;
+      if (ar < m && kk < k) a = TA ? A[kk * lda + ar] : A[ar * lda + kk];
+      if (bc < n && kk < k) b = TB ? B[bc * ldb + kk] : B[kk * ldb + bc];
+      if (sub) a = -a;
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c0), "+d"(c1)
+                   : "d"(a), "d"(b));
+    }
+    if (r < m) {
+      if (cc < n && (!lower || cc <= r)) C[r * ldc + cc] = c0;
+      if (cc + 1 < n && (!lower || cc + 1 <= r)) C[r * ldc + cc + 1] = c1;
+    }
+  }
+}
+
+// One warp: factor the nb×nb diagonal block D (row stride n, lower triangle holds
+// the updated A) in place and write its inverse to Di (8×8, zero padded).
+// Returns false (uniformly) on a pivot <= 0.
+__device__ __forceinline__ bool w_factor_diag(int lane, int n, int nb, double* D, double* Di) {
+  for (int j = 0; j < nb; ++j) {
+    const double x = D[j * n + j];
+    if (x <= 0.0) return false;
+    const double piv = sqrt(x);
+    if (lane > j && lane < nb) D[lane * n + j] = D[lane * n + j] / piv;
+    __syncwarp();
+    if (lane == 0) D[j * n + j] = piv;
+    for (int e = lane; e < kNB * kNB; e += 32) {
+      const int i = e >> 3, jj = e & 7;
+      if (i < nb && jj > j && jj <= i) D[i * n + jj] -= D[i * n + j] * D[jj * n + j];
+    }
+    __syncwarp();
+  }
+  if (lane < kNB) {  // column `lane` of D^{-1} by forward substitution
+    const int j = lane;
+    double x[kNB];
+#pragma unroll
+    for (int i = 0; i < kNB; ++i) {
+      double v = 0.0;
+      if (j < nb && i < nb && i >= j) {
+        double s = i == j ? 1.0 : 0.0;
+#pragma unroll
+        for (int l = 0; l < i; ++l)
+          if (l >= j) s -= D[i * n + l] * x[l];
+        v = s / D[i * n + i];
+      }
+      x[i] = v;
+      Di[i * kNB + j] = v;
+    }
+  }
+  __syncwarp();
+  return true;
+}
+
+// Right-looking blocked LLT of L (lower triangle already holds A, upper zero).
+__device__ __forceinline__ bool g_llt_blocked(const Grp& g, int n, double* L, int* flag,
+                                              double* dinv) {
+  if (g.lane == 0) *flag = 1;
+  for (int kb = 0; kb < n; kb += kNB) {
+    const int nb = n - kb < kNB ? n - kb : kNB;
+    double* Di = dinv + (kb / kNB) * kNB * kNB;
+    if (g.lane < 32) {
+      const bool ok = w_factor_diag(g.lane, n, nb, L + kb * n + kb, Di);
+      if (!ok && g.lane == 0) *flag = 0;
+    }
+    g.sync();
+    if (*flag == 0) {
+      g.sync();
+      return false;
+    }
+    const int rest = n - kb - nb;
+    if (rest <= 0) break;
+    double* P = L + (kb + nb) * n + kb;
+    g_dmma<false, true>(g, rest, nb, nb, P, n, Di, kNB, P, n, false, false);  // P D^{-T}
+    g.sync();
+    g_dmma<false, true>(g, rest, nb, rest, P, n, P, n, P + nb, n, true, true);  // L22 -= P P^T
+    g.sync();
+  }
+  return true;
+}
+
+// In-place L Y = B (B n×r, row stride ldb) with the inverted diagonal blocks.
+__device__ __forceinline__ void g_trsm_lower_blocked(const Grp& g, int n, const double* L,
+                                                     const double* dinv, int r, double* B,
+                                                     int ldb) {
+  for (int kb = 0; kb < n; kb += kNB) {
+    const int nb = n - kb < kNB ? n - kb : kNB;
+    double* Bk = B + kb * ldb;
+    g_dmma<false, false>(g, nb, nb, r, dinv + (kb / kNB) * kNB * kNB, kNB, Bk, ldb, Bk, ldb, false,
+                         false);
+    g.sync();
+    const int rest = n - kb - nb;
+    if (rest <= 0) break;
+    g_dmma<false, false>(g, rest, nb, r, L + (kb + nb) * n + kb, n, Bk, ldb, Bk + nb * ldb, ldb,
+                         true, false);
+    g.sync();
+  }
+}
+
+// In-place L^T X = Y.
+__device__ __forceinline__ void g_trsm_lower_t_blocked(const Grp& g, int n, const double* L,
+                                                       const double* dinv, int r, double* B,
+                                                       int ldb) {
+  const int nblk = (n + kNB - 1) / kNB;
+  for (int bi = nblk - 1; bi >= 0; --bi) {
+    const int kb = bi * kNB;
+    const int nb = n - kb < kNB ? n - kb : kNB;
+    double* Bk = B + kb * ldb;
+    g_dmma<true, false>(g, nb, nb, r, dinv + bi * kNB * kNB, kNB, Bk, ldb, Bk, ldb, false, false);
+    g.sync();
+    if (kb == 0) break;
+    g_dmma<true, false>(g, kb, nb, r, L + kb * n, n, Bk, ldb, B, ldb, true, false);
+    g.sync();
+  }
+}
+
+// One warp: in-place L z = r (vector) with the inverted diagonal blocks.
+__device__ __forceinline__ void w_lower_solve_vec(int lane, int n, const double* L,
+                                                  const double* dinv, double* r) {
+  for (int kb = 0; kb < n; kb += kNB) {
+    const int nb = n - kb < kNB ? n - kb : kNB;
+    const double* Di = dinv + (kb / kNB) * kNB * kNB;
+    double z = 0.0;
+    if (lane < nb)
+      for (int l = 0; l <= lane; ++l) z += Di[lane * kNB + l] * r[kb + l];
+    __syncwarp();
+    if (lane < nb) r[kb + lane] = z;
+    __syncwarp();
+    for (int i = kb + nb + lane; i < n; i += 32) {
+      double s = r[i];
+      for (int l = 0; l < nb; ++l) s -= L[i * n + kb + l] * r[kb + l];
+      r[i] = s;
+    }
+    __syncwarp();
+  }
+}
+
+// fixed-order warp sum (lane-strided partials, then an xor tree): deterministic
+__device__ __forceinline__ double w_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+constexpr double kLog2PiB = 1.8378770664093454835606594728112;
+
+// One warp: log N(x; mean, L L^T) with the inverted diagonal blocks; work: n doubles.
+__device__ __forceinline__ double w_log_pdf_factored(int lane, int n, const double* x,
+                                                     const double* mean, const double* L,
+                                                     const double* dinv, double* work) {
+  for (int i = lane; i < n; i += 32) work[i] = x[i] - mean[i];
+  __syncwarp();
+  w_lower_solve_vec(lane, n, L, dinv, work);
+  double sq = 0.0, ld = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    sq += work[i] * work[i];
+    ld += log(L[i * n + i]);
+  }
+  sq = w_sum(sq);
+  ld = w_sum(ld);
+  return -0.5 * (n * kLog2PiB + sq) - ld;
+}
+
+__device__ __forceinline__ bool use_blocked(const Grp& g, int n) { return g.block && n >= 16; }
+
 // ---------------------------------------------------------------- Cholesky
 // LLT of the lower triangle of A (n×n) into L; Eigen semantics: fail iff a
 // pivot x <= 0 (NaN passes).  Right-looking: the trailing update of column k is
@@ -228,9 +437,20 @@ __device__ __forceinline__ bool g_llt(const Grp& g, int n, const double* A, doub
 
 // factor_psd (gauss.cpp:26-35): LLT, then + eps*s*I for eps in {1e-10, 1e-8}.
 // scratch: n*n doubles.  Returns 0 ok, 2 (AUXMC_E_FACTOR) on failure.
+// Blocked (CTA, n >= 16): the jittered matrix is built in L directly and
+// scratch (>= dinv_doubles(n)) receives the inverted diagonal blocks, which
+// g_llt_solve / g_log_pdf_factored take as `dinv`.
 __device__ __forceinline__ int g_factor_psd(const Grp& g, int n, const double* A, double* L,
                                             double* scratch, int* flag, double* red) {
-  if (g_llt(g, n, A, L, flag)) return 0;
+  const bool blk = use_blocked(g, n);
+  if (blk) {
+    for (int i = g.ty(); i < n; i += g.ny())
+      for (int j = g.tx(); j < n; j += 16) L[i * n + j] = j <= i ? A[i * n + j] : 0.0;
+    g.sync();
+    if (g_llt_blocked(g, n, L, flag, scratch)) return 0;
+  } else if (g_llt(g, n, A, L, flag)) {
+    return 0;
+  }
   if (g.lane == 0) {  // jitter scale (gauss.cpp:20-24)
     double tr = 0.0;
     for (int i = 0; i < n; ++i) tr += A[i * n + i];
@@ -246,6 +466,14 @@ __device__ __forceinline__ int g_factor_psd(const Grp& g, int n, const double* A
   const double s = *red;
   const double eps[2] = {1e-10, 1e-8};
   for (int e = 0; e < 2; ++e) {
+    if (blk) {
+      for (int i = g.ty(); i < n; i += g.ny())
+        for (int j = g.tx(); j < n; j += 16)
+          L[i * n + j] = j <= i ? A[i * n + j] + (i == j ? (eps[e] * s) * 1.0 : 0.0) : 0.0;
+      g.sync();
+      if (g_llt_blocked(g, n, L, flag, scratch)) return 0;
+      continue;
+    }
     for (int i = g.ty(); i < n; i += g.ny())
       for (int j = g.tx(); j < n; j += 16)
         scratch[i * n + j] = A[i * n + j] + (i == j ? (eps[e] * s) * 1.0 : 0.0);
@@ -271,19 +499,25 @@ __device__ __forceinline__ int g_chol_psd(const Grp& g, int n, const double* A, 
 // the lane that applies the last update to row i+1 also divides it by L_{i+1,i+1},
 // so each x is divided exactly once (x_i = (b_i - Σ_j L_ij x_j) / L_ii in
 // ascending j, the reference's order) and there is one group sync per row.
+// dinv: the inverted diagonal blocks from a blocked g_factor_psd (CTA, n >= 16).
 __device__ __forceinline__ void g_llt_solve(const Grp& g, int n, const double* L, int r,
-                                            double* B) {
+                                            double* B, const double* dinv = nullptr) {
+  if (dinv && use_blocked(g, n)) {
+    g_trsm_lower_blocked(g, n, L, dinv, r, B, r);
+    g_trsm_lower_t_blocked(g, n, L, dinv, r, B, r);
+    return;
+  }
   const int ny = g.ny();
   for (int c = g.lane; c < r; c += g.size) B[c] = B[c] / L[0];
   g.sync();
   for (int i = 0; i < n; ++i) {  // forward: L Y = B
     for (int j = i + 1 + g.ty(); j < n; j += ny) {
       const double lji = L[j * n + i];
-      const bool last = j == i + 1;
-      const double ljj = L[j * n + j];
-      for (int c = g.tx(); c < r; c += 16) {
-        const double v = B[j * r + c] - lji * B[i * r + c];
-        B[j * r + c] = last ? v / ljj : v;
+      if (j == i + 1) {  // last update of row j: finish it
+        const double ljj = L[j * n + j];
+        for (int c = g.tx(); c < r; c += 16) B[j * r + c] = (B[j * r + c] - lji * B[i * r + c]) / ljj;
+      } else {
+        for (int c = g.tx(); c < r; c += 16) B[j * r + c] -= lji * B[i * r + c];
       }
     }
     g.sync();
@@ -294,11 +528,11 @@ __device__ __forceinline__ void g_llt_solve(const Grp& g, int n, const double* L
   for (int i = n - 1; i >= 0; --i) {  // backward: L^T X = Y
     for (int j = g.ty(); j < i; j += ny) {
       const double lij = L[i * n + j];
-      const bool last = j == i - 1;
-      const double ljj = L[j * n + j];
-      for (int c = g.tx(); c < r; c += 16) {
-        const double v = B[j * r + c] - lij * B[i * r + c];
-        B[j * r + c] = last ? v / ljj : v;
+      if (j == i - 1) {
+        const double ljj = L[j * n + j];
+        for (int c = g.tx(); c < r; c += 16) B[j * r + c] = (B[j * r + c] - lij * B[i * r + c]) / ljj;
+      } else {
+        for (int c = g.tx(); c < r; c += 16) B[j * r + c] -= lij * B[i * r + c];
       }
     }
     g.sync();
@@ -311,8 +545,8 @@ __device__ __forceinline__ void g_lower_solve_vec(const Grp& g, int n, const dou
   g.sync();
   for (int i = 0; i < n; ++i) {
     for (int j = i + 1 + g.lane; j < n; j += g.size) {
-      const double v = r[j] - L[j * n + i] * r[i];
-      r[j] = j == i + 1 ? v / L[j * n + j] : v;
+      if (j == i + 1) r[j] = (r[j] - L[j * n + i] * r[i]) / L[j * n + j];
+      else r[j] -= L[j * n + i] * r[i];
     }
     g.sync();
   }
@@ -337,7 +571,18 @@ constexpr double kLog2Pi = 1.8378770664093454835606594728112;
 // work: n doubles.  Returns value on all lanes.
 __device__ __forceinline__ double g_log_pdf_factored(const Grp& g, int n, const double* x,
                                                      const double* mean, const double* L,
-                                                     double* work, double* red) {
+                                                     double* work, double* red,
+                                                     const double* dinv = nullptr) {
+  if (dinv && use_blocked(g, n)) {
+    if (g.lane < 32) {
+      const double v = w_log_pdf_factored(g.lane, n, x, mean, L, dinv, work);
+      if (g.lane == 0) *red = v;
+    }
+    g.sync();
+    const double v = *red;
+    g.sync();
+    return v;
+  }
   for (int i = g.lane; i < n; i += g.size) work[i] = x[i] - mean[i];
   g.sync();
   g_lower_solve_vec(g, n, L, work);

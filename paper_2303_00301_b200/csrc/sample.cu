@@ -58,7 +58,7 @@ __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel&
     g.sync();
     st = g_factor_psd(g, d, S, L, scr, flag, red);
     if (st) return st;
-    g_llt_solve(g, d, L, d, W);
+    g_llt_solve(g, d, L, d, W, scr);  // scr: inverted diagonal blocks (CTA, d >= 16)
     for (int i = g.lane; i < dd; i += g.size) G[i] = W[(i % d) * d + i / d];
     g.sync();
   }

@@ -59,6 +59,43 @@ def test_kalman_filter_matches_oracle(gpu, oracle, case):
     assert_close(fr.log_marginal[0].cpu(), want.log_marginal, RTOL, "log_marginal")
 
 
+# CTA-group kernels (dims > 16): blocked LLT / triangular solves with DMMA
+# panel updates, odd sizes to exercise partial 8-wide blocks and tiles.
+LARGE_CASES = [
+    (6, 20, 17, True, True, 31),
+    (4, 17, 40, False, False, 32),
+    (3, 40, 60, True, False, 33),
+]
+
+
+@pytest.mark.parametrize("case", LARGE_CASES)
+def test_kalman_filter_large_dims_match_oracle(gpu, oracle, case):
+    lgssm, _, _ = gpu
+    m, obs = _oracle_case(oracle, *case)
+    want = oracle.kalman_filter(m, obs)
+    fr = lgssm.kalman_filter(to_gpu_model(m), obs)
+    assert int(fr.status[0]) == 0
+    assert_close(fr.pred_cov[0].cpu(), want.pred_cov, RTOL, "pred_cov")
+    assert_close(fr.filt_mean[0].cpu(), want.filt_mean, RTOL, "filt_mean")
+    assert_close(fr.filt_cov[0].cpu(), want.filt_cov, RTOL, "filt_cov")
+    assert_close(fr.log_marginal[0].cpu(), want.log_marginal, RTOL, "log_marginal")
+
+
+@pytest.mark.parametrize("case", LARGE_CASES)
+def test_backward_sampler_large_dims_match_oracle(gpu, oracle, case):
+    lgssm, pit, _ = gpu
+    m, obs = _oracle_case(oracle, *case)
+    fr_o = oracle.kalman_filter(m, obs)
+    gm = to_gpu_model(m)
+    fr = lgssm.kalman_filter(gm, obs)
+    B = 3
+    term, back, bridge = predrawn(np.random.default_rng(case[-1]), B, m.T, m.dx,
+                                  pit.dnc_bridge_count(m.T))
+    want = _oracle_paths(oracle, 0, m, fr_o, term, back, bridge)
+    got = lgssm.PathSampler(gm, B, 0, True)(fr, lgssm.Noise.predrawn(term, back, bridge))
+    assert_close(got.cpu(), want, RTOL, "backward sampler")
+
+
 def test_kalman_filter_batched_sequences(gpu, oracle):
     lgssm, _, _ = gpu
     m, _ = _oracle_case(oracle, 30, 3, 2, True, True, 11)
