@@ -53,10 +53,8 @@ def parse():
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    from paper_2303_00301_b200.shard import dist_env as env
+    return env()
 
 
 class Clocks:
@@ -129,14 +127,15 @@ def ncu_traffic(kernel):
 # ---------------------------------------------------------------------------- C2
 def c2_setup(args, rank, device):
     import torch
-    from paper_2303_00301_b200 import bench_models as bm, lgssm, rng
+    from paper_2303_00301_b200 import bench_models as bm, lgssm, rng, shard
     T = args.T or 65536
     C = args.chains or 1024
     spec = bm.ModelSpec(kind="lgssm-synthetic", T=T, dx=4, dy=1, data_seed=1)
     lat, data = bm.simulate(spec)
     model = bm.synthetic_lgssm(spec, device=device)
     fr = lgssm.kalman_filter(model, data)
-    keys = rng.chain_keys(1, C, first=rank * C, device=device)  # from_seed(1).derive(kChain, c)
+    sh = shard.weak_shard(rank, int(os.environ.get("WORLD_SIZE", "1")), C)
+    keys = rng.chain_keys(1, sh.count, first=sh.first, device=device)  # derive(kChain, c)
     if args.noise == "predrawn":
         term = rng.normals(keys, rng.kTerminalDraw, 0, 1, 4).reshape(C, 4)
         back = rng.normals(keys, rng.kBackwardNoise, 0, T, 4)
@@ -216,10 +215,9 @@ def timed(fn, steps, world):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        from paper_2303_00301_b200.shard import max_over_ranks
+        ms = max_over_ranks(ms, world, device="cuda")
         dist.barrier()
-        ms = float(t.item())
     return ms
 
 

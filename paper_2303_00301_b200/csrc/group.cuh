@@ -52,30 +52,13 @@ __device__ __forceinline__ void g_eye(const Grp& g, int n, double* dst) {
 // shared memory with bounds guards, so no padding is needed.
 // TA/TB: operand transposed in memory (A^T B, A B^T forms).
 template <bool TA, bool TB>
+__device__ __forceinline__ void g_dmma(const Grp& g, int m, int k, int n, const double* A, int lda,
+                                       const double* B, int ldb, double* C, int ldc, bool sub,
+                                       bool lower, const double* Dadd);
+template <bool TA, bool TB>
 __device__ __forceinline__ void g_mm_dmma(const Grp& g, int m, int k, int n, const double* A,
                                           const double* B, double* C, const double* D) {
-  const int warp = g.lane >> 5, lane = g.lane & 31, nw = g.size >> 5;
-  const int gi = lane >> 2, ti = lane & 3;
-  const int mt = (m + 7) >> 3, nt = (n + 7) >> 3, kt = (k + 3) >> 2;
-  for (int tile = warp; tile < mt * nt; tile += nw) {
-    const int I = (tile / nt) * 8, J = (tile % nt) * 8;
-    double c0 = 0.0, c1 = 0.0;
-    const int ar = I + gi, bc = J + gi;
-    for (int K = 0; K < kt; ++K) {
-      const int kk = K * 4 + ti;
-      double a = 0.0, b = 0.0;
-      if (ar < m && kk < k) a = TA ? A[kk * m + ar] : A[ar * k + kk];
-      if (bc < n && kk < k) b = TB ? B[bc * k + kk] : B[kk * n + bc];
-      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                   : "+d"(c0), "+d"(c1)
-                   : "d"(a), "d"(b));
-    }
-    const int r = I + gi, cc = J + 2 * ti;
-    if (r < m) {
-      if (cc < n) C[r * n + cc] = D ? c0 + D[r * n + cc] : c0;
-      if (cc + 1 < n) C[r * n + cc + 1] = D ? c1 + D[r * n + cc + 1] : c1;
-    }
-  }
+  g_dmma<TA, TB>(g, m, k, n, A, TA ? m : k, B, TB ? k : n, C, n, false, false, D);
 }
 
 __device__ __forceinline__ bool use_dmma(const Grp& g, int m, int k, int n) {
@@ -215,79 +198,130 @@ constexpr int kNB = 8;
 
 __host__ __device__ constexpr int dinv_doubles(int n) { return 64 * ((n + 7) / 8); }
 
-// C (m×n, ldc) = op(A) op(B)  or  C -= op(A) op(B)  (sub); A(i,l) = TA ? A[l*lda+i] :
-// A[i*lda+l], B(l,j) = TB ? B[j*ldb+l] : B[l*ldb+j]; lower: only j <= i is written
-// (and tiles above the diagonal skipped).  For sub the accumulator starts at C
-// and the A fragment is negated (one fused chain C - Σ a b).  A tile loads its
-// whole k-range before it stores, so C may alias the rows of A when n <= 8, or
-// the columns of B when m <= 8.
+// C (m×n, ldc) = op(A) op(B) [+ Dadd]  or  C -= op(A) op(B)  (sub);
+// A(i,l) = TA ? A[l*lda+i] : A[i*lda+l], B(l,j) = TB ? B[j*ldb+l] : B[l*ldb+j];
+// lower: only j <= i is written (tiles above the diagonal skipped).  For sub
+// the accumulator starts at C and the A fragment is negated (one fused chain
+// C - Σ a b).  Each warp owns a pair of horizontally adjacent 8×8 tiles (two
+// independent DMMA chains sharing the A fragment).  A tile loads its whole
+// k-range before it stores, so C may alias the rows of A when n <= 8, or the
+// columns of B when m <= 8.
 template <bool TA, bool TB>
 __device__ __forceinline__ void g_dmma(const Grp& g, int m, int k, int n, const double* A, int lda,
                                        const double* B, int ldb, double* C, int ldc, bool sub,
-                                       bool lower) {
+                                       bool lower, const double* Dadd = nullptr) {
   const int warp = g.lane >> 5, lane = g.lane & 31, nw = g.size >> 5;
   const int gi = lane >> 2, ti = lane & 3;
   const int mt = (m + 7) >> 3, nt = (n + 7) >> 3, kt = (k + 3) >> 2;
-  for (int tile = warp; tile < mt * nt; tile += nw) {
-    const int It = tile / nt, Jt = tile - It * nt;
+  const int np = (nt + 1) >> 1;
+  const float rnp = 1.0f / (float)np;
+  for (int w = warp; w < mt * np; w += nw) {
+    const int It = (int)(((float)w + 0.5f) * rnp);  // exact for these small ranges
+    const int Jt = (w - It * np) * 2;
     if (lower && Jt > It) continue;
-    const int I = It * 8, J = Jt * 8;
-    const int r = I + gi, cc = J + 2 * ti;
-    double c0 = 0.0, c1 = 0.0;
-    if (sub) {
-      if (r < m && cc < n) c0 = C[r * ldc + cc];
-      if (r < m && cc + 1 < n) c1 = C[r * ldc + cc + 1];
+    const bool two = Jt + 1 < nt && !(lower && Jt + 1 > It);
+    const int r = It * 8 + gi;
+    const int c0c = Jt * 8 + 2 * ti, c1c = c0c + 8;
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+    if (sub && r < m) {
+      if (c0c < n) c00 = C[r * ldc + c0c];
+      if (c0c + 1 < n) c01 = C[r * ldc + c0c + 1];
+      if (two && c1c < n) c10 = C[r * ldc + c1c];
+      if (two && c1c + 1 < n) c11 = C[r * ldc + c1c + 1];
     }
-    const int ar = I + gi, bc = J + gi;
+    const int b0 = Jt * 8 + gi, b1 = b0 + 8;
     for (int K = 0; K < kt; ++K) {
       const int kk = K * 4 + ti;
-      double a = 0.0, b = 0.0;
-      if (ar < m && kk < k) a = TA ? A[kk * lda + ar] : A[ar * lda + kk];
-      if (bc < n && kk < k) b = TB ? B[bc * ldb + kk] : B[kk * ldb + bc];
+      double a = 0.0, x0 = 0.0, x1 = 0.0;
+      if (r < m && kk < k) a = TA ? A[kk * lda + r] : A[r * lda + kk];
+      if (kk < k) {
+        if (b0 < n) x0 = TB ? B[b0 * ldb + kk] : B[kk * ldb + b0];
+        if (two && b1 < n) x1 = TB ? B[b1 * ldb + kk] : B[kk * ldb + b1];
+      }
       if (sub) a = -a;
       asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                   : "+d"(c0), "+d"(c1)
-                   : "d"(a), "d"(b));
+                   : "+d"(c00), "+d"(c01)
+                   : "d"(a), "d"(x0));
+      if (two)
+        asm volatile(
+            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+            : "+d"(c10), "+d"(c11)
+            : "d"(a), "d"(x1));
     }
     if (r < m) {
-      if (cc < n && (!lower || cc <= r)) C[r * ldc + cc] = c0;
-      if (cc + 1 < n && (!lower || cc + 1 <= r)) C[r * ldc + cc + 1] = c1;
+      if (c0c < n && (!lower || c0c <= r))
+        C[r * ldc + c0c] = Dadd ? c00 + Dadd[r * ldc + c0c] : c00;
+      if (c0c + 1 < n && (!lower || c0c + 1 <= r))
+        C[r * ldc + c0c + 1] = Dadd ? c01 + Dadd[r * ldc + c0c + 1] : c01;
+      if (two && c1c < n && (!lower || c1c <= r))
+        C[r * ldc + c1c] = Dadd ? c10 + Dadd[r * ldc + c1c] : c10;
+      if (two && c1c + 1 < n && (!lower || c1c + 1 <= r))
+        C[r * ldc + c1c + 1] = Dadd ? c11 + Dadd[r * ldc + c1c + 1] : c11;
     }
   }
 }
 
 // One warp: factor the nb×nb diagonal block D (row stride n, lower triangle holds
 // the updated A) in place and write its inverse to Di (8×8, zero padded).
-// Returns false (uniformly) on a pivot <= 0.
+// Rows live in registers of lanes 0..7 (column broadcasts by shuffle), so the
+// serial chain per column is one rsqrt and two shuffles; columns are scaled by
+// the reciprocal pivot.  Returns false (warp-uniformly) on a
+// pivot <= 0 (NaN passes, as in Eigen).
 __device__ __forceinline__ bool w_factor_diag(int lane, int n, int nb, double* D, double* Di) {
-  for (int j = 0; j < nb; ++j) {
-    const double x = D[j * n + j];
-    if (x <= 0.0) return false;
-    const double piv = sqrt(x);
-    if (lane > j && lane < nb) D[lane * n + j] = D[lane * n + j] / piv;
-    __syncwarp();
-    if (lane == 0) D[j * n + j] = piv;
-    for (int e = lane; e < kNB * kNB; e += 32) {
-      const int i = e >> 3, jj = e & 7;
-      if (i < nb && jj > j && jj <= i) D[i * n + jj] -= D[i * n + j] * D[jj * n + j];
-    }
-    __syncwarp();
+  const int i = lane & 7;
+  double a[kNB], inv[kNB];
+#pragma unroll
+  for (int k = 0; k < kNB; ++k) {
+    a[k] = (i < nb && k <= i) ? D[i * n + k] : (k == i ? 1.0 : 0.0);
+    inv[k] = 0.0;
   }
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < kNB; ++j) {
+    if (j < nb) {
+      const double d = __shfl_sync(0xffffffffu, a[j], j);
+      if (d <= 0.0) {
+        ok = false;
+        break;
+      }
+      const double r = rsqrt(d);  // 1/sqrt(d) to ~1 ulp; the pivot is d * r
+      const double piv = d * r;
+      inv[j] = r;
+      if (i > j) a[j] = a[j] * r;
+      else if (i == j) a[j] = piv;
+#pragma unroll
+      for (int k = j + 1; k < kNB; ++k) {
+        const double lkj = __shfl_sync(0xffffffffu, a[j], k);
+        if (k <= i && i > j) a[k] -= a[j] * lkj;
+      }
+    }
+  }
+  if (!ok) return false;
+  if (lane < nb) {
+#pragma unroll
+    for (int k = 0; k < kNB; ++k)
+      if (k <= i) D[i * n + k] = a[k];
+  }
+  __syncwarp();
   if (lane < kNB) {  // column `lane` of D^{-1} by forward substitution
     const int j = lane;
     double x[kNB];
 #pragma unroll
-    for (int i = 0; i < kNB; ++i) {
+    for (int r = 0; r < kNB; ++r) {
       double v = 0.0;
-      if (j < nb && i < nb && i >= j) {
-        double s = i == j ? 1.0 : 0.0;
+      if (j < nb && r < nb && r >= j) {
+        if (r == j) {
+          v = inv[r];
+        } else {
+          double s = 0.0;
 #pragma unroll
-        for (int l = 0; l < i; ++l)
-          if (l >= j) s -= D[i * n + l] * x[l];
-        v = s / D[i * n + i];
+          for (int l = 0; l < r; ++l)
+            if (l >= j) s += D[r * n + l] * x[l];
+          v = -s * inv[r];
+        }
       }
-      x[i] = v;
-      Di[i * kNB + j] = v;
+      x[r] = v;
+      Di[r * kNB + j] = v;
     }
   }
   __syncwarp();

@@ -38,8 +38,7 @@ __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel&
   double* A = L + dd;
   double* W = A + dd;
   double* G = W + dd;
-  double* scr = G + dd;
-  double* v = scr + dd;
+  double* v = G + dd;  // factor scratch (jitter matrix / inverted diagonal blocks): X, then S
   double* red = v + 2 * d;
   const double* Ft = m.Ft(t, k);
   g_copy(g, dd, fc + (size_t)t * dd, P);
@@ -56,9 +55,9 @@ __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel&
     // rhs = cross^T (into W), X := S^{-1} cross^T, G = X^T
     for (int i = g.lane; i < dd; i += g.size) W[i] = X[(i % d) * d + i / d];
     g.sync();
-    st = g_factor_psd(g, d, S, L, scr, flag, red);
+    st = g_factor_psd(g, d, S, L, X, flag, red);  // X (cross) is consumed
     if (st) return st;
-    g_llt_solve(g, d, L, d, W, scr);  // scr: inverted diagonal blocks (CTA, d >= 16)
+    g_llt_solve(g, d, L, d, W, X);
     for (int i = g.lane; i < dd; i += g.size) G[i] = W[(i % d) * d + i / d];
     g.sync();
   }
@@ -101,7 +100,7 @@ __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel&
   g_symm(g, d, X);
   g.sync();
   if (!store_cov) {
-    st = g_chol_psd(g, d, X, L, scr, flag, red);
+    st = g_chol_psd(g, d, X, L, S, flag, red);  // S (Q) is consumed
     if (st) return st;
   }
   for (int i = g.lane; i < dd; i += g.size) {
@@ -122,7 +121,7 @@ __global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
   extern __shared__ double smem[];
   const int d = m.dx, dd = d * d;
   const int T = m.T;
-  const int per = 9 * dd + 4 * d + 4;
+  const int per = 8 * dd + 4 * d + 4;
   Grp g = BLOCK ? block_group() : warp_group();
   const int gid = BLOCK ? 0 : (threadIdx.x >> 5);
   const int groups_per_block = BLOCK ? 1 : (blockDim.x >> 5);
@@ -568,7 +567,7 @@ int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, 
                         int Bfr, double* elems, double* term, int* st_fr, int store_cov,
                         cudaStream_t stream) {
   const int d = dm.dx;
-  const int per = 9 * d * d + 4 * d + 4;
+  const int per = 8 * d * d + 4 * d + 4;
   const long long n_items = (long long)Bfr * (dm.T + 1);
   if (d <= 4) {
     const int grid = (int)std::min<long long>((n_items + 127) / 128, 148LL * 16);

@@ -20,7 +20,7 @@ FP64_PEAK_TFLOPS = 37.0  # datasheet placeholder (no measured DFMA peak in MEASU
 def run(args, rank, world, local):
     import torch
     from bench import Clocks, timed
-    from paper_2303_00301_b200 import _lib, auxk, bench_models as bm, fkpg
+    from paper_2303_00301_b200 import _lib, auxk, bench_models as bm, fkpg, shard
     device = f"cuda:{local}"
     torch.cuda.set_device(local)
     lib = _lib.load()
@@ -47,12 +47,14 @@ def run(args, rank, world, local):
         torch.as_tensor(lat * 0 + tg.m0.cpu().numpy(), device=device)
     if cfg == "c4":
         variant = fkpg.Variant.kReference if args.sampler == "dnc" else fkpg.Variant.kPit
-        ch = fkpg.init_pg(tg, x0, delta, 1, C, N, first=rank * C)
+        sh = shard.weak_shard(rank, world, C)
+        ch = fkpg.init_pg(tg, x0, delta, 1, sh.count, N, first=sh.first)
 
         def step():
             ch.aux_pgibbs_step(variant)
     else:
-        ch = auxk.init_chains(tg, x0, delta, 1, C, first=rank * C)
+        sh = shard.weak_shard(rank, world, C)
+        ch = auxk.init_chains(tg, x0, delta, 1, sh.count, first=sh.first)
 
         # C1 is one short chain: the scan filter (KernelOptions::parallel_filter)
         # parallelizes the horizon; C3 has 256 chains and uses the sequential filter.
