@@ -183,6 +183,210 @@ __global__ void k_filter_seq(DevModel m, const double* __restrict__ obs, int B,
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_filter_cta: the CTA-group filter for large dims (dx > 16 or dy > 16), laid
+// out to fit two CTAs per SM (one sequence each), so one sequence's serial
+// phases (diagonal-block factorizations, triangular-solve steps) overlap the
+// other's tensor-core products.  The innovation covariance is factored in
+// place; its symmetrized R is restaged from global memory where needed.  The
+// jitter ladder of factor_psd (gauss.cpp:26-35) rebuilds S and retries with
+// + eps*s*I, as the reference does.
+struct CtaFilterLayout {
+  int dx, dy, W;
+  int o_mm, o_v, o_innov, o_v2, o_p, o_tmp, o_a, o_Hs, o_X, o_SL, o_work, o_dinv, o_red, total;
+  __host__ __device__ CtaFilterLayout(int dx_, int dy_) : dx(dx_), dy(dy_) {
+    W = dx > dy ? dx : dy;
+    const int ddx = dx * dx, ddy = dy * dy;
+    int o = 0;
+    o_mm = o; o += (dx + 1) & ~1;
+    o_v = o; o += (W + 1) & ~1;
+    o_innov = o; o += (W + 1) & ~1;
+    o_v2 = o; o += (W + 1) & ~1;
+    o_p = o; o += ddx;
+    o_tmp = o; o += ddx;
+    o_a = o; o += ddx;
+    o_Hs = o; o += dy * dx;
+    o_X = o; o += dy * dx;
+    o_SL = o; o += ddy;
+    // Qs / (a p a^T) need dx*dx: the S/L region when large enough
+    if (ddy >= ddx) { o_work = o_SL; } else { o_work = o; o += ddx; }
+    // inverted diagonal blocks of L live in tmp when they fit
+    if (dinv_doubles(dy) <= ddx) { o_dinv = o_tmp; } else { o_dinv = o; o += dinv_doubles(dy); }
+    o_red = o; o += 4;
+    total = o;
+  }
+};
+
+__global__ void __launch_bounds__(256, 2)
+k_filter_cta(DevModel m, const double* __restrict__ obs, int B, double* pred_mean,
+             double* pred_cov, double* filt_mean, double* filt_cov, double* log_marginal,
+             int* status) {
+  extern __shared__ double smem[];
+  const int dx = m.dx, dy = m.dy, T = m.T;
+  const CtaFilterLayout lo(dx, dy);
+  const Grp g = block_group();
+  double* mm = smem + lo.o_mm;
+  double* v = smem + lo.o_v;
+  double* innov = smem + lo.o_innov;
+  double* v2 = smem + lo.o_v2;
+  double* p = smem + lo.o_p;
+  double* tmp = smem + lo.o_tmp;
+  double* a = smem + lo.o_a;
+  double* Hs = smem + lo.o_Hs;
+  double* X = smem + lo.o_X;
+  double* SL = smem + lo.o_SL;
+  double* work = smem + lo.o_work;
+  double* dinv = smem + lo.o_dinv;
+  double* red = smem + lo.o_red;
+  int* flag = reinterpret_cast<int*>(red + 2);
+  const int ddx = dx * dx;
+  const bool blk = dy >= 16;
+  for (int b = blockIdx.x; b < B; b += gridDim.x) {
+    const double* y_all = obs + (size_t)b * (T + 1) * dy;
+    double* pm_out = pred_mean + (size_t)b * (T + 1) * dx;
+    double* pc_out = pred_cov + (size_t)b * (T + 1) * ddx;
+    double* fm_out = filt_mean + (size_t)b * (T + 1) * dx;
+    double* fc_out = filt_cov + (size_t)b * (T + 1) * ddx;
+    double ll = 0.0;
+    int st = 0;
+    for (int i = g.lane; i < dx; i += g.size) mm[i] = m.m0[i];
+    g_copy(g, ddx, m.P0, p);
+    g.sync();
+    g_symm(g, dx, p);
+    g.sync();
+    for (int t = 0; t <= T; ++t) {
+      if (t > 0) {  // predict: m = F m + b, P = symm(F P F^T + symm(Q))
+        g_copy(g, ddx, m.Ft(t - 1, b), a);
+        g_copy(g, ddx, m.Qt(t - 1, b), work);
+        g.sync();
+        g_mv4<false>(g, dx, dx, a, dx, mm, v, m.bt(t - 1, b));
+        g_symm(g, dx, work);
+        g_mm(g, dx, dx, dx, a, p, tmp);
+        g.sync();
+        for (int i = g.lane; i < dx; i += g.size) mm[i] = v[i];
+        g_mm_nt(g, dx, dx, dx, tmp, a, p, work);
+        g.sync();
+        g_symm(g, dx, p);
+        g.sync();
+      }
+      for (int i = g.lane; i < dx; i += g.size) pm_out[(size_t)t * dx + i] = mm[i];
+      for (int i = g.lane; i < ddx; i += g.size) pc_out[(size_t)t * ddx + i] = p[i];
+      if (m.observed(t)) {
+        const double* c = m.ct(t, b);
+        const double* y = y_all + (size_t)t * dy;
+        const double* R = m.Rt(t, b);
+        g_copy(g, dy * dx, m.Ht(t, b), Hs);
+        g.sync();
+        {  // innovation v = (y - H m) - c and the log-pdf mean H m + c
+          const int q = g.lane & 3, rows = g.size >> 2;
+          for (int i0 = 0; i0 < dy; i0 += rows) {
+            const int i = i0 + (g.lane >> 2);
+            double s = 0.0;
+            if (i < dy)
+              for (int j = q; j < dx; j += 4) s += Hs[i * dx + j] * mm[j];
+            s = quad_sum(s);
+            if (i < dy && q == 0) {
+              innov[i] = (y[i] - s) - c[i];
+              v2[i] = s + c[i];
+            }
+          }
+        }
+        g_mm(g, dy, dx, dx, Hs, p, X);  // H P (solved in place below)
+        double jit = 0.0;
+        bool ok = false;
+        for (int attempt = 0; attempt < 3 && !ok; ++attempt) {
+          // S = symm(H P H^T + symm(R)) [+ eps*s*I]
+          g_copy(g, dy * dy, R, SL);
+          g.sync();
+          g_symm(g, dy, SL);
+          g.sync();
+          g_mm_nt(g, dy, dx, dy, X, Hs, SL, SL);
+          g.sync();
+          g_symm(g, dy, SL);
+          g.sync();
+          if (attempt > 0) {
+            if (attempt == 1) {  // jitter scale (gauss.cpp:20-24) from the rebuilt S
+              if (g.lane == 0) {
+                double tr = 0.0;
+                for (int i = 0; i < dy; ++i) tr += SL[i * dy + i];
+                double sc = tr / static_cast<double>(dy);
+                if (sc <= 0.0) {
+                  double mx = 0.0;
+                  for (int i = 0; i < dy * dy; ++i) mx = fabs(SL[i]) > mx ? fabs(SL[i]) : mx;
+                  sc = mx;
+                }
+                *red = sc;
+              }
+              g.sync();
+              jit = *red;
+              g.sync();
+            }
+            const double eps = attempt == 1 ? 1e-10 : 1e-8;
+            for (int i = g.lane; i < dy; i += g.size) SL[i * dy + i] = SL[i * dy + i] + (eps * jit) * 1.0;
+            g.sync();
+          }
+          // lower triangle in place, upper zeroed
+          for (int i = g.ty(); i < dy; i += g.ny())
+            for (int j = i + 1 + g.tx(); j < dy; j += 16) SL[i * dy + j] = 0.0;
+          g.sync();
+          ok = blk ? g_llt_blocked(g, dy, SL, flag, dinv) : g_llt(g, dy, SL, SL, flag);
+        }
+        if (!ok) {
+          st = 2;
+          break;
+        }
+        g_llt_solve(g, dy, SL, dx, X, blk ? dinv : nullptr);  // X = S^{-1} H P ; gain = X^T
+        if (blk) {
+          // warp 0: log-likelihood term; the other warps: mean update and a = I - X^T H
+          if (g.lane < 32) {
+            ll += w_log_pdf_factored(g.lane, dy, y, v2, SL, dinv, v);
+          } else {
+            const Grp gw = warps_group(1, g.size / 32 - 1, 1);
+            g_mv4<true>(gw, dx, dy, X, dx, innov, mm, mm);
+            g_mm_tn(gw, dx, dy, dx, X, Hs, a);
+            gw.sync();
+            for (int i = gw.ty(); i < dx; i += gw.ny())
+              for (int j = gw.tx(); j < dx; j += 16)
+                a[i * dx + j] = (i == j ? 1.0 : 0.0) - a[i * dx + j];
+          }
+          g.sync();
+        } else {
+          ll += g_log_pdf_factored(g, dy, y, v2, SL, v, red);
+          g_mv4<true>(g, dx, dy, X, dx, innov, mm, mm);
+          g_mm_tn(g, dx, dy, dx, X, Hs, a);
+          g.sync();
+          for (int i = g.ty(); i < dx; i += g.ny())
+            for (int j = g.tx(); j < dx; j += 16) a[i * dx + j] = (i == j ? 1.0 : 0.0) - a[i * dx + j];
+          g.sync();
+        }
+        // Joseph form P = symm(a P a^T + X^T Rs X); Rs restaged into SL
+        g_copy(g, dy * dy, R, SL);
+        g_mm(g, dx, dx, dx, a, p, tmp);  // a P
+        g.sync();
+        g_symm(g, dy, SL);
+        g.sync();
+        g_mm_tn(g, dx, dy, dy, X, SL, Hs);  // X^T Rs (dx×dy) into the H slot
+        g.sync();
+        g_mm_nt(g, dx, dx, dx, tmp, a, work);  // a P a^T (work may alias SL: Rs consumed)
+        g_mm(g, dx, dy, dx, Hs, X, p);         // X^T Rs X
+        g.sync();
+        for (int i = g.lane; i < ddx; i += g.size) p[i] = work[i] + p[i];
+        g.sync();
+        g_symm(g, dx, p);
+        g.sync();
+      }
+      for (int i = g.lane; i < dx; i += g.size) fm_out[(size_t)t * dx + i] = mm[i];
+      for (int i = g.lane; i < ddx; i += g.size) fc_out[(size_t)t * ddx + i] = p[i];
+      g.sync();
+    }
+    if (g.lane == 0) {
+      log_marginal[b] = ll;
+      status[b] = st;
+    }
+    g.sync();
+  }
+}
+
 // Register path for small dims: one thread per sequence, state and covariance
 // in registers (D <= 6, observation rows <= DY).  Same operation order as the
 // group kernel (lgssm.cpp:73-112).
@@ -419,11 +623,12 @@ int launch_filter_seq(const DevModel& dm, const double* obs, int B, auxmc_filter
   const int per = filter_smem_doubles(dm.dx, dm.dy);
   const bool block = (dm.dx > 16 || dm.dy > 16);
   if (block) {
-    const size_t smem = sizeof(double) * per;
-    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_filter_seq<true>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    AUXMC_LAUNCH(k_filter_seq<true>, B, 256, smem, stream, dm, obs, B, out->pred_mean,
-                 out->pred_cov, out->filt_mean, out->filt_cov, out->log_marginal, status);
+    const size_t smem = sizeof(double) * CtaFilterLayout(dm.dx, dm.dy).total;
+    if (smem > 227 * 1024) return AUXMC_E_DIM;
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_filter_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    AUXMC_LAUNCH(k_filter_cta, B, 256, smem, stream, dm, obs, B, out->pred_mean, out->pred_cov,
+                 out->filt_mean, out->filt_cov, out->log_marginal, status);
   } else {
     const int warps = 4;
     const size_t smem = sizeof(double) * per * warps;

@@ -154,6 +154,30 @@ __device__ __forceinline__ void g_mtv(const Grp& g, int m, int n, const double* 
     y[j] = s;
   }
 }
+// Quad dot products: lanes 4i..4i+3 of a group own row i and sum interleaved
+// terms (j ≡ q mod 4), combined as (s0+s1)+(s2+s3) by xor shuffles — four short
+// FMA chains instead of one long one, fixed order.  The row loop is uniform
+// over the group so every shuffle is full-warp.
+__device__ __forceinline__ double quad_sum(double s) {
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  return s;
+}
+// y[i] = Σ_j A(i,j) x[j] (+ add[i]) ; A(i,j) = TA ? A[j*lda+i] : A[i*lda+j]
+template <bool TA>
+__device__ __forceinline__ void g_mv4(const Grp& g, int m, int n, const double* A, int lda,
+                                      const double* x, double* y, const double* add = nullptr) {
+  const int q = g.lane & 3, rows = g.size >> 2;
+  for (int i0 = 0; i0 < m; i0 += rows) {
+    const int i = i0 + (g.lane >> 2);
+    double s = 0.0;
+    if (i < m)
+      for (int j = q; j < n; j += 4) s += (TA ? A[j * lda + i] : A[i * lda + j]) * x[j];
+    s = quad_sum(s);
+    if (i < m && q == 0) y[i] = add ? s + add[i] : s;
+  }
+}
+
 // in-place symm(A) = (A + A^T)/2 ; caller syncs before (A complete) and after
 __device__ __forceinline__ void g_symm(const Grp& g, int n, double* A) {
   for (int i = g.ty(); i < n; i += g.ny())

@@ -14,7 +14,7 @@ import ctypes
 import json
 
 METRIC = "chain-timesteps/sec (device-timed) at 1/2/4/8 B200; MCMC iters/sec; % HBM/FP64 roofline"
-FP64_PEAK_TFLOPS = 37.0  # datasheet placeholder (no measured DFMA peak in MEASURED_PEAKS.json)
+FP64_PEAK_TFLOPS = 37.1  # measured: DMMA m8n8k4 throughput, tools/micro/lat.cu (profiles/r1_micro_latency_fp64.txt)
 
 
 def run(args, rank, world, local):
@@ -94,7 +94,7 @@ def run(args, rank, world, local):
                          "achieved": tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": tflops / FP64_PEAK_TFLOPS, "traffic": None,
                          "algorithmic_flops_per_chain_timestep": flops_ct,
-                         "peak_source": "datasheet placeholder (no measured FP64 peak)"},
+                         "peak_source": "measured DMMA FP64 throughput (profiles/r1_micro_latency_fp64.txt)"},
             "cpu_baseline": None, "e2e": None, "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
