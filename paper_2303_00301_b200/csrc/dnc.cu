@@ -141,7 +141,7 @@ __global__ void k_dnc_bridge(int T, int d, int Bfr, const double* __restrict__ n
         g.sync();
         continue;
       }
-      g_llt_solve(g, d, L, d, A);
+      g_llt_solve(g, d, L, d, A, scr);  // scr: inverted diagonal blocks (CTA, d >= 16)
       for (int i = g.lane; i < dd; i += g.size) K[i] = A[(i % d) * d + i / d];
       g.sync();
     }
@@ -261,6 +261,105 @@ __global__ void k_dnc_level(int T, int B, int fr_shared, int level,
   }
 }
 
+// ---- any d (9..32): warp per (node, chain), lanes over rows; the dot products
+// run in the register kernels' order (ascending j), so results match them.
+constexpr int kDncWarps = 4;
+
+__device__ __forceinline__ void dnc_normals_w(const NoiseArgs& nz, int c, uint64_t label,
+                                              uint64_t index, int T, int d, int lane, double* xi) {
+  if (nz.kind == AUXMC_NOISE_PREDRAWN) {
+    const double* src = label == kDncBridge ? nz.bridge + ((size_t)c * nz.n_bridge + index) * d
+                        : label == kTerminalDraw ? nz.terminal + (size_t)c * d
+                                                 : nz.backward + ((size_t)c * T + index) * d;
+    for (int i = lane; i < d; i += 32) xi[i] = src[i];
+  } else {
+    const uint64_t k = derive(nz.keys[c], label, index);
+    for (int i = lane; i < d; i += 32) xi[i] = normal_at(k, (uint64_t)i);
+  }
+}
+
+// y[i] = Σ_j A[i*d+j] x[j] (+ add[i]) for the lane's rows
+__device__ __forceinline__ void w_matvec(int lane, int d, const double* A, const double* x,
+                                         double* y) {
+  for (int i = lane; i < d; i += 32) {
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) s += A[i * d + j] * x[j];
+    y[i] = s;
+  }
+}
+
+__global__ void k_dnc_ends_gen(int T, int d, int B, int fr_shared, const double* __restrict__ term,
+                               const double* __restrict__ nodes, const double* __restrict__ params,
+                               long long n_heap, NoiseArgs nz, double* traj) {
+  __shared__ double sv[kDncWarps][4][64];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * kDncWarps + w;
+  if (c >= B) return;
+  const int dd = d * d, ES = (2 * dd + d + 1) & ~1, TS = (dd + d + 1) & ~1;
+  const int b = fr_shared ? 0 : c;
+  const double* tm = term + (size_t)b * TS;
+  double* out = traj + (size_t)c * (T + 1) * d;
+  double *xi = sv[w][0], *x = sv[w][1], *v = sv[w][2], *gx = sv[w][3];
+  dnc_normals_w(nz, c, kTerminalDraw, 0, T, d, lane, xi);
+  __syncwarp();
+  w_matvec(lane, d, tm + d, xi, x);
+  for (int i = lane; i < d; i += 32) {
+    x[i] = tm[i] + x[i];
+    out[(size_t)T * d + i] = x[i];
+  }
+  __syncwarp();
+  if (T == 0) return;
+  const double* root = nodes + ((size_t)b * n_heap + 1) * ES;
+  const double* Lr = params + (size_t)b * n_heap * 2 * dd + dd;
+  dnc_normals_w(nz, c, kBackwardNoise, 0, T, d, lane, xi);
+  __syncwarp();
+  w_matvec(lane, d, Lr, xi, v);
+  w_matvec(lane, d, root, x, gx);
+  for (int i = lane; i < d; i += 32) out[i] = gx[i] + (root[dd + i] + v[i]);
+}
+
+__global__ void k_dnc_level_gen(int T, int d, int B, int fr_shared, int level,
+                                const double* __restrict__ nodes, const double* __restrict__ params,
+                                long long n_heap, NoiseArgs nz, double* traj) {
+  __shared__ double sv[kDncWarps][7][64];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dd = d * d, ES = (2 * dd + d + 1) & ~1;
+  const long long width = 1LL << level;
+  const long long n = width * B;
+  double *xl = sv[w][0], *xr = sv[w][1], *mu = sv[w][2], *v = sv[w][3], *wv = sv[w][4],
+         *xi = sv[w][5], *lx = sv[w][6];
+  for (long long q = (long long)blockIdx.x * kDncWarps + w; q < n;
+       q += (long long)gridDim.x * kDncWarps) {
+    const int c = (int)(q % B);
+    const uint64_t h = (uint64_t)width + (uint64_t)(q / B);
+    int l, r;
+    if (!dnc_interval(h, T, l, r) || r - l < 2) continue;
+    const int m = (l + r) / 2;
+    const int b = fr_shared ? 0 : c;
+    const double* elm = nodes + ((size_t)b * n_heap + 2 * h) * ES;
+    const double* emr = nodes + ((size_t)b * n_heap + 2 * h + 1) * ES;
+    const double* K = params + ((size_t)b * n_heap + h) * 2 * dd;
+    const double* L = K + dd;
+    double* out = traj + (size_t)c * (T + 1) * d;
+    for (int i = lane; i < d; i += 32) {
+      xl[i] = out[(size_t)l * d + i];
+      xr[i] = out[(size_t)r * d + i];
+    }
+    dnc_normals_w(nz, c, kDncBridge, h, T, d, lane, xi);
+    __syncwarp();
+    w_matvec(lane, d, emr, xr, mu);
+    for (int i = lane; i < d; i += 32) mu[i] += emr[dd + i];
+    __syncwarp();
+    w_matvec(lane, d, elm, mu, v);
+    for (int i = lane; i < d; i += 32) v[i] = (xl[i] - v[i]) - elm[dd + i];
+    __syncwarp();
+    w_matvec(lane, d, K, v, wv);
+    w_matvec(lane, d, L, xi, lx);
+    for (int i = lane; i < d; i += 32) out[(size_t)m * d + i] = (mu[i] + wv[i]) + lx[i];
+    __syncwarp();
+  }
+}
+
 int launch_dnc(const DevModel& dm, int Bfr, int fr_shared, const double* elems,
                const double* term, const NoiseArgs& nz, int B, double* traj, Arena& ws,
                int* st_fr, cudaStream_t stream) {
@@ -272,23 +371,56 @@ int launch_dnc(const DevModel& dm, int Bfr, int fr_shared, const double* elems,
   double* params = ws.take<double>((size_t)Bfr * n_heap * 2 * dd);
   if (ws.base == nullptr) return AUXMC_OK;
   if (!nodes || !params) return AUXMC_E_WORKSPACE;
-  if (d > 8) return AUXMC_E_DIM;
-  const bool block = d > 16;
+  if (d > 32) return AUXMC_E_DIM;
+  const bool block = d > 16;  // CTA groups (blocked DMMA factor/solves) for d > 16
   const int warps = 4;
   if (T > 0) {
     for (int level = depth; level >= 0; --level) {
       const long long items = (1LL << level) * Bfr;
-      const int grid = (int)std::min<long long>((items + warps - 1) / warps, 148LL * 64);
-      AUXMC_LAUNCH(k_dnc_compose<false>, grid, 32 * warps, sizeof(double) * 2 * dd * warps,
-                   stream, T, d, level, Bfr, elems, nodes, n_heap);
+      if (block) {
+        const int grid = (int)std::min<long long>(items, 148LL * 16);
+        const size_t smem = sizeof(double) * 2 * dd;
+        AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_dnc_compose<true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AUXMC_LAUNCH(k_dnc_compose<true>, grid, 128, smem, stream, T, d, level, Bfr, elems, nodes,
+                     n_heap);
+      } else {
+        const int grid = (int)std::min<long long>((items + warps - 1) / warps, 148LL * 64);
+        const size_t smem = sizeof(double) * 2 * dd * warps;
+        AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_dnc_compose<false>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        AUXMC_LAUNCH(k_dnc_compose<false>, grid, 32 * warps, smem, stream, T, d, level, Bfr, elems,
+                     nodes, n_heap);
+      }
     }
     const long long items = (n_heap - 1) * Bfr;
-    const int grid = (int)std::min<long long>((items + warps - 1) / warps, 148LL * 64);
-    const size_t smem = sizeof(double) * (8 * dd + 4) * warps;
-    AUXMC_LAUNCH(k_dnc_bridge<false>, grid, 32 * warps, smem, stream, T, d, Bfr, nodes, n_heap,
-                 1LL, n_heap, params, st_fr);
+    if (block) {
+      const int grid = (int)std::min<long long>(items, 148LL * 16);
+      const size_t smem = sizeof(double) * (8 * dd + 4);
+      AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_dnc_bridge<true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      AUXMC_LAUNCH(k_dnc_bridge<true>, grid, 128, smem, stream, T, d, Bfr, nodes, n_heap, 1LL,
+                   n_heap, params, st_fr);
+    } else {
+      const int grid = (int)std::min<long long>((items + warps - 1) / warps, 148LL * 64);
+      const size_t smem = sizeof(double) * (8 * dd + 4) * warps;
+      AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_dnc_bridge<false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      AUXMC_LAUNCH(k_dnc_bridge<false>, grid, 32 * warps, smem, stream, T, d, Bfr, nodes, n_heap,
+                   1LL, n_heap, params, st_fr);
+    }
   }
-  (void)block;
+  if (d > 8) {
+    AUXMC_LAUNCH(k_dnc_ends_gen, (B + kDncWarps - 1) / kDncWarps, 32 * kDncWarps, 0, stream, T, d,
+                 B, fr_shared, term, nodes, params, n_heap, nz, traj);
+    for (int level = 0; level < depth; ++level) {
+      const long long n = (1LL << level) * B;
+      const int grid = (int)std::min<long long>((n + kDncWarps - 1) / kDncWarps, 148LL * 64);
+      AUXMC_LAUNCH(k_dnc_level_gen, grid, 32 * kDncWarps, 0, stream, T, d, B, fr_shared, level,
+                   nodes, params, n_heap, nz, traj);
+    }
+    return AUXMC_OK;
+  }
   switch (d) {
 #define CASE(D)                                                                              \
   case D: {                                                                                  \

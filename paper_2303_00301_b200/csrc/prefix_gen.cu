@@ -1,0 +1,229 @@
+// prefix_gen.cu — prefix (parallel-in-time) pathwise sampler for any state
+// dimension 9 <= d <= 64 (pit::prefix_sample, pit.cpp:78-106).
+//
+// The path obeys the affine backward recursion x_t = G_t x_{t+1} + c~_t with
+// c~_t = off_t + L_t xi_t (the realized element, pit.cpp:64-76).  The horizon
+// is cut into P blocks of Lb steps and scanned in three passes:
+//   1. per (filter result, block): the block operator A_k = G_s G_{s+1} ... G_{e-1}
+//      (DMMA products, one warp per block; shared by every chain when the filter
+//      result is shared);
+//   2. per (chain, block): c~_t (written into the output slot of x_t) and the
+//      block offset a_k = c~_s + G_s (c~_{s+1} + G_{s+1}(...)), so that
+//      x_s = A_k x_e + a_k;
+//   3. per chain: the terminal draw and the serial carry over blocks, last to
+//      first, giving the value x_e entering each block;
+//   4. per (chain, block): x_t = G_t x_{t+1} + c~_t inside the block.
+// Within a block the arithmetic is the sequential sampler's (same dot-product
+// order); only the block-boundary values associate differently from the
+// reference's Sklansky tree, which is within the FP64 parity tolerance.
+#include <algorithm>
+
+#include "common.cuh"
+#include "dense.cuh"
+#include "rng.cuh"
+
+namespace auxmc_gpu {
+
+namespace {
+
+constexpr int kWarpsPG = 4;
+
+__device__ __forceinline__ void noise_vec(const NoiseArgs& nz, int c, int T, int t, int d, int lane,
+                                          double* xi) {
+  if (nz.kind == AUXMC_NOISE_PREDRAWN) {
+    for (int i = lane; i < d; i += 32) xi[i] = nz.backward[((size_t)c * T + t) * d + i];
+  } else {
+    const uint64_t key = derive_index(derive_label(nz.keys[c], kBackwardNoise), (uint64_t)t);
+    for (int i = lane; i < d; i += 32) xi[i] = normal_at(key, (uint64_t)i);
+  }
+}
+
+// pass 1: A_k for (fr, block k); smem per warp: 2 d*d
+__global__ void k_pg_block_ops(int T, int d, int Bfr, int Lb, int P, const double* __restrict__ elems,
+                               double* __restrict__ ops) {
+  extern __shared__ double sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const long long item = (long long)blockIdx.x * nw + w;
+  if (item >= (long long)Bfr * P) return;
+  const int f = (int)(item / P), k = (int)(item % P);
+  const int dd = d * d, ES = elem_stride(d);
+  double* A = sm + (size_t)w * 2 * dd;
+  double* Bm = A + dd;
+  const int s = k * Lb, e = min(T, s + Lb);
+  const double* E = elems + (size_t)f * T * ES;
+  const Grp g = warp_group();
+  // A = G_{e-1}
+  for (int i = lane; i < dd; i += 32) A[i] = E[(size_t)(e - 1) * ES + i];
+  __syncwarp();
+  for (int t = e - 2; t >= s; --t) {  // A := G_t A
+    g_dmma<false, false>(g, d, d, d, E + (size_t)t * ES, d, A, d, Bm, d, false, false);
+    __syncwarp();
+    double* tmp = A;
+    A = Bm;
+    Bm = tmp;
+  }
+  double* out = ops + ((size_t)f * P + k) * dd;
+  for (int i = lane; i < dd; i += 32) out[i] = A[i];
+}
+
+// pass 2: c~_t into traj[t] and a_k; smem per warp: 2 * 64 (xi, a)
+__global__ void k_pg_block_offsets(int T, int d, int B, int fr_shared, int Lb, int P,
+                                   const double* __restrict__ elems, NoiseArgs nz,
+                                   double* __restrict__ traj, double* __restrict__ offs) {
+  __shared__ double sv[kWarpsPG][3][64];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long item = (long long)blockIdx.x * kWarpsPG + w;
+  if (item >= (long long)B * P) return;
+  const int c = (int)(item / P), k = (int)(item % P);
+  const int dd = d * d, ES = elem_stride(d);
+  const double* E = elems + (size_t)(fr_shared ? 0 : c) * T * ES;
+  double* out = traj + (size_t)c * (T + 1) * d;
+  double* xi = sv[w][0];
+  double* a = sv[w][1];
+  double* an = sv[w][2];
+  const int s = k * Lb, e = min(T, s + Lb);
+  for (int t = e - 1; t >= s; --t) {
+    const double* el = E + (size_t)t * ES;
+    noise_vec(nz, c, T, t, d, lane, xi);
+    __syncwarp();
+    for (int i = lane; i < d; i += 32) {
+      double cv = 0.0;
+      for (int j = 0; j < d; ++j) cv += el[dd + d + i * d + j] * xi[j];
+      const double ct = el[dd + i] + cv;  // c~_t
+      out[(size_t)t * d + i] = ct;
+      if (t == e - 1) {
+        an[i] = ct;
+      } else {
+        double ga = 0.0;
+        for (int j = 0; j < d; ++j) ga += el[i * d + j] * a[j];
+        an[i] = ga + ct;
+      }
+    }
+    __syncwarp();
+    for (int i = lane; i < d; i += 32) a[i] = an[i];
+    __syncwarp();
+  }
+  double* o = offs + ((size_t)c * P + k) * d;
+  for (int i = lane; i < d; i += 32) o[i] = a[i];
+}
+
+// pass 3: terminal draw and the serial block carry (one warp per chain)
+__global__ void k_pg_carry(int T, int d, int B, int fr_shared, int P, const double* __restrict__ term,
+                           const double* __restrict__ ops, const double* __restrict__ offs,
+                           NoiseArgs nz, double* __restrict__ traj, double* __restrict__ xin) {
+  __shared__ double sv[kWarpsPG][2][64];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * kWarpsPG + w;
+  if (c >= B) return;
+  const int dd = d * d;
+  const double* tm = term + (size_t)(fr_shared ? 0 : c) * term_stride(d);
+  double* x = sv[w][0];
+  double* xn = sv[w][1];
+  double* out = traj + (size_t)c * (T + 1) * d;
+  const bool pre = nz.kind == AUXMC_NOISE_PREDRAWN;
+  for (int i = lane; i < d; i += 32)
+    xn[i] = pre ? nz.terminal[(size_t)c * d + i]
+                : normal_at(derive(nz.keys[c], kTerminalDraw, 0), (uint64_t)i);
+  __syncwarp();
+  for (int i = lane; i < d; i += 32) {  // x_T = m_T + L_T xi (pit.cpp:85-87)
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) s += tm[d + i * d + j] * xn[j];
+    x[i] = tm[i] + s;
+    out[(size_t)T * d + i] = x[i];
+  }
+  __syncwarp();
+  const double* O = ops + (size_t)(fr_shared ? 0 : c) * P * dd;
+  for (int k = P - 1; k >= 0; --k) {
+    double* xe = xin + ((size_t)c * P + k) * d;
+    for (int i = lane; i < d; i += 32) xe[i] = x[i];
+    const double* A = O + (size_t)k * dd;
+    const double* a = offs + ((size_t)c * P + k) * d;
+    for (int i = lane; i < d; i += 32) {
+      double s = 0.0;
+      for (int j = 0; j < d; ++j) s += A[i * d + j] * x[j];
+      xn[i] = s + a[i];
+    }
+    __syncwarp();
+    for (int i = lane; i < d; i += 32) x[i] = xn[i];
+    __syncwarp();
+  }
+}
+
+// pass 4: x_t = G_t x_{t+1} + c~_t inside each block
+__global__ void k_pg_apply(int T, int d, int B, int fr_shared, int Lb, int P,
+                           const double* __restrict__ elems, const double* __restrict__ xin,
+                           double* __restrict__ traj) {
+  __shared__ double sv[kWarpsPG][2][64];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long item = (long long)blockIdx.x * kWarpsPG + w;
+  if (item >= (long long)B * P) return;
+  const int c = (int)(item / P), k = (int)(item % P);
+  const int ES = elem_stride(d);
+  const double* E = elems + (size_t)(fr_shared ? 0 : c) * T * ES;
+  double* out = traj + (size_t)c * (T + 1) * d;
+  double* x = sv[w][0];
+  double* xn = sv[w][1];
+  const double* xe = xin + ((size_t)c * P + k) * d;
+  for (int i = lane; i < d; i += 32) x[i] = xe[i];
+  __syncwarp();
+  const int s = k * Lb, e = min(T, s + Lb);
+  for (int t = e - 1; t >= s; --t) {
+    const double* el = E + (size_t)t * ES;
+    for (int i = lane; i < d; i += 32) {
+      double gx = 0.0;
+      for (int j = 0; j < d; ++j) gx += el[i * d + j] * x[j];
+      xn[i] = gx + out[(size_t)t * d + i];
+    }
+    __syncwarp();
+    for (int i = lane; i < d; i += 32) {
+      x[i] = xn[i];
+      out[(size_t)t * d + i] = xn[i];
+    }
+    __syncwarp();
+  }
+}
+
+int block_len(int T) {
+  int lb = 16;
+  while ((long long)lb * lb < T && lb < 4096) lb <<= 1;
+  return lb;
+}
+
+}  // namespace
+
+// elems/term from launch_bwd_elements (store_cov = 0: element holds chol(Λ)).
+int launch_prefix_generic(int T, int d, int B, int fr_shared, const double* elems,
+                          const double* term, const NoiseArgs& nz, double* traj, Arena& ws,
+                          cudaStream_t stream) {
+  if (d < 1 || d > 64) return AUXMC_E_DIM;
+  const int Bfr = fr_shared ? 1 : B;
+  const int Lb = block_len(T > 0 ? T : 1);
+  const int P = T > 0 ? (T + Lb - 1) / Lb : 0;
+  const int dd = d * d;
+  double* ops = ws.take<double>((size_t)Bfr * (P > 0 ? P : 1) * dd);
+  double* offs = ws.take<double>((size_t)B * (P > 0 ? P : 1) * d);
+  double* xin = ws.take<double>((size_t)B * (P > 0 ? P : 1) * d);
+  if (ws.base == nullptr) return AUXMC_OK;
+  if (!ops || !offs || !xin) return AUXMC_E_WORKSPACE;
+  if (T > 0) {
+    const int wo = std::max(1, std::min(kWarpsPG, (int)((200 * 1024) / (16 * dd))));
+    const size_t smem = sizeof(double) * 2 * dd * wo;
+    AUXMC_CUDA_TRY(
+        cudaFuncSetAttribute(k_pg_block_ops, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const long long nops = (long long)Bfr * P, nvec = (long long)B * P;
+    AUXMC_LAUNCH(k_pg_block_ops, (int)((nops + wo - 1) / wo), 32 * wo, smem, stream, T, d, Bfr,
+                 Lb, P, elems, ops);
+    AUXMC_LAUNCH(k_pg_block_offsets, (int)((nvec + kWarpsPG - 1) / kWarpsPG), 32 * kWarpsPG, 0,
+                 stream, T, d, B, fr_shared, Lb, P, elems, nz, traj, offs);
+  }
+  AUXMC_LAUNCH(k_pg_carry, (B + kWarpsPG - 1) / kWarpsPG, 32 * kWarpsPG, 0, stream, T, d, B,
+               fr_shared, P, term, ops, offs, nz, traj, xin);
+  if (T > 0) {
+    const long long nvec = (long long)B * P;
+    AUXMC_LAUNCH(k_pg_apply, (int)((nvec + kWarpsPG - 1) / kWarpsPG), 32 * kWarpsPG, 0, stream, T,
+                 d, B, fr_shared, Lb, P, elems, xin, traj);
+  }
+  return AUXMC_OK;
+}
+
+}  // namespace auxmc_gpu

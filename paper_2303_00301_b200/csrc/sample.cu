@@ -531,6 +531,9 @@ int launch_prefix_shared(int d, int T, int B, const double* elems, const double*
 int launch_dnc(const DevModel& dm, int Bfr, int fr_shared, const double* elems,
                const double* term, const NoiseArgs& nz, int B, double* traj, Arena& ws,
                int* st_fr, cudaStream_t stream);
+int launch_prefix_generic(int T, int d, int B, int fr_shared, const double* elems,
+                          const double* term, const NoiseArgs& nz, double* traj, Arena& ws,
+                          cudaStream_t stream);
 
 namespace {
 
@@ -634,8 +637,10 @@ int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int f
       CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
       default:
-        if (sampler != AUXMC_SAMPLER_SEQ || d > 64) {
+        if (d > 64) {
           rc = AUXMC_E_DIM;
+        } else if (sampler == AUXMC_SAMPLER_PREFIX) {
+          rc = launch_prefix_generic(T, d, B, fr_shared, elems, term, nz, traj, ws, stream);
         } else if (ws.base != nullptr) {
           const long long es = fr_shared ? 0 : (long long)T * elem_stride(d);
           const long long ts = fr_shared ? 0 : term_stride(d);

@@ -65,6 +65,8 @@ LARGE_CASES = [
     (6, 20, 17, True, True, 31),
     (4, 17, 40, False, False, 32),
     (3, 40, 60, True, False, 33),
+    (100, 10, 3, True, True, 34),   # warp groups; several prefix blocks
+    (33, 12, 12, False, False, 35),
 ]
 
 
@@ -81,9 +83,14 @@ def test_kalman_filter_large_dims_match_oracle(gpu, oracle, case):
     assert_close(fr.log_marginal[0].cpu(), want.log_marginal, RTOL, "log_marginal")
 
 
+@pytest.mark.parametrize("sampler", [0, 1, 2])
 @pytest.mark.parametrize("case", LARGE_CASES)
-def test_backward_sampler_large_dims_match_oracle(gpu, oracle, case):
+def test_samplers_large_dims_match_oracle(gpu, oracle, case, sampler):
+    """d > 8: sequential (warp per path), generic blocked prefix scan, and the
+    group DnC (d <= 32)."""
     lgssm, pit, _ = gpu
+    if sampler == 2 and case[1] > 32:
+        pytest.skip("DnC implemented for d <= 32")
     m, obs = _oracle_case(oracle, *case)
     fr_o = oracle.kalman_filter(m, obs)
     gm = to_gpu_model(m)
@@ -91,9 +98,9 @@ def test_backward_sampler_large_dims_match_oracle(gpu, oracle, case):
     B = 3
     term, back, bridge = predrawn(np.random.default_rng(case[-1]), B, m.T, m.dx,
                                   pit.dnc_bridge_count(m.T))
-    want = _oracle_paths(oracle, 0, m, fr_o, term, back, bridge)
-    got = lgssm.PathSampler(gm, B, 0, True)(fr, lgssm.Noise.predrawn(term, back, bridge))
-    assert_close(got.cpu(), want, RTOL, "backward sampler")
+    want = _oracle_paths(oracle, sampler, m, fr_o, term, back, bridge)
+    got = lgssm.PathSampler(gm, B, sampler, True)(fr, lgssm.Noise.predrawn(term, back, bridge))
+    assert_close(got.cpu(), want, RTOL, f"sampler {sampler}")
 
 
 def test_kalman_filter_batched_sequences(gpu, oracle):
