@@ -671,9 +671,12 @@ static int run_pf(const DevModel& dm, const double* obs, int B, auxmc_filter_res
   return AUXMC_OK;
 }
 
+int dispatch_pf_generic(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
+                        int* status, Arena& ws, cudaStream_t s);
+
 static int dispatch_pf(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
                        int* status, Arena& ws, cudaStream_t s) {
-  if (dm.dy > kMaxDY) return AUXMC_E_DIM;
+  if (dm.dy > kMaxDY || dm.dx > 6) return dispatch_pf_generic(dm, obs, B, out, status, ws, s);
   switch (dm.dx) {
     case 1: return run_pf<1>(dm, obs, B, out, status, ws, s);
     case 2: return run_pf<2>(dm, obs, B, out, status, ws, s);

@@ -1,0 +1,555 @@
+// pfilter_gen.cu — pit::parallel_filter (pit.cpp:117-188) for state dims
+// 7 <= dx <= 32 (or observation rows > 8): the same blocked scan as pfilter.cu
+// (S1 block reductions, S2 serial carries, S3 inclusive application, then the
+// recovery pass), with every element build / combine / recovery done by a
+// cooperative group on shared memory — a warp when dx, dy <= 16, a 128-thread
+// CTA otherwise (DMMA products and blocked factorizations from group.cuh).
+// Results follow the register kernels' operation order where the group
+// routines do (scalar products, row-sequential LU solves); DMMA products and
+// blocked Cholesky associate differently, within the FP64 parity tolerance.
+#include <algorithm>
+
+#include "common.cuh"
+#include "dense.cuh"
+
+namespace auxmc_gpu {
+
+namespace {
+
+__host__ __device__ inline int fe_size_g(int d) { return 3 * d * d + 2 * d; }
+
+// ---------------------------------------------------------------- partial-pivot LU
+// Row-pivoted LU in place (Eigen PartialPivLU: the first row of largest |.|
+// in the column is the pivot, zero pivots skip the elimination).  perm in
+// shared memory; idx: 1 int of scratch.
+__device__ void g_lu_factor(const Grp& g, int d, double* M, int* perm, int* idx) {
+  for (int i = g.lane; i < d; i += g.size) perm[i] = i;
+  g.sync();
+  for (int k = 0; k < d; ++k) {
+    if (g.lane < 32) {  // pivot search in warp 0: first max of |M[i][k]|, i >= k
+      double best = -1.0;
+      int bi = d;
+      for (int i = k + g.lane; i < d; i += 32) {
+        const double v = fabs(M[i * d + k]);
+        if (v > best) {
+          best = v;
+          bi = i;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (g.lane == 0) *idx = bi < d ? bi : k;  // all-NaN column: keep row k
+    }
+    g.sync();
+    const int p = *idx;
+    if (p != k) {
+      for (int j = g.lane; j < d; j += g.size) {
+        const double t = M[k * d + j];
+        M[k * d + j] = M[p * d + j];
+        M[p * d + j] = t;
+      }
+      if (g.lane == 0) {
+        const int t = perm[k];
+        perm[k] = perm[p];
+        perm[p] = t;
+      }
+    }
+    g.sync();
+    const double piv = M[k * d + k];
+    if (piv != 0.0) {
+      for (int i = k + 1 + g.lane; i < d; i += g.size) M[i * d + k] = M[i * d + k] / piv;
+      g.sync();
+      for (int i = k + 1 + g.ty(); i < d; i += g.ny()) {
+        const double f = M[i * d + k];
+        for (int j = k + 1 + g.tx(); j < d; j += 16) M[i * d + j] -= f * M[k * d + j];
+      }
+    }
+    g.sync();
+  }
+}
+
+// X (d×r) = M^{-1} B (B row-major d×r, may not alias X); lanes over columns
+__device__ void g_lu_solve(const Grp& g, int d, const double* LU, const int* perm, int r,
+                           const double* B, double* X) {
+  for (int c = g.lane; c < r; c += g.size) {
+    for (int i = 0; i < d; ++i) {
+      double s = B[perm[i] * r + c];
+      for (int j = 0; j < i; ++j) s -= LU[i * d + j] * X[j * r + c];
+      X[i * r + c] = s;
+    }
+    for (int i = d - 1; i >= 0; --i) {
+      double s = X[i * r + c];
+      for (int j = i + 1; j < d; ++j) s -= LU[i * d + j] * X[j * r + c];
+      X[i * r + c] = s / LU[i * d + i];
+    }
+  }
+}
+
+// o = combine(u, v) (pit.cpp:36-51); scratch: 5 dd + 2 d doubles, 2 d + 1 ints
+struct CombScratch {
+  double *M1, *M2, *S, *T1, *T2, *t, *w;
+  int *p1, *p2, *idx;
+};
+
+__device__ void g_combine(const Grp& g, int d, const double* u, const double* v, double* o,
+                          const CombScratch& s) {
+  const int dd = d * d;
+  const double *uA = u, *ub = u + dd, *uC = u + dd + d, *ueta = u + 2 * dd + d,
+               *uJ = u + 2 * dd + 2 * d;
+  const double *vA = v, *vb = v + dd, *vC = v + dd + d, *veta = v + 2 * dd + d,
+               *vJ = v + 2 * dd + 2 * d;
+  double *oA = o, *ob = o + dd, *oC = o + dd + d, *oeta = o + 2 * dd + d, *oJ = o + 2 * dd + 2 * d;
+  g_mm(g, d, d, d, uC, vJ, s.M1);
+  g_mm(g, d, d, d, vJ, uC, s.M2);
+  g.sync();
+  for (int i = g.lane; i < d; i += g.size) {
+    s.M1[i * d + i] += 1.0;
+    s.M2[i * d + i] += 1.0;
+  }
+  g.sync();
+  g_lu_factor(g, d, s.M1, s.p1, s.idx);
+  g_lu_factor(g, d, s.M2, s.p2, s.idx);
+  // A = vA M1^{-1} uA
+  g_lu_solve(g, d, s.M1, s.p1, d, uA, s.S);
+  g.sync();
+  g_mm(g, d, d, d, vA, s.S, oA);
+  // t = uC veta + ub
+  for (int i = g.lane; i < d; i += g.size) {
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) acc += uC[i * d + k] * veta[k];
+    s.t[i] = acc + ub[i];
+  }
+  g.sync();
+  g_lu_solve(g, d, s.M1, s.p1, 1, s.t, s.w);
+  g.sync();
+  for (int i = g.lane; i < d; i += g.size) {
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) acc += vA[i * d + k] * s.w[k];
+    ob[i] = acc + vb[i];
+  }
+  // C = symm(vA M1^{-1} uC vA^T + vC)
+  g_lu_solve(g, d, s.M1, s.p1, d, uC, s.S);
+  g.sync();
+  g_mm(g, d, d, d, vA, s.S, s.T1);
+  g.sync();
+  g_mm_nt(g, d, d, d, s.T1, vA, s.T2, vC);
+  g.sync();
+  for (int i = g.ty(); i < d; i += g.ny())
+    for (int j = g.tx(); j < d; j += 16) oC[i * d + j] = 0.5 * (s.T2[i * d + j] + s.T2[j * d + i]);
+  // eta = uA^T M2^{-1} (veta - vJ ub) + ueta
+  for (int i = g.lane; i < d; i += g.size) {
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) acc += vJ[i * d + k] * ub[k];
+    s.t[i] = veta[i] - acc;
+  }
+  g.sync();
+  g_lu_solve(g, d, s.M2, s.p2, 1, s.t, s.w);
+  g.sync();
+  for (int i = g.lane; i < d; i += g.size) {
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) acc += uA[k * d + i] * s.w[k];
+    oeta[i] = acc + ueta[i];
+  }
+  // J = symm(uA^T M2^{-1} vJ uA + uJ)
+  g_lu_solve(g, d, s.M2, s.p2, d, vJ, s.S);
+  g.sync();
+  g_mm_tn(g, d, d, d, uA, s.S, s.T1);
+  g.sync();
+  g_mm(g, d, d, d, s.T1, uA, s.T2, uJ);
+  g.sync();
+  for (int i = g.ty(); i < d; i += g.ny())
+    for (int j = g.tx(); j < d; j += 16) oJ[i * d + j] = 0.5 * (s.T2[i * d + j] + s.T2[j * d + i]);
+  g.sync();
+}
+
+__host__ __device__ inline int comb_doubles(int d) { return 5 * d * d + 2 * d; }
+__host__ __device__ inline int comb_ints(int d) { return 2 * d + 2; }
+
+__device__ CombScratch comb_scratch(int d, double* base, int* ibase) {
+  CombScratch s;
+  const int dd = d * d;
+  s.M1 = base;
+  s.M2 = s.M1 + dd;
+  s.S = s.M2 + dd;
+  s.T1 = s.S + dd;
+  s.T2 = s.T1 + dd;
+  s.t = s.T2 + dd;
+  s.w = s.t + d;
+  s.p1 = ibase;
+  s.p2 = ibase + d;
+  s.idx = ibase + 2 * d;
+  return s;
+}
+
+struct GrpCfg {
+  bool block;
+  int groups;  // per CTA
+  int threads;
+};
+
+__host__ __device__ inline GrpCfg grp_cfg(int dx, int dy) {
+  if (dx <= 16 && dy <= 16) return GrpCfg{false, 4, 128};
+  return GrpCfg{true, 1, 128};
+}
+
+// ---------------------------------------------------------------- element build
+// per (b, t); smem per group: f, q, a, t1, t2 (dd), hq, X1, X2, gr (dy*dx), s, L, scr (dy^2),
+// innov, hv, bd (vectors)
+__host__ __device__ inline int elem_smem(int d, int dy) {
+  const int W = d > dy ? d : dy;
+  return 5 * d * d + 4 * dy * d + 4 * dy * dy + 3 * W + 8;
+}
+
+template <bool BLOCK>
+__global__ void k_pfg_elements(DevModel m, const double* __restrict__ obs, int B, double* el,
+                               int* status) {
+  extern __shared__ double smem[];
+  const int T = m.T, d = m.dx, dy = m.dy, dd = d * d, ES = fe_size_g(d);
+  const int W = d > dy ? d : dy;
+  const Grp g = BLOCK ? block_group() : warp_group();
+  const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
+  double* sm = smem + (size_t)gid * elem_smem(d, dy);
+  double *f = sm, *qm = f + dd, *a = qm + dd, *t1 = a + dd, *t2 = t1 + dd;
+  double *hq = t2 + dd, *X1 = hq + dy * d, *X2 = X1 + dy * d, *gr = X2 + dy * d;
+  double *s = gr + dy * d, *L = s + dy * dy, *scr = L + dy * dy, *fs = scr + dy * dy;
+  double *innov = fs + dy * dy, *hv = innov + W, *bd = hv + W;
+  double* red = bd + W;
+  int* flag = reinterpret_cast<int*>(red + 2);
+  const long long n = (long long)B * (T + 1);
+  for (long long q = (long long)blockIdx.x * gpb + gid; q < n; q += (long long)gridDim.x * gpb) {
+    const int b = (int)(q / (T + 1)), t = (int)(q % (T + 1));
+    double* e = el + (size_t)q * ES;
+    double *eA = e, *eb = e + dd, *eC = e + dd + d, *eeta = e + 2 * dd + d, *eJ = e + 2 * dd + 2 * d;
+    const double* Qs = t == 0 ? m.P0 : m.Qt(t - 1, b);
+    for (int i = g.ty(); i < d; i += g.ny())
+      for (int j = g.tx(); j < d; j += 16) {
+        f[i * d + j] = t == 0 ? (i == j ? 1.0 : 0.0) : m.Ft(t - 1, b)[i * d + j];
+        qm[i * d + j] = 0.5 * (Qs[i * d + j] + Qs[j * d + i]);  // Model ctor symmetrization
+      }
+    for (int i = g.lane; i < d; i += g.size) bd[i] = t == 0 ? m.m0[i] : m.bt(t - 1, b)[i];
+    g.sync();
+    int st = 0;
+    if (dy > 0 && m.observed(t)) {
+      const double* h = m.Ht(t, b);
+      const double* c = m.ct(t, b);
+      const double* R = m.Rt(t, b);
+      const double* y = obs + (size_t)q * dy;
+      for (int i = g.lane; i < dy; i += g.size) {
+        double acc = 0.0;
+        for (int j = 0; j < d; ++j) acc += h[i * d + j] * bd[j];
+        innov[i] = (y[i] - acc) - c[i];
+      }
+      g_mm(g, dy, d, d, h, qm, hq);
+      for (int i = g.ty(); i < dy; i += g.ny())
+        for (int j = g.tx(); j < dy; j += 16) scr[i * dy + j] = 0.5 * (R[i * dy + j] + R[j * dy + i]);
+      g.sync();
+      g_mm_nt(g, dy, d, dy, hq, h, s, scr);
+      g.sync();
+      g_symm(g, dy, s);
+      g.sync();
+      st = g_factor_psd(g, dy, s, L, fs, flag, red);  // fs: jitter matrix / inverted blocks
+      if (st == 0) {
+        g_copy(g, dy * d, hq, X1);
+        g_copy(g, dy * d, h, X2);
+        g.sync();
+        g_llt_solve(g, dy, L, d, X1, fs);  // gain = X1^T
+        g_llt_solve(g, dy, L, d, X2, fs);  // hs = X2^T
+        // a = I - gain h ; A = a f
+        g_mm_tn(g, d, dy, d, X1, h, a);
+        g.sync();
+        for (int i = g.ty(); i < d; i += g.ny())
+          for (int j = g.tx(); j < d; j += 16) a[i * d + j] = (i == j ? 1.0 : 0.0) - a[i * d + j];
+        g.sync();
+        g_mm(g, d, d, d, a, f, eA);
+        for (int i = g.lane; i < d; i += g.size) {
+          double acc = 0.0;
+          for (int k = 0; k < dy; ++k) acc += X1[k * d + i] * innov[k];
+          eb[i] = bd[i] + acc;
+        }
+        // C = symm(a q a^T + gain Rs gain^T)
+        g_mm(g, d, d, d, a, qm, t1);
+        g_mm_tn(g, d, dy, dy, X1, scr, gr);
+        g.sync();
+        g_mm_nt(g, d, d, d, t1, a, t2);
+        g.sync();
+        g_mm(g, d, dy, d, gr, X1, t1, t2);
+        g.sync();
+        for (int i = g.ty(); i < d; i += g.ny())
+          for (int j = g.tx(); j < d; j += 16) eC[i * d + j] = 0.5 * (t1[i * d + j] + t1[j * d + i]);
+        // eta = f^T (hs innov) ; J = symm(((f^T hs) h) f)
+        for (int i = g.lane; i < d; i += g.size) {
+          double acc = 0.0;
+          for (int k = 0; k < dy; ++k) acc += X2[k * d + i] * innov[k];
+          hv[i] = acc;
+        }
+        g.sync();
+        for (int i = g.lane; i < d; i += g.size) {
+          double acc = 0.0;
+          for (int k = 0; k < d; ++k) acc += f[k * d + i] * hv[k];
+          eeta[i] = acc;
+        }
+        g_mm(g, dy, d, d, X2, f, gr);  // (f^T hs)^T = X2 f  (dy×d)
+        g.sync();
+        g_mm_tn(g, d, dy, d, gr, h, t1);  // (f^T hs) h
+        g.sync();
+        g_mm(g, d, d, d, t1, f, t2);
+        g.sync();
+        for (int i = g.ty(); i < d; i += g.ny())
+          for (int j = g.tx(); j < d; j += 16) eJ[i * d + j] = 0.5 * (t2[i * d + j] + t2[j * d + i]);
+      }
+    } else {
+      for (int i = g.lane; i < dd; i += g.size) {
+        eA[i] = f[i];
+        eC[i] = qm[i];
+        eJ[i] = 0.0;
+      }
+      for (int i = g.lane; i < d; i += g.size) {
+        eb[i] = bd[i];
+        eeta[i] = 0.0;
+      }
+    }
+    g.sync();
+    if (t == 0)
+      for (int i = g.lane; i < dd; i += g.size) eA[i] = 0.0;
+    if (st && g.lane == 0 && status) atomicMax(status + b, st);
+    g.sync();
+  }
+}
+
+// ---------------------------------------------------------------- S1 / S2 / S3
+__host__ __device__ inline int scan_smem(int d) { return 3 * fe_size_g(d) + comb_doubles(d) + comb_ints(d); }
+
+template <bool BLOCK>
+__global__ void k_pfg_reduce(int T, int d, int B, int LB, const double* __restrict__ el, double* agg) {
+  extern __shared__ double smem[];
+  const int ES = fe_size_g(d);
+  const Grp g = BLOCK ? block_group() : warp_group();
+  const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
+  double* sm = smem + (size_t)gid * scan_smem(d);
+  double *acc = sm, *o = acc + ES, *tmpd = o + ES;
+  const CombScratch cs = comb_scratch(d, tmpd + ES, reinterpret_cast<int*>(tmpd + ES + comb_doubles(d)));
+  const int nblk = (T + 1 + LB - 1) / LB;
+  const long long n = (long long)B * nblk;
+  for (long long q = (long long)blockIdx.x * gpb + gid; q < n; q += (long long)gridDim.x * gpb) {
+    const int b = (int)(q / nblk), k = (int)(q % nblk);
+    const int lo = k * LB, hi = min(lo + LB, T + 1);
+    const double* base = el + (size_t)b * (T + 1) * ES;
+    g_copy(g, ES, base + (size_t)lo * ES, acc);
+    g.sync();
+    for (int t = lo + 1; t < hi; ++t) {
+      g_combine(g, d, acc, base + (size_t)t * ES, o, cs);
+      g_copy(g, ES, o, acc);
+      g.sync();
+    }
+    g_copy(g, ES, acc, agg + (size_t)q * ES);
+    g.sync();
+  }
+}
+
+template <bool BLOCK>
+__global__ void k_pfg_carry(int T, int d, int B, int LB, const double* __restrict__ agg, double* carry) {
+  extern __shared__ double smem[];
+  const int ES = fe_size_g(d);
+  const Grp g = BLOCK ? block_group() : warp_group();
+  const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
+  double* sm = smem + (size_t)gid * scan_smem(d);
+  double *acc = sm, *o = acc + ES, *tmpd = o + ES;
+  const CombScratch cs = comb_scratch(d, tmpd + ES, reinterpret_cast<int*>(tmpd + ES + comb_doubles(d)));
+  const int nblk = (T + 1 + LB - 1) / LB;
+  for (int b = blockIdx.x * gpb + gid; b < B; b += gridDim.x * gpb) {
+    g_copy(g, ES, agg + (size_t)b * nblk * ES, acc);
+    g.sync();
+    for (int k = 1; k < nblk; ++k) {
+      g_copy(g, ES, acc, carry + ((size_t)b * nblk + k) * ES);
+      g_combine(g, d, acc, agg + ((size_t)b * nblk + k) * ES, o, cs);
+      g_copy(g, ES, o, acc);
+      g.sync();
+    }
+  }
+}
+
+template <bool BLOCK>
+__global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restrict__ el,
+                            const double* __restrict__ carry, double* filt_mean, double* filt_cov) {
+  extern __shared__ double smem[];
+  const int ES = fe_size_g(d), dd = d * d;
+  const Grp g = BLOCK ? block_group() : warp_group();
+  const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
+  double* sm = smem + (size_t)gid * scan_smem(d);
+  double *acc = sm, *o = acc + ES, *cy = o + ES;
+  const CombScratch cs = comb_scratch(d, cy + ES, reinterpret_cast<int*>(cy + ES + comb_doubles(d)));
+  const int nblk = (T + 1 + LB - 1) / LB;
+  const long long n = (long long)B * nblk;
+  for (long long q = (long long)blockIdx.x * gpb + gid; q < n; q += (long long)gridDim.x * gpb) {
+    const int b = (int)(q / nblk), k = (int)(q % nblk);
+    const int lo = k * LB, hi = min(lo + LB, T + 1);
+    const double* base = el + (size_t)b * (T + 1) * ES;
+    if (k == 0) {
+      g_copy(g, ES, base + (size_t)lo * ES, acc);
+      g.sync();
+    } else {
+      g_copy(g, ES, carry + (size_t)q * ES, cy);
+      g.sync();
+      g_combine(g, d, cy, base + (size_t)lo * ES, acc, cs);
+    }
+    for (int t = lo;; ++t) {
+      for (int i = g.lane; i < d; i += g.size)
+        filt_mean[((size_t)b * (T + 1) + t) * d + i] = acc[dd + i];
+      for (int i = g.lane; i < dd; i += g.size)
+        filt_cov[((size_t)b * (T + 1) + t) * dd + i] = acc[dd + d + i];
+      if (t + 1 >= hi) break;
+      g_combine(g, d, acc, base + (size_t)(t + 1) * ES, o, cs);
+      g_copy(g, ES, o, acc);
+      g.sync();
+    }
+    g.sync();
+  }
+}
+
+// ---------------------------------------------------------------- recovery
+__host__ __device__ inline int rec_smem(int d, int dy) {
+  const int W = d > dy ? d : dy;
+  return 3 * d * d + dy * d + 3 * dy * dy + 2 * W + 8;
+}
+
+template <bool BLOCK>
+__global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
+                              const double* __restrict__ fm, const double* __restrict__ fc,
+                              double* pm, double* pc, double* terms, int* status) {
+  extern __shared__ double smem[];
+  const int T = m.T, d = m.dx, dy = m.dy, dd = d * d;
+  const int W = d > dy ? d : dy;
+  const Grp g = BLOCK ? block_group() : warp_group();
+  const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
+  double* sm = smem + (size_t)gid * rec_smem(d, dy);
+  double *P = sm, *t1 = P + dd, *qs = t1 + dd, *hp = qs + dd, *s = hp + dy * d, *L = s + dy * dy,
+         *scr = L + dy * dy;
+  double *mp = scr + dy * dy, *r = mp + W, *red = r + W;
+  int* flag = reinterpret_cast<int*>(red + 2);
+  const long long n = (long long)B * (T + 1);
+  for (long long q = (long long)blockIdx.x * gpb + gid; q < n; q += (long long)gridDim.x * gpb) {
+    const int b = (int)(q / (T + 1)), t = (int)(q % (T + 1));
+    if (t == 0) {
+      for (int i = g.lane; i < d; i += g.size) mp[i] = m.m0[i];
+      for (int i = g.ty(); i < d; i += g.ny())
+        for (int j = g.tx(); j < d; j += 16) P[i * d + j] = 0.5 * (m.P0[i * d + j] + m.P0[j * d + i]);
+      g.sync();
+    } else {
+      const double* F = m.Ft(t - 1, b);
+      const double* bb = m.bt(t - 1, b);
+      const double* Q = m.Qt(t - 1, b);
+      const double* x = fm + (size_t)(q - 1) * d;
+      const double* C = fc + (size_t)(q - 1) * dd;
+      for (int i = g.lane; i < d; i += g.size) {
+        double acc = 0.0;
+        for (int k = 0; k < d; ++k) acc += F[i * d + k] * x[k];
+        mp[i] = acc + bb[i];
+      }
+      g_mm(g, d, d, d, F, C, t1);
+      for (int i = g.ty(); i < d; i += g.ny())
+        for (int j = g.tx(); j < d; j += 16) qs[i * d + j] = 0.5 * (Q[i * d + j] + Q[j * d + i]);
+      g.sync();
+      g_mm_nt(g, d, d, d, t1, F, P, qs);
+      g.sync();
+      g_symm(g, d, P);
+      g.sync();
+    }
+    for (int i = g.lane; i < d; i += g.size) pm[(size_t)q * d + i] = mp[i];
+    for (int i = g.lane; i < dd; i += g.size) pc[(size_t)q * dd + i] = P[i];
+    double term = 0.0;
+    if (dy > 0 && m.observed(t)) {
+      const double* h = m.Ht(t, b);
+      const double* c = m.ct(t, b);
+      const double* R = m.Rt(t, b);
+      const double* y = obs + (size_t)q * dy;
+      for (int i = g.lane; i < dy; i += g.size) {
+        double acc = 0.0;
+        for (int k = 0; k < d; ++k) acc += h[i * d + k] * mp[k];
+        r[i] = acc + c[i];  // mean H m + c
+      }
+      g_mm(g, dy, d, d, h, P, hp);
+      g.sync();
+      g_mm_nt(g, dy, d, dy, hp, h, s, R);
+      g.sync();
+      g_symm(g, dy, s);
+      g.sync();
+      const int st = g_factor_psd(g, dy, s, L, scr, flag, red);
+      if (st) {
+        if (g.lane == 0 && status) atomicMax(status + b, st);
+      } else {
+        term = g_log_pdf_factored(g, dy, y, r, L, hp /* work */, red, scr);
+      }
+    }
+    if (g.lane == 0) terms[q] = term;
+    g.sync();
+  }
+}
+
+__global__ void k_pfg_sum(int T, int B, const double* terms, double* out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double s = 0.0;
+  for (int t = 0; t <= T; ++t) s += terms[(size_t)b * (T + 1) + t];
+  out[b] = s;
+}
+
+int pf_block_g(int T) {
+  int lb = 1;
+  while ((long long)lb * lb < T + 1) lb <<= 1;
+  return lb < 4 ? 4 : lb;
+}
+
+template <bool BLOCK>
+int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out, int* status,
+            Arena& ws, cudaStream_t s) {
+  const int T = dm.T, d = dm.dx, dy = dm.dy, LB = pf_block_g(T);
+  const int ES = fe_size_g(d);
+  const int nblk = (T + 1 + LB - 1) / LB;
+  double* el = ws.take<double>((size_t)B * (T + 1) * ES);
+  double* agg = ws.take<double>((size_t)B * nblk * ES);
+  double* carry = ws.take<double>((size_t)B * nblk * ES);
+  double* terms = ws.take<double>((size_t)B * (T + 1));
+  if (ws.base == nullptr) return AUXMC_OK;
+  if (!el || !agg || !carry || !terms) return AUXMC_E_WORKSPACE;
+  const GrpCfg cfg = grp_cfg(d, dy);
+  const int gp = cfg.groups;
+  const size_t sm_el = sizeof(double) * elem_smem(d, dy) * gp;
+  const size_t sm_sc = sizeof(double) * scan_smem(d) * gp;
+  const size_t sm_rc = sizeof(double) * rec_smem(d, dy) * gp;
+  if (sm_el > 227 * 1024 || sm_sc > 227 * 1024 || sm_rc > 227 * 1024) return AUXMC_E_DIM;
+  if (status) AUXMC_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int) * B, s));
+  const long long n = (long long)B * (T + 1);
+  const long long nb = (long long)B * nblk;
+  auto grid = [gp](long long k) { return (int)std::max(1LL, std::min((k + gp - 1) / gp, 148LL * 16)); };
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_elements<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_el));
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_reduce<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_carry<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_apply<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_recover<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rc));
+  AUXMC_LAUNCH(k_pfg_elements<BLOCK>, grid(n), cfg.threads, sm_el, s, dm, obs, B, el, status);
+  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, grid(nb), cfg.threads, sm_sc, s, T, d, B, LB, el, agg);
+  AUXMC_LAUNCH(k_pfg_carry<BLOCK>, grid(B), cfg.threads, sm_sc, s, T, d, B, LB, agg, carry);
+  AUXMC_LAUNCH(k_pfg_apply<BLOCK>, grid(nb), cfg.threads, sm_sc, s, T, d, B, LB, el, carry,
+               out->filt_mean, out->filt_cov);
+  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, grid(n), cfg.threads, sm_rc, s, dm, obs, B, out->filt_mean,
+               out->filt_cov, out->pred_mean, out->pred_cov, terms, status);
+  AUXMC_LAUNCH(k_pfg_sum, (B + 127) / 128, 128, 0, s, T, B, terms, out->log_marginal);
+  return AUXMC_OK;
+}
+
+}  // namespace
+
+int dispatch_pf_generic(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
+                        int* status, Arena& ws, cudaStream_t s) {
+  if (dm.dx > 32 || dm.dy > 64) return AUXMC_E_DIM;
+  return grp_cfg(dm.dx, dm.dy).block ? run_pfg<true>(dm, obs, B, out, status, ws, s)
+                                     : run_pfg<false>(dm, obs, B, out, status, ws, s);
+}
+
+}  // namespace auxmc_gpu

@@ -153,6 +153,27 @@ def test_parallel_filter_option(aux, oracle, backend):
         assert_close(ch.x[c].cpu().numpy(), o.x, 1e-8, "path")
 
 
+@pytest.mark.parametrize("backend", [1, 2])
+def test_parallel_filter_option_spatio_temporal_d9(aux, oracle, backend):
+    """C5 class at small T: spatio-temporal grid 3 (d = 9), scan filter inside the
+    aux-K step, prefix / DnC backends (group kernels for d > 8)."""
+    auxk, bm = aux
+    so = oracle.spec("spatio-temporal", T=24, grid=3, data_seed=7)
+    lat, data = oracle.simulate(so)
+    otg = oracle.make_target(so, data)
+    gtg = auxk.make_target(bm.ModelSpec(kind="spatio-temporal", T=24, grid=3, data_seed=7), data)
+    ch = auxk.init_chains(gtg, lat, 0.5, 6, 2)
+    oc = [oracle.AuxChain(otg, lat, 0.5) for _ in range(2)]
+    root = oracle.from_seed(6)
+    for it in range(4):
+        ch.kernel_step(backend, parallel_filter=True)
+        for c, o in enumerate(oc):
+            o.step(oracle.derive(root, oracle.L_CHAIN, c), backend, 1)
+        assert np.array_equal(ch.accepted.cpu().numpy(), [o.c.stats.accepted for o in oc])
+    for c, o in enumerate(oc):
+        assert_close(ch.x[c].cpu().numpy(), o.x, 1e-8, "path")
+
+
 @pytest.mark.parametrize("backend", [0, 1, 2])
 def test_sharded_chains_equal_unsharded(aux, backend):
     """Multi-GPU sharding contract: chain c depends only on its global index, so

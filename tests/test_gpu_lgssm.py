@@ -269,6 +269,23 @@ def test_parallel_filter_matches_oracle(gpu, oracle, case):
     assert_close(fr.filt_mean[0].cpu(), seq.filt_mean, 1e-6, "filt_mean vs sequential")
 
 
+@pytest.mark.parametrize("case", LARGE_CASES[:2] + LARGE_CASES[3:] + [(20, 3, 11, True, True, 36),
+                                                                     (40, 9, 4, True, True, 37)])
+def test_parallel_filter_large_dims_matches_oracle(gpu, oracle, case):
+    """Group (warp / CTA) scan filter for dx > 6 or dy > 8: group LU combine,
+    element build and recovery vs the oracle's Sklansky scan."""
+    lgssm, _, _ = gpu
+    m, obs = _oracle_case(oracle, *case)
+    par, _ = oracle.parallel_filter(m, obs)
+    fr = lgssm.parallel_filter(to_gpu_model(m), obs)
+    assert int(fr.status[0]) == 0
+    assert_close(fr.filt_mean[0].cpu(), par.filt_mean, 1e-8, "filt_mean vs oracle scan")
+    assert_close(fr.filt_cov[0].cpu(), par.filt_cov, 1e-8, "filt_cov vs oracle scan")
+    assert_close(fr.pred_mean[0].cpu(), par.pred_mean, 1e-8, "pred_mean vs oracle scan")
+    assert_close(fr.pred_cov[0].cpu(), par.pred_cov, 1e-8, "pred_cov vs oracle scan")
+    assert_close(fr.log_marginal[0].cpu(), par.log_marginal, 1e-9, "log_marginal")
+
+
 def test_parallel_filter_batched_long(gpu, oracle):
     lgssm, _, _ = gpu
     s = oracle.spec("lgssm-synthetic", T=5000, dx=4, dy=1, data_seed=1)
