@@ -114,4 +114,30 @@ struct NoiseArgs {
   long long n_bridge;
 };
 
+
+// Deterministic CTA-wide sum of get(0..n): each thread sums a contiguous chunk in
+// index order, then a fixed pairwise tree over the (power-of-two) thread
+// partials.  Replaces the reference's left-to-right sums over the horizon
+// (same terms, different association: within the FP64 parity tolerance).
+// red: blockDim.x doubles of shared memory.  Returns the sum on all threads.
+template <class Get>
+__device__ __forceinline__ double cta_sum_fixed(long long n, Get get, double* red) {
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const long long chunk = (n + nt - 1) / nt;
+  const long long lo = tid * chunk;
+  const long long hi = lo + chunk < n ? lo + chunk : n;
+  double s = 0.0;
+  for (long long i = lo; i < hi; ++i) s += get(i);
+  red[tid] = s;
+  __syncthreads();
+  for (int w = nt >> 1; w > 0; w >>= 1) {
+    if (tid < w) red[tid] = red[tid] + red[tid + w];
+    __syncthreads();
+  }
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+constexpr int kSumThreads = 256;
+
 }  // namespace auxmc_gpu

@@ -61,8 +61,10 @@ __device__ __forceinline__ void g_mm_dmma(const Grp& g, int m, int k, int n, con
   g_dmma<TA, TB>(g, m, k, n, A, TA ? m : k, B, TB ? k : n, C, n, false, false, D);
 }
 
+// CTA groups and single warps (mma.sync is warp-wide) on operands of at least
+// 16×16: below that the scalar loops have less latency than DMMA tiles.
 __device__ __forceinline__ bool use_dmma(const Grp& g, int m, int k, int n) {
-  return g.block && m >= 16 && n >= 16 && k >= 8;
+  return (g.block || g.size == 32) && m >= 16 && n >= 16 && k >= 8;
 }
 
 // ---------------------------------------------------------------- products

@@ -125,16 +125,19 @@ __global__ void k_path_terms(DevModel m, const double* __restrict__ obs, long lo
 __global__ void k_path_sum(int T, int B, const double* terms, const uint8_t* mask, int dy,
                            const double* log_marginal, int fr_shared, const int* fst,
                            double* out, int* status) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  const int K = 2 * T + 2;
+  __shared__ double red[kSumThreads];
+  const int b = blockIdx.x;
+  const long long K = 2LL * T + 2;
   const double* tm = terms + (size_t)b * K;
-  double lp = tm[0];
-  for (int t = 0; t < T; ++t) lp += tm[1 + t];
-  for (int t = 0; t <= T; ++t)
-    if (dy > 0 && (mask == nullptr || mask[t])) lp += tm[T + 1 + t];
-  out[b] = lp - log_marginal[fr_shared ? 0 : b];
-  status[b] = *fst;
+  const double lp = cta_sum_fixed(K, [&](long long i) {
+    if (i <= T) return tm[i];
+    const long long t = i - T - 1;
+    return (dy > 0 && (mask == nullptr || mask[t])) ? tm[i] : 0.0;
+  }, red);
+  if (threadIdx.x == 0) {
+    out[b] = lp - log_marginal[fr_shared ? 0 : b];
+    status[b] = *fst;
+  }
 }
 
 }  // namespace auxmc_gpu
@@ -164,7 +167,7 @@ int launch_path_logpdf(const DevModel& dm, const double* obs, long long obs_stri
   const long long n = (long long)B * K;
   AUXMC_LAUNCH(k_path_terms, (int)std::min<long long>((n + 127) / 128, 148LL * 64), 128, 0, s, dm,
                obs, obs_stride, traj, B, Ls, logdet, terms);
-  AUXMC_LAUNCH(k_path_sum, (B + 127) / 128, 128, 0, s, dm.T, B, terms, dm.mask, dm.dy,
+  AUXMC_LAUNCH(k_path_sum, B, kSumThreads, 0, s, dm.T, B, terms, dm.mask, dm.dy,
                log_marginal, lm_shared, fst, out, status);
   cudaFreeAsync(Ls, s);
   cudaFreeAsync(logdet, s);

@@ -631,11 +631,11 @@ __global__ void k_pf_recover(DevModel m, const double* __restrict__ obs, int B,
 }
 
 __global__ void k_pf_sum(int T, int B, const double* terms, double* out) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  double s = 0.0;
-  for (int t = 0; t <= T; ++t) s += terms[(size_t)b * (T + 1) + t];
-  out[b] = s;
+  __shared__ double red[kSumThreads];
+  const int b = blockIdx.x;
+  const double* tm = terms + (size_t)b * (T + 1);
+  const double s = cta_sum_fixed((long long)T + 1, [&](long long i) { return tm[i]; }, red);
+  if (threadIdx.x == 0) out[b] = s;
 }
 
 static int pf_block(int T) {
@@ -667,7 +667,7 @@ static int run_pf(const DevModel& dm, const double* obs, int B, auxmc_filter_res
                out->filt_cov);
   AUXMC_LAUNCH(k_pf_recover<D>, grid(n), 128, 0, s, dm, obs, B, out->filt_mean, out->filt_cov,
                out->pred_mean, out->pred_cov, terms, status);
-  AUXMC_LAUNCH(k_pf_sum, (B + 127) / 128, 128, 0, s, T, B, terms, out->log_marginal);
+  AUXMC_LAUNCH(k_pf_sum, B, kSumThreads, 0, s, T, B, terms, out->log_marginal);
   return AUXMC_OK;
 }
 

@@ -374,6 +374,45 @@ __global__ void k_pfg_carry(int T, int d, int B, int LB, const double* __restric
   }
 }
 
+// S2 for many blocks, second level: carries of the level-1 aggregates from the
+// exclusive carries of super-blocks of LB2 aggregates (carry2, from k_pfg_carry
+// over the super-block aggregates).
+template <bool BLOCK>
+__global__ void k_pfg_carry_seg(int nblk, int d, int B, int LB2, const double* __restrict__ agg,
+                                const double* __restrict__ carry2, double* carry) {
+  extern __shared__ double smem[];
+  const int ES = fe_size_g(d);
+  const Grp g = BLOCK ? block_group() : warp_group();
+  const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
+  double* sm = smem + (size_t)gid * scan_smem(d);
+  double *acc = sm, *o = acc + ES, *tmpd = o + ES;
+  const CombScratch cs = comb_scratch(d, tmpd + ES, reinterpret_cast<int*>(tmpd + ES + comb_doubles(d)));
+  const int nsup = (nblk + LB2 - 1) / LB2;
+  const long long n = (long long)B * nsup;
+  for (long long q = (long long)blockIdx.x * gpb + gid; q < n; q += (long long)gridDim.x * gpb) {
+    const int b = (int)(q / nsup), j = (int)(q % nsup);
+    const int lo = j * LB2, hi = min(lo + LB2, nblk);
+    const double* A = agg + (size_t)b * nblk * ES;
+    double* Cy = carry + (size_t)b * nblk * ES;
+    int k = lo;
+    if (j == 0) {
+      g_copy(g, ES, A + (size_t)lo * ES, acc);
+      k = lo + 1;
+    } else {
+      g_copy(g, ES, carry2 + (size_t)q * ES, acc);
+    }
+    g.sync();
+    for (; k < hi; ++k) {
+      g_copy(g, ES, acc, Cy + (size_t)k * ES);
+      if (k + 1 < hi) {
+        g_combine(g, d, acc, A + (size_t)k * ES, o, cs);
+        g_copy(g, ES, o, acc);
+      }
+      g.sync();
+    }
+  }
+}
+
 template <bool BLOCK>
 __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restrict__ el,
                             const double* __restrict__ carry, double* filt_mean, double* filt_cov) {
@@ -492,18 +531,21 @@ __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
 }
 
 __global__ void k_pfg_sum(int T, int B, const double* terms, double* out) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  double s = 0.0;
-  for (int t = 0; t <= T; ++t) s += terms[(size_t)b * (T + 1) + t];
-  out[b] = s;
+  __shared__ double red[kSumThreads];
+  const int b = blockIdx.x;
+  const double* tm = terms + (size_t)b * (T + 1);
+  const double s = cta_sum_fixed((long long)T + 1, [&](long long i) { return tm[i]; }, red);
+  if (threadIdx.x == 0) out[b] = s;
 }
 
+// block length ~ (T+1)^(1/3): S1 and S3 run LB sequential combines, S2 runs two
+// levels of ~LB when there are many blocks.
 int pf_block_g(int T) {
-  int lb = 1;
-  while ((long long)lb * lb < T + 1) lb <<= 1;
-  return lb < 4 ? 4 : lb;
+  int lb = 4;
+  while ((long long)lb * lb * lb < T + 1) lb <<= 1;
+  return lb;
 }
+constexpr int kPfTwoLevel = 64;  // blocks above which S2 is itself blocked
 
 template <bool BLOCK>
 int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out, int* status,
@@ -515,8 +557,12 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   double* agg = ws.take<double>((size_t)B * nblk * ES);
   double* carry = ws.take<double>((size_t)B * nblk * ES);
   double* terms = ws.take<double>((size_t)B * (T + 1));
+  const bool two = nblk > kPfTwoLevel;
+  const int LB2 = LB, nsup = (nblk + LB2 - 1) / LB2;
+  double* agg2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
+  double* carry2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!el || !agg || !carry || !terms) return AUXMC_E_WORKSPACE;
+  if (!el || !agg || !carry || !terms || (two && (!agg2 || !carry2))) return AUXMC_E_WORKSPACE;
   const GrpCfg cfg = grp_cfg(d, dy);
   const int gp = cfg.groups;
   const size_t sm_el = sizeof(double) * elem_smem(d, dy) * gp;
@@ -534,12 +580,24 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_recover<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rc));
   AUXMC_LAUNCH(k_pfg_elements<BLOCK>, grid(n), cfg.threads, sm_el, s, dm, obs, B, el, status);
   AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, grid(nb), cfg.threads, sm_sc, s, T, d, B, LB, el, agg);
-  AUXMC_LAUNCH(k_pfg_carry<BLOCK>, grid(B), cfg.threads, sm_sc, s, T, d, B, LB, agg, carry);
+  if (two) {
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_carry_seg<BLOCK>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
+    const long long ns = (long long)B * nsup;
+    AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, grid(ns), cfg.threads, sm_sc, s, nblk - 1, d, B, LB2, agg,
+                 agg2);
+    AUXMC_LAUNCH(k_pfg_carry<BLOCK>, grid(B), cfg.threads, sm_sc, s, nsup - 1, d, B, 1, agg2,
+                 carry2);
+    AUXMC_LAUNCH(k_pfg_carry_seg<BLOCK>, grid(ns), cfg.threads, sm_sc, s, nblk, d, B, LB2, agg,
+                 carry2, carry);
+  } else {
+    AUXMC_LAUNCH(k_pfg_carry<BLOCK>, grid(B), cfg.threads, sm_sc, s, T, d, B, LB, agg, carry);
+  }
   AUXMC_LAUNCH(k_pfg_apply<BLOCK>, grid(nb), cfg.threads, sm_sc, s, T, d, B, LB, el, carry,
                out->filt_mean, out->filt_cov);
   AUXMC_LAUNCH(k_pfg_recover<BLOCK>, grid(n), cfg.threads, sm_rc, s, dm, obs, B, out->filt_mean,
                out->filt_cov, out->pred_mean, out->pred_cov, terms, status);
-  AUXMC_LAUNCH(k_pfg_sum, (B + 127) / 128, 128, 0, s, T, B, terms, out->log_marginal);
+  AUXMC_LAUNCH(k_pfg_sum, B, kSumThreads, 0, s, T, B, terms, out->log_marginal);
   return AUXMC_OK;
 }
 

@@ -286,6 +286,19 @@ def test_parallel_filter_large_dims_matches_oracle(gpu, oracle, case):
     assert_close(fr.log_marginal[0].cpu(), par.log_marginal, 1e-9, "log_marginal")
 
 
+def test_parallel_filter_generic_two_level_carry(gpu, oracle):
+    """Generic scan filter with more than 64 blocks: the block carries are
+    themselves scanned in two levels; d = 7 (warp groups), T = 3000."""
+    lgssm, _, _ = gpu
+    m, obs = _oracle_case(oracle, 3000, 7, 2, False, True, 38)
+    seq = oracle.kalman_filter(m, obs)
+    fr = lgssm.parallel_filter(to_gpu_model(m), obs)
+    assert int(fr.status[0]) == 0
+    assert_close(fr.filt_mean[0].cpu(), seq.filt_mean, 1e-8, "filt_mean vs sequential")
+    assert_close(fr.filt_cov[0].cpu(), seq.filt_cov, 1e-8, "filt_cov vs sequential")
+    assert_close(fr.log_marginal[0].cpu(), seq.log_marginal, 1e-9, "log_marginal")
+
+
 def test_parallel_filter_batched_long(gpu, oracle):
     lgssm, _, _ = gpu
     s = oracle.spec("lgssm-synthetic", T=5000, dx=4, dy=1, data_seed=1)

@@ -6,6 +6,8 @@ c3: Lorenz-96 d = 40 diffusion smoothing, auxiliary Kalman sampler, T = 4096,
     256 chains, sequential backend (configs[2]).
 c4: stochastic volatility d = 3, auxiliary particle Gibbs, N = 256, T = 2^14
     (configs[3]), parallel-in-time cSMC (--sampler dnc selects the reference cSMC).
+c5: spatio-temporal grid 4 (d = 16), T = 2^20, 1 chain, aux-Kalman with the scan
+    filter and prefix sampler (configs[4]; single GPU, no time sharding yet).
 Units: chain-timesteps/s = chains * (T+1) * iterations / device seconds.
 """
 from __future__ import annotations
@@ -35,6 +37,12 @@ def run(args, rank, world, local):
         spec = bm.ModelSpec(kind="lorenz96", T=T, dx=40, data_seed=3)
         backend, delta = auxk.Backend.kSequential, 0.05
         flops_ct = 2.14e6  # F_seq at d = 40, q = 20
+    elif cfg == "c5":
+        T, C, d = args.T or (1 << 20), args.chains or 1, 16
+        spec = bm.ModelSpec(kind="spatio-temporal", T=T, grid=4, data_seed=7)
+        backend = auxk.Backend.kDnc if args.sampler == "dnc" else auxk.Backend.kPrefix
+        delta = 0.5
+        flops_ct = 464e3  # F_pit at d = 16
     else:
         T, C, d = args.T or 16384, args.chains or 148, 3
         spec = bm.ModelSpec(kind="stochvol", T=T, dx=3, data_seed=11)
@@ -56,9 +64,9 @@ def run(args, rank, world, local):
         sh = shard.weak_shard(rank, world, C)
         ch = auxk.init_chains(tg, x0, delta, 1, sh.count, first=sh.first)
 
-        # C1 is one short chain: the scan filter (KernelOptions::parallel_filter)
+        # C1 / C5 are single chains: the scan filter (KernelOptions::parallel_filter)
         # parallelizes the horizon; C3 has 256 chains and uses the sequential filter.
-        pf = cfg == "c1"
+        pf = cfg in ("c1", "c5")
 
         def step():
             ch.kernel_step(backend, parallel_filter=pf)
@@ -87,7 +95,10 @@ def run(args, rank, world, local):
             "data": "synthetic",
             "config": {"workload": {"c1": "C1 aux-Kalman 1-D LGSSM prefix backend",
                                     "c3": "C3 aux-Kalman Lorenz-96 d=40 sequential backend",
-                                    "c4": "C4 stochvol aux particle Gibbs N=256"}[cfg],
+                                    "c4": "C4 stochvol aux particle Gibbs N=256",
+                                    "c5": "C5 spatio-temporal grid 4 (d=16) aux-Kalman, scan "
+                                          "filter + prefix sampler, 1 chain (1 GPU: no time "
+                                          "sharding)"}[cfg],
                        "T": T, "chains_per_gpu": C, "mcmc_iters_per_sec": 1e3 * args.steps / ms,
                        **extra},
             "roofline": {"bound": "fp64" if cfg != "c1" else "latency",
