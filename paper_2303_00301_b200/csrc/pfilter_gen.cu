@@ -97,6 +97,11 @@ struct CombScratch {
   int *p1, *p2, *idx;
 };
 
+// With C and J symmetric (every element and every combine output is
+// symmetrized), M2 = I + vJ uC is exactly M1^T for M1 = I + uC vJ (same
+// products, same summation order), so one LU gives both solves: Minv = M1^{-1}
+// (LU with partial pivoting, solved against I) and M2^{-1} = Minv^T; the
+// remaining algebra is dense products.
 __device__ void g_combine(const Grp& g, int d, const double* u, const double* v, double* o,
                           const CombScratch& s) {
   const int dd = d * d;
@@ -105,66 +110,65 @@ __device__ void g_combine(const Grp& g, int d, const double* u, const double* v,
   const double *vA = v, *vb = v + dd, *vC = v + dd + d, *veta = v + 2 * dd + d,
                *vJ = v + 2 * dd + 2 * d;
   double *oA = o, *ob = o + dd, *oC = o + dd + d, *oeta = o + 2 * dd + d, *oJ = o + 2 * dd + 2 * d;
+  double* Minv = s.M2;
   g_mm(g, d, d, d, uC, vJ, s.M1);
-  g_mm(g, d, d, d, vJ, uC, s.M2);
+  g_eye(g, d, s.T2);
   g.sync();
-  for (int i = g.lane; i < d; i += g.size) {
-    s.M1[i * d + i] += 1.0;
-    s.M2[i * d + i] += 1.0;
-  }
+  for (int i = g.lane; i < d; i += g.size) s.M1[i * d + i] += 1.0;
   g.sync();
   g_lu_factor(g, d, s.M1, s.p1, s.idx);
-  g_lu_factor(g, d, s.M2, s.p2, s.idx);
-  // A = vA M1^{-1} uA
-  g_lu_solve(g, d, s.M1, s.p1, d, uA, s.S);
+  g_lu_solve(g, d, s.M1, s.p1, d, s.T2, Minv);  // M1^{-1}
+  // t = uC veta + ub ; t2 = veta - vJ ub
+  for (int i = g.lane; i < d; i += g.size) {
+    double acc = 0.0, acc2 = 0.0;
+    for (int k = 0; k < d; ++k) {
+      acc += uC[i * d + k] * veta[k];
+      acc2 += vJ[i * d + k] * ub[k];
+    }
+    s.t[i] = acc + ub[i];
+    s.w[i] = veta[i] - acc2;
+  }
+  g.sync();
+  // A = vA (Minv uA) ; S = Minv uC ; T2 = Minv^T vJ
+  g_mm(g, d, d, d, Minv, uA, s.S);
+  g_mm(g, d, d, d, Minv, uC, s.T1);
+  g_mm_tn(g, d, d, d, Minv, vJ, s.T2);
+  // b = vA (Minv t) + vb ; eta = uA^T (Minv^T t2) + ueta  (vectors kept in M1's rows)
+  double* mt = s.M1;
+  double* mt2 = s.M1 + d;
+  for (int i = g.lane; i < d; i += g.size) {
+    double acc = 0.0, acc2 = 0.0;
+    for (int k = 0; k < d; ++k) {
+      acc += Minv[i * d + k] * s.t[k];
+      acc2 += Minv[k * d + i] * s.w[k];
+    }
+    mt[i] = acc;
+    mt2[i] = acc2;
+  }
   g.sync();
   g_mm(g, d, d, d, vA, s.S, oA);
-  // t = uC veta + ub
   for (int i = g.lane; i < d; i += g.size) {
-    double acc = 0.0;
-    for (int k = 0; k < d; ++k) acc += uC[i * d + k] * veta[k];
-    s.t[i] = acc + ub[i];
-  }
-  g.sync();
-  g_lu_solve(g, d, s.M1, s.p1, 1, s.t, s.w);
-  g.sync();
-  for (int i = g.lane; i < d; i += g.size) {
-    double acc = 0.0;
-    for (int k = 0; k < d; ++k) acc += vA[i * d + k] * s.w[k];
+    double acc = 0.0, acc2 = 0.0;
+    for (int k = 0; k < d; ++k) {
+      acc += vA[i * d + k] * mt[k];
+      acc2 += uA[k * d + i] * mt2[k];
+    }
     ob[i] = acc + vb[i];
+    oeta[i] = acc2 + ueta[i];
   }
-  // C = symm(vA M1^{-1} uC vA^T + vC)
-  g_lu_solve(g, d, s.M1, s.p1, d, uC, s.S);
+  // C = symm(vA (Minv uC) vA^T + vC) ; J = symm(uA^T (Minv^T vJ) uA + uJ)
+  g_mm(g, d, d, d, vA, s.T1, Minv);  // Minv consumed
   g.sync();
-  g_mm(g, d, d, d, vA, s.S, s.T1);
+  g_mm_tn(g, d, d, d, uA, s.T2, s.S);
+  g_mm_nt(g, d, d, d, Minv, vA, s.T1, vC);
   g.sync();
-  g_mm_nt(g, d, d, d, s.T1, vA, s.T2, vC);
+  g_mm(g, d, d, d, s.S, uA, s.T2, uJ);
   g.sync();
   for (int i = g.ty(); i < d; i += g.ny())
-    for (int j = g.tx(); j < d; j += 16) oC[i * d + j] = 0.5 * (s.T2[i * d + j] + s.T2[j * d + i]);
-  // eta = uA^T M2^{-1} (veta - vJ ub) + ueta
-  for (int i = g.lane; i < d; i += g.size) {
-    double acc = 0.0;
-    for (int k = 0; k < d; ++k) acc += vJ[i * d + k] * ub[k];
-    s.t[i] = veta[i] - acc;
-  }
-  g.sync();
-  g_lu_solve(g, d, s.M2, s.p2, 1, s.t, s.w);
-  g.sync();
-  for (int i = g.lane; i < d; i += g.size) {
-    double acc = 0.0;
-    for (int k = 0; k < d; ++k) acc += uA[k * d + i] * s.w[k];
-    oeta[i] = acc + ueta[i];
-  }
-  // J = symm(uA^T M2^{-1} vJ uA + uJ)
-  g_lu_solve(g, d, s.M2, s.p2, d, vJ, s.S);
-  g.sync();
-  g_mm_tn(g, d, d, d, uA, s.S, s.T1);
-  g.sync();
-  g_mm(g, d, d, d, s.T1, uA, s.T2, uJ);
-  g.sync();
-  for (int i = g.ty(); i < d; i += g.ny())
-    for (int j = g.tx(); j < d; j += 16) oJ[i * d + j] = 0.5 * (s.T2[i * d + j] + s.T2[j * d + i]);
+    for (int j = g.tx(); j < d; j += 16) {
+      oC[i * d + j] = 0.5 * (s.T1[i * d + j] + s.T1[j * d + i]);
+      oJ[i * d + j] = 0.5 * (s.T2[i * d + j] + s.T2[j * d + i]);
+    }
   g.sync();
 }
 
