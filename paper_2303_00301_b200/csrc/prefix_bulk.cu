@@ -26,7 +26,10 @@ struct BulkGeom {
   static constexpr int S = NSUB * LS;      // steps per superchunk
   static constexpr int LP = D * (D + 1) / 2;
   static constexpr int ES = D * D + D + LP;
-  static constexpr int SUB = LS * ES + ((LS * ES) % 2 == 0 ? 1 : 0);  // odd: spreads a warp's blocks
+  // D = 4: sub-chunk blocks 16-B aligned (LDS.128) and 976 B apart, which puts
+  // a warp's 4 sub-chunks on disjoint bank quads; odd D: an odd stride.
+  static constexpr bool VEC = (ES % 2 == 0);
+  static constexpr int SUB = VEC ? LS * ES + 2 : LS * ES + ((LS * ES) % 2 == 0 ? 1 : 0);
   static constexpr int EB = NSUB * SUB;
   static constexpr int TAB = 3 * NSUB * D * D;  // Gsub | Gpair | Gin
   static constexpr int TB = (EB + TAB + 1) & ~1;
@@ -87,7 +90,7 @@ __global__ void k_bulk_pack1(const double* __restrict__ elems, int T, double* ti
 #pragma unroll
       for (int i = 0; i < D * D; ++i) P[i] = Q[i];
     }
-    blk[G::LS * G::ES] = 0.0;
+    for (int i = G::LS * G::ES; i < G::SUB; ++i) blk[i] = 0.0;
     double* gs = tile + G::EB + j * D * D;
 #pragma unroll
     for (int i = 0; i < D * D; ++i) gs[i] = P[i];
@@ -125,6 +128,17 @@ __global__ void k_bulk_pack2(int T, double* tiles) {
 #pragma unroll
       for (int i = 0; i < D * D; ++i) gpair[j * D * D + i] = 0.0;
     }
+  }
+}
+
+// n (even) doubles from a 16-B aligned shared-memory address as LDS.128
+template <int N>
+__device__ __forceinline__ void lds_vec(const double* p, double* v) {
+#pragma unroll
+  for (int i = 0; i < N; i += 2) {
+    const double2 t = *reinterpret_cast<const double2*>(p + i);
+    v[i] = t.x;
+    v[i + 1] = t.y;
   }
 }
 
@@ -235,15 +249,21 @@ __global__ void __launch_bounds__(BulkGeom<D>::WARPS * 32, 1)
 #pragma unroll
           for (int i = 0; i < D; ++i) xi[i] = normal_at(key, (uint64_t)i);
         }
+        double ev[G::VEC ? ES : 1];
+        const double* er = e;
+        if constexpr (G::VEC) {
+          lds_vec<ES>(e, ev);
+          er = ev;
+        }
         double gy[D];
-        r_matvec<D>(e, y, gy);
+        r_matvec<D>(er, y, gy);
         int w = 0;
 #pragma unroll
         for (int r = 0; r < D; ++r) {
           double acc = 0.0;
 #pragma unroll
-          for (int cc = 0; cc <= r; ++cc) acc += e[D * D + D + w++] * xi[cc];
-          const double cv = e[D * D + r] + acc;
+          for (int cc = 0; cc <= r; ++cc) acc += er[D * D + D + w++] * xi[cc];
+          const double cv = er[D * D + r] + acc;
           cs[s * D + r] = cv;
           y[r] = gy[r] + cv;
         }
@@ -309,7 +329,13 @@ __global__ void __launch_bounds__(BulkGeom<D>::WARPS * 32, 1)
         const int t = lo + s;
         if (full || t < t1) {
           double gx[D];
-          r_matvec<D>(E + s * ES, x, gx);
+          if constexpr (G::VEC) {
+            double gm[D * D];
+            lds_vec<D * D>(E + s * ES, gm);
+            r_matvec<D>(gm, x, gx);
+          } else {
+            r_matvec<D>(E + s * ES, x, gx);
+          }
 #pragma unroll
           for (int i = 0; i < D; ++i) x[i] = gx[i] + cs[s * D + i];
 #pragma unroll
