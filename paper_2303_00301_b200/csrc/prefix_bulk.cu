@@ -22,7 +22,8 @@ namespace auxmc_gpu {
 template <int D>
 struct BulkGeom {
   static constexpr int LS = 16 / D;        // steps per sub-chunk (D = 2, 4)
-  static constexpr int NSUB = 32, WARPS = 8, SLOTS = 8;
+  static constexpr int NSUB = 32, WARPS = 8, SLOTS = 8;  // compute warps; lane slots
+  static constexpr int ROWS = 7;           // chains per CTA (148 CTAs cover 1036 chains)
   static constexpr int S = NSUB * LS;      // steps per superchunk
   static constexpr int LP = D * (D + 1) / 2;
   static constexpr int ES = D * D + D + LP;
@@ -34,15 +35,16 @@ struct BulkGeom {
   static constexpr int TAB = 3 * NSUB * D * D;  // Gsub | Gpair | Gin
   static constexpr int TB = (EB + TAB + 1) & ~1;
   static constexpr int ROW = S * D + 2;    // io row stride: slot stride = 4 banks
-  static constexpr int IOB = SLOTS * ROW;
-  static constexpr int STAGES = 2;         // in: (tables + noise) double-buffered
-  static constexpr int STG = TB + IOB;
+  static constexpr int IOB = ROWS * ROW;
+  static constexpr int TSTG = 3, NSTG = 2; // element-tile stages, noise stages
   static constexpr int CS = D + 2;         // per-(warp, slot) carry stride: conflict-free LDS.128
-  // + 2 out tiles (paths) so a bulk store drains while the next superchunk computes
-  static constexpr size_t SMEM =
-      sizeof(double) * (STAGES * STG + 2 * IOB + 2 * SLOTS * WARPS * CS + SLOTS * D) +
-      STAGES * sizeof(uint64_t);
+  static constexpr int CB = SLOTS * WARPS * CS;
+  static constexpr size_t SMEM = sizeof(double) * (TSTG * TB + NSTG * IOB + IOB + 3 * CB +
+                                                   SLOTS * D) +
+                                 (TSTG + NSTG) * sizeof(uint64_t);
 };
+static_assert(BulkGeom<4>::SMEM <= 227 * 1024, "one CTA per SM");
+static_assert(BulkGeom<2>::SMEM <= 227 * 1024, "one CTA per SM");
 
 template <int D>
 __device__ __forceinline__ void mat_mul(const double* A, const double* B, double* C) {
@@ -148,23 +150,31 @@ __device__ __forceinline__ void shfl_down_vec(const double* v, double* out, int 
   for (int i = 0; i < D; ++i) out[i] = __shfl_down_sync(0xffffffffu, v[i], delta);
 }
 
+// Software-pipelined sweep.  Eight compute warps own (chain slot, sub-chunk)
+// pairs; a ninth "carry" warp runs the serial pass over warp aggregates and
+// drives the TMA engine.  Iteration k overlaps the carry pass of superchunk k
+// with the reduction (phase A) of superchunk k-1, then expands superchunk k
+// (phase C): two CTA barriers per superchunk.  Element tiles are triple
+// buffered (tiles k and k-1 are live while k-2 streams in), noise rows double
+// buffered, path rows single buffered (drained during the next phase A).
 template <int D, bool PRE>
-__global__ void __launch_bounds__(BulkGeom<D>::WARPS * 32, 1)
+__global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
     k_prefix_bulk(int T, int C, const double* __restrict__ tiles, const double* __restrict__ term,
                   NoiseArgs noise, double* __restrict__ traj) {
   using G = BulkGeom<D>;
-  constexpr int LS = G::LS, ES = G::ES, S = G::S, NS = G::NSUB, W = G::WARPS;
+  constexpr int LS = G::LS, ES = G::ES, S = G::S, NS = G::NSUB, W = G::WARPS, CS = G::CS;
   extern __shared__ __align__(16) double sm[];
-  constexpr int CS = G::CS;
-  auto tile = [&](int b) { return sm + b * G::STG; };
-  auto xit = [&](int b) { return sm + b * G::STG + G::TB; };
-  auto xot = [&](int b) { return sm + G::STAGES * G::STG + b * G::IOB; };
-  double* cagg = sm + G::STAGES * G::STG + 2 * G::IOB;  // [W][SLOTS][CS]
-  double* xwtop = cagg + G::SLOTS * W * CS;    // [W][SLOTS][CS]
-  double* carry = xwtop + G::SLOTS * W * CS;   // [SLOTS][D]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(carry + G::SLOTS * D);
+  auto tile = [&](int k) { return sm + (k % G::TSTG) * G::TB; };
+  auto xin = [&](int k) { return sm + G::TSTG * G::TB + (k % G::NSTG) * G::IOB; };
+  double* xo = sm + G::TSTG * G::TB + G::NSTG * G::IOB;
+  auto cagg = [&](int k) { return xo + G::IOB + (k & 1) * G::CB; };  // [W][SLOTS][CS]
+  double* xwtop = xo + G::IOB + 2 * G::CB;                             // [W][SLOTS][CS]
+  double* carry = xwtop + G::CB;                                       // [SLOTS][D]
+  uint64_t* barT = reinterpret_cast<uint64_t*>(carry + G::SLOTS * D);
+  uint64_t* barN = barT + G::TSTG;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool cw = warp == W;  // carry warp
   const int slot = lane & 7, q = lane >> 3, j = warp * 4 + q;
   const int c_begin = (int)(((long long)blockIdx.x * C) / gridDim.x);
   const int c_end = (int)(((long long)(blockIdx.x + 1) * C) / gridDim.x);
@@ -174,10 +184,11 @@ __global__ void __launch_bounds__(BulkGeom<D>::WARPS * 32, 1)
   const long long row = (long long)(T + 1) * D;
 
   if (tid == 0) {
-    for (int b = 0; b < G::STAGES; ++b) mbar_init(&bar[b], 1);
+    for (int b = 0; b < G::TSTG; ++b) mbar_init(&barT[b], 1);
+    for (int b = 0; b < G::NSTG; ++b) mbar_init(&barN[b], 1);
     mbar_fence_init();
   }
-  if (active && j == 0) {  // x_T = m_T + L_T xi (pit.cpp:85-87)
+  if (cw && lane < 8 && active) {  // x_T = m_T + L_T xi (pit.cpp:85-87)
     double xi[D], x[D];
     if (PRE) {
 #pragma unroll
@@ -198,37 +209,57 @@ __global__ void __launch_bounds__(BulkGeom<D>::WARPS * 32, 1)
   __syncthreads();
   if (T == 0) return;
   const int K = (T + S - 1) / S;
-  auto issue = [&](int k) {
-    const int b = k % G::STAGES, t0 = k * S, len = min(S, T - t0);
+  auto issue_tile = [&](int k) {
     const unsigned tb = G::TB * sizeof(double);
-    const unsigned xb = (unsigned)(len * D * sizeof(double));
-    mbar_expect_tx(&bar[b], tb + (PRE ? xb * nc : 0u));
-    bulk_g2s(tile(b), tiles + (size_t)k * G::TB, tb, &bar[b]);
-    if (PRE)
-      for (int ch = 0; ch < nc; ++ch)
-        bulk_g2s(xit(b) + ch * G::ROW, noise.backward + ((size_t)(c_begin + ch) * T + t0) * D, xb,
-                 &bar[b]);
+    uint64_t* bar = &barT[k % G::TSTG];
+    mbar_expect_tx(bar, tb);
+    bulk_g2s(tile(k), tiles + (size_t)k * G::TB, tb, bar);
   };
-  if (tid == 0) issue(K - 1);
-  unsigned phase_bits = 0u;
+  auto issue_noise = [&](int k) {
+    const int t0 = k * S, len = min(S, T - t0);
+    const unsigned xb = (unsigned)(len * D * sizeof(double));
+    uint64_t* bar = &barN[k % G::NSTG];
+    mbar_expect_tx(bar, xb * nc);
+    for (int ch = 0; ch < nc; ++ch)
+      bulk_g2s(xin(k) + ch * G::ROW, noise.backward + ((size_t)(c_begin + ch) * T + t0) * D, xb,
+               bar);
+  };
+  if (cw && lane == 0) {
+    issue_tile(K - 1);
+    if (PRE) issue_noise(K - 1);
+    if (K >= 2) {
+      issue_tile(K - 2);
+      if (PRE) issue_noise(K - 2);
+    }
+  }
+  unsigned tph = 0u, nph = 0u;  // per-stage mbarrier parities seen by this thread
+  auto wait_tile = [&](int k) {
+    const int b = k % G::TSTG;
+    mbar_wait(&barT[b], (tph >> b) & 1u);
+    tph ^= 1u << b;
+  };
+  auto wait_noise = [&](int k) {
+    const int b = k % G::NSTG;
+    mbar_wait(&barN[b], (nph >> b) & 1u);
+    nph ^= 1u << b;
+  };
   uint64_t klabel = 0;
-  if (!PRE && active) klabel = derive_label(noise.keys[c], kBackwardNoise);
+  if (!PRE && !cw && active) klabel = derive_label(noise.keys[c], kBackwardNoise);
 
-  for (int k = K - 1; k >= 0; --k) {
-    const int buf = k % G::STAGES;
-    if (tid == 0 && k > 0) issue(k - 1);  // stage (k-1) % 2 was released by superchunk k+1
-    mbar_wait(&bar[buf], (phase_bits >> buf) & 1u);
-    phase_bits ^= 1u << buf;
+  // Phase A for superchunk k: realize c_t = off_t + L_t xi_t, reduce each
+  // sub-chunk (zero carry), Kogge-Stone over the warp's 4 sub-chunks; the warp
+  // aggregates go to cagg(k).
+  auto phase_a = [&](int k, double* cs, double* y) {
+    wait_tile(k);
+    if (PRE) wait_noise(k);
+    const double* tl = tile(k);
     const int t0 = k * S, t1 = min(t0 + S, T);
     const int lo = t0 + j * LS;
     const bool full = (t1 - t0) == S;
-    const double* E = tile(buf) + j * G::SUB;
-    const double* gsub = tile(buf) + G::EB;
+    const double* E = tl + j * G::SUB;
+    const double* gsub = tl + G::EB;
     const double* gpair = gsub + NS * D * D;
-    const double* gin = gpair + NS * D * D;
-    double* X = xit(buf) + slot * G::ROW + j * LS * D;
-    // Phase A: realize c_t = off_t + L_t xi_t and reduce the sub-chunk (zero carry)
-    double cs[LS * D], y[D];
+    const double* X = xin(k) + slot * G::ROW + j * LS * D;
 #pragma unroll
     for (int i = 0; i < D; ++i) y[i] = 0.0;
 #pragma unroll
@@ -272,58 +303,80 @@ __global__ void __launch_bounds__(BulkGeom<D>::WARPS * 32, 1)
         for (int r = 0; r < D; ++r) cs[s * D + r] = 0.0;
       }
     }
-    // Kogge-Stone over the warp's 4 sub-chunks (suffix direction): y -> c over [j, group end)
-    {
-      double yn[D], gy[D];
-      shfl_down_vec<D>(y, yn, 8);
-      if (q < 3) {
-        r_matvec<D>(gsub + j * D * D, yn, gy);
+    double yn[D], gy[D];  // suffix Kogge-Stone: y -> c over [j, group end)
+    shfl_down_vec<D>(y, yn, 8);
+    if (q < 3) {
+      r_matvec<D>(gsub + j * D * D, yn, gy);
 #pragma unroll
-        for (int i = 0; i < D; ++i) y[i] = gy[i] + y[i];
-      }
-      shfl_down_vec<D>(y, yn, 16);
-      if (q < 2) {
-        r_matvec<D>(gpair + j * D * D, yn, gy);
+      for (int i = 0; i < D; ++i) y[i] = gy[i] + y[i];
+    }
+    shfl_down_vec<D>(y, yn, 16);
+    if (q < 2) {
+      r_matvec<D>(gpair + j * D * D, yn, gy);
 #pragma unroll
-        for (int i = 0; i < D; ++i) y[i] = gy[i] + y[i];
-      }
+      for (int i = 0; i < D; ++i) y[i] = gy[i] + y[i];
     }
     if (q == 0) {
 #pragma unroll
-      for (int i = 0; i < D; ++i) cagg[(warp * G::SLOTS + slot) * CS + i] = y[i];
+      for (int i = 0; i < D; ++i) cagg(k)[(warp * G::SLOTS + slot) * CS + i] = y[i];
     }
-    if (tid == 0) bulk_wait_read<1>();  // the store of superchunk k+2 has left xot(k & 1)
-    __syncthreads();
-    // Phase B: serial pass over the 8 warp aggregates of each chain, top-down
-    if (warp == 0 && lane < 8 && active) {
-      double x[D];
-#pragma unroll
-      for (int i = 0; i < D; ++i) x[i] = carry[slot * D + i];
-      for (int w = W - 1; w >= 0; --w) {
-#pragma unroll
-        for (int i = 0; i < D; ++i) xwtop[(w * G::SLOTS + slot) * CS + i] = x[i];
-        if (t0 + 4 * w * LS >= t1) continue;
-        double gx[D];
-        r_matvec<D>(gin + 4 * w * D * D, x, gx);
-#pragma unroll
-        for (int i = 0; i < D; ++i) x[i] = gx[i] + cagg[(w * G::SLOTS + slot) * CS + i];
+  };
+
+  double csA[LS * D], yA[D], csB[LS * D], yB[D];
+  if (!cw) phase_a(K - 1, csA, yA);
+  __syncthreads();
+
+  for (int k = K - 1; k >= 0; --k) {
+    const int t0 = k * S, t1 = min(t0 + S, T);
+    if (cw) {
+      if (lane == 0) {
+        bulk_wait_read<0>();  // the store of superchunk k+1 has left xo
+        if (k >= 2) {          // stages of k+1 (tile) and k (noise) are free
+          issue_tile(k - 2);
+          if (PRE) issue_noise(k - 2);
+        }
       }
+      // Phase B (carry): serial pass over the 8 warp aggregates, top-down
+      wait_tile(k);
+      if (lane < 8 && active) {
+        const double* gin = tile(k) + G::EB + 2 * NS * D * D;
+        const double* ca = cagg(k);
+        double x[D];
 #pragma unroll
-      for (int i = 0; i < D; ++i) carry[slot * D + i] = x[i];
+        for (int i = 0; i < D; ++i) x[i] = carry[slot * D + i];
+        for (int w = W - 1; w >= 0; --w) {
+#pragma unroll
+          for (int i = 0; i < D; ++i) xwtop[(w * G::SLOTS + slot) * CS + i] = x[i];
+          if (t0 + 4 * w * LS >= t1) continue;
+          double gx[D];
+          r_matvec<D>(gin + 4 * w * D * D, x, gx);
+#pragma unroll
+          for (int i = 0; i < D; ++i) x[i] = gx[i] + ca[(w * G::SLOTS + slot) * CS + i];
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) carry[slot * D + i] = x[i];
+      }
+    } else if (k >= 1) {
+      phase_a(k - 1, csB, yB);
     }
     __syncthreads();
-    // Phase C: x at the top of each sub-chunk, then expand x_t = G_t x_{t+1} + c_t
-    {
+    if (!cw) {  // Phase C: x at the top of each sub-chunk, then x_t = G_t x_{t+1} + c_t
+      const double* tl = tile(k);
+      const double* E = tl + j * G::SUB;
+      const double* gin = tl + G::EB + 2 * NS * D * D;
+      const int lo = t0 + j * LS;
+      const bool full = (t1 - t0) == S;
       double xt[D], xb[D], xn[D], x[D];
 #pragma unroll
       for (int i = 0; i < D; ++i) xt[i] = xwtop[(warp * G::SLOTS + slot) * CS + i];
       r_matvec<D>(gin + j * D * D, xt, xb);
 #pragma unroll
-      for (int i = 0; i < D; ++i) xb[i] = xb[i] + y[i];
+      for (int i = 0; i < D; ++i) xb[i] = xb[i] + yA[i];
       shfl_down_vec<D>(xb, xn, 8);
 #pragma unroll
       for (int i = 0; i < D; ++i) x[i] = q < 3 ? xn[i] : xt[i];
-      double* XO = xot(k & 1) + slot * G::ROW + j * LS * D;
+      double* XO = xo + slot * G::ROW + j * LS * D;
+      const bool live = slot < G::ROWS;
 #pragma unroll
       for (int s = LS - 1; s >= 0; --s) {
         const int t = lo + s;
@@ -337,23 +390,29 @@ __global__ void __launch_bounds__(BulkGeom<D>::WARPS * 32, 1)
             r_matvec<D>(E + s * ES, x, gx);
           }
 #pragma unroll
-          for (int i = 0; i < D; ++i) x[i] = gx[i] + cs[s * D + i];
+          for (int i = 0; i < D; ++i) x[i] = gx[i] + csA[s * D + i];
+          if (live) {
 #pragma unroll
-          for (int i = 0; i < D; i += 2)
-            *reinterpret_cast<double2*>(XO + s * D + i) = make_double2(x[i], x[i + 1]);
+            for (int i = 0; i < D; i += 2)
+              *reinterpret_cast<double2*>(XO + s * D + i) = make_double2(x[i], x[i + 1]);
+          }
         }
       }
+      fence_proxy_async();
+#pragma unroll
+      for (int i = 0; i < LS * D; ++i) csA[i] = csB[i];
+#pragma unroll
+      for (int i = 0; i < D; ++i) yA[i] = yB[i];
     }
-    fence_proxy_async();
     __syncthreads();
-    if (tid == 0) {
+    if (cw && lane == 0) {
       const unsigned xb = (unsigned)((t1 - t0) * D * sizeof(double));
       for (int ch = 0; ch < nc; ++ch)
-        bulk_s2g(traj + (size_t)(c_begin + ch) * row + (size_t)t0 * D, xot(k & 1) + ch * G::ROW, xb);
+        bulk_s2g(traj + (size_t)(c_begin + ch) * row + (size_t)t0 * D, xo + ch * G::ROW, xb);
       bulk_commit();
     }
   }
-  if (tid == 0) bulk_wait<0>();
+  if (cw && lane == 0) bulk_wait<0>();
 }
 
 template <int D>
@@ -370,17 +429,17 @@ int run_prefix_bulk(int T, int B, const double* elems, const double* term, Arena
     AUXMC_LAUNCH(k_bulk_pack1<D>, grid, 128, 0, stream, elems, T, tiles);
     AUXMC_LAUNCH(k_bulk_pack2<D>, grid, 128, 0, stream, T, tiles);
   }
-  const int grid = std::max((B + G::SLOTS - 1) / G::SLOTS, std::min(B, num_sms()));
+  const int grid = std::max((B + G::ROWS - 1) / G::ROWS, std::min(B, num_sms()));
   if (nz.kind == AUXMC_NOISE_PREDRAWN) {
     AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_prefix_bulk<D, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-    AUXMC_LAUNCH((k_prefix_bulk<D, true>), grid, G::WARPS * 32, G::SMEM, stream, T, B, tiles, term,
-                 nz, traj);
+    AUXMC_LAUNCH((k_prefix_bulk<D, true>), grid, (G::WARPS + 1) * 32, G::SMEM, stream, T, B, tiles,
+                 term, nz, traj);
   } else {
     AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_prefix_bulk<D, false>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-    AUXMC_LAUNCH((k_prefix_bulk<D, false>), grid, G::WARPS * 32, G::SMEM, stream, T, B, tiles,
-                 term, nz, traj);
+    AUXMC_LAUNCH((k_prefix_bulk<D, false>), grid, (G::WARPS + 1) * 32, G::SMEM, stream, T, B,
+                 tiles, term, nz, traj);
   }
   return AUXMC_OK;
 }
