@@ -262,6 +262,40 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
     const double* X = xin(k) + slot * G::ROW + j * LS * D;
 #pragma unroll
     for (int i = 0; i < D; ++i) y[i] = 0.0;
+    if (full && G::VEC) {
+      // full superchunk: the LS offsets c_t are independent — realize them all
+      // first, then run the dependent chain y = G_t y + c_t (same arithmetic)
+#pragma unroll
+      for (int s = LS - 1; s >= 0; --s) {
+        const int t = lo + s;
+        double xi[D];
+        if (PRE) {
+          lds_vec<D>(X + s * D, xi);
+        } else {
+          const uint64_t key = derive_index(klabel, (uint64_t)t);
+#pragma unroll
+          for (int i = 0; i < D; ++i) xi[i] = normal_at(key, (uint64_t)i);
+        }
+        double lv[D + G::LP];  // off | L packed
+        lds_vec<D + G::LP>(E + s * ES + D * D, lv);
+        int w = 0;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          double acc = 0.0;
+#pragma unroll
+          for (int cc = 0; cc <= r; ++cc) acc += lv[D + w++] * xi[cc];
+          cs[s * D + r] = lv[r] + acc;
+        }
+      }
+#pragma unroll
+      for (int s = LS - 1; s >= 0; --s) {
+        double gm[D * D], gy[D];
+        lds_vec<D * D>(E + s * ES, gm);
+        r_matvec<D>(gm, y, gy);
+#pragma unroll
+        for (int r = 0; r < D; ++r) y[r] = gy[r] + cs[s * D + r];
+      }
+    } else {
 #pragma unroll
     for (int s = LS - 1; s >= 0; --s) {
       const int t = lo + s;
@@ -302,6 +336,7 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
 #pragma unroll
         for (int r = 0; r < D; ++r) cs[s * D + r] = 0.0;
       }
+    }
     }
     double yn[D], gy[D];  // suffix Kogge-Stone: y -> c over [j, group end)
     shfl_down_vec<D>(y, yn, 8);
@@ -344,14 +379,28 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
         double x[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = carry[slot * D + i];
-        for (int w = W - 1; w >= 0; --w) {
+        // warps whose sub-chunks start at or past t1 (partial last superchunk) pass x through
+        const int wlive = min(W, (t1 - t0 + 4 * LS - 1) / (4 * LS));
+        for (int w = W - 1; w >= wlive; --w) {
 #pragma unroll
           for (int i = 0; i < D; ++i) xwtop[(w * G::SLOTS + slot) * CS + i] = x[i];
-          if (t0 + 4 * w * LS >= t1) continue;
-          double gx[D];
-          r_matvec<D>(gin + 4 * w * D * D, x, gx);
+        }
 #pragma unroll
-          for (int i = 0; i < D; ++i) x[i] = gx[i] + ca[(w * G::SLOTS + slot) * CS + i];
+        for (int w = W - 1; w >= 0; --w) {
+          if (w < wlive) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) xwtop[(w * G::SLOTS + slot) * CS + i] = x[i];
+            double gm[D * D], gx[D];
+            if constexpr (G::VEC) {
+              lds_vec<D * D>(gin + 4 * w * D * D, gm);
+            } else {
+#pragma unroll
+              for (int i = 0; i < D * D; ++i) gm[i] = gin[4 * w * D * D + i];
+            }
+            r_matvec<D>(gm, x, gx);
+#pragma unroll
+            for (int i = 0; i < D; ++i) x[i] = gx[i] + ca[(w * G::SLOTS + slot) * CS + i];
+          }
         }
 #pragma unroll
         for (int i = 0; i < D; ++i) carry[slot * D + i] = x[i];
@@ -377,6 +426,24 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
       for (int i = 0; i < D; ++i) x[i] = q < 3 ? xn[i] : xt[i];
       double* XO = xo + slot * G::ROW + j * LS * D;
       const bool live = slot < G::ROWS;
+      if (full && G::VEC) {
+        double xs[LS * D];
+#pragma unroll
+        for (int s = LS - 1; s >= 0; --s) {
+          double gm[D * D], gx[D];
+          lds_vec<D * D>(E + s * ES, gm);
+          r_matvec<D>(gm, x, gx);
+#pragma unroll
+          for (int i = 0; i < D; ++i) x[i] = gx[i] + csA[s * D + i];
+#pragma unroll
+          for (int i = 0; i < D; ++i) xs[s * D + i] = x[i];
+        }
+        if (live) {
+#pragma unroll
+          for (int i = 0; i < LS * D; i += 2)
+            *reinterpret_cast<double2*>(XO + i) = make_double2(xs[i], xs[i + 1]);
+        }
+      } else
 #pragma unroll
       for (int s = LS - 1; s >= 0; --s) {
         const int t = lo + s;
