@@ -175,7 +175,11 @@ def c2_e2e(args, st, steps, warmup, world):
     else:
         h_in.append((noise.terminal.cpu().pin_memory(), torch.empty_like(noise.terminal)))
         h_in.append((noise.backward.cpu().pin_memory(), torch.empty_like(noise.backward)))
-        d_noise = lgssm.Noise(terminal=h_in[0][1], backward=h_in[1][1])
+        bridge = None
+        if noise.bridge is not None:  # DnC bridge variates
+            h_in.append((noise.bridge.cpu().pin_memory(), torch.empty_like(noise.bridge)))
+            bridge = h_in[2][1]
+        d_noise = lgssm.Noise(terminal=h_in[0][1], backward=h_in[1][1], bridge=bridge)
     h_out = torch.empty(st["out"].shape, dtype=torch.float64).pin_memory()
     h2d = sum(h.numel() * h.element_size() for h in (h_fm, h_fc, h_pc, h_lm)) + \
         sum(h.numel() * h.element_size() for h, _ in h_in)
@@ -317,13 +321,15 @@ def run_c2(args, rank, world, local):
     pk = peaks()
     bytes_per_ct = (16 * d if args.noise == "predrawn" else 8 * d) if st["sampler"] == 1 else \
         (32 * d if st["sampler"] == 2 else 16 * d)
-    kernel_ms = tot.value / max(cnt.value, 1)
-    launch_bytes = bytes_per_ct * C * (T + 1)
-    achieved = launch_bytes / (kernel_ms / 1e3) / 1e9 if cnt.value else None
+    # the hot kernel's device time per step (DnC: all level launches of a sweep)
+    kernel_ms = tot.value / max(args.steps, 1)
+    step_bytes = bytes_per_ct * C * (T + 1)
+    achieved = step_bytes / (kernel_ms / 1e3) / 1e9 if cnt.value else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
             "frac": (achieved / pk["hbm_gbs"]) if achieved else None,
             "traffic": ncu_traffic(f"{hot}:{args.noise}:{T}:{C}"),
-            "kernel": hot, "kernel_ms": kernel_ms, "kernel_share_of_step":
+            "kernel": hot, "kernel_ms": kernel_ms,
+            "kernel_launches_per_step": cnt.value / max(args.steps, 1), "kernel_share_of_step":
                 (tot.value / ms) if ms else None,
             "algorithmic_bytes_per_chain_timestep": bytes_per_ct,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else "")}

@@ -242,6 +242,10 @@ int auxmc_sample_paths(const auxmc_lgssm* model, const auxmc_filter_result* fr, 
   if (noise->kind == AUXMC_NOISE_PREDRAWN &&
       (!noise->terminal || (model->T > 0 && !noise->backward)))
     return AUXMC_E_ARG;
+  // DnC with pre-drawn variates needs the bridge draws (one row per heap id)
+  if (noise->kind == AUXMC_NOISE_PREDRAWN && sampler == AUXMC_SAMPLER_DNC && model->T > 1 &&
+      (!noise->bridge || noise->n_bridge < auxmc_dnc_bridge_count(model->T)))
+    return AUXMC_E_ARG;
   if (B == 0) return AUXMC_OK;
   if (!workspace) return AUXMC_E_WORKSPACE;
   Arena ws{(char*)workspace, workspace_bytes, 0};

@@ -309,3 +309,15 @@ def test_parallel_filter_batched_long(gpu, oracle):
     for b in range(2):
         assert_close(fr.filt_mean[b].cpu(), seq.filt_mean, 1e-8, "filt_mean")
         assert_close(fr.log_marginal[b].cpu(), seq.log_marginal, 1e-9, "log_marginal")
+
+
+def test_dnc_predrawn_requires_bridge_draws(gpu, oracle):
+    """Pre-drawn DnC without the bridge variates is an argument error (AUXMC_E_ARG),
+    never a read through a null pointer."""
+    lgssm, _, _ = gpu
+    m, obs = _oracle_case(oracle, 20, 2, 1, False, False, 3)
+    gm = to_gpu_model(m)
+    fr = lgssm.kalman_filter(gm, obs)
+    term, back, _ = predrawn(np.random.default_rng(0), 2, m.T, m.dx, 32)
+    with pytest.raises(Exception):
+        lgssm.PathSampler(gm, 2, 2, True)(fr, lgssm.Noise.predrawn(term, back, None))
