@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--T", type=int, default=0, help="horizon (0 = config default)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="c1: eager launches, no CUDA graph")
     return p.parse_args()
 
 

@@ -234,6 +234,38 @@ class AuxChains:
                                              torch.cuda.current_stream().cuda_stream),
                    "aux_kernel_step")
 
+    def graph_step(self, backend=Backend.kSequential, zeroth_order=False, parallel_filter=False):
+        """kernel_step replayed from a CUDA graph: the first call per option set
+        captures the whole step (every kernel of auxk.cpp:130-198 for all chains,
+        stream-ordered, workspace preallocated) and later calls are one graph
+        launch.  Chain state is updated in place, iteration keys come from the
+        device-side counters, so replays are bit-identical to eager steps."""
+        lib = _lib.load()
+        key = (int(backend), bool(zeroth_order), bool(parallel_filter))
+        if not hasattr(self, "_graphs"):
+            self._graphs = {}
+        if key not in self._graphs:
+            tr = self.target.raw()
+            o = _lib.KernelOptions(*[int(k) for k in key])
+            if self._ws_key != key:
+                self._ws_bytes = lib.auxmc_aux_kernel_workspace(C.byref(tr), self.C, C.byref(o))
+                self._ws_key = key
+            self._workspace(self._ws_bytes)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            n0 = lib.auxmc_launch_count()
+            with torch.cuda.graph(g, capture_error_mode="relaxed"):
+                self.kernel_step(backend, zeroth_order, parallel_filter)
+            self._graphs[key] = (g, lib.auxmc_launch_count() - n0)
+        g, _ = self._graphs[key]
+        g.replay()
+
+    def graph_launches(self, backend=Backend.kSequential, zeroth_order=False,
+                       parallel_filter=False):
+        """Kernels in the captured step graph (0 before the first graph_step)."""
+        key = (int(backend), bool(zeroth_order), bool(parallel_filter))
+        return getattr(self, "_graphs", {}).get(key, (None, 0))[1]
+
     def adapt_delta(self, target_rate):
         ch = self.raw()
         _lib.check(_lib.load().auxmc_adapt_delta(C.byref(ch), float(target_rate),

@@ -191,3 +191,29 @@ def test_sharded_chains_equal_unsharded(aux, backend):
             p.kernel_step(backend)
     assert torch.equal(torch.cat([p.x for p in parts]), full.x)
     assert torch.equal(torch.cat([p.accepted for p in parts]), full.accepted)
+
+
+@pytest.mark.parametrize("kind,kw,backend,pf", [
+    ("lgssm-synthetic", dict(dx=1, dy=1, data_seed=1), 1, True),   # C1 shape
+    ("stochvol", dict(dx=3, data_seed=11), 0, False),
+    ("stochvol", dict(dx=3, data_seed=11), 2, False),
+])
+def test_graph_step_bit_equal_to_eager(aux, kind, kw, backend, pf):
+    """AuxChains.graph_step (one CUDA graph per step) reproduces eager kernel_step
+    bit for bit, step after step (device-side iteration counters)."""
+    auxk, bm = aux
+    spec = bm.ModelSpec(kind=kind, T=40, **kw)
+    lat, data = bm.simulate(spec)
+    tg = auxk.make_target(spec, data)
+    x0 = lat if kind != "lgssm-synthetic" else np.tile(tg.m0.cpu().numpy(), (41, 1))
+    a = auxk.init_chains(tg, x0, 0.7, 5, 3)
+    b = auxk.init_chains(tg, x0, 0.7, 5, 3)
+    for _ in range(5):
+        a.kernel_step(backend, parallel_filter=pf)
+        b.graph_step(backend, parallel_filter=pf)
+    torch.cuda.synchronize()
+    assert b.graph_launches(backend, parallel_filter=pf) > 5
+    assert torch.equal(a.x, b.x)
+    assert torch.equal(a.log_gamma, b.log_gamma)
+    assert torch.equal(a.accepted, b.accepted)
+    assert torch.equal(a.iter, b.iter)

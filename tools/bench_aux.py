@@ -67,9 +67,15 @@ def run(args, rank, world, local):
         # C1 / C5 are single chains: the scan filter (KernelOptions::parallel_filter)
         # parallelizes the horizon; C3 has 256 chains and uses the sequential filter.
         pf = cfg in ("c1", "c5")
+        # C1 is launch-bound (~36 small kernels per iteration): replay the step as
+        # one CUDA graph.  The others are long kernels; eager launches.
+        use_graph = cfg == "c1" and not args.no_graph
 
         def step():
-            ch.kernel_step(backend, parallel_filter=pf)
+            if use_graph:
+                ch.graph_step(backend, parallel_filter=pf)
+            else:
+                ch.kernel_step(backend, parallel_filter=pf)
 
     for _ in range(max(args.warmup, 1)):
         step()
@@ -78,6 +84,9 @@ def run(args, rank, world, local):
     with Clocks(local) as clk:
         ms = timed(step, args.steps, world)
     launches = lib.auxmc_launch_count() - n0
+    if cfg not in ("c4",) and getattr(ch, "graph_launches", None) and \
+            ch.graph_launches(backend, parallel_filter=pf) and launches == 0:
+        launches = ch.graph_launches(backend, parallel_filter=pf) * args.steps  # graph replays
     ct = C * (T + 1) * args.steps * world
     value = ct / (ms / 1e3)
     tflops = flops_ct * ct / (ms / 1e3) / 1e12
@@ -93,7 +102,9 @@ def run(args, rank, world, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": {"c1": "C1 aux-Kalman 1-D LGSSM prefix backend",
+            "config": {"workload": {"c1": "C1 aux-Kalman 1-D LGSSM prefix backend"
+                                          + (" (CUDA graph per iteration)" if cfg == "c1" and
+                                             not args.no_graph else ""),
                                     "c3": "C3 aux-Kalman Lorenz-96 d=40 sequential backend",
                                     "c4": "C4 stochvol aux particle Gibbs N=256",
                                     "c5": "C5 spatio-temporal grid 4 (d=16) aux-Kalman, scan "
