@@ -494,6 +494,46 @@ __global__ void k_pf_apply(int T, int B, int LB, const double* __restrict__ el,
   }
 }
 
+// Small horizons: the whole scan of one sequence in one CTA, with the
+// reference's own Sklansky fan (scan.hpp:22-41: at stride s, element j with
+// bit s set absorbs the prefix ending at (j & ~(s-1)) - 1), elements resident
+// in shared memory; ⌈log2 n⌉ barriers instead of the three launches and ~3
+// sqrt(n) sequential combines of the blocked scan.
+template <int D>
+__global__ void __launch_bounds__(D == 1 ? 1024 : 256) k_pf_sklansky(int T, int B, const double* __restrict__ el,
+                                                      double* filt_mean, double* filt_cov) {
+  extern __shared__ double sm[];
+  constexpr int ES = fe_size<D>();
+  const int n = T + 1, b = blockIdx.x;
+  const double* base = el + (size_t)b * n * ES;
+  for (int i = threadIdx.x; i < n * ES; i += blockDim.x) sm[i] = base[i];
+  __syncthreads();
+  for (int stride = 1; stride < n; stride <<= 1) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      if (!(j & stride)) continue;
+      const int pivot = (j & ~(stride - 1)) - 1;
+      FElem<D> u, v, o;
+      fe_load<D>(sm + (size_t)pivot * ES, u);
+      fe_load<D>(sm + (size_t)j * ES, v);
+      fe_combine<D>(u, v, o);  // a level writes only bit-set slots and reads only pivots
+      fe_store<D>(sm + (size_t)j * ES, o);
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) filt_mean[((size_t)b * n + t) * D + i] = sm[(size_t)t * ES + D * D + i];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i)
+      filt_cov[((size_t)b * n + t) * D * D + i] = sm[(size_t)t * ES + D * D + D + i];
+  }
+}
+
+template <int D>
+constexpr int sklansky_max_n() {
+  return (200 * 1024) / (int)(sizeof(double) * fe_size<D>());
+}
+
 // recovery (pit.cpp:167-186): predictive moments from filt[t-1]; log-likelihood terms
 template <int D>
 __global__ void k_pf_recover(DevModel m, const double* __restrict__ obs, int B,
@@ -661,10 +701,19 @@ static int run_pf(const DevModel& dm, const double* obs, int B, auxmc_filter_res
   const long long nb = (long long)B * nblk;
   auto grid = [](long long k) { return (int)std::max(1LL, std::min((k + 127) / 128, 148LL * 16)); };
   AUXMC_LAUNCH(k_pf_elements<D>, grid(n), 128, 0, s, dm, obs, B, el, status);
-  AUXMC_LAUNCH(k_pf_reduce<D>, grid(nb), 128, 0, s, T, B, LB, el, agg);
-  AUXMC_LAUNCH(k_pf_carry<D>, (B + 127) / 128, 128, 0, s, T, B, LB, agg, carry);
-  AUXMC_LAUNCH(k_pf_apply<D>, grid(nb), 128, 0, s, T, B, LB, el, carry, out->filt_mean,
-               out->filt_cov);
+  if (T + 1 <= sklansky_max_n<D>() && B <= 2 * 148) {
+    // few short sequences: one CTA each, Sklansky in shared memory
+    const size_t smem = sizeof(double) * (size_t)(T + 1) * ES;
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pf_sklansky<D>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int threads = std::min(D == 1 ? 1024 : 256, std::max(32, ((T + 1 + 31) / 32) * 32));
+    AUXMC_LAUNCH(k_pf_sklansky<D>, B, threads, smem, s, T, B, el, out->filt_mean, out->filt_cov);
+  } else {
+    AUXMC_LAUNCH(k_pf_reduce<D>, grid(nb), 128, 0, s, T, B, LB, el, agg);
+    AUXMC_LAUNCH(k_pf_carry<D>, (B + 127) / 128, 128, 0, s, T, B, LB, agg, carry);
+    AUXMC_LAUNCH(k_pf_apply<D>, grid(nb), 128, 0, s, T, B, LB, el, carry, out->filt_mean,
+                 out->filt_cov);
+  }
   AUXMC_LAUNCH(k_pf_recover<D>, grid(n), 128, 0, s, dm, obs, B, out->filt_mean, out->filt_cov,
                out->pred_mean, out->pred_cov, terms, status);
   AUXMC_LAUNCH(k_pf_sum, B, kSumThreads, 0, s, T, B, terms, out->log_marginal);
