@@ -387,7 +387,8 @@ __global__ void k_pit_forward_backward(DevTarget tg, FactorRef f, PgArgs a, cons
   double* cum = W + N;           // N
   double* mprev = cum + N;       // N*d dynamics means of the previous particles
   double* red = mprev + (size_t)N * d;  // 40
-  double* chosen = red + 40;     // d
+  double* chosen = red + 40;     // d (<= 64)
+  double* partial = chosen + 64; // (blockDim / N) * N partial sums
   const double* P = a.part + (size_t)c * (T + 1) * N * d;
   const double* LW = lw + (size_t)c * (T + 1) * N;
   double* A = a.Wt + (size_t)c * (T + 1) * N;
@@ -411,88 +412,145 @@ __global__ void k_pit_forward_backward(DevTarget tg, FactorRef f, PgArgs a, cons
     const int jq = jq0 + (f.fl.nQ > 1 ? t - 1 : 0);
     const double* LQ = f.L(jq);
     const double ldq = f.logdet[jq];
+    if constexpr (DT > 0) {
+      // Whitened form: with v_i = L_Q^{-1} m_i (previous particles' dynamics
+      // means) and w_j = L_Q^{-1} x_t^j, log p(x_t^j | x_{t-1}^i) = M - |w_j - v_i|^2 / 2,
+      // M = -d/2 log 2π - log|L_Q|: no triangular solve (and no division) per pair.
+      // Every term is <= M and alpha - am <= 0, so exp(.) never overflows; P
+      // thread groups split the i range (fixed order partial sums).
+      double* vi = mprev;  // N*DT, whitened in place
+      double* ai = cum;    // alpha_i - am
+      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        double z[DT];
+#pragma unroll
+        for (int k = 0; k < DT; ++k) {
+          double acc = mprev[i * DT + k];
+#pragma unroll
+          for (int l = 0; l < k; ++l) acc -= LQ[k * DT + l] * z[l];
+          z[k] = acc / LQ[k * DT + k];
+        }
+#pragma unroll
+        for (int k = 0; k < DT; ++k) vi[i * DT + k] = z[k];
+        ai[i] = alpha[i] - am;
+      }
+      __syncthreads();
+      const double M = -0.5 * (DT * kLog2Pi) - ldq;
+      const int parts = blockDim.x / N > 0 ? blockDim.x / N : 1;
+      const int part = threadIdx.x / N;
+      const int ilo = part * (N / parts), ihi = part == parts - 1 ? N : ilo + N / parts;
+      for (int j = threadIdx.x % N; j < N && part < parts; j += (blockDim.x < N ? blockDim.x : N)) {
+        const double* xj = P + ((size_t)t * N + j) * DT;
+        double w[DT];
+#pragma unroll
+        for (int k = 0; k < DT; ++k) {
+          double acc = xj[k];
+#pragma unroll
+          for (int l = 0; l < k; ++l) acc -= LQ[k * DT + l] * w[l];
+          w[k] = acc / LQ[k * DT + k];
+        }
+        double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+        int i = ilo;
+        for (; i + 4 <= ihi; i += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            double sq = 0.0;
+#pragma unroll
+            for (int k = 0; k < DT; ++k) {
+              const double z = w[k] - vi[(i + u) * DT + k];
+              sq += z * z;
+            }
+            acc4[u] += exp(ai[i + u] - 0.5 * sq);
+          }
+        }
+        for (; i < ihi; ++i) {
+          double sq = 0.0;
+#pragma unroll
+          for (int k = 0; k < DT; ++k) {
+            const double z = w[k] - vi[i * DT + k];
+            sq += z * z;
+          }
+          acc4[0] += exp(ai[i] - 0.5 * sq);
+        }
+        const double sp = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+        if (parts == 1) {
+          double s = sp, m = 0.0;
+          if (!(s > 0.0)) {  // total underflow: exact online log-sum-exp relative to M
+            m = -INFINITY;
+            s = 0.0;
+            for (int i2 = 0; i2 < N; ++i2) {
+              double sq = 0.0;
+#pragma unroll
+              for (int k = 0; k < DT; ++k) {
+                const double z = w[k] - vi[i2 * DT + k];
+                sq += z * z;
+              }
+              const double v = ai[i2] - 0.5 * sq;
+              if (v > m) {
+                s = s * exp(m - v) + 1.0;
+                m = v;
+              } else {
+                s += exp(v - m);
+              }
+            }
+          }
+          W[j] = LW[(size_t)t * N + j] + (am + ((M + m) + log(s)));
+        } else {
+          partial[part * N + j] = sp;
+        }
+      }
+      if (parts > 1) {
+        __syncthreads();
+        for (int j = threadIdx.x; j < N; j += blockDim.x) {
+          double s = 0.0;
+          for (int p2 = 0; p2 < parts; ++p2) s += partial[p2 * N + j];
+          double m = 0.0;
+          if (!(s > 0.0)) {
+            const double* xj = P + ((size_t)t * N + j) * DT;
+            double w[DT];
+#pragma unroll
+            for (int k = 0; k < DT; ++k) {
+              double acc = xj[k];
+#pragma unroll
+              for (int l = 0; l < k; ++l) acc -= LQ[k * DT + l] * w[l];
+              w[k] = acc / LQ[k * DT + k];
+            }
+            m = -INFINITY;
+            s = 0.0;
+            for (int i2 = 0; i2 < N; ++i2) {
+              double sq = 0.0;
+#pragma unroll
+              for (int k = 0; k < DT; ++k) {
+                const double z = w[k] - vi[i2 * DT + k];
+                sq += z * z;
+              }
+              const double v = ai[i2] - 0.5 * sq;
+              if (v > m) {
+                s = s * exp(m - v) + 1.0;
+                m = v;
+              } else {
+                s += exp(v - m);
+              }
+            }
+          }
+          W[j] = LW[(size_t)t * N + j] + (am + ((M + m) + log(s)));
+        }
+      }
+    } else {
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
       const double* xj = P + ((size_t)t * N + j) * d;
       double m = -INFINITY, s = 0.0;  // online log-sum-exp over i
-      if constexpr (DT > 0) {
-        // register path: x_t^j and the lower factor of Q held in registers
-        double xr[DT], Lr[DT * DT];
-#pragma unroll
-        for (int k = 0; k < DT; ++k) xr[k] = xj[k];
-#pragma unroll
-        for (int k = 0; k < DT * DT; ++k) Lr[k] = LQ[k];
-        // Every transition log-density is <= M = -0.5 d log 2π - log|L_Q| and
-        // alpha - am <= 0, so exp(v - M) never overflows: four independent
-        // accumulators give ILP without a running max.  If everything
-        // underflows (s == 0) the exact online log-sum-exp below takes over.
-        const double M = -0.5 * (DT * kLog2Pi) - ldq;
-        double acc4[4] = {0.0, 0.0, 0.0, 0.0};
-        int i = 0;
-        for (; i + 4 <= N; i += 4) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            double z[DT], sq = 0.0;
-#pragma unroll
-            for (int k = 0; k < DT; ++k) {
-              double acc = xr[k] - mprev[(i + u) * DT + k];
-#pragma unroll
-              for (int l = 0; l < k; ++l) acc -= Lr[k * DT + l] * z[l];
-              z[k] = acc / Lr[k * DT + k];
-              sq += z[k] * z[k];
-            }
-            const double v = (alpha[i + u] - am) + (-0.5 * (DT * kLog2Pi + sq) - ldq);
-            acc4[u] += exp(v - M);
-          }
-        }
-        for (; i < N; ++i) {
-          double z[DT], sq = 0.0;
-#pragma unroll
-          for (int k = 0; k < DT; ++k) {
-            double acc = xr[k] - mprev[i * DT + k];
-#pragma unroll
-            for (int l = 0; l < k; ++l) acc -= Lr[k * DT + l] * z[l];
-            z[k] = acc / Lr[k * DT + k];
-            sq += z[k] * z[k];
-          }
-          acc4[0] += exp((alpha[i] - am) + (-0.5 * (DT * kLog2Pi + sq) - ldq) - M);
-        }
-        s = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-        m = M;
-        if (!(s > 0.0)) {  // total underflow: exact online log-sum-exp
-          m = -INFINITY;
-          s = 0.0;
-          for (int i2 = 0; i2 < N; ++i2) {
-            double z[DT], sq = 0.0;
-#pragma unroll
-            for (int k = 0; k < DT; ++k) {
-              double acc = xr[k] - mprev[i2 * DT + k];
-#pragma unroll
-              for (int l = 0; l < k; ++l) acc -= Lr[k * DT + l] * z[l];
-              z[k] = acc / Lr[k * DT + k];
-              sq += z[k] * z[k];
-            }
-            const double v = (alpha[i2] - am) + (-0.5 * (DT * kLog2Pi + sq) - ldq);
-            if (v > m) {
-              s = s * exp(m - v) + 1.0;
-              m = v;
-            } else {
-              s += exp(v - m);
-            }
-          }
-        }
-      } else {
-        for (int i = 0; i < N; ++i) {
-          for (int k = 0; k < d; ++k) r[k] = xj[k] - mprev[i * d + k];
-          const double v = (alpha[i] - am) + gauss_term(d, r, LQ, ldq);
-          if (v > m) {
-            s = s * exp(m - v) + 1.0;
-            m = v;
-          } else {
-            s += exp(v - m);
-          }
+      for (int i = 0; i < N; ++i) {
+        for (int k = 0; k < d; ++k) r[k] = xj[k] - mprev[i * d + k];
+        const double v = (alpha[i] - am) + gauss_term(d, r, LQ, ldq);
+        if (v > m) {
+          s = s * exp(m - v) + 1.0;
+          m = v;
+        } else {
+          s += exp(v - m);
         }
       }
       W[j] = LW[(size_t)t * N + j] + (am + (m + log(s)));
+    }
     }
     __syncthreads();
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
@@ -623,14 +681,17 @@ static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int variant, Arena&
     const long long np = nct * N;
     AUXMC_LAUNCH(k_pit_particles, (int)std::min<long long>((np + 255) / 256, 148LL * 64), 256, 0, s,
                  tg, f, a, lw);
-    const size_t smem = sizeof(double) * (3 * N + (size_t)N * d + 40 + 64);
+    // PIT forward: 2 thread groups split each LSE for N = 256 (16 warps per SM)
+    const int pthreads = N <= 512 ? std::min(1024, 2 * ((N + 31) / 32) * 32) : threads;
+    const size_t smem = sizeof(double) * (3 * N + (size_t)N * d + 40 + 64 +
+                                          (size_t)std::max(1, pthreads / N) * N);
     switch (d) {
 #define PCASE(DT)                                                                        \
   case DT:                                                                               \
     AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pit_forward_backward<DT>,                      \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                                         (int)smem));                                     \
-    AUXMC_LAUNCH((k_pit_forward_backward<DT>), C, threads, smem, s, tg, f, a, lw);       \
+    AUXMC_LAUNCH((k_pit_forward_backward<DT>), C, pthreads, smem, s, tg, f, a, lw);      \
     break;
       PCASE(1) PCASE(2) PCASE(3) PCASE(4) PCASE(5) PCASE(6) PCASE(7) PCASE(8)
 #undef PCASE

@@ -48,7 +48,11 @@ def run(args, rank, world, local):
         spec = bm.ModelSpec(kind="stochvol", T=T, dx=3, data_seed=11)
         delta = 1.0
         N = 256
-        flops_ct = N * N * (3 * d * d + d + 20.0)
+        # per (i, j) pair after whitening (L_Q^{-1} applied once per particle, not per
+        # pair): d differences + d squares/FMAs + 2 scale/adds + exp (counted as 20
+        # flops) + accumulate — the minimal structure-aware count, below SURVEY's
+        # N^2 (3d^2 + d + exp) which assumed a triangular solve per pair
+        flops_ct = N * N * (2 * d + 3 + 20.0)
     lat, data = bm.simulate(spec)
     tg = auxk.make_target(spec, data, device=device)
     x0 = torch.as_tensor(lat, device=device) if cfg != "c1" else \
