@@ -15,7 +15,7 @@ far larger than the 126 MB L2, so no explicit flush is needed between steps.
 Under torchrun each rank runs its own chains; the step time is the max over
 ranks (CUDA events, barrier + synchronize on both sides).  Rank 0 prints one
 JSON line.  `--impl reference` times the reference algorithm on the host
-cores instead (oracle/_ref when built, else the oracle port) on rank 0.
+cores instead (the oracle port of the reference algorithm) on rank 0.
 """
 from __future__ import annotations
 
@@ -227,8 +227,9 @@ def timed(fn, steps, world):
 
 
 def cpu_reference_prefix(T, d, n_chains, threads, sampler="prefix", seed=1):
-    """Time the CPU reference algorithm (oracle/_ref if built, else the oracle
-    port) on n_chains chains of the C2 workload; returns (ct/s, seconds, kind)."""
+    """Time the CPU reference algorithm (the oracle port: the reference itself
+    cannot be compiled here, Eigen3 is absent) on n_chains chains of the C2
+    workload; returns (ct/s, seconds, kind)."""
     import concurrent.futures as cf
     from oracle import pyoracle as O
     kind = "port"
@@ -237,13 +238,6 @@ def cpu_reference_prefix(T, d, n_chains, threads, sampler="prefix", seed=1):
     m = O.synthetic_lgssm(s)
     fr = O.kalman_filter(m, data)
     fn = {"prefix": O.prefix_sample, "seq": O.backward_sample, "dnc": O.dnc_sample}[sampler]
-    try:
-        from oracle import ref_runner  # compiled reference via the Eigen shim (oracle/_ref)
-        if ref_runner.available():
-            kind = "reference"
-            fn = ref_runner.sampler(sampler, m, fr)
-    except Exception:
-        pass
 
     def one(c):
         return fn(m, fr, O.stream_noise(O.derive(O.from_seed(seed), O.L_CHAIN, c)))
