@@ -256,23 +256,51 @@ __device__ __forceinline__ void g_dmma(const Grp& g, int m, int k, int n, const 
       if (two && c1c + 1 < n) c11 = C[r * ldc + c1c + 1];
     }
     const int b0 = Jt * 8 + gi, b1 = b0 + 8;
-    for (int K = 0; K < kt; ++K) {
-      const int kk = K * 4 + ti;
-      double a = 0.0, x0 = 0.0, x1 = 0.0;
-      if (r < m && kk < k) a = TA ? A[kk * lda + r] : A[r * lda + kk];
-      if (kk < k) {
-        if (b0 < n) x0 = TB ? B[b0 * ldb + kk] : B[kk * ldb + b0];
-        if (two && b1 < n) x1 = TB ? B[b1 * ldb + kk] : B[kk * ldb + b1];
+    const double sg = sub ? -1.0 : 1.0;
+    // interior tiles (the common case): unguarded fragment loads, pointer walks
+    const bool inner = (k & 3) == 0 && It * 8 + 8 <= m && Jt * 8 + (two ? 16 : 8) <= n;
+    if (inner) {
+      const double* pa = TA ? A + ti * lda + r : A + r * lda + ti;
+      const double* p0 = TB ? B + b0 * ldb + ti : B + ti * ldb + b0;
+      const double* p1 = TB ? B + b1 * ldb + ti : B + ti * ldb + b1;
+      const int sa = TA ? 4 * lda : 4, sb = TB ? 4 : 4 * ldb;
+#pragma unroll 2
+      for (int K = 0; K < kt; ++K) {
+        const double a = sg * pa[0];
+        const double x0 = p0[0];
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+            : "+d"(c00), "+d"(c01)
+            : "d"(a), "d"(x0));
+        if (two) {
+          const double x1 = p1[0];
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(c10), "+d"(c11)
+              : "d"(a), "d"(x1));
+        }
+        pa += sa;
+        p0 += sb;
+        p1 += sb;
       }
-      if (sub) a = -a;
-      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                   : "+d"(c00), "+d"(c01)
-                   : "d"(a), "d"(x0));
-      if (two)
+    } else {
+      for (int K = 0; K < kt; ++K) {
+        const int kk = K * 4 + ti;
+        double a = 0.0, x0 = 0.0, x1 = 0.0;
+        if (r < m && kk < k) a = TA ? A[kk * lda + r] : A[r * lda + kk];
+        if (kk < k) {
+          if (b0 < n) x0 = TB ? B[b0 * ldb + kk] : B[kk * ldb + b0];
+          if (two && b1 < n) x1 = TB ? B[b1 * ldb + kk] : B[kk * ldb + b1];
+        }
+        a = sg * a;
         asm volatile(
             "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-            : "+d"(c10), "+d"(c11)
-            : "d"(a), "d"(x1));
+            : "+d"(c00), "+d"(c01)
+            : "d"(a), "d"(x0));
+        if (two)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(c10), "+d"(c11)
+              : "d"(a), "d"(x1));
+      }
     }
     if (r < m) {
       if (c0c < n && (!lower || c0c <= r))
