@@ -298,7 +298,7 @@ def run_c2(args, rank, world, local):
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
-    hot = {1: "k_prefix", 2: "k_dnc_level", 0: "k_seq_sample"}[st["sampler"]]
+    hot = {1: "k_prefix", 2: "k_dnc_", 0: "k_seq_sample"}[st["sampler"]]
     launches0 = lib.auxmc_launch_count()
     lib.auxmc_profile_begin()
     with Clocks(local) as clk:

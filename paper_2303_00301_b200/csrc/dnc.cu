@@ -261,6 +261,185 @@ __global__ void k_dnc_level(int T, int B, int fr_shared, int level,
   }
 }
 
+// Deep levels.  Each bridge is affine in its end states:
+//   x_m = mu + K (x_l - G_l mu - c_l) + L xi,  mu = G_r x_r + c_r
+//       = A x_r + K x_l + a + L xi,  A = (I - K G_l) G_r,  a = (I - K G_l) c_r - K c_l,
+// with (A, a) chain-independent when the filter result is shared, precomputed
+// once per node (k_dnc_affine).  Every node at level L0 roots a subtree of at
+// most kDncSpan steps that needs only its two end states, so one CTA (thread =
+// chain) stages the subtree's node parameters in shared memory once and runs all
+// remaining levels with the chain's states in shared memory; each state is
+// written to HBM once, contiguously per chain, and only the subtree ends are read.
+constexpr int kDncSpan = 16;
+constexpr int kDncSubThreads = 128;
+
+template <int D>
+constexpr int dnc_aff_stride() {  // A | K | a | L per node, 16-B aligned
+  return (3 * D * D + D + 1) & ~1;
+}
+template <int D>
+constexpr int dnc_lane_stride() {  // odd (in doubles): conflict-free per-thread rows
+  return ((kDncSpan + 1) * D) | 1;
+}
+
+template <int D>
+__global__ void k_dnc_affine(int T, int Bfr, const double* __restrict__ nodes,
+                             const double* __restrict__ params, long long n_heap, long long h_lo,
+                             double* aff) {
+  constexpr int ES = (2 * D * D + D + 1) & ~1, AS = dnc_aff_stride<D>();
+  const long long n = (n_heap - h_lo) * Bfr;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(q / (n_heap - h_lo));
+    const uint64_t h = (uint64_t)(h_lo + q % (n_heap - h_lo));
+    int l, r;
+    if (!dnc_interval(h, T, l, r) || r - l < 2) continue;
+    const double* elm = nodes + ((size_t)b * n_heap + 2 * h) * ES;
+    const double* emr = nodes + ((size_t)b * n_heap + 2 * h + 1) * ES;
+    const double* K = params + ((size_t)b * n_heap + h) * 2 * D * D;
+    const double* L = K + D * D;
+    double* o = aff + ((size_t)b * n_heap + h) * AS;
+    double M[D * D];  // I - K G_l
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc += K[i * D + k] * elm[k * D + j];
+        M[i * D + j] = (i == j ? 1.0 : 0.0) - acc;
+      }
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc += M[i * D + k] * emr[k * D + j];
+        o[i * D + j] = acc;                 // A
+        o[D * D + i * D + j] = K[i * D + j];  // K
+        o[2 * D * D + D + i * D + j] = L[i * D + j];  // L
+      }
+      double acc = 0.0, acc2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        acc += M[i * D + k] * emr[D * D + k];
+        acc2 += K[i * D + k] * elm[D * D + k];
+      }
+      o[2 * D * D + i] = acc - acc2;  // a
+    }
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void dnc_noise_vec(const NoiseArgs& nz, int c, uint64_t h, int T,
+                                              double* xi) {
+  if (nz.kind == AUXMC_NOISE_PREDRAWN) {
+    const double* src = nz.bridge + ((size_t)c * nz.n_bridge + h) * D;
+    if constexpr (D % 2 == 0) {
+#pragma unroll
+      for (int i = 0; i < D; i += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(src + i);
+        xi[i] = v.x;
+        xi[i + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < D; ++i) xi[i] = src[i];
+    }
+  } else {
+    dnc_normals<D>(nz, c, kDncBridge, h, T, xi);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kDncSubThreads)
+    k_dnc_subtree(int T, int B, int fr_shared, int L0, int depth, const double* __restrict__ aff,
+                  long long n_heap, NoiseArgs nz, double* traj) {
+  extern __shared__ __align__(16) double smx[];
+  constexpr int AS = dnc_aff_stride<D>(), LSTR = dnc_lane_stride<D>();
+  double* pn = smx;  // kDncSpan node parameter blocks, indexed by local heap id
+  int* lrm = reinterpret_cast<int*>(smx + kDncSpan * AS);  // [kDncSpan] (l, r) or l = -1
+  double* xs = smx + kDncSpan * AS + kDncSpan + (size_t)threadIdx.x * LSTR;
+  const long long width = 1LL << L0;
+  const int cgroups = (B + kDncSubThreads - 1) / kDncSubThreads;
+  const long long n_items = width * cgroups;
+  const int n_local = 1 << (depth - L0);  // local ids 1 .. n_local-1, level order
+  for (long long q = blockIdx.x; q < n_items; q += gridDim.x) {
+    const int c = (int)(q % cgroups) * kDncSubThreads + threadIdx.x;
+    const bool live = c < B;
+    const uint64_t h0 = (uint64_t)width + (uint64_t)(q / cgroups);
+    int l0, r0;
+    if (!dnc_interval(h0, T, l0, r0) || r0 - l0 < 2) continue;  // CTA-uniform
+    const int fb = fr_shared ? 0 : (live ? c : 0);
+    __syncthreads();
+    for (int lid = 1 + threadIdx.x; lid < n_local; lid += blockDim.x) {
+      const int lev = 31 - __clz(lid);
+      const uint64_t h = (h0 << lev) + (uint64_t)(lid - (1 << lev));
+      int l, r;
+      const bool ok = dnc_interval(h, T, l, r) && r - l >= 2;
+      lrm[2 * lid] = ok ? l : -1;
+      lrm[2 * lid + 1] = r;
+    }
+    if (fr_shared)
+      for (int e = threadIdx.x; e < (n_local - 1) * AS; e += blockDim.x) {
+        const int lid = 1 + e / AS, o = e % AS;
+        const int lev = 31 - __clz(lid);
+        const uint64_t h = (h0 << lev) + (uint64_t)(lid - (1 << lev));
+        pn[lid * AS + o] = h < (uint64_t)n_heap ? aff[(size_t)h * AS + o] : 0.0;
+      }
+    __syncthreads();
+    if (!live) continue;
+    double* out = traj + (size_t)c * (T + 1) * D;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      xs[i] = out[(size_t)l0 * D + i];
+      xs[(r0 - l0) * D + i] = out[(size_t)r0 * D + i];
+    }
+    auto hid = [&](int lid) {
+      const int lev = 31 - __clz(lid);
+      return (h0 << lev) + (uint64_t)(lid - (1 << lev));
+    };
+    double xin[D];  // noise of the next node, loaded one node ahead
+    dnc_noise_vec<D>(nz, c, hid(1), T, xin);
+    for (int lid = 1; lid < n_local; ++lid) {
+      double xi[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) xi[j] = xin[j];
+      if (lid + 1 < n_local) dnc_noise_vec<D>(nz, c, hid(lid + 1), T, xin);
+      const int l = lrm[2 * lid], r = lrm[2 * lid + 1];
+      if (l < 0) continue;
+      const int m = (l + r) / 2;
+      const uint64_t h = hid(lid);
+      const double* P = fr_shared ? pn + lid * AS : aff + ((size_t)fb * n_heap + h) * AS;
+      double xl[D], xr[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        xl[j] = xs[(l - l0) * D + j];
+        xr[j] = xs[(r - l0) * D + j];
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double u = 0.0, v = 0.0, w = 0.0;
+#pragma unroll
+        for (int k2 = 0; k2 < D; ++k2) {
+          u += P[j * D + k2] * xr[k2];
+          v += P[D * D + j * D + k2] * xl[k2];
+          w += P[2 * D * D + D + j * D + k2] * xi[k2];
+        }
+        xs[(m - l0) * D + j] = ((u + v) + P[2 * D * D + j]) + w;
+      }
+    }
+    const int nv = (r0 - l0 - 1) * D;  // x_(l0+1) .. x_(r0-1), contiguous in the path
+    if constexpr (D % 2 == 0) {
+      double2* o2 = reinterpret_cast<double2*>(out + (size_t)(l0 + 1) * D);
+      for (int i = 0; i < nv / 2; ++i) o2[i] = make_double2(xs[D + 2 * i], xs[D + 2 * i + 1]);
+    } else {
+      for (int i = 0; i < nv; ++i) out[(size_t)(l0 + 1) * D + i] = xs[D + i];
+    }
+  }
+}
+
 // ---- any d (9..32): warp per (node, chain), lanes over rows; the dot products
 // run in the register kernels' order (ascending j), so results match them.
 constexpr int kDncWarps = 4;
@@ -369,8 +548,9 @@ int launch_dnc(const DevModel& dm, int Bfr, int fr_shared, const double* elems,
   const long long n_heap = 2LL << depth;  // ids < 2^(depth+1)
   double* nodes = ws.take<double>((size_t)Bfr * n_heap * ES);
   double* params = ws.take<double>((size_t)Bfr * n_heap * 2 * dd);
+  double* aff = d <= 8 ? ws.take<double>((size_t)Bfr * n_heap * ((3 * dd + d + 1) & ~1)) : nullptr;
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!nodes || !params) return AUXMC_E_WORKSPACE;
+  if (!nodes || !params || (d <= 8 && !aff)) return AUXMC_E_WORKSPACE;
   if (d > 32) return AUXMC_E_DIM;
   const bool block = d > 16;  // CTA groups (blocked DMMA factor/solves) for d > 16
   const int warps = 4;
@@ -421,16 +601,35 @@ int launch_dnc(const DevModel& dm, int Bfr, int fr_shared, const double* elems,
     }
     return AUXMC_OK;
   }
+  // levels >= L0 run as subtrees of at most kDncSpan steps (intervals at level L
+  // span at most ceil(T / 2^L) steps)
+  int L0 = 0;
+  while (L0 < depth && ((long long)T + (1LL << L0) - 1) / (1LL << L0) > kDncSpan) ++L0;
   switch (d) {
 #define CASE(D)                                                                              \
   case D: {                                                                                  \
     AUXMC_LAUNCH(k_dnc_ends<D>, (B + 127) / 128, 128, 0, stream, T, B, fr_shared, term, nodes, \
                  params, n_heap, nz, traj);                                                  \
-    for (int level = 0; level < depth; ++level) {                                            \
+    for (int level = 0; level < L0; ++level) {                                               \
       const long long n = (1LL << level) * B;                                                \
       const int grid = (int)std::min<long long>((n + 255) / 256, 148LL * 32);                \
       AUXMC_LAUNCH(k_dnc_level<D>, grid, 256, 0, stream, T, B, fr_shared, level, nodes,      \
                    params, n_heap, nz, traj);                                                \
+    }                                                                                        \
+    if (L0 < depth) {                                                                        \
+      const long long h_lo = 1LL << L0;                                                      \
+      const long long na = (n_heap - h_lo) * Bfr;                                            \
+      AUXMC_LAUNCH(k_dnc_affine<D>, (int)std::min<long long>((na + 255) / 256, 148LL * 32),  \
+                   256, 0, stream, T, Bfr, nodes, params, n_heap, h_lo, aff);                \
+      const size_t smem = sizeof(double) * (kDncSpan * dnc_aff_stride<D>() + kDncSpan +      \
+                                            (size_t)dnc_lane_stride<D>() * kDncSubThreads);  \
+      AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_dnc_subtree<D>,                                  \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                          (int)smem));                                       \
+      const long long n = (1LL << L0) * ((B + kDncSubThreads - 1) / kDncSubThreads);         \
+      const int grid = (int)std::min<long long>(n, 148LL * 16);                              \
+      AUXMC_LAUNCH(k_dnc_subtree<D>, grid, kDncSubThreads, smem, stream, T, B, fr_shared, L0, \
+                   depth, aff, n_heap, nz, traj);                                            \
     }                                                                                        \
     break;                                                                                   \
   }
