@@ -595,6 +595,26 @@ __device__ __forceinline__ void g_llt_solve(const Grp& g, int n, const double* L
     g_trsm_lower_t_blocked(g, n, L, dinv, r, B, r);
     return;
   }
+  if (!g.block && r <= 32) {
+    // one warp: lane c owns column c (conflict-free rows, broadcast L reads) and
+    // runs both substitutions without synchronization; same operation order as
+    // the row-synchronous form below (ascending / descending update sequences)
+    const int c = g.lane;
+    if (c < r) {
+      for (int i = 0; i < n; ++i) {
+        double v = B[i * r + c];
+        for (int j = 0; j < i; ++j) v -= L[i * n + j] * B[j * r + c];
+        B[i * r + c] = v / L[i * n + i];
+      }
+      for (int i = n - 1; i >= 0; --i) {
+        double v = B[i * r + c];
+        for (int j = n - 1; j > i; --j) v -= L[j * n + i] * B[j * r + c];
+        B[i * r + c] = v / L[i * n + i];
+      }
+    }
+    __syncwarp();
+    return;
+  }
   const int ny = g.ny();
   for (int c = g.lane; c < r; c += g.size) B[c] = B[c] / L[0];
   g.sync();
