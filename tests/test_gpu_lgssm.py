@@ -67,6 +67,9 @@ LARGE_CASES = [
     (3, 40, 60, True, False, 33),
     (100, 10, 3, True, True, 34),   # warp groups; several prefix blocks
     (33, 12, 12, False, False, 35),
+    (0, 10, 2, False, False, 39),   # edge horizons on the generic kernels
+    (1, 12, 3, True, False, 40),
+    (2, 9, 9, True, True, 41),
 ]
 
 
