@@ -119,6 +119,32 @@ int auxmc_kalman_filter(const auxmc_lgssm* model, const double* obs, int B, int 
                         size_t workspace_bytes, void* stream);
 size_t auxmc_kalman_filter_workspace(const auxmc_lgssm* model, int B, int mode);
 
+/* ---- time-sharded scan filter (pit::parallel_filter, pit.cpp:117-188, over G ranks)
+ * One observation sequence; the horizon's block tree (blocks of LB steps,
+ * super-blocks of SB = LB*LB steps, nsup of them) depends only on T.  A rank owns
+ * the super-blocks [sup_lo, sup_hi) (contiguous, any split) and runs:
+ *   1. auxmc_tshard_filter_local: elements, block and super-block aggregates of its
+ *      range; writes its (sup_hi - sup_lo) aggregates, elem_doubles each, to sup_out;
+ *   2. the caller all-gathers every rank's aggregates, in super-block order, into
+ *      sup_all (nsup * elem_doubles) — the only exchange;
+ *   3. auxmc_tshard_filter_finish: carries, filtered and predictive moments for
+ *      t in [sup_lo*SB, min(sup_hi*SB, T+1)) (plus the predictive moments at the
+ *      range end) written into full-length result arrays, and the log-likelihood
+ *      partial sum of each owned super-block into ll_out;
+ *   4. log_marginal = auxmc_tshard_sum over all ranks' partials in order.
+ * Every split (G = 1, 2, 4, 8, ...) gives bit-identical results. */
+int auxmc_tshard_geometry(int T, int dx, int* LB, int* nblk, int* nsup, int* SB,
+                          int* elem_doubles);
+size_t auxmc_tshard_filter_workspace(const auxmc_lgssm* model);
+int auxmc_tshard_filter_local(const auxmc_lgssm* model, const double* obs, int sup_lo,
+                              int sup_hi, void* workspace, size_t workspace_bytes,
+                              double* sup_out, int* status, void* stream);
+int auxmc_tshard_filter_finish(const auxmc_lgssm* model, const double* obs, int sup_lo,
+                               int sup_hi, void* workspace, size_t workspace_bytes,
+                               const double* sup_all, auxmc_filter_result* out, double* ll_out,
+                               int* status, void* stream);
+int auxmc_tshard_sum(const double* partials, int n, double* out, void* stream);
+
 /* ---- noise sources (rng.hpp:123-137) ----
  * kind 0 (stream): per-problem stream keys; draws at keys[b].derive(label, index).
  * kind 1 (pre-drawn): arrays addressed by (label, index); the NoiseSource

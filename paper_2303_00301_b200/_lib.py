@@ -105,6 +105,16 @@ SIGNATURES = {
                                       C.POINTER(FilterResult), VP, VP, C.c_size_t, VP]),
     "auxmc_kalman_filter_workspace": (C.c_size_t, [C.POINTER(Lgssm), C.c_int, C.c_int]),
     "auxmc_dnc_bridge_count": (C.c_longlong, [C.c_int]),
+    "auxmc_tshard_geometry": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int)]),
+    "auxmc_tshard_filter_workspace": (C.c_size_t, [C.POINTER(Lgssm)]),
+    "auxmc_tshard_filter_local": (C.c_int, [C.POINTER(Lgssm), VP, C.c_int, C.c_int, VP,
+                                            C.c_size_t, VP, VP, VP]),
+    "auxmc_tshard_filter_finish": (C.c_int, [C.POINTER(Lgssm), VP, C.c_int, C.c_int, VP,
+                                             C.c_size_t, VP, C.POINTER(FilterResult), VP, VP,
+                                             VP]),
+    "auxmc_tshard_sum": (C.c_int, [VP, C.c_int, VP, VP]),
     "auxmc_sample_paths": (C.c_int, [C.POINTER(Lgssm), C.POINTER(FilterResult), C.c_int,
                                      C.POINTER(Noise), C.c_int, C.c_int, VP, VP, VP, C.c_size_t,
                                      VP]),

@@ -35,6 +35,12 @@ static cudaEvent_t prof_event() {
   return e;
 }
 
+__global__ void k_seq_sum(const double* v, int n, double* out) {  // in index order
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s += v[i];
+  *out = s;
+}
+
 void prof_mark(const char* name, cudaStream_t s, bool begin) {
   std::lock_guard<std::mutex> lock(g_prof_mu);
   if (begin) {
@@ -97,6 +103,13 @@ int launch_filter_seq(const DevModel& dm, const double* obs, int B, auxmc_filter
 int launch_filter_pit(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
                       int* status, Arena& ws, cudaStream_t stream);
 size_t filter_pit_workspace(const DevModel& dm, int B);
+int tshard_geometry(int T, int* LB, int* nblk, int* nsup, int* SB);
+int tshard_filter_local(const DevModel& dm, const double* obs, int j_lo, int j_hi, Arena& ws,
+                        double* sup_out, int* status, cudaStream_t s);
+int tshard_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_hi, Arena& ws,
+                         const double* sup_all, auxmc_filter_result* out, double* ll_out,
+                         int* status, cudaStream_t s);
+int tshard_elem_doubles(int dx);
 int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int fr_shared,
                         const auxmc_noise* noise, int B, int sampler, double* traj, int* status,
                         Arena& ws, cudaStream_t stream);
@@ -213,6 +226,55 @@ int auxmc_kalman_filter(const auxmc_lgssm* model, const double* obs, int B, int 
     return launch_filter_pit(dm, obs, B, out, status, ws, (cudaStream_t)stream);
   }
   return AUXMC_E_ARG;
+}
+
+int auxmc_tshard_geometry(int T, int dx, int* LB, int* nblk, int* nsup, int* SB,
+                          int* elem_doubles) {
+  if (T < 0 || dx < 1 || !LB || !nblk || !nsup || !SB || !elem_doubles) return AUXMC_E_ARG;
+  tshard_geometry(T, LB, nblk, nsup, SB);
+  *elem_doubles = tshard_elem_doubles(dx);
+  return AUXMC_OK;
+}
+
+size_t auxmc_tshard_filter_workspace(const auxmc_lgssm* model) {
+  if (!model) return 0;
+  Arena ws{nullptr, 0, 0};
+  tshard_filter_local(to_dev(*model), nullptr, 0, 1, ws, nullptr, nullptr, nullptr);
+  return ws.used + 1024;
+}
+
+int auxmc_tshard_filter_local(const auxmc_lgssm* model, const double* obs, int sup_lo,
+                              int sup_hi, void* workspace, size_t workspace_bytes,
+                              double* sup_out, int* status, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  int st = check_model(model);
+  if (st) return st;
+  if (!sup_out || !status || (model->dy > 0 && !obs) || !workspace) return AUXMC_E_ARG;
+  AUXMC_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), (cudaStream_t)stream));
+  Arena ws{(char*)workspace, workspace_bytes, 0};
+  return tshard_filter_local(to_dev(*model), obs, sup_lo, sup_hi, ws, sup_out, status,
+                             (cudaStream_t)stream);
+}
+
+int auxmc_tshard_filter_finish(const auxmc_lgssm* model, const double* obs, int sup_lo,
+                               int sup_hi, void* workspace, size_t workspace_bytes,
+                               const double* sup_all, auxmc_filter_result* out, double* ll_out,
+                               int* status, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  int st = check_model(model);
+  if (st) return st;
+  if (!sup_all || !out || !ll_out || !status || (model->dy > 0 && !obs) || !workspace)
+    return AUXMC_E_ARG;
+  Arena ws{(char*)workspace, workspace_bytes, 0};
+  return tshard_filter_finish(to_dev(*model), obs, sup_lo, sup_hi, ws, sup_all, out, ll_out,
+                              status, (cudaStream_t)stream);
+}
+
+int auxmc_tshard_sum(const double* partials, int n, double* out, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  if (!partials || !out || n < 0) return AUXMC_E_ARG;
+  AUXMC_LAUNCH(k_seq_sum, 1, 1, 0, stream, partials, n, out);
+  return AUXMC_OK;
 }
 
 long long auxmc_dnc_bridge_count(int T) {

@@ -212,7 +212,7 @@ __host__ __device__ inline int elem_smem(int d, int dy) {
 
 template <bool BLOCK>
 __global__ void k_pfg_elements(DevModel m, const double* __restrict__ obs, int B, double* el,
-                               int* status) {
+                               int* status, int t_lo, int t_hi) {
   extern __shared__ double smem[];
   const int T = m.T, d = m.dx, dy = m.dy, dd = d * d, ES = fe_size_g(d);
   const int W = d > dy ? d : dy;
@@ -225,9 +225,11 @@ __global__ void k_pfg_elements(DevModel m, const double* __restrict__ obs, int B
   double *innov = fs + dy * dy, *hv = innov + W, *bd = hv + W;
   double* red = bd + W;
   int* flag = reinterpret_cast<int*>(red + 2);
-  const long long n = (long long)B * (T + 1);
-  for (long long q = (long long)blockIdx.x * gpb + gid; q < n; q += (long long)gridDim.x * gpb) {
-    const int b = (int)(q / (T + 1)), t = (int)(q % (T + 1));
+  const int span = t_hi - t_lo;  // time range [t_lo, t_hi) of this launch
+  const long long n = (long long)B * span;
+  for (long long qq = (long long)blockIdx.x * gpb + gid; qq < n; qq += (long long)gridDim.x * gpb) {
+    const int b = (int)(qq / span), t = t_lo + (int)(qq % span);
+    const long long q = (long long)b * (T + 1) + t;
     double* e = el + (size_t)q * ES;
     double *eA = e, *eb = e + dd, *eC = e + dd + d, *eeta = e + 2 * dd + d, *eJ = e + 2 * dd + 2 * d;
     const double* Qs = t == 0 ? m.P0 : m.Qt(t - 1, b);
@@ -330,7 +332,8 @@ __global__ void k_pfg_elements(DevModel m, const double* __restrict__ obs, int B
 __host__ __device__ inline int scan_smem(int d) { return 3 * fe_size_g(d) + comb_doubles(d) + comb_ints(d); }
 
 template <bool BLOCK>
-__global__ void k_pfg_reduce(int T, int d, int B, int LB, const double* __restrict__ el, double* agg) {
+__global__ void k_pfg_reduce(int T, int d, int B, int LB, const double* __restrict__ el, double* agg,
+                             int k_lo, int k_hi) {
   extern __shared__ double smem[];
   const int ES = fe_size_g(d);
   const Grp g = BLOCK ? block_group() : warp_group();
@@ -339,9 +342,11 @@ __global__ void k_pfg_reduce(int T, int d, int B, int LB, const double* __restri
   double *acc = sm, *o = acc + ES, *tmpd = o + ES;
   const CombScratch cs = comb_scratch(d, tmpd + ES, reinterpret_cast<int*>(tmpd + ES + comb_doubles(d)));
   const int nblk = (T + 1 + LB - 1) / LB;
-  const long long n = (long long)B * nblk;
-  for (long long q = (long long)blockIdx.x * gpb + gid; q < n; q += (long long)gridDim.x * gpb) {
-    const int b = (int)(q / nblk), k = (int)(q % nblk);
+  const int span = k_hi - k_lo;  // block range [k_lo, k_hi) of this launch
+  const long long n = (long long)B * span;
+  for (long long qq = (long long)blockIdx.x * gpb + gid; qq < n; qq += (long long)gridDim.x * gpb) {
+    const int b = (int)(qq / span), k = k_lo + (int)(qq % span);
+    const long long q = (long long)b * nblk + k;
     const int lo = k * LB, hi = min(lo + LB, T + 1);
     const double* base = el + (size_t)b * (T + 1) * ES;
     g_copy(g, ES, base + (size_t)lo * ES, acc);
@@ -383,7 +388,8 @@ __global__ void k_pfg_carry(int T, int d, int B, int LB, const double* __restric
 // over the super-block aggregates).
 template <bool BLOCK>
 __global__ void k_pfg_carry_seg(int nblk, int d, int B, int LB2, const double* __restrict__ agg,
-                                const double* __restrict__ carry2, double* carry) {
+                                const double* __restrict__ carry2, double* carry, int j_lo,
+                                int j_hi) {
   extern __shared__ double smem[];
   const int ES = fe_size_g(d);
   const Grp g = BLOCK ? block_group() : warp_group();
@@ -392,9 +398,11 @@ __global__ void k_pfg_carry_seg(int nblk, int d, int B, int LB2, const double* _
   double *acc = sm, *o = acc + ES, *tmpd = o + ES;
   const CombScratch cs = comb_scratch(d, tmpd + ES, reinterpret_cast<int*>(tmpd + ES + comb_doubles(d)));
   const int nsup = (nblk + LB2 - 1) / LB2;
-  const long long n = (long long)B * nsup;
-  for (long long q = (long long)blockIdx.x * gpb + gid; q < n; q += (long long)gridDim.x * gpb) {
-    const int b = (int)(q / nsup), j = (int)(q % nsup);
+  const int span = j_hi - j_lo;  // super-block range [j_lo, j_hi) of this launch
+  const long long n = (long long)B * span;
+  for (long long qq = (long long)blockIdx.x * gpb + gid; qq < n; qq += (long long)gridDim.x * gpb) {
+    const int b = (int)(qq / span), j = j_lo + (int)(qq % span);
+    const long long q = (long long)b * nsup + j;
     const int lo = j * LB2, hi = min(lo + LB2, nblk);
     const double* A = agg + (size_t)b * nblk * ES;
     double* Cy = carry + (size_t)b * nblk * ES;
@@ -419,7 +427,8 @@ __global__ void k_pfg_carry_seg(int nblk, int d, int B, int LB2, const double* _
 
 template <bool BLOCK>
 __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restrict__ el,
-                            const double* __restrict__ carry, double* filt_mean, double* filt_cov) {
+                            const double* __restrict__ carry, double* filt_mean, double* filt_cov,
+                            int k_lo, int k_hi) {
   extern __shared__ double smem[];
   const int ES = fe_size_g(d), dd = d * d;
   const Grp g = BLOCK ? block_group() : warp_group();
@@ -428,9 +437,11 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
   double *acc = sm, *o = acc + ES, *cy = o + ES;
   const CombScratch cs = comb_scratch(d, cy + ES, reinterpret_cast<int*>(cy + ES + comb_doubles(d)));
   const int nblk = (T + 1 + LB - 1) / LB;
-  const long long n = (long long)B * nblk;
-  for (long long q = (long long)blockIdx.x * gpb + gid; q < n; q += (long long)gridDim.x * gpb) {
-    const int b = (int)(q / nblk), k = (int)(q % nblk);
+  const int span = k_hi - k_lo;
+  const long long n = (long long)B * span;
+  for (long long qq = (long long)blockIdx.x * gpb + gid; qq < n; qq += (long long)gridDim.x * gpb) {
+    const int b = (int)(qq / span), k = k_lo + (int)(qq % span);
+    const long long q = (long long)b * nblk + k;
     const int lo = k * LB, hi = min(lo + LB, T + 1);
     const double* base = el + (size_t)b * (T + 1) * ES;
     if (k == 0) {
@@ -464,7 +475,8 @@ __host__ __device__ inline int rec_smem(int d, int dy) {
 template <bool BLOCK>
 __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
                               const double* __restrict__ fm, const double* __restrict__ fc,
-                              double* pm, double* pc, double* terms, int* status) {
+                              double* pm, double* pc, double* terms, int* status, int t_lo,
+                              int t_hi, int sb = 0, const double* bnd = nullptr) {
   extern __shared__ double smem[];
   const int T = m.T, d = m.dx, dy = m.dy, dd = d * d;
   const int W = d > dy ? d : dy;
@@ -475,9 +487,11 @@ __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
          *scr = L + dy * dy;
   double *mp = scr + dy * dy, *r = mp + W, *red = r + W;
   int* flag = reinterpret_cast<int*>(red + 2);
-  const long long n = (long long)B * (T + 1);
-  for (long long q = (long long)blockIdx.x * gpb + gid; q < n; q += (long long)gridDim.x * gpb) {
-    const int b = (int)(q / (T + 1)), t = (int)(q % (T + 1));
+  const int span = t_hi - t_lo;
+  const long long n = (long long)B * span;
+  for (long long qq = (long long)blockIdx.x * gpb + gid; qq < n; qq += (long long)gridDim.x * gpb) {
+    const int b = (int)(qq / span), t = t_lo + (int)(qq % span);
+    const long long q = (long long)b * (T + 1) + t;
     if (t == 0) {
       for (int i = g.lane; i < d; i += g.size) mp[i] = m.m0[i];
       for (int i = g.ty(); i < d; i += g.ny())
@@ -487,8 +501,11 @@ __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
       const double* F = m.Ft(t - 1, b);
       const double* bb = m.bt(t - 1, b);
       const double* Q = m.Qt(t - 1, b);
-      const double* x = fm + (size_t)(q - 1) * d;
-      const double* C = fc + (size_t)(q - 1) * dd;
+      // time-sharded filter: at a super-block start the previous filtered moments
+      // are the super-block carry's (b, C), so every rank split sees the same bits
+      const bool at_sb = sb > 0 && t % sb == 0;
+      const double* x = at_sb ? bnd + (size_t)(t / sb) * (d + dd) : fm + (size_t)(q - 1) * d;
+      const double* C = at_sb ? x + d : fc + (size_t)(q - 1) * dd;
       for (int i = g.lane; i < d; i += g.size) {
         double acc = 0.0;
         for (int k = 0; k < d; ++k) acc += F[i * d + k] * x[k];
@@ -582,30 +599,186 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_carry<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
   AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_apply<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
   AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_recover<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rc));
-  AUXMC_LAUNCH(k_pfg_elements<BLOCK>, grid(n), cfg.threads, sm_el, s, dm, obs, B, el, status);
-  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, grid(nb), cfg.threads, sm_sc, s, T, d, B, LB, el, agg);
+  AUXMC_LAUNCH(k_pfg_elements<BLOCK>, grid(n), cfg.threads, sm_el, s, dm, obs, B, el, status, 0,
+               T + 1);
+  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, grid(nb), cfg.threads, sm_sc, s, T, d, B, LB, el, agg, 0,
+               nblk);
   if (two) {
     AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_carry_seg<BLOCK>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
     const long long ns = (long long)B * nsup;
     AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, grid(ns), cfg.threads, sm_sc, s, nblk - 1, d, B, LB2, agg,
-                 agg2);
+                 agg2, 0, nsup);
     AUXMC_LAUNCH(k_pfg_carry<BLOCK>, grid(B), cfg.threads, sm_sc, s, nsup - 1, d, B, 1, agg2,
                  carry2);
     AUXMC_LAUNCH(k_pfg_carry_seg<BLOCK>, grid(ns), cfg.threads, sm_sc, s, nblk, d, B, LB2, agg,
-                 carry2, carry);
+                 carry2, carry, 0, nsup);
   } else {
     AUXMC_LAUNCH(k_pfg_carry<BLOCK>, grid(B), cfg.threads, sm_sc, s, T, d, B, LB, agg, carry);
   }
   AUXMC_LAUNCH(k_pfg_apply<BLOCK>, grid(nb), cfg.threads, sm_sc, s, T, d, B, LB, el, carry,
-               out->filt_mean, out->filt_cov);
+               out->filt_mean, out->filt_cov, 0, nblk);
   AUXMC_LAUNCH(k_pfg_recover<BLOCK>, grid(n), cfg.threads, sm_rc, s, dm, obs, B, out->filt_mean,
-               out->filt_cov, out->pred_mean, out->pred_cov, terms, status);
+               out->filt_cov, out->pred_mean, out->pred_cov, terms, status, 0, T + 1);
   AUXMC_LAUNCH(k_pfg_sum, B, kSumThreads, 0, s, T, B, terms, out->log_marginal);
   return AUXMC_OK;
 }
 
+// ---------------------------------------------------------------- time-sharded scan filter
+// One sequence, horizon split over ranks by runs of super-blocks (SB = LB * LB2
+// steps).  The whole block tree — blocks, super-blocks, the serial carry over
+// super-block aggregates, the per-super-block log-likelihood partial sums —
+// depends only on T, so every rank count reproduces the single-rank result bit
+// for bit.  Exchange between the two phases: an all-gather of the super-block
+// aggregates (ES doubles each).
+struct TsGeom {
+  int LB, nblk, LB2, nsup, SB;
+};
+TsGeom ts_geom(int T) {
+  TsGeom g;
+  g.LB = pf_block_g(T);
+  g.nblk = (T + 1 + g.LB - 1) / g.LB;
+  g.LB2 = g.LB;
+  g.nsup = (g.nblk + g.LB2 - 1) / g.LB2;
+  g.SB = g.LB * g.LB2;
+  return g;
+}
+
+struct TsBufs {
+  double *el, *agg, *carry, *terms, *agg2, *carry2, *bnd;
+};
+TsBufs ts_take(const DevModel& dm, Arena& ws) {
+  const TsGeom G = ts_geom(dm.T);
+  const int ES = fe_size_g(dm.dx), T = dm.T;
+  TsBufs b;
+  b.el = ws.take<double>((size_t)(T + 1) * ES);
+  b.agg = ws.take<double>((size_t)G.nblk * ES);
+  b.carry = ws.take<double>((size_t)G.nblk * ES);
+  b.terms = ws.take<double>((size_t)(T + 2));
+  b.agg2 = ws.take<double>((size_t)G.nsup * ES);
+  b.carry2 = ws.take<double>((size_t)G.nsup * ES);
+  b.bnd = ws.take<double>((size_t)G.nsup * (dm.dx + dm.dx * dm.dx));
+  return b;
+}
+
+// filtered moments just before each owned super-block start j*SB (j > 0): (b, C)
+// of the composed prefix that ends there, i.e. the carry of the super-block's
+// first block
+__global__ void k_ts_boundary(int d, int LB2, int j_lo, int j_hi, const double* carry, double* bnd) {
+  const int dd = d * d, ES = fe_size_g(d);
+  for (int j = max(j_lo, 1) + blockIdx.x; j < j_hi; j += gridDim.x) {
+    const double* ck = carry + (size_t)j * LB2 * ES;
+    for (int i = threadIdx.x; i < d + dd; i += blockDim.x)
+      bnd[(size_t)j * (d + dd) + i] = ck[dd + i];  // (b | C) are contiguous in the element
+  }
+}
+
+// sequential log-likelihood partial sum of each super-block in [j_lo, j_hi)
+__global__ void k_ts_partials(int T, int SB, int j_lo, int j_hi, const double* terms, double* out) {
+  const int j = j_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= j_hi) return;
+  double s = 0.0;
+  const int hi = min((j + 1) * SB, T + 1);
+  for (int t = j * SB; t < hi; ++t) s += terms[t];
+  out[j - j_lo] = s;
+}
+
+template <bool BLOCK>
+int ts_filter_local(const DevModel& dm, const double* obs, int j_lo, int j_hi, Arena& ws,
+                    double* sup_out, int* status, cudaStream_t s) {
+  const int T = dm.T, d = dm.dx, dy = dm.dy, ES = fe_size_g(d);
+  const TsGeom G = ts_geom(T);
+  const TsBufs b = ts_take(dm, ws);
+  if (ws.base == nullptr) return AUXMC_OK;
+  if (!b.el || !b.carry2) return AUXMC_E_WORKSPACE;
+  if (j_lo < 0 || j_hi > G.nsup || j_lo >= j_hi) return AUXMC_E_ARG;
+  const GrpCfg cfg = grp_cfg(d, dy);
+  const int gp = cfg.groups;
+  const size_t sm_el = sizeof(double) * elem_smem(d, dy) * gp;
+  const size_t sm_sc = sizeof(double) * scan_smem(d) * gp;
+  if (sm_el > 227 * 1024 || sm_sc > 227 * 1024) return AUXMC_E_DIM;
+  auto grid = [gp](long long k) { return (int)std::max(1LL, std::min((k + gp - 1) / gp, 148LL * 16)); };
+  const int t_lo = j_lo * G.SB, t_hi = std::min(j_hi * G.SB, T + 1);
+  const int k_lo = j_lo * G.LB2, k_hi = std::min(j_hi * G.LB2, G.nblk);
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_elements<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_el));
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_reduce<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
+  AUXMC_LAUNCH(k_pfg_elements<BLOCK>, grid(t_hi - t_lo), cfg.threads, sm_el, s, dm, obs, 1, b.el,
+               status, t_lo, t_hi);
+  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, grid(k_hi - k_lo), cfg.threads, sm_sc, s, T, d, 1, G.LB, b.el,
+               b.agg, k_lo, k_hi);
+  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, grid(j_hi - j_lo), cfg.threads, sm_sc, s, G.nblk - 1, d, 1,
+               G.LB2, b.agg, b.agg2, j_lo, j_hi);
+  AUXMC_CUDA_TRY(cudaMemcpyAsync(sup_out, b.agg2 + (size_t)j_lo * ES,
+                                 sizeof(double) * (size_t)(j_hi - j_lo) * ES,
+                                 cudaMemcpyDeviceToDevice, s));
+  return AUXMC_OK;
+}
+
+template <bool BLOCK>
+int ts_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_hi, Arena& ws,
+                     const double* sup_all, auxmc_filter_result* out, double* ll_out, int* status,
+                     cudaStream_t s) {
+  const int T = dm.T, d = dm.dx, dy = dm.dy, ES = fe_size_g(d);
+  const TsGeom G = ts_geom(T);
+  const TsBufs b = ts_take(dm, ws);
+  if (ws.base == nullptr) return AUXMC_OK;
+  if (!b.el || !b.carry2) return AUXMC_E_WORKSPACE;
+  if (j_lo < 0 || j_hi > G.nsup || j_lo >= j_hi) return AUXMC_E_ARG;
+  const GrpCfg cfg = grp_cfg(d, dy);
+  const int gp = cfg.groups;
+  const size_t sm_sc = sizeof(double) * scan_smem(d) * gp;
+  const size_t sm_rc = sizeof(double) * rec_smem(d, dy) * gp;
+  if (sm_sc > 227 * 1024 || sm_rc > 227 * 1024) return AUXMC_E_DIM;
+  auto grid = [gp](long long k) { return (int)std::max(1LL, std::min((k + gp - 1) / gp, 148LL * 16)); };
+  const int t_lo = j_lo * G.SB, t_hi = std::min(j_hi * G.SB, T + 1);
+  const int k_lo = j_lo * G.LB2, k_hi = std::min(j_hi * G.LB2, G.nblk);
+  AUXMC_CUDA_TRY(cudaMemcpyAsync(b.agg2, sup_all, sizeof(double) * (size_t)G.nsup * ES,
+                                 cudaMemcpyDeviceToDevice, s));
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_carry<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_carry_seg<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_apply<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_recover<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rc));
+  // every rank runs the same serial carry over all super-block aggregates
+  AUXMC_LAUNCH(k_pfg_carry<BLOCK>, 1, cfg.threads, sm_sc, s, G.nsup - 1, d, 1, 1, b.agg2, b.carry2);
+  AUXMC_LAUNCH(k_pfg_carry_seg<BLOCK>, grid(j_hi - j_lo), cfg.threads, sm_sc, s, G.nblk, d, 1,
+               G.LB2, b.agg, b.carry2, b.carry, j_lo, j_hi);
+  AUXMC_LAUNCH(k_pfg_apply<BLOCK>, grid(k_hi - k_lo), cfg.threads, sm_sc, s, T, d, 1, G.LB, b.el,
+               b.carry, out->filt_mean, out->filt_cov, k_lo, k_hi);
+  AUXMC_LAUNCH(k_ts_boundary, std::max(1, j_hi - j_lo), 128, 0, s, d, G.LB2, j_lo, j_hi, b.carry,
+               b.bnd);
+  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, grid(t_hi - t_lo), cfg.threads, sm_rc, s, dm, obs, 1,
+               out->filt_mean, out->filt_cov, out->pred_mean, out->pred_cov, b.terms, status, t_lo,
+               t_hi, G.SB, b.bnd);
+  AUXMC_LAUNCH(k_ts_partials, (j_hi - j_lo + 127) / 128, 128, 0, s, T, G.SB, j_lo, j_hi, b.terms,
+               ll_out);
+  return AUXMC_OK;
+}
+
 }  // namespace
+
+int tshard_geometry(int T, int* LB, int* nblk, int* nsup, int* SB) {
+  const TsGeom G = ts_geom(T);
+  *LB = G.LB;
+  *nblk = G.nblk;
+  *nsup = G.nsup;
+  *SB = G.SB;
+  return AUXMC_OK;
+}
+int tshard_filter_local(const DevModel& dm, const double* obs, int j_lo, int j_hi, Arena& ws,
+                        double* sup_out, int* status, cudaStream_t s) {
+  if (dm.dx > 32 || dm.dy > 64) return AUXMC_E_DIM;
+  return grp_cfg(dm.dx, dm.dy).block ? ts_filter_local<true>(dm, obs, j_lo, j_hi, ws, sup_out, status, s)
+                                     : ts_filter_local<false>(dm, obs, j_lo, j_hi, ws, sup_out, status, s);
+}
+int tshard_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_hi, Arena& ws,
+                         const double* sup_all, auxmc_filter_result* out, double* ll_out,
+                         int* status, cudaStream_t s) {
+  if (dm.dx > 32 || dm.dy > 64) return AUXMC_E_DIM;
+  return grp_cfg(dm.dx, dm.dy).block
+             ? ts_filter_finish<true>(dm, obs, j_lo, j_hi, ws, sup_all, out, ll_out, status, s)
+             : ts_filter_finish<false>(dm, obs, j_lo, j_hi, ws, sup_all, out, ll_out, status, s);
+}
+int tshard_elem_doubles(int dx) { return fe_size_g(dx); }
 
 int dispatch_pf_generic(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
                         int* status, Arena& ws, cudaStream_t s) {

@@ -1,0 +1,144 @@
+"""Time-sharded scan filter: pit::parallel_filter (pit.cpp:117-188) for one long
+sequence split over ranks.
+
+The horizon's block tree (blocks of LB steps, super-blocks of SB = LB² steps)
+depends only on T.  Rank r owns a contiguous run of super-blocks
+(`shard.strong_shard` over the super-block count); the only exchange is one
+all-gather of the super-block aggregates (the filtering-element tuple
+(A, b, C, η, J), 3d² + 2d doubles each) and one of the per-super-block
+log-likelihood partials.  Every rank count reproduces one rank bit for bit.
+
+`exchange` is any all-gather of equally shaped device tensors in rank order:
+`torch.distributed.all_gather` under NCCL (ranks on their own GPUs) or gloo (host
+tensors), or `LocalExchange` to run several shards in one process.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .lgssm import FilterResult, Model, _dev, _stream
+from .shard import strong_shard
+
+
+@dataclass(frozen=True)
+class TShardGeom:
+    T: int
+    LB: int
+    nblk: int
+    nsup: int
+    SB: int
+    elem_doubles: int
+
+    @staticmethod
+    def of(T: int, dx: int) -> "TShardGeom":
+        v = [C.c_int() for _ in range(5)]
+        _lib.check(_lib.load().auxmc_tshard_geometry(T, dx, *[C.byref(x) for x in v]),
+                   "tshard_geometry")
+        return TShardGeom(T, *[x.value for x in v])
+
+    def owned(self, rank: int, world: int):
+        """Super-block range [lo, hi) and time range [t_lo, t_hi) of a rank."""
+        sh = strong_shard(rank, world, self.nsup)
+        lo, hi = sh.first, sh.first + sh.count
+        return lo, hi, lo * self.SB, min(hi * self.SB, self.T + 1)
+
+
+def torch_exchange(group=None):
+    """All-gather through torch.distributed (NCCL device tensors or gloo host tensors)."""
+    import torch.distributed as dist
+
+    def ex(t: torch.Tensor) -> list:
+        backend = dist.get_backend(group)
+        x = t if backend == "nccl" else t.cpu()
+        parts = [torch.empty_like(x) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(parts, x.contiguous(), group=group)
+        return [p.to(t.device) for p in parts]
+    return ex
+
+
+class ShardedScanFilter:
+    """One rank's share of the scan filter of `obs` ([T+1, dy]) under `model`."""
+
+    def __init__(self, model: Model, rank: int, world: int):
+        self.model, self.rank, self.world = model, rank, world
+        self.geom = TShardGeom.of(model.T, model.dx)
+        self.sup_lo, self.sup_hi, self.t_lo, self.t_hi = self.geom.owned(rank, world)
+        lib = _lib.load()
+        self._mr = model.raw()
+        self.ws_bytes = lib.auxmc_tshard_filter_workspace(C.byref(self._mr))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=model.device)
+        self.max_owned = -(-self.geom.nsup // world)  # ceil: rows each rank contributes
+
+    def local(self, obs) -> torch.Tensor:
+        """Phase 1: this rank's super-block aggregates, padded to max_owned rows."""
+        g, dev = self.geom, self.model.device
+        self.obs = _dev(obs, dev).contiguous()
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        out = torch.zeros((self.max_owned, g.elem_doubles), dtype=torch.float64, device=dev)
+        if self.sup_hi > self.sup_lo:
+            _lib.check(_lib.load().auxmc_tshard_filter_local(
+                C.byref(self._mr), self.obs.data_ptr(), self.sup_lo, self.sup_hi,
+                self.ws.data_ptr(), self.ws_bytes, out.data_ptr(), self.status.data_ptr(),
+                _stream()), "tshard_filter_local")
+        return out
+
+    def _concat(self, parts, rows_of):
+        return torch.cat([p[:rows_of(r)] for r, p in enumerate(parts)], 0).contiguous()
+
+    def _rows(self, r):
+        lo, hi, _, _ = self.geom.owned(r, self.world)
+        return hi - lo
+
+    def finish(self, gathered_aggs, fr: FilterResult | None = None):
+        """Phase 2 (after the all-gather): moments for this rank's time range and its
+        log-likelihood partials (padded to max_owned)."""
+        g, dev = self.geom, self.model.device
+        sup_all = self._concat(gathered_aggs, self._rows)
+        assert sup_all.shape[0] == g.nsup
+        if fr is None:
+            fr = FilterResult.empty(1, g.T, self.model.dx, dev)
+        ll = torch.zeros(self.max_owned, dtype=torch.float64, device=dev)
+        if self.sup_hi > self.sup_lo:
+            raw = fr.raw()
+            _lib.check(_lib.load().auxmc_tshard_filter_finish(
+                C.byref(self._mr), self.obs.data_ptr(), self.sup_lo, self.sup_hi,
+                self.ws.data_ptr(), self.ws_bytes, sup_all.data_ptr(), C.byref(raw),
+                ll.data_ptr(), self.status.data_ptr(), _stream()), "tshard_filter_finish")
+        return fr, ll
+
+    def log_marginal(self, gathered_ll) -> torch.Tensor:
+        """Sum of every super-block partial in super-block order (device scalar)."""
+        parts = self._concat(gathered_ll, self._rows)
+        out = torch.empty(1, dtype=torch.float64, device=self.model.device)
+        _lib.check(_lib.load().auxmc_tshard_sum(parts.data_ptr(), parts.numel(), out.data_ptr(),
+                                                 _stream()), "tshard_sum")
+        return out
+
+
+def sharded_filter(model: Model, obs, rank: int, world: int, exchange):
+    """Run the time-sharded scan filter; returns (FilterResult with this rank's time
+    range filled, log_marginal, (t_lo, t_hi))."""
+    sf = ShardedScanFilter(model, rank, world)
+    aggs = sf.local(obs)
+    fr, ll = sf.finish(exchange(aggs))
+    lm = sf.log_marginal(exchange(ll))
+    fr.log_marginal.copy_(lm)
+    return fr, lm, (sf.t_lo, sf.t_hi)
+
+
+class LocalExchange:
+    """Runs `world` shards in one process: collects each shard's tensor, then hands
+    every shard the rank-ordered list (for tests and single-GPU checks)."""
+
+    @staticmethod
+    def run(model: Model, obs, world: int):
+        shards = [ShardedScanFilter(model, r, world) for r in range(world)]
+        aggs = [s.local(obs) for s in shards]
+        outs = [s.finish(aggs) for s in shards]
+        lls = [ll for _, ll in outs]
+        lm = shards[0].log_marginal(lls)
+        return shards, [fr for fr, _ in outs], lm

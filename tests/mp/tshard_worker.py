@@ -1,0 +1,63 @@
+"""One rank of the time-sharded scan filter test (tests/test_gpu_tshard.py):
+launched by torch.distributed.run with the gloo backend; every rank drives its
+own time range on cuda:0 (no kernel waits on another rank: the exchange is a
+host all-gather), rank 0 compares with a one-rank run and writes a verdict."""
+import json
+import pathlib
+import sys
+
+ROOT = pathlib.Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+
+def main(out_path):
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(0)
+    from oracle import pyoracle as O
+    from testutil import random_model, simulate_obs, to_gpu_model
+    from paper_2303_00301_b200 import tshard
+    s = O.derive(O.from_seed(71), O.L_SIMULATE, 2)
+    m = random_model(s, 2500, 3, 2, True, True)
+    obs = simulate_obs(m, O.from_seed(72))
+    gm = to_gpu_model(m)
+    fr, lm, (t_lo, t_hi) = tshard.sharded_filter(gm, obs, rank, world, tshard.torch_exchange())
+    torch.cuda.synchronize()
+    sl = slice(t_lo, t_hi)
+    mine = torch.cat([fr.filt_mean[0, sl].reshape(-1), fr.filt_cov[0, sl].reshape(-1),
+                      fr.pred_mean[0, sl].reshape(-1), fr.pred_cov[0, sl].reshape(-1)]).cpu()
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([mine.numel()]))
+    nmax = int(max(int(n) for n in sizes))
+    padded = torch.zeros(nmax, dtype=torch.float64)
+    padded[:mine.numel()] = mine
+    parts = [torch.zeros(nmax, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(parts, padded)
+    parts = [p[:int(n)] for p, n in zip(parts, sizes)]
+    if rank == 0:
+        shards, frs, lm1 = tshard.LocalExchange.run(gm, obs, 1)
+        ref = frs[0]
+        ok = True
+        for r in range(world):
+            g = tshard.TShardGeom.of(m.T, m.dx)
+            _, _, a, b = g.owned(r, world)
+            want = torch.cat([ref.filt_mean[0, a:b].reshape(-1), ref.filt_cov[0, a:b].reshape(-1),
+                              ref.pred_mean[0, a:b].reshape(-1),
+                              ref.pred_cov[0, a:b].reshape(-1)]).cpu()
+            ok = ok and torch.equal(parts[r], want)
+        ok = ok and torch.equal(lm.cpu(), lm1.cpu())
+        want_o = O.kalman_filter(m, obs)
+        err = abs(float(lm1.item()) - want_o.log_marginal) / max(1.0, abs(want_o.log_marginal))
+        json.dump({"bit_identical": bool(ok), "world": world, "lm_rel_err": err},
+                  open(out_path, "w"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
