@@ -145,6 +145,7 @@ int auxmc_tshard_filter_finish(const auxmc_lgssm* model, const double* obs, int 
                                int* status, void* stream);
 int auxmc_tshard_sum(const double* partials, int n, double* out, void* stream);
 
+
 /* ---- noise sources (rng.hpp:123-137) ----
  * kind 0 (stream): per-problem stream keys; draws at keys[b].derive(label, index).
  * kind 1 (pre-drawn): arrays addressed by (label, index); the NoiseSource
@@ -163,6 +164,27 @@ typedef struct {
 /* Number of bridge ids a pre-drawn DnC noise array must cover for horizon T
  * (heap ids of the BFS segment tree, pit.cpp:214-234). */
 long long auxmc_dnc_bridge_count(int T);
+
+/* ---- time-sharded prefix sampler (pit::prefix_sample, pit.cpp:78-115, one path)
+ * On the same time ranges as the sharded filter ([t_lo, t_hi) of the rank's
+ * super-blocks; sampler blocks of Lb steps, P of them, never straddle a range):
+ *   1. auxmc_tshard_prefix_local: backward elements of the range (the sharded
+ *      filter result supplies the predictive covariance at t_hi), the rows
+ *      (A_k | a_k), d*d + d doubles, of its blocks into blk_out, and — on the rank
+ *      with t_hi == T+1 — the terminal draw x_T into xT_out;
+ *   2. the caller all-gathers the rows of all P blocks in order and x_T;
+ *   3. auxmc_tshard_prefix_finish: the serial block carry (all ranks, same bits)
+ *      and the path for the range.  Noise: stream keys or pre-drawn, B = 1. */
+int auxmc_tshard_prefix_geometry(int T, int* Lb, int* P);
+size_t auxmc_tshard_prefix_workspace(const auxmc_lgssm* model);
+int auxmc_tshard_prefix_local(const auxmc_lgssm* model, const auxmc_filter_result* fr,
+                              const auxmc_noise* noise, int t_lo, int t_hi, void* workspace,
+                              size_t workspace_bytes, double* blk_out, double* xT_out,
+                              double* traj, int* status, void* stream);
+int auxmc_tshard_prefix_finish(const auxmc_lgssm* model, const auxmc_noise* noise, int t_lo,
+                               int t_hi, void* workspace, size_t workspace_bytes,
+                               const double* blk_all, const double* xT, double* traj,
+                               void* stream);
 
 /* Pathwise posterior draws of B paths traj [B][T+1][dx] from filter results.
  * fr_shared = 1: one filter result (B_fr = 1) shared by all paths (the C2

@@ -115,6 +115,13 @@ SIGNATURES = {
                                              C.c_size_t, VP, C.POINTER(FilterResult), VP, VP,
                                              VP]),
     "auxmc_tshard_sum": (C.c_int, [VP, C.c_int, VP, VP]),
+    "auxmc_tshard_prefix_geometry": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "auxmc_tshard_prefix_workspace": (C.c_size_t, [C.POINTER(Lgssm)]),
+    "auxmc_tshard_prefix_local": (C.c_int, [C.POINTER(Lgssm), C.POINTER(FilterResult),
+                                            C.POINTER(Noise), C.c_int, C.c_int, VP, C.c_size_t,
+                                            VP, VP, VP, VP, VP]),
+    "auxmc_tshard_prefix_finish": (C.c_int, [C.POINTER(Lgssm), C.POINTER(Noise), C.c_int,
+                                             C.c_int, VP, C.c_size_t, VP, VP, VP, VP]),
     "auxmc_sample_paths": (C.c_int, [C.POINTER(Lgssm), C.POINTER(FilterResult), C.c_int,
                                      C.POINTER(Noise), C.c_int, C.c_int, VP, VP, VP, C.c_size_t,
                                      VP]),

@@ -110,6 +110,14 @@ int tshard_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_
                          const double* sup_all, auxmc_filter_result* out, double* ll_out,
                          int* status, cudaStream_t s);
 int tshard_elem_doubles(int dx);
+int tshard_prefix_geometry(int T, int* Lb, int* P);
+size_t tshard_prefix_workspace(const DevModel& dm);
+int tshard_prefix_local(const DevModel& dm, const double* fm, const double* fc, const double* pc,
+                        const NoiseArgs& nz, int t_lo, int t_hi, Arena& ws, double* blk_out,
+                        double* xT_out, double* traj, int* status, cudaStream_t stream);
+int tshard_prefix_finish(const DevModel& dm, const NoiseArgs& nz, int t_lo, int t_hi, Arena& ws,
+                         const double* blk_all, const double* xT, double* traj,
+                         cudaStream_t stream);
 int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int fr_shared,
                         const auxmc_noise* noise, int B, int sampler, double* traj, int* status,
                         Arena& ws, cudaStream_t stream);
@@ -275,6 +283,57 @@ int auxmc_tshard_sum(const double* partials, int n, double* out, void* stream) {
   if (!partials || !out || n < 0) return AUXMC_E_ARG;
   AUXMC_LAUNCH(k_seq_sum, 1, 1, 0, stream, partials, n, out);
   return AUXMC_OK;
+}
+
+static NoiseArgs noise_args(const auxmc_noise* noise) {
+  NoiseArgs nz{};
+  nz.kind = noise->kind;
+  nz.keys = noise->keys;
+  nz.terminal = noise->terminal;
+  nz.backward = noise->backward;
+  nz.bridge = noise->bridge;
+  nz.n_bridge = noise->n_bridge;
+  return nz;
+}
+
+int auxmc_tshard_prefix_geometry(int T, int* Lb, int* P) {
+  if (T < 0 || !Lb || !P) return AUXMC_E_ARG;
+  return tshard_prefix_geometry(T, Lb, P);
+}
+
+size_t auxmc_tshard_prefix_workspace(const auxmc_lgssm* model) {
+  if (!model) return 0;
+  return tshard_prefix_workspace(to_dev(*model));
+}
+
+int auxmc_tshard_prefix_local(const auxmc_lgssm* model, const auxmc_filter_result* fr,
+                              const auxmc_noise* noise, int t_lo, int t_hi, void* workspace,
+                              size_t workspace_bytes, double* blk_out, double* xT_out,
+                              double* traj, int* status, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  int st = check_model(model);
+  if (st) return st;
+  if (!fr || !noise || !blk_out || !xT_out || !traj || !status || !workspace) return AUXMC_E_ARG;
+  if (noise->kind == AUXMC_NOISE_STREAM ? !noise->keys
+                                        : (!noise->terminal || (model->T > 0 && !noise->backward)))
+    return AUXMC_E_ARG;
+  Arena ws{(char*)workspace, workspace_bytes, 0};
+  return tshard_prefix_local(to_dev(*model), fr->filt_mean, fr->filt_cov, fr->pred_cov,
+                             noise_args(noise), t_lo, t_hi, ws, blk_out, xT_out, traj, status,
+                             (cudaStream_t)stream);
+}
+
+int auxmc_tshard_prefix_finish(const auxmc_lgssm* model, const auxmc_noise* noise, int t_lo,
+                               int t_hi, void* workspace, size_t workspace_bytes,
+                               const double* blk_all, const double* xT, double* traj,
+                               void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  int st = check_model(model);
+  if (st) return st;
+  if (!noise || !blk_all || !xT || !traj || !workspace) return AUXMC_E_ARG;
+  Arena ws{(char*)workspace, workspace_bytes, 0};
+  return tshard_prefix_finish(to_dev(*model), noise_args(noise), t_lo, t_hi, ws, blk_all, xT,
+                              traj, (cudaStream_t)stream);
 }
 
 long long auxmc_dnc_bridge_count(int T) {

@@ -54,7 +54,7 @@ __device__ __forceinline__ void g_eye(const Grp& g, int n, double* dst) {
 template <bool TA, bool TB>
 __device__ __forceinline__ void g_dmma(const Grp& g, int m, int k, int n, const double* A, int lda,
                                        const double* B, int ldb, double* C, int ldc, bool sub,
-                                       bool lower, const double* Dadd);
+                                       bool lower, const double* Dadd = nullptr);
 template <bool TA, bool TB>
 __device__ __forceinline__ void g_mm_dmma(const Grp& g, int m, int k, int n, const double* A,
                                           const double* B, double* C, const double* D) {
@@ -235,7 +235,7 @@ __host__ __device__ constexpr int dinv_doubles(int n) { return 64 * ((n + 7) / 8
 template <bool TA, bool TB>
 __device__ __forceinline__ void g_dmma(const Grp& g, int m, int k, int n, const double* A, int lda,
                                        const double* B, int ldb, double* C, int ldc, bool sub,
-                                       bool lower, const double* Dadd = nullptr) {
+                                       bool lower, const double* Dadd) {
   const int warp = g.lane >> 5, lane = g.lane & 31, nw = g.size >> 5;
   const int gi = lane >> 2, ti = lane & 3;
   const int mt = (m + 7) >> 3, nt = (n + 7) >> 3, kt = (k + 3) >> 2;

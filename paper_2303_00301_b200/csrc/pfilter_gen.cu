@@ -664,10 +664,12 @@ TsBufs ts_take(const DevModel& dm, Arena& ws) {
 // filtered moments just before each owned super-block start j*SB (j > 0): (b, C)
 // of the composed prefix that ends there, i.e. the carry of the super-block's
 // first block
-__global__ void k_ts_boundary(int d, int LB2, int j_lo, int j_hi, const double* carry, double* bnd) {
+// (the carry of a super-block's first block is the super-block carry itself, so
+// it is taken from carry2, which every rank holds)
+__global__ void k_ts_boundary(int d, int j_lo, int j_hi, const double* carry2, double* bnd) {
   const int dd = d * d, ES = fe_size_g(d);
   for (int j = max(j_lo, 1) + blockIdx.x; j < j_hi; j += gridDim.x) {
-    const double* ck = carry + (size_t)j * LB2 * ES;
+    const double* ck = carry2 + (size_t)j * ES;
     for (int i = threadIdx.x; i < d + dd; i += blockDim.x)
       bnd[(size_t)j * (d + dd) + i] = ck[dd + i];  // (b | C) are contiguous in the element
   }
@@ -744,11 +746,15 @@ int ts_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_hi, 
                G.LB2, b.agg, b.carry2, b.carry, j_lo, j_hi);
   AUXMC_LAUNCH(k_pfg_apply<BLOCK>, grid(k_hi - k_lo), cfg.threads, sm_sc, s, T, d, 1, G.LB, b.el,
                b.carry, out->filt_mean, out->filt_cov, k_lo, k_hi);
-  AUXMC_LAUNCH(k_ts_boundary, std::max(1, j_hi - j_lo), 128, 0, s, d, G.LB2, j_lo, j_hi, b.carry,
+  const int jb_hi = std::min(j_hi + 1, G.nsup);  // owned super-blocks and the next one's start
+  AUXMC_LAUNCH(k_ts_boundary, std::max(1, jb_hi - j_lo), 128, 0, s, d, j_lo, jb_hi, b.carry2,
                b.bnd);
-  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, grid(t_hi - t_lo), cfg.threads, sm_rc, s, dm, obs, 1,
+  // + the predictive moments at t_hi (the next range's first step, from the
+  // carry of super-block j_hi: identical bits on both ranks) for the sampler
+  const int r_hi = std::min(t_hi + 1, T + 1);
+  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, grid(r_hi - t_lo), cfg.threads, sm_rc, s, dm, obs, 1,
                out->filt_mean, out->filt_cov, out->pred_mean, out->pred_cov, b.terms, status, t_lo,
-               t_hi, G.SB, b.bnd);
+               r_hi, G.SB, b.bnd);
   AUXMC_LAUNCH(k_ts_partials, (j_hi - j_lo + 127) / 128, 128, 0, s, T, G.SB, j_lo, j_hi, b.terms,
                ll_out);
   return AUXMC_OK;

@@ -40,12 +40,13 @@ __device__ __forceinline__ void noise_vec(const NoiseArgs& nz, int c, int T, int
 
 // pass 1: A_k for (fr, block k); smem per warp: 2 d*d
 __global__ void k_pg_block_ops(int T, int d, int Bfr, int Lb, int P, const double* __restrict__ elems,
-                               double* __restrict__ ops) {
+                               double* __restrict__ ops, int k_lo, int k_hi) {
   extern __shared__ double sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const long long item = (long long)blockIdx.x * nw + w;
-  if (item >= (long long)Bfr * P) return;
-  const int f = (int)(item / P), k = (int)(item % P);
+  const int span = k_hi - k_lo;  // blocks [k_lo, k_hi)
+  if (item >= (long long)Bfr * span) return;
+  const int f = (int)(item / span), k = k_lo + (int)(item % span);
   const int dd = d * d, ES = elem_stride(d);
   double* A = sm + (size_t)w * 2 * dd;
   double* Bm = A + dd;
@@ -69,12 +70,14 @@ __global__ void k_pg_block_ops(int T, int d, int Bfr, int Lb, int P, const doubl
 // pass 2: c~_t into traj[t] and a_k; smem per warp: 2 * 64 (xi, a)
 __global__ void k_pg_block_offsets(int T, int d, int B, int fr_shared, int Lb, int P,
                                    const double* __restrict__ elems, NoiseArgs nz,
-                                   double* __restrict__ traj, double* __restrict__ offs) {
+                                   double* __restrict__ traj, double* __restrict__ offs, int k_lo,
+                                   int k_hi) {
   __shared__ double sv[kWarpsPG][3][64];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long item = (long long)blockIdx.x * kWarpsPG + w;
-  if (item >= (long long)B * P) return;
-  const int c = (int)(item / P), k = (int)(item % P);
+  const int span = k_hi - k_lo;
+  if (item >= (long long)B * span) return;
+  const int c = (int)(item / span), k = k_lo + (int)(item % span);
   const int dd = d * d, ES = elem_stride(d);
   const double* E = elems + (size_t)(fr_shared ? 0 : c) * T * ES;
   double* out = traj + (size_t)c * (T + 1) * d;
@@ -110,7 +113,8 @@ __global__ void k_pg_block_offsets(int T, int d, int B, int fr_shared, int Lb, i
 // pass 3: terminal draw and the serial block carry (one warp per chain)
 __global__ void k_pg_carry(int T, int d, int B, int fr_shared, int P, const double* __restrict__ term,
                            const double* __restrict__ ops, const double* __restrict__ offs,
-                           NoiseArgs nz, double* __restrict__ traj, double* __restrict__ xin) {
+                           NoiseArgs nz, double* __restrict__ traj, double* __restrict__ xin,
+                           const double* __restrict__ xT_in) {
   __shared__ double sv[kWarpsPG][2][64];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * kWarpsPG + w;
@@ -121,15 +125,22 @@ __global__ void k_pg_carry(int T, int d, int B, int fr_shared, int P, const doub
   double* xn = sv[w][1];
   double* out = traj + (size_t)c * (T + 1) * d;
   const bool pre = nz.kind == AUXMC_NOISE_PREDRAWN;
-  for (int i = lane; i < d; i += 32)
-    xn[i] = pre ? nz.terminal[(size_t)c * d + i]
-                : normal_at(derive(nz.keys[c], kTerminalDraw, 0), (uint64_t)i);
-  __syncwarp();
-  for (int i = lane; i < d; i += 32) {  // x_T = m_T + L_T xi (pit.cpp:85-87)
-    double s = 0.0;
-    for (int j = 0; j < d; ++j) s += tm[d + i * d + j] * xn[j];
-    x[i] = tm[i] + s;
-    out[(size_t)T * d + i] = x[i];
+  if (xT_in) {  // time-sharded: x_T drawn by the rank that owns T
+    for (int i = lane; i < d; i += 32) {
+      x[i] = xT_in[(size_t)c * d + i];
+      out[(size_t)T * d + i] = x[i];
+    }
+  } else {
+    for (int i = lane; i < d; i += 32)
+      xn[i] = pre ? nz.terminal[(size_t)c * d + i]
+                  : normal_at(derive(nz.keys[c], kTerminalDraw, 0), (uint64_t)i);
+    __syncwarp();
+    for (int i = lane; i < d; i += 32) {  // x_T = m_T + L_T xi (pit.cpp:85-87)
+      double s = 0.0;
+      for (int j = 0; j < d; ++j) s += tm[d + i * d + j] * xn[j];
+      x[i] = tm[i] + s;
+      out[(size_t)T * d + i] = x[i];
+    }
   }
   __syncwarp();
   const double* O = ops + (size_t)(fr_shared ? 0 : c) * P * dd;
@@ -152,12 +163,13 @@ __global__ void k_pg_carry(int T, int d, int B, int fr_shared, int P, const doub
 // pass 4: x_t = G_t x_{t+1} + c~_t inside each block
 __global__ void k_pg_apply(int T, int d, int B, int fr_shared, int Lb, int P,
                            const double* __restrict__ elems, const double* __restrict__ xin,
-                           double* __restrict__ traj) {
+                           double* __restrict__ traj, int k_lo, int k_hi) {
   __shared__ double sv[kWarpsPG][2][64];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long item = (long long)blockIdx.x * kWarpsPG + w;
-  if (item >= (long long)B * P) return;
-  const int c = (int)(item / P), k = (int)(item % P);
+  const int span = k_hi - k_lo;
+  if (item >= (long long)B * span) return;
+  const int c = (int)(item / span), k = k_lo + (int)(item % span);
   const int ES = elem_stride(d);
   const double* E = elems + (size_t)(fr_shared ? 0 : c) * T * ES;
   double* out = traj + (size_t)c * (T + 1) * d;
@@ -212,16 +224,135 @@ int launch_prefix_generic(int T, int d, int B, int fr_shared, const double* elem
         cudaFuncSetAttribute(k_pg_block_ops, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long nops = (long long)Bfr * P, nvec = (long long)B * P;
     AUXMC_LAUNCH(k_pg_block_ops, (int)((nops + wo - 1) / wo), 32 * wo, smem, stream, T, d, Bfr,
-                 Lb, P, elems, ops);
+                 Lb, P, elems, ops, 0, P);
     AUXMC_LAUNCH(k_pg_block_offsets, (int)((nvec + kWarpsPG - 1) / kWarpsPG), 32 * kWarpsPG, 0,
-                 stream, T, d, B, fr_shared, Lb, P, elems, nz, traj, offs);
+                 stream, T, d, B, fr_shared, Lb, P, elems, nz, traj, offs, 0, P);
   }
   AUXMC_LAUNCH(k_pg_carry, (B + kWarpsPG - 1) / kWarpsPG, 32 * kWarpsPG, 0, stream, T, d, B,
-               fr_shared, P, term, ops, offs, nz, traj, xin);
+               fr_shared, P, term, ops, offs, nz, traj, xin, nullptr);
   if (T > 0) {
     const long long nvec = (long long)B * P;
     AUXMC_LAUNCH(k_pg_apply, (int)((nvec + kWarpsPG - 1) / kWarpsPG), 32 * kWarpsPG, 0, stream, T,
-                 d, B, fr_shared, Lb, P, elems, xin, traj);
+                 d, B, fr_shared, Lb, P, elems, xin, traj, 0, P);
+  }
+  return AUXMC_OK;
+}
+
+// ---------------------------------------------------------------- time-sharded prefix sampler
+// One path (B = 1, pit::prefix_sample, pit.cpp:78-115) with the horizon split like
+// the time-sharded filter: a rank owns the steps [t_lo, t_hi) of its super-blocks,
+// whose edges fall on sampler blocks (Lb divides the super-block length).  Phase 1
+// builds the rank's backward elements (the one at t_hi - 1 uses the predictive
+// covariance at t_hi that the sharded filter also produced), block operators and
+// offsets (+ x_T on the rank that owns T); the caller all-gathers the (A_k | a_k)
+// rows of every block in order and x_T; phase 2 runs the serial block carry over all
+// blocks (every rank, same bits) and expands the rank's blocks.
+int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, const double* pc,
+                        int Bfr, double* elems, double* term, int* st_fr, int store_cov,
+                        cudaStream_t stream, int t_lo, int t_hi);
+
+namespace {
+struct TsPrefixBufs {
+  double *elems, *term, *ops, *offs, *xin;
+  int* st;
+};
+TsPrefixBufs tsp_take(const DevModel& dm, Arena& ws) {
+  const int T = dm.T, d = dm.dx, Lb = block_len(T > 0 ? T : 1);
+  const int P = T > 0 ? (T + Lb - 1) / Lb : 1;
+  TsPrefixBufs b;
+  b.elems = ws.take<double>((size_t)(T > 0 ? T : 1) * elem_stride(d));
+  b.term = ws.take<double>((size_t)term_stride(d));
+  b.ops = ws.take<double>((size_t)P * d * d);
+  b.offs = ws.take<double>((size_t)P * d);
+  b.xin = ws.take<double>((size_t)P * d);
+  b.st = ws.take<int>(1);
+  return b;
+}
+
+__global__ void k_tsp_pack(int d, int k_lo, int k_hi, const double* ops, const double* offs,
+                           double* out) {  // rows (A_k | a_k) of blocks [k_lo, k_hi)
+  const int dd = d * d, R = dd + d;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (k_hi - k_lo) * R;
+       e += gridDim.x * blockDim.x) {
+    const int r = e / R, o = e % R, k = k_lo + r;
+    out[e] = o < dd ? ops[(size_t)k * dd + o] : offs[(size_t)k * d + (o - dd)];
+  }
+}
+__global__ void k_tsp_unpack(int d, int P, const double* in, double* ops, double* offs) {
+  const int dd = d * d, R = dd + d;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < P * R; e += gridDim.x * blockDim.x) {
+    const int k = e / R, o = e % R;
+    if (o < dd) ops[(size_t)k * dd + o] = in[e];
+    else offs[(size_t)k * d + (o - dd)] = in[e];
+  }
+}
+}  // namespace
+
+int tshard_prefix_geometry(int T, int* Lb, int* P) {
+  *Lb = block_len(T > 0 ? T : 1);
+  *P = T > 0 ? (T + *Lb - 1) / *Lb : 0;
+  return AUXMC_OK;
+}
+
+size_t tshard_prefix_workspace(const DevModel& dm) {
+  Arena ws{nullptr, 0, 0};
+  tsp_take(dm, ws);
+  return ws.used + 1024;
+}
+
+int tshard_prefix_local(const DevModel& dm, const double* fm, const double* fc, const double* pc,
+                        const NoiseArgs& nz, int t_lo, int t_hi, Arena& ws, double* blk_out,
+                        double* xT_out, double* traj, int* status, cudaStream_t stream) {
+  const int T = dm.T, d = dm.dx, Lb = block_len(T > 0 ? T : 1);
+  if (d < 1 || d > 64) return AUXMC_E_DIM;
+  const TsPrefixBufs b = tsp_take(dm, ws);
+  if (ws.base == nullptr) return AUXMC_OK;
+  if (!b.elems || !b.st) return AUXMC_E_WORKSPACE;
+  if (t_lo < 0 || t_hi > T + 1 || t_lo >= t_hi || t_lo % Lb != 0) return AUXMC_E_ARG;
+  AUXMC_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), stream));
+  // elements for steps [t_lo, min(t_hi, T)) and the terminal law when T is owned
+  int rc = launch_bwd_elements(dm, fm, fc, pc, 1, b.elems, b.term, status, 0, stream, t_lo, t_hi);
+  if (rc) return rc;
+  const int s_hi = std::min(t_hi, T);
+  if (s_hi > t_lo) {
+    const int k_lo = t_lo / Lb, k_hi = (s_hi + Lb - 1) / Lb, P = (T + Lb - 1) / Lb;
+    const int wo = std::max(1, std::min(kWarpsPG, (int)((200 * 1024) / (16 * d * d))));
+    const size_t smem = sizeof(double) * 2 * d * d * wo;
+    AUXMC_CUDA_TRY(
+        cudaFuncSetAttribute(k_pg_block_ops, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int nk = k_hi - k_lo;
+    AUXMC_LAUNCH(k_pg_block_ops, (nk + wo - 1) / wo, 32 * wo, smem, stream, T, d, 1, Lb, P,
+                 b.elems, b.ops, k_lo, k_hi);
+    AUXMC_LAUNCH(k_pg_block_offsets, (nk + kWarpsPG - 1) / kWarpsPG, 32 * kWarpsPG, 0, stream, T, d,
+                 1, 1, Lb, P, b.elems, nz, traj, b.offs, k_lo, k_hi);
+    AUXMC_LAUNCH(k_tsp_pack, 64, 256, 0, stream, d, k_lo, k_hi, b.ops, b.offs, blk_out);
+  }
+  if (t_hi == T + 1) {  // x_T = m_T + L_T xi on the rank that owns T
+    AUXMC_LAUNCH(k_pg_carry, 1, 32 * kWarpsPG, 0, stream, T, d, 1, 1, 0, b.term, b.ops, b.offs, nz,
+                 traj, b.xin, nullptr);
+    AUXMC_CUDA_TRY(cudaMemcpyAsync(xT_out, traj + (size_t)T * d, sizeof(double) * d,
+                                   cudaMemcpyDeviceToDevice, stream));
+  }
+  return AUXMC_OK;
+}
+
+int tshard_prefix_finish(const DevModel& dm, const NoiseArgs& nz, int t_lo, int t_hi, Arena& ws,
+                         const double* blk_all, const double* xT, double* traj,
+                         cudaStream_t stream) {
+  const int T = dm.T, d = dm.dx, Lb = block_len(T > 0 ? T : 1);
+  const TsPrefixBufs b = tsp_take(dm, ws);
+  if (ws.base == nullptr) return AUXMC_OK;
+  if (!b.elems || !b.st) return AUXMC_E_WORKSPACE;
+  if (T == 0) return AUXMC_OK;
+  const int P = (T + Lb - 1) / Lb;
+  AUXMC_LAUNCH(k_tsp_unpack, 64, 256, 0, stream, d, P, blk_all, b.ops, b.offs);
+  AUXMC_LAUNCH(k_pg_carry, 1, 32 * kWarpsPG, 0, stream, T, d, 1, 1, P, b.term, b.ops, b.offs, nz,
+               traj, b.xin, xT);
+  const int s_hi = std::min(t_hi, T);
+  if (s_hi > t_lo) {
+    const int k_lo = t_lo / Lb, k_hi = (s_hi + Lb - 1) / Lb;
+    AUXMC_LAUNCH(k_pg_apply, (k_hi - k_lo + kWarpsPG - 1) / kWarpsPG, 32 * kWarpsPG, 0, stream, T,
+                 d, 1, 1, Lb, P, b.elems, b.xin, traj, k_lo, k_hi);
   }
   return AUXMC_OK;
 }

@@ -117,7 +117,7 @@ template <bool BLOCK>
 __global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
                                const double* __restrict__ filt_cov,
                                const double* __restrict__ pred_cov, int Bfr, double* elems,
-                               double* term, int* status, int store_cov) {
+                               double* term, int* status, int store_cov, int t_lo, int t_hi) {
   extern __shared__ double smem[];
   const int d = m.dx, dd = d * d;
   const int T = m.T;
@@ -127,11 +127,12 @@ __global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
   const int groups_per_block = BLOCK ? 1 : (blockDim.x >> 5);
   double* sm = smem + (size_t)gid * per;
   int* flag = reinterpret_cast<int*>(sm + per - 2);
-  const long long n_items = (long long)Bfr * (T + 1);
+  const int span = t_hi - t_lo;  // items (b, t) for t in [t_lo, t_hi)
+  const long long n_items = (long long)Bfr * span;
   for (long long item = (long long)blockIdx.x * groups_per_block + gid; item < n_items;
        item += (long long)gridDim.x * groups_per_block) {
-    const int b = (int)(item / (T + 1));
-    const int t = (int)(item % (T + 1));
+    const int b = (int)(item / span);
+    const int t = t_lo + (int)(item % span);
     const double* fm = filt_mean + (size_t)b * (T + 1) * d;
     const double* fc = filt_cov + (size_t)b * (T + 1) * dd;
     const double* pc = pred_cov + (size_t)b * (T + 1) * dd;
@@ -161,13 +162,14 @@ template <int D>
 __global__ void k_bwd_elements_reg(DevModel m, const double* __restrict__ filt_mean,
                                    const double* __restrict__ filt_cov,
                                    const double* __restrict__ pred_cov, int Bfr, double* elems,
-                                   double* term, int* status, int store_cov) {
+                                   double* term, int* status, int store_cov, int t_lo, int t_hi) {
   constexpr int DD = D * D;
   const int T = m.T;
-  const long long n_items = (long long)Bfr * (T + 1);
+  const int span = t_hi - t_lo;
+  const long long n_items = (long long)Bfr * span;
   for (long long item = (long long)blockIdx.x * blockDim.x + threadIdx.x; item < n_items;
        item += (long long)gridDim.x * blockDim.x) {
-    const int b = (int)(item / (T + 1)), t = (int)(item % (T + 1));
+    const int b = (int)(item / span), t = t_lo + (int)(item % span);
     const double* fm = filt_mean + (size_t)b * (T + 1) * D;
     const double* fc = filt_cov + (size_t)b * (T + 1) * DD;
     double P[DD], L[DD];
@@ -566,19 +568,23 @@ int run_sampler(int sampler, int T, int B, int fr_shared, const double* elems,
 
 }  // namespace
 
+// items (b, t) for t in [t_lo, t_hi) (default: the whole horizon [0, T]; t = T is the
+// terminal law)
 int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, const double* pc,
                         int Bfr, double* elems, double* term, int* st_fr, int store_cov,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, int t_lo = 0, int t_hi = -1) {
   const int d = dm.dx;
   const int per = 8 * d * d + 4 * d + 4;
-  const long long n_items = (long long)Bfr * (dm.T + 1);
+  if (t_hi < 0) t_hi = dm.T + 1;
+  if (t_hi <= t_lo) return AUXMC_OK;
+  const long long n_items = (long long)Bfr * (t_hi - t_lo);
   if (d <= 4) {
     const int grid = (int)std::min<long long>((n_items + 127) / 128, 148LL * 16);
     switch (d) {
 #define CASE(D)                                                                                  \
   case D:                                                                                        \
     AUXMC_LAUNCH(k_bwd_elements_reg<D>, grid, 128, 0, stream, dm, fm, fc, pc, Bfr, elems, term, \
-                 st_fr, store_cov);                                                              \
+                 st_fr, store_cov, t_lo, t_hi);                                                  \
     break;
       CASE(1) CASE(2) CASE(3) CASE(4)
 #undef CASE
@@ -589,7 +595,7 @@ int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, 
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = (int)std::min<long long>(n_items, 148LL * 64);
     AUXMC_LAUNCH(k_bwd_elements<true>, grid, 128, smem, stream, dm, fm, fc, pc, Bfr, elems, term,
-                 st_fr, store_cov);
+                 st_fr, store_cov, t_lo, t_hi);
   } else {
     const int warps = 4;
     const size_t smem = sizeof(double) * per * warps;
@@ -597,7 +603,7 @@ int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, 
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = (int)std::min<long long>((n_items + warps - 1) / warps, 148LL * 64);
     AUXMC_LAUNCH(k_bwd_elements<false>, grid, 32 * warps, smem, stream, dm, fm, fc, pc, Bfr, elems,
-                 term, st_fr, store_cov);
+                 term, st_fr, store_cov, t_lo, t_hi);
   }
   return AUXMC_OK;
 }

@@ -1,5 +1,6 @@
-"""Time-sharded scan filter: pit::parallel_filter (pit.cpp:117-188) for one long
-sequence split over ranks.
+"""Time-sharded scan filter and prefix sampler: pit::parallel_filter
+(pit.cpp:117-188) and pit::prefix_sample (pit.cpp:78-115) for one long sequence
+split over ranks.
 
 The horizon's block tree (blocks of LB steps, super-blocks of SB = LB² steps)
 depends only on T.  Rank r owns a contiguous run of super-blocks
@@ -130,15 +131,99 @@ def sharded_filter(model: Model, obs, rank: int, world: int, exchange):
     return fr, lm, (sf.t_lo, sf.t_hi)
 
 
+class ShardedPrefixSampler:
+    """One rank's share of pit::prefix_sample for one path, on the time range of its
+    ShardedScanFilter (same super-blocks)."""
+
+    def __init__(self, sf: ShardedScanFilter):
+        self.sf, self.model = sf, sf.model
+        lib = _lib.load()
+        Lb, P = C.c_int(), C.c_int()
+        _lib.check(lib.auxmc_tshard_prefix_geometry(self.model.T, C.byref(Lb), C.byref(P)),
+                   "tshard_prefix_geometry")
+        self.Lb, self.P = Lb.value, P.value
+        if sf.geom.SB % self.Lb:
+            raise ValueError("sampler blocks must divide the filter super-blocks")
+        self.ws_bytes = lib.auxmc_tshard_prefix_workspace(C.byref(sf._mr))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.model.device)
+        self.rows = self.model.dx * self.model.dx + self.model.dx
+        self.max_blocks = max(1, (sf.geom.SB // self.Lb) * sf.max_owned)  # rows per rank
+
+    def _blocks(self, r):
+        _, _, t_lo, t_hi = self.sf.geom.owned(r, self.sf.world)
+        s_hi = min(t_hi, self.model.T)
+        return (t_lo // self.Lb, -(-s_hi // self.Lb)) if s_hi > t_lo else (0, 0)
+
+    def local(self, fr: FilterResult, noise, traj: torch.Tensor):
+        """Phase 1: block rows of this rank (padded) and x_T (zeros unless this rank owns T)."""
+        dev, d = self.model.device, self.model.dx
+        self.noise_raw = noise.raw()
+        k_lo, k_hi = self._blocks(self.sf.rank)
+        out = torch.zeros((self.max_blocks, self.rows), dtype=torch.float64, device=dev)
+        xT = torch.zeros(d, dtype=torch.float64, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        if self.sf.t_hi > self.sf.t_lo:
+            raw = fr.raw()
+            _lib.check(_lib.load().auxmc_tshard_prefix_local(
+                C.byref(self.sf._mr), C.byref(raw), C.byref(self.noise_raw), self.sf.t_lo,
+                self.sf.t_hi, self.ws.data_ptr(), self.ws_bytes, out.data_ptr(), xT.data_ptr(),
+                traj.data_ptr(), self.status.data_ptr(), _stream()), "tshard_prefix_local")
+        return out, xT
+
+    def finish(self, gathered_rows, gathered_xT, traj: torch.Tensor):
+        """Phase 2: the path on this rank's time range (written into traj [T+1, d])."""
+        parts = []
+        for r, p in enumerate(gathered_rows):
+            k_lo, k_hi = self._blocks(r)
+            parts.append(p[:k_hi - k_lo])
+        blk_all = torch.cat(parts, 0).contiguous()
+        assert blk_all.shape[0] == self.P, (blk_all.shape, self.P)
+        owner = max(r for r in range(self.sf.world) if self.sf.geom.owned(r, self.sf.world)[3] ==
+                    self.model.T + 1)
+        xT = gathered_xT[owner].contiguous()
+        if self.sf.t_hi > self.sf.t_lo:
+            _lib.check(_lib.load().auxmc_tshard_prefix_finish(
+                C.byref(self.sf._mr), C.byref(self.noise_raw), self.sf.t_lo, self.sf.t_hi,
+                self.ws.data_ptr(), self.ws_bytes, blk_all.data_ptr(), xT.data_ptr(),
+                traj.data_ptr(), _stream()), "tshard_prefix_finish")
+        return traj
+
+
+def sharded_filter_and_prefix(model: Model, obs, noise, rank: int, world: int, exchange):
+    """Scan filter + prefix path of one sequence split over ranks; returns
+    (FilterResult, log_marginal, traj [T+1, d], (t_lo, t_hi)) with this rank's time
+    range filled (traj row T on every rank)."""
+    sf = ShardedScanFilter(model, rank, world)
+    fr, ll = sf.finish(exchange(sf.local(obs)))
+    lm = sf.log_marginal(exchange(ll))
+    fr.log_marginal.copy_(lm)
+    ps = ShardedPrefixSampler(sf)
+    traj = torch.zeros((model.T + 1, model.dx), dtype=torch.float64, device=model.device)
+    rows, xT = ps.local(fr, noise, traj)
+    ps.finish(exchange(rows), exchange(xT), traj)
+    return fr, lm, traj, (sf.t_lo, sf.t_hi)
+
+
 class LocalExchange:
     """Runs `world` shards in one process: collects each shard's tensor, then hands
     every shard the rank-ordered list (for tests and single-GPU checks)."""
 
     @staticmethod
-    def run(model: Model, obs, world: int):
+    def run(model: Model, obs, world: int, noise=None):
         shards = [ShardedScanFilter(model, r, world) for r in range(world)]
         aggs = [s.local(obs) for s in shards]
         outs = [s.finish(aggs) for s in shards]
         lls = [ll for _, ll in outs]
         lm = shards[0].log_marginal(lls)
-        return shards, [fr for fr, _ in outs], lm
+        frs = [fr for fr, _ in outs]
+        if noise is None:
+            return shards, frs, lm
+        samplers = [ShardedPrefixSampler(s) for s in shards]
+        trajs = [torch.zeros((model.T + 1, model.dx), dtype=torch.float64, device=model.device)
+                 for _ in shards]
+        loc = [p.local(fr, noise, tr) for p, fr, tr in zip(samplers, frs, trajs)]
+        rows = [r for r, _ in loc]
+        xts = [x for _, x in loc]
+        for p, tr in zip(samplers, trajs):
+            p.finish(rows, xts, tr)
+        return shards, frs, lm, trajs

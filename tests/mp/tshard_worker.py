@@ -26,11 +26,16 @@ def main(out_path):
     m = random_model(s, 2500, 3, 2, True, True)
     obs = simulate_obs(m, O.from_seed(72))
     gm = to_gpu_model(m)
-    fr, lm, (t_lo, t_hi) = tshard.sharded_filter(gm, obs, rank, world, tshard.torch_exchange())
+    from paper_2303_00301_b200 import lgssm, rng
+    noise = lgssm.Noise.stream(rng.chain_keys(73, 1))
+    fr, lm, traj, (t_lo, t_hi) = tshard.sharded_filter_and_prefix(gm, obs, noise, rank, world,
+                                                                   tshard.torch_exchange())
     torch.cuda.synchronize()
     sl = slice(t_lo, t_hi)
+    ps = slice(t_lo, min(t_hi, m.T))
     mine = torch.cat([fr.filt_mean[0, sl].reshape(-1), fr.filt_cov[0, sl].reshape(-1),
-                      fr.pred_mean[0, sl].reshape(-1), fr.pred_cov[0, sl].reshape(-1)]).cpu()
+                      fr.pred_mean[0, sl].reshape(-1), fr.pred_cov[0, sl].reshape(-1),
+                      traj[ps].reshape(-1), traj[m.T]]).cpu()
     sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(sizes, torch.tensor([mine.numel()]))
     nmax = int(max(int(n) for n in sizes))
@@ -40,15 +45,16 @@ def main(out_path):
     dist.all_gather(parts, padded)
     parts = [p[:int(n)] for p, n in zip(parts, sizes)]
     if rank == 0:
-        shards, frs, lm1 = tshard.LocalExchange.run(gm, obs, 1)
-        ref = frs[0]
+        shards, frs, lm1, trajs = tshard.LocalExchange.run(gm, obs, 1, noise)
+        ref, rtraj = frs[0], trajs[0]
         ok = True
         for r in range(world):
             g = tshard.TShardGeom.of(m.T, m.dx)
             _, _, a, b = g.owned(r, world)
             want = torch.cat([ref.filt_mean[0, a:b].reshape(-1), ref.filt_cov[0, a:b].reshape(-1),
                               ref.pred_mean[0, a:b].reshape(-1),
-                              ref.pred_cov[0, a:b].reshape(-1)]).cpu()
+                              ref.pred_cov[0, a:b].reshape(-1),
+                              rtraj[a:min(b, m.T)].reshape(-1), rtraj[m.T]]).cpu()
             ok = ok and torch.equal(parts[r], want)
         ok = ok and torch.equal(lm.cpu(), lm1.cpu())
         want_o = O.kalman_filter(m, obs)

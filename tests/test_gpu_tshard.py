@@ -70,3 +70,34 @@ def test_tshard_world2_gloo_processes(tmp_path):
     res = json.load(open(out))
     assert res["world"] == 2 and res["bit_identical"], res
     assert res["lm_rel_err"] < 1e-9, res
+
+
+@pytest.mark.parametrize("T,dx,dy,seed", [(3000, 3, 2, 81), (1200, 10, 4, 82)])
+def test_tshard_prefix_bit_identical_and_matches_oracle(oracle, T, dx, dy, seed):
+    """Sharded prefix sampler: every split gives the same path bits; the path is the
+    oracle's prefix_sample (stream noise, same key) to FP64 tolerance."""
+    from paper_2303_00301_b200 import lgssm, rng, tshard
+    s = oracle.derive(oracle.from_seed(seed), oracle.L_SIMULATE, 2)
+    m = random_model(s, T, dx, dy, True, False)
+    obs = simulate_obs(m, oracle.from_seed(seed + 100))
+    gm = to_gpu_model(m)
+    keys = rng.chain_keys(seed, 1)
+    noise = lgssm.Noise.stream(keys)
+    g = tshard.TShardGeom.of(T, dx)
+    base = None
+    for world in (1, 2, 3, min(8, g.nsup)):
+        shards, frs, lm, trajs = tshard.LocalExchange.run(gm, obs, world, noise)
+        path = torch.empty_like(trajs[0])
+        for sh, tr in zip(shards, trajs):
+            path[sh.t_lo:min(sh.t_hi, T)] = tr[sh.t_lo:min(sh.t_hi, T)]
+        path[T] = trajs[-1][T]
+        for tr in trajs:
+            assert torch.equal(tr[T], path[T])
+        if base is None:
+            base = path
+            fr_o = oracle.kalman_filter(m, obs)
+            want = oracle.prefix_sample(m, fr_o, oracle.stream_noise(
+                oracle.derive(oracle.from_seed(seed), oracle.L_CHAIN, 0)))
+            assert_close(path.cpu(), want, 1e-8, "sharded prefix path")
+        else:
+            assert torch.equal(path, base), f"world {world} path differs"
