@@ -10,7 +10,7 @@ Inputs (filter result, pre-drawn variates, 2.1 GB) and outputs (2.1 GB) are
 far larger than the 126 MB L2, so no explicit flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config c2|c1|c3|c4|c5] [--sampler prefix|dnc|seq] [--noise predrawn|rng]
+                    [--config c2|c1|c3|c4|c5|c5ts] [--sampler prefix|dnc|seq] [--noise predrawn|rng]
 
 Under torchrun each rank runs its own chains; the step time is the max over
 ranks (CUDA events, barrier + synchronize on both sides).  Rank 0 prints one
@@ -42,7 +42,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="c2", choices=["c2", "c1", "c3", "c4", "c5"])
+    p.add_argument("--config", default="c2", choices=["c2", "c1", "c3", "c4", "c5", "c5ts"])
     p.add_argument("--sampler", default="prefix", choices=["prefix", "dnc", "seq"])
     p.add_argument("--noise", default="predrawn", choices=["predrawn", "rng"])
     p.add_argument("--chains", type=int, default=0, help="chains per GPU (0 = config default)")

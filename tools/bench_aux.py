@@ -37,6 +37,9 @@ def run(args, rank, world, local):
         spec = bm.ModelSpec(kind="lorenz96", T=T, dx=40, data_seed=3)
         backend, delta = auxk.Backend.kSequential, 0.05
         flops_ct = 2.14e6  # F_seq at d = 40, q = 20
+    elif cfg == "c5ts":
+        T, C, d = args.T or (1 << 20), 1, 16
+        spec, backend, delta, flops_ct = None, None, None, 464e3
     elif cfg == "c5":
         T, C, d = args.T or (1 << 20), args.chains or 1, 16
         spec = bm.ModelSpec(kind="spatio-temporal", T=T, grid=4, data_seed=7)
@@ -53,6 +56,8 @@ def run(args, rank, world, local):
         # flops) + accumulate — the minimal structure-aware count, below SURVEY's
         # N^2 (3d^2 + d + exp) which assumed a triangular solve per pair
         flops_ct = N * N * (2 * d + 3 + 20.0)
+    if cfg == "c5ts":
+        return run_c5ts(args, rank, world, local, device)
     lat, data = bm.simulate(spec)
     tg = auxk.make_target(spec, data, device=device)
     x0 = torch.as_tensor(lat, device=device) if cfg != "c1" else \
@@ -121,6 +126,63 @@ def run(args, rank, world, local):
                          "frac": tflops / FP64_PEAK_TFLOPS, "traffic": None,
                          "algorithmic_flops_per_chain_timestep": flops_ct,
                          "peak_source": "measured DMMA FP64 throughput (profiles/r1_micro_latency_fp64.txt)"},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_c5ts(args, rank, world, local, device):
+    """C5 time-sharded: the scan filter and the prefix sampler of ONE path of a
+    d = 16 linear-Gaussian model (the shape of C5's auxiliary LGSSM: dx = dy = 16)
+    with the horizon split over the ranks (tshard.py); strong scaling (T fixed).
+    A step = sharded filter + sharded path draw, including the all-gathers."""
+    import numpy as np
+    import torch
+    from bench import Clocks, timed
+    from paper_2303_00301_b200 import _lib, bench_models as bm, lgssm, rng, tshard
+    T = args.T or (1 << 20)
+    spec = bm.ModelSpec(kind="lgssm-synthetic", T=T, dx=16, dy=16, data_seed=7)
+    lat, data = bm.simulate(spec)
+    model = bm.synthetic_lgssm(spec, device=device)
+    obs = torch.as_tensor(np.asarray(data), dtype=torch.float64, device=device)
+    noise = lgssm.Noise.stream(rng.chain_keys(1, 1, device=device))
+    if world > 1:
+        exchange = tshard.torch_exchange()
+    else:
+        def exchange(t):
+            return [t]
+    lib = _lib.load()
+
+    def step():
+        tshard.sharded_filter_and_prefix(model, obs, noise, rank, world, exchange)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    n0 = lib.auxmc_launch_count()
+    with Clocks(local) as clk:
+        ms = timed(step, args.steps, world)
+    launches = lib.auxmc_launch_count() - n0
+    value = (T + 1) * args.steps / (ms / 1e3)
+    F_pit = 113.333 * 16 ** 3 + 8 * 16 * 256 + 8 * 256 * 16 + 2 / 3 * 16 ** 3  # SURVEY §8(d)
+    tflops = F_pit * value / 1e12
+    if rank == 0:
+        g = tshard.TShardGeom.of(T, 16)
+        line = {
+            "metric": METRIC, "value": value, "unit": "path-timesteps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "C5 time-sharded scan filter + prefix sampler, one path, "
+                                   "d = 16 LGSSM (C5's auxiliary-model shape)", "T": T,
+                       "super_blocks": g.nsup, "super_block_steps": g.SB,
+                       "parallelism": f"time sharded over {world} GPU(s), all-gather per phase"},
+            "roofline": {"bound": "fp64", "achieved": tflops, "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": tflops / FP64_PEAK_TFLOPS, "traffic": None,
+                         "algorithmic_flops_per_chain_timestep": F_pit,
+                         "peak_source": "measured DMMA FP64 throughput "
+                                        "(profiles/r1_micro_latency_fp64.txt)"},
             "cpu_baseline": None, "e2e": None, "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
