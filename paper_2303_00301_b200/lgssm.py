@@ -202,6 +202,82 @@ class PathSampler:
         return out
 
 
+class HostPipeline:
+    """Pathwise draws for B chains from pinned HOST buffers with copy/compute overlap.
+
+    The shared filter result is copied once per call; chains go in `chunks` equal
+    chunks, and chunk i's host-to-device copy, chunk i-1's draw and chunk i-2's
+    device-to-host copy run on three streams (double-buffered device staging), so
+    the two PCIe directions overlap each other and the kernels.  Same draws as one
+    PathSampler call over all B chains (chain c keeps its noise rows)."""
+
+    def __init__(self, model: Model, B: int, sampler: int, chunks: int = 8):
+        if B % chunks:
+            raise ValueError("HostPipeline: chunks must divide the chain count")
+        self.model, self.B, self.sampler, self.chunks = model, B, sampler, chunks
+        self.Bc = B // chunks
+        self.ps = PathSampler(model, self.Bc, sampler, True)
+        self.s_in, self.s_run, self.s_out = (torch.cuda.Stream(model.device) for _ in range(3))
+        self._buf = None
+
+    def _alloc(self, noise: Noise, fr: FilterResult):
+        m, dev, Bc = self.model, self.model.device, self.Bc
+        def like(t, rows):
+            return torch.empty((rows,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+        bufs = []
+        for _ in range(2):
+            b = {"out": torch.empty((Bc, m.T + 1, m.dx), dtype=torch.float64, device=dev)}
+            for k in ("keys", "terminal", "backward", "bridge"):
+                v = getattr(noise, k)
+                b[k] = None if v is None else like(v, Bc)
+            bufs.append(b)
+        self._fr = FilterResult(*(torch.empty_like(t, device=dev) for t in
+                                  (fr.pred_mean, fr.pred_cov, fr.filt_mean, fr.filt_cov,
+                                   fr.log_marginal)), torch.zeros(1, dtype=torch.int32,
+                                                                  device=dev))
+        self._buf = bufs
+
+    def __call__(self, fr_host: FilterResult, noise_host: Noise, out_host: torch.Tensor):
+        if self._buf is None:
+            self._alloc(noise_host, fr_host)
+        main = torch.cuda.current_stream(self.model.device)
+        ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "run", "out")}
+        self.s_in.wait_stream(main)
+        with torch.cuda.stream(self.s_in):  # shared filter result, once
+            for d, h in ((self._fr.pred_mean, fr_host.pred_mean), (self._fr.pred_cov,
+                         fr_host.pred_cov), (self._fr.filt_mean, fr_host.filt_mean),
+                         (self._fr.filt_cov, fr_host.filt_cov),
+                         (self._fr.log_marginal, fr_host.log_marginal)):
+                d.copy_(h, non_blocking=True)
+        fr_ready = torch.cuda.Event()
+        fr_ready.record(self.s_in)
+        self.s_run.wait_event(fr_ready)
+        for i in range(self.chunks):
+            j, b = i % 2, self._buf[i % 2]
+            sl = slice(i * self.Bc, (i + 1) * self.Bc)
+            if i >= 2:
+                self.s_in.wait_event(ev["run"][j])   # staging j consumed by draw i-2
+                self.s_run.wait_event(ev["out"][j])  # output j drained by copy i-2
+            with torch.cuda.stream(self.s_in):
+                for k in ("keys", "terminal", "backward", "bridge"):
+                    if b[k] is not None:
+                        b[k].copy_(getattr(noise_host, k)[sl], non_blocking=True)
+                ev["in"][j].record(self.s_in)
+            self.s_run.wait_event(ev["in"][j])
+            with torch.cuda.stream(self.s_run):
+                nz = Noise(keys=b["keys"], terminal=b["terminal"], backward=b["backward"],
+                           bridge=b["bridge"])
+                self.ps(self._fr, nz, b["out"])
+                ev["run"][j].record(self.s_run)
+            self.s_out.wait_event(ev["run"][j])
+            with torch.cuda.stream(self.s_out):
+                out_host[sl].copy_(b["out"], non_blocking=True)
+                ev["out"][j].record(self.s_out)
+        main.wait_stream(self.s_out)
+        main.wait_stream(self.s_run)
+        return out_host
+
+
 def _sample(model, fr, noise, sampler):
     B = noise.B
     shared = fr.filt_mean.shape[0] == 1

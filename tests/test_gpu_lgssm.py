@@ -324,3 +324,27 @@ def test_dnc_predrawn_requires_bridge_draws(gpu, oracle):
     term, back, _ = predrawn(np.random.default_rng(0), 2, m.T, m.dx, 32)
     with pytest.raises(Exception):
         lgssm.PathSampler(gm, 2, 2, True)(fr, lgssm.Noise.predrawn(term, back, None))
+
+
+@pytest.mark.parametrize("sampler", [1, 2])
+def test_host_pipeline_equals_device_call(gpu, oracle, sampler):
+    """lgssm.HostPipeline (chunked host<->device copies on three streams) returns
+    exactly the paths of one device-side PathSampler call."""
+    lgssm, pit, _ = gpu
+    m, obs = _oracle_case(oracle, 200, 4, 1, False, False, 44)
+    gm = to_gpu_model(m)
+    fr = lgssm.kalman_filter(gm, obs)
+    B = 16
+    term, back, bridge = predrawn(np.random.default_rng(9), B, m.T, m.dx,
+                                  pit.dnc_bridge_count(m.T))
+    noise = lgssm.Noise.predrawn(term, back, bridge if sampler == 2 else None)
+    want = lgssm.PathSampler(gm, B, sampler, True)(fr, noise).cpu()
+    pin = lambda t: None if t is None else t.cpu().pin_memory()  # noqa: E731
+    h_fr = lgssm.FilterResult(pin(fr.pred_mean), pin(fr.pred_cov), pin(fr.filt_mean),
+                              pin(fr.filt_cov), pin(fr.log_marginal), fr.status.cpu())
+    h_noise = lgssm.Noise(terminal=pin(noise.terminal), backward=pin(noise.backward),
+                          bridge=pin(noise.bridge))
+    out = torch.empty((B, m.T + 1, m.dx), dtype=torch.float64).pin_memory()
+    lgssm.HostPipeline(gm, B, sampler, chunks=4)(h_fr, h_noise, out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
