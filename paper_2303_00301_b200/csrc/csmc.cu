@@ -375,6 +375,34 @@ __global__ void k_pit_particles(DevTarget tg, FactorRef f, PgArgs a, double* lw)
   }
 }
 
+// exp(x) for x <= 0 in the LSE inner loop: x = k ln2 + r, |r| <= ln2/2, exp(r) by
+// its degree-11 Taylor polynomial (truncation < 1e-15 relative), 2^k by exponent
+// construction; x < -708 returns 0 (below DBL_MIN: the sum's exact online
+// fallback handles total underflow).  About half the instructions of the libm
+// routine, which also handles overflow, NaN and subnormal results.
+__device__ __forceinline__ double exp_nonpos(double x) {
+  const double kLog2e = 1.4426950408889634, kLn2Hi = 6.93147180369123816490e-01,
+               kLn2Lo = 1.90821492927058770002e-10;
+  const double kd = rint(x * kLog2e);
+  double r = fma(-kd, kLn2Hi, x);
+  r = fma(-kd, kLn2Lo, r);
+  double p = 2.505210838544172e-08;  // 1/11!
+  p = fma(p, r, 2.755731922398589e-07);
+  p = fma(p, r, 2.7557319223985893e-06);
+  p = fma(p, r, 2.48015873015873e-05);
+  p = fma(p, r, 1.984126984126984e-04);
+  p = fma(p, r, 1.388888888888889e-03);
+  p = fma(p, r, 8.333333333333333e-03);
+  p = fma(p, r, 4.1666666666666664e-02);
+  p = fma(p, r, 1.6666666666666666e-01);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int k = (int)kd;
+  const double scale = __hiloint2double((k + 1023) << 20, 0);
+  return x < -708.0 ? 0.0 : p * scale;
+}
+
 // Forward log-messages alpha_t(j) = lw_t(j) + LSE_i(alpha_{t-1}(i) + log p(x_t^j | x_{t-1}^i)),
 // one CTA per chain, then backward index sampling with the reference's addresses.
 template <int DT>
@@ -459,7 +487,7 @@ __global__ void k_pit_forward_backward(DevTarget tg, FactorRef f, PgArgs a, cons
               const double z = w[k] - vi[(i + u) * DT + k];
               sq += z * z;
             }
-            acc4[u] += exp(ai[i + u] - 0.5 * sq);
+            acc4[u] += exp_nonpos(ai[i + u] - 0.5 * sq);
           }
         }
         for (; i < ihi; ++i) {
@@ -469,7 +497,7 @@ __global__ void k_pit_forward_backward(DevTarget tg, FactorRef f, PgArgs a, cons
             const double z = w[k] - vi[i * DT + k];
             sq += z * z;
           }
-          acc4[0] += exp(ai[i] - 0.5 * sq);
+          acc4[0] += exp_nonpos(ai[i] - 0.5 * sq);
         }
         const double sp = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
         if (parts == 1) {
