@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kDncSubThreads)
   }
 }
 
-// ---- any d (9..32): warp per (node, chain), lanes over rows; the dot products
+// ---- any d (9..60): warp per (node, chain), lanes over rows; the dot products
 // run in the register kernels' order (ascending j), so results match them.
 constexpr int kDncWarps = 4;
 
@@ -551,7 +551,8 @@ int launch_dnc(const DevModel& dm, int Bfr, int fr_shared, const double* elems,
   double* aff = d <= 8 ? ws.take<double>((size_t)Bfr * n_heap * ((3 * dd + d + 1) & ~1)) : nullptr;
   if (ws.base == nullptr) return AUXMC_OK;
   if (!nodes || !params || (d <= 8 && !aff)) return AUXMC_E_WORKSPACE;
-  if (d > 32) return AUXMC_E_DIM;
+  // CTA bridges keep 8 d*d + 4 doubles in shared memory: d <= 60
+  if (d > 64 || sizeof(double) * (8 * (size_t)dd + 4) > 227 * 1024) return AUXMC_E_DIM;
   const bool block = d > 16;  // CTA groups (blocked DMMA factor/solves) for d > 16
   const int warps = 4;
   if (T > 0) {

@@ -90,10 +90,9 @@ def test_kalman_filter_large_dims_match_oracle(gpu, oracle, case):
 @pytest.mark.parametrize("case", LARGE_CASES)
 def test_samplers_large_dims_match_oracle(gpu, oracle, case, sampler):
     """d > 8: sequential (warp per path), generic blocked prefix scan, and the
-    group DnC (d <= 32)."""
+    group DnC (CTA bridges for d > 16)."""
     lgssm, pit, _ = gpu
-    if sampler == 2 and case[1] > 32:
-        pytest.skip("DnC implemented for d <= 32")
+
     m, obs = _oracle_case(oracle, *case)
     fr_o = oracle.kalman_filter(m, obs)
     gm = to_gpu_model(m)
