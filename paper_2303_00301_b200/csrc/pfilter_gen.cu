@@ -91,6 +91,61 @@ __device__ void g_lu_solve(const Grp& g, int d, const double* LU, const int* per
   }
 }
 
+// One warp, d <= 16: Minv = M^{-1} by Gauss-Jordan with partial pivoting on the
+// augmented [M | I], lane j holding column j in registers (2d <= 32 lanes).  The
+// pivot rule is PartialPivLU's (first row of largest |.| at or below the
+// diagonal); rows are swapped and eliminated inside every lane's column, the
+// pivot column is broadcast by shuffles — no shared-memory round trips.
+__device__ void w_inverse_gj(int lane, int d, const double* M, double* Minv) {
+  constexpr int MX = 16;
+  double col[MX];
+  const int j = lane;
+#pragma unroll
+  for (int i = 0; i < MX; ++i)
+    col[i] = (i < d && j < 2 * d) ? (j < d ? M[i * d + j] : (i == j - d ? 1.0 : 0.0)) : 0.0;
+  for (int k = 0; k < d; ++k) {
+    // pivot search by the lane owning column k
+    double best = -1.0;
+    int p = k;
+#pragma unroll
+    for (int i = 0; i < MX; ++i)
+      if (i >= k && i < d && fabs(col[i]) > best) {
+        best = fabs(col[i]);
+        p = i;
+      }
+    p = __shfl_sync(0xffffffffu, p, k);
+    // swap rows k and p in every column
+    double vk = 0.0, vp = 0.0;
+#pragma unroll
+    for (int i = 0; i < MX; ++i) {
+      vk = i == k ? col[i] : vk;
+      vp = i == p ? col[i] : vp;
+    }
+#pragma unroll
+    for (int i = 0; i < MX; ++i) {
+      if (i == k) col[i] = vp;
+      else if (i == p) col[i] = vk;
+    }
+    // eliminate with the pivot column (broadcast from lane k)
+    const double piv = __shfl_sync(0xffffffffu, vp, k);
+    double rowk = 0.0;
+#pragma unroll
+    for (int i = 0; i < MX; ++i) rowk = i == k ? col[i] : rowk;
+    const double xk = rowk / piv;  // this column's entry of the normalized pivot row
+#pragma unroll
+    for (int i = 0; i < MX; ++i) {
+      const double m = __shfl_sync(0xffffffffu, col[i], k);  // pivot column entry, row i
+      if (i < d) col[i] = i == k ? xk : fma(-m, xk, col[i]);
+    }
+  }
+  if (j >= d && j < 2 * d) {
+#pragma unroll
+    for (int i = 0; i < MX; ++i)
+      if (i < d) Minv[i * d + (j - d)] = col[i];
+  }
+  __syncwarp();
+}
+
 // o = combine(u, v) (pit.cpp:36-51); scratch: 5 dd + 2 d doubles, 2 d + 1 ints
 struct CombScratch {
   double *M1, *M2, *S, *T1, *T2, *t, *w;
@@ -116,8 +171,12 @@ __device__ void g_combine(const Grp& g, int d, const double* u, const double* v,
   g.sync();
   for (int i = g.lane; i < d; i += g.size) s.M1[i * d + i] += 1.0;
   g.sync();
-  g_lu_factor(g, d, s.M1, s.p1, s.idx);
-  g_lu_solve(g, d, s.M1, s.p1, d, s.T2, Minv);  // M1^{-1}
+  if (!g.block && d <= 16) {
+    w_inverse_gj(g.lane, d, s.M1, Minv);  // M1^{-1}, registers and shuffles
+  } else {
+    g_lu_factor(g, d, s.M1, s.p1, s.idx);
+    g_lu_solve(g, d, s.M1, s.p1, d, s.T2, Minv);  // M1^{-1}
+  }
   // t = uC veta + ub ; t2 = veta - vJ ub
   for (int i = g.lane; i < d; i += g.size) {
     double acc = 0.0, acc2 = 0.0;
