@@ -103,35 +103,30 @@ __device__ void w_inverse_gj(int lane, int d, const double* M, double* Minv) {
 #pragma unroll
   for (int i = 0; i < MX; ++i)
     col[i] = (i < d && j < 2 * d) ? (j < d ? M[i * d + j] : (i == j - d ? 1.0 : 0.0)) : 0.0;
-  for (int k = 0; k < d; ++k) {
-    // pivot search by the lane owning column k
+#pragma unroll
+  for (int k = 0; k < MX; ++k) {  // fully unrolled: every index but the pivot row is static
+    if (k >= d) break;
+    // pivot search by the lane owning column k (rows k..d-1)
     double best = -1.0;
     int p = k;
 #pragma unroll
-    for (int i = 0; i < MX; ++i)
-      if (i >= k && i < d && fabs(col[i]) > best) {
+    for (int i = k; i < MX; ++i)
+      if (i < d && fabs(col[i]) > best) {
         best = fabs(col[i]);
         p = i;
       }
     p = __shfl_sync(0xffffffffu, p, k);
-    // swap rows k and p in every column
-    double vk = 0.0, vp = 0.0;
+    // swap rows k and p (p >= k) in every column
+    const double vk = col[k];
+    double vp = vk;
 #pragma unroll
-    for (int i = 0; i < MX; ++i) {
-      vk = i == k ? col[i] : vk;
-      vp = i == p ? col[i] : vp;
-    }
+    for (int i = k + 1; i < MX; ++i) vp = i == p ? col[i] : vp;
 #pragma unroll
-    for (int i = 0; i < MX; ++i) {
-      if (i == k) col[i] = vp;
-      else if (i == p) col[i] = vk;
-    }
+    for (int i = k + 1; i < MX; ++i) col[i] = i == p ? vk : col[i];
+    col[k] = vp;
     // eliminate with the pivot column (broadcast from lane k)
     const double piv = __shfl_sync(0xffffffffu, vp, k);
-    double rowk = 0.0;
-#pragma unroll
-    for (int i = 0; i < MX; ++i) rowk = i == k ? col[i] : rowk;
-    const double xk = rowk / piv;  // this column's entry of the normalized pivot row
+    const double xk = vp / piv;  // this column's entry of the normalized pivot row
 #pragma unroll
     for (int i = 0; i < MX; ++i) {
       const double m = __shfl_sync(0xffffffffu, col[i], k);  // pivot column entry, row i
