@@ -526,6 +526,18 @@ __host__ __device__ inline int rec_smem(int d, int dy) {
   return 3 * d * d + dy * d + 3 * dy * dy + 2 * W + 8;
 }
 
+// warp groups per CTA: as many (<= 8) as the largest per-group shared-memory
+// footprint allows — the combine chains are latency-bound, so occupancy matters
+GrpCfg launch_cfg(int d, int dy) {
+  GrpCfg c = grp_cfg(d, dy);
+  if (c.block) return c;
+  const size_t per = sizeof(double) * (size_t)std::max(elem_smem(d, dy),
+                                                       std::max(scan_smem(d), rec_smem(d, dy)));
+  c.groups = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / per));
+  c.threads = 32 * c.groups;
+  return c;
+}
+
 template <bool BLOCK>
 __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
                               const double* __restrict__ fm, const double* __restrict__ fc,
@@ -638,7 +650,7 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   double* carry2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
   if (ws.base == nullptr) return AUXMC_OK;
   if (!el || !agg || !carry || !terms || (two && (!agg2 || !carry2))) return AUXMC_E_WORKSPACE;
-  const GrpCfg cfg = grp_cfg(d, dy);
+  const GrpCfg cfg = launch_cfg(d, dy);
   const int gp = cfg.groups;
   const size_t sm_el = sizeof(double) * elem_smem(d, dy) * gp;
   const size_t sm_sc = sizeof(double) * scan_smem(d) * gp;
@@ -748,7 +760,7 @@ int ts_filter_local(const DevModel& dm, const double* obs, int j_lo, int j_hi, A
   if (ws.base == nullptr) return AUXMC_OK;
   if (!b.el || !b.carry2) return AUXMC_E_WORKSPACE;
   if (j_lo < 0 || j_hi > G.nsup || j_lo >= j_hi) return AUXMC_E_ARG;
-  const GrpCfg cfg = grp_cfg(d, dy);
+  const GrpCfg cfg = launch_cfg(d, dy);
   const int gp = cfg.groups;
   const size_t sm_el = sizeof(double) * elem_smem(d, dy) * gp;
   const size_t sm_sc = sizeof(double) * scan_smem(d) * gp;
@@ -780,7 +792,7 @@ int ts_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_hi, 
   if (ws.base == nullptr) return AUXMC_OK;
   if (!b.el || !b.carry2) return AUXMC_E_WORKSPACE;
   if (j_lo < 0 || j_hi > G.nsup || j_lo >= j_hi) return AUXMC_E_ARG;
-  const GrpCfg cfg = grp_cfg(d, dy);
+  const GrpCfg cfg = launch_cfg(d, dy);
   const int gp = cfg.groups;
   const size_t sm_sc = sizeof(double) * scan_smem(d) * gp;
   const size_t sm_rc = sizeof(double) * rec_smem(d, dy) * gp;
