@@ -285,6 +285,30 @@ size_t auxmc_aux_kernel_workspace(const auxmc_target* target, int C,
                                   const auxmc_kernel_options* opts);
 /* auxk::adapt_delta (auxk.cpp:213-218) for every chain. */
 int auxmc_adapt_delta(auxmc_chains* chains, double target_rate, void* stream);
+
+/* ---- time-sharded auxiliary Kalman step (one chain, kernel_step, auxk.cpp:130-198,
+ * with the prefix backend and the scan filter split over ranks; tshard.py drives it):
+ *   begin: iteration key, aux observations, surrogate LGSSM at x (described in
+ *          model_out; pseudo-observations at *z_out) — whole horizon, every rank;
+ *   the caller: sharded filter of (model, z), sharded prefix draw with the key at
+ *          *it_out, all-gather of the path into *prop_out;
+ *   middle: log q(x'|x), log gamma(x'), gradients at x', surrogate at x' (into *z_out);
+ *   the caller: sharded filter of the reverse surrogate;
+ *   end: log q(x|x'), aux likelihoods, the MH decision, accept.
+ * status_fwd = {filter, sampler} and status_rev = {filter} are maxima over ranks. */
+size_t auxmc_tshard_aux_workspace(const auxmc_target* target);
+int auxmc_tshard_aux_begin(const auxmc_target* target, auxmc_chains* chains,
+                           const auxmc_kernel_options* opts, void* workspace,
+                           size_t workspace_bytes, auxmc_lgssm* model_out, double** z_out,
+                           double** prop_out, uint64_t** it_out, void* stream);
+int auxmc_tshard_aux_middle(const auxmc_target* target, auxmc_chains* chains,
+                            const auxmc_kernel_options* opts, void* workspace,
+                            size_t workspace_bytes, const double* log_marginal_fwd,
+                            const int* status_fwd, void* stream);
+int auxmc_tshard_aux_end(const auxmc_target* target, auxmc_chains* chains,
+                         const auxmc_kernel_options* opts, void* workspace, size_t workspace_bytes,
+                         const double* log_marginal_rev, const int* status_rev, void* stream);
+int auxmc_copy_device(void* dst, const void* src, size_t bytes, void* stream);
 /* target.log_gamma (target.cpp:100-108) of B paths. */
 int auxmc_log_gamma(const auxmc_target* target, const double* traj, int B, double* out,
                     int* status, void* stream);

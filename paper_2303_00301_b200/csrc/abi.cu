@@ -336,6 +336,13 @@ int auxmc_tshard_prefix_finish(const auxmc_lgssm* model, const auxmc_noise* nois
                               traj, (cudaStream_t)stream);
 }
 
+int auxmc_copy_device(void* dst, const void* src, size_t bytes, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  if ((!dst || !src) && bytes) return AUXMC_E_ARG;
+  AUXMC_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  return AUXMC_OK;
+}
+
 long long auxmc_dnc_bridge_count(int T) {
   long long cap = 1;
   while (cap < T) cap <<= 1;  // internal heap ids are < 2^ceil(log2 T)

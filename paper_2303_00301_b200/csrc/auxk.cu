@@ -520,6 +520,61 @@ int launch_aux_obs(int C, int T, int d, const double* x, const double* delta, co
 
 using namespace auxmc_gpu;
 
+// ---------------------------------------------------------------- time-sharded aux step
+// One chain (C = 1) whose scans are split over ranks (tshard.py): the caller
+// runs `begin`, the sharded forward filter and prefix sampler on the auxiliary
+// LGSSM it describes, all-gathers the proposal path, `middle`, the sharded reverse
+// filter, then `end`.  Everything outside the scans is cheap per-t work that every
+// rank repeats on the whole horizon, so every split gives the same bits.
+namespace {
+struct TsAux {
+  uint64_t* it;
+  double *u, *prop, *gprop, *z, *Fa, *ba, *H, *cv, *R, *terms;
+  StepScalars sc;
+  int* ints;
+  DevModel dm;
+};
+TsAux ts_aux_take(const DevTarget& tg, Arena& ws) {
+  const int T = tg.T, d = tg.dx, p = d + tg.q;
+  const int nH = tg.exact_tv ? T + 1 : 1;
+  const size_t nx = (size_t)(T + 1) * d;
+  TsAux a;
+  a.it = ws.take<uint64_t>(1);
+  a.u = ws.take<double>(nx);
+  a.prop = ws.take<double>(nx);
+  a.gprop = ws.take<double>(nx);
+  a.z = ws.take<double>((size_t)(T + 1) * p);
+  a.Fa = tg.linear ? nullptr : ws.take<double>((size_t)(T > 0 ? T : 1) * d * d);
+  a.ba = tg.linear ? nullptr : ws.take<double>((size_t)(T > 0 ? T : 1) * d);
+  a.H = ws.take<double>((size_t)nH * p * d);
+  a.cv = ws.take<double>((size_t)nH * p);
+  a.R = ws.take<double>((size_t)nH * p * p);
+  a.terms = ws.take<double>((size_t)(T + 1));
+  double* scal = ws.take<double>(5);
+  a.ints = ws.take<int>(9);
+  if (scal) {
+    a.sc.logq_fwd = scal; a.sc.logq_rev = scal + 1; a.sc.lg_prop = scal + 2;
+    a.sc.aux_prop = scal + 3; a.sc.aux_x = scal + 4;
+  }
+  if (a.ints) {
+    a.sc.st_filt = a.ints; a.sc.st_samp = a.ints + 1; a.sc.st_lqf = a.ints + 2;
+    a.sc.st_lg = a.ints + 3; a.sc.bad = a.ints + 4; a.sc.st_filt_r = a.ints + 5;
+    a.sc.st_lqr = a.ints + 6; a.sc.accept = a.ints + 7;
+  }
+  DevModel& dm = a.dm;
+  dm.T = T; dm.dx = d; dm.dy = p;
+  dm.m0 = tg.m0; dm.P0 = tg.P0;
+  dm.F = tg.linear ? tg.F : a.Fa; dm.nF = tg.linear ? tg.nF : (T > 0 ? T : 1); dm.sF = 0;
+  dm.b = tg.linear ? tg.b : a.ba; dm.nb = dm.nF; dm.sb = 0;
+  dm.Q = tg.Q; dm.nQ = tg.linear ? tg.nF : 1; dm.sQ = 0;
+  dm.H = a.H; dm.nH = nH; dm.sH = 0;
+  dm.c = a.cv; dm.nc = nH; dm.sc = 0;
+  dm.R = a.R; dm.nR = nH; dm.sR = 0;
+  dm.mask = nullptr;
+  return a;
+}
+}  // namespace
+
 extern "C" {
 
 size_t auxmc_aux_kernel_workspace(const auxmc_target* target, int C,
@@ -592,6 +647,118 @@ int auxmc_log_gamma(const auxmc_target* target, const double* traj, int B, doubl
   st = launch_log_gamma(tg, B, traj, out, status, ws, (cudaStream_t)stream);
   cudaFreeAsync(buf, (cudaStream_t)stream);
   return st;
+}
+
+
+size_t auxmc_tshard_aux_workspace(const auxmc_target* target) {
+  if (check_target(target)) return 0;
+  const DevTarget tg = to_dev_target(*target);
+  Arena ws{nullptr, 0, 0};
+  ts_aux_take(tg, ws);
+  Arena sub = ws;
+  launch_log_gamma(tg, 1, nullptr, nullptr, nullptr, sub, nullptr);
+  Arena sub2 = ws;
+  launch_grads(tg, 1, nullptr, nullptr, nullptr, sub2, nullptr);
+  return std::max(sub.used, sub2.used) + 4096;
+}
+
+int auxmc_tshard_aux_begin(const auxmc_target* target, auxmc_chains* ch,
+                           const auxmc_kernel_options* opts, void* workspace,
+                           size_t workspace_bytes, auxmc_lgssm* model_out, double** z_out,
+                           double** prop_out, uint64_t** it_out, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  int st = check_target(target);
+  if (st) return st;
+  if (!ch || ch->C != 1 || !opts || !workspace || !model_out || !z_out || !prop_out || !it_out)
+    return AUXMC_E_ARG;
+  const DevTarget tg = to_dev_target(*target);
+  Arena ws{(char*)workspace, workspace_bytes, 0};
+  const TsAux a = ts_aux_take(tg, ws);
+  if (!a.ints || !a.R) return AUXMC_E_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int T = tg.T, d = tg.dx, p = d + tg.q, nH = a.dm.nH;
+  AUXMC_CUDA_TRY(cudaMemsetAsync(a.ints, 0, sizeof(int) * 9, s));
+  AUXMC_LAUNCH(k_iter_keys, 1, 32, 0, s, 1, ch->root_keys, ch->iter, a.it);
+  AUXMC_LAUNCH(k_aux_obs, grid_for((long long)(T + 1) * d), 256, 0, s, 1, T, d, ch->x, ch->delta,
+               a.it, a.u);
+  AUXMC_LAUNCH(k_build_HR, grid_for((long long)nH * p * p), 256, 0, s, tg, 1, nH, ch->delta, a.H,
+               a.cv, a.R);
+  AUXMC_LAUNCH(k_build_aux, grid_for((long long)(T + 1), 128), 128, 0, s, tg, 1, opts->zeroth_order,
+               ch->x, ch->grad_gen, a.u, ch->delta, a.z, a.Fa, a.ba);
+  auxmc_lgssm& m = *model_out;
+  m.T = T; m.dx = d; m.dy = p;
+  m.m0 = a.dm.m0; m.P0 = a.dm.P0;
+  m.F = a.dm.F; m.nF = a.dm.nF; m.b = a.dm.b; m.nb = a.dm.nb; m.Q = a.dm.Q; m.nQ = a.dm.nQ;
+  m.H = a.H; m.nH = nH; m.c = a.cv; m.nc = nH; m.R = a.R; m.nR = nH; m.mask = nullptr;
+  *z_out = a.z;
+  *prop_out = a.prop;
+  *it_out = a.it;
+  return AUXMC_OK;
+}
+
+int auxmc_tshard_aux_middle(const auxmc_target* target, auxmc_chains* ch,
+                            const auxmc_kernel_options* opts, void* workspace,
+                            size_t workspace_bytes, const double* log_marginal_fwd,
+                            const int* status_fwd, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  int st = check_target(target);
+  if (st) return st;
+  if (!ch || ch->C != 1 || !opts || !workspace || !log_marginal_fwd || !status_fwd)
+    return AUXMC_E_ARG;
+  const DevTarget tg = to_dev_target(*target);
+  Arena ws{(char*)workspace, workspace_bytes, 0};
+  const TsAux a = ts_aux_take(tg, ws);
+  if (!a.ints) return AUXMC_E_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int T = tg.T, p = tg.dx + tg.q;
+  // filter / sampler status of every shard (max over ranks, gathered by the caller)
+  AUXMC_CUDA_TRY(cudaMemcpyAsync(a.sc.st_filt, status_fwd, 2 * sizeof(int),
+                                 cudaMemcpyDeviceToDevice, s));
+  int rc = launch_path_logpdf(a.dm, a.z, (long long)(T + 1) * p, a.prop, log_marginal_fwd, 0, 1,
+                              a.sc.logq_fwd, a.sc.st_lqf, s);
+  if (rc) return rc;
+  {
+    Arena sub = ws;
+    rc = launch_log_gamma(tg, 1, a.prop, a.sc.lg_prop, a.sc.st_lg, sub, s);
+    if (rc) return rc;
+    Arena sub2 = ws;
+    rc = launch_grads(tg, 1, a.prop, a.gprop, a.sc.bad, sub2, s);
+    if (rc) return rc;
+  }
+  AUXMC_LAUNCH(k_build_aux, grid_for((long long)(T + 1), 128), 128, 0, s, tg, 1, opts->zeroth_order,
+               a.prop, a.gprop, a.u, ch->delta, a.z, a.Fa, a.ba);
+  return AUXMC_OK;
+}
+
+int auxmc_tshard_aux_end(const auxmc_target* target, auxmc_chains* ch,
+                         const auxmc_kernel_options* opts, void* workspace, size_t workspace_bytes,
+                         const double* log_marginal_rev, const int* status_rev, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  int st = check_target(target);
+  if (st) return st;
+  if (!ch || ch->C != 1 || !opts || !workspace || !log_marginal_rev || !status_rev)
+    return AUXMC_E_ARG;
+  const DevTarget tg = to_dev_target(*target);
+  Arena ws{(char*)workspace, workspace_bytes, 0};
+  const TsAux a = ts_aux_take(tg, ws);
+  if (!a.ints) return AUXMC_E_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int T = tg.T, d = tg.dx, p = d + tg.q;
+  AUXMC_CUDA_TRY(cudaMemcpyAsync(a.sc.st_filt_r, status_rev, sizeof(int),
+                                 cudaMemcpyDeviceToDevice, s));
+  int rc = launch_path_logpdf(a.dm, a.z, (long long)(T + 1) * p, ch->x, log_marginal_rev, 0, 1,
+                              a.sc.logq_rev, a.sc.st_lqr, s);
+  if (rc) return rc;
+  AUXMC_LAUNCH(k_aux_lik_terms, grid_for((long long)(T + 1)), 256, 0, s, 1, T, d, a.u, a.prop,
+               ch->delta, a.terms);
+  AUXMC_LAUNCH(k_row_sum, 1, kSumThreads, 0, s, 1, T + 1, a.terms, a.sc.aux_prop);
+  AUXMC_LAUNCH(k_aux_lik_terms, grid_for((long long)(T + 1)), 256, 0, s, 1, T, d, a.u, ch->x,
+               ch->delta, a.terms);
+  AUXMC_LAUNCH(k_row_sum, 1, kSumThreads, 0, s, 1, T + 1, a.terms, a.sc.aux_x);
+  AUXMC_LAUNCH(k_mh, 1, 32, 0, s, 1, a.sc, a.it, ch->log_gamma, ch->iter, ch->stats);
+  AUXMC_LAUNCH(k_accept_copy, grid_for((long long)(T + 1) * d), 256, 0, s, 1,
+               (long long)(T + 1) * d, a.sc.accept, a.prop, a.gprop, ch->x, ch->grad_gen);
+  return AUXMC_OK;
 }
 
 }  // extern "C"

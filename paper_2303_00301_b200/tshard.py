@@ -45,7 +45,7 @@ class TShardGeom:
         """Super-block range [lo, hi) and time range [t_lo, t_hi) of a rank."""
         sh = strong_shard(rank, world, self.nsup)
         lo, hi = sh.first, sh.first + sh.count
-        return lo, hi, lo * self.SB, min(hi * self.SB, self.T + 1)
+        return lo, hi, min(lo * self.SB, self.T + 1), min(hi * self.SB, self.T + 1)
 
 
 def torch_exchange(group=None):
@@ -75,14 +75,19 @@ class ShardedScanFilter:
         self.max_owned = -(-self.geom.nsup // world)  # ceil: rows each rank contributes
 
     def local(self, obs) -> torch.Tensor:
-        """Phase 1: this rank's super-block aggregates, padded to max_owned rows."""
+        """Phase 1: this rank's super-block aggregates, padded to max_owned rows.
+        `obs` is a [T+1, dy] array or a device pointer (int) to one."""
         g, dev = self.geom, self.model.device
-        self.obs = _dev(obs, dev).contiguous()
+        if isinstance(obs, int):
+            self.obs, self._obs_ptr = None, obs
+        else:
+            self.obs = _dev(obs, dev).contiguous()
+            self._obs_ptr = self.obs.data_ptr()
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         out = torch.zeros((self.max_owned, g.elem_doubles), dtype=torch.float64, device=dev)
         if self.sup_hi > self.sup_lo:
             _lib.check(_lib.load().auxmc_tshard_filter_local(
-                C.byref(self._mr), self.obs.data_ptr(), self.sup_lo, self.sup_hi,
+                C.byref(self._mr), self._obs_ptr, self.sup_lo, self.sup_hi,
                 self.ws.data_ptr(), self.ws_bytes, out.data_ptr(), self.status.data_ptr(),
                 _stream()), "tshard_filter_local")
         return out
@@ -106,7 +111,7 @@ class ShardedScanFilter:
         if self.sup_hi > self.sup_lo:
             raw = fr.raw()
             _lib.check(_lib.load().auxmc_tshard_filter_finish(
-                C.byref(self._mr), self.obs.data_ptr(), self.sup_lo, self.sup_hi,
+                C.byref(self._mr), self._obs_ptr, self.sup_lo, self.sup_hi,
                 self.ws.data_ptr(), self.ws_bytes, sup_all.data_ptr(), C.byref(raw),
                 ll.data_ptr(), self.status.data_ptr(), _stream()), "tshard_filter_finish")
         return fr, ll
@@ -178,14 +183,17 @@ class ShardedPrefixSampler:
             parts.append(p[:k_hi - k_lo])
         blk_all = torch.cat(parts, 0).contiguous()
         assert blk_all.shape[0] == self.P, (blk_all.shape, self.P)
-        owner = max(r for r in range(self.sf.world) if self.sf.geom.owned(r, self.sf.world)[3] ==
-                    self.model.T + 1)
+        owner = next(r for r in range(self.sf.world)
+                     if self.sf.geom.owned(r, self.sf.world)[2] < self.model.T + 1 ==
+                     self.sf.geom.owned(r, self.sf.world)[3])
         xT = gathered_xT[owner].contiguous()
         if self.sf.t_hi > self.sf.t_lo:
             _lib.check(_lib.load().auxmc_tshard_prefix_finish(
                 C.byref(self.sf._mr), C.byref(self.noise_raw), self.sf.t_lo, self.sf.t_hi,
                 self.ws.data_ptr(), self.ws_bytes, blk_all.data_ptr(), xT.data_ptr(),
                 traj.data_ptr(), _stream()), "tshard_prefix_finish")
+        else:  # a rank that owns no super-block still gets row T
+            traj[self.model.T].copy_(xT)
         return traj
 
 
@@ -227,3 +235,152 @@ class LocalExchange:
         for p, tr in zip(samplers, trajs):
             p.finish(rows, xts, tr)
         return shards, frs, lm, trajs
+
+
+class RawModel:
+    """An auxmc_lgssm struct produced by the library (device pointers), with the
+    attributes the sharded scans read."""
+
+    def __init__(self, raw, device):
+        self._raw, self.device = raw, device
+        self.T, self.dx, self.dy = raw.T, raw.dx, raw.dy
+
+    def raw(self):
+        return self._raw
+
+
+class _KeyNoise:
+    """Stream noise keyed by one device key (the iteration key of the aux step)."""
+
+    def __init__(self, key_ptr: int):
+        self.key_ptr = key_ptr
+
+    def raw(self):
+        n = _lib.Noise()
+        n.kind = _lib.NOISE_STREAM
+        n.keys = self.key_ptr
+        return n
+
+
+class ShardedAuxChain:
+    """One chain's auxiliary Kalman step (auxk::kernel_step, prefix backend, scan
+    filter) with the horizon split over ranks: the forward filter, the path draw
+    and the reverse filter are time-sharded (tshard filter / prefix), the proposal
+    path is all-gathered, and the per-step work around them (aux observations,
+    surrogate models, path log-densities, log gamma, gradients, MH) is repeated by
+    every rank on the whole horizon — so every split gives the same bits."""
+
+    def __init__(self, chains, rank: int, world: int, exchange, zeroth_order=False):
+        if chains.C != 1:
+            raise ValueError("ShardedAuxChain: one chain")
+        self.ch, self.rank, self.world, self.exchange = chains, rank, world, exchange
+        self.tg = chains.target
+        self.opts = _lib.KernelOptions(1, 1, int(zeroth_order))  # prefix, scan filter
+        lib = _lib.load()
+        self._tr = self.tg.raw()
+        self.ws_bytes = lib.auxmc_tshard_aux_workspace(C.byref(self._tr))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.tg.device)
+
+    def _max_status(self, st: torch.Tensor) -> torch.Tensor:
+        parts = self.exchange(st)
+        return torch.stack(parts).amax(0).to(torch.int32).contiguous()
+
+    def step(self):
+        lib, dev = _lib.load(), self.tg.device
+        T, d = self.tg.T, self.tg.dx
+        ch = self.ch.raw()
+        model = _lib.Lgssm()
+        z, prop, it = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _lib.check(lib.auxmc_tshard_aux_begin(
+            C.byref(self._tr), C.byref(ch), C.byref(self.opts), self.ws.data_ptr(),
+            self.ws_bytes, C.byref(model), C.byref(z), C.byref(prop), C.byref(it), _stream()),
+            "tshard_aux_begin")
+        rm = RawModel(model, dev)
+        # forward filter and the path draw, time-sharded
+        sf = ShardedScanFilter(rm, self.rank, self.world)
+        fr, ll = sf.finish(self.exchange(sf.local(z.value)))
+        lm_fwd = sf.log_marginal(self.exchange(ll))
+        fr.log_marginal.copy_(lm_fwd)
+        ps = ShardedPrefixSampler(sf)
+        traj = torch.zeros((T + 1, d), dtype=torch.float64, device=dev)
+        rows, xT = ps.local(fr, _KeyNoise(it.value), traj)
+        ps.finish(self.exchange(rows), self.exchange(xT), traj)
+        # the whole proposal path on every rank
+        mine = traj[sf.t_lo:min(sf.t_hi, T)].contiguous()
+        pad = torch.zeros((ps.max_blocks * ps.Lb, d), dtype=torch.float64, device=dev)
+        pad[:mine.shape[0]] = mine
+        parts = self.exchange(pad)
+        full = torch.empty((T + 1, d), dtype=torch.float64, device=dev)
+        for r, part in enumerate(parts):
+            _, _, a, b = sf.geom.owned(r, self.world)
+            b = min(b, T)
+            if b > a:
+                full[a:b] = part[:b - a]
+        full[T] = traj[T]
+        _lib.check(lib.auxmc_copy_device(prop.value, full.data_ptr(), full.numel() * 8,
+                                         _stream()), "copy")
+        st_fwd = self._max_status(torch.stack([sf.status[0], ps.status[0]]).to(torch.int32))
+        _lib.check(lib.auxmc_tshard_aux_middle(
+            C.byref(self._tr), C.byref(ch), C.byref(self.opts), self.ws.data_ptr(),
+            self.ws_bytes, lm_fwd.data_ptr(), st_fwd.data_ptr(), _stream()), "tshard_aux_middle")
+        # reverse filter on the surrogate at x'
+        sr = ShardedScanFilter(rm, self.rank, self.world)
+        _, llr = sr.finish(self.exchange(sr.local(z.value)))
+        lm_rev = sr.log_marginal(self.exchange(llr))
+        st_rev = self._max_status(sr.status.to(torch.int32))
+        _lib.check(lib.auxmc_tshard_aux_end(
+            C.byref(self._tr), C.byref(ch), C.byref(self.opts), self.ws.data_ptr(),
+            self.ws_bytes, lm_rev.data_ptr(), st_rev.data_ptr(), _stream()), "tshard_aux_end")
+
+
+class LocalShardedAux:
+    """Runs `world` ShardedAuxChain ranks in one process (tests): each rank owns
+    its own chain state copy; every exchange is served once all ranks posted."""
+
+    @staticmethod
+    def run(make_chains, world: int, steps: int):
+        return LocalShardedAux.run_on([make_chains() for _ in range(world)], steps)
+
+    @staticmethod
+    def run_on(chains, steps: int):
+        """Continue `len(chains)` rank states for `steps` more sharded steps."""
+        import threading
+        world = len(chains)
+        barrier = threading.Barrier(world)
+        box = {}
+        lock = threading.Lock()
+        errors = []
+
+        def make_ex(rank):
+            seq = [0]
+
+            def ex(t):
+                k = seq[0]
+                seq[0] += 1
+                torch.cuda.synchronize()
+                with lock:
+                    box.setdefault(k, [None] * world)[rank] = t.clone()
+                barrier.wait()
+                out = [x.to(t.device) for x in box[k]]
+                barrier.wait()
+                return out
+            return ex
+
+        def worker(r):
+            try:
+                sa = ShardedAuxChain(chains[r], r, world, make_ex(r))
+                for _ in range(steps):
+                    sa.step()
+                torch.cuda.synchronize()
+            except Exception as e:  # noqa: BLE001
+                errors.append(e)
+                barrier.abort()
+
+        th = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if errors:
+            raise errors[0]
+        return chains

@@ -59,8 +59,24 @@ def main(out_path):
         ok = ok and torch.equal(lm.cpu(), lm1.cpu())
         want_o = O.kalman_filter(m, obs)
         err = abs(float(lm1.item()) - want_o.log_marginal) / max(1.0, abs(want_o.log_marginal))
-        json.dump({"bit_identical": bool(ok), "world": world, "lm_rel_err": err},
-                  open(out_path, "w"))
+        res = {"bit_identical": bool(ok), "world": world, "lm_rel_err": err}
+    # the full auxiliary Kalman step, time-sharded over the ranks
+    from paper_2303_00301_b200 import auxk, bench_models as bm
+    spec = bm.ModelSpec(kind="spatio-temporal", T=300, grid=3, data_seed=7)
+    lat, data = bm.simulate(spec)
+    tg = auxk.make_target(spec, data)
+    ch = auxk.init_chains(tg, lat, 0.5, 9, 1)
+    sa = tshard.ShardedAuxChain(ch, rank, world, tshard.torch_exchange())
+    for _ in range(3):
+        sa.step()
+    torch.cuda.synchronize()
+    if rank == 0:
+        one = tshard.LocalShardedAux.run(lambda: auxk.init_chains(tg, lat, 0.5, 9, 1), 1, 3)[0]
+        res["aux_bit_identical"] = bool(torch.equal(one.x, ch.x) and
+                                        torch.equal(one.log_gamma, ch.log_gamma) and
+                                        torch.equal(one.accepted, ch.accepted))
+        res["aux_accepted"] = int(ch.accepted.cpu()[0])
+        json.dump(res, open(out_path, "w"))
     dist.barrier()
     dist.destroy_process_group()
 

@@ -70,6 +70,7 @@ def test_tshard_world2_gloo_processes(tmp_path):
     res = json.load(open(out))
     assert res["world"] == 2 and res["bit_identical"], res
     assert res["lm_rel_err"] < 1e-9, res
+    assert res["aux_bit_identical"], res
 
 
 @pytest.mark.parametrize("T,dx,dy,seed", [(3000, 3, 2, 81), (1200, 10, 4, 82)])
