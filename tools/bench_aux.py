@@ -7,7 +7,8 @@ c3: Lorenz-96 d = 40 diffusion smoothing, auxiliary Kalman sampler, T = 4096,
 c4: stochastic volatility d = 3, auxiliary particle Gibbs, N = 256, T = 2^14
     (configs[3]), parallel-in-time cSMC (--sampler dnc selects the reference cSMC).
 c5: spatio-temporal grid 4 (d = 16), T = 2^20, 1 chain, aux-Kalman with the scan
-    filter and prefix sampler (configs[4]; single GPU, no time sharding yet).
+    filter and prefix sampler (configs[4]; one GPU per chain).
+c5ts: the same iteration time-sharded over the ranks (strong scaling).
 Units: chain-timesteps/s = chains * (T+1) * iterations / device seconds.
 """
 from __future__ import annotations
@@ -16,6 +17,7 @@ import ctypes
 import json
 
 METRIC = "chain-timesteps/sec (device-timed) at 1/2/4/8 B200; MCMC iters/sec; % HBM/FP64 roofline"
+C5_DELTA = 5e-4
 FP64_PEAK_TFLOPS = 37.1  # measured: DMMA m8n8k4 throughput, tools/micro/lat.cu (profiles/r1_micro_latency_fp64.txt)
 
 
@@ -44,7 +46,9 @@ def run(args, rank, world, local):
         T, C, d = args.T or (1 << 20), args.chains or 1, 16
         spec = bm.ModelSpec(kind="spatio-temporal", T=T, grid=4, data_seed=7)
         backend = auxk.Backend.kDnc if args.sampler == "dnc" else auxk.Backend.kPrefix
-        delta = 0.5
+        # log α scales with d·T: δ = 5e-4 accepts about 2/3 of moves at T = 2^20
+        # (δ = 0.002 → |log α| ≈ 13, δ = 0.5 → 1.8e5); the cost does not depend on δ
+        delta = C5_DELTA
         flops_ct = 464e3  # F_pit at d = 16
     else:
         T, C, d = args.T or 16384, args.chains or 148, 3
@@ -133,29 +137,29 @@ def run(args, rank, world, local):
 
 
 def run_c5ts(args, rank, world, local, device):
-    """C5 time-sharded: the scan filter and the prefix sampler of ONE path of a
-    d = 16 linear-Gaussian model (the shape of C5's auxiliary LGSSM: dx = dy = 16)
-    with the horizon split over the ranks (tshard.py); strong scaling (T fixed).
-    A step = sharded filter + sharded path draw, including the all-gathers."""
-    import numpy as np
+    """C5 time-sharded: the full auxiliary Kalman iteration of ONE chain on the C5
+    target (spatio-temporal grid 4, d = 16, T = 2^20) with the horizon split over
+    the ranks (tshard.ShardedAuxChain): forward filter, path draw and reverse filter
+    time-sharded, per-t model work repeated; strong scaling (T fixed).  A step =
+    one MCMC iteration including the all-gathers."""
     import torch
     from bench import Clocks, timed
-    from paper_2303_00301_b200 import _lib, bench_models as bm, lgssm, rng, tshard
+    from paper_2303_00301_b200 import _lib, auxk, bench_models as bm, tshard
     T = args.T or (1 << 20)
-    spec = bm.ModelSpec(kind="lgssm-synthetic", T=T, dx=16, dy=16, data_seed=7)
+    spec = bm.ModelSpec(kind="spatio-temporal", T=T, grid=4, data_seed=7)
     lat, data = bm.simulate(spec)
-    model = bm.synthetic_lgssm(spec, device=device)
-    obs = torch.as_tensor(np.asarray(data), dtype=torch.float64, device=device)
-    noise = lgssm.Noise.stream(rng.chain_keys(1, 1, device=device))
+    tg = auxk.make_target(spec, data, device=device)
+    ch = auxk.init_chains(tg, torch.as_tensor(lat, device=device), C5_DELTA, 1, 1)
     if world > 1:
         exchange = tshard.torch_exchange()
     else:
         def exchange(t):
             return [t]
     lib = _lib.load()
+    sa = tshard.ShardedAuxChain(ch, rank, world, exchange)
 
     def step():
-        tshard.sharded_filter_and_prefix(model, obs, noise, rank, world, exchange)
+        sa.step()
 
     for _ in range(max(args.warmup, 1)):
         step()
@@ -165,17 +169,20 @@ def run_c5ts(args, rank, world, local, device):
         ms = timed(step, args.steps, world)
     launches = lib.auxmc_launch_count() - n0
     value = (T + 1) * args.steps / (ms / 1e3)
-    F_pit = 113.333 * 16 ** 3 + 8 * 16 * 256 + 8 * 256 * 16 + 2 / 3 * 16 ** 3
+    F_pit = 464e3  # per chain-timestep at d = 16, as the c5 line
     tflops = F_pit * value / 1e12
     if rank == 0:
         g = tshard.TShardGeom.of(T, 16)
         line = {
-            "metric": METRIC, "value": value, "unit": "path-timesteps/s", "n_gpus": world,
+            "metric": METRIC, "value": value, "unit": "chain-timesteps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": "C5 time-sharded scan filter + prefix sampler, one path, "
-                                   "d = 16 LGSSM (C5's auxiliary-model shape)", "T": T,
+            "config": {"workload": "C5 spatio-temporal grid 4 (d=16) aux-Kalman iteration, "
+                                   "1 chain, time-sharded (forward/reverse scan filter + "
+                                   "prefix sampler split over ranks)", "T": T,
+                       "accept_rate": float(ch.accepted.sum()) / max(1, float(
+                           (ch.accepted + ch.rejected).sum())),
                        "super_blocks": g.nsup, "super_block_steps": g.SB,
                        "parallelism": f"time sharded over {world} GPU(s), all-gather per phase"},
             "roofline": {"bound": "fp64", "achieved": tflops, "peak": FP64_PEAK_TFLOPS,
