@@ -6,10 +6,13 @@ sm_100 device is usable, compute entry points raise.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import pathlib
 
 PKG = pathlib.Path(__file__).resolve().parent
-LIB_PATH = PKG / "libauxmc_b200.so"
+# AUXMC_LIB_PATH: an alternative in-tree build (tools/exp_build.sh kernel experiments)
+LIB_PATH = pathlib.Path(os.environ["AUXMC_LIB_PATH"]) if os.environ.get("AUXMC_LIB_PATH") \
+    else PKG / "libauxmc_b200.so"
 
 OK, E_DIM, E_FACTOR, E_DEGENERATE, E_CONTRACT, E_CONFIG, E_CUDA, E_ARG, E_WORKSPACE = range(9)
 NOISE_STREAM, NOISE_PREDRAWN = 0, 1

@@ -96,8 +96,13 @@ __device__ void g_lu_solve(const Grp& g, int d, const double* LU, const int* per
 // pivot rule is PartialPivLU's (first row of largest |.| at or below the
 // diagonal); rows are swapped and eliminated inside every lane's column, the
 // pivot column is broadcast by shuffles — no shared-memory round trips.
-__device__ void w_inverse_gj(int lane, int d, const double* M, double* Minv) {
-  constexpr int MX = 16;
+// DN > 0: the dimension is the compile-time DN (every bound static); DN = 0: d <= 16
+// at run time.  Same operations in the same order either way.
+template <int DN>
+__device__ __forceinline__ void w_inverse_gj_t(int lane, int d_rt, const double* M,
+                                               double* Minv) {
+  constexpr int MX = DN ? DN : 16;
+  const int d = DN ? DN : d_rt;
   double col[MX];
   const int j = lane;
 #pragma unroll
@@ -141,9 +146,11 @@ __device__ void w_inverse_gj(int lane, int d, const double* M, double* Minv) {
   __syncwarp();
 }
 
-// o = combine(u, v) (pit.cpp:36-51); scratch: 5 dd + 2 d doubles, 2 d + 1 ints
+// o = combine(u, v) (pit.cpp:36-51); scratch: 3 dd + 2 d doubles, 2 d + 1 ints.  The
+// LU / inverse work matrices M1, Minv live in o's C and J blocks, which are only
+// written at the very end (o never aliases u or v).
 struct CombScratch {
-  double *M1, *M2, *S, *T1, *T2, *t, *w;
+  double *S, *T1, *T2, *t, *w;
   int *p1, *p2, *idx;
 };
 
@@ -152,25 +159,28 @@ struct CombScratch {
 // products, same summation order), so one LU gives both solves: Minv = M1^{-1}
 // (LU with partial pivoting, solved against I) and M2^{-1} = Minv^T; the
 // remaining algebra is dense products.
-__device__ void g_combine(const Grp& g, int d, const double* u, const double* v, double* o,
-                          const CombScratch& s) {
+template <int DC>
+__device__ __forceinline__ void g_combine_t(const Grp& g, int d_rt, const double* u,
+                                            const double* v, double* o, const CombScratch& s) {
+  const int d = DC ? DC : d_rt;
   const int dd = d * d;
   const double *uA = u, *ub = u + dd, *uC = u + dd + d, *ueta = u + 2 * dd + d,
                *uJ = u + 2 * dd + 2 * d;
   const double *vA = v, *vb = v + dd, *vC = v + dd + d, *veta = v + 2 * dd + d,
                *vJ = v + 2 * dd + 2 * d;
   double *oA = o, *ob = o + dd, *oC = o + dd + d, *oeta = o + 2 * dd + d, *oJ = o + 2 * dd + 2 * d;
-  double* Minv = s.M2;
-  g_mm(g, d, d, d, uC, vJ, s.M1);
+  double* const M1 = oC;
+  double* Minv = oJ;
+  g_mm(g, d, d, d, uC, vJ, M1);
   g_eye(g, d, s.T2);
   g.sync();
-  for (int i = g.lane; i < d; i += g.size) s.M1[i * d + i] += 1.0;
+  for (int i = g.lane; i < d; i += g.size) M1[i * d + i] += 1.0;
   g.sync();
   if (!g.block && d <= 16) {
-    w_inverse_gj(g.lane, d, s.M1, Minv);  // M1^{-1}, registers and shuffles
+    w_inverse_gj_t<DC>(g.lane, d, M1, Minv);  // M1^{-1}, registers and shuffles
   } else {
-    g_lu_factor(g, d, s.M1, s.p1, s.idx);
-    g_lu_solve(g, d, s.M1, s.p1, d, s.T2, Minv);  // M1^{-1}
+    g_lu_factor(g, d, M1, s.p1, s.idx);
+    g_lu_solve(g, d, M1, s.p1, d, s.T2, Minv);  // M1^{-1}
   }
   // t = uC veta + ub ; t2 = veta - vJ ub
   for (int i = g.lane; i < d; i += g.size) {
@@ -188,8 +198,8 @@ __device__ void g_combine(const Grp& g, int d, const double* u, const double* v,
   g_mm(g, d, d, d, Minv, uC, s.T1);
   g_mm_tn(g, d, d, d, Minv, vJ, s.T2);
   // b = vA (Minv t) + vb ; eta = uA^T (Minv^T t2) + ueta  (vectors kept in M1's rows)
-  double* mt = s.M1;
-  double* mt2 = s.M1 + d;
+  double* mt = M1;
+  double* mt2 = M1 + d;
   for (int i = g.lane; i < d; i += g.size) {
     double acc = 0.0, acc2 = 0.0;
     for (int k = 0; k < d; ++k) {
@@ -226,15 +236,21 @@ __device__ void g_combine(const Grp& g, int d, const double* u, const double* v,
   g.sync();
 }
 
-__host__ __device__ inline int comb_doubles(int d) { return 5 * d * d + 2 * d; }
+// d = 16 (the C5 state dimension) gets a fully static instance: the Gauss-Jordan
+// inverse dominated the generic combine's instruction count (runtime bounds).
+__device__ __noinline__ void g_combine(const Grp& g, int d, const double* u, const double* v,
+                                       double* o, const CombScratch& s) {
+  if (d == 16) g_combine_t<16>(g, d, u, v, o, s);
+  else g_combine_t<0>(g, d, u, v, o, s);
+}
+
+__host__ __device__ inline int comb_doubles(int d) { return 3 * d * d + 2 * d; }
 __host__ __device__ inline int comb_ints(int d) { return 2 * d + 2; }
 
 __device__ CombScratch comb_scratch(int d, double* base, int* ibase) {
   CombScratch s;
   const int dd = d * d;
-  s.M1 = base;
-  s.M2 = s.M1 + dd;
-  s.S = s.M2 + dd;
+  s.S = base;
   s.T1 = s.S + dd;
   s.T2 = s.T1 + dd;
   s.t = s.T2 + dd;
@@ -256,6 +272,9 @@ __host__ __device__ inline GrpCfg grp_cfg(int dx, int dy) {
   return GrpCfg{true, 1, 128};
 }
 
+// gain^T and hs factors of the time-invariant step (k_pfg_elem_fill)
+__host__ __device__ inline int proto_doubles(int d, int dy) { return 2 * dy * d; }
+
 // ---------------------------------------------------------------- element build
 // per (b, t); smem per group: f, q, a, t1, t2 (dd), hq, X1, X2, gr (dy*dx), s, L, scr (dy^2),
 // innov, hv, bd (vectors)
@@ -266,7 +285,7 @@ __host__ __device__ inline int elem_smem(int d, int dy) {
 
 template <bool BLOCK>
 __global__ void k_pfg_elements(DevModel m, const double* __restrict__ obs, int B, double* el,
-                               int* status, int t_lo, int t_hi) {
+                               int* status, int t_lo, int t_hi, double* proto = nullptr) {
   extern __shared__ double smem[];
   const int T = m.T, d = m.dx, dy = m.dy, dd = d * d, ES = fe_size_g(d);
   const int W = d > dy ? d : dy;
@@ -362,6 +381,10 @@ __global__ void k_pfg_elements(DevModel m, const double* __restrict__ obs, int B
         g.sync();
         for (int i = g.ty(); i < d; i += g.ny())
           for (int j = g.tx(); j < d; j += 16) eJ[i * d + j] = 0.5 * (t2[i * d + j] + t2[j * d + i]);
+        if (proto && t == 1) {  // gain^T and hs of the time-invariant step (k_pfg_elem_fill)
+          g_copy(g, dy * d, X1, proto + (size_t)b * proto_doubles(d, dy));
+          g_copy(g, dy * d, X2, proto + (size_t)b * proto_doubles(d, dy) + dy * d);
+        }
       }
     } else {
       for (int i = g.lane; i < dd; i += g.size) {
@@ -382,8 +405,103 @@ __global__ void k_pfg_elements(DevModel m, const double* __restrict__ obs, int B
   }
 }
 
+// ---------------------------------------------------------------- time-invariant elements
+// When F, b, Q, H, c, R are shared by every step (strides 0, no mask; e.g. the
+// auxiliary LGSSM of a linear-dynamics target), the elements of t >= 1 differ
+// only in (b, eta): A, C, J and the gain / hs factors are those of t = 1.  One
+// group builds t = 1 in full (k_pfg_elements, proto != nullptr keeps X1, X2);
+// k_pfg_elem_fill then forms every other step's vectors with the same loops in
+// the same order as the full build and copies the matrices — identical bits.
+inline bool pfg_time_invariant(const DevModel& m) {
+  return m.T >= 2 && m.dy > 0 && m.mask == nullptr && m.dx <= 16 && m.dy <= 16 && m.nF <= 1 &&
+         m.nb <= 1 && m.nQ <= 1 && m.nH <= 1 && m.nc <= 1 && m.nR <= 1;
+}
+
+constexpr int kFillWarps = 8;
+// warp w of a CTA: 32 consecutive steps of sequence b, lane = step
+__global__ void __launch_bounds__(kFillWarps * 32)
+    k_pfg_elem_fill(DevModel m, const double* __restrict__ obs, int B, double* el,
+                    const double* __restrict__ proto, int t_lo, int t_hi) {
+  __shared__ double s_mat[3 * 256], s_x1[256], s_x2[256], s_h[256], s_f[256], s_c[16], s_bd[16];
+  const int T = m.T, d = m.dx, dy = m.dy, dd = d * d, ES = fe_size_g(d);
+  const int span = t_hi - t_lo;
+  const int per_b = (span + 32 * kFillWarps - 1) / (32 * kFillWarps);
+  const int b = blockIdx.x / per_b, chunk = blockIdx.x % per_b;
+  if (b >= B) return;
+  const double* e1 = el + ((size_t)b * (T + 1) + 1) * ES;
+  const double* pr = proto + (size_t)b * proto_doubles(d, dy);
+  for (int i = threadIdx.x; i < dd; i += blockDim.x) {
+    s_mat[i] = e1[i];                    // A
+    s_mat[dd + i] = e1[dd + d + i];      // C
+    s_mat[2 * dd + i] = e1[2 * dd + 2 * d + i];  // J
+    s_f[i] = m.Ft(0, b)[i];
+  }
+  for (int i = threadIdx.x; i < dy * d; i += blockDim.x) {
+    s_x1[i] = pr[i];
+    s_x2[i] = pr[dy * d + i];
+    s_h[i] = m.Ht(0, b)[i];
+  }
+  for (int i = threadIdx.x; i < dy; i += blockDim.x) s_c[i] = m.ct(0, b)[i];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) s_bd[i] = m.bt(0, b)[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = t_lo + (chunk * kFillWarps + warp) * 32;
+  if (t0 >= t_hi) return;
+  const int t = t0 + lane;
+  if (t < t_hi) {
+    double* e = el + ((size_t)b * (T + 1) + t) * ES;
+    const double* y = obs + ((size_t)b * (T + 1) + t) * dy;
+    double innov[16], hv[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < dy) {
+        double acc = 0.0;
+        for (int j = 0; j < d; ++j) acc += s_h[i * d + j] * s_bd[j];
+        innov[i] = (y[i] - acc) - s_c[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < d) {
+        double acc = 0.0, acc2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k < dy) {
+            acc += s_x1[k * d + i] * innov[k];
+            acc2 += s_x2[k * d + i] * innov[k];
+          }
+        e[dd + i] = s_bd[i] + acc;  // b
+        hv[i] = acc2;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < d) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k < d) acc += s_f[k * d + i] * hv[k];
+        e[2 * dd + d + i] = acc;  // eta
+      }
+    }
+  }
+  // A, C, J of the warp's 32 steps, coalesced
+  const int nt = min(32, t_hi - t0);
+  for (int u = 0; u < nt; ++u) {
+    double* e = el + ((size_t)b * (T + 1) + t0 + u) * ES;
+    for (int i = lane; i < dd; i += 32) {
+      e[i] = s_mat[i];
+      e[dd + d + i] = s_mat[dd + i];
+      e[2 * dd + 2 * d + i] = s_mat[2 * dd + i];
+    }
+  }
+}
+
 // ---------------------------------------------------------------- S1 / S2 / S3
-__host__ __device__ inline int scan_smem(int d) { return 3 * fe_size_g(d) + comb_doubles(d) + comb_ints(d); }
+// per group: nes element buffers (2 for S1/S2, 3 for S3) + combine scratch
+__host__ __device__ inline int scan_smem(int d, int nes) {
+  return nes * fe_size_g(d) + comb_doubles(d) + comb_ints(d);
+}
 
 template <bool BLOCK>
 __global__ void k_pfg_reduce(int T, int d, int B, int LB, const double* __restrict__ el, double* agg,
@@ -392,9 +510,9 @@ __global__ void k_pfg_reduce(int T, int d, int B, int LB, const double* __restri
   const int ES = fe_size_g(d);
   const Grp g = BLOCK ? block_group() : warp_group();
   const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
-  double* sm = smem + (size_t)gid * scan_smem(d);
-  double *acc = sm, *o = acc + ES, *tmpd = o + ES;
-  const CombScratch cs = comb_scratch(d, tmpd + ES, reinterpret_cast<int*>(tmpd + ES + comb_doubles(d)));
+  double* sm = smem + (size_t)gid * scan_smem(d, 2);
+  double *acc = sm, *o = acc + ES;
+  const CombScratch cs = comb_scratch(d, o + ES, reinterpret_cast<int*>(o + ES + comb_doubles(d)));
   const int nblk = (T + 1 + LB - 1) / LB;
   const int span = k_hi - k_lo;  // block range [k_lo, k_hi) of this launch
   const long long n = (long long)B * span;
@@ -421,9 +539,9 @@ __global__ void k_pfg_carry(int T, int d, int B, int LB, const double* __restric
   const int ES = fe_size_g(d);
   const Grp g = BLOCK ? block_group() : warp_group();
   const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
-  double* sm = smem + (size_t)gid * scan_smem(d);
-  double *acc = sm, *o = acc + ES, *tmpd = o + ES;
-  const CombScratch cs = comb_scratch(d, tmpd + ES, reinterpret_cast<int*>(tmpd + ES + comb_doubles(d)));
+  double* sm = smem + (size_t)gid * scan_smem(d, 2);
+  double *acc = sm, *o = acc + ES;
+  const CombScratch cs = comb_scratch(d, o + ES, reinterpret_cast<int*>(o + ES + comb_doubles(d)));
   const int nblk = (T + 1 + LB - 1) / LB;
   for (int b = blockIdx.x * gpb + gid; b < B; b += gridDim.x * gpb) {
     g_copy(g, ES, agg + (size_t)b * nblk * ES, acc);
@@ -448,9 +566,9 @@ __global__ void k_pfg_carry_seg(int nblk, int d, int B, int LB2, const double* _
   const int ES = fe_size_g(d);
   const Grp g = BLOCK ? block_group() : warp_group();
   const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
-  double* sm = smem + (size_t)gid * scan_smem(d);
-  double *acc = sm, *o = acc + ES, *tmpd = o + ES;
-  const CombScratch cs = comb_scratch(d, tmpd + ES, reinterpret_cast<int*>(tmpd + ES + comb_doubles(d)));
+  double* sm = smem + (size_t)gid * scan_smem(d, 2);
+  double *acc = sm, *o = acc + ES;
+  const CombScratch cs = comb_scratch(d, o + ES, reinterpret_cast<int*>(o + ES + comb_doubles(d)));
   const int nsup = (nblk + LB2 - 1) / LB2;
   const int span = j_hi - j_lo;  // super-block range [j_lo, j_hi) of this launch
   const long long n = (long long)B * span;
@@ -487,7 +605,7 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
   const int ES = fe_size_g(d), dd = d * d;
   const Grp g = BLOCK ? block_group() : warp_group();
   const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
-  double* sm = smem + (size_t)gid * scan_smem(d);
+  double* sm = smem + (size_t)gid * scan_smem(d, 3);
   double *acc = sm, *o = acc + ES, *cy = o + ES;
   const CombScratch cs = comb_scratch(d, cy + ES, reinterpret_cast<int*>(cy + ES + comb_doubles(d)));
   const int nblk = (T + 1 + LB - 1) / LB;
@@ -526,16 +644,63 @@ __host__ __device__ inline int rec_smem(int d, int dy) {
   return 3 * d * d + dy * d + 3 * dy * dy + 2 * W + 8;
 }
 
-// warp groups per CTA: as many (<= 8) as the largest per-group shared-memory
-// footprint allows — the combine chains are latency-bound, so occupancy matters
-GrpCfg launch_cfg(int d, int dy) {
-  GrpCfg c = grp_cfg(d, dy);
-  if (c.block) return c;
-  const size_t per = sizeof(double) * (size_t)std::max(elem_smem(d, dy),
-                                                       std::max(scan_smem(d), rec_smem(d, dy)));
-  c.groups = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / per));
-  c.threads = 32 * c.groups;
-  return c;
+// warp groups per CTA, per kernel: as many as its per-group shared-memory
+// footprint and its register count allow (<= 12) — the combine chains are
+// latency-bound, so occupancy matters
+struct KCfg {
+  int gp, threads;
+  size_t smem;
+};
+template <typename K>
+KCfg kcfg(K kernel, int d, int dy, int per_doubles) {
+  const GrpCfg c = grp_cfg(d, dy);
+  const size_t per = sizeof(double) * (size_t)per_doubles;
+  if (c.block) return KCfg{1, c.threads, per};
+  cudaFuncAttributes fa{};
+  int regs = 128;
+  if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess && fa.numRegs > 0) regs = fa.numRegs;
+  const int by_regs = 65536 / (32 * ((regs + 7) / 8 * 8));
+  const int gp = (int)std::max<size_t>(
+      1, std::min<size_t>({(size_t)12, (size_t)by_regs, (220 * 1024) / per}));
+  return KCfg{gp, 32 * gp, per * gp};
+}
+inline int kgrid(const KCfg& c, long long k) {
+  return (int)std::max(1LL, std::min((k + c.gp - 1) / c.gp, 148LL * 16));
+}
+template <typename K>
+int set_smem(K kernel, const KCfg& c) {
+  if (c.smem > 227 * 1024) return AUXMC_E_DIM;
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)c.smem));
+  return AUXMC_OK;
+}
+#define PFG_TRY(x)          \
+  do {                      \
+    const int rc_ = (x);    \
+    if (rc_) return rc_;    \
+  } while (0)
+
+// elements of [t_lo, t_hi): the fill path when the model is time-invariant
+// (t = 1 always built in full for its factors), the full build otherwise
+template <bool BLOCK>
+int launch_elements(const DevModel& dm, const double* obs, int B, double* el, double* proto,
+                    int* status, int t_lo, int t_hi, const KCfg& ce, cudaStream_t s) {
+  if (t_hi <= t_lo) return AUXMC_OK;
+  if (!proto || !pfg_time_invariant(dm) || BLOCK) {
+    AUXMC_LAUNCH(k_pfg_elements<BLOCK>, kgrid(ce, (long long)B * (t_hi - t_lo)), ce.threads,
+                 ce.smem, s, dm, obs, B, el, status, t_lo, t_hi, (double*)nullptr);
+    return AUXMC_OK;
+  }
+  const int f_lo = t_lo == 0 ? 0 : 1;  // full build of t = 1 (and t = 0 when owned)
+  AUXMC_LAUNCH(k_pfg_elements<BLOCK>, kgrid(ce, (long long)B * (2 - f_lo)), ce.threads, ce.smem,
+               s, dm, obs, B, el, status, f_lo, 2, proto);
+  const int g_lo = std::max(t_lo, 2);
+  if (t_hi > g_lo) {
+    const int per_b = (t_hi - g_lo + 32 * kFillWarps - 1) / (32 * kFillWarps);
+    AUXMC_LAUNCH(k_pfg_elem_fill, B * per_b, 32 * kFillWarps, 0, s, dm, obs, B, el, proto, g_lo,
+                 t_hi);
+  }
+  return AUXMC_OK;
 }
 
 template <bool BLOCK>
@@ -644,48 +809,48 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   double* agg = ws.take<double>((size_t)B * nblk * ES);
   double* carry = ws.take<double>((size_t)B * nblk * ES);
   double* terms = ws.take<double>((size_t)B * (T + 1));
+  double* proto = ws.take<double>((size_t)B * proto_doubles(d, dy));
   const bool two = nblk > kPfTwoLevel;
   const int LB2 = LB, nsup = (nblk + LB2 - 1) / LB2;
   double* agg2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
   double* carry2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!el || !agg || !carry || !terms || (two && (!agg2 || !carry2))) return AUXMC_E_WORKSPACE;
-  const GrpCfg cfg = launch_cfg(d, dy);
-  const int gp = cfg.groups;
-  const size_t sm_el = sizeof(double) * elem_smem(d, dy) * gp;
-  const size_t sm_sc = sizeof(double) * scan_smem(d) * gp;
-  const size_t sm_rc = sizeof(double) * rec_smem(d, dy) * gp;
-  if (sm_el > 227 * 1024 || sm_sc > 227 * 1024 || sm_rc > 227 * 1024) return AUXMC_E_DIM;
+  if (!el || !agg || !carry || !terms || !proto || (two && (!agg2 || !carry2)))
+    return AUXMC_E_WORKSPACE;
+  const KCfg ce = kcfg(k_pfg_elements<BLOCK>, d, dy, elem_smem(d, dy));
+  const KCfg c2 = kcfg(k_pfg_reduce<BLOCK>, d, dy, scan_smem(d, 2));
+  const KCfg cc = kcfg(k_pfg_carry<BLOCK>, d, dy, scan_smem(d, 2));
+  const KCfg cg = kcfg(k_pfg_carry_seg<BLOCK>, d, dy, scan_smem(d, 2));
+  const KCfg c3 = kcfg(k_pfg_apply<BLOCK>, d, dy, scan_smem(d, 3));
+  const KCfg cr = kcfg(k_pfg_recover<BLOCK>, d, dy, rec_smem(d, dy));
+  PFG_TRY(set_smem(k_pfg_elements<BLOCK>, ce));
+  PFG_TRY(set_smem(k_pfg_reduce<BLOCK>, c2));
+  PFG_TRY(set_smem(k_pfg_carry<BLOCK>, cc));
+  PFG_TRY(set_smem(k_pfg_carry_seg<BLOCK>, cg));
+  PFG_TRY(set_smem(k_pfg_apply<BLOCK>, c3));
+  PFG_TRY(set_smem(k_pfg_recover<BLOCK>, cr));
   if (status) AUXMC_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int) * B, s));
   const long long n = (long long)B * (T + 1);
   const long long nb = (long long)B * nblk;
-  auto grid = [gp](long long k) { return (int)std::max(1LL, std::min((k + gp - 1) / gp, 148LL * 16)); };
-  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_elements<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_el));
-  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_reduce<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
-  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_carry<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
-  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_apply<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
-  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_recover<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rc));
-  AUXMC_LAUNCH(k_pfg_elements<BLOCK>, grid(n), cfg.threads, sm_el, s, dm, obs, B, el, status, 0,
-               T + 1);
-  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, grid(nb), cfg.threads, sm_sc, s, T, d, B, LB, el, agg, 0,
+  PFG_TRY(launch_elements<BLOCK>(dm, obs, B, el, proto, status, 0, T + 1, ce, s));
+  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, nb), c2.threads, c2.smem, s, T, d, B, LB, el, agg, 0,
                nblk);
   if (two) {
-    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_carry_seg<BLOCK>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
     const long long ns = (long long)B * nsup;
-    AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, grid(ns), cfg.threads, sm_sc, s, nblk - 1, d, B, LB2, agg,
-                 agg2, 0, nsup);
-    AUXMC_LAUNCH(k_pfg_carry<BLOCK>, grid(B), cfg.threads, sm_sc, s, nsup - 1, d, B, 1, agg2,
+    AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, ns), c2.threads, c2.smem, s, nblk - 1, d, B, LB2,
+                 agg, agg2, 0, nsup);
+    AUXMC_LAUNCH(k_pfg_carry<BLOCK>, kgrid(cc, B), cc.threads, cc.smem, s, nsup - 1, d, B, 1, agg2,
                  carry2);
-    AUXMC_LAUNCH(k_pfg_carry_seg<BLOCK>, grid(ns), cfg.threads, sm_sc, s, nblk, d, B, LB2, agg,
-                 carry2, carry, 0, nsup);
+    AUXMC_LAUNCH(k_pfg_carry_seg<BLOCK>, kgrid(cg, ns), cg.threads, cg.smem, s, nblk, d, B, LB2,
+                 agg, carry2, carry, 0, nsup);
   } else {
-    AUXMC_LAUNCH(k_pfg_carry<BLOCK>, grid(B), cfg.threads, sm_sc, s, T, d, B, LB, agg, carry);
+    AUXMC_LAUNCH(k_pfg_carry<BLOCK>, kgrid(cc, B), cc.threads, cc.smem, s, T, d, B, LB, agg, carry);
   }
-  AUXMC_LAUNCH(k_pfg_apply<BLOCK>, grid(nb), cfg.threads, sm_sc, s, T, d, B, LB, el, carry,
+  AUXMC_LAUNCH(k_pfg_apply<BLOCK>, kgrid(c3, nb), c3.threads, c3.smem, s, T, d, B, LB, el, carry,
                out->filt_mean, out->filt_cov, 0, nblk);
-  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, grid(n), cfg.threads, sm_rc, s, dm, obs, B, out->filt_mean,
-               out->filt_cov, out->pred_mean, out->pred_cov, terms, status, 0, T + 1);
+  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, kgrid(cr, n), cr.threads, cr.smem, s, dm, obs, B,
+               out->filt_mean, out->filt_cov, out->pred_mean, out->pred_cov, terms, status, 0,
+               T + 1);
   AUXMC_LAUNCH(k_pfg_sum, B, kSumThreads, 0, s, T, B, terms, out->log_marginal);
   return AUXMC_OK;
 }
@@ -711,7 +876,7 @@ TsGeom ts_geom(int T) {
 }
 
 struct TsBufs {
-  double *el, *agg, *carry, *terms, *agg2, *carry2, *bnd;
+  double *el, *agg, *carry, *terms, *agg2, *carry2, *bnd, *proto;
 };
 TsBufs ts_take(const DevModel& dm, Arena& ws) {
   const TsGeom G = ts_geom(dm.T);
@@ -724,6 +889,7 @@ TsBufs ts_take(const DevModel& dm, Arena& ws) {
   b.agg2 = ws.take<double>((size_t)G.nsup * ES);
   b.carry2 = ws.take<double>((size_t)G.nsup * ES);
   b.bnd = ws.take<double>((size_t)G.nsup * (dm.dx + dm.dx * dm.dx));
+  b.proto = ws.take<double>((size_t)proto_doubles(dm.dx, dm.dy));
   return b;
 }
 
@@ -758,24 +924,19 @@ int ts_filter_local(const DevModel& dm, const double* obs, int j_lo, int j_hi, A
   const TsGeom G = ts_geom(T);
   const TsBufs b = ts_take(dm, ws);
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!b.el || !b.carry2) return AUXMC_E_WORKSPACE;
+  if (!b.el || !b.carry2 || !b.proto) return AUXMC_E_WORKSPACE;
   if (j_lo < 0 || j_hi > G.nsup || j_lo >= j_hi) return AUXMC_E_ARG;
-  const GrpCfg cfg = launch_cfg(d, dy);
-  const int gp = cfg.groups;
-  const size_t sm_el = sizeof(double) * elem_smem(d, dy) * gp;
-  const size_t sm_sc = sizeof(double) * scan_smem(d) * gp;
-  if (sm_el > 227 * 1024 || sm_sc > 227 * 1024) return AUXMC_E_DIM;
-  auto grid = [gp](long long k) { return (int)std::max(1LL, std::min((k + gp - 1) / gp, 148LL * 16)); };
+  const KCfg ce = kcfg(k_pfg_elements<BLOCK>, d, dy, elem_smem(d, dy));
+  const KCfg c2 = kcfg(k_pfg_reduce<BLOCK>, d, dy, scan_smem(d, 2));
+  PFG_TRY(set_smem(k_pfg_elements<BLOCK>, ce));
+  PFG_TRY(set_smem(k_pfg_reduce<BLOCK>, c2));
   const int t_lo = j_lo * G.SB, t_hi = std::min(j_hi * G.SB, T + 1);
   const int k_lo = j_lo * G.LB2, k_hi = std::min(j_hi * G.LB2, G.nblk);
-  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_elements<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_el));
-  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_reduce<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
-  AUXMC_LAUNCH(k_pfg_elements<BLOCK>, grid(t_hi - t_lo), cfg.threads, sm_el, s, dm, obs, 1, b.el,
-               status, t_lo, t_hi);
-  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, grid(k_hi - k_lo), cfg.threads, sm_sc, s, T, d, 1, G.LB, b.el,
-               b.agg, k_lo, k_hi);
-  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, grid(j_hi - j_lo), cfg.threads, sm_sc, s, G.nblk - 1, d, 1,
-               G.LB2, b.agg, b.agg2, j_lo, j_hi);
+  PFG_TRY(launch_elements<BLOCK>(dm, obs, 1, b.el, b.proto, status, t_lo, t_hi, ce, s));
+  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, k_hi - k_lo), c2.threads, c2.smem, s, T, d, 1, G.LB,
+               b.el, b.agg, k_lo, k_hi);
+  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, j_hi - j_lo), c2.threads, c2.smem, s, G.nblk - 1, d,
+               1, G.LB2, b.agg, b.agg2, j_lo, j_hi);
   AUXMC_CUDA_TRY(cudaMemcpyAsync(sup_out, b.agg2 + (size_t)j_lo * ES,
                                  sizeof(double) * (size_t)(j_hi - j_lo) * ES,
                                  cudaMemcpyDeviceToDevice, s));
@@ -790,35 +951,34 @@ int ts_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_hi, 
   const TsGeom G = ts_geom(T);
   const TsBufs b = ts_take(dm, ws);
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!b.el || !b.carry2) return AUXMC_E_WORKSPACE;
+  if (!b.el || !b.carry2 || !b.proto) return AUXMC_E_WORKSPACE;
   if (j_lo < 0 || j_hi > G.nsup || j_lo >= j_hi) return AUXMC_E_ARG;
-  const GrpCfg cfg = launch_cfg(d, dy);
-  const int gp = cfg.groups;
-  const size_t sm_sc = sizeof(double) * scan_smem(d) * gp;
-  const size_t sm_rc = sizeof(double) * rec_smem(d, dy) * gp;
-  if (sm_sc > 227 * 1024 || sm_rc > 227 * 1024) return AUXMC_E_DIM;
-  auto grid = [gp](long long k) { return (int)std::max(1LL, std::min((k + gp - 1) / gp, 148LL * 16)); };
+  const KCfg cc = kcfg(k_pfg_carry<BLOCK>, d, dy, scan_smem(d, 2));
+  const KCfg cg = kcfg(k_pfg_carry_seg<BLOCK>, d, dy, scan_smem(d, 2));
+  const KCfg c3 = kcfg(k_pfg_apply<BLOCK>, d, dy, scan_smem(d, 3));
+  const KCfg cr = kcfg(k_pfg_recover<BLOCK>, d, dy, rec_smem(d, dy));
+  PFG_TRY(set_smem(k_pfg_carry<BLOCK>, cc));
+  PFG_TRY(set_smem(k_pfg_carry_seg<BLOCK>, cg));
+  PFG_TRY(set_smem(k_pfg_apply<BLOCK>, c3));
+  PFG_TRY(set_smem(k_pfg_recover<BLOCK>, cr));
   const int t_lo = j_lo * G.SB, t_hi = std::min(j_hi * G.SB, T + 1);
   const int k_lo = j_lo * G.LB2, k_hi = std::min(j_hi * G.LB2, G.nblk);
   AUXMC_CUDA_TRY(cudaMemcpyAsync(b.agg2, sup_all, sizeof(double) * (size_t)G.nsup * ES,
                                  cudaMemcpyDeviceToDevice, s));
-  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_carry<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
-  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_carry_seg<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
-  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_apply<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sc));
-  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_recover<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_rc));
   // every rank runs the same serial carry over all super-block aggregates
-  AUXMC_LAUNCH(k_pfg_carry<BLOCK>, 1, cfg.threads, sm_sc, s, G.nsup - 1, d, 1, 1, b.agg2, b.carry2);
-  AUXMC_LAUNCH(k_pfg_carry_seg<BLOCK>, grid(j_hi - j_lo), cfg.threads, sm_sc, s, G.nblk, d, 1,
-               G.LB2, b.agg, b.carry2, b.carry, j_lo, j_hi);
-  AUXMC_LAUNCH(k_pfg_apply<BLOCK>, grid(k_hi - k_lo), cfg.threads, sm_sc, s, T, d, 1, G.LB, b.el,
-               b.carry, out->filt_mean, out->filt_cov, k_lo, k_hi);
+  AUXMC_LAUNCH(k_pfg_carry<BLOCK>, 1, cc.threads, cc.smem, s, G.nsup - 1, d, 1, 1, b.agg2,
+               b.carry2);
+  AUXMC_LAUNCH(k_pfg_carry_seg<BLOCK>, kgrid(cg, j_hi - j_lo), cg.threads, cg.smem, s, G.nblk, d,
+               1, G.LB2, b.agg, b.carry2, b.carry, j_lo, j_hi);
+  AUXMC_LAUNCH(k_pfg_apply<BLOCK>, kgrid(c3, k_hi - k_lo), c3.threads, c3.smem, s, T, d, 1, G.LB,
+               b.el, b.carry, out->filt_mean, out->filt_cov, k_lo, k_hi);
   const int jb_hi = std::min(j_hi + 1, G.nsup);  // owned super-blocks and the next one's start
   AUXMC_LAUNCH(k_ts_boundary, std::max(1, jb_hi - j_lo), 128, 0, s, d, j_lo, jb_hi, b.carry2,
                b.bnd);
   // + the predictive moments at t_hi (the next range's first step, from the
   // carry of super-block j_hi: identical bits on both ranks) for the sampler
   const int r_hi = std::min(t_hi + 1, T + 1);
-  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, grid(r_hi - t_lo), cfg.threads, sm_rc, s, dm, obs, 1,
+  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, kgrid(cr, r_hi - t_lo), cr.threads, cr.smem, s, dm, obs, 1,
                out->filt_mean, out->filt_cov, out->pred_mean, out->pred_cov, b.terms, status, t_lo,
                r_hi, G.SB, b.bnd);
   AUXMC_LAUNCH(k_ts_partials, (j_hi - j_lo + 127) / 128, 128, 0, s, T, G.SB, j_lo, j_hi, b.terms,

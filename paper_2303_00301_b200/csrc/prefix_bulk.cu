@@ -17,6 +17,12 @@
 #include "rng.cuh"
 #include "tma.cuh"
 
+// Kernel experiments (tools/exp_build.sh only; the product build leaves it 0):
+// 1 = no tile / noise / path traffic (arithmetic and barriers alone).
+#ifndef AUXMC_PB_EXP
+#define AUXMC_PB_EXP 0
+#endif
+
 namespace auxmc_gpu {
 
 template <int D>
@@ -210,12 +216,14 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
   if (T == 0) return;
   const int K = (T + S - 1) / S;
   auto issue_tile = [&](int k) {
+    if (AUXMC_PB_EXP == 1) return;
     const unsigned tb = G::TB * sizeof(double);
     uint64_t* bar = &barT[k % G::TSTG];
     mbar_expect_tx(bar, tb);
     bulk_g2s(tile(k), tiles + (size_t)k * G::TB, tb, bar);
   };
   auto issue_noise = [&](int k) {
+    if (AUXMC_PB_EXP == 1) return;
     const int t0 = k * S, len = min(S, T - t0);
     const unsigned xb = (unsigned)(len * D * sizeof(double));
     uint64_t* bar = &barN[k % G::NSTG];
@@ -234,11 +242,13 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
   }
   unsigned tph = 0u, nph = 0u;  // per-stage mbarrier parities seen by this thread
   auto wait_tile = [&](int k) {
+    if (AUXMC_PB_EXP == 1) return;
     const int b = k % G::TSTG;
     mbar_wait(&barT[b], (tph >> b) & 1u);
     tph ^= 1u << b;
   };
   auto wait_noise = [&](int k) {
+    if (AUXMC_PB_EXP == 1) return;
     const int b = k % G::NSTG;
     mbar_wait(&barN[b], (nph >> b) & 1u);
     nph ^= 1u << b;
@@ -472,7 +482,7 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
       for (int i = 0; i < D; ++i) yA[i] = yB[i];
     }
     __syncthreads();
-    if (cw && lane == 0) {
+    if (cw && lane == 0 && AUXMC_PB_EXP != 1) {
       const unsigned xb = (unsigned)((t1 - t0) * D * sizeof(double));
       for (int ch = 0; ch < nc; ++ch)
         bulk_s2g(traj + (size_t)(c_begin + ch) * row + (size_t)t0 * D, xo + ch * G::ROW, xb);

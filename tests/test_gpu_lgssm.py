@@ -272,7 +272,9 @@ def test_parallel_filter_matches_oracle(gpu, oracle, case):
 
 
 @pytest.mark.parametrize("case", LARGE_CASES[:2] + LARGE_CASES[3:] + [(20, 3, 11, True, True, 36),
-                                                                     (40, 9, 4, True, True, 37)])
+                                                                     (40, 9, 4, True, True, 37),
+                                                                     (60, 16, 16, True, True, 42),
+                                                                     (150, 16, 5, False, True, 43)])
 def test_parallel_filter_large_dims_matches_oracle(gpu, oracle, case):
     """Group (warp / CTA) scan filter for dx > 6 or dy > 8: group LU combine,
     element build and recovery vs the oracle's Sklansky scan."""
@@ -347,3 +349,26 @@ def test_host_pipeline_equals_device_call(gpu, oracle, sampler):
     lgssm.HostPipeline(gm, B, sampler, chunks=4)(h_fr, h_noise, out)
     torch.cuda.synchronize()
     assert torch.equal(out, want)
+
+
+@pytest.mark.parametrize("T,dx,dy,seed", [(300, 16, 16, 44), (200, 10, 3, 45), (2, 12, 5, 46)])
+def test_parallel_filter_time_invariant_fill_bit_identical(gpu, oracle, T, dx, dy, seed):
+    """Generic scan filter: a model with shared F, b, Q, H, c, R takes the
+    element fill path (t = 1 built in full, other steps copy its matrices and form
+    their vectors in the same order); the same model given with per-step copies
+    of every matrix takes the full element build.  Results must be identical
+    bits, and match the oracle's scan."""
+    lgssm, _, _ = gpu
+    m, obs = _oracle_case(oracle, T, dx, dy, False, False, seed)
+    shared = to_gpu_model(m)
+    def rep(a, n):
+        return np.repeat(np.asarray(a), n, axis=0)  # shared arrays have a leading 1
+    per_step = lgssm.Model(m.T, m.m0, m.P0, rep(m.F, T), rep(m.b, T), rep(m.Q, T),
+                           rep(m.H, T + 1), rep(m.c, T + 1), rep(m.R, T + 1), None)
+    a = lgssm.parallel_filter(shared, obs)
+    b = lgssm.parallel_filter(per_step, obs)
+    for name in ("filt_mean", "filt_cov", "pred_mean", "pred_cov", "log_marginal"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
+    par, _ = oracle.parallel_filter(m, obs)
+    assert_close(a.filt_mean[0].cpu(), par.filt_mean, 1e-8, "filt_mean vs oracle scan")
+    assert_close(a.log_marginal[0].cpu(), par.log_marginal, 1e-9, "log_marginal")

@@ -16,6 +16,7 @@ CASES = [
     ("spatio-temporal", dict(grid=3, data_seed=7), 150, 0.5),
     ("lgssm-synthetic", dict(dx=2, dy=1, data_seed=3), 300, 0.7),
     ("stochvol", dict(dx=3, data_seed=11), 120, 0.5),
+    ("spatio-temporal", dict(grid=4, data_seed=7), 130, 0.01),  # d = 16 (C5)
 ]
 
 
