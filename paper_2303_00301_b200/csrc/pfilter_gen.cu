@@ -161,7 +161,8 @@ struct CombScratch {
 // remaining algebra is dense products.
 template <int DC>
 __device__ __forceinline__ void g_combine_t(const Grp& g, int d_rt, const double* u,
-                                            const double* v, double* o, const CombScratch& s) {
+                                            const double* v, double* o, const CombScratch& s,
+                                            double* save_minv) {
   const int d = DC ? DC : d_rt;
   const int dd = d * d;
   const double *uA = u, *ub = u + dd, *uC = u + dd + d, *ueta = u + 2 * dd + d,
@@ -193,6 +194,7 @@ __device__ __forceinline__ void g_combine_t(const Grp& g, int d_rt, const double
     s.w[i] = veta[i] - acc2;
   }
   g.sync();
+  if (save_minv) g_copy(g, dd, Minv, save_minv);  // k_pfg_reduce_proto
   // A = vA (Minv uA) ; S = Minv uC ; T2 = Minv^T vJ
   g_mm(g, d, d, d, Minv, uA, s.S);
   g_mm(g, d, d, d, Minv, uC, s.T1);
@@ -239,9 +241,10 @@ __device__ __forceinline__ void g_combine_t(const Grp& g, int d_rt, const double
 // d = 16 (the C5 state dimension) gets a fully static instance: the Gauss-Jordan
 // inverse dominated the generic combine's instruction count (runtime bounds).
 __device__ __noinline__ void g_combine(const Grp& g, int d, const double* u, const double* v,
-                                       double* o, const CombScratch& s) {
-  if (d == 16) g_combine_t<16>(g, d, u, v, o, s);
-  else g_combine_t<0>(g, d, u, v, o, s);
+                                       double* o, const CombScratch& s,
+                                       double* save_minv = nullptr) {
+  if (d == 16) g_combine_t<16>(g, d, u, v, o, s, save_minv);
+  else g_combine_t<0>(g, d, u, v, o, s, save_minv);
 }
 
 __host__ __device__ inline int comb_doubles(int d) { return 3 * d * d + 2 * d; }
@@ -533,6 +536,131 @@ __global__ void k_pfg_reduce(int T, int d, int B, int LB, const double* __restri
   }
 }
 
+// S1 for a time-invariant model (pfg_time_invariant): every block but the first
+// combines elements whose matrix parts are those of t = 1, so the running
+// aggregate's matrices after p combines, and the inverse each combine forms, are
+// the same in every block.  k_pfg_reduce_proto runs that matrix sequence once
+// (on el[1] alone) and keeps, per position p, [A_p | C_p | J_p | Minv_{p+1}];
+// k_pfg_reduce_fill then carries each block's (b, eta) through the combine's
+// vector formulas, in g_combine's loop order — identical bits to k_pfg_reduce.
+__host__ __device__ inline int rproto_doubles(int d, int LB) { return 4 * d * d * LB; }
+
+template <bool BLOCK>
+__global__ void k_pfg_reduce_proto(int T, int d, int B, int LB, const double* __restrict__ el,
+                                   double* mats) {
+  extern __shared__ double smem[];
+  const int ES = fe_size_g(d), dd = d * d;
+  const Grp g = BLOCK ? block_group() : warp_group();
+  const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
+  double* sm = smem + (size_t)gid * scan_smem(d, 2);
+  double *acc = sm, *o = acc + ES;
+  const CombScratch cs = comb_scratch(d, o + ES, reinterpret_cast<int*>(o + ES + comb_doubles(d)));
+  for (int b = blockIdx.x * gpb + gid; b < B; b += gridDim.x * gpb) {
+    const double* e1 = el + ((size_t)b * (T + 1) + 1) * ES;
+    double* M = mats + (size_t)b * rproto_doubles(d, LB);
+    g_copy(g, ES, e1, acc);
+    g.sync();
+    for (int p = 0; p < LB; ++p) {
+      double* Mp = M + (size_t)p * 4 * dd;
+      g_copy(g, dd, acc, Mp);
+      g_copy(g, dd, acc + dd + d, Mp + dd);
+      g_copy(g, dd, acc + 2 * dd + 2 * d, Mp + 2 * dd);
+      g.sync();
+      if (p + 1 < LB) {
+        g_combine(g, d, acc, e1, o, cs, Mp + 3 * dd);
+        g_copy(g, ES, o, acc);
+        g.sync();
+      }
+    }
+  }
+}
+
+// thread per (sequence, block), blocks [max(k_lo, 1), k_hi)
+__global__ void k_pfg_reduce_fill(int T, int d, int B, int LB, const double* __restrict__ el,
+                                  const double* __restrict__ mats, double* agg, int k_lo,
+                                  int k_hi) {
+  constexpr int MX = 16;
+  const int ES = fe_size_g(d), dd = d * d;
+  const int nblk = (T + 1 + LB - 1) / LB;
+  const int k0 = max(k_lo, 1), span = k_hi - k0;
+  const long long n = (long long)B * span;
+  for (long long qq = (long long)blockIdx.x * blockDim.x + threadIdx.x; qq < n;
+       qq += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(qq / span), k = k0 + (int)(qq % span);
+    const int lo = k * LB, hi = min(lo + LB, T + 1);
+    const double* base = el + (size_t)b * (T + 1) * ES;
+    const double* M = mats + (size_t)b * rproto_doubles(d, LB);
+    const double* e1 = base + ES;  // v matrices (shared by every t >= 1)
+    const double *vA = e1, *vJ = e1 + 2 * dd + 2 * d;
+    double ub[MX], ueta[MX];
+    const double* e = base + (size_t)lo * ES;
+#pragma unroll
+    for (int i = 0; i < MX; ++i)
+      if (i < d) {
+        ub[i] = e[dd + i];
+        ueta[i] = e[2 * dd + d + i];
+      }
+    for (int t = lo + 1; t < hi; ++t) {
+      const int p = t - lo - 1;  // u = aggregate after p combines
+      const double* Mp = M + (size_t)p * 4 * dd;
+      const double *uA = Mp, *uC = Mp + dd, *Minv = Mp + 3 * dd;
+      const double* ev = base + (size_t)t * ES;
+      const double *vb = ev + dd, *veta = ev + 2 * dd + d;
+      double tt[MX], w[MX], mt[MX], mt2[MX];
+#pragma unroll
+      for (int i = 0; i < MX; ++i)
+        if (i < d) {
+          double acc = 0.0, acc2 = 0.0;
+          for (int q = 0; q < d; ++q) {
+            acc += uC[i * d + q] * veta[q];
+            acc2 += vJ[i * d + q] * ub[q];
+          }
+          tt[i] = acc + ub[i];
+          w[i] = veta[i] - acc2;
+        }
+#pragma unroll
+      for (int i = 0; i < MX; ++i)
+        if (i < d) {
+          double acc = 0.0, acc2 = 0.0;
+#pragma unroll
+          for (int q = 0; q < MX; ++q)
+            if (q < d) {
+              acc += Minv[i * d + q] * tt[q];
+              acc2 += Minv[q * d + i] * w[q];
+            }
+          mt[i] = acc;
+          mt2[i] = acc2;
+        }
+#pragma unroll
+      for (int i = 0; i < MX; ++i)
+        if (i < d) {
+          double acc = 0.0, acc2 = 0.0;
+#pragma unroll
+          for (int q = 0; q < MX; ++q)
+            if (q < d) {
+              acc += vA[i * d + q] * mt[q];
+              acc2 += uA[q * d + i] * mt2[q];
+            }
+          ub[i] = acc + vb[i];
+          ueta[i] = acc2 + ueta[i];
+        }
+    }
+    const double* Mf = M + (size_t)(hi - lo - 1) * 4 * dd;
+    double* out = agg + ((size_t)b * nblk + k) * ES;
+    for (int i = 0; i < dd; ++i) {
+      out[i] = Mf[i];
+      out[dd + d + i] = Mf[dd + i];
+      out[2 * dd + 2 * d + i] = Mf[2 * dd + i];
+    }
+#pragma unroll
+    for (int i = 0; i < MX; ++i)
+      if (i < d) {
+        out[dd + i] = ub[i];
+        out[2 * dd + d + i] = ueta[i];
+      }
+  }
+}
+
 template <bool BLOCK>
 __global__ void k_pfg_carry(int T, int d, int B, int LB, const double* __restrict__ agg, double* carry) {
   extern __shared__ double smem[];
@@ -703,6 +831,31 @@ int launch_elements(const DevModel& dm, const double* obs, int B, double* el, do
   return AUXMC_OK;
 }
 
+// S1 over blocks [k_lo, k_hi): the proto + fill path for time-invariant models
+template <bool BLOCK>
+int launch_reduce(const DevModel& dm, int B, int LB, const double* el, double* mats, double* agg,
+                  int k_lo, int k_hi, const KCfg& c2, const KCfg& cp, cudaStream_t s) {
+  const int T = dm.T, d = dm.dx;
+  if (k_hi <= k_lo) return AUXMC_OK;
+  if (!mats || BLOCK || !pfg_time_invariant(dm) || LB < 2) {
+    AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, (long long)B * (k_hi - k_lo)), c2.threads,
+                 c2.smem, s, T, d, B, LB, el, agg, k_lo, k_hi);
+    return AUXMC_OK;
+  }
+  AUXMC_LAUNCH(k_pfg_reduce_proto<BLOCK>, kgrid(cp, B), cp.threads, cp.smem, s, T, d, B, LB, el,
+               mats);
+  if (k_lo == 0)
+    AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, B), c2.threads, c2.smem, s, T, d, B, LB, el, agg,
+                 0, 1);
+  const int k0 = std::max(k_lo, 1);
+  if (k_hi > k0) {
+    const long long n = (long long)B * (k_hi - k0);
+    AUXMC_LAUNCH(k_pfg_reduce_fill, (int)std::min<long long>((n + 127) / 128, 148LL * 16), 128, 0,
+                 s, T, d, B, LB, el, mats, agg, k_lo, k_hi);
+  }
+  return AUXMC_OK;
+}
+
 template <bool BLOCK>
 __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
                               const double* __restrict__ fm, const double* __restrict__ fc,
@@ -810,21 +963,24 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   double* carry = ws.take<double>((size_t)B * nblk * ES);
   double* terms = ws.take<double>((size_t)B * (T + 1));
   double* proto = ws.take<double>((size_t)B * proto_doubles(d, dy));
+  double* mats = ws.take<double>((size_t)B * rproto_doubles(d, LB));
   const bool two = nblk > kPfTwoLevel;
   const int LB2 = LB, nsup = (nblk + LB2 - 1) / LB2;
   double* agg2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
   double* carry2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!el || !agg || !carry || !terms || !proto || (two && (!agg2 || !carry2)))
+  if (!el || !agg || !carry || !terms || !proto || !mats || (two && (!agg2 || !carry2)))
     return AUXMC_E_WORKSPACE;
   const KCfg ce = kcfg(k_pfg_elements<BLOCK>, d, dy, elem_smem(d, dy));
   const KCfg c2 = kcfg(k_pfg_reduce<BLOCK>, d, dy, scan_smem(d, 2));
+  const KCfg cp = kcfg(k_pfg_reduce_proto<BLOCK>, d, dy, scan_smem(d, 2));
   const KCfg cc = kcfg(k_pfg_carry<BLOCK>, d, dy, scan_smem(d, 2));
   const KCfg cg = kcfg(k_pfg_carry_seg<BLOCK>, d, dy, scan_smem(d, 2));
   const KCfg c3 = kcfg(k_pfg_apply<BLOCK>, d, dy, scan_smem(d, 3));
   const KCfg cr = kcfg(k_pfg_recover<BLOCK>, d, dy, rec_smem(d, dy));
   PFG_TRY(set_smem(k_pfg_elements<BLOCK>, ce));
   PFG_TRY(set_smem(k_pfg_reduce<BLOCK>, c2));
+  PFG_TRY(set_smem(k_pfg_reduce_proto<BLOCK>, cp));
   PFG_TRY(set_smem(k_pfg_carry<BLOCK>, cc));
   PFG_TRY(set_smem(k_pfg_carry_seg<BLOCK>, cg));
   PFG_TRY(set_smem(k_pfg_apply<BLOCK>, c3));
@@ -833,8 +989,7 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   const long long n = (long long)B * (T + 1);
   const long long nb = (long long)B * nblk;
   PFG_TRY(launch_elements<BLOCK>(dm, obs, B, el, proto, status, 0, T + 1, ce, s));
-  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, nb), c2.threads, c2.smem, s, T, d, B, LB, el, agg, 0,
-               nblk);
+  PFG_TRY(launch_reduce<BLOCK>(dm, B, LB, el, mats, agg, 0, nblk, c2, cp, s));
   if (two) {
     const long long ns = (long long)B * nsup;
     AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, ns), c2.threads, c2.smem, s, nblk - 1, d, B, LB2,
@@ -876,7 +1031,7 @@ TsGeom ts_geom(int T) {
 }
 
 struct TsBufs {
-  double *el, *agg, *carry, *terms, *agg2, *carry2, *bnd, *proto;
+  double *el, *agg, *carry, *terms, *agg2, *carry2, *bnd, *proto, *mats;
 };
 TsBufs ts_take(const DevModel& dm, Arena& ws) {
   const TsGeom G = ts_geom(dm.T);
@@ -890,6 +1045,7 @@ TsBufs ts_take(const DevModel& dm, Arena& ws) {
   b.carry2 = ws.take<double>((size_t)G.nsup * ES);
   b.bnd = ws.take<double>((size_t)G.nsup * (dm.dx + dm.dx * dm.dx));
   b.proto = ws.take<double>((size_t)proto_doubles(dm.dx, dm.dy));
+  b.mats = ws.take<double>((size_t)rproto_doubles(dm.dx, G.LB));
   return b;
 }
 
@@ -924,17 +1080,18 @@ int ts_filter_local(const DevModel& dm, const double* obs, int j_lo, int j_hi, A
   const TsGeom G = ts_geom(T);
   const TsBufs b = ts_take(dm, ws);
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!b.el || !b.carry2 || !b.proto) return AUXMC_E_WORKSPACE;
+  if (!b.el || !b.carry2 || !b.proto || !b.mats) return AUXMC_E_WORKSPACE;
   if (j_lo < 0 || j_hi > G.nsup || j_lo >= j_hi) return AUXMC_E_ARG;
   const KCfg ce = kcfg(k_pfg_elements<BLOCK>, d, dy, elem_smem(d, dy));
   const KCfg c2 = kcfg(k_pfg_reduce<BLOCK>, d, dy, scan_smem(d, 2));
+  const KCfg cp = kcfg(k_pfg_reduce_proto<BLOCK>, d, dy, scan_smem(d, 2));
   PFG_TRY(set_smem(k_pfg_elements<BLOCK>, ce));
   PFG_TRY(set_smem(k_pfg_reduce<BLOCK>, c2));
+  PFG_TRY(set_smem(k_pfg_reduce_proto<BLOCK>, cp));
   const int t_lo = j_lo * G.SB, t_hi = std::min(j_hi * G.SB, T + 1);
   const int k_lo = j_lo * G.LB2, k_hi = std::min(j_hi * G.LB2, G.nblk);
   PFG_TRY(launch_elements<BLOCK>(dm, obs, 1, b.el, b.proto, status, t_lo, t_hi, ce, s));
-  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, k_hi - k_lo), c2.threads, c2.smem, s, T, d, 1, G.LB,
-               b.el, b.agg, k_lo, k_hi);
+  PFG_TRY(launch_reduce<BLOCK>(dm, 1, G.LB, b.el, b.mats, b.agg, k_lo, k_hi, c2, cp, s));
   AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, j_hi - j_lo), c2.threads, c2.smem, s, G.nblk - 1, d,
                1, G.LB2, b.agg, b.agg2, j_lo, j_hi);
   AUXMC_CUDA_TRY(cudaMemcpyAsync(sup_out, b.agg2 + (size_t)j_lo * ES,
@@ -951,7 +1108,7 @@ int ts_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_hi, 
   const TsGeom G = ts_geom(T);
   const TsBufs b = ts_take(dm, ws);
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!b.el || !b.carry2 || !b.proto) return AUXMC_E_WORKSPACE;
+  if (!b.el || !b.carry2 || !b.proto || !b.mats) return AUXMC_E_WORKSPACE;
   if (j_lo < 0 || j_hi > G.nsup || j_lo >= j_hi) return AUXMC_E_ARG;
   const KCfg cc = kcfg(k_pfg_carry<BLOCK>, d, dy, scan_smem(d, 2));
   const KCfg cg = kcfg(k_pfg_carry_seg<BLOCK>, d, dy, scan_smem(d, 2));
