@@ -111,16 +111,25 @@ __device__ __forceinline__ void w_inverse_gj_t(int lane, int d_rt, const double*
 #pragma unroll
   for (int k = 0; k < MX; ++k) {  // fully unrolled: every index but the pivot row is static
     if (k >= d) break;
-    // pivot search by the lane owning column k (rows k..d-1)
-    double best = -1.0;
-    int p = k;
+    // pivot search by the lane owning column k (rows k..d-1): pairwise tree over
+    // the candidates, a later row wins only when strictly larger — the first
+    // row of largest |.|, as a sequential scan finds it
+    double av[MX];
+    int ai[MX];
 #pragma unroll
-    for (int i = k; i < MX; ++i)
-      if (i < d && fabs(col[i]) > best) {
-        best = fabs(col[i]);
-        p = i;
-      }
-    p = __shfl_sync(0xffffffffu, p, k);
+    for (int i = 0; i < MX; ++i) {
+      av[i] = (i >= k && i < d) ? fabs(col[i]) : -1.0;
+      ai[i] = i;
+    }
+#pragma unroll
+    for (int w = 1; w < MX; w *= 2)
+#pragma unroll
+      for (int i = 0; i + w < MX; i += 2 * w)
+        if (av[i + w] > av[i]) {
+          av[i] = av[i + w];
+          ai[i] = ai[i + w];
+        }
+    int p = __shfl_sync(0xffffffffu, ai[0] < k ? k : ai[0], k);  // NaN column: row k
     // swap rows k and p (p >= k) in every column
     const double vk = col[k];
     double vp = vk;
