@@ -212,10 +212,13 @@ __device__ __forceinline__ void fe_combine(const FElem<D>& u, const FElem<D>& v,
 }
 
 // ---- element build (pit.cpp:126-152), thread per (b, t)
-template <int D>
+// DY > 0: the observation count is the compile-time DY (static loop bounds, every
+// array in registers); DY = 0: any dy <= kMaxDY (arrays in local memory).
+template <int D, int DY>
 __global__ void k_pf_elements(DevModel m, const double* __restrict__ obs, int B, double* el,
                               int* status) {
-  const int T = m.T, dy = m.dy;
+  constexpr int MY = DY > 0 ? DY : kMaxDY;
+  const int T = m.T, dy = DY > 0 ? DY : m.dy;
   const long long n = (long long)B * (T + 1);
   constexpr int ES = fe_size<D>();
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
@@ -238,8 +241,8 @@ __global__ void k_pf_elements(DevModel m, const double* __restrict__ obs, int B,
       const double* c = m.ct(t, b);
       const double* R = m.Rt(t, b);
       const double* y = obs + ((size_t)b * (T + 1) + t) * dy;
-      double innov[kMaxDY], s[kMaxDY * kMaxDY], L[kMaxDY * kMaxDY], hq[kMaxDY * D],
-          X1[kMaxDY * D], X2[kMaxDY * D];
+      double innov[MY], s[MY * MY], L[MY * MY], hq[MY * D],
+          X1[MY * D], X2[MY * D];
       for (int i = 0; i < dy; ++i) {
         double acc = 0.0;
         for (int j = 0; j < D; ++j) acc += h[i * D + j] * bd[j];
@@ -289,7 +292,7 @@ __global__ void k_pf_elements(DevModel m, const double* __restrict__ obs, int B,
           for (int i = 0; i < dy * dy; ++i) sc = fabs(s[i]) > sc ? fabs(s[i]) : sc;
         }
         bool ok = false;
-        double sj[kMaxDY * kMaxDY];
+        double sj[MY * MY];
         for (int e2 = 0; e2 < 2 && !ok; ++e2) {
           const double eps = e2 == 0 ? 1e-10 : 1e-8;
           for (int i = 0; i < dy * dy; ++i) sj[i] = s[i] + ((i / dy == i % dy) ? (eps * sc) * 1.0 : 0.0);
@@ -345,19 +348,19 @@ __global__ void k_pf_elements(DevModel m, const double* __restrict__ obs, int B,
           t2[i * D + j] = acc;
         }
       // + gain R gain^T
-      double gr[D * kMaxDY];
+      double gr[D * MY];
       for (int i = 0; i < D; ++i)
         for (int j = 0; j < dy; ++j) {
           double acc = 0.0;
           for (int k = 0; k < dy; ++k) acc += X1[k * D + i] * (0.5 * (R[k * dy + j] + R[j * dy + k]));
-          gr[i * kMaxDY + j] = acc;
+          gr[i * MY + j] = acc;
         }
 #pragma unroll
       for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           double acc = 0.0;
-          for (int k = 0; k < dy; ++k) acc += gr[i * kMaxDY + k] * X1[k * D + j];
+          for (int k = 0; k < dy; ++k) acc += gr[i * MY + k] * X1[k * D + j];
           t2[i * D + j] += acc;
         }
 #pragma unroll
@@ -379,19 +382,19 @@ __global__ void k_pf_elements(DevModel m, const double* __restrict__ obs, int B,
         for (int k = 0; k < D; ++k) acc += f[k * D + i] * hv[k];
         e.eta[i] = acc;
       }
-      double fh[D * kMaxDY];
+      double fh[D * MY];
       for (int i = 0; i < D; ++i)
         for (int j = 0; j < dy; ++j) {
           double acc = 0.0;
           for (int k = 0; k < D; ++k) acc += f[k * D + i] * X2[j * D + k];
-          fh[i * kMaxDY + j] = acc;
+          fh[i * MY + j] = acc;
         }
 #pragma unroll
       for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           double acc = 0.0;
-          for (int k = 0; k < dy; ++k) acc += fh[i * kMaxDY + k] * h[k * D + j];
+          for (int k = 0; k < dy; ++k) acc += fh[i * MY + k] * h[k * D + j];
           t1[i * D + j] = acc;
         }
       mm<D>(t1, f, t2);
@@ -535,11 +538,12 @@ constexpr int sklansky_max_n() {
 }
 
 // recovery (pit.cpp:167-186): predictive moments from filt[t-1]; log-likelihood terms
-template <int D>
+template <int D, int DY>
 __global__ void k_pf_recover(DevModel m, const double* __restrict__ obs, int B,
                              const double* __restrict__ fm, const double* __restrict__ fc,
                              double* pm, double* pc, double* terms, int* status) {
-  const int T = m.T, dy = m.dy;
+  constexpr int MY = DY > 0 ? DY : kMaxDY;
+  const int T = m.T, dy = DY > 0 ? DY : m.dy;
   const long long n = (long long)B * (T + 1);
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
        q += (long long)gridDim.x * blockDim.x) {
@@ -604,7 +608,7 @@ __global__ void k_pf_recover(DevModel m, const double* __restrict__ obs, int B,
       const double* c = m.ct(t, b);
       const double* R = m.Rt(t, b);
       const double* y = obs + (size_t)q * dy;
-      double s[kMaxDY * kMaxDY], L[kMaxDY * kMaxDY], r[kMaxDY], hp[kMaxDY * D];
+      double s[MY * MY], L[MY * MY], r[MY], hp[MY * D];
       for (int i = 0; i < dy; ++i) {
         double acc = 0.0;
         for (int k = 0; k < D; ++k) acc += h[i * D + k] * mp[k];
@@ -700,7 +704,16 @@ static int run_pf(const DevModel& dm, const double* obs, int B, auxmc_filter_res
   const long long n = (long long)B * (T + 1);
   const long long nb = (long long)B * nblk;
   auto grid = [](long long k) { return (int)std::max(1LL, std::min((k + 127) / 128, 148LL * 16)); };
-  AUXMC_LAUNCH(k_pf_elements<D>, grid(n), 128, 0, s, dm, obs, B, el, status);
+  switch (dm.dy) {  // small observation counts: register-resident element builds
+#define PF_EL(DYV)                                                                         \
+  case DYV:                                                                                \
+    AUXMC_LAUNCH((k_pf_elements<D, DYV>), grid(n), 128, 0, s, dm, obs, B, el, status);  \
+    break;
+    PF_EL(1) PF_EL(2) PF_EL(3) PF_EL(4)
+#undef PF_EL
+    default:
+      AUXMC_LAUNCH((k_pf_elements<D, 0>), grid(n), 128, 0, s, dm, obs, B, el, status);
+  }
   if (T + 1 <= sklansky_max_n<D>() && B <= 2 * 148) {
     // few short sequences: one CTA each, Sklansky in shared memory
     const size_t smem = sizeof(double) * (size_t)(T + 1) * ES;
@@ -714,8 +727,18 @@ static int run_pf(const DevModel& dm, const double* obs, int B, auxmc_filter_res
     AUXMC_LAUNCH(k_pf_apply<D>, grid(nb), 128, 0, s, T, B, LB, el, carry, out->filt_mean,
                  out->filt_cov);
   }
-  AUXMC_LAUNCH(k_pf_recover<D>, grid(n), 128, 0, s, dm, obs, B, out->filt_mean, out->filt_cov,
-               out->pred_mean, out->pred_cov, terms, status);
+  switch (dm.dy) {
+#define PF_RC(DYV)                                                                          \
+  case DYV:                                                                                 \
+    AUXMC_LAUNCH((k_pf_recover<D, DYV>), grid(n), 128, 0, s, dm, obs, B, out->filt_mean,   \
+                 out->filt_cov, out->pred_mean, out->pred_cov, terms, status);              \
+    break;
+    PF_RC(1) PF_RC(2) PF_RC(3) PF_RC(4)
+#undef PF_RC
+    default:
+      AUXMC_LAUNCH((k_pf_recover<D, 0>), grid(n), 128, 0, s, dm, obs, B, out->filt_mean,
+                   out->filt_cov, out->pred_mean, out->pred_cov, terms, status);
+  }
   AUXMC_LAUNCH(k_pf_sum, B, kSumThreads, 0, s, T, B, terms, out->log_marginal);
   return AUXMC_OK;
 }

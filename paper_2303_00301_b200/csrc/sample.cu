@@ -452,7 +452,10 @@ __global__ void __launch_bounds__(NS)
     for (int i = 0; i < D; ++i) y[i] = 0.0;
 #pragma unroll
     for (int i = 0; i < D * D; ++i) P[i] = (i / D == i % D) ? 1.0 : 0.0;
-    for (int t = hi - 1; t >= lo; --t) {
+#pragma unroll(D <= 4 ? LS : 1)
+    for (int u = LS - 1; u >= 0; --u) {  // t = hi-1 .. lo, unrolled so the loads issue early
+      const int t = lo + u;
+      if (t >= hi) continue;
       const double* e = E + (size_t)t * ES;
       double xi[D], cv[D], gy[D], Q[D * D];
       if (PRE) {
@@ -506,7 +509,10 @@ __global__ void __launch_bounds__(NS)
     double x[D];
 #pragma unroll
     for (int i = 0; i < D; ++i) x[i] = xtop[j * D + i];
-    for (int t = hi - 1; t >= lo; --t) {
+#pragma unroll(D <= 4 ? LS : 1)
+    for (int u = LS - 1; u >= 0; --u) {
+      const int t = lo + u;
+      if (t >= hi) continue;
       const double* e = E + (size_t)t * ES;
       double gx[D];
       r_matvec<D>(e, x, gx);
@@ -540,6 +546,7 @@ int launch_prefix_generic(int T, int d, int B, int fr_shared, const double* elem
 namespace {
 
 constexpr int kNSp = 32, kLSp = 8;             // per-path prefix tiling
+constexpr int kNSs = 64, kLSs = 16;            // few paths (B <= 2 per SM): one 1024-step superchunk
 
 template <int D>
 int run_sampler(int sampler, int T, int B, int fr_shared, const double* elems,
@@ -552,10 +559,16 @@ int run_sampler(int sampler, int T, int B, int fr_shared, const double* elems,
   const long long es = fr_shared ? 0 : (long long)T * elem_stride(D);
   const long long ts = fr_shared ? 0 : term_stride(D);
   if (sampler == AUXMC_SAMPLER_PREFIX) {
-    if (pre)
+    if (B <= 2 * 148 && D <= 4) {
+      if (pre)
+        AUXMC_LAUNCH((k_prefix_private<D, kNSs, kLSs, true>), B, kNSs, 0, stream, T, elems, term, nz, traj);
+      else
+        AUXMC_LAUNCH((k_prefix_private<D, kNSs, kLSs, false>), B, kNSs, 0, stream, T, elems, term, nz, traj);
+    } else if (pre) {
       AUXMC_LAUNCH((k_prefix_private<D, kNSp, kLSp, true>), B, kNSp, 0, stream, T, elems, term, nz, traj);
-    else
+    } else {
       AUXMC_LAUNCH((k_prefix_private<D, kNSp, kLSp, false>), B, kNSp, 0, stream, T, elems, term, nz, traj);
+    }
     return AUXMC_OK;
   }
   const int grid = (B + 127) / 128;
