@@ -313,6 +313,29 @@ __device__ __forceinline__ void stream_normals(uint64_t key, double* xi) {
   for (int i = 0; i < D; ++i) xi[i] = normal_at(key, (uint64_t)i);
 }
 
+// The stream variates of B paths, drawn in parallel ahead of a latency-bound
+// sampler (same keys and indices as the samplers' own draws, so the paths are
+// bit-identical): thread per (path, t), t = T the terminal draw.
+template <int D>
+__global__ void k_draw_stream(int T, int B, const uint64_t* __restrict__ keys, double* term,
+                              double* back) {
+  const long long n = (long long)B * (T + 1);
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(q / (T + 1)), t = (int)(q % (T + 1));
+    double xi[D];
+    if (t == T) {
+      stream_normals<D>(derive(keys[c], kTerminalDraw, 0), xi);
+#pragma unroll
+      for (int i = 0; i < D; ++i) term[(size_t)c * D + i] = xi[i];
+    } else {
+      stream_normals<D>(derive_index(derive_label(keys[c], kBackwardNoise), (uint64_t)t), xi);
+#pragma unroll
+      for (int i = 0; i < D; ++i) back[((size_t)c * T + t) * D + i] = xi[i];
+    }
+  }
+}
+
 // ---------------------------------------------------------------- sequential / per-path elements
 // Thread per path; elements either shared (es = 0) or per path.
 template <int D, bool PRE>
@@ -555,15 +578,30 @@ int run_sampler(int sampler, int T, int B, int fr_shared, const double* elems,
   const bool pre = nz.kind == AUXMC_NOISE_PREDRAWN;
   if (sampler == AUXMC_SAMPLER_PREFIX && fr_shared)
     return launch_prefix_shared(D, T, B, elems, term, ws, nz, traj, stream);
+  const bool few = B <= 2 * 148 && D <= 4;
+  double *nterm = nullptr, *nback = nullptr;
+  if (sampler == AUXMC_SAMPLER_PREFIX && few && !pre) {
+    nterm = ws.take<double>((size_t)B * D);
+    nback = ws.take<double>((size_t)B * (T > 0 ? T : 1) * D);
+  }
   if (ws.base == nullptr) return AUXMC_OK;
   const long long es = fr_shared ? 0 : (long long)T * elem_stride(D);
   const long long ts = fr_shared ? 0 : term_stride(D);
   if (sampler == AUXMC_SAMPLER_PREFIX) {
-    if (B <= 2 * 148 && D <= 4) {
-      if (pre)
-        AUXMC_LAUNCH((k_prefix_private<D, kNSs, kLSs, true>), B, kNSs, 0, stream, T, elems, term, nz, traj);
-      else
-        AUXMC_LAUNCH((k_prefix_private<D, kNSs, kLSs, false>), B, kNSs, 0, stream, T, elems, term, nz, traj);
+    if (few) {
+      NoiseArgs pz = nz;
+      if (nterm && nback) {  // few long serial chains: draw the variates in parallel first
+        const long long n = (long long)B * (T + 1);
+        AUXMC_LAUNCH(k_draw_stream<D>, (int)std::min<long long>((n + 127) / 128, 148LL * 16),
+                     128, 0, stream, T, B, nz.keys, nterm, nback);
+        pz.kind = AUXMC_NOISE_PREDRAWN;
+        pz.terminal = nterm;
+        pz.backward = nback;
+      } else if (!pre) {
+        return AUXMC_E_WORKSPACE;
+      }
+      AUXMC_LAUNCH((k_prefix_private<D, kNSs, kLSs, true>), B, kNSs, 0, stream, T, elems, term, pz,
+                   traj);
     } else if (pre) {
       AUXMC_LAUNCH((k_prefix_private<D, kNSp, kLSp, true>), B, kNSp, 0, stream, T, elems, term, nz, traj);
     } else {
