@@ -78,5 +78,27 @@ def build(verbose: bool = False) -> pathlib.Path:
     return LIB
 
 
+TEST_SRC = PKG.parent / "tests" / "cpp" / "test_facade.cpp"
+TEST_BIN = PKG.parent / "tests" / "cpp" / "build" / "test_facade"
+
+
+def build_tests() -> pathlib.Path:
+    """C++ facade parity test (tests/cpp/test_facade.cpp), linked against the
+    product library and the CPU oracle (test infrastructure; build it first with
+    oracle/pyoracle.build()).  rpaths are relative so the binary runs from any
+    checkout, including the GPU box's copy of the repo."""
+    oracle_lib = PKG.parent / "oracle" / "build" / "liboracle.so"
+    TEST_BIN.parent.mkdir(parents=True, exist_ok=True)
+    deps = [TEST_SRC, LIB, oracle_lib, PKG.parent / "include" / "auxmc_b200.hpp"]
+    if TEST_BIN.exists() and all(d.stat().st_mtime <= TEST_BIN.stat().st_mtime for d in deps):
+        return TEST_BIN
+    _compile(["g++", "-O2", "-std=c++17", "-Wall", "-I", str(PKG.parent / "include"),
+              "-I", str(PKG.parent / "oracle"), str(TEST_SRC), "-o", str(TEST_BIN),
+              "-L", str(PKG), "-lauxmc_b200", "-L", str(oracle_lib.parent), "-loracle",
+              "-Wl,-rpath,$ORIGIN/../../../paper_2303_00301_b200",
+              "-Wl,-rpath,$ORIGIN/../../../oracle/build"])
+    return TEST_BIN
+
+
 if __name__ == "__main__":
     print(build(verbose=True))
