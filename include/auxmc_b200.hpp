@@ -397,7 +397,7 @@ class AuxChains {
 
 }  // namespace auxk
 
-/* ---- fkpg.hpp:58-109 (gradient proposal linearized at the aux observation) ---- */
+/* ---- fkpg.hpp:58-109 (proposals linearized at the aux observation) ---- */
 namespace fkpg {
 
 enum class ProposalMode { kPrior, kGradient, kFullyAdapted };
@@ -460,7 +460,8 @@ namespace bench {
 struct RunConfig {
   std::string sampler = "aux-kalman-seq";
   // aux-kalman-seq | aux-kalman-prefix | aux-kalman-dnc |
-  // pgibbs-gradient (reference cSMC) | pgibbs-pit (parallel-in-time cSMC, new)
+  // pgibbs-prior | pgibbs-gradient | pgibbs-adapted (reference cSMC) |
+  // pgibbs-pit (parallel-in-time cSMC, gradient proposals; new)
   long chain_length = 1000;
   long burn_in = 100;
   int particles = 16;

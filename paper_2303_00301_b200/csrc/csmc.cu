@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "dense.cuh"
+#include "group.cuh"
 #include "rng.cuh"
 #include "target.cuh"
 
@@ -240,7 +241,105 @@ struct PgArgs {
   int* anc;         // optional [C][T+1][N]
   int* sel;         // optional [C][T+1]
   const int* grad_bad;
+  int mode;         // AUXMC_PG_PRIOR / GRADIENT / ADAPTED (fkpg.hpp:58)
+  const double* adf;  // ADAPTED: [C][nad][2 d^2 + 1] gain | L | logdet per proposal class
+  int nad;
+  const int* ad_bad;  // ADAPTED: [C] factorization failure of a proposal class
 };
+
+// proposal class of step t: 0 = prior at t = 0 (m0, P0), 1 + j = dynamics with Q_j
+__device__ __forceinline__ int prop_class(const FactorRef& f, int t) {
+  return t == 0 ? 0 : 1 + (f.fl.nQ > 1 ? t - 1 : 0);
+}
+
+// Fully adapted proposal factors (fkpg.cpp:173-185) per (chain, class): the
+// conjugate combination of N(prior_mean, prior_cov) with z = x + N(0, (δ/2) I).
+// gain and cov depend on (δ, class) only; the mean depends on the parent.
+// One warp per item: S = pc + hI, gain = solve_spd(S, pc)^T, a = I - gain,
+// cov = symm(a pc a^T + h gain gain^T), L = chol_psd(cov).
+__global__ void k_pg_adapted(DevTarget tg, int C, int nad, const double* __restrict__ delta,
+                             double* adf, int* bad) {
+  extern __shared__ double smem[];
+  const int d = tg.dx, dd = d * d;
+  Grp g = warp_group();
+  const int gid = threadIdx.x >> 5, gpb = blockDim.x >> 5;
+  double* pc = smem + (size_t)gid * (6 * dd + 4);
+  double* S = pc + dd;
+  double* L = S + dd;
+  double* X = L + dd;
+  double* A = X + dd;
+  double* Wm = A + dd;
+  double* red = Wm + dd;
+  int* flag = reinterpret_cast<int*>(red + 2);
+  for (int j = blockIdx.x * gpb + gid; j < C * nad; j += gridDim.x * gpb) {
+    const int c = j / nad, k = j % nad;
+    const double* src = k == 0 ? tg.P0 : tg.Q + (size_t)(k - 1) * dd;
+    const double h = delta[c] / 2.0;
+    for (int i = g.lane; i < dd; i += g.size) {
+      pc[i] = src[i];
+      S[i] = src[i] + (i / d == i % d ? h * 1.0 : 0.0);
+      X[i] = src[i];
+    }
+    g.sync();
+    int st = g_factor_psd(g, d, S, L, Wm, flag, red);  // solve_spd (gauss.cpp:87-89)
+    g_llt_solve(g, d, L, d, X);
+    g.sync();
+    for (int i = g.lane; i < dd; i += g.size) {
+      A[i] = X[(i % d) * d + i / d];                         // gain
+      Wm[i] = (i / d == i % d ? 1.0 : 0.0) - X[(i % d) * d + i / d];  // a = I - gain
+    }
+    g.sync();
+    g_mm(g, d, d, d, Wm, pc, X);       // a pc
+    g.sync();
+    g_mm_nt(g, d, d, d, X, Wm, S);     // (a pc) a^T
+    g.sync();
+    g_mm_nt(g, d, d, d, A, A, X);      // gain gain^T
+    g.sync();
+    for (int i = g.lane; i < dd; i += g.size) S[i] = S[i] + h * X[i];
+    g.sync();
+    g_symm(g, d, S);                   // Gaussian ctor (gauss.cpp:38-42)
+    g.sync();
+    st |= g_chol_psd(g, d, S, L, Wm, flag, red);
+    double* out = adf + (size_t)j * (2 * dd + 1);
+    for (int i = g.lane; i < dd; i += g.size) {
+      out[i] = A[i];
+      out[dd + i] = L[i];
+    }
+    if (g.lane == 0) {
+      double ld = 0.0;
+      for (int i = 0; i < d; ++i) ld += log(L[i * d + i]);
+      out[2 * dd] = ld;
+      if (st) atomicOr(bad + c, 1);
+    }
+    g.sync();
+  }
+}
+
+// mean of the prior / fully adapted proposal of step t given the parent
+// (fkpg.cpp:154-185); also returns its factor and log-determinant.
+__device__ __forceinline__ void parent_proposal(const DevTarget& tg, const FactorRef& f,
+                                                const PgArgs& a, int c, int t, const double* parent,
+                                                const double* mq_t, double* mean, const double** Lp,
+                                                double* ldp) {
+  const int d = tg.dx;
+  for (int k = 0; k < d; ++k) mean[k] = t == 0 ? tg.m0[k] : dyn_mean_i(tg, t - 1, parent, k);
+  const int cls = prop_class(f, t);
+  if (a.mode == AUXMC_PG_PRIOR) {
+    *Lp = f.L(cls);  // factor list: 0 = P0, 1 + j = Q_j
+    *ldp = f.logdet[cls];
+    return;
+  }
+  const double* ad = a.adf + ((size_t)c * a.nad + cls) * (2 * d * d + 1);
+  double z[64];
+  for (int k = 0; k < d; ++k) z[k] = mq_t[k] - mean[k];
+  for (int k = 0; k < d; ++k) {
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) s += ad[k * d + j] * z[j];
+    mean[k] = mean[k] + s;
+  }
+  *Lp = ad + d * d;
+  *ldp = ad[2 * d * d];
+}
 
 // ---------------------------------------------------------------- K6 reference cSMC
 __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
@@ -261,9 +360,14 @@ __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
   const double* uc = a.u + (size_t)c * (T + 1) * d;
   const double* mqc = a.mq + (size_t)c * (T + 1) * d;
   const double* ref = a.x + (size_t)c * (T + 1) * d;
-  double r[64], xv[64];
-  if (a.grad_bad && a.grad_bad[c]) {  // non-finite proposal mean: treat as degenerate
+  double r[64], xv[64], pmean[64];
+  if (a.mode != AUXMC_PG_PRIOR && a.grad_bad && a.grad_bad[c]) {
+    // non-finite proposal mean: treat as degenerate
     if (threadIdx.x == 0) { a.status[c] = AUXMC_E_DEGENERATE; a.bad_t[c] = 0; }
+    return;
+  }
+  if (a.mode == AUXMC_PG_ADAPTED && a.ad_bad && a.ad_bad[c]) {  // solve_spd / chol failed
+    if (threadIdx.x == 0) { a.status[c] = AUXMC_E_FACTOR; a.bad_t[c] = 0; }
     return;
   }
   for (int t = 0; t <= T; ++t) {
@@ -277,6 +381,36 @@ __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
     }
     const uint64_t kp = derive_label(st, kParticle);
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const double* parent = t > 0 ? P + ((size_t)(t - 1) * N + anc[i]) * d : nullptr;
+      if (a.mode != AUXMC_PG_GRADIENT) {
+        // prior / fully adapted: the proposal depends on the parent (fkpg.cpp:154-185)
+        const double* Lp;
+        double ldp;
+        parent_proposal(tg, f, a, c, t, parent, mqc + (size_t)t * d, pmean, &Lp, &ldp);
+        if (i == 0) {
+          for (int k = 0; k < d; ++k) xv[k] = ref[(size_t)t * d + k];
+        } else {
+          const uint64_t pk = derive_index(kp, (uint64_t)i);
+          double xi[64];
+          for (int k = 0; k < d; ++k) xi[k] = normal_at(pk, (uint64_t)k);
+          for (int k = 0; k < d; ++k) {  // mean + L xi (gauss.cpp:64-67)
+            double s = 0.0;
+            for (int j = 0; j <= k; ++j) s += Lp[k * d + j] * xi[j];
+            xv[k] = pmean[k] + s;
+          }
+        }
+        for (int k = 0; k < d; ++k) P[((size_t)t * N + i) * d + k] = xv[k];
+        // pot (fkpg.cpp:212-223)
+        double lg = log_pot_dev(tg, f, t, xv, r) + iso_dev(d, uc + (size_t)t * d, xv, delta / 2.0);
+        if (a.mode == AUXMC_PG_ADAPTED) {
+          const double ld = t == 0 ? log_prior_dev(tg, f, xv, r) : log_dyn_dev(tg, f, t - 1, parent, xv, r);
+          for (int k = 0; k < d; ++k) r[k] = xv[k] - pmean[k];
+          lg += ld - gauss_term(d, r, Lp, ldp);
+        }
+        logw[i] = lg;
+        if (a.anc) a.anc[((size_t)c * (T + 1) + t) * N + i] = t > 0 ? anc[i] : 0;
+        continue;
+      }
       if (i == 0) {
         for (int k = 0; k < d; ++k) xv[k] = ref[(size_t)t * d + k];
       } else {
@@ -284,7 +418,6 @@ __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
         for (int k = 0; k < d; ++k) xv[k] = mqc[(size_t)t * d + k] + sq2 * normal_at(pk, (uint64_t)k);
       }
       for (int k = 0; k < d; ++k) P[((size_t)t * N + i) * d + k] = xv[k];
-      const double* parent = t > 0 ? P + ((size_t)(t - 1) * N + anc[i]) * d : nullptr;
       logw[i] = potential_dev(tg, f, t, parent, xv, uc + (size_t)t * d, mqc + (size_t)t * d, delta,
                               sq2, r);
       if (a.anc) a.anc[((size_t)c * (T + 1) + t) * N + i] = t > 0 ? anc[i] : 0;
@@ -323,6 +456,19 @@ __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
     const double mlp = log_q_dev(d, chosen, mq1, sq2);
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       const double* xi = P + ((size_t)t * N + i) * d;
+      if (a.mode != AUXMC_PG_GRADIENT) {
+        // log W + m_logpdf(t+1, x_t^i, chosen) + log_g(t+1, x_t^i, chosen) (fkpg.cpp:137-143)
+        const double* Lp;
+        double ldp;
+        parent_proposal(tg, f, a, c, t + 1, xi, mq1, pmean, &Lp, &ldp);
+        for (int k = 0; k < d; ++k) r[k] = chosen[k] - pmean[k];
+        const double lq = gauss_term(d, r, Lp, ldp);
+        double lg = log_pot_dev(tg, f, t + 1, chosen, r) +
+                    iso_dev(d, uc + (size_t)(t + 1) * d, chosen, delta / 2.0);
+        if (a.mode == AUXMC_PG_ADAPTED) lg += log_dyn_dev(tg, f, t, xi, chosen, r) - lq;
+        logw[i] = log(Wg[(size_t)t * N + i]) + lq + lg;
+        continue;
+      }
       const double lg = potential_dev(tg, f, t + 1, xi, chosen, uc + (size_t)(t + 1) * d, mq1,
                                       delta, sq2, r);
       logw[i] = log(Wg[(size_t)t * N + i]) + mlp + lg;
@@ -666,7 +812,7 @@ __global__ void k_pg_adapt(int C, const long long* iter, const double* last_upda
   delta[c] = exp(log(delta[c]) + pow(n, -0.6) * (last_update[c] - target));
 }
 
-static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int variant, Arena& ws,
+static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int mode, int variant, Arena& ws,
                    cudaStream_t s) {
   const int C = ch->C, N = ch->N, T = tg.T, d = tg.dx;
   const FactorLayout fl = factor_layout(tg);
@@ -681,7 +827,12 @@ static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int variant, Arena&
   double* Ls = ws.take<double>((size_t)fl.total() * fl.W * fl.W);
   double* logdet = ws.take<double>(fl.total());
   int* ints = ws.take<int>((size_t)C + 1);
+  const int nad = 1 + fl.nQ;  // proposal classes: P0, then each Q_j
+  double* adf = mode == AUXMC_PG_ADAPTED ? ws.take<double>((size_t)C * nad * (2 * d * d + 1))
+                                         : nullptr;
+  int* ad_bad = mode == AUXMC_PG_ADAPTED ? ws.take<int>((size_t)C) : nullptr;
   if (ws.base == nullptr) return AUXMC_OK;
+  if (mode == AUXMC_PG_ADAPTED && (!adf || !ad_bad)) return AUXMC_E_WORKSPACE;
   if (!it || !u || !mq || !part || !Wt || !traj || !tkeys || !Ls || !logdet || !ints ||
       (variant == AUXMC_CSMC_PIT && !lw))
     return AUXMC_E_WORKSPACE;
@@ -697,8 +848,17 @@ static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int variant, Arena&
   const long long nct = (long long)C * (T + 1);
   AUXMC_LAUNCH(k_pg_prop_mean, (int)std::min<long long>((nct + 127) / 128, 148LL * 32), 128, 0, s,
                tg, f, C, u, ch->delta, mq, ints);
+  if (mode == AUXMC_PG_ADAPTED) {
+    AUXMC_CUDA_TRY(cudaMemsetAsync(ad_bad, 0, sizeof(int) * C, s));
+    const size_t per = sizeof(double) * (6 * d * d + 4);
+    const int warps = (int)std::max<size_t>(1, std::min<size_t>(4, (200u << 10) / per));
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pg_adapted, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(per * warps)));
+    AUXMC_LAUNCH(k_pg_adapted, (C * nad + warps - 1) / warps, 32 * warps, per * warps, s, tg, C, nad,
+                 ch->delta, adf, ad_bad);
+  }
   PgArgs a{C, N, ch->x, ch->keys, ch->delta, it, u, mq, part, Wt, traj, tkeys, ch->status,
-           ch->bad_t, ch->ancestors, ch->selected, ints};
+           ch->bad_t, ch->ancestors, ch->selected, ints, mode, adf, nad, ad_bad};
   const int threads = N >= 256 ? 256 : ((N + 31) / 32) * 32;
   if (variant == AUXMC_CSMC_REFERENCE) {
     const size_t smem = sizeof(double) * (3 * N + 40 + 64) + sizeof(int) * N;
@@ -746,7 +906,7 @@ size_t auxmc_aux_pgibbs_workspace(const auxmc_target* target, int C, int N, int 
   auxmc_pg_chains ch{};
   ch.C = C;
   ch.N = N;
-  pg_step(to_dev_target(*target), &ch, variant, ws, nullptr);
+  pg_step(to_dev_target(*target), &ch, AUXMC_PG_ADAPTED, variant, ws, nullptr);  // largest mode
   return ws.used + 4096;
 }
 
@@ -755,8 +915,10 @@ int auxmc_aux_pgibbs_step(const auxmc_target* target, auxmc_pg_chains* chains, i
   if (!device_ok()) return AUXMC_E_CUDA;
   int st = check_target(target);
   if (st) return st;
-  if (mode != AUXMC_PG_GRADIENT) return AUXMC_E_ARG;  // prior / fully adapted: see DESIGN.md
+  if (mode < AUXMC_PG_PRIOR || mode > AUXMC_PG_ADAPTED) return AUXMC_E_ARG;
   if (variant != AUXMC_CSMC_REFERENCE && variant != AUXMC_CSMC_PIT) return AUXMC_E_ARG;
+  // the PIT lattice needs parent-free (independent) proposals: gradient mode only
+  if (variant == AUXMC_CSMC_PIT && mode != AUXMC_PG_GRADIENT) return AUXMC_E_ARG;
   if (!chains || chains->C < 0 || chains->N < 1 || chains->N > 4096 || !chains->x ||
       !chains->keys || !chains->delta || !chains->iter || !chains->updates ||
       !chains->last_update || !chains->root_keys || !chains->status || !chains->bad_t)
@@ -764,7 +926,7 @@ int auxmc_aux_pgibbs_step(const auxmc_target* target, auxmc_pg_chains* chains, i
   if (chains->C == 0) return AUXMC_OK;
   if (!workspace) return AUXMC_E_WORKSPACE;
   Arena ws{(char*)workspace, workspace_bytes, 0};
-  return pg_step(to_dev_target(*target), chains, variant, ws, (cudaStream_t)stream);
+  return pg_step(to_dev_target(*target), chains, mode, variant, ws, (cudaStream_t)stream);
 }
 
 int auxmc_pg_adapt_delta(auxmc_pg_chains* chains, double target_rate, void* stream) {

@@ -2,11 +2,12 @@
 
 `PGChains` holds C particle-Gibbs states (PGState, fkpg.hpp:92-99) in HBM.
 `aux_pgibbs_step` runs one sweep for every chain (fkpg.cpp:260-274) with the
-gradient proposal linearized at the auxiliary observation, in one of two
-variants:
+proposal mode of PgOptions (prior, gradient or fully adapted, linearized at the
+auxiliary observation; fkpg.cpp:154-185), in one of two variants:
   Variant.kReference — the reference conditional SMC (multinomial resampling,
                        backward index sampling; fkpg.cpp:44-152);
-  Variant.kPit       — parallel-in-time cSMC with independent proposals.
+  Variant.kPit       — parallel-in-time cSMC with independent proposals
+                       (gradient mode only: the lattice needs parent-free proposals).
 """
 from __future__ import annotations
 

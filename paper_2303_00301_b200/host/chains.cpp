@@ -317,16 +317,22 @@ PGChains::PGChains(PGChains&&) noexcept = default;
 
 void PGChains::aux_pgibbs_step(const PgOptions& opts) {
   Impl& m = *impl_;
-  if (opts.mode != ProposalMode::kGradient || opts.linearize != LinearizeAt::kAuxObs)
-    throw ConfigError("aux_pgibbs_step: the device path implements the gradient proposal "
-                      "linearized at the auxiliary observation (fkpg.cpp:166-171)");
+  if (opts.linearize != LinearizeAt::kAuxObs)
+    throw ConfigError("aux_pgibbs_step: the device path linearizes at the auxiliary "
+                      "observation (LinearizeAt::kAuxObs, fkpg.cpp:166-171)");
+  if (opts.variant == Variant::kPit && opts.mode != ProposalMode::kGradient)
+    throw ConfigError("aux_pgibbs_step: the parallel-in-time cSMC needs parent-free "
+                      "(gradient) proposals");
   const auxmc_target& t = m.target.device();
   const int variant = opts.variant == Variant::kPit ? AUXMC_CSMC_PIT : AUXMC_CSMC_REFERENCE;
   if (variant != m.variant) {
     m.wsb = auxmc_aux_pgibbs_workspace(&t, m.C, m.N, variant);
     m.variant = variant;
   }
-  check_status(auxmc_aux_pgibbs_step(&t, &m.desc, AUXMC_PG_GRADIENT, variant, m.ws.get(m.wsb),
+  const int mode = opts.mode == ProposalMode::kPrior      ? AUXMC_PG_PRIOR
+                   : opts.mode == ProposalMode::kGradient ? AUXMC_PG_GRADIENT
+                                                          : AUXMC_PG_ADAPTED;
+  check_status(auxmc_aux_pgibbs_step(&t, &m.desc, mode, variant, m.ws.get(m.wsb),
                                      m.wsb, nullptr),
                "aux_pgibbs_step");
   std::vector<int> st(m.C), bt(m.C);
@@ -454,7 +460,10 @@ using clk = std::chrono::steady_clock;
 bool is_aux_family(const std::string& s) {
   return s == "aux-kalman-seq" || s == "aux-kalman-prefix" || s == "aux-kalman-dnc";
 }
-bool is_pgibbs_family(const std::string& s) { return s == "pgibbs-gradient" || s == "pgibbs-pit"; }
+bool is_pgibbs_family(const std::string& s) {
+  return s == "pgibbs-prior" || s == "pgibbs-gradient" || s == "pgibbs-adapted" ||
+         s == "pgibbs-pit";
+}
 
 static auxk::Backend backend_of(const std::string& s) {  // runner.cpp:31-36
   if (s == "aux-kalman-seq") return auxk::Backend::kSequential;
@@ -569,6 +578,8 @@ RunResult run(const RunConfig& cfg_in) {
   } else {
     fkpg::PgOptions opts;
     opts.variant = cfg.sampler == "pgibbs-pit" ? fkpg::Variant::kPit : fkpg::Variant::kReference;
+    if (cfg.sampler == "pgibbs-prior") opts.mode = fkpg::ProposalMode::kPrior;  // runner.cpp:38-43
+    if (cfg.sampler == "pgibbs-adapted") opts.mode = fkpg::ProposalMode::kFullyAdapted;
     fkpg::PGChains ch =
         fkpg::PGChains::seeded(target, x0, cfg.delta_init, cfg.seed, C, cfg.particles);
     std::vector<long> mark(C, 0);

@@ -341,6 +341,34 @@ static void gpu_tests() {
     ao_pg_free(&op);
   });
 
+  for (const auto mode : {fkpg::ProposalMode::kPrior, fkpg::ProposalMode::kFullyAdapted}) {
+    const std::string name = std::string("fkpg::aux_pgibbs_step ") +
+                             (mode == fkpg::ProposalMode::kPrior ? "prior" : "fully adapted") +
+                             " proposals vs oracle, 3 sweeps (fkpg.cpp:154-185)";
+    run_test(name.c_str(), [&] {
+      const int N = 12;
+      const RngStream r = RngStream::from_seed(6).derive(stream::kChain, 1);
+      fkpg::PGState st = fkpg::init_pg(svs.latent, 1.0);
+      ao_pg op{};
+      ao_init_pg(&otg, svs.latent.data(), 1.0, &op);
+      fkpg::PgOptions o;
+      o.mode = mode;
+      for (int i = 0; i < 3; ++i) {
+        fkpg::aux_pgibbs_step(tg, st, N, r, o);
+        int bad = 0;
+        const int s = ao_aux_pgibbs_step(&otg, &op, N, ao_from_key(r.key()),
+                                         mode == fkpg::ProposalMode::kPrior ? AO_PG_PRIOR
+                                                                            : AO_PG_ADAPTED,
+                                         nullptr, nullptr, &bad);
+        EXPECT(s == AO_OK, "oracle status %d", s);
+      }
+      EXPECT(st.updates == op.updates, "updates %ld vs %ld", st.updates, op.updates);
+      EXPECT(rel_err(st.x.data(), op.x, st.x.size()) < 1e-9, "x: %g",
+             rel_err(st.x.data(), op.x, st.x.size()));
+      ao_pg_free(&op);
+    });
+  }
+
   run_test("fkpg::PGChains PIT variant runs and moves every chain", [&] {
     fkpg::PGChains ch = fkpg::PGChains::seeded(tg, svs.latent, 1.0, 5, 3, 32);
     fkpg::PgOptions o;
@@ -349,7 +377,8 @@ static void gpu_tests() {
     for (long u : ch.updates()) EXPECT(u >= 1, "updates %ld", u);
     fkpg::PgOptions prior;
     prior.mode = fkpg::ProposalMode::kPrior;
-    EXPECT(throws<ConfigError>([&] { ch.aux_pgibbs_step(prior); }), "prior mode must throw");
+    prior.variant = fkpg::Variant::kPit;
+    EXPECT(throws<ConfigError>([&] { ch.aux_pgibbs_step(prior); }), "PIT + prior must throw");
   });
 
   run_test("bench::run aux-kalman-prefix, 4 chains, exact target: rate 1, files", [&] {

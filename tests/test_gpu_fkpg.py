@@ -56,6 +56,48 @@ def test_reference_csmc_indices_bit_exact(pg, oracle, kind, kw, N):
     assert np.array_equal(ch.updates.cpu().numpy(), [o.p.updates for o in oc])
 
 
+@pytest.mark.parametrize("mode", [0, 2])  # ProposalMode kPrior, kFullyAdapted
+@pytest.mark.parametrize("kind,kw,N", [("stochvol", dict(dx=3, data_seed=11), 16),
+                                       ("lgssm-synthetic", dict(dx=2, dy=1, data_seed=3), 8),
+                                       ("diffusion-smoothing", dict(data_seed=2), 12)])
+def test_reference_csmc_prior_and_adapted_modes(pg, oracle, kind, kw, N, mode):
+    """Parent-dependent proposals (fkpg.cpp:154-185): the prior N(dyn_mean, Q) and
+    the conjugate fully adapted proposal; ancestors / backward indices exact,
+    paths to 1e-9, adapted deltas equal."""
+    auxk, bm, fkpg = pg
+    T = 20
+    lat, otg, gtg = _targets(oracle, auxk, bm, kind, T, kw)
+    C = 3
+    ch = fkpg.init_pg(gtg, lat, 1.0, 7, C, N, trace=True)
+    oc = [oracle.PGChain(otg, lat, 1.0) for _ in range(C)]
+    root = oracle.from_seed(7)
+    for it in range(3):
+        ch.aux_pgibbs_step(fkpg.Variant.kReference, mode=mode)
+        ch.adapt_delta(0.9)
+        anc = ch.ancestors.cpu().numpy()
+        sel = ch.selected.cpu().numpy()
+        assert int(ch.status.max()) == 0
+        for c in range(C):
+            st, bad, oanc, osel = oc[c].step(N, oracle.derive(root, oracle.L_CHAIN, c), mode,
+                                             trace=True)
+            oc[c].adapt(0.9)
+            assert st == 0
+            assert np.array_equal(anc[c], oanc), f"iter {it} chain {c}: ancestors differ"
+            assert np.array_equal(sel[c], osel), f"iter {it} chain {c}: backward indices differ"
+            assert_close(ch.x[c].cpu().numpy(), oc[c].x, 1e-9, f"iter {it} chain {c} path")
+    assert np.array_equal(ch.updates.cpu().numpy(), [o.p.updates for o in oc])
+    assert_close(ch.delta.cpu().numpy(), [o.p.delta for o in oc], 1e-12, "delta")
+
+
+def test_pit_variant_rejects_parent_dependent_proposals(pg, oracle):
+    auxk, bm, fkpg = pg
+    lat, otg, gtg = _targets(oracle, auxk, bm, "stochvol", 8, dict(dx=3, data_seed=11))
+    ch = fkpg.init_pg(gtg, lat, 1.0, 1, 1, 8)
+    from paper_2303_00301_b200 import _lib
+    with pytest.raises(_lib.AuxmcError):
+        ch.aux_pgibbs_step(fkpg.Variant.kPit, mode=0)
+
+
 def test_reference_csmc_single_particle_identity(pg, oracle):
     """test_fkpg.cpp:113-123: N = 1 returns the reference unchanged."""
     auxk, bm, fkpg = pg

@@ -341,8 +341,10 @@ def test_pgibbs_single_particle_keeps_reference(oracle):
     assert pg.p.updates == 0
 
 
-def test_pgibbs_invariance_small_lgssm(oracle):
-    """runner.cpp:315-336: pgibbs moments agree with the dense posterior (|z| < 4)."""
+@pytest.mark.parametrize("mode", [0, 1, 2])  # kPrior, kGradient, kFullyAdapted
+def test_pgibbs_invariance_small_lgssm(oracle, mode):
+    """runner.cpp:315-336 / acceptance.cpp:204-244: pgibbs moments agree with the
+    dense posterior (|z| < 4.5) in every proposal mode."""
     s = oracle.spec("lgssm-synthetic", T=3, dx=1, dy=1, data_seed=11)
     lat, data = oracle.simulate(s)
     m = oracle.synthetic_lgssm(s)
@@ -352,7 +354,7 @@ def test_pgibbs_invariance_small_lgssm(oracle):
     rng = oracle.from_seed(7)
     draws = []
     for _ in range(3000):
-        pg.step(8, rng)
+        pg.step(8, rng, mode)
         draws.append(pg.x[:, 0].copy())
     draws = np.array(draws)
     # batch-means standard error
