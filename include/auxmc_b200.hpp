@@ -179,6 +179,15 @@ struct Workspace {
 void synchronize();
 }  // namespace detail
 
+/* ---- gauss.hpp: the Gaussian law type ---- */
+namespace gauss {
+struct Gaussian {
+  Vec mean;
+  Mat cov;
+  int dim() const { return static_cast<int>(mean.size()); }
+};
+}  // namespace gauss
+
 /* ---- lgssm.hpp:19-91 ---- */
 namespace lgssm {
 
@@ -223,6 +232,8 @@ struct FilterResult {
 };
 
 FilterResult kalman_filter(const Model& model, const Mat& obs);
+/* Marginal smoothing distributions N(m_t^s, P_t^s) per t (lgssm.cpp:114-127). */
+std::vector<gauss::Gaussian> rts_smoother(const Model& model, const FilterResult& fr);
 Trajectory backward_sample(const Model& model, const FilterResult& fr, NoiseSource& noise);
 Trajectory backward_sample(const Model& model, const FilterResult& fr, RngStream rng);
 double path_logpdf(const Model& model, const Mat& obs, const Trajectory& traj,
@@ -245,6 +256,12 @@ Trajectory dnc_sample(const lgssm::Model& model, const lgssm::FilterResult& fr,
                       NoiseSource& noise, int workers = 1);
 Trajectory dnc_sample(const lgssm::Model& model, const lgssm::FilterResult& fr,
                       RngStream rng, int workers = 1);
+
+/* Exact induced law over the flattened path (index t*d_x + j), pit.cpp:303-332:
+ * the zero noise and every basis noise vector pushed through the device sampler
+ * as one pre-drawn batch.  Test-scale (memory grows as ((T+1) d_x)^2). */
+gauss::Gaussian extract_affine_law(Sampler which, const lgssm::Model& model,
+                                   const lgssm::FilterResult& fr);
 
 /* Batched pathwise draws (new): C paths from one filter result, path c drawn with
  * StreamNoise(roots[c]) — the C2 workload (one model, many chains).  The filter

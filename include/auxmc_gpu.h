@@ -201,6 +201,28 @@ int auxmc_sample_paths(const auxmc_lgssm* model, const auxmc_filter_result* fr, 
                        void* workspace, size_t workspace_bytes, void* stream);
 size_t auxmc_sample_paths_workspace(const auxmc_lgssm* model, int fr_shared, int B, int sampler);
 
+/* lgssm::rts_smoother (lgssm.cpp:114-127) for B filter results (batch-major):
+ * smoothed marginals mean [B][T+1][dx], cov [B][T+1][dx][dx]; status[B]. */
+int auxmc_rts_smoother(const auxmc_lgssm* model, const auxmc_filter_result* fr, int B,
+                       double* mean, double* cov, int* status, void* workspace,
+                       size_t workspace_bytes, void* stream);
+size_t auxmc_rts_smoother_workspace(const auxmc_lgssm* model, int B);
+
+/* pit::extract_affine_law (pit.cpp:303-332) for sampler 0/1/2 on one filter
+ * result: the exact Gaussian law N(mean, cov) of the sampled path over the flat
+ * index t*dx + j, from the zero noise and every basis noise vector pushed through
+ * the sampler as one pre-drawn batch.  mean [n], cov [n][n], n = (T+1)*dx;
+ * status[0] = the worst sampler status.  Memory grows as n^2 (a test-scale tool,
+ * like the reference's). */
+int auxmc_affine_law(const auxmc_lgssm* model, const auxmc_filter_result* fr, int sampler,
+                     double* mean, double* cov, int* status, void* workspace,
+                     size_t workspace_bytes, void* stream);
+size_t auxmc_affine_law_workspace(const auxmc_lgssm* model, int sampler);
+
+/* testhooks::flip_backward_gain (testhooks.hpp:11): negate every backward gain
+ * (a deliberate bug the law checks must catch, runner.cpp:301-312). */
+int auxmc_test_flip_backward_gain(int on);
+
 /* Host-buffer convenience entry for the reference-facing facade: copies the
  * model, filter result and noise keys to the device, draws B paths and copies
  * them back into traj_host [B][T+1][dx] (pinned or pageable).  All host pointers. */

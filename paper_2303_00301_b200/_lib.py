@@ -131,6 +131,13 @@ SIGNATURES = {
     "auxmc_sample_paths_workspace": (C.c_size_t, [C.POINTER(Lgssm), C.c_int, C.c_int, C.c_int]),
     "auxmc_sample_paths_host": (C.c_int, [C.POINTER(Lgssm), C.POINTER(FilterResult), C.c_int,
                                           VP, C.c_int, C.c_int, VP, VP]),
+    "auxmc_rts_smoother": (C.c_int, [C.POINTER(Lgssm), C.POINTER(FilterResult), C.c_int, VP, VP,
+                                     VP, VP, C.c_size_t, VP]),
+    "auxmc_rts_smoother_workspace": (C.c_size_t, [C.POINTER(Lgssm), C.c_int]),
+    "auxmc_affine_law": (C.c_int, [C.POINTER(Lgssm), C.POINTER(FilterResult), C.c_int, VP, VP,
+                                   VP, VP, C.c_size_t, VP]),
+    "auxmc_affine_law_workspace": (C.c_size_t, [C.POINTER(Lgssm), C.c_int]),
+    "auxmc_test_flip_backward_gain": (C.c_int, [C.c_int]),
     "auxmc_path_logpdf": (C.c_int, [C.POINTER(Lgssm), VP, C.c_int, VP, C.POINTER(FilterResult),
                                     C.c_int, C.c_int, VP, VP, VP]),
     "auxmc_init_chains": (C.c_int, [C.POINTER(Target), C.POINTER(Chains), VP, C.c_size_t, VP]),

@@ -712,3 +712,13 @@ int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int f
 }
 
 }  // namespace auxmc_gpu
+
+extern "C" int auxmc_test_flip_backward_gain(int on) {
+  // testhooks::flip_backward_gain (testhooks.hpp:11): deliberately wrong gains so
+  // the law checks must fail (runner.cpp:301-312)
+  if (!auxmc_gpu::device_ok()) return AUXMC_E_CUDA;
+  const int v = on ? 1 : 0;
+  return cudaMemcpyToSymbol(auxmc_gpu::g_flip_backward_gain, &v, sizeof v) == cudaSuccess
+             ? AUXMC_OK
+             : AUXMC_E_CUDA;
+}

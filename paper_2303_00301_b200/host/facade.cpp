@@ -330,6 +330,33 @@ Trajectory backward_sample(const Model& model, const FilterResult& fr, RngStream
   return backward_sample(model, fr, n);
 }
 
+std::vector<gauss::Gaussian> rts_smoother(const Model& model, const FilterResult& fr) {
+  const int T = model.horizon(), dx = model.dx();
+  const auxmc_lgssm& m = model.device();
+  detail::DeviceFilter dfr(fr, T, dx);
+  DeviceBuffer mean(sizeof(double) * (T + 1) * dx), cov(sizeof(double) * (T + 1) * dx * dx),
+      status(sizeof(int));
+  const size_t wsb = auxmc_rts_smoother_workspace(&m, 1);
+  DeviceBuffer ws(std::max<size_t>(wsb, 1));
+  check_status(auxmc_rts_smoother(&m, &dfr.desc, 1, mean.as<double>(), cov.as<double>(),
+                                  status.as<int>(), ws.get(), wsb, nullptr),
+               "rts_smoother");
+  int st = 0;
+  status.download(&st, sizeof(int));
+  check_status(st, "rts_smoother");
+  std::vector<double> hm((T + 1) * dx), hc((T + 1) * dx * dx);
+  mean.download(hm.data(), hm.size() * sizeof(double));
+  cov.download(hc.data(), hc.size() * sizeof(double));
+  std::vector<gauss::Gaussian> out;
+  for (int t = 0; t <= T; ++t) {
+    gauss::Gaussian g{Vec(hm.begin() + t * dx, hm.begin() + (t + 1) * dx), Mat(dx, dx)};
+    std::memcpy(g.cov.data(), hc.data() + static_cast<size_t>(t) * dx * dx,
+                sizeof(double) * dx * dx);
+    out.push_back(std::move(g));
+  }
+  return out;
+}
+
 double path_logpdf(const Model& model, const Mat& obs, const Trajectory& traj,
                    const FilterResult& fr) {
   const int T = model.horizon(), dx = model.dx();
@@ -380,6 +407,27 @@ Trajectory dnc_sample(const lgssm::Model& model, const lgssm::FilterResult& fr, 
                       int workers) {
   StreamNoise n(rng);
   return dnc_sample(model, fr, n, workers);
+}
+
+gauss::Gaussian extract_affine_law(Sampler which, const lgssm::Model& model,
+                                   const lgssm::FilterResult& fr) {
+  const int T = model.horizon(), dx = model.dx(), n = (T + 1) * dx;
+  const auxmc_lgssm& m = model.device();
+  detail::DeviceFilter dfr(fr, T, dx);
+  const int s = static_cast<int>(which);
+  DeviceBuffer mean(sizeof(double) * n), cov(sizeof(double) * n * n), status(sizeof(int));
+  const size_t wsb = auxmc_affine_law_workspace(&m, s);
+  DeviceBuffer ws(std::max<size_t>(wsb, 1));
+  check_status(auxmc_affine_law(&m, &dfr.desc, s, mean.as<double>(), cov.as<double>(),
+                                status.as<int>(), ws.get(), wsb, nullptr),
+               "extract_affine_law");
+  int st = 0;
+  status.download(&st, sizeof(int));
+  check_status(st, "extract_affine_law");
+  gauss::Gaussian g{Vec(n), Mat(n, n)};
+  mean.download(g.mean.data(), sizeof(double) * n);
+  cov.download(g.cov.data(), sizeof(double) * n * n);
+  return g;
 }
 
 struct PathBatch::Impl {

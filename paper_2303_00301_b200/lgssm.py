@@ -306,3 +306,22 @@ def path_logpdf(model: Model, obs, traj, fr: FilterResult) -> torch.Tensor:
         int(fr.filt_mean.shape[0] == 1), B, out.data_ptr(), status.data_ptr(), _stream()),
         "path_logpdf")
     return out
+
+
+def rts_smoother(model: Model, fr: FilterResult):
+    """lgssm::rts_smoother (lgssm.cpp:114-127): smoothed marginals
+    (mean [B, T+1, dx], cov [B, T+1, dx, dx]) for every filter result in fr."""
+    B = fr.filt_mean.shape[0]
+    dev = model.device
+    mean = torch.empty((B, model.T + 1, model.dx), dtype=torch.float64, device=dev)
+    cov = torch.empty((B, model.T + 1, model.dx, model.dx), dtype=torch.float64, device=dev)
+    status = torch.zeros(B, dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    mr, fr_raw = model.raw(), fr.raw()
+    n = lib.auxmc_rts_smoother_workspace(C.byref(mr), B)
+    ws = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    _lib.check(lib.auxmc_rts_smoother(C.byref(mr), C.byref(fr_raw), B, mean.data_ptr(),
+                                      cov.data_ptr(), status.data_ptr(), ws.data_ptr(), n,
+                                      _stream()), "rts_smoother")
+    _lib.check(int(status.max()), "rts_smoother")
+    return mean, cov

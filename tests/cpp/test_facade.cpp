@@ -210,6 +210,35 @@ static void gpu_tests() {
     });
   }
 
+  run_test("pit::extract_affine_law (all samplers) and rts_smoother vs dense posterior", [&] {
+    bench::ModelSpec small = spec;
+    small.T = 12;
+    const bench::SimResult ss = bench::simulate(small);
+    const lgssm::Model sm = bench::synthetic_lgssm(small);
+    OModel osm(sm);
+    const int n = (small.T + 1) * d;
+    std::vector<double> pm(n), pc(static_cast<size_t>(n) * n);
+    double le = 0.0;
+    EXPECT(ao_dense_oracle(&osm.m, ss.data.data(), 256, pm.data(), pc.data(), &le) == AO_OK,
+           "dense oracle");
+    const lgssm::FilterResult sfr = lgssm::kalman_filter(sm, ss.data);
+    for (const pit::Sampler w : {pit::Sampler::kSequential, pit::Sampler::kPrefix,
+                                 pit::Sampler::kDnc}) {
+      const gauss::Gaussian law = pit::extract_affine_law(w, sm, sfr);
+      EXPECT(rel_err(law.mean.data(), pm.data(), n) < 1e-8, "law mean (sampler %d)", (int)w);
+      EXPECT(rel_err(law.cov.data(), pc.data(), pc.size()) < 1e-8, "law cov (sampler %d)",
+             (int)w);
+    }
+    const std::vector<gauss::Gaussian> sm_marg = lgssm::rts_smoother(sm, sfr);
+    for (int t = 0; t <= small.T; ++t)
+      for (int i = 0; i < d; ++i) {
+        EXPECT(std::fabs(sm_marg[t].mean[i] - pm[t * d + i]) < 1e-8, "rts mean t=%d", t);
+        for (int j = 0; j < d; ++j)
+          EXPECT(std::fabs(sm_marg[t].cov(i, j) - pc[(size_t)(t * d + i) * n + t * d + j]) < 1e-8,
+                 "rts cov t=%d", t);
+      }
+  });
+
   run_test("pit::PathBatch: chain c equals the single-chain prefix_sample", [&] {
     const int C = 5;
     std::vector<RngStream> roots;
