@@ -631,3 +631,47 @@ def pit_csmc_marginals(tg: OTarget, u, delta, particles):
     _check(lib().ao_pit_csmc_marginals(C.byref(tg.raw), _p(u), delta, _p(particles), N,
                                        _p(marg)), "pit_csmc_marginals")
     return marg
+
+
+# ---------------------------------------------------------------- grid HMM oracle
+def _logsumexp(v, axis=None):
+    m = np.max(v, axis=axis, keepdims=True)
+    m = np.where(np.isfinite(m), m, 0.0)
+    return np.squeeze(m, axis=axis) + np.log(np.sum(np.exp(v - m), axis=axis))
+
+
+def grid_hmm_posterior(tg: OTarget, lo: float, hi: float, n: int):
+    """bench::grid_hmm_posterior (grid_hmm.cpp:17-97): smoothing marginals of a
+    1-d target with linear dynamics on an equispaced midpoint grid, exact HMM
+    forward-backward in log space.  Returns (points, marginals, mean, var, log_evidence)."""
+    a = tg.arrays()
+    if a["dx"] != 1 or not a["linear"]:
+        raise ValueError("grid_hmm_posterior: 1-d linear-dynamics targets only")
+    T = tg.T
+    h = (hi - lo) / n
+    logh = np.log(h)
+    pts = lo + (np.arange(n) + 0.5) * h
+    lpot = np.array([[tg.log_pot(t, [p]) for p in pts] for t in range(T + 1)])
+    m0, p0 = a["m0"][0], a["P0"][0]
+    nF = a["nF"]
+
+    def lm(t):  # lm[i, j] = log p(x_{t+1} = pts[j] | x_t = pts[i]) (grid_hmm.cpp:38-47)
+        k = t if nF > 1 else 0
+        f, b, q = a["F"][k], a["b"][k], a["Q"][k]
+        pred = f * pts + b
+        return -0.5 * np.log(2.0 * np.pi * q) - (pts[None, :] - pred[:, None]) ** 2 / (2.0 * q)
+
+    la = np.zeros((T + 1, n))
+    lb = np.zeros((T + 1, n))
+    la[0] = -0.5 * np.log(2.0 * np.pi * p0) - (pts - m0) ** 2 / (2.0 * p0) + lpot[0] + logh
+    for t in range(T):
+        la[t + 1] = _logsumexp(la[t][:, None] + lm(t), axis=0) + lpot[t + 1] + logh
+    log_ev = float(_logsumexp(la[T]))
+    for t in range(T - 1, -1, -1):
+        lb[t] = _logsumexp(lm(t) + (lpot[t + 1] + lb[t + 1])[None, :], axis=1) + logh
+    lg = la + lb
+    lg -= _logsumexp(lg, axis=1)[:, None]
+    marg = np.exp(lg)
+    mean = marg @ pts
+    var = marg @ (pts ** 2) - mean ** 2
+    return pts, marg, mean, var, log_ev

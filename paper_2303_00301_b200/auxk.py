@@ -26,9 +26,8 @@ class Backend:
 
 
 def _t(a, device, dtype=torch.float64):
-    return torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=np.float64 if dtype ==
-                                                           torch.float64 else np.uint8))
-                           ).to(device=device, dtype=dtype).contiguous()
+    host = np.array(a, dtype=np.float64 if dtype == torch.float64 else np.uint8, copy=True)
+    return torch.from_numpy(host).to(device=device, dtype=dtype).contiguous()
 
 
 class GenSSMTarget:

@@ -363,3 +363,18 @@ def test_pgibbs_invariance_small_lgssm(oracle, mode):
     se = bm.std(axis=0, ddof=1) / np.sqrt(nb)
     z = np.abs(draws.mean(axis=0) - mean) / se
     assert np.all(z < 4.5), z
+
+
+def test_grid_hmm_oracle_matches_dense_posterior(oracle):
+    """grid_hmm.cpp:17-97 pinned on a 1-d linear Gaussian model, where the exact
+    posterior is the dense conditioning one (midpoint-grid accuracy)."""
+    s = oracle.spec("lgssm-synthetic", T=6, dx=1, dy=1, data_seed=4)
+    lat, data = oracle.simulate(s)
+    m = oracle.synthetic_lgssm(s)
+    mean, cov, le = oracle.dense_oracle(m, data)
+    tg = oracle.make_target(s, data)
+    _, marg, gmean, gvar, gle = oracle.grid_hmm_posterior(tg, -8.0, 8.0, 1600)
+    assert np.allclose(marg.sum(axis=1), 1.0)
+    assert np.max(np.abs(gmean - mean)) < 1e-4
+    assert np.max(np.abs(gvar - np.diag(cov))) < 1e-4
+    assert abs(gle - le) < 1e-4
