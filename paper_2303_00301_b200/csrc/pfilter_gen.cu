@@ -256,6 +256,77 @@ __device__ __noinline__ void g_combine(const Grp& g, int d, const double* u, con
   else g_combine_t<0>(g, d, u, v, o, s, save_minv);
 }
 
+// (u then v) when u is a prefix from t = 0, whose A is exactly zero (the first
+// element sets A := 0, pit.cpp:151, and A_out = v.A solve(u.A) keeps it zero):
+// b and C depend on (u.b, u.C, v) alone and are formed by exactly the operations
+// g_combine_t uses for them; with u.A = 0 the full combine's other outputs reduce
+// to A = 0, eta = 0 + u.eta, J = symm(0 + u.J), written directly.  The output is
+// bit-identical to g_combine_t's, at 4 instead of 9 d^3 products.
+template <int DC>
+__device__ __forceinline__ void g_combine_bc_t(const Grp& g, int d_rt, const double* u,
+                                               const double* v, double* o,
+                                               const CombScratch& s) {
+  const int d = DC ? DC : d_rt;
+  const int dd = d * d;
+  const double *ub = u + dd, *uC = u + dd + d, *ueta = u + 2 * dd + d, *uJ = u + 2 * dd + 2 * d;
+  const double *vA = v, *vb = v + dd, *vC = v + dd + d, *veta = v + 2 * dd + d,
+               *vJ = v + 2 * dd + 2 * d;
+  double *oA = o, *ob = o + dd, *oC = o + dd + d, *oeta = o + 2 * dd + d, *oJ = o + 2 * dd + 2 * d;
+  double* const M1 = oC;
+  double* Minv = oJ;
+  g_mm(g, d, d, d, uC, vJ, M1);
+  g_eye(g, d, s.T2);
+  g.sync();
+  for (int i = g.lane; i < d; i += g.size) M1[i * d + i] += 1.0;
+  g.sync();
+  if (!g.block && d <= 16) {
+    w_inverse_gj_t<DC>(g.lane, d, M1, Minv);
+  } else {
+    g_lu_factor(g, d, M1, s.p1, s.idx);
+    g_lu_solve(g, d, M1, s.p1, d, s.T2, Minv);
+  }
+  for (int i = g.lane; i < d; i += g.size) {
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) acc += uC[i * d + k] * veta[k];
+    s.t[i] = acc + ub[i];
+  }
+  g.sync();
+  g_mm(g, d, d, d, Minv, uC, s.T1);
+  double* mt = M1;
+  for (int i = g.lane; i < d; i += g.size) {
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) acc += Minv[i * d + k] * s.t[k];
+    mt[i] = acc;
+  }
+  g.sync();
+  for (int i = g.lane; i < d; i += g.size) {
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) acc += vA[i * d + k] * mt[k];
+    ob[i] = acc + vb[i];
+    oeta[i] = 0.0 + ueta[i];
+  }
+  g_mm(g, d, d, d, vA, s.T1, Minv);  // Minv consumed
+  g.sync();
+  g_mm_nt(g, d, d, d, Minv, vA, s.T1, vC);
+  g.sync();
+  for (int i = g.ty(); i < d; i += g.ny())
+    for (int j = g.tx(); j < d; j += 16) {
+      oC[i * d + j] = 0.5 * (s.T1[i * d + j] + s.T1[j * d + i]);
+      oA[i * d + j] = 0.0;
+    }
+  g.sync();  // oJ held Minv until the last product
+  for (int i = g.ty(); i < d; i += g.ny())
+    for (int j = g.tx(); j < d; j += 16)
+      oJ[i * d + j] = 0.5 * ((0.0 + uJ[i * d + j]) + (0.0 + uJ[j * d + i]));
+  g.sync();
+}
+
+__device__ __noinline__ void g_combine_bc(const Grp& g, int d, const double* u, const double* v,
+                                          double* o, const CombScratch& s) {
+  if (d == 16) g_combine_bc_t<16>(g, d, u, v, o, s);
+  else g_combine_bc_t<0>(g, d, u, v, o, s);
+}
+
 __host__ __device__ inline int comb_doubles(int d) { return 3 * d * d + 2 * d; }
 __host__ __device__ inline int comb_ints(int d) { return 2 * d + 2; }
 
@@ -685,7 +756,7 @@ __global__ void k_pfg_carry(int T, int d, int B, int LB, const double* __restric
     g.sync();
     for (int k = 1; k < nblk; ++k) {
       g_copy(g, ES, acc, carry + ((size_t)b * nblk + k) * ES);
-      g_combine(g, d, acc, agg + ((size_t)b * nblk + k) * ES, o, cs);
+      g_combine_bc(g, d, acc, agg + ((size_t)b * nblk + k) * ES, o, cs);  // prefixes
       g_copy(g, ES, o, acc);
       g.sync();
     }
@@ -726,7 +797,7 @@ __global__ void k_pfg_carry_seg(int nblk, int d, int B, int LB2, const double* _
     for (; k < hi; ++k) {
       g_copy(g, ES, acc, Cy + (size_t)k * ES);
       if (k + 1 < hi) {
-        g_combine(g, d, acc, A + (size_t)k * ES, o, cs);
+        g_combine_bc(g, d, acc, A + (size_t)k * ES, o, cs);  // prefixes
         g_copy(g, ES, o, acc);
       }
       g.sync();
@@ -759,7 +830,7 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
     } else {
       g_copy(g, ES, carry + (size_t)q * ES, cy);
       g.sync();
-      g_combine(g, d, cy, base + (size_t)lo * ES, acc, cs);
+      g_combine_bc(g, d, cy, base + (size_t)lo * ES, acc, cs);  // carries are prefixes
     }
     for (int t = lo;; ++t) {
       for (int i = g.lane; i < d; i += g.size)
@@ -767,7 +838,7 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
       for (int i = g.lane; i < dd; i += g.size)
         filt_cov[((size_t)b * (T + 1) + t) * dd + i] = acc[dd + d + i];
       if (t + 1 >= hi) break;
-      g_combine(g, d, acc, base + (size_t)(t + 1) * ES, o, cs);
+      g_combine_bc(g, d, acc, base + (size_t)(t + 1) * ES, o, cs);
       g_copy(g, ES, o, acc);
       g.sync();
     }
