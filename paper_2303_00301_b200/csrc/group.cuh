@@ -497,8 +497,48 @@ __device__ __forceinline__ bool use_blocked(const Grp& g, int n) { return g.bloc
 // LLT of the lower triangle of A (n×n) into L; Eigen semantics: fail iff a
 // pivot x <= 0 (NaN passes).  Right-looking: the trailing update of column k is
 // spread over the group, so the serial depth is O(n) syncs.
+// One warp, n <= NM: lane i holds row i of the factor in registers; column k's
+// pivot and the L_jk of the trailing update travel by shuffles.  Every lane
+// performs exactly the divisions and fused updates of g_llt's shared-memory
+// loop below in the same order, so the factor is bit-identical — without the
+// two warp barriers and shared round trips per column.  A may alias L.
+template <int NM>
+__device__ __forceinline__ bool w_llt_reg(int lane, int n, const double* A, double* L) {
+  double a[NM];
+#pragma unroll
+  for (int j = 0; j < NM; ++j) a[j] = (lane < n && j < n && j <= lane) ? A[lane * n + j] : 0.0;
+  __syncwarp();
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < NM; ++k) {
+    if (k >= n) break;
+    const double x = __shfl_sync(0xffffffffu, a[k], k);
+    if (x <= 0.0) {  // uniform: every lane holds the same pivot
+      ok = false;
+      break;
+    }
+    const double piv = sqrt(x);
+    if (lane > k && lane < n) a[k] = a[k] / piv;
+#pragma unroll
+    for (int j = k + 1; j < NM; ++j) {
+      if (j >= n) break;
+      const double ljk = __shfl_sync(0xffffffffu, a[k], j);
+      if (lane >= j && lane < n) a[j] -= a[k] * ljk;
+    }
+    if (lane == k) a[k] = piv;
+  }
+  if (ok && lane < n) {
+#pragma unroll
+    for (int j = 0; j < NM; ++j)
+      if (j < n) L[lane * n + j] = j <= lane ? a[j] : 0.0;
+  }
+  __syncwarp();
+  return ok;
+}
+
 __device__ __forceinline__ bool g_llt(const Grp& g, int n, const double* A, double* L,
                                       int* flag) {
+  if (!g.block && n <= 16) return w_llt_reg<16>(g.lane, n, A, L);
   for (int i = g.ty(); i < n; i += g.ny())
     for (int j = g.tx(); j < n; j += 16) L[i * n + j] = j <= i ? A[i * n + j] : 0.0;
   (void)flag;
@@ -690,6 +730,29 @@ __device__ __forceinline__ double g_log_pdf_factored(const Grp& g, int n, const 
     const double v = *red;
     g.sync();
     return v;
+  }
+  if (!g.block && n <= 32) {
+    // one warp: lane j owns r_j; forward substitution by shuffles with the same
+    // operations as g_lower_solve_vec, and the n logs of the diagonal in
+    // parallel, summed in index order (gauss.cpp:51-57) on every lane
+    const int j = g.lane;
+    double r = j < n ? x[j] - mean[j] : 0.0;
+    if (j == 0) r = r / L[0];
+    for (int i = 0; i < n; ++i) {
+      const double ri = __shfl_sync(0xffffffffu, r, i);
+      if (j == i + 1) r = (r - L[j * n + i] * ri) / L[j * n + j];
+      else if (j > i + 1 && j < n) r -= L[j * n + i] * ri;
+    }
+    const double lg = j < n ? log(L[j * n + j]) : 0.0;
+    if (j < n) work[j] = r;
+    double sq = 0.0, ld = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double wi = __shfl_sync(0xffffffffu, r, i);
+      sq += wi * wi;
+    }
+    for (int i = 0; i < n; ++i) ld += __shfl_sync(0xffffffffu, lg, i);
+    __syncwarp();
+    return -0.5 * (n * kLog2Pi + sq) - ld;
   }
   for (int i = g.lane; i < n; i += g.size) work[i] = x[i] - mean[i];
   g.sync();
