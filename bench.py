@@ -170,7 +170,8 @@ def c2_e2e(args, st, steps, warmup, world):
                           backward=pin(noise.backward), bridge=pin(noise.bridge))
     h_out = torch.empty(st["out"].shape, dtype=torch.float64).pin_memory()
     C = st["C"]
-    chunks = 8 if C % 8 == 0 else 1
+    chunks = int(os.environ.get("AUXMC_E2E_CHUNKS", "32"))
+    chunks = chunks if C % chunks == 0 else 1
     pipe = lgssm.HostPipeline(st["model"], C, st["sampler"], chunks)
     h2d = sum(t.numel() * t.element_size() for t in (h_fr.pred_mean, h_fr.pred_cov,
                                                       h_fr.filt_mean, h_fr.filt_cov,
