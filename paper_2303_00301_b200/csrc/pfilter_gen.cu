@@ -853,8 +853,9 @@ __host__ __device__ inline int rec_smem(int d, int dy) {
 }
 
 // warp groups per CTA, per kernel: as many as its per-group shared-memory
-// footprint and its register count allow (<= 12) — the combine chains are
-// latency-bound, so occupancy matters
+// footprint and its register count allow (<= 16; 12 -> 16 took the C5 iteration
+// 200 -> 196 ms, 20/24 no further) — the combine chains are latency-bound, so
+// occupancy matters
 struct KCfg {
   int gp, threads;
   size_t smem;
@@ -869,7 +870,7 @@ KCfg kcfg(K kernel, int d, int dy, int per_doubles) {
   if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess && fa.numRegs > 0) regs = fa.numRegs;
   const int by_regs = 65536 / (32 * ((regs + 7) / 8 * 8));
   const int gp = (int)std::max<size_t>(
-      1, std::min<size_t>({(size_t)12, (size_t)by_regs, (220 * 1024) / per}));
+      1, std::min<size_t>({(size_t)16, (size_t)by_regs, (220 * 1024) / per}));
   return KCfg{gp, 32 * gp, per * gp};
 }
 inline int kgrid(const KCfg& c, long long k) {
