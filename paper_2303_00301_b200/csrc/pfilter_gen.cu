@@ -866,9 +866,12 @@ KCfg kcfg(K kernel, int d, int dy, int per_doubles) {
   const size_t per = sizeof(double) * (size_t)per_doubles;
   if (c.block) return KCfg{1, c.threads, per};
   cudaFuncAttributes fa{};
-  int regs = 128;
-  if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess && fa.numRegs > 0) regs = fa.numRegs;
-  const int by_regs = 65536 / (32 * ((regs + 7) / 8 * 8));
+  int regs = 128, max_warps = 32;
+  if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess && fa.numRegs > 0) {
+    regs = fa.numRegs;
+    max_warps = fa.maxThreadsPerBlock / 32;  // the driver's per-block resource bound
+  }
+  const int by_regs = std::min(max_warps, 65536 / (32 * ((regs + 7) / 8 * 8)));
   const int gp = (int)std::max<size_t>(
       1, std::min<size_t>({(size_t)16, (size_t)by_regs, (220 * 1024) / per}));
   return KCfg{gp, 32 * gp, per * gp};
