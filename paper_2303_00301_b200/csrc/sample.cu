@@ -23,36 +23,48 @@ namespace auxmc_gpu {
 __device__ int g_flip_backward_gain = 0;  // testhooks::flip_backward_gain (testhooks.hpp:11)
 
 // ---------------------------------------------------------------- elements
-// smem per group: 9 d*d + 4 d doubles + 2 ints
+// smem per group: bwd_buffers(f_smem) d*d matrices + 4 d doubles + 2 ints.  Five
+// d*d buffers rotate through the step (liveness below); the sixth holds F when
+// f_smem, else F is read from global memory (L1-resident: the same d*d block is
+// read by every product).  The operation sequence is the same either way, so the
+// elements are bit-identical to the eight-buffer layout; fewer buffers put three
+// d = 40 items on an SM instead of two.
+__host__ __device__ constexpr int bwd_buffers(bool f_smem) { return f_smem ? 6 : 5; }
 __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel& m, int t,
                                                    const double* fm, const double* fc,
                                                    const double* pc, double* sm, int* flag,
                                                    double* out /* G | off | L (or Λ) */, int k,
-                                                   int store_cov) {
+                                                   int store_cov, bool f_smem) {
   const int d = m.dx, dd = d * d;
-  double* P = sm;
-  double* F = P + dd;
-  double* S = F + dd;
-  double* X = S + dd;   // cross, then solve rhs/result
-  double* L = X + dd;
-  double* A = L + dd;
-  double* W = A + dd;
-  double* G = W + dd;
-  double* v = G + dd;  // factor scratch (jitter matrix / inverted diagonal blocks): X, then S
+  double* B0 = sm;         // P; then G Q G^T; then factor scratch
+  double* B1 = B0 + dd;    // S (predicted covariance); then G
+  double* B2 = B1 + dd;    // cross; factor scratch (jitter matrix / inverted blocks); then Λ
+  double* B3 = B2 + dd;    // L (factor of S); then A = I - G F; then Q
+  double* B4 = B3 + dd;    // solve rhs/result; then products; then chol(Λ)
+  double* v = B4 + (f_smem ? 2 : 1) * dd;
   double* red = v + 2 * d;
-  const double* Ft = m.Ft(t, k);
+  const double* F = m.Ft(t, k);
+  if (f_smem) {
+    g_copy(g, dd, F, B4 + dd);
+    F = B4 + dd;
+  }
+  double* P = B0;
+  double* S = B1;
+  double* X = B2;
+  double* L = B3;
+  double* W = B4;
   g_copy(g, dd, fc + (size_t)t * dd, P);
-  g_copy(g, dd, Ft, F);
   g_copy(g, dd, pc + (size_t)(t + 1) * dd, S);
   g.sync();
   g_mm_nt(g, d, d, d, P, F, X);  // cross = P F^T
   g.sync();
+  double* G = B1;  // S is dead once the gain is solved
   int st = 0;
   if (g_all_zero(g, dd, X, flag)) {
     g_zero(g, dd, G);
     g.sync();
   } else {
-    // rhs = cross^T (into W), X := S^{-1} cross^T, G = X^T
+    // rhs = cross^T (into W), W := S^{-1} cross^T, G = W^T
     for (int i = g.lane; i < dd; i += g.size) W[i] = X[(i % d) * d + i / d];
     g.sync();
     st = g_factor_psd(g, d, S, L, X, flag, red);  // X (cross) is consumed
@@ -80,6 +92,7 @@ __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel&
     v[d + i] = mt[i] - s;
   }
   // A = I - G F
+  double* A = B3;
   g_mm(g, d, d, d, G, F, A);
   g.sync();
   for (int i = g.lane; i < dd; i += g.size) A[i] = (i / d == i % d ? 1.0 : 0.0) - A[i];
@@ -89,9 +102,10 @@ __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel&
   g.sync();
   g_mm_nt(g, d, d, d, W, A, X);  // X = A P A^T
   g.sync();
-  g_copy(g, dd, m.Qt(t, k), S);
+  double* Q = B3;
+  g_copy(g, dd, m.Qt(t, k), Q);
   g.sync();
-  g_mm(g, d, d, d, G, S, W);
+  g_mm(g, d, d, d, G, Q, W);
   g.sync();
   g_mm_nt(g, d, d, d, W, G, P);  // P = G Q G^T
   g.sync();
@@ -99,13 +113,14 @@ __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel&
   g.sync();
   g_symm(g, d, X);
   g.sync();
+  double* Lam = B4;
   if (!store_cov) {
-    st = g_chol_psd(g, d, X, L, S, flag, red);  // S (Q) is consumed
+    st = g_chol_psd(g, d, X, Lam, P, flag, red);  // P (G Q G^T) is consumed
     if (st) return st;
   }
   for (int i = g.lane; i < dd; i += g.size) {
     out[i] = G[i];
-    out[dd + d + i] = store_cov ? X[i] : L[i];
+    out[dd + d + i] = store_cov ? X[i] : Lam[i];
   }
   for (int i = g.lane; i < d; i += g.size) out[dd + i] = v[d + i];
   g.sync();
@@ -121,7 +136,7 @@ __global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
   extern __shared__ double smem[];
   const int d = m.dx, dd = d * d;
   const int T = m.T;
-  const int per = 8 * dd + 4 * d + 4;
+  const int per = bwd_buffers(!BLOCK) * dd + 4 * d + 4;
   Grp g = BLOCK ? block_group() : warp_group();
   const int gid = BLOCK ? 0 : (threadIdx.x >> 5);
   const int groups_per_block = BLOCK ? 1 : (blockDim.x >> 5);
@@ -150,7 +165,7 @@ __global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
       for (int i = g.lane; i < dd; i += g.size) out[d + i] = L[i];
     } else {
       st = backward_step_group(g, m, t, fm, fc, pc, sm, flag,
-                               elems + ((size_t)b * T + t) * elem_stride(d), b, store_cov);
+                               elems + ((size_t)b * T + t) * elem_stride(d), b, store_cov, !BLOCK);
     }
     if (st && g.lane == 0) atomicMax(status + b, st);
     g.sync();
@@ -625,7 +640,8 @@ int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, 
                         int Bfr, double* elems, double* term, int* st_fr, int store_cov,
                         cudaStream_t stream, int t_lo = 0, int t_hi = -1) {
   const int d = dm.dx;
-  const int per = 8 * d * d + 4 * d + 4;
+  const int per_blk = bwd_buffers(false) * d * d + 4 * d + 4;  // CTA items: F from global
+  const int per = bwd_buffers(true) * d * d + 4 * d + 4;       // warp items: F staged
   if (t_hi < 0) t_hi = dm.T + 1;
   if (t_hi <= t_lo) return AUXMC_OK;
   const long long n_items = (long long)Bfr * (t_hi - t_lo);
@@ -641,7 +657,7 @@ int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, 
 #undef CASE
     }
   } else if (d > 16) {
-    const size_t smem = sizeof(double) * per;
+    const size_t smem = sizeof(double) * per_blk;
     AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_bwd_elements<true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = (int)std::min<long long>(n_items, 148LL * 64);

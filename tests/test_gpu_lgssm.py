@@ -105,6 +105,25 @@ def test_samplers_large_dims_match_oracle(gpu, oracle, case, sampler):
     assert_close(got.cpu(), want, RTOL, f"sampler {sampler}")
 
 
+@pytest.mark.parametrize("sampler", [0, 1])
+def test_samplers_d64_match_oracle(gpu, oracle, sampler):
+    """d = 64: the backward elements' five-buffer CTA layout (F read from global)
+    fits where the eight-buffer one exceeded shared memory; sequential and
+    blocked prefix samplers against the oracle (DnC stops at d = 60)."""
+    lgssm, pit, _ = gpu
+    m, obs = _oracle_case(oracle, 5, 64, 8, True, False, 42)
+    fr_o = oracle.kalman_filter(m, obs)
+    gm = to_gpu_model(m)
+    fr = lgssm.kalman_filter(gm, obs)
+    assert int(fr.status[0]) == 0
+    B = 2
+    term, back, bridge = predrawn(np.random.default_rng(42), B, m.T, m.dx,
+                                  pit.dnc_bridge_count(m.T))
+    want = _oracle_paths(oracle, sampler, m, fr_o, term, back, bridge)
+    got = lgssm.PathSampler(gm, B, sampler, True)(fr, lgssm.Noise.predrawn(term, back, bridge))
+    assert_close(got.cpu(), want, RTOL, f"sampler {sampler}")
+
+
 def test_kalman_filter_batched_sequences(gpu, oracle):
     lgssm, _, _ = gpu
     m, _ = _oracle_case(oracle, 30, 3, 2, True, True, 11)
