@@ -333,7 +333,12 @@ __device__ __forceinline__ bool w_factor_diag(int lane, int n, int nb, double* D
 #pragma unroll
   for (int j = 0; j < kNB; ++j) {
     if (j < nb) {
+      // the column's unscaled entries travel while the pivot's rsqrt runs; the
+      // receiving lane forms l_kj = a_kj * r itself (the same product lane k forms)
       const double d = __shfl_sync(0xffffffffu, a[j], j);
+      double akj[kNB];
+#pragma unroll
+      for (int k = j + 1; k < kNB; ++k) akj[k] = __shfl_sync(0xffffffffu, a[j], k);
       if (d <= 0.0) {
         ok = false;
         break;
@@ -345,18 +350,24 @@ __device__ __forceinline__ bool w_factor_diag(int lane, int n, int nb, double* D
       else if (i == j) a[j] = piv;
 #pragma unroll
       for (int k = j + 1; k < kNB; ++k) {
-        const double lkj = __shfl_sync(0xffffffffu, a[j], k);
+        const double lkj = akj[k] * r;
         if (k <= i && i > j) a[k] -= a[j] * lkj;
       }
     }
   }
   if (!ok) return false;
+  // rows of L by shuffle (lane r holds row r) before any store: the forward
+  // substitution below runs from registers, no shared-memory round trip
+  double Lr[kNB][kNB];
+#pragma unroll
+  for (int r = 1; r < kNB; ++r)
+#pragma unroll
+    for (int l = 0; l < r; ++l) Lr[r][l] = __shfl_sync(0xffffffffu, a[l], r);
   if (lane < nb) {
 #pragma unroll
     for (int k = 0; k < kNB; ++k)
       if (k <= i) D[i * n + k] = a[k];
   }
-  __syncwarp();
   if (lane < kNB) {  // column `lane` of D^{-1} by forward substitution
     const int j = lane;
     double x[kNB];
@@ -370,7 +381,7 @@ __device__ __forceinline__ bool w_factor_diag(int lane, int n, int nb, double* D
           double s = 0.0;
 #pragma unroll
           for (int l = 0; l < r; ++l)
-            if (l >= j) s += D[r * n + l] * x[l];
+            if (l >= j) s += Lr[r][l] * x[l];
           v = -s * inv[r];
         }
       }
