@@ -176,6 +176,20 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return red[32];
 }
 
+// Sequential running sum of x[0..N) in the reference's left-to-right order.  x
+// and cum are distinct shared arrays (__restrict__): with the loop unrolled by 8
+// the loads of a group issue ahead of its dependent adds and stores, instead of
+// one load-after-store round trip per element.
+__device__ __forceinline__ void serial_cumsum(int N, const double* __restrict__ x,
+                                              double* __restrict__ cum) {
+  double acc = 0.0;
+#pragma unroll 8
+  for (int i = 0; i < N; ++i) {
+    acc += x[i];
+    cum[i] = acc;
+  }
+}
+
 // normalize (fkpg.cpp:19-27) over logw[0..N) in shared memory -> W (shared),
 // sequential sum as the reference's order; returns false if degenerate.
 __device__ __forceinline__ bool block_normalize(int N, const double* logw, double* W, double* red) {
@@ -191,6 +205,7 @@ __device__ __forceinline__ bool block_normalize(int N, const double* logw, doubl
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
+#pragma unroll 8
     for (int i = 0; i < N; ++i) s += W[i];
     red[33] = s;
   }
@@ -203,13 +218,7 @@ __device__ __forceinline__ bool block_normalize(int N, const double* logw, doubl
 
 // cumulative weights in the reference's sequential order (fkpg.cpp:29-37)
 __device__ __forceinline__ void block_cumsum(int N, const double* W, double* cum) {
-  if (threadIdx.x == 0) {
-    double acc = 0.0;
-    for (int i = 0; i < N; ++i) {
-      acc += W[i];
-      cum[i] = acc;
-    }
-  }
+  if (threadIdx.x == 0) serial_cumsum(N, W, cum);
   __syncthreads();
 }
 
