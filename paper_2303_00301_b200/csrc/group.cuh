@@ -281,6 +281,32 @@ __device__ __forceinline__ void g_dmma(const Grp& g, int m, int k, int n, const 
         p0 += sb;
         p1 += sb;
       }
+    } else if ((k & 3) == 0) {
+      // edge tiles with a whole k range: the interior pointer walks, with the
+      // out-of-range rows / columns predicated to zero (the guarded loop's values)
+      const bool ra = r < m, rb0 = b0 < n, rb1 = two && b1 < n;
+      const double* pa = TA ? A + ti * lda + r : A + r * lda + ti;
+      const double* p0 = TB ? B + b0 * ldb + ti : B + ti * ldb + b0;
+      const double* p1 = TB ? B + b1 * ldb + ti : B + ti * ldb + b1;
+      const int sa = TA ? 4 * lda : 4, sb = TB ? 4 : 4 * ldb;
+#pragma unroll 2
+      for (int K = 0; K < kt; ++K) {
+        double a = ra ? pa[0] : 0.0;
+        const double x0 = rb0 ? p0[0] : 0.0;
+        a = sg * a;
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+            : "+d"(c00), "+d"(c01)
+            : "d"(a), "d"(x0));
+        if (two) {
+          const double x1 = rb1 ? p1[0] : 0.0;
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(c10), "+d"(c11)
+              : "d"(a), "d"(x1));
+        }
+        pa += sa;
+        p0 += sb;
+        p1 += sb;
+      }
     } else {
       for (int K = 0; K < kt; ++K) {
         const int kk = K * 4 + ti;
