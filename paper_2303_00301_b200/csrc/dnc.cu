@@ -79,6 +79,7 @@ __global__ void k_dnc_compose(int T, int d, int level, int Bfr, const double* __
 
 // Bridge parameters per internal node (pit.cpp:270-291): K (gain), L = chol(cov).
 // Root (h = 1): L = chol_psd(root cov) (pit.cpp:259-263).
+constexpr int kBridgeBuffers = 6;
 template <bool BLOCK>
 __global__ void k_dnc_bridge(int T, int d, int Bfr, const double* __restrict__ nodes,
                              long long n_heap, long long n_first, long long n_last,
@@ -88,16 +89,20 @@ __global__ void k_dnc_bridge(int T, int d, int Bfr, const double* __restrict__ n
   Grp g = BLOCK ? block_group() : warp_group();
   const int gid = BLOCK ? 0 : (threadIdx.x >> 5);
   const int gpb = BLOCK ? 1 : (blockDim.x >> 5);
-  const int per = 8 * dd + 4;
+  const int per = kBridgeBuffers * dd + 4;
   double* sm = smem + (size_t)gid * per;
+  // six d*d buffers rotate with the liveness of the step (same operation
+  // sequence as with one buffer per quantity): B0 cross, then K; B1 s; B2 A, then
+  // the output factor; B3 W; B4 the first factor, then cov; B5 factor scratch
   double* cross = sm;
   double* s = cross + dd;
-  double* K = s + dd;
-  double* A = K + dd;
-  double* cov = A + dd;
-  double* W = cov + dd;
+  double* A = s + dd;
+  double* W = A + dd;
   double* L = W + dd;
   double* scr = L + dd;
+  double* K = cross;  // cross is dead once K = (s^{-1} cross^T)^T is formed
+  double* cov = L;    // the first factor is dead after the solve
+  double* Lc = A;     // A is dead once cov is formed
   double* red = scr + dd;
   int* flag = reinterpret_cast<int*>(red + 2);
   const long long width = n_last - n_first;
@@ -162,10 +167,10 @@ __global__ void k_dnc_bridge(int T, int d, int Bfr, const double* __restrict__ n
     g.sync();
     g_symm(g, d, cov);
     g.sync();
-    st = g_chol_psd(g, d, cov, L, scr, flag, red);
+    st = g_chol_psd(g, d, cov, Lc, scr, flag, red);
     if (st && g.lane == 0) atomicMax(status + b, st);
     g_copy(g, dd, K, out);
-    g_copy(g, dd, L, out + dd);
+    g_copy(g, dd, Lc, out + dd);
     g.sync();
   }
 }
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(kDncSubThreads)
   }
 }
 
-// ---- any d (9..60): warp per (node, chain), lanes over rows; the dot products
+// ---- any d (9..64): warp per (node, chain), lanes over rows; the dot products
 // run in the register kernels' order (ascending j), so results match them.
 constexpr int kDncWarps = 4;
 
@@ -551,8 +556,10 @@ int launch_dnc(const DevModel& dm, int Bfr, int fr_shared, const double* elems,
   double* aff = d <= 8 ? ws.take<double>((size_t)Bfr * n_heap * ((3 * dd + d + 1) & ~1)) : nullptr;
   if (ws.base == nullptr) return AUXMC_OK;
   if (!nodes || !params || (d <= 8 && !aff)) return AUXMC_E_WORKSPACE;
-  // CTA bridges keep 8 d*d + 4 doubles in shared memory: d <= 60
-  if (d > 64 || sizeof(double) * (8 * (size_t)dd + 4) > 227 * 1024) return AUXMC_E_DIM;
+  // CTA bridges keep 6 d*d + 4 doubles in shared memory; the warp-level draw
+  // kernels stage 64-wide vectors: d <= 64
+  if (d > 64 || sizeof(double) * (kBridgeBuffers * (size_t)dd + 4) > 227 * 1024)
+    return AUXMC_E_DIM;
   const bool block = d > 16;  // CTA groups (blocked DMMA factor/solves) for d > 16
   const int warps = 4;
   if (T > 0) {
@@ -577,14 +584,14 @@ int launch_dnc(const DevModel& dm, int Bfr, int fr_shared, const double* elems,
     const long long items = (n_heap - 1) * Bfr;
     if (block) {
       const int grid = (int)std::min<long long>(items, 148LL * 16);
-      const size_t smem = sizeof(double) * (8 * dd + 4);
+      const size_t smem = sizeof(double) * (kBridgeBuffers * dd + 4);
       AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_dnc_bridge<true>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       AUXMC_LAUNCH(k_dnc_bridge<true>, grid, 128, smem, stream, T, d, Bfr, nodes, n_heap, 1LL,
                    n_heap, params, st_fr);
     } else {
       const int grid = (int)std::min<long long>((items + warps - 1) / warps, 148LL * 64);
-      const size_t smem = sizeof(double) * (8 * dd + 4) * warps;
+      const size_t smem = sizeof(double) * (kBridgeBuffers * dd + 4) * warps;
       AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_dnc_bridge<false>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       AUXMC_LAUNCH(k_dnc_bridge<false>, grid, 32 * warps, smem, stream, T, d, Bfr, nodes, n_heap,

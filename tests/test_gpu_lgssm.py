@@ -105,11 +105,11 @@ def test_samplers_large_dims_match_oracle(gpu, oracle, case, sampler):
     assert_close(got.cpu(), want, RTOL, f"sampler {sampler}")
 
 
-@pytest.mark.parametrize("sampler", [0, 1])
+@pytest.mark.parametrize("sampler", [0, 1, 2])
 def test_samplers_d64_match_oracle(gpu, oracle, sampler):
-    """d = 64: the backward elements' five-buffer CTA layout (F read from global)
-    fits where the eight-buffer one exceeded shared memory; sequential and
-    blocked prefix samplers against the oracle (DnC stops at d = 60)."""
+    """d = 64: the backward elements' five-buffer and the DnC bridges' six-buffer
+    CTA layouts fit where the eight-buffer ones exceeded shared memory;
+    sequential, blocked prefix and DnC samplers against the oracle."""
     lgssm, pit, _ = gpu
     m, obs = _oracle_case(oracle, 5, 64, 8, True, False, 42)
     fr_o = oracle.kalman_filter(m, obs)

@@ -12,7 +12,7 @@ for d, dy in ((5, 3), (16, 4), (40, 20), (64, 8)):
     model = bm.synthetic_lgssm(spec)
     fr = lgssm.kalman_filter(model, data)
     keys = rng.chain_keys(7, 3)
-    for smp in (0, 1):
+    for smp in (0, 1, 2):
         try:
             x = lgssm.PathSampler(model, 3, smp, True)(fr, lgssm.Noise.stream(keys))
             res[f"d{d}_s{smp}"] = x.cpu().numpy()
