@@ -307,6 +307,16 @@ size_t auxmc_aux_kernel_workspace(const auxmc_target* target, int C,
                                   const auxmc_kernel_options* opts);
 /* auxk::adapt_delta (auxk.cpp:213-218) for every chain. */
 int auxmc_adapt_delta(auxmc_chains* chains, double target_rate, void* stream);
+/* gamma_move (bench/runner.cpp:61-85): random-walk MH on log γ, the diffusion
+ * coefficient of a Lorenz target (Q = h γ² I; Lorenz-63 as in the reference, Lorenz-96
+ * with the same density at d = dx), N(0, 1) prior on log γ.  x [C][T+1][dx] device
+ * paths; per chain the stream root_keys[c].derive(kParam = 15, iter) (runner.cpp:160-161);
+ * gamma [C] updated in place on acceptance, moved [C] = 1 if accepted.  The caller
+ * rebuilds the chain's target with the new γ, as runner.cpp:162-167 does.
+ * AUXMC_E_CONFIG for a non-Lorenz target. */
+int auxmc_gamma_move(const auxmc_target* target, int C, const double* x,
+                     const uint64_t* root_keys, long long iter, double step, double* gamma,
+                     int* moved, void* stream);
 
 /* ---- time-sharded auxiliary Kalman step (one chain, kernel_step, auxk.cpp:130-198,
  * with the prefix backend and the scan filter split over ranks; tshard.py drives it):

@@ -299,3 +299,41 @@ void ao_adapt_delta(ao_chain* st, double target_rate) {
   const double step = pow(n, -0.6);
   st->delta = exp(log(st->delta) + step * (st->stats.last_accept_prob - target_rate));
 }
+
+/* runner.cpp:61-85 gamma_move: random-walk MH on log gamma (the diffusion
+ * coefficient, Q = h gamma^2 I) with a standard normal prior on log gamma.  The drift
+ * does not depend on gamma, so the residual sum of squares is computed once (:65-70).
+ * The reference hard-codes d = 3 (Lorenz-63, "-1.5 * T"); the same density with
+ * 0.5 * d covers Lorenz-96 (0.5 * 3 == 1.5 exactly, so d = 3 is bit-identical).
+ * s = root.derive(kParam, iter) (:160-161); normal at counter 0, uniform at 1.
+ * Returns 1 and updates *gamma when the move is accepted. */
+int ao_gamma_move(const ao_target* tg, const double* x, double* gamma, double step,
+                  ao_stream s) {
+  const int T = tg->T, d = tg->dx;
+  double* mean = (double*)malloc(sizeof(double) * d);
+  double sse = 0.0;
+  for (int t = 0; t < T; ++t) {
+    ao_dyn_mean(tg, t, x + (size_t)t * d, mean);
+    double sq = 0.0;
+    for (int i = 0; i < d; ++i) {
+      const double r = x[(size_t)(t + 1) * d + i] - mean[i];
+      sq += r * r;
+    }
+    sse += sq;
+  }
+  free(mean);
+  const double h = tg->kind == AO_KIND_LORENZ63 ? tg->spec.lz_h : tg->spec.l96_h;
+  const double hd = 0.5 * d;
+  const double g0 = *gamma;
+#define AO_GLL(g) (-hd * T * log(2.0 * M_PI * h * (g) * (g)) - sse / (2.0 * h * (g) * (g)))
+  const double lg = log(g0);
+  const double lg_prop = lg + step * ao_next_normal(&s);
+  const double g_prop = exp(lg_prop);
+  const double log_r = AO_GLL(g_prop) - 0.5 * lg_prop * lg_prop - (AO_GLL(g0) - 0.5 * lg * lg);
+#undef AO_GLL
+  if (log(ao_next_uniform(&s)) < log_r) {
+    *gamma = g_prop;
+    return 1;
+  }
+  return 0;
+}

@@ -225,6 +225,9 @@ int ao_kernel_step(const ao_target* tg, ao_chain* st, ao_stream rng, int backend
 double ao_mh_log_ratio(const ao_target* tg, const double* x, const double* xp,
                        const double* u, double delta, int zeroth_order, int* status);
 void ao_adapt_delta(ao_chain* st, double target_rate);
+/* runner.cpp:61-85 diffusion-coefficient RW-MH move; returns 1 if accepted */
+int ao_gamma_move(const ao_target* tg, const double* x, double* gamma, double step,
+                  ao_stream s);
 
 /* ---------------- particle Gibbs (fkpg.cpp), gradient mode ---------------- */
 typedef struct {

@@ -158,6 +158,7 @@ def _declare(L):
     L.ao_kernel_step.argtypes = [C.POINTER(Target), C.POINTER(Chain), Stream, C.c_int, C.c_int,
                                  C.c_int]
     L.ao_adapt_delta.argtypes = [C.POINTER(Chain), C.c_double]
+    L.ao_gamma_move.argtypes = [C.POINTER(Target), PD, C.POINTER(C.c_double), C.c_double, Stream]
     L.ao_mh_log_ratio.restype = C.c_double
     L.ao_mh_log_ratio.argtypes = [C.POINTER(Target), PD, PD, PD, C.c_double, C.c_int, PI]
     L.ao_sample_aux_obs.argtypes = [PD, C.c_int, C.c_int, C.c_double, Stream, PD]
@@ -543,6 +544,13 @@ class AuxChain:
 
     def adapt(self, target_rate):
         lib().ao_adapt_delta(C.byref(self.c), target_rate)
+
+
+def gamma_move(tg: OTarget, x, gamma: float, step: float, s: Stream):
+    """runner.cpp:61-85: RW-MH on log gamma; returns (new gamma, accepted)."""
+    g = C.c_double(gamma)
+    moved = lib().ao_gamma_move(C.byref(tg.raw), _p(_f64(x)), C.byref(g), step, s)
+    return g.value, bool(moved)
 
 
 def aux_model_filter(tg: OTarget, x, u, delta, zeroth_order=False):

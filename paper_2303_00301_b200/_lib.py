@@ -146,6 +146,8 @@ SIGNATURES = {
     "auxmc_aux_kernel_workspace": (C.c_size_t, [C.POINTER(Target), C.c_int,
                                                 C.POINTER(KernelOptions)]),
     "auxmc_adapt_delta": (C.c_int, [C.POINTER(Chains), C.c_double, VP]),
+    "auxmc_gamma_move": (C.c_int, [C.POINTER(Target), C.c_int, VP, VP, C.c_longlong, C.c_double,
+                                  VP, VP, VP]),
     "auxmc_tshard_aux_workspace": (C.c_size_t, [C.POINTER(Target)]),
     "auxmc_tshard_aux_begin": (C.c_int, [C.POINTER(Target), C.POINTER(Chains),
                                          C.POINTER(KernelOptions), VP, C.c_size_t,

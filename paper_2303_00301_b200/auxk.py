@@ -300,3 +300,30 @@ class AuxChains:
 def init_chains(target: GenSSMTarget, x0, delta, seed: int, n_chains: int, first: int = 0):
     """Batched init_chain with chain roots from_seed(seed).derive(kChain, c) (runner.cpp:132)."""
     return AuxChains(target, x0, delta, chain_keys(seed, n_chains, first, target.device))
+
+
+def gamma_move(target: GenSSMTarget, x, root_keys: torch.Tensor, iter: int, step: float,
+               gamma) -> tuple[torch.Tensor, torch.Tensor]:
+    """bench/runner.cpp:61-85 `gamma_move` for C chains: random-walk MH on log γ (the
+    diffusion coefficient of a Lorenz target, Q = h γ² I) with a N(0, 1) prior on log γ,
+    stream root.derive(kParam, iter) per chain.  `x` [C, T+1, dx] device paths, `gamma`
+    a scalar or [C].  Returns (new γ [C], accepted [C] bool).  Like the reference, the
+    caller rebuilds the target with the new γ (runner.cpp:162-167)."""
+    x = torch.as_tensor(x, dtype=torch.float64, device=target.device)
+    if x.dim() == 2:
+        x = x.unsqueeze(0)
+    x = x.contiguous()
+    Cn = x.shape[0]
+    keys = root_keys.to(target.device).contiguous()
+    if keys.shape[0] != Cn:
+        raise ValueError("gamma_move: one root key per chain")
+    g = torch.full((Cn,), float(gamma), dtype=torch.float64, device=target.device) \
+        if np.isscalar(gamma) else torch.as_tensor(gamma, dtype=torch.float64,
+                                                   device=target.device).clone().contiguous()
+    moved = torch.zeros(Cn, dtype=torch.int32, device=target.device)
+    r = target.raw()
+    _lib.check(_lib.load().auxmc_gamma_move(C.byref(r), Cn, x.data_ptr(), keys.data_ptr(), int(iter),
+                                            float(step), g.data_ptr(), moved.data_ptr(),
+                                            torch.cuda.current_stream().cuda_stream),
+               "gamma_move")
+    return g, moved.bool()
