@@ -29,6 +29,8 @@ namespace auxmc_gpu {
 template <int D>
 int run_prefix_bulk(int T, int B, const double* elems, const double* term, Arena& ws,
                     const NoiseArgs& nz, double* traj, cudaStream_t stream);
+int run_prefix_mma(int T, int B, const double* elems, const double* term, Arena& ws,
+                   const NoiseArgs& nz, double* traj, cudaStream_t stream);
 
 template <int D>
 struct PfxGeom {
@@ -301,7 +303,7 @@ int launch_prefix_shared(int d, int T, int B, const double* elems, const double*
     case 1: return run_prefix_tiles<1>(T, B, elems, term, ws, nz, traj, stream);
     case 2: return run_prefix_bulk<2>(T, B, elems, term, ws, nz, traj, stream);
     case 3: return run_prefix_tiles<3>(T, B, elems, term, ws, nz, traj, stream);
-    case 4: return run_prefix_bulk<4>(T, B, elems, term, ws, nz, traj, stream);
+    case 4: return run_prefix_mma(T, B, elems, term, ws, nz, traj, stream);  // C2 (DMMA)
     case 5: return run_prefix_tiles<5>(T, B, elems, term, ws, nz, traj, stream);
     case 6: return run_prefix_tiles<6>(T, B, elems, term, ws, nz, traj, stream);
     case 7: return run_prefix_tiles<7>(T, B, elems, term, ws, nz, traj, stream);

@@ -164,7 +164,7 @@ __device__ __forceinline__ void shfl_down_vec(const double* v, double* out, int 
 // buffered (tiles k and k-1 are live while k-2 streams in), noise rows double
 // buffered, path rows single buffered (drained during the next phase A).
 template <int D, bool PRE>
-__global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
+__global__ void __launch_bounds__((BulkGeom<D>::WARPS + 2) * 32, 1)
     k_prefix_bulk(int T, int C, const double* __restrict__ tiles, const double* __restrict__ term,
                   NoiseArgs noise, double* __restrict__ traj) {
   using G = BulkGeom<D>;
@@ -180,7 +180,8 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
   uint64_t* barN = barT + G::TSTG;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool cw = warp == W;  // carry warp
+  const bool cw = warp == W;      // carry warp (phase B)
+  const bool pw = warp == W + 1;  // producer warp: every TMA load and store
   const int slot = lane & 7, q = lane >> 3, j = warp * 4 + q;
   const int c_begin = (int)(((long long)blockIdx.x * C) / gridDim.x);
   const int c_end = (int)(((long long)(blockIdx.x + 1) * C) / gridDim.x);
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
       bulk_g2s(xin(k) + ch * G::ROW, noise.backward + ((size_t)(c_begin + ch) * T + t0) * D, xb,
                bar);
   };
-  if (cw && lane == 0) {
+  if (pw && lane == 0) {
     issue_tile(K - 1);
     if (PRE) issue_noise(K - 1);
     if (K >= 2) {
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
     nph ^= 1u << b;
   };
   uint64_t klabel = 0;
-  if (!PRE && !cw && active) klabel = derive_label(noise.keys[c], kBackwardNoise);
+  if (!PRE && !cw && !pw && active) klabel = derive_label(noise.keys[c], kBackwardNoise);
 
   // Phase A for superchunk k: realize c_t = off_t + L_t xi_t, reduce each
   // sub-chunk (zero carry), Kogge-Stone over the warp's 4 sub-chunks; the warp
@@ -368,19 +369,24 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
   };
 
   double csA[LS * D], yA[D], csB[LS * D], yB[D];
-  if (!cw) phase_a(K - 1, csA, yA);
+  if (!cw && !pw) phase_a(K - 1, csA, yA);
   __syncthreads();
 
   for (int k = K - 1; k >= 0; --k) {
     const int t0 = k * S, t1 = min(t0 + S, T);
-    if (cw) {
+    if (pw) {
+      // loads of superchunk k-2 into the stages of tile k+1 / noise k (consumed), then
+      // the path store of superchunk k+1 must have left xo before phase C(k) rewrites
+      // it: the wait overlaps phases A / B instead of delaying them
       if (lane == 0) {
-        bulk_wait_read<0>();  // the store of superchunk k+1 has left xo
-        if (k >= 2) {          // stages of k+1 (tile) and k (noise) are free
+        if (k >= 2) {
           issue_tile(k - 2);
           if (PRE) issue_noise(k - 2);
         }
+        bulk_wait_read<0>();
       }
+      __syncwarp();
+    } else if (cw) {
       // Phase B (carry): serial pass over the 8 warp aggregates, top-down
       wait_tile(k);
       if (lane < 8 && active) {
@@ -419,7 +425,7 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
       phase_a(k - 1, csB, yB);
     }
     __syncthreads();
-    if (!cw) {  // Phase C: x at the top of each sub-chunk, then x_t = G_t x_{t+1} + c_t
+    if (!cw && !pw) {  // Phase C: x at the top of each sub-chunk, then x_t = G_t x_{t+1} + c_t
       const double* tl = tile(k);
       const double* E = tl + j * G::SUB;
       const double* gin = tl + G::EB + 2 * NS * D * D;
@@ -482,14 +488,14 @@ __global__ void __launch_bounds__((BulkGeom<D>::WARPS + 1) * 32, 1)
       for (int i = 0; i < D; ++i) yA[i] = yB[i];
     }
     __syncthreads();
-    if (cw && lane == 0 && AUXMC_PB_EXP != 1) {
+    if (pw && lane == 0 && AUXMC_PB_EXP != 1) {
       const unsigned xb = (unsigned)((t1 - t0) * D * sizeof(double));
       for (int ch = 0; ch < nc; ++ch)
         bulk_s2g(traj + (size_t)(c_begin + ch) * row + (size_t)t0 * D, xo + ch * G::ROW, xb);
       bulk_commit();
     }
   }
-  if (cw && lane == 0) bulk_wait<0>();
+  if (pw && lane == 0) bulk_wait<0>();
 }
 
 template <int D>
@@ -500,6 +506,8 @@ int run_prefix_bulk(int T, int B, const double* elems, const double* term, Arena
   double* tiles = ws.take<double>((size_t)K * G::TB);
   if (ws.base == nullptr) return AUXMC_OK;
   if (!tiles) return AUXMC_E_WORKSPACE;
+  if (nz.kind == AUXMC_NOISE_PREDRAWN && (reinterpret_cast<uintptr_t>(nz.backward) & 15))
+    return AUXMC_E_ARG;  // cp.async.bulk stages noise rows: 16-B aligned source required
   if (T > 0) {
     const int n_sub = K * G::NSUB;
     const int grid = std::min((n_sub + 127) / 128, 148 * 16);
@@ -510,12 +518,12 @@ int run_prefix_bulk(int T, int B, const double* elems, const double* term, Arena
   if (nz.kind == AUXMC_NOISE_PREDRAWN) {
     AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_prefix_bulk<D, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-    AUXMC_LAUNCH((k_prefix_bulk<D, true>), grid, (G::WARPS + 1) * 32, G::SMEM, stream, T, B, tiles,
+    AUXMC_LAUNCH((k_prefix_bulk<D, true>), grid, (G::WARPS + 2) * 32, G::SMEM, stream, T, B, tiles,
                  term, nz, traj);
   } else {
     AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_prefix_bulk<D, false>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-    AUXMC_LAUNCH((k_prefix_bulk<D, false>), grid, (G::WARPS + 1) * 32, G::SMEM, stream, T, B,
+    AUXMC_LAUNCH((k_prefix_bulk<D, false>), grid, (G::WARPS + 2) * 32, G::SMEM, stream, T, B,
                  tiles, term, nz, traj);
   }
   return AUXMC_OK;
@@ -523,7 +531,6 @@ int run_prefix_bulk(int T, int B, const double* elems, const double* term, Arena
 
 template int run_prefix_bulk<2>(int, int, const double*, const double*, Arena&, const NoiseArgs&,
                                 double*, cudaStream_t);
-template int run_prefix_bulk<4>(int, int, const double*, const double*, Arena&, const NoiseArgs&,
-                                double*, cudaStream_t);
+
 
 }  // namespace auxmc_gpu

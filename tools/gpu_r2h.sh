@@ -1,0 +1,4 @@
+timeout 600 python -m pytest tests/test_gpu_lgssm.py tests/test_gpu_law.py -x -q -m gpu 2>&1 | tail -2
+timeout 300 python bench.py --config c2 --no-e2e --no-cpu --steps 20 2>/dev/null | python -c "import json,sys; l=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c2', round(l['roofline']['kernel_ms'],4), l['roofline']['frac'], l['spot_check']['max_rel_err'])"
+timeout 300 python bench.py --config c2 --noise rng --no-e2e --no-cpu --steps 20 2>/dev/null | python -c "import json,sys; l=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c2rng', round(l['roofline']['kernel_ms'],4), l['spot_check']['max_rel_err'])"
+AUXMC_LIB_PATH=tools/_exp/m9.so python tools/c2_stamps.py | tail -2
