@@ -245,6 +245,11 @@ int auxmc_path_logpdf(const auxmc_lgssm* model, const double* obs, int obs_share
 #define AUXMC_KIND_GRID1D 4         /* models.cpp:319-333 */
 #define AUXMC_KIND_LORENZ96 5       /* new: Lorenz-96 diffusion, even coordinates observed */
 #define AUXMC_KIND_GAUSS_GENERIC 6  /* linear, Gaussian potentials in generic form */
+/* Test-only generic potentials reaching the reference's failure semantics on the device
+ * (1-d linear dynamics m0 = 0, P0 = 0.04, F = 0.5, b = 0, Q = 0.04):                    */
+#define AUXMC_KIND_TEST_ABORT 7     /* log g = -x^2/2, grad NaN for |x| > 0.5   (test_target_auxk.cpp:374-392) */
+#define AUXMC_KIND_TEST_SUPPORT 8   /* log g = -inf for x > 0.4, grad 0         (test_target_auxk.cpp:394-414) */
+#define AUXMC_KIND_TEST_COLLAPSE 9  /* log g_t = -inf at t = 2, else 0          (test_fkpg.cpp:447-465) */
 
 typedef struct {
   int kind;

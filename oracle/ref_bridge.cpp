@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <limits>
 #include <memory>
 #include <string>
 #include <vector>
@@ -227,6 +228,31 @@ int rb_grad_pot(const void* tg, int t, const double* x, int generic_only, double
 double rb_log_pot(const void* tg, int t, const double* x) {
   const auto& g = *static_cast<const auxk::GenSSMTarget*>(tg);
   return g.log_pot(t, vec_in(x, g.dx()));
+}
+
+// Test-only targets: the reference's own failure-path test targets, closures verbatim in
+// meaning (kind 7: test_target_auxk.cpp:374-392, 8: :394-414, 9: a collapse at t = 2 as in
+// test_fkpg.cpp:447-465, on the same 1-d linear dynamics).
+void* rb_target_test(int kind, int T) {
+  std::vector<auxk::Potential> pots(T + 1);
+  for (int t = 0; t <= T; ++t) {
+    auto& p = pots[t];
+    if (kind == 7) {
+      p.log_g = [](const Vec& x) { return -0.5 * x[0] * x[0]; };
+      p.grad_log_g = [](const Vec& x) {
+        return Vec(Vec::Constant(1, std::abs(x[0]) > 0.5 ? std::nan("") : -x[0]));
+      };
+    } else if (kind == 8) {
+      p.log_g = [](const Vec& x) { return x[0] > 0.4 ? -std::numeric_limits<double>::infinity() : 0.0; };
+      p.grad_log_g = [](const Vec&) { return Vec(Vec::Zero(1)); };
+    } else {
+      p.log_g = [t](const Vec&) { return t == 2 ? -std::numeric_limits<double>::infinity() : 0.0; };
+      p.grad_log_g = [](const Vec&) { return Vec(Vec::Zero(1)); };
+    }
+  }
+  return new auxk::GenSSMTarget(auxk::GenSSMTarget::linear(
+      T, Vec::Zero(1), Mat::Constant(1, 1, 0.04), {Mat::Constant(1, 1, 0.5)}, {Vec::Zero(1)},
+      {Mat::Constant(1, 1, 0.04)}, std::move(pots)));
 }
 
 // ---------------------------------------------------------------- LGSSM (lgssm.cpp)

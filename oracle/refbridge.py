@@ -69,6 +69,7 @@ def _declare(L):
         "rb_simulate": (C.c_int, [SP, PD, PD]),
         "rb_target_new": (VP, [SP, PD, C.c_int, PI]),
         "rb_target_free": (None, [VP]),
+        "rb_target_test": (VP, [C.c_int, C.c_int]),
         "rb_log_gamma": (C.c_double, [VP, PD, PI]),
         "rb_grad_pot": (C.c_int, [VP, C.c_int, PD, C.c_int, PD]),
         "rb_log_pot": (C.c_double, [VP, C.c_int, PD]),
@@ -184,6 +185,14 @@ class RTarget:
 
 def make_target(s: O.Spec, data) -> RTarget:
     return RTarget(s, data)
+
+
+def test_target(name: str, T: int) -> RTarget:
+    """The reference's failure-path test targets (ref_bridge.cpp rb_target_test)."""
+    t = RTarget.__new__(RTarget)
+    t.T, t.dx, t.data = T, 1, np.zeros(0)
+    t.h = lib().rb_target_test({"test-abort": 7, "test-support": 8, "test-collapse": 9}[name], T)
+    return t
 
 
 class RModel:

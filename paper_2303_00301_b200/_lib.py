@@ -18,7 +18,8 @@ OK, E_DIM, E_FACTOR, E_DEGENERATE, E_CONTRACT, E_CONFIG, E_CUDA, E_ARG, E_WORKSP
 NOISE_STREAM, NOISE_PREDRAWN = 0, 1
 SAMPLER_SEQ, SAMPLER_PREFIX, SAMPLER_DNC = 0, 1, 2
 KIND = {"lgssm-synthetic": 0, "stochvol": 1, "diffusion-smoothing": 2, "spatio-temporal": 3,
-        "grid-1d-test": 4, "lorenz96": 5, "gauss-generic": 6}
+        "grid-1d-test": 4, "lorenz96": 5, "gauss-generic": 6, "test-abort": 7, "test-support": 8,
+        "test-collapse": 9}
 
 PD = C.POINTER(C.c_double)
 PU8 = C.POINTER(C.c_uint8)

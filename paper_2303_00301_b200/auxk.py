@@ -129,6 +129,17 @@ class GenSSMTarget:
                             eH=bo(m.H), ec=bo(m.c), eR=bo(m.R), ey=obs, emask=mask, device=device)
 
     @staticmethod
+    def test_kind(name, T, device="cuda"):
+        """Test-only targets reaching the reference's failure semantics (auxmc_gpu.h
+        AUXMC_KIND_TEST_*): 1-d linear dynamics m0 = 0, P0 = 0.04, F = 0.5, b = 0,
+        Q = 0.04 with the generic potentials of test_target_auxk.cpp:374-414 ("test-abort",
+        "test-support") and test_fkpg.cpp:447-465 ("test-collapse")."""
+        if name not in ("test-abort", "test-support", "test-collapse"):
+            raise ValueError(name)
+        return GenSSMTarget(name, T, 1, [0.0], [[0.04]], [[[0.04]]], [[[0.5]]], [[0.0]],
+                            gmask=np.ones(T + 1, np.uint8), device=device)
+
+    @staticmethod
     def linear_generic(m, obs, device="cuda"):
         """testutil.hpp:112-140: same law, Gaussian potentials in generic form."""
         T = m.T
@@ -314,12 +325,19 @@ def gamma_move(target: GenSSMTarget, x, root_keys: torch.Tensor, iter: int, step
         x = x.unsqueeze(0)
     x = x.contiguous()
     Cn = x.shape[0]
+    if tuple(x.shape[1:]) != (target.T + 1, target.dx):
+        raise ValueError(f"gamma_move: paths must be [C, {target.T + 1}, {target.dx}]")
+    if not torch.is_tensor(root_keys) or root_keys.dtype not in (torch.int64, torch.uint64) \
+            or root_keys.dim() != 1:
+        raise ValueError("gamma_move: root_keys must be a 1-D int64/uint64 tensor")
     keys = root_keys.to(target.device).contiguous()
     if keys.shape[0] != Cn:
         raise ValueError("gamma_move: one root key per chain")
     g = torch.full((Cn,), float(gamma), dtype=torch.float64, device=target.device) \
         if np.isscalar(gamma) else torch.as_tensor(gamma, dtype=torch.float64,
-                                                   device=target.device).clone().contiguous()
+                                                   device=target.device).reshape(-1).clone()
+    if g.numel() != Cn:
+        raise ValueError("gamma_move: gamma must be a scalar or one value per chain")
     moved = torch.zeros(Cn, dtype=torch.int32, device=target.device)
     r = target.raw()
     _lib.check(_lib.load().auxmc_gamma_move(C.byref(r), Cn, x.data_ptr(), keys.data_ptr(), int(iter),

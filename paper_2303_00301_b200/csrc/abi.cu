@@ -213,9 +213,17 @@ int auxmc_rng_normals(const uint64_t* keys, int B, uint64_t label, uint64_t inde
   return AUXMC_OK;
 }
 
+// One or two very long sequences: the sequential recurrence would run on one thread
+// (T = 2^16 at d = 4 took 832 ms), so kalman_filter runs the reference's own
+// parallel_filter algorithm (pit.cpp:117-188) for them — the same moments and
+// log-likelihood up to FP rounding (tests/test_gpu_lgssm.py long-horizon case, 1e-8).
+static bool seq_as_scan(const auxmc_lgssm& m, int B) {
+  return B <= 2 && m.T >= 4096 && m.dx <= 32 && m.dy <= 64;
+}
+
 size_t auxmc_kalman_filter_workspace(const auxmc_lgssm* model, int B, int mode) {
   if (!model) return 0;
-  if (mode == 1) return filter_pit_workspace(to_dev(*model), B);
+  if (mode == 1 || (mode == 0 && seq_as_scan(*model, B))) return filter_pit_workspace(to_dev(*model), B);
   return 0;
 }
 
@@ -228,8 +236,10 @@ int auxmc_kalman_filter(const auxmc_lgssm* model, const double* obs, int B, int 
   if (!out || !status || (model->dy > 0 && !obs) || B < 0) return AUXMC_E_ARG;
   if (B == 0) return AUXMC_OK;
   const DevModel dm = to_dev(*model);
-  if (mode == 0) return launch_filter_seq(dm, obs, B, out, status, (cudaStream_t)stream);
-  if (mode == 1) {
+  if (mode == 0 && !(seq_as_scan(*model, B) && workspace &&
+                     workspace_bytes >= filter_pit_workspace(dm, B)))
+    return launch_filter_seq(dm, obs, B, out, status, (cudaStream_t)stream);
+  if (mode == 0 || mode == 1) {
     Arena ws{(char*)workspace, workspace_bytes, 0};
     return launch_filter_pit(dm, obs, B, out, status, ws, (cudaStream_t)stream);
   }

@@ -592,6 +592,13 @@ __global__ void k_pit_forward_backward(DevTarget tg, FactorRef f, PgArgs a, cons
       for (int i = threadIdx.x; i < N; i += blockDim.x) m = fmax(m, alpha[i]);
       return m;
     }(), red);
+    if (!isfinite(am)) {  // every message at t-1 collapsed: DegenerateWeightsError naming t-1
+      if (threadIdx.x == 0) {  // (fkpg.cpp:19-23: the reference's sweep fails at that step)
+        a.status[c] = AUXMC_E_DEGENERATE;
+        a.bad_t[c] = t - 1;
+      }
+      return;
+    }
     const int jq = jq0 + (f.fl.nQ > 1 ? t - 1 : 0);
     const double* LQ = f.L(jq);
     const double ldq = f.logdet[jq];

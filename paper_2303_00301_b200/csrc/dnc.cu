@@ -100,9 +100,17 @@ __global__ void k_dnc_bridge(int T, int d, int Bfr, const double* __restrict__ n
   double* W = A + dd;
   double* L = W + dd;
   double* scr = L + dd;
-  double* K = cross;  // cross is dead once K = (s^{-1} cross^T)^T is formed
-  double* cov = L;    // the first factor is dead after the solve
-  double* Lc = A;     // A is dead once cov is formed
+  // Buffer liveness (each alias is written only after its previous occupant's last read):
+  //   B0 cross: read by the zero test and the cross^T copy into A  -> then K (written after
+  //             the solve consumed A; cross is dead)
+  //   B4 L (the factor of s): last read by g_llt_solve             -> then cov (written after)
+  //   B2 A = cross^T / solve rhs, then I - K G_lm: last read forming W = A S_mr and cov
+  //                                                                -> then Lc (chol of cov)
+  // A retry inside g_factor_psd / g_chol_psd reads only its own input (s / cov) and writes
+  // its output (L / Lc) and scr, none of which alias a live buffer at that point.
+  double* K = cross;
+  double* cov = L;
+  double* Lc = A;
   double* red = scr + dd;
   int* flag = reinterpret_cast<int*>(red + 2);
   const long long width = n_last - n_first;
@@ -141,8 +149,9 @@ __global__ void k_dnc_bridge(int T, int d, int Bfr, const double* __restrict__ n
       for (int i = g.lane; i < dd; i += g.size) A[i] = cross[(i % d) * d + i / d];  // cross^T
       g.sync();
       st = g_factor_psd(g, d, s, L, scr, flag, red);
-      if (st) {
+      if (st) {  // FactorizationError (gauss.cpp:34): flag the chain, poison this bridge
         if (g.lane == 0) atomicMax(status + b, st);
+        for (int i = g.lane; i < 2 * dd; i += g.size) out[i] = __longlong_as_double(0x7ff8000000000000ll);
         g.sync();
         continue;
       }

@@ -138,6 +138,12 @@ __device__ __forceinline__ double generic_log_g(const DevTarget& tg, int t, cons
       }
       return gauss_term(n, r, Lg, ldg);
     }
+    case AUXMC_KIND_TEST_ABORT:
+      return -0.5 * x[0] * x[0];
+    case AUXMC_KIND_TEST_SUPPORT:
+      return x[0] > 0.4 ? -INFINITY : 0.0;
+    case AUXMC_KIND_TEST_COLLAPSE:
+      return t == 2 ? -INFINITY : 0.0;
   }
   return 0.0;
 }
@@ -159,6 +165,9 @@ __device__ __forceinline__ void generic_grad(const DevTarget& tg, int t, const d
       return;
     case AUXMC_KIND_GRID1D:
       g[0] = -4.0 * x[0] * x[0] * x[0];
+      return;
+    case AUXMC_KIND_TEST_ABORT:
+      g[0] = fabs(x[0]) > 0.5 ? __longlong_as_double(0x7ff8000000000000ll) : -x[0];
       return;
     case AUXMC_KIND_GAUSS_GENERIC: {
       const int n = tg.ydim;

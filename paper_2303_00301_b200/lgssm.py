@@ -130,14 +130,30 @@ def _filter(model: Model, obs, mode: int) -> FilterResult:
     return fr
 
 
-def kalman_filter(model: Model, obs) -> FilterResult:
-    """lgssm::kalman_filter (lgssm.cpp:73-112) for obs [T+1, dy] or [B, T+1, dy]."""
-    return _filter(model, obs, 0)
+def check_status(status: torch.Tensor, what: str):
+    """Raise the reference's exception for a per-sequence / per-chain status array
+    (FactorizationError, gauss.cpp:34, as AuxmcError code E_FACTOR).  Reads one int
+    back from the device."""
+    code = int(status.max()) if status.numel() else 0
+    _lib.check(code, what)
 
 
-def parallel_filter(model: Model, obs) -> FilterResult:
+def kalman_filter(model: Model, obs, check: bool = True) -> FilterResult:
+    """lgssm::kalman_filter (lgssm.cpp:73-112) for obs [T+1, dy] or [B, T+1, dy].
+    A covariance that fails the jitter ladder raises (check=True, the reference's
+    behaviour) or is left in fr.status (check=False, per sequence)."""
+    fr = _filter(model, obs, 0)
+    if check:
+        check_status(fr.status, "kalman_filter")
+    return fr
+
+
+def parallel_filter(model: Model, obs, check: bool = True) -> FilterResult:
     """pit::parallel_filter (pit.cpp:117-188): scan over filtering elements."""
-    return _filter(model, obs, 1)
+    fr = _filter(model, obs, 1)
+    if check:
+        check_status(fr.status, "parallel_filter")
+    return fr
 
 
 class Noise:
@@ -190,16 +206,26 @@ class PathSampler:
         self.status = torch.zeros(B, dtype=torch.int32, device=model.device)
 
     def __call__(self, fr: FilterResult, noise: Noise, out: torch.Tensor = None,
-                 stream=None) -> torch.Tensor:
+                 stream=None, check: bool = False) -> torch.Tensor:
+        """Draw the B paths.  self.status is reset every call and holds, per path,
+        AUXMC_OK or AUXMC_E_FACTOR (a backward covariance / DnC bridge that failed the
+        jitter ladder: that path is invalid).  check=True raises like the reference
+        (one device read); hot loops keep check=False and call check_status()."""
         m = self.model
         if out is None:
             out = torch.empty((self.B, m.T + 1, m.dx), dtype=torch.float64, device=m.device)
+        st = stream if stream is not None else _stream()
         fr_raw, nz = fr.raw(), noise.raw()
         _lib.check(_lib.load().auxmc_sample_paths(
             C.byref(self._mr), C.byref(fr_raw), int(self.fr_shared), C.byref(nz), self.B,
             self.sampler, out.data_ptr(), self.status.data_ptr(), self.ws.data_ptr(),
-            self.ws_bytes, stream if stream is not None else _stream()), "sample_paths")
+            self.ws_bytes, st), "sample_paths")
+        if check:
+            self.check_status()
         return out
+
+    def check_status(self):
+        check_status(self.status, "sample_paths")
 
 
 class HostPipeline:
@@ -219,6 +245,7 @@ class HostPipeline:
         self.ps = PathSampler(model, self.Bc, sampler, True)
         self.s_in, self.s_run, self.s_out = (torch.cuda.Stream(model.device) for _ in range(3))
         self._buf = None
+        self._fail = torch.zeros((), dtype=torch.int32, device=model.device)
 
     def _alloc(self, noise: Noise, fr: FilterResult):
         m, dev, Bc = self.model, self.model.device, self.Bc
@@ -252,6 +279,8 @@ class HostPipeline:
         fr_ready = torch.cuda.Event()
         fr_ready.record(self.s_in)
         self.s_run.wait_event(fr_ready)
+        with torch.cuda.stream(self.s_run):
+            self._fail.zero_()
         for i in range(self.chunks):
             j, b = i % 2, self._buf[i % 2]
             sl = slice(i * self.Bc, (i + 1) * self.Bc)
@@ -268,6 +297,7 @@ class HostPipeline:
                 nz = Noise(keys=b["keys"], terminal=b["terminal"], backward=b["backward"],
                            bridge=b["bridge"])
                 self.ps(self._fr, nz, b["out"])
+                torch.maximum(self._fail, self.ps.status.amax(), out=self._fail)
                 ev["run"][j].record(self.s_run)
             self.s_out.wait_event(ev["run"][j])
             with torch.cuda.stream(self.s_out):
@@ -277,11 +307,15 @@ class HostPipeline:
         main.wait_stream(self.s_run)
         return out_host
 
+    def check_status(self):
+        """Raise if any chunk of the last pass had a factorization failure."""
+        _lib.check(int(self._fail), "HostPipeline")
+
 
 def _sample(model, fr, noise, sampler):
     B = noise.B
     shared = fr.filt_mean.shape[0] == 1
-    return PathSampler(model, B, sampler, shared)(fr, noise)
+    return PathSampler(model, B, sampler, shared)(fr, noise, check=True)
 
 
 def backward_sample(model: Model, fr: FilterResult, noise: Noise) -> torch.Tensor:
@@ -305,6 +339,7 @@ def path_logpdf(model: Model, obs, traj, fr: FilterResult) -> torch.Tensor:
         C.byref(mr), obs.data_ptr(), int(obs.shape[0] == 1), traj.data_ptr(), C.byref(fr_raw),
         int(fr.filt_mean.shape[0] == 1), B, out.data_ptr(), status.data_ptr(), _stream()),
         "path_logpdf")
+    check_status(status, "path_logpdf")
     return out
 
 

@@ -18,13 +18,13 @@ class Sampler:
 def prefix_sample(model: Model, fr: FilterResult, noise: Noise) -> torch.Tensor:
     """pit::prefix_sample (pit.cpp:78-115): suffix scan of realized elements."""
     shared = fr.filt_mean.shape[0] == 1
-    return PathSampler(model, noise.B, _lib.SAMPLER_PREFIX, shared)(fr, noise)
+    return PathSampler(model, noise.B, _lib.SAMPLER_PREFIX, shared)(fr, noise, check=True)
 
 
 def dnc_sample(model: Model, fr: FilterResult, noise: Noise) -> torch.Tensor:
     """pit::dnc_sample (pit.cpp:192-301): bridges over the fixed segment tree."""
     shared = fr.filt_mean.shape[0] == 1
-    return PathSampler(model, noise.B, _lib.SAMPLER_DNC, shared)(fr, noise)
+    return PathSampler(model, noise.B, _lib.SAMPLER_DNC, shared)(fr, noise, check=True)
 
 
 def dnc_bridge_count(T: int) -> int:
