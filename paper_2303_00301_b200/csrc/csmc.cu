@@ -16,6 +16,8 @@
 //   index sampling with the reference's stream addresses.
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "dense.cuh"
 #include "group.cuh"
@@ -441,7 +443,6 @@ __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
   }
   // terminal index (fkpg.cpp:127-133) and backward index sampling (:135-150)
   block_cumsum(N, W, cum);
-  __shared__ int s_sel;
   double* tr = a.traj + (size_t)c * (T + 1) * d;
   uint64_t* tk = a.tkeys + (size_t)c * (T + 1);
   auto pm_key = [&](int t, int i) -> uint64_t {
@@ -450,7 +451,6 @@ __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
   };
   if (threadIdx.x == 0) {
     const int sel = draw_index(N, cum, uniform_at(derive(it, kTerminalIndex, 0), 0));
-    s_sel = sel;
     for (int k = 0; k < d; ++k) {
       chosen[k] = P[((size_t)T * N + sel) * d + k];
       tr[(size_t)T * d + k] = chosen[k];
@@ -558,9 +558,427 @@ __device__ __forceinline__ double exp_nonpos(double x) {
   return x < -708.0 ? 0.0 : p * scale;
 }
 
+// ---------------------------------------------------------------- PIT forward, cluster form
+// Forward log-messages alpha_t(j) = lw_t(j) + LSE_i(alpha_{t-1}(i) + log p(x_t^j | x_{t-1}^i))
+// with the whitened pair term (see k_pit_forward_backward), for small state dims.  One
+// thread-block CLUSTER of CS CTAs per chain: CTA r owns the j-slice
+// [r N / CS, (r+1) N / CS) of every step, and after each step the CTAs exchange their
+// slices of alpha_t through distributed shared memory (one cluster barrier per step,
+// slices double-buffered by step parity).  CS = 8 puts one chain on 8 SMs: the
+// single-chain latency case (SURVEY.md §8(d) C4 "report 1 chain"); CS = 1 is the
+// many-chain batch.  The time axis stays a recursion: an associative scan over the N x N
+// log-semiring transition operators would cost O(T N^3) exp evaluations (2.7e11 at
+// C4's N = 256, T = 2^14) against O(T N^2) here.
+//
+// The LSE over i uses one canonical partition for every cluster size, so a chain's
+// messages (and hence its draws) do not depend on the batch size: 32 contiguous i-parts
+// [p N / 32, (p+1) N / 32), each summed with four interleaved accumulators, combined by a
+// pairwise tree; total underflow falls back to the exact online LSE over all i.
+#ifndef AUXMC_PIT_EXP
+#define AUXMC_PIT_EXP 0  // 9: clock64 stamps of the cluster forward pass (timing only)
+#endif
+constexpr int kPitParts = 32;
+constexpr int kChaseBlock = 64;  // table rows staged per chase block (64 x N ints)
+
+template <int DT>
+__device__ __forceinline__ void pit_whiten(const double* LQ, const double* x, double* w) {
+#pragma unroll
+  for (int k = 0; k < DT; ++k) {
+    double acc = x[k];
+#pragma unroll
+    for (int l = 0; l < k; ++l) acc -= LQ[k * DT + l] * w[l];
+    w[k] = acc / LQ[k * DT + k];
+  }
+}
+
+// Pre-pass: the whitened operands of every forward step, V[c][t-1][i] =
+// L_q^{-1} mean(x_{t-1}^i) and X[c][t-1][j] = L_q^{-1} x_t^j (q = q(t), t = 1..T), for all
+// (chain, t, i) in parallel — off the forward recursion's critical path.
+template <int DT>
+__global__ void k_pit_whiten(DevTarget tg, FactorRef f, PgArgs a, double* V, double* X) {
+  const int N = a.N, T = tg.T;
+  const long long n = (long long)a.C * T * N;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(q % N);
+    const long long ct = q / N;
+    const int t = (int)(ct % T) + 1, c = (int)(ct / T);
+    const double* LQ = f.L(1 + (f.fl.nQ > 1 ? t - 1 : 0));
+    const double* P = a.part + (size_t)c * (T + 1) * N * DT;
+    double m[DT];
+#pragma unroll
+    for (int k = 0; k < DT; ++k) m[k] = dyn_mean_i(tg, t - 1, P + ((size_t)(t - 1) * N + i) * DT, k);
+    pit_whiten<DT>(LQ, m, V + q * DT);
+    pit_whiten<DT>(LQ, P + ((size_t)t * N + i) * DT, X + q * DT);
+  }
+}
+
+// The forward recursion.  Per step: am = max alpha_{t-1} (CS > 1: from the maxima the
+// CTAs pushed with their slices), the pair sums of the own j-slice over the canonical
+// i-partition, then each CTA pushes its alpha_t slice (and its maximum) into every CTA's
+// shared memory (parity double buffers) and the cluster synchronizes once.  The next
+// step's whitened operands are prefetched into registers during the pair loop.
+template <int DT>
+__global__ void __launch_bounds__(1024, 1)
+    k_pit_forward_cluster(DevTarget tg, FactorRef f, PgArgs a, const double* lw, const double* V,
+                          const double* X, int CS) {
+  namespace cg = cooperative_groups;
+  extern __shared__ double sm[];
+  const int N = a.N, T = tg.T;
+  const int rank = (int)blockIdx.x % CS;
+  const int c = (int)blockIdx.x / CS;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int j0 = (int)((long long)rank * N / CS), j1 = (int)((long long)(rank + 1) * N / CS);
+  const int JL = j1 - j0, JLmax = (N + CS - 1) / CS;
+  double* alpha = sm;                                // 2 x N   alpha_{t}, by parity
+  double* vbuf = alpha + 2 * N;                      // 2 x N*DT
+  double* xbuf = vbuf + (size_t)2 * N * DT;          // 2 x JLmax*DT
+  double* ai = xbuf + (size_t)2 * JLmax * DT;        // N
+  double* partial = ai + N;                          // kPitParts x JLmax
+  double* smaxs = partial + kPitParts * JLmax;       // 2 x CS pushed slice maxima
+  double* red = smaxs + 2 * CS;                      // 40
+  const double* LW = lw + (size_t)c * (T + 1) * N;
+  double* A = a.Wt + (size_t)c * (T + 1) * N;
+  const double* Vc = V + (size_t)c * T * N * DT;
+  const double* Xc = X + (size_t)c * T * N * DT;
+  const int nV = N * DT, nX = JL * DT;
+  // operands of step t into buffer t & 1 (thread-strided; one or two values per thread)
+  auto load_ops = [&](int t, double* vdst, double* xdst) {
+    for (int q = threadIdx.x; q < nV + nX; q += blockDim.x) {
+      if (q < nV) vdst[q] = Vc[(size_t)(t - 1) * nV + q];
+      else xdst[q - nV] = Xc[((size_t)(t - 1) * N + j0) * DT + (q - nV)];
+    }
+  };
+  for (int i = threadIdx.x; i < N; i += blockDim.x) alpha[i] = LW[i];
+  for (int j = j0 + (int)threadIdx.x; j < j1; j += blockDim.x) A[j] = LW[j];
+  if (T >= 1) load_ops(1, vbuf + (size_t)1 * nV, xbuf + (size_t)1 * JLmax * DT);
+  __syncthreads();
+#if AUXMC_PIT_EXP == 9
+  __shared__ long long pts[16 * 8];
+  auto pst = [&](int t, int e) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && t >= 1000 && t < 1016) pts[(t - 1000) * 8 + e] = clock64();
+  };
+#else
+  auto pst = [](int, int) {};
+#endif
+  for (int t = 1; t <= T; ++t) {
+    pst(t, 0);
+    const double* aprev = alpha + (size_t)((t - 1) & 1) * N;
+    double am;
+    if (t > 1 && CS > 1 && JLmax <= 32) {
+      am = -INFINITY;
+      for (int r = 0; r < CS; ++r) am = fmax(am, smaxs[((t - 1) & 1) * CS + r]);
+    } else {
+      am = block_max([&] {
+        double m = -INFINITY;
+        for (int i = threadIdx.x; i < N; i += blockDim.x) m = fmax(m, aprev[i]);
+        return m;
+      }(), red);
+    }
+    if (!isfinite(am)) {  // every message at t-1 collapsed (fkpg.cpp:19-23 names t-1)
+      if (rank == 0 && threadIdx.x == 0) {
+        a.status[c] = AUXMC_E_DEGENERATE;
+        a.bad_t[c] = t - 1;
+      }
+      break;  // uniform over the cluster: every CTA computed the same am
+    }
+    for (int i = threadIdx.x; i < N; i += blockDim.x) ai[i] = aprev[i] - am;
+    // prefetch step t+1's operands into registers (written to the other buffer below)
+    double pf[2] = {0.0, 0.0};
+    if (t < T) {
+      int k = 0;
+      for (int q = threadIdx.x; q < nV + nX && k < 2; q += blockDim.x, ++k)
+        pf[k] = q < nV ? Vc[(size_t)t * nV + q] : Xc[((size_t)t * N + j0) * DT + (q - nV)];
+    }
+    __syncthreads();
+    pst(t, 1);
+    const int jq = 1 + (f.fl.nQ > 1 ? t - 1 : 0);
+    const double M = -0.5 * (DT * kLog2Pi) - f.logdet[jq];
+    const double* vi = vbuf + (size_t)(t & 1) * nV;
+    const double* wj = xbuf + (size_t)(t & 1) * JLmax * DT;
+    for (int item = threadIdx.x; item < JL * kPitParts; item += blockDim.x) {
+      const int jl = item % JL, p = item / JL;
+      const int ilo = (int)((long long)p * N / kPitParts), ihi = (int)((long long)(p + 1) * N / kPitParts);
+      double w[DT];
+#pragma unroll
+      for (int k = 0; k < DT; ++k) w[k] = wj[jl * DT + k];
+      double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+      int i = ilo;
+      for (; i + 4 <= ihi; i += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          double sq = 0.0;
+#pragma unroll
+          for (int k = 0; k < DT; ++k) {
+            const double z = w[k] - vi[(i + u) * DT + k];
+            sq += z * z;
+          }
+          acc4[u] += exp_nonpos(ai[i + u] - 0.5 * sq);
+        }
+      }
+      for (; i < ihi; ++i) {
+        double sq = 0.0;
+#pragma unroll
+        for (int k = 0; k < DT; ++k) {
+          const double z = w[k] - vi[i * DT + k];
+          sq += z * z;
+        }
+        acc4[0] += exp_nonpos(ai[i] - 0.5 * sq);
+      }
+      partial[p * JLmax + jl] = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+    }
+    if (t < T) {
+      double* vdst = vbuf + (size_t)((t + 1) & 1) * nV;
+      double* xdst = xbuf + (size_t)((t + 1) & 1) * JLmax * DT;
+      int k = 0;
+      for (int q = threadIdx.x; q < nV + nX && k < 2; q += blockDim.x, ++k) {
+        if (q < nV) vdst[q] = pf[k];
+        else xdst[q - nV] = pf[k];
+      }
+      for (int q = threadIdx.x + 2 * (int)blockDim.x; q < nV + nX; q += blockDim.x) {  // rest
+        if (q < nV) vdst[q] = Vc[(size_t)t * nV + q];
+        else xdst[q - nV] = Xc[((size_t)t * N + j0) * DT + (q - nV)];
+      }
+    }
+    __syncthreads();
+    pst(t, 2);
+    double al = -INFINITY;
+    for (int jl = threadIdx.x; jl < JL; jl += blockDim.x) {
+      double q[kPitParts];  // canonical pairwise tree over the 32 parts
+#pragma unroll
+      for (int p = 0; p < kPitParts; ++p) q[p] = partial[p * JLmax + jl];
+#pragma unroll
+      for (int w = kPitParts / 2; w >= 1; w >>= 1)
+#pragma unroll
+        for (int p = 0; p < w; ++p) q[p] = q[2 * p] + q[2 * p + 1];
+      double s = q[0];
+      double m = 0.0;
+      if (!(s > 0.0)) {  // total underflow: exact online log-sum-exp relative to M
+        const double* w = wj + jl * DT;
+        m = -INFINITY;
+        s = 0.0;
+        for (int i2 = 0; i2 < N; ++i2) {
+          double sq = 0.0;
+#pragma unroll
+          for (int k = 0; k < DT; ++k) {
+            const double z = w[k] - vi[i2 * DT + k];
+            sq += z * z;
+          }
+          const double v = ai[i2] - 0.5 * sq;
+          if (v > m) {
+            s = s * exp(m - v) + 1.0;
+            m = v;
+          } else {
+            s += exp(v - m);
+          }
+        }
+      }
+      const int j = j0 + jl;
+      al = LW[(size_t)t * N + j] + (am + ((M + m) + log(s)));
+      A[(size_t)t * N + j] = al;
+      for (int r = 0; r < CS; ++r)  // push into every CTA's alpha_t buffer
+        cluster.map_shared_rank(alpha, r)[(size_t)(t & 1) * N + j] = al;
+    }
+    if (CS > 1 && JLmax <= 32 && threadIdx.x < 32) {  // push this slice's maximum
+      double v = (int)threadIdx.x < JL ? al : -INFINITY;
+      for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (threadIdx.x < CS) cluster.map_shared_rank(smaxs, threadIdx.x)[(t & 1) * CS + rank] = v;
+    }
+    pst(t, 3);
+    if (CS > 1) cluster.sync();  // alpha_t complete everywhere; step t-1 buffers free
+    else __syncthreads();
+    pst(t, 4);
+  }
+  if (CS > 1) cluster.sync();  // no CTA leaves while peers may still write its buffers
+#if AUXMC_PIT_EXP == 9
+  if (blockIdx.x == 0 && threadIdx.x < 128) reinterpret_cast<long long*>(a.Wt)[threadIdx.x] = pts[threadIdx.x];
+#endif
+}
+
+// Backward draws for few chains, precomputed in parallel: the uniform of every step is
+// known in advance (root.derive(kBackwardIndex, t)), so for every step t and every
+// possible chosen particle j at t+1 the drawn index sel(t, j) is a pure function of the
+// forward messages — exactly the reference's per-step normalize + sequential cumulative
+// draw (fkpg.cpp:19-37, 137-149), evaluated for all N rows of every step at once across
+// the GPU (CTA per (chain, t), thread per j; three passes over i: max, sequential sum,
+// sequential cumulative search).  The sequential chain is then an index chase through
+// the [T][N] table (k_pit_backward_chase).  -1 marks a degenerate row.
+__global__ void k_pit_backward_table(DevTarget tg, FactorRef f, PgArgs a, int* seltab) {
+  extern __shared__ double sm[];
+  const int N = a.N, T = tg.T, d = tg.dx;
+  const int c = (int)(blockIdx.x / T), t = (int)(blockIdx.x % T);
+  if (a.status[c] != AUXMC_OK) return;
+  double* mean = sm;           // N*d dynamics means of x_t^i
+  double* At = mean + (size_t)N * d;  // N
+  const double* P = a.part + (size_t)c * (T + 1) * N * d;
+  const double* A = a.Wt + (size_t)c * (T + 1) * N;
+  for (int q = threadIdx.x; q < N * d; q += blockDim.x)
+    mean[q] = dyn_mean_i(tg, t, P + ((size_t)t * N + q / d) * d, q % d);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) At[i] = A[(size_t)t * N + i];
+  __syncthreads();
+  const int jq = 1 + (f.fl.nQ > 1 ? t : 0);
+  const double* L = f.L(jq);
+  const double ld = f.logdet[jq];
+  const double u = uniform_at(derive(a.it[c], kBackwardIndex, (uint64_t)t), 0);
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    const double* ch = P + ((size_t)(t + 1) * N + j) * d;
+    double chosen[8], r[8];
+    for (int k = 0; k < d; ++k) chosen[k] = ch[k];
+    auto logb = [&](int i) {
+      for (int k = 0; k < d; ++k) r[k] = chosen[k] - mean[i * d + k];
+      return At[i] + gauss_term(d, r, L, ld);
+    };
+    double m = -INFINITY;
+    for (int i = 0; i < N; ++i) m = fmax(m, logb(i));
+    int sel = -1;
+    if (isfinite(m)) {
+      double s = 0.0;
+      for (int i = 0; i < N; ++i) s += exp(logb(i) - m);
+      double acc = 0.0;
+      sel = N - 1;
+      for (int i = 0; i < N; ++i) {
+        acc += exp(logb(i) - m) / s;
+        if (u <= acc) {
+          sel = i;
+          break;
+        }
+      }
+    }
+    seltab[((size_t)c * T + t) * N + j] = sel;
+  }
+}
+
+// The index chase: i_T from alpha_T (normalize + cumulative draw), then
+// i_t = sel(t, i_{t+1}) down to t = 0, table rows staged through shared memory in
+// blocks of steps.  Writes the new path, its keys and the optional selection trace.
+__global__ void k_pit_backward_chase(DevTarget tg, PgArgs a, const int* seltab) {
+  extern __shared__ double sm[];
+  const int N = a.N, T = tg.T, d = tg.dx;
+  const int c = blockIdx.x;
+  if (a.status[c] != AUXMC_OK) return;
+  double* alpha = sm;
+  double* W = alpha + N;
+  double* cum = W + N;
+  double* red = cum + N;  // 40
+  int* rows = reinterpret_cast<int*>(red + 40);
+  int* selp = rows + (size_t)kChaseBlock * N;
+  int* blk = selp + 1;  // the block's chased indices
+  const double* P = a.part + (size_t)c * (T + 1) * N * d;
+  const double* A = a.Wt + (size_t)c * (T + 1) * N;
+  double* tr = a.traj + (size_t)c * (T + 1) * d;
+  uint64_t* tk = a.tkeys + (size_t)c * (T + 1);
+  const uint64_t it = a.it[c];
+  auto pm_key = [&](int t, int i) -> uint64_t {
+    if (i == 0) return a.keys[(size_t)c * (T + 1) + t];
+    return key_at(derive(derive(it, kStep, (uint64_t)t), kPmKey, (uint64_t)i), 0);
+  };
+  auto take = [&](int t, int sel) {
+    for (int k = 0; k < d; ++k) tr[(size_t)t * d + k] = P[((size_t)t * N + sel) * d + k];
+    tk[t] = pm_key(t, sel);
+    if (a.sel) a.sel[(size_t)c * (T + 1) + t] = sel;
+  };
+  for (int i = threadIdx.x; i < N; i += blockDim.x) alpha[i] = A[(size_t)T * N + i];
+  __syncthreads();
+  if (!block_normalize(N, alpha, W, red)) {
+    if (threadIdx.x == 0) { a.status[c] = AUXMC_E_DEGENERATE; a.bad_t[c] = T; }
+    return;
+  }
+  block_cumsum(N, W, cum);
+  if (threadIdx.x == 0) {
+    const int sel = draw_index(N, cum, uniform_at(derive(it, kTerminalIndex, 0), 0));
+    *selp = sel;
+    take(T, sel);
+  }
+  __syncthreads();
+  const int* tab = seltab + (size_t)c * T * N;
+  for (int hi = T; hi > 0; hi -= kChaseBlock) {  // steps [lo, hi)
+    const int lo = hi > kChaseBlock ? hi - kChaseBlock : 0;
+    for (int q = threadIdx.x; q < (hi - lo) * N; q += blockDim.x) rows[q] = tab[(size_t)lo * N + q];
+    __syncthreads();
+    if (threadIdx.x == 0) {  // the chase alone; the path writes follow in parallel
+      int sel = *selp;
+      for (int t = hi - 1; t >= lo; --t) {
+        sel = rows[(t - lo) * N + sel];
+        blk[t - lo] = sel;
+        if (sel < 0) {
+          a.status[c] = AUXMC_E_DEGENERATE;
+          a.bad_t[c] = t;
+          break;
+        }
+      }
+      *selp = sel;
+    }
+    __syncthreads();
+    const bool bad = *selp < 0;
+    for (int t = lo + (int)threadIdx.x; t < hi; t += blockDim.x)
+      if (!bad) take(t, blk[t - lo]);
+    __syncthreads();
+    if (bad) return;
+  }
+}
+
+// Backward index sampling from the stored forward messages (rank 0 of the forward
+// cluster's chain, one CTA per chain): i_T ∝ exp(alpha_T), i_t ∝ exp(alpha_t(i))
+// p(x_{t+1}^{i_{t+1}} | x_t^i), with the reference's index uniforms.
+__global__ void k_pit_backward(DevTarget tg, FactorRef f, PgArgs a) {
+  extern __shared__ double sm[];
+  const int N = a.N, T = tg.T, d = tg.dx;
+  const int c = blockIdx.x;
+  if (a.status[c] != AUXMC_OK) return;  // degenerate forward pass
+  double* alpha = sm;
+  double* W = alpha + N;
+  double* cum = W + N;
+  double* red = cum + N;       // 40
+  double* chosen = red + 40;   // 64
+  const double* P = a.part + (size_t)c * (T + 1) * N * d;
+  const double* A = a.Wt + (size_t)c * (T + 1) * N;
+  double r[64];
+  double* tr = a.traj + (size_t)c * (T + 1) * d;
+  uint64_t* tk = a.tkeys + (size_t)c * (T + 1);
+  const uint64_t it = a.it[c];
+  auto pm_key = [&](int t, int i) -> uint64_t {
+    if (i == 0) return a.keys[(size_t)c * (T + 1) + t];
+    return key_at(derive(derive(it, kStep, (uint64_t)t), kPmKey, (uint64_t)i), 0);
+  };
+  for (int i = threadIdx.x; i < N; i += blockDim.x) alpha[i] = A[(size_t)T * N + i];
+  __syncthreads();
+  if (!block_normalize(N, alpha, W, red)) {
+    if (threadIdx.x == 0) { a.status[c] = AUXMC_E_DEGENERATE; a.bad_t[c] = T; }
+    return;
+  }
+  block_cumsum(N, W, cum);
+  if (threadIdx.x == 0) {
+    const int sel = draw_index(N, cum, uniform_at(derive(it, kTerminalIndex, 0), 0));
+    for (int k = 0; k < d; ++k) chosen[k] = tr[(size_t)T * d + k] = P[((size_t)T * N + sel) * d + k];
+    tk[T] = pm_key(T, sel);
+    if (a.sel) a.sel[(size_t)c * (T + 1) + T] = sel;
+  }
+  __syncthreads();
+  for (int t = T - 1; t >= 0; --t) {
+    const int jq = 1 + (f.fl.nQ > 1 ? t : 0);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const double* xi = P + ((size_t)t * N + i) * d;
+      for (int k = 0; k < d; ++k) r[k] = chosen[k] - dyn_mean_i(tg, t, xi, k);
+      alpha[i] = A[(size_t)t * N + i] + gauss_term(d, r, f.L(jq), f.logdet[jq]);
+    }
+    __syncthreads();
+    if (!block_normalize(N, alpha, W, red)) {
+      if (threadIdx.x == 0) { a.status[c] = AUXMC_E_DEGENERATE; a.bad_t[c] = t; }
+      return;
+    }
+    block_cumsum(N, W, cum);
+    if (threadIdx.x == 0) {
+      const int sel = draw_index(N, cum, uniform_at(derive(it, kBackwardIndex, (uint64_t)t), 0));
+      for (int k = 0; k < d; ++k) chosen[k] = tr[(size_t)t * d + k] = P[((size_t)t * N + sel) * d + k];
+      tk[t] = pm_key(t, sel);
+      if (a.sel) a.sel[(size_t)c * (T + 1) + t] = sel;
+    }
+    __syncthreads();
+  }
+}
+
 // Forward log-messages alpha_t(j) = lw_t(j) + LSE_i(alpha_{t-1}(i) + log p(x_t^j | x_{t-1}^i)),
 // one CTA per chain, then backward index sampling with the reference's addresses.
-template <int DT>
 __global__ void k_pit_forward_backward(DevTarget tg, FactorRef f, PgArgs a, const double* lw) {
   extern __shared__ double sm[];
   const int N = a.N, T = tg.T, d = tg.dx;
@@ -602,130 +1020,6 @@ __global__ void k_pit_forward_backward(DevTarget tg, FactorRef f, PgArgs a, cons
     const int jq = jq0 + (f.fl.nQ > 1 ? t - 1 : 0);
     const double* LQ = f.L(jq);
     const double ldq = f.logdet[jq];
-    if constexpr (DT > 0) {
-      // Whitened form: with v_i = L_Q^{-1} m_i (previous particles' dynamics
-      // means) and w_j = L_Q^{-1} x_t^j, log p(x_t^j | x_{t-1}^i) = M - |w_j - v_i|^2 / 2,
-      // M = -d/2 log 2π - log|L_Q|: no triangular solve (and no division) per pair.
-      // Every term is <= M and alpha - am <= 0, so exp(.) never overflows; P
-      // thread groups split the i range (fixed order partial sums).
-      double* vi = mprev;  // N*DT, whitened in place
-      double* ai = cum;    // alpha_i - am
-      for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        double z[DT];
-#pragma unroll
-        for (int k = 0; k < DT; ++k) {
-          double acc = mprev[i * DT + k];
-#pragma unroll
-          for (int l = 0; l < k; ++l) acc -= LQ[k * DT + l] * z[l];
-          z[k] = acc / LQ[k * DT + k];
-        }
-#pragma unroll
-        for (int k = 0; k < DT; ++k) vi[i * DT + k] = z[k];
-        ai[i] = alpha[i] - am;
-      }
-      __syncthreads();
-      const double M = -0.5 * (DT * kLog2Pi) - ldq;
-      const int parts = blockDim.x / N > 0 ? blockDim.x / N : 1;
-      const int part = threadIdx.x / N;
-      const int ilo = part * (N / parts), ihi = part == parts - 1 ? N : ilo + N / parts;
-      for (int j = threadIdx.x % N; j < N && part < parts; j += (blockDim.x < N ? blockDim.x : N)) {
-        const double* xj = P + ((size_t)t * N + j) * DT;
-        double w[DT];
-#pragma unroll
-        for (int k = 0; k < DT; ++k) {
-          double acc = xj[k];
-#pragma unroll
-          for (int l = 0; l < k; ++l) acc -= LQ[k * DT + l] * w[l];
-          w[k] = acc / LQ[k * DT + k];
-        }
-        double acc4[4] = {0.0, 0.0, 0.0, 0.0};
-        int i = ilo;
-        for (; i + 4 <= ihi; i += 4) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            double sq = 0.0;
-#pragma unroll
-            for (int k = 0; k < DT; ++k) {
-              const double z = w[k] - vi[(i + u) * DT + k];
-              sq += z * z;
-            }
-            acc4[u] += exp_nonpos(ai[i + u] - 0.5 * sq);
-          }
-        }
-        for (; i < ihi; ++i) {
-          double sq = 0.0;
-#pragma unroll
-          for (int k = 0; k < DT; ++k) {
-            const double z = w[k] - vi[i * DT + k];
-            sq += z * z;
-          }
-          acc4[0] += exp_nonpos(ai[i] - 0.5 * sq);
-        }
-        const double sp = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-        if (parts == 1) {
-          double s = sp, m = 0.0;
-          if (!(s > 0.0)) {  // total underflow: exact online log-sum-exp relative to M
-            m = -INFINITY;
-            s = 0.0;
-            for (int i2 = 0; i2 < N; ++i2) {
-              double sq = 0.0;
-#pragma unroll
-              for (int k = 0; k < DT; ++k) {
-                const double z = w[k] - vi[i2 * DT + k];
-                sq += z * z;
-              }
-              const double v = ai[i2] - 0.5 * sq;
-              if (v > m) {
-                s = s * exp(m - v) + 1.0;
-                m = v;
-              } else {
-                s += exp(v - m);
-              }
-            }
-          }
-          W[j] = LW[(size_t)t * N + j] + (am + ((M + m) + log(s)));
-        } else {
-          partial[part * N + j] = sp;
-        }
-      }
-      if (parts > 1) {
-        __syncthreads();
-        for (int j = threadIdx.x; j < N; j += blockDim.x) {
-          double s = 0.0;
-          for (int p2 = 0; p2 < parts; ++p2) s += partial[p2 * N + j];
-          double m = 0.0;
-          if (!(s > 0.0)) {
-            const double* xj = P + ((size_t)t * N + j) * DT;
-            double w[DT];
-#pragma unroll
-            for (int k = 0; k < DT; ++k) {
-              double acc = xj[k];
-#pragma unroll
-              for (int l = 0; l < k; ++l) acc -= LQ[k * DT + l] * w[l];
-              w[k] = acc / LQ[k * DT + k];
-            }
-            m = -INFINITY;
-            s = 0.0;
-            for (int i2 = 0; i2 < N; ++i2) {
-              double sq = 0.0;
-#pragma unroll
-              for (int k = 0; k < DT; ++k) {
-                const double z = w[k] - vi[i2 * DT + k];
-                sq += z * z;
-              }
-              const double v = ai[i2] - 0.5 * sq;
-              if (v > m) {
-                s = s * exp(m - v) + 1.0;
-                m = v;
-              } else {
-                s += exp(v - m);
-              }
-            }
-          }
-          W[j] = LW[(size_t)t * N + j] + (am + ((M + m) + log(s)));
-        }
-      }
-    } else {
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
       const double* xj = P + ((size_t)t * N + j) * d;
       double m = -INFINITY, s = 0.0;  // online log-sum-exp over i
@@ -740,7 +1034,6 @@ __global__ void k_pit_forward_backward(DevTarget tg, FactorRef f, PgArgs a, cons
         }
       }
       W[j] = LW[(size_t)t * N + j] + (am + (m + log(s)));
-    }
     }
     __syncthreads();
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
@@ -828,6 +1121,48 @@ __global__ void k_pg_adapt(int C, const long long* iter, const double* last_upda
   delta[c] = exp(log(delta[c]) + pow(n, -0.6) * (last_update[c] - target));
 }
 
+template <int DT>
+static int launch_pit_forward_dt(int C, int CS, int threads, size_t smem, cudaStream_t s,
+                                 const DevTarget& tg, const FactorRef& f, const PgArgs& a,
+                                 const double* lw, double* V, double* X) {
+  const long long n = (long long)C * tg.T * a.N;
+  if (n > 0)
+    AUXMC_LAUNCH(k_pit_whiten<DT>, (int)std::min<long long>((n + 255) / 256, 148LL * 64), 256, 0, s,
+                 tg, f, a, V, X);
+  auto kern = k_pit_forward_cluster<DT>;
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * CS);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const bool prof = g_prof_on.load(std::memory_order_relaxed);
+  if (prof) prof_mark("k_pit_forward_cluster", s, true);
+  AUXMC_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tg, f, a, lw, (const double*)V, (const double*)X, CS));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (prof) prof_mark("k_pit_forward_cluster", s, false);
+  return AUXMC_OK;
+}
+
+static int launch_pit_forward(int d, int C, int CS, int threads, size_t smem, cudaStream_t s,
+                              const DevTarget& tg, const FactorRef& f, const PgArgs& a,
+                              const double* lw, double* V, double* X) {
+  switch (d) {
+#define PCASE(DT) \
+  case DT: return launch_pit_forward_dt<DT>(C, CS, threads, smem, s, tg, f, a, lw, V, X);
+    PCASE(1) PCASE(2) PCASE(3) PCASE(4) PCASE(5) PCASE(6) PCASE(7) PCASE(8)
+#undef PCASE
+  }
+  return AUXMC_E_DIM;
+}
+
 static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int mode, int variant, Arena& ws,
                    cudaStream_t s) {
   const int C = ch->C, N = ch->N, T = tg.T, d = tg.dx;
@@ -838,6 +1173,12 @@ static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int mode, int varia
   double* part = ws.take<double>((size_t)C * (T + 1) * N * d);
   double* Wt = ws.take<double>((size_t)C * (T + 1) * N);
   double* lw = variant == AUXMC_CSMC_PIT ? ws.take<double>((size_t)C * (T + 1) * N) : nullptr;
+  // few-chain PIT: cluster forward + precomputed backward draws (k_pit_backward_table)
+  const bool pit_few = variant == AUXMC_CSMC_PIT && d <= 8 && N >= 64 && C * 8 <= num_sms();
+  int* seltab = pit_few && T > 0 ? ws.take<int>((size_t)C * T * N) : nullptr;
+  const bool pit_small = variant == AUXMC_CSMC_PIT && d <= 8;
+  double* pV = pit_small ? ws.take<double>((size_t)C * T * N * d + 1) : nullptr;
+  double* pX = pit_small ? ws.take<double>((size_t)C * T * N * d + 1) : nullptr;
   double* traj = ws.take<double>((size_t)C * (T + 1) * d);
   uint64_t* tkeys = ws.take<uint64_t>((size_t)C * (T + 1));
   double* Ls = ws.take<double>((size_t)fl.total() * fl.W * fl.W);
@@ -852,6 +1193,7 @@ static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int mode, int varia
   if (!it || !u || !mq || !part || !Wt || !traj || !tkeys || !Ls || !logdet || !ints ||
       (variant == AUXMC_CSMC_PIT && !lw))
     return AUXMC_E_WORKSPACE;
+  if ((pit_few && T > 0 && !seltab) || (pit_small && (!pV || !pX))) return AUXMC_E_WORKSPACE;
   AUXMC_CUDA_TRY(cudaMemsetAsync(ch->status, 0, sizeof(int) * C, s));
   AUXMC_CUDA_TRY(cudaMemsetAsync(ch->bad_t, 0xff, sizeof(int) * C, s));
   AUXMC_CUDA_TRY(cudaMemsetAsync(ints, 0, sizeof(int) * (C + 1), s));
@@ -885,24 +1227,34 @@ static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int mode, int varia
     const long long np = nct * N;
     AUXMC_LAUNCH(k_pit_particles, (int)std::min<long long>((np + 255) / 256, 148LL * 64), 256, 0, s,
                  tg, f, a, lw);
-    // PIT forward: 2 thread groups split each LSE for N = 256 (16 warps per SM)
-    const int pthreads = N <= 512 ? std::min(1024, 2 * ((N + 31) / 32) * 32) : threads;
-    const size_t smem = sizeof(double) * (3 * N + (size_t)N * d + 40 + 64 +
-                                          (size_t)std::max(1, pthreads / N) * N);
-    switch (d) {
-#define PCASE(DT)                                                                        \
-  case DT:                                                                               \
-    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pit_forward_backward<DT>,                      \
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                        (int)smem));                                     \
-    AUXMC_LAUNCH((k_pit_forward_backward<DT>), C, pthreads, smem, s, tg, f, a, lw);      \
-    break;
-      PCASE(1) PCASE(2) PCASE(3) PCASE(4) PCASE(5) PCASE(6) PCASE(7) PCASE(8)
-#undef PCASE
-      default:
-        AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pit_forward_backward<0>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        AUXMC_LAUNCH((k_pit_forward_backward<0>), C, threads, smem, s, tg, f, a, lw);
+    if (d <= 8) {
+      // cluster-parallel forward messages: 8 SMs per chain when the batch leaves SMs idle
+      const int CS = pit_few ? 8 : 1;
+      const int JLmax = (N + CS - 1) / CS;
+      const int fthreads = 1024;
+      const size_t fsmem = sizeof(double) * (2 * (size_t)N + 2 * (size_t)N * d + 2 * (size_t)JLmax * d +
+                                             N + kPitParts * JLmax + 2 * CS + 40);
+      int rc2 = launch_pit_forward(d, C, CS, fthreads, fsmem, s, tg, f, a, lw, pV, pX);
+      if (rc2) return rc2;
+      if (pit_few && T > 0) {
+        const size_t tsmem = sizeof(double) * ((size_t)N * d + N);
+        AUXMC_LAUNCH(k_pit_backward_table, C * T, threads, tsmem, s, tg, f, a, seltab);
+        const size_t csmem = sizeof(double) * (3 * (size_t)N + 40) +
+                             sizeof(int) * ((size_t)kChaseBlock * (N + 1) + 1);
+        AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pit_backward_chase,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+        AUXMC_LAUNCH(k_pit_backward_chase, C, threads, csmem, s, tg, a, seltab);
+      } else {
+        const size_t bsmem = sizeof(double) * (3 * (size_t)N + 40 + 64);
+        AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pit_backward, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)bsmem));
+        AUXMC_LAUNCH(k_pit_backward, C, threads, bsmem, s, tg, f, a);
+      }
+    } else {
+      const size_t smem = sizeof(double) * (3 * N + (size_t)N * d + 40 + 64 + (size_t)N);
+      AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pit_forward_backward,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      AUXMC_LAUNCH((k_pit_forward_backward), C, threads, smem, s, tg, f, a, lw);
     }
   }
   AUXMC_LAUNCH(k_pg_commit, C, 256, 0, s, C, T, d, traj, tkeys, ch->status, ch->x, ch->keys,

@@ -1,0 +1,5 @@
+# PIT cSMC: cluster forward pass
+timeout 900 python -m pytest tests/test_gpu_fkpg.py tests/test_gpu_shapes.py tests/test_gpu_failures.py -q -m gpu -k "pit or fkpg or c4 or collapse" 2>&1 | tail -3
+for c in c4_1chain c4; do :; done
+timeout 600 python bench.py --config c4 --chains 1 --no-e2e --no-cpu 2>/dev/null | python -c "import json,sys; l=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c4 1 chain', l['ms_per_step'], l['value'])"
+timeout 600 python bench.py --config c4 --no-e2e --no-cpu 2>/dev/null | python -c "import json,sys; l=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c4 148 chains', l['ms_per_step'], l['value'], l['roofline']['frac'])"
