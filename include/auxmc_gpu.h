@@ -369,7 +369,18 @@ typedef struct {
   int* bad_t;           /* [C] step named by DegenerateWeightsError */
   int* ancestors;       /* optional [C][T+1][N] trace of ancestor indices (NULL = off) */
   int* selected;        /* optional [C][T+1] trace of selected indices (NULL = off) */
+  int pm_kind;          /* pseudo-marginal potentials (fkpg.cpp:233-250 pm_potential), AUXMC_PM_* */
 } auxmc_pg_chains;
+/* Pseudo-marginal wrappers of the auxiliary FK potentials (reference cSMC only).  The
+ * reference wraps any user estimator (t, x_prev, x, key) -> est >= 0; on the device the
+ * estimator is one of a fixed family evaluated from the particle's aux key
+ * (st.derive(kPmKey, i).next_key(), fkpg.cpp:72), log g' = est > 0 ? log(est) : -inf, and
+ * NaN or est < 0 is the reference's ContractError (AUXMC_E_CONTRACT, bad_t = t):       */
+#define AUXMC_PM_NONE 0       /* the plain potentials */
+#define AUXMC_PM_TWO_POINT 1  /* est = exp(log g) * (U(key) < 0.5 ? 0.5 : 1.5), unbiased
+                                 (acceptance.cpp:249-290, test_fkpg.cpp:402-434) */
+#define AUXMC_PM_EXACT 2      /* est = exp(log g): zero variance (test_fkpg.cpp:365-381) */
+#define AUXMC_PM_NEGATIVE 3   /* est = -0.1: contract violation (test_fkpg.cpp:436-445) */
 
 int auxmc_aux_pgibbs_step(const auxmc_target* target, auxmc_pg_chains* chains, int mode,
                           int variant, void* workspace, size_t workspace_bytes, void* stream);

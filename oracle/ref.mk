@@ -40,7 +40,7 @@ $(OUT)/libauxmc_ref.so: $(LIB_OBJS)
 # C bridge (oracle/ref_bridge.cpp, our code): flat extern "C" entry points over the
 # reference's C++ API for the Python parity tests and the CPU baseline.
 $(OUT)/libref_bridge.so: $(HERE)ref_bridge.cpp $(OUT)/libauxmc_ref.so $(SHIM_DEPS)
-	$(CXX) $(CXXFLAGS) $(INC) -shared -o $@ $< -L$(OUT) -lauxmc_ref -Wl,-rpath,'$$ORIGIN' -lpthread
+	$(CXX) $(CXXFLAGS) $(INC) -I$(REF)/tests -shared -o $@ $< -L$(OUT) -lauxmc_ref -Wl,-rpath,'$$ORIGIN' -lpthread
 
 $(OUT)/auxmc_tests: $(TEST_OBJS) $(OUT)/libauxmc_ref.so
 	$(CXX) -o $@ $(TEST_OBJS) -L$(OUT) -lauxmc_ref -Wl,-rpath,'$$ORIGIN' -lpthread

@@ -27,6 +27,7 @@
 #include "auxmc/rng.hpp"
 #include "auxmc/target.hpp"
 #include "auxmc/testhooks.hpp"
+#include "testutil.hpp"  // the reference's own test targets (proj/tests/testutil.hpp:86-140)
 
 using namespace auxmc;
 
@@ -255,6 +256,15 @@ void* rb_target_test(int kind, int T) {
       {Mat::Constant(1, 1, 0.04)}, std::move(pots)));
 }
 
+// The LGSSM posterior as a target: exact Gaussian potentials (testutil.hpp:88-108) or the
+// same factors as generic log-potentials (:112-140).
+void* rb_target_lgssm(const void* model, const double* obs, int generic) {
+  const auto& m = *static_cast<const lgssm::Model*>(model);
+  const Mat o = mat_in(obs, m.horizon() + 1, m.dy());
+  return new auxk::GenSSMTarget(generic ? testutil::lgssm_target_generic(m, o)
+                                        : testutil::lgssm_target_exact(m, o));
+}
+
 // ---------------------------------------------------------------- LGSSM (lgssm.cpp)
 void* rb_lgssm_synthetic(const rb_spec* s, int* status) {
   lgssm::Model* m = nullptr;
@@ -423,6 +433,40 @@ int rb_pg_step(const void* tg, void* s, int N, std::uint64_t root_key, int mode,
     return RB_E_OTHER;
   }
 }
+// aux_pgibbs_step with PgOptions::fk_transform = pm_potential(fk, estimator) and the
+// estimators of the reference's own tests (auxmc_gpu.h AUXMC_PM_*): 1 two-point noise
+// (acceptance.cpp:256-268), 2 exact (test_fkpg.cpp:370-373), 3 negative (:441-442).
+int rb_pg_step_pm(const void* tg, void* s, int N, std::uint64_t root_key, int mode, int pm, int* bad_t) {
+  const auto& t = *static_cast<const auxk::GenSSMTarget*>(tg);
+  auto& st = *static_cast<fkpg::PGState*>(s);
+  fkpg::PgOptions o;
+  o.mode = static_cast<fkpg::ProposalMode>(mode);
+  o.fk_transform = [pm](const fkpg::FeynmanKacModel& fk) {
+    fkpg::FeynmanKacModel orig = fk;
+    return fkpg::pm_potential(fk, [orig, pm](int t, const Vec& prev, const Vec& cur, std::uint64_t key) {
+      if (pm == 3) return -0.1;
+      const double lg = t == 0 ? orig.log_g0(cur, 0) : orig.log_g(t, prev, cur, 0);
+      if (pm == 2) return std::exp(lg);
+      RngStream ks = RngStream::from_key(key);
+      const double eps = ks.next_uniform() < 0.5 ? 0.5 : 1.5;
+      return std::exp(lg) * eps;
+    });
+  };
+  *bad_t = -1;
+  try {
+    fkpg::aux_pgibbs_step(t, st, N, RngStream::from_key(root_key), o);
+    return RB_OK;
+  } catch (const ContractError&) {
+    return RB_E_CONTRACT;
+  } catch (const DegenerateWeightsError& e) {
+    const char* p = std::strstr(e.what(), "t=");
+    if (p) *bad_t = std::atoi(p + 2);
+    return RB_E_DEGENERATE;
+  } catch (const std::exception&) {
+    return RB_E_OTHER;
+  }
+}
+
 void rb_pg_adapt(void* s, double rate) { fkpg::adapt_delta(*static_cast<fkpg::PGState*>(s), rate); }
 // scal: delta, last_update; ints: iter, updates
 void rb_pg_get(const void* s, double* x, std::uint64_t* keys, double* scal, long* ints) {

@@ -70,6 +70,7 @@ def _declare(L):
         "rb_target_new": (VP, [SP, PD, C.c_int, PI]),
         "rb_target_free": (None, [VP]),
         "rb_target_test": (VP, [C.c_int, C.c_int]),
+        "rb_target_lgssm": (VP, [VP, PD, C.c_int]),
         "rb_log_gamma": (C.c_double, [VP, PD, PI]),
         "rb_grad_pot": (C.c_int, [VP, C.c_int, PD, C.c_int, PD]),
         "rb_log_pot": (C.c_double, [VP, C.c_int, PD]),
@@ -94,6 +95,7 @@ def _declare(L):
         "rb_pg_free": (None, [VP]),
         "rb_pg_step": (C.c_int, [VP, VP, C.c_int, C.c_uint64, C.c_int, PI]),
         "rb_pg_adapt": (None, [VP, C.c_double]),
+        "rb_pg_step_pm": (C.c_int, [VP, VP, C.c_int, C.c_uint64, C.c_int, C.c_int, PI]),
         "rb_pg_get": (None, [VP, PD, PU64, PD, PL]),
         "rb_csmc_trace": (C.c_int, [VP, PD, PU64, PD, C.c_double, C.c_int, C.c_uint64, C.c_int,
                                     PI, PD, PI]),
@@ -185,6 +187,16 @@ class RTarget:
 
 def make_target(s: O.Spec, data) -> RTarget:
     return RTarget(s, data)
+
+
+def target_from_lgssm(m, obs, generic=False) -> RTarget:
+    """testutil.hpp:88-140: the LGSSM posterior with exact or generic potentials."""
+    rm = model(m)
+    t = RTarget.__new__(RTarget)
+    t.T, t.dx, t.data = rm.T, rm.dx, _f64(obs)
+    t._model = rm
+    t.h = lib().rb_target_lgssm(rm.h, _p(t.data), int(generic))
+    return t
 
 
 def test_target(name: str, T: int) -> RTarget:
@@ -360,10 +372,14 @@ class PGChain:
         except Exception:
             pass
 
-    def step(self, N, root, mode=1):
-        """aux_pgibbs_step; returns (status, bad_t)."""
+    def step(self, N, root, mode=1, pm=0):
+        """aux_pgibbs_step; returns (status, bad_t).  pm: the pseudo-marginal estimator
+        (fkpg.cpp:233-250) of the reference's tests, see rb_pg_step_pm."""
         bad = C.c_int(-1)
-        st = lib().rb_pg_step(self.tg.h, self.h, N, _key(root), mode, C.byref(bad))
+        if pm:
+            st = lib().rb_pg_step_pm(self.tg.h, self.h, N, _key(root), mode, pm, C.byref(bad))
+        else:
+            st = lib().rb_pg_step(self.tg.h, self.h, N, _key(root), mode, C.byref(bad))
         return st, bad.value
 
     def adapt(self, target_rate):

@@ -78,7 +78,8 @@ class PgChains(C.Structure):
     _fields_ = [("C", C.c_int), ("N", C.c_int), ("x", C.c_void_p), ("keys", C.c_void_p),
                 ("delta", C.c_void_p), ("iter", C.c_void_p), ("updates", C.c_void_p),
                 ("last_update", C.c_void_p), ("root_keys", C.c_void_p), ("status", C.c_void_p),
-                ("bad_t", C.c_void_p), ("ancestors", C.c_void_p), ("selected", C.c_void_p)]
+                ("bad_t", C.c_void_p), ("ancestors", C.c_void_p), ("selected", C.c_void_p),
+                ("pm_kind", C.c_int)]
 
 
 class ModelSpec(C.Structure):

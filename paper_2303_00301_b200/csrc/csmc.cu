@@ -256,7 +256,28 @@ struct PgArgs {
   const double* adf;  // ADAPTED: [C][nad][2 d^2 + 1] gain | L | logdet per proposal class
   int nad;
   const int* ad_bad;  // ADAPTED: [C] factorization failure of a proposal class
+  int pm;             // AUXMC_PM_*: pseudo-marginal estimator of the potentials
 };
+
+// pm_potential (fkpg.cpp:233-250) with the device estimator family: the estimate from
+// the particle's aux key, NaN / negative -> ContractError (flagged), log(est) or -inf.
+__device__ __forceinline__ double pm_apply(int kind, double lg, uint64_t key, int* contract) {
+  if (kind == AUXMC_PM_NONE) return lg;
+  double est;
+  if (kind == AUXMC_PM_TWO_POINT) {
+    const double eps = uniform_at(key, 0) < 0.5 ? 0.5 : 1.5;
+    est = exp(lg) * eps;
+  } else if (kind == AUXMC_PM_EXACT) {
+    est = exp(lg);
+  } else {
+    est = -0.1;
+  }
+  if (est != est || est < 0.0) {
+    atomicOr(contract, 1);
+    return -INFINITY;
+  }
+  return est > 0.0 ? log(est) : -INFINITY;
+}
 
 // proposal class of step t: 0 = prior at t = 0 (m0, P0), 1 + j = dynamics with Q_j
 __device__ __forceinline__ int prop_class(const FactorRef& f, int t) {
@@ -363,6 +384,7 @@ __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
   double* red = cum + N;       // 40
   double* chosen = red + 40;   // d
   int* anc = reinterpret_cast<int*>(chosen + 64);  // N
+  int* contract = anc + N;     // pseudo-marginal ContractError flag
   const double delta = a.delta[c];
   const double sq2 = sqrt(delta / 2.0);  // LLT of (δ/2) I (gauss.cpp:64-67)
   const uint64_t it = a.it[c];
@@ -381,6 +403,14 @@ __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
     if (threadIdx.x == 0) { a.status[c] = AUXMC_E_FACTOR; a.bad_t[c] = 0; }
     return;
   }
+  double* tr = a.traj + (size_t)c * (T + 1) * d;
+  uint64_t* tk = a.tkeys + (size_t)c * (T + 1);
+  auto pm_key = [&](int t, int i) -> uint64_t {
+    if (i == 0) return a.keys[(size_t)c * (T + 1) + t];
+    return key_at(derive(derive(it, kStep, (uint64_t)t), kPmKey, (uint64_t)i), 0);
+  };
+  if (threadIdx.x == 0) *contract = 0;
+  __syncthreads();
   for (int t = 0; t <= T; ++t) {
     const uint64_t st = derive(it, kStep, (uint64_t)t);
     if (t > 0) {
@@ -418,7 +448,7 @@ __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
           for (int k = 0; k < d; ++k) r[k] = xv[k] - pmean[k];
           lg += ld - gauss_term(d, r, Lp, ldp);
         }
-        logw[i] = lg;
+        logw[i] = a.pm ? pm_apply(a.pm, lg, pm_key(t, i), contract) : lg;
         if (a.anc) a.anc[((size_t)c * (T + 1) + t) * N + i] = t > 0 ? anc[i] : 0;
         continue;
       }
@@ -429,11 +459,16 @@ __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
         for (int k = 0; k < d; ++k) xv[k] = mqc[(size_t)t * d + k] + sq2 * normal_at(pk, (uint64_t)k);
       }
       for (int k = 0; k < d; ++k) P[((size_t)t * N + i) * d + k] = xv[k];
-      logw[i] = potential_dev(tg, f, t, parent, xv, uc + (size_t)t * d, mqc + (size_t)t * d, delta,
-                              sq2, r);
+      const double lgp = potential_dev(tg, f, t, parent, xv, uc + (size_t)t * d, mqc + (size_t)t * d,
+                                       delta, sq2, r);
+      logw[i] = a.pm ? pm_apply(a.pm, lgp, pm_key(t, i), contract) : lgp;
       if (a.anc) a.anc[((size_t)c * (T + 1) + t) * N + i] = t > 0 ? anc[i] : 0;
     }
     __syncthreads();
+    if (*contract) {  // ContractError from the pseudo-marginal estimator (fkpg.cpp:241-243)
+      if (threadIdx.x == 0) { a.status[c] = AUXMC_E_CONTRACT; a.bad_t[c] = t; }
+      return;
+    }
     if (!block_normalize(N, logw, W, red)) {
       if (threadIdx.x == 0) { a.status[c] = AUXMC_E_DEGENERATE; a.bad_t[c] = t; }
       return;
@@ -443,12 +478,6 @@ __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
   }
   // terminal index (fkpg.cpp:127-133) and backward index sampling (:135-150)
   block_cumsum(N, W, cum);
-  double* tr = a.traj + (size_t)c * (T + 1) * d;
-  uint64_t* tk = a.tkeys + (size_t)c * (T + 1);
-  auto pm_key = [&](int t, int i) -> uint64_t {
-    if (i == 0) return a.keys[(size_t)c * (T + 1) + t];
-    return key_at(derive(derive(it, kStep, (uint64_t)t), kPmKey, (uint64_t)i), 0);
-  };
   if (threadIdx.x == 0) {
     const int sel = draw_index(N, cum, uniform_at(derive(it, kTerminalIndex, 0), 0));
     for (int k = 0; k < d; ++k) {
@@ -475,14 +504,20 @@ __global__ void k_csmc_reference(DevTarget tg, FactorRef f, PgArgs a) {
         double lg = log_pot_dev(tg, f, t + 1, chosen, r) +
                     iso_dev(d, uc + (size_t)(t + 1) * d, chosen, delta / 2.0);
         if (a.mode == AUXMC_PG_ADAPTED) lg += log_dyn_dev(tg, f, t, xi, chosen, r) - lq;
+        if (a.pm) lg = pm_apply(a.pm, lg, tk[t + 1], contract);
         logw[i] = log(Wg[(size_t)t * N + i]) + lq + lg;
         continue;
       }
-      const double lg = potential_dev(tg, f, t + 1, xi, chosen, uc + (size_t)(t + 1) * d, mq1,
-                                      delta, sq2, r);
+      double lg = potential_dev(tg, f, t + 1, xi, chosen, uc + (size_t)(t + 1) * d, mq1,
+                                delta, sq2, r);
+      if (a.pm) lg = pm_apply(a.pm, lg, tk[t + 1], contract);
       logw[i] = log(Wg[(size_t)t * N + i]) + mlp + lg;
     }
     __syncthreads();
+    if (*contract) {
+      if (threadIdx.x == 0) { a.status[c] = AUXMC_E_CONTRACT; a.bad_t[c] = t; }
+      return;
+    }
     if (!block_normalize(N, logw, W, red)) {
       if (threadIdx.x == 0) { a.status[c] = AUXMC_E_DEGENERATE; a.bad_t[c] = t; }
       return;
@@ -1216,10 +1251,10 @@ static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int mode, int varia
                  ch->delta, adf, ad_bad);
   }
   PgArgs a{C, N, ch->x, ch->keys, ch->delta, it, u, mq, part, Wt, traj, tkeys, ch->status,
-           ch->bad_t, ch->ancestors, ch->selected, ints, mode, adf, nad, ad_bad};
+           ch->bad_t, ch->ancestors, ch->selected, ints, mode, adf, nad, ad_bad, ch->pm_kind};
   const int threads = N >= 256 ? 256 : ((N + 31) / 32) * 32;
   if (variant == AUXMC_CSMC_REFERENCE) {
-    const size_t smem = sizeof(double) * (3 * N + 40 + 64) + sizeof(int) * N;
+    const size_t smem = sizeof(double) * (3 * N + 40 + 64) + sizeof(int) * (N + 1);
     AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_csmc_reference,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     AUXMC_LAUNCH(k_csmc_reference, C, threads, smem, s, tg, f, a);
@@ -1287,6 +1322,9 @@ int auxmc_aux_pgibbs_step(const auxmc_target* target, auxmc_pg_chains* chains, i
   if (variant != AUXMC_CSMC_REFERENCE && variant != AUXMC_CSMC_PIT) return AUXMC_E_ARG;
   // the PIT lattice needs parent-free (independent) proposals: gradient mode only
   if (variant == AUXMC_CSMC_PIT && mode != AUXMC_PG_GRADIENT) return AUXMC_E_ARG;
+  if (chains && (chains->pm_kind < AUXMC_PM_NONE || chains->pm_kind > AUXMC_PM_NEGATIVE ||
+                 (chains->pm_kind != AUXMC_PM_NONE && variant != AUXMC_CSMC_REFERENCE)))
+    return AUXMC_E_ARG;
   if (!chains || chains->C < 0 || chains->N < 1 || chains->N > 4096 || !chains->x ||
       !chains->keys || !chains->delta || !chains->iter || !chains->updates ||
       !chains->last_update || !chains->root_keys || !chains->status || !chains->bad_t)

@@ -32,9 +32,18 @@ class Variant:
     kPit = 1
 
 
+class PseudoMarginal:
+    """Device pseudo-marginal estimators (auxmc_gpu.h AUXMC_PM_*): the reference's
+    pm_potential (fkpg.cpp:233-250) with the estimators of its own tests."""
+    kNone = 0
+    kTwoPoint = 1   # exp(log g) * (U(key) < 0.5 ? 0.5 : 1.5), acceptance.cpp:249-290
+    kExact = 2      # exp(log g), test_fkpg.cpp:365-381
+    kNegative = 3   # -0.1: ContractError, test_fkpg.cpp:436-445
+
+
 class PGChains:
     def __init__(self, target: GenSSMTarget, x0, delta, root_keys: torch.Tensor, N: int,
-                 trace: bool = False):
+                 trace: bool = False, pm: int = 0):
         dev = target.device
         self.target, self.N = target, int(N)
         Cn = root_keys.shape[0]
@@ -56,6 +65,7 @@ class PGChains:
         self.selected = torch.zeros((Cn, T1), dtype=torch.int32, device=dev) if trace else None
         self._ws = None
         self._ws_variant = None
+        self.pm = int(pm)  # PseudoMarginal.* (fkpg.cpp:233-250 with a device estimator)
 
     def raw(self) -> _lib.PgChains:
         r = _lib.PgChains()
@@ -65,6 +75,7 @@ class PGChains:
         r.updates, r.last_update, r.root_keys = p(self.updates), p(self.last_update), p(self.root_keys)
         r.status, r.bad_t = p(self.status), p(self.bad_t)
         r.ancestors, r.selected = p(self.ancestors), p(self.selected)
+        r.pm_kind = self.pm
         return r
 
     def aux_pgibbs_step(self, variant=Variant.kReference, mode=ProposalMode.kGradient, stream=None):
