@@ -324,27 +324,41 @@ int auxmc_gamma_move(const auxmc_target* target, int C, const double* x,
                      int* moved, void* stream);
 
 /* ---- time-sharded auxiliary Kalman step (one chain, kernel_step, auxk.cpp:130-198,
- * with the prefix backend and the scan filter split over ranks; tshard.py drives it):
- *   begin: iteration key, aux observations, surrogate LGSSM at x (described in
- *          model_out; pseudo-observations at *z_out) — whole horizon, every rank;
- *   the caller: sharded filter of (model, z), sharded prefix draw with the key at
- *          *it_out, all-gather of the path into *prop_out;
- *   middle: log q(x'|x), log gamma(x'), gradients at x', surrogate at x' (into *z_out);
- *   the caller: sharded filter of the reverse surrogate;
- *   end: log q(x|x'), aux likelihoods, the MH decision, accept.
- * status_fwd = {filter, sampler} and status_rev = {filter} are maxima over ranks. */
+ * with the prefix backend and the scan filter split over ranks; tshard.py drives it).
+ * Rank r owns the time range [t_lo, t_hi) of whole filter super-blocks (t_hi = T+1 on
+ * the last rank) and keeps the chain's path valid on [t_lo-1, t_hi] (halo rows):
+ *   begin:  iteration key, aux observations and the surrogate LGSSM at x on the halo'd
+ *           range (model_out; pseudo-observations at *z_out);
+ *   caller: sharded filter of (model, z), sharded prefix draw with the key at *it_out
+ *           into *prop_out on [t_lo, t_hi), then the halo rows x'_{t_lo-1}, x'_{t_hi}
+ *           from the neighbours (d doubles each);
+ *   middle: per-t terms of log q(x'|x) and log gamma(x') on [t_lo, t_hi) summed per
+ *           super-block into part_out[:, 0:2], gradients at x', surrogate at x';
+ *   caller: sharded reverse filter;
+ *   end:    per-t terms of log q(x|x') and both aux likelihoods -> part_out[:, 2:5];
+ *   caller: all-gather of every rank's super-block partials and flags (a few KB);
+ *   decide: the sums in super-block order, the MH decision (every rank identical), the
+ *           accepted path on the halo'd range.
+ * part_out: [owned super-blocks][5]; flags_out: int[8] of this rank (filter / sampler /
+ * path-logpdf / log-gamma factor failures, non-finite gradients), max-reduced by the
+ * caller into decide's flags.  Every split gives the same bits: every sum is per
+ * super-block in t order, then over super-blocks in order. */
 size_t auxmc_tshard_aux_workspace(const auxmc_target* target);
 int auxmc_tshard_aux_begin(const auxmc_target* target, auxmc_chains* chains,
                            const auxmc_kernel_options* opts, void* workspace,
-                           size_t workspace_bytes, auxmc_lgssm* model_out, double** z_out,
-                           double** prop_out, uint64_t** it_out, void* stream);
+                           size_t workspace_bytes, int t_lo, int t_hi, auxmc_lgssm* model_out,
+                           double** z_out, double** prop_out, uint64_t** it_out, void* stream);
 int auxmc_tshard_aux_middle(const auxmc_target* target, auxmc_chains* chains,
                             const auxmc_kernel_options* opts, void* workspace,
-                            size_t workspace_bytes, const double* log_marginal_fwd,
-                            const int* status_fwd, void* stream);
+                            size_t workspace_bytes, int t_lo, int t_hi, double* part_out,
+                            int* flags_out, void* stream);
 int auxmc_tshard_aux_end(const auxmc_target* target, auxmc_chains* chains,
                          const auxmc_kernel_options* opts, void* workspace, size_t workspace_bytes,
-                         const double* log_marginal_rev, const int* status_rev, void* stream);
+                         int t_lo, int t_hi, double* part_out, int* flags_out, void* stream);
+int auxmc_tshard_aux_decide(const auxmc_target* target, auxmc_chains* chains, void* workspace,
+                            size_t workspace_bytes, int t_lo, int t_hi, const double* parts_all,
+                            int nsup, const double* log_marginal_fwd,
+                            const double* log_marginal_rev, const int* flags, void* stream);
 int auxmc_copy_device(void* dst, const void* src, size_t bytes, void* stream);
 /* target.log_gamma (target.cpp:100-108) of B paths. */
 int auxmc_log_gamma(const auxmc_target* target, const double* traj, int B, double* out,

@@ -152,14 +152,17 @@ SIGNATURES = {
                                   VP, VP, VP]),
     "auxmc_tshard_aux_workspace": (C.c_size_t, [C.POINTER(Target)]),
     "auxmc_tshard_aux_begin": (C.c_int, [C.POINTER(Target), C.POINTER(Chains),
-                                         C.POINTER(KernelOptions), VP, C.c_size_t,
-                                         C.POINTER(Lgssm), C.POINTER(C.c_void_p),
+                                         C.POINTER(KernelOptions), VP, C.c_size_t, C.c_int,
+                                         C.c_int, C.POINTER(Lgssm), C.POINTER(C.c_void_p),
                                          C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), VP]),
     "auxmc_tshard_aux_middle": (C.c_int, [C.POINTER(Target), C.POINTER(Chains),
-                                          C.POINTER(KernelOptions), VP, C.c_size_t, VP, VP,
-                                          VP]),
+                                          C.POINTER(KernelOptions), VP, C.c_size_t, C.c_int,
+                                          C.c_int, VP, VP, VP]),
     "auxmc_tshard_aux_end": (C.c_int, [C.POINTER(Target), C.POINTER(Chains),
-                                       C.POINTER(KernelOptions), VP, C.c_size_t, VP, VP, VP]),
+                                       C.POINTER(KernelOptions), VP, C.c_size_t, C.c_int, C.c_int,
+                                       VP, VP, VP]),
+    "auxmc_tshard_aux_decide": (C.c_int, [C.POINTER(Target), C.POINTER(Chains), VP, C.c_size_t,
+                                          C.c_int, C.c_int, VP, C.c_int, VP, VP, VP, VP]),
     "auxmc_copy_device": (C.c_int, [VP, VP, C.c_size_t, VP]),
     "auxmc_log_gamma": (C.c_int, [C.POINTER(Target), VP, C.c_int, VP, VP, VP]),
     "auxmc_aux_pgibbs_step": (C.c_int, [C.POINTER(Target), C.POINTER(PgChains), C.c_int,

@@ -19,6 +19,7 @@
 #include "dense.cuh"
 #include "rng.cuh"
 #include "target.cuh"
+#include "terms.cuh"
 
 namespace auxmc_gpu {
 
@@ -73,47 +74,13 @@ __global__ void k_target_factors(DevTarget tg, FactorLayout fl, double* Ls, doub
 __global__ void k_gamma_terms(DevTarget tg, FactorLayout fl, int C, const double* __restrict__ traj,
                               const double* __restrict__ Ls, const double* __restrict__ logdet,
                               double* terms) {
-  const int T = tg.T, d = tg.dx, W = fl.W;
+  const int T = tg.T, d = tg.dx;
   const int K = 2 * T + 2;
   const long long n = (long long)C * K;
-  double r[64];
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
        q += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(q / K), k = (int)(q % K);
-    const double* x = traj + (size_t)c * (T + 1) * d;
-    double v;
-    if (k == 0) {
-      for (int i = 0; i < d; ++i) r[i] = x[i] - tg.m0[i];
-      v = gauss_term(d, r, Ls, logdet[0]);
-    } else if (k <= T) {
-      const int t = k - 1;
-      for (int i = 0; i < d; ++i) r[i] = x[(size_t)(t + 1) * d + i] - dyn_mean_i(tg, t, x + (size_t)t * d, i);
-      const int jq = 1 + (fl.nQ > 1 ? t : 0);
-      v = gauss_term(d, r, Ls + (size_t)jq * W * W, logdet[jq]);
-    } else {
-      const int t = k - T - 1;
-      const double* xt = x + (size_t)t * d;
-      double lp = 0.0;
-      if (tg.q > 0 && tg.emask[t]) {
-        const double* H = tg.eHt(t);
-        const double* cc = tg.ect(t);
-        const double* y = tg.ey + (size_t)t * tg.q;
-        for (int i = 0; i < tg.q; ++i) {
-          double s = 0.0;
-          for (int j = 0; j < d; ++j) s += H[i * d + j] * xt[j];
-          r[i] = y[i] - (s + cc[i]);
-        }
-        const int je = 1 + fl.nQ + (tg.ne > 1 ? t : 0);
-        lp += gauss_term(tg.q, r, Ls + (size_t)je * W * W, logdet[je]);
-      }
-      if (tg.gmask[t]) {
-        const int jg = 1 + fl.nQ + fl.nE + (tg.ne > 1 ? t : 0);
-        lp += generic_log_g(tg, t, xt, fl.nG ? Ls + (size_t)jg * W * W : nullptr,
-                            fl.nG ? logdet[jg] : 0.0, r);
-      }
-      v = lp;
-    }
-    terms[q] = v;
+    terms[q] = gamma_term_k(tg, fl, traj + (size_t)c * (T + 1) * d, Ls, logdet, k);
   }
 }
 
@@ -518,6 +485,142 @@ int launch_aux_obs(int C, int T, int d, const double* x, const double* delta, co
 
 }  // namespace auxmc_gpu
 
+namespace auxmc_gpu {
+// ---- time-sharded aux step kernels (one chain; t ranges are absolute steps)
+int tshard_geometry(int T, int* LB, int* nblk, int* nsup, int* SB);
+__global__ void k_factor_list(DevModel m, int nQb, int nRb, double* Ls, double* logdet,
+                              int* status);  // logpdf.cu
+
+// aux observations (if u_out) and the surrogate LGSSM rows at the path xs on [t0, t1)
+__global__ void k_ts_prep(DevTarget tg, int zeroth, const double* __restrict__ xs,
+                          const double* __restrict__ gs, const double* __restrict__ delta,
+                          const uint64_t* __restrict__ it, int t0, int t1, int make_u,
+                          double* u, double* z, double* Fa, double* ba) {
+  const int T = tg.T, d = tg.dx, p = d + tg.q;
+  const double h = delta[0] / 2.0, sd = sqrt(delta[0] / 2.0);
+  for (int t = t0 + blockIdx.x * blockDim.x + threadIdx.x; t < t1; t += gridDim.x * blockDim.x) {
+    const double* xt = xs + (size_t)t * d;
+    if (make_u) {
+      const uint64_t k = derive(it[0], kAuxObs, (uint64_t)t);
+      for (int i = 0; i < d; ++i) u[(size_t)t * d + i] = xt[i] + sd * normal_at(k, (uint64_t)i);
+    }
+    double* zt = z + (size_t)t * p;
+    for (int i = 0; i < d; ++i) {
+      double v = u[(size_t)t * d + i];
+      if (!zeroth) v += h * gs[(size_t)t * d + i];
+      zt[i] = v;
+    }
+    for (int k = 0; k < tg.q; ++k) zt[d + k] = tg.emask[t] ? tg.ey[(size_t)t * tg.q + k] : 0.0;
+    if (!tg.linear && t < T) {
+      double* F = Fa + (size_t)t * d * d;
+      double* bb = ba + (size_t)t * d;
+      for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j) F[i * d + j] = dyn_jac_ij(tg, t, xt, i, j);
+      for (int i = 0; i < d; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < d; ++j) s += F[i * d + j] * xt[j];
+        bb[i] = dyn_mean_i(tg, t, xt, i) - s;
+      }
+    }
+  }
+}
+
+// generic gradients on [t0, t1); non-finite ones on the own range [a, b) flag an abort
+__global__ void k_ts_grads(DevTarget tg, FactorLayout fl, const double* __restrict__ traj,
+                           const double* __restrict__ Ls, int t0, int t1, int a, int b,
+                           double* grads, int* bad) {
+  const int d = tg.dx;
+  double r[64], g[64];
+  for (int t = t0 + blockIdx.x * blockDim.x + threadIdx.x; t < t1; t += gridDim.x * blockDim.x) {
+    const int jg = 1 + fl.nQ + fl.nE + (tg.ne > 1 ? t : 0);
+    generic_grad(tg, t, traj + (size_t)t * d, fl.nG ? Ls + (size_t)jg * fl.W * fl.W : nullptr, r, g);
+    bool ok = true;
+    for (int i = 0; i < d; ++i) {
+      grads[(size_t)t * d + i] = g[i];
+      ok = ok && isfinite(g[i]);
+    }
+    if (!ok && t >= a && t < b) atomicOr(bad, 1);
+  }
+}
+
+// per-t sums of a path's log-density terms: v_t = ((prior) + transition t) + observation t
+__global__ void k_ts_path_v(DevModel m, const double* __restrict__ obs, const double* __restrict__ x,
+                            const double* __restrict__ Ls, const double* __restrict__ logdet,
+                            int a, int b, double* v) {
+  const int T = m.T;
+  for (int t = a + blockIdx.x * blockDim.x + threadIdx.x; t < b; t += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    if (t == 0) s += path_term_k(m, obs, x, 0, 1, Ls, logdet, 0);
+    if (t < T) s += path_term_k(m, obs, x, 0, 1, Ls, logdet, 1 + t);
+    s += path_term_k(m, obs, x, 0, 1, Ls, logdet, T + 1 + t);
+    v[t] = s;
+  }
+}
+__global__ void k_ts_gamma_v(DevTarget tg, FactorLayout fl, const double* __restrict__ x,
+                             const double* __restrict__ Ls, const double* __restrict__ logdet,
+                             int a, int b, double* v) {
+  const int T = tg.T;
+  for (int t = a + blockIdx.x * blockDim.x + threadIdx.x; t < b; t += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    if (t == 0) s += gamma_term_k(tg, fl, x, Ls, logdet, 0);
+    if (t < T) s += gamma_term_k(tg, fl, x, Ls, logdet, 1 + t);
+    s += gamma_term_k(tg, fl, x, Ls, logdet, T + 1 + t);
+    v[t] = s;
+  }
+}
+__global__ void k_ts_aux_v(int d, const double* __restrict__ u, const double* __restrict__ x,
+                           const double* __restrict__ delta, int a, int b, double* v) {
+  const double var = delta[0] / 2.0;
+  for (int t = a + blockIdx.x * blockDim.x + threadIdx.x; t < b; t += gridDim.x * blockDim.x) {
+    double sq = 0.0;
+    for (int i = 0; i < d; ++i) {
+      const double r = u[(size_t)t * d + i] - x[(size_t)t * d + i];
+      sq += r * r;
+    }
+    v[t] = -0.5 * (d * (kLog2Pi + log(var)) + sq / var);  // gauss.cpp:59-62
+  }
+}
+// super-block partial sums (t order) of v over the rank's super-blocks
+__global__ void k_ts_sb_sum(const double* __restrict__ v, int T, int SB, int sup_lo, int sup_hi,
+                            double* part, int col) {
+  for (int s = sup_lo + blockIdx.x * blockDim.x + threadIdx.x; s < sup_hi; s += gridDim.x * blockDim.x) {
+    const int lo = s * SB, hi = min((s + 1) * SB, T + 1);
+    double acc = 0.0;
+    for (int t = lo; t < hi; ++t) acc += v[t];
+    part[(size_t)(s - sup_lo) * 5 + col] = acc;
+  }
+}
+// the MH inputs from every rank's partials (super-block order) and the reduced flags
+__global__ void k_ts_scalars(const double* __restrict__ parts, int nsup, const double* lm_fwd,
+                             const double* lm_rev, const int* __restrict__ flags, StepScalars sc) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int k = 0; k < nsup; ++k)
+    for (int c = 0; c < 5; ++c) s[c] += parts[(size_t)k * 5 + c];
+  sc.logq_fwd[0] = s[0] - lm_fwd[0];
+  sc.lg_prop[0] = s[1];
+  sc.logq_rev[0] = s[2] - lm_rev[0];
+  sc.aux_prop[0] = s[3];
+  sc.aux_x[0] = s[4];
+  sc.st_filt[0] = flags[0];
+  sc.st_samp[0] = flags[1];
+  sc.st_lqf[0] = flags[2];
+  sc.st_lg[0] = flags[3];
+  sc.bad[0] = flags[4];
+  sc.st_filt_r[0] = flags[5];
+  sc.st_lqr[0] = flags[6];
+}
+__global__ void k_ts_accept(int d, int t0, int t1, const int* accept, const double* prop,
+                            const double* gprop, double* x, double* grad) {
+  if (!accept[0]) return;
+  const long long lo = (long long)t0 * d, hi = (long long)t1 * d;
+  for (long long q = lo + blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += gridDim.x * blockDim.x) {
+    x[q] = prop[q];
+    grad[q] = gprop[q];
+  }
+}
+}  // namespace auxmc_gpu
+
 using namespace auxmc_gpu;
 
 // ---------------------------------------------------------------- time-sharded aux step
@@ -662,29 +765,47 @@ size_t auxmc_tshard_aux_workspace(const auxmc_target* target) {
   return std::max(sub.used, sub2.used) + 4096;
 }
 
+static int ts_geom(const DevTarget& tg, int t_lo, int t_hi, int* SB, int* sup_lo, int* sup_hi) {
+  int LB, nblk, nsup;
+  tshard_geometry(tg.T, &LB, &nblk, &nsup, SB);
+  if (t_lo < 0 || t_hi > tg.T + 1 || t_hi < t_lo) return AUXMC_E_ARG;
+  if (t_hi == t_lo) {  // a rank that owns no super-block
+    *sup_lo = *sup_hi = 0;
+    return AUXMC_OK;
+  }
+  if (t_lo % *SB) return AUXMC_E_ARG;
+  *sup_lo = t_lo / *SB;
+  *sup_hi = (t_hi + *SB - 1) / *SB;
+  return AUXMC_OK;
+}
+static inline int grid_t(int n) { return std::max(1, std::min((n + 127) / 128, 148 * 16)); }
+
 int auxmc_tshard_aux_begin(const auxmc_target* target, auxmc_chains* ch,
                            const auxmc_kernel_options* opts, void* workspace,
-                           size_t workspace_bytes, auxmc_lgssm* model_out, double** z_out,
-                           double** prop_out, uint64_t** it_out, void* stream) {
+                           size_t workspace_bytes, int t_lo, int t_hi, auxmc_lgssm* model_out,
+                           double** z_out, double** prop_out, uint64_t** it_out, void* stream) {
   if (!device_ok()) return AUXMC_E_CUDA;
   int st = check_target(target);
   if (st) return st;
   if (!ch || ch->C != 1 || !opts || !workspace || !model_out || !z_out || !prop_out || !it_out)
     return AUXMC_E_ARG;
   const DevTarget tg = to_dev_target(*target);
+  int SB, slo, shi;
+  if ((st = ts_geom(tg, t_lo, t_hi, &SB, &slo, &shi))) return st;
   Arena ws{(char*)workspace, workspace_bytes, 0};
   const TsAux a = ts_aux_take(tg, ws);
   if (!a.ints || !a.R) return AUXMC_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   const int T = tg.T, d = tg.dx, p = d + tg.q, nH = a.dm.nH;
+  const bool own = t_hi > t_lo;
+  const int h0 = own ? std::max(t_lo - 1, 0) : 0, h1 = own ? std::min(t_hi + 1, T + 1) : 0;
   AUXMC_CUDA_TRY(cudaMemsetAsync(a.ints, 0, sizeof(int) * 9, s));
   AUXMC_LAUNCH(k_iter_keys, 1, 32, 0, s, 1, ch->root_keys, ch->iter, a.it);
-  AUXMC_LAUNCH(k_aux_obs, grid_for((long long)(T + 1) * d), 256, 0, s, 1, T, d, ch->x, ch->delta,
-               a.it, a.u);
   AUXMC_LAUNCH(k_build_HR, grid_for((long long)nH * p * p), 256, 0, s, tg, 1, nH, ch->delta, a.H,
                a.cv, a.R);
-  AUXMC_LAUNCH(k_build_aux, grid_for((long long)(T + 1), 128), 128, 0, s, tg, 1, opts->zeroth_order,
-               ch->x, ch->grad_gen, a.u, ch->delta, a.z, a.Fa, a.ba);
+  if (h1 > h0)
+    AUXMC_LAUNCH(k_ts_prep, grid_t(h1 - h0), 128, 0, s, tg, opts->zeroth_order, ch->x, ch->grad_gen,
+                 ch->delta, a.it, h0, h1, 1, a.u, a.z, a.Fa, a.ba);
   auxmc_lgssm& m = *model_out;
   m.T = T; m.dx = d; m.dy = p;
   m.m0 = a.dm.m0; m.P0 = a.dm.P0;
@@ -696,68 +817,134 @@ int auxmc_tshard_aux_begin(const auxmc_target* target, auxmc_chains* ch,
   return AUXMC_OK;
 }
 
+// path-logpdf terms of `traj` under the current surrogate (a.dm, pseudo-observations a.z)
+static int ts_path_part(const TsAux& a, const double* traj, int t_lo, int t_hi, int SB, int slo,
+                        int shi, double* part, int col, int* fst, cudaStream_t s) {
+  const DevModel& dm = a.dm;
+  const int W = dm.dx > dm.dy ? dm.dx : dm.dy;
+  const int n_mats = 1 + dm.nQ + (dm.dy > 0 ? dm.nR : 0);
+  double *Ls = nullptr, *logdet = nullptr;
+  AUXMC_CUDA_TRY(cudaMallocAsync(&Ls, sizeof(double) * n_mats * W * W, s));
+  AUXMC_CUDA_TRY(cudaMallocAsync(&logdet, sizeof(double) * n_mats, s));
+  const int warps = factor_warps(W);
+  const size_t smem = sizeof(double) * (3 * W * W + 4) * warps;
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_factor_list, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  AUXMC_LAUNCH(k_factor_list, std::min((n_mats + warps - 1) / warps, 148 * 8), 32 * warps, smem, s,
+               dm, 1, 1, Ls, logdet, fst);
+  if (t_hi > t_lo) {
+    AUXMC_LAUNCH(k_ts_path_v, grid_t(t_hi - t_lo), 128, 0, s, dm, a.z, traj, Ls, logdet, t_lo, t_hi,
+                 a.terms);
+    AUXMC_LAUNCH(k_ts_sb_sum, 1, 128, 0, s, a.terms, dm.T, SB, slo, shi, part, col);
+  }
+  cudaFreeAsync(Ls, s);
+  cudaFreeAsync(logdet, s);
+  return AUXMC_OK;
+}
+
 int auxmc_tshard_aux_middle(const auxmc_target* target, auxmc_chains* ch,
                             const auxmc_kernel_options* opts, void* workspace,
-                            size_t workspace_bytes, const double* log_marginal_fwd,
-                            const int* status_fwd, void* stream) {
+                            size_t workspace_bytes, int t_lo, int t_hi, double* part_out,
+                            int* flags_out, void* stream) {
   if (!device_ok()) return AUXMC_E_CUDA;
   int st = check_target(target);
   if (st) return st;
-  if (!ch || ch->C != 1 || !opts || !workspace || !log_marginal_fwd || !status_fwd)
-    return AUXMC_E_ARG;
+  if (!ch || ch->C != 1 || !opts || !workspace || !part_out || !flags_out) return AUXMC_E_ARG;
   const DevTarget tg = to_dev_target(*target);
+  int SB, slo, shi;
+  if ((st = ts_geom(tg, t_lo, t_hi, &SB, &slo, &shi))) return st;
   Arena ws{(char*)workspace, workspace_bytes, 0};
   const TsAux a = ts_aux_take(tg, ws);
   if (!a.ints) return AUXMC_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
-  const int T = tg.T, p = tg.dx + tg.q;
-  // filter / sampler status of every shard (max over ranks, gathered by the caller)
-  AUXMC_CUDA_TRY(cudaMemcpyAsync(a.sc.st_filt, status_fwd, 2 * sizeof(int),
-                                 cudaMemcpyDeviceToDevice, s));
-  int rc = launch_path_logpdf(a.dm, a.z, (long long)(T + 1) * p, a.prop, log_marginal_fwd, 0, 1,
-                              a.sc.logq_fwd, a.sc.st_lqf, s);
+  const int T = tg.T;
+  const bool own = t_hi > t_lo;
+  const int h0 = own ? std::max(t_lo - 1, 0) : 0, h1 = own ? std::min(t_hi + 1, T + 1) : 0;
+  // log q(x'|x): the forward surrogate's path terms at the proposal
+  int rc = ts_path_part(a, a.prop, t_lo, t_hi, SB, slo, shi, part_out, 0, flags_out + 2, s);
   if (rc) return rc;
-  {
-    Arena sub = ws;
-    rc = launch_log_gamma(tg, 1, a.prop, a.sc.lg_prop, a.sc.st_lg, sub, s);
-    if (rc) return rc;
-    Arena sub2 = ws;
-    rc = launch_grads(tg, 1, a.prop, a.gprop, a.sc.bad, sub2, s);
-    if (rc) return rc;
+  // log gamma(x') terms and the gradients at x' (target factors)
+  const FactorLayout fl = factor_layout(tg);
+  Arena sub = ws;
+  double* Ls = sub.take<double>((size_t)fl.total() * fl.W * fl.W);
+  double* logdet = sub.take<double>(fl.total());
+  if (!Ls || !logdet) return AUXMC_E_WORKSPACE;
+  const int warps = factor_warps(fl.W);
+  const size_t smem = sizeof(double) * (3 * fl.W * fl.W + 4) * warps;
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_target_factors, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  AUXMC_LAUNCH(k_target_factors, (fl.total() + warps - 1) / warps, 32 * warps, smem, s, tg, fl, Ls,
+               logdet, flags_out + 3);
+  if (t_hi > t_lo) {
+    AUXMC_LAUNCH(k_ts_gamma_v, grid_t(t_hi - t_lo), 128, 0, s, tg, fl, a.prop, Ls, logdet, t_lo,
+                 t_hi, a.terms);
+    AUXMC_LAUNCH(k_ts_sb_sum, 1, 128, 0, s, a.terms, T, SB, slo, shi, part_out, 1);
   }
-  AUXMC_LAUNCH(k_build_aux, grid_for((long long)(T + 1), 128), 128, 0, s, tg, 1, opts->zeroth_order,
-               a.prop, a.gprop, a.u, ch->delta, a.z, a.Fa, a.ba);
+  if (h1 > h0) {
+    AUXMC_LAUNCH(k_ts_grads, grid_t(h1 - h0), 128, 0, s, tg, fl, a.prop, Ls, h0, h1, t_lo, t_hi,
+                 a.gprop, flags_out + 4);
+    // the reverse surrogate at x' (pseudo-observations and linearized dynamics)
+    AUXMC_LAUNCH(k_ts_prep, grid_t(h1 - h0), 128, 0, s, tg, opts->zeroth_order, a.prop, a.gprop,
+                 ch->delta, a.it, h0, h1, 0, a.u, a.z, a.Fa, a.ba);
+  }
   return AUXMC_OK;
 }
 
 int auxmc_tshard_aux_end(const auxmc_target* target, auxmc_chains* ch,
                          const auxmc_kernel_options* opts, void* workspace, size_t workspace_bytes,
-                         const double* log_marginal_rev, const int* status_rev, void* stream) {
+                         int t_lo, int t_hi, double* part_out, int* flags_out, void* stream) {
   if (!device_ok()) return AUXMC_E_CUDA;
   int st = check_target(target);
   if (st) return st;
-  if (!ch || ch->C != 1 || !opts || !workspace || !log_marginal_rev || !status_rev)
-    return AUXMC_E_ARG;
+  if (!ch || ch->C != 1 || !opts || !workspace || !part_out || !flags_out) return AUXMC_E_ARG;
   const DevTarget tg = to_dev_target(*target);
+  int SB, slo, shi;
+  if ((st = ts_geom(tg, t_lo, t_hi, &SB, &slo, &shi))) return st;
   Arena ws{(char*)workspace, workspace_bytes, 0};
   const TsAux a = ts_aux_take(tg, ws);
   if (!a.ints) return AUXMC_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
-  const int T = tg.T, d = tg.dx, p = d + tg.q;
-  AUXMC_CUDA_TRY(cudaMemcpyAsync(a.sc.st_filt_r, status_rev, sizeof(int),
-                                 cudaMemcpyDeviceToDevice, s));
-  int rc = launch_path_logpdf(a.dm, a.z, (long long)(T + 1) * p, ch->x, log_marginal_rev, 0, 1,
-                              a.sc.logq_rev, a.sc.st_lqr, s);
+  const int T = tg.T, d = tg.dx;
+  // log q(x|x'): the reverse surrogate's path terms at the current path
+  int rc = ts_path_part(a, ch->x, t_lo, t_hi, SB, slo, shi, part_out, 2, flags_out + 6, s);
   if (rc) return rc;
-  AUXMC_LAUNCH(k_aux_lik_terms, grid_for((long long)(T + 1)), 256, 0, s, 1, T, d, a.u, a.prop,
-               ch->delta, a.terms);
-  AUXMC_LAUNCH(k_row_sum, 1, kSumThreads, 0, s, 1, T + 1, a.terms, a.sc.aux_prop);
-  AUXMC_LAUNCH(k_aux_lik_terms, grid_for((long long)(T + 1)), 256, 0, s, 1, T, d, a.u, ch->x,
-               ch->delta, a.terms);
-  AUXMC_LAUNCH(k_row_sum, 1, kSumThreads, 0, s, 1, T + 1, a.terms, a.sc.aux_x);
+  if (t_hi > t_lo) {
+    AUXMC_LAUNCH(k_ts_aux_v, grid_t(t_hi - t_lo), 128, 0, s, d, a.u, a.prop, ch->delta, t_lo, t_hi,
+                 a.terms);
+    AUXMC_LAUNCH(k_ts_sb_sum, 1, 128, 0, s, a.terms, T, SB, slo, shi, part_out, 3);
+    AUXMC_LAUNCH(k_ts_aux_v, grid_t(t_hi - t_lo), 128, 0, s, d, a.u, ch->x, ch->delta, t_lo, t_hi,
+                 a.terms);
+    AUXMC_LAUNCH(k_ts_sb_sum, 1, 128, 0, s, a.terms, T, SB, slo, shi, part_out, 4);
+  }
+  return AUXMC_OK;
+}
+
+int auxmc_tshard_aux_decide(const auxmc_target* target, auxmc_chains* ch, void* workspace,
+                            size_t workspace_bytes, int t_lo, int t_hi, const double* parts_all,
+                            int nsup, const double* log_marginal_fwd,
+                            const double* log_marginal_rev, const int* flags, void* stream) {
+  if (!device_ok()) return AUXMC_E_CUDA;
+  int st = check_target(target);
+  if (st) return st;
+  if (!ch || ch->C != 1 || !workspace || !parts_all || !log_marginal_fwd || !log_marginal_rev ||
+      !flags || nsup < 1)
+    return AUXMC_E_ARG;
+  const DevTarget tg = to_dev_target(*target);
+  int SB, slo, shi;
+  if ((st = ts_geom(tg, t_lo, t_hi, &SB, &slo, &shi))) return st;
+  Arena ws{(char*)workspace, workspace_bytes, 0};
+  const TsAux a = ts_aux_take(tg, ws);
+  if (!a.ints) return AUXMC_E_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int T = tg.T, d = tg.dx;
+  const bool own = t_hi > t_lo;
+  const int h0 = own ? std::max(t_lo - 1, 0) : 0, h1 = own ? std::min(t_hi + 1, T + 1) : 0;
+  AUXMC_LAUNCH(k_ts_scalars, 1, 32, 0, s, parts_all, nsup, log_marginal_fwd, log_marginal_rev, flags,
+               a.sc);
   AUXMC_LAUNCH(k_mh, 1, 32, 0, s, 1, a.sc, a.it, ch->log_gamma, ch->iter, ch->stats);
-  AUXMC_LAUNCH(k_accept_copy, grid_for((long long)(T + 1) * d), 256, 0, s, 1,
-               (long long)(T + 1) * d, a.sc.accept, a.prop, a.gprop, ch->x, ch->grad_gen);
+  if (h1 > h0)
+    AUXMC_LAUNCH(k_ts_accept, grid_t((h1 - h0) * d), 128, 0, s, d, h0, h1, a.sc.accept, a.prop, a.gprop,
+                 ch->x, ch->grad_gen);
   return AUXMC_OK;
 }
 

@@ -7,6 +7,7 @@
 // reference's order (prior, transitions t = 0..T-1, observations t = 0..T).
 #include "common.cuh"
 #include "dense.cuh"
+#include "terms.cuh"
 
 namespace auxmc_gpu {
 
@@ -61,64 +62,14 @@ __global__ void k_factor_list(DevModel m, int nQb, int nRb, double* Ls, double* 
 __global__ void k_path_terms(DevModel m, const double* __restrict__ obs, long long obs_stride,
                              const double* __restrict__ traj, int B, const double* __restrict__ Ls,
                              const double* __restrict__ logdet, double* terms) {
-  const int T = m.T, dx = m.dx, dy = m.dy;
-  const int W = dx > dy ? dx : dy;
+  const int T = m.T;
   const int K = 2 * T + 2;
   const long long n = (long long)B * K;
-  double r[64];
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
        q += (long long)gridDim.x * blockDim.x) {
     const int b = (int)(q / K), k = (int)(q % K);
-    const double* x = traj + (size_t)b * (T + 1) * dx;
-    const double* L;
-    double ld;
-    int nn;
-    if (k == 0) {
-      nn = dx;
-      for (int i = 0; i < dx; ++i) r[i] = x[i] - m.m0[i];
-      L = Ls;
-      ld = logdet[0];
-    } else if (k <= T) {
-      const int t = k - 1;
-      nn = dx;
-      const double* F = m.Ft(t, b);
-      const double* bb = m.bt(t, b);
-      for (int i = 0; i < dx; ++i) {
-        double s = 0.0;
-        for (int j = 0; j < dx; ++j) s += F[i * dx + j] * x[(size_t)t * dx + j];
-        r[i] = x[(size_t)(t + 1) * dx + i] - (s + bb[i]);
-      }
-      const int j = 1 + (m.sQ ? b * m.nQ : 0) + (m.nQ > 1 ? t : 0);
-      L = Ls + (size_t)j * W * W;
-      ld = logdet[j];
-    } else {
-      const int t = k - T - 1;
-      if (!m.observed(t) || dy == 0) {
-        terms[q] = 0.0;
-        continue;
-      }
-      nn = dy;
-      const double* H = m.Ht(t, b);
-      const double* cc = m.ct(t, b);
-      const double* y = obs + (size_t)b * obs_stride + (size_t)t * dy;
-      for (int i = 0; i < dy; ++i) {
-        double s = 0.0;
-        for (int j = 0; j < dx; ++j) s += H[i * dx + j] * x[(size_t)t * dx + j];
-        r[i] = y[i] - (s + cc[i]);
-      }
-      const int nq = (m.sQ ? B : 1) * m.nQ;
-      const int j = 1 + nq + (m.sR ? b * m.nR : 0) + (m.nR > 1 ? t : 0);
-      L = Ls + (size_t)j * W * W;
-      ld = logdet[j];
-    }
-    double sq = 0.0;
-    for (int i = 0; i < nn; ++i) {
-      double s = r[i];
-      for (int j = 0; j < i; ++j) s -= L[i * nn + j] * r[j];
-      r[i] = s / L[i * nn + i];
-      sq += r[i] * r[i];
-    }
-    terms[q] = -0.5 * (nn * kLog2Pi + sq) - ld;
+    terms[q] = path_term_k(m, obs + (size_t)b * obs_stride, traj + (size_t)b * (T + 1) * m.dx, b, B,
+                           Ls, logdet, k);
   }
 }
 

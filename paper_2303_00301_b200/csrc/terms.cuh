@@ -1,0 +1,111 @@
+// terms.cuh — per-term bodies of the path log-densities, shared by the full-horizon
+// kernels (one thread per (path, term), fixed-order sums: logpdf.cu, auxk.cu) and the
+// time-sharded aux step (per-t sums over super-blocks, auxk.cu tshard section).
+//
+// Term index k of a path of T steps: 0 prior, 1..T transitions t = k-1, T+1..2T+1
+// observations t = k-T-1 (lgssm.cpp:179-199, target.cpp:100-108).
+#pragma once
+#include "common.cuh"
+#include "dense.cuh"
+#include "target.cuh"
+
+namespace auxmc_gpu {
+
+// lgssm::path_logpdf term k of path b (x = its [T+1][dx] rows, obs_b its [T+1][dy] rows).
+// Masked or absent observations contribute 0 (lgssm.cpp:193-196).
+__device__ __forceinline__ double path_term_k(const DevModel& m, const double* __restrict__ obs_b,
+                                              const double* __restrict__ x, int b, int B,
+                                              const double* __restrict__ Ls,
+                                              const double* __restrict__ logdet, int k) {
+  const int T = m.T, dx = m.dx, dy = m.dy;
+  const int W = dx > dy ? dx : dy;
+  double r[64];
+  const double* L;
+  double ld;
+  int nn;
+  if (k == 0) {
+    nn = dx;
+    for (int i = 0; i < dx; ++i) r[i] = x[i] - m.m0[i];
+    L = Ls;
+    ld = logdet[0];
+  } else if (k <= T) {
+    const int t = k - 1;
+    nn = dx;
+    const double* F = m.Ft(t, b);
+    const double* bb = m.bt(t, b);
+    for (int i = 0; i < dx; ++i) {
+      double s = 0.0;
+      for (int j = 0; j < dx; ++j) s += F[i * dx + j] * x[(size_t)t * dx + j];
+      r[i] = x[(size_t)(t + 1) * dx + i] - (s + bb[i]);
+    }
+    const int j = 1 + (m.sQ ? b * m.nQ : 0) + (m.nQ > 1 ? t : 0);
+    L = Ls + (size_t)j * W * W;
+    ld = logdet[j];
+  } else {
+    const int t = k - T - 1;
+    if (!m.observed(t) || dy == 0) return 0.0;
+    nn = dy;
+    const double* H = m.Ht(t, b);
+    const double* cc = m.ct(t, b);
+    const double* y = obs_b + (size_t)t * dy;
+    for (int i = 0; i < dy; ++i) {
+      double s = 0.0;
+      for (int j = 0; j < dx; ++j) s += H[i * dx + j] * x[(size_t)t * dx + j];
+      r[i] = y[i] - (s + cc[i]);
+    }
+    const int nq = (m.sQ ? B : 1) * m.nQ;
+    const int j = 1 + nq + (m.sR ? b * m.nR : 0) + (m.nR > 1 ? t : 0);
+    L = Ls + (size_t)j * W * W;
+    ld = logdet[j];
+  }
+  double sq = 0.0;
+  for (int i = 0; i < nn; ++i) {
+    double s = r[i];
+    for (int j = 0; j < i; ++j) s -= L[i * nn + j] * r[j];
+    r[i] = s / L[i * nn + i];
+    sq += r[i] * r[i];
+  }
+  return -0.5 * (nn * kLog2Pi + sq) - ld;
+}
+
+// target.log_gamma term k of the path x (target.cpp:100-108), with the target's factors.
+__device__ __forceinline__ double gamma_term_k(const DevTarget& tg, const FactorLayout& fl,
+                                               const double* __restrict__ x,
+                                               const double* __restrict__ Ls,
+                                               const double* __restrict__ logdet, int k) {
+  const int T = tg.T, d = tg.dx, W = fl.W;
+  double r[64];
+  if (k == 0) {
+    for (int i = 0; i < d; ++i) r[i] = x[i] - tg.m0[i];
+    return gauss_term(d, r, Ls, logdet[0]);
+  }
+  if (k <= T) {
+    const int t = k - 1;
+    for (int i = 0; i < d; ++i) r[i] = x[(size_t)(t + 1) * d + i] - dyn_mean_i(tg, t, x + (size_t)t * d, i);
+    const int jq = 1 + (fl.nQ > 1 ? t : 0);
+    return gauss_term(d, r, Ls + (size_t)jq * W * W, logdet[jq]);
+  }
+  const int t = k - T - 1;
+  const double* xt = x + (size_t)t * d;
+  double lp = 0.0;
+  if (tg.q > 0 && tg.emask[t]) {
+    const double* H = tg.eHt(t);
+    const double* cc = tg.ect(t);
+    const double* y = tg.ey + (size_t)t * tg.q;
+    for (int i = 0; i < tg.q; ++i) {
+      double s = 0.0;
+      for (int j = 0; j < d; ++j) s += H[i * d + j] * xt[j];
+      r[i] = y[i] - (s + cc[i]);
+    }
+    const int je = 1 + fl.nQ + (tg.ne > 1 ? t : 0);
+    lp += gauss_term(tg.q, r, Ls + (size_t)je * W * W, logdet[je]);
+  }
+  if (tg.gmask[t]) {
+    const int jg = 1 + fl.nQ + fl.nE + (tg.ne > 1 ? t : 0);
+    lp += generic_log_g(tg, t, xt, fl.nG ? Ls + (size_t)jg * W * W : nullptr,
+                        fl.nG ? logdet[jg] : 0.0, r);
+  }
+  return lp;
+}
+
+}  // namespace auxmc_gpu

@@ -264,11 +264,14 @@ class _KeyNoise:
 
 class ShardedAuxChain:
     """One chain's auxiliary Kalman step (auxk::kernel_step, prefix backend, scan
-    filter) with the horizon split over ranks: the forward filter, the path draw
-    and the reverse filter are time-sharded (tshard filter / prefix), the proposal
-    path is all-gathered, and the per-step work around them (aux observations,
-    surrogate models, path log-densities, log gamma, gradients, MH) is repeated by
-    every rank on the whole horizon — so every split gives the same bits."""
+    filter) with the horizon split over ranks.  Rank r works only on
+    its own time range [t_lo, t_hi) of whole filter super-blocks (plus one halo row on
+    each side): aux observations, surrogate models, path log-densities, log gamma,
+    gradients, the two sharded filters and the sharded prefix draw.  Per step the ranks
+    exchange the filters' super-block aggregates and log-likelihood partials, the
+    sampler's block rows, the proposal's halo rows (2 d doubles per rank) and the step's
+    super-block partials with the status flags (6 doubles per super-block) — never a
+    path.  Every split gives the same bits (tests/test_gpu_tshard_aux.py)."""
 
     def __init__(self, chains, rank: int, world: int, exchange, zeroth_order=False):
         if chains.C != 1:
@@ -280,10 +283,32 @@ class ShardedAuxChain:
         self._tr = self.tg.raw()
         self.ws_bytes = lib.auxmc_tshard_aux_workspace(C.byref(self._tr))
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.tg.device)
+        self.geom = TShardGeom.of(self.tg.T, self.tg.dx)
+        self.sup_lo, self.sup_hi, self.t_lo, self.t_hi = self.geom.owned(rank, world)
+        self.max_owned = -(-self.geom.nsup // world)
+        self.traj = torch.zeros((self.tg.T + 1, self.tg.dx), dtype=torch.float64,
+                                device=self.tg.device)
 
-    def _max_status(self, st: torch.Tensor) -> torch.Tensor:
-        parts = self.exchange(st)
-        return torch.stack(parts).amax(0).to(torch.int32).contiguous()
+    def _halo(self, traj):
+        """x'_{t_lo-1} and x'_{t_hi} from the neighbours (every rank sends its first and
+        last own rows)."""
+        d, dev = self.tg.dx, self.tg.device
+        lo, hi = self.t_lo, self.t_hi
+        edge = torch.zeros((2, d), dtype=torch.float64, device=dev)
+        if hi > lo:
+            edge[0] = traj[lo]
+            edge[1] = traj[hi - 1]
+        parts = self.exchange(edge)
+        if hi <= lo:
+            return
+        if lo > 0:
+            prev = max(r for r in range(self.rank) if self.geom.owned(r, self.world)[3] >
+                       self.geom.owned(r, self.world)[2])
+            traj[lo - 1] = parts[prev][1]
+        if hi <= self.tg.T:
+            nxt = min(r for r in range(self.rank + 1, self.world)
+                      if self.geom.owned(r, self.world)[3] > self.geom.owned(r, self.world)[2])
+            traj[hi] = parts[nxt][0]
 
     def step(self):
         lib, dev = _lib.load(), self.tg.device
@@ -291,10 +316,11 @@ class ShardedAuxChain:
         ch = self.ch.raw()
         model = _lib.Lgssm()
         z, prop, it = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        lo, hi = self.t_lo, self.t_hi
         _lib.check(lib.auxmc_tshard_aux_begin(
             C.byref(self._tr), C.byref(ch), C.byref(self.opts), self.ws.data_ptr(),
-            self.ws_bytes, C.byref(model), C.byref(z), C.byref(prop), C.byref(it), _stream()),
-            "tshard_aux_begin")
+            self.ws_bytes, lo, hi, C.byref(model), C.byref(z), C.byref(prop), C.byref(it),
+            _stream()), "tshard_aux_begin")
         rm = RawModel(model, dev)
         # forward filter and the path draw, time-sharded
         sf = ShardedScanFilter(rm, self.rank, self.world)
@@ -302,40 +328,67 @@ class ShardedAuxChain:
         lm_fwd = sf.log_marginal(self.exchange(ll))
         fr.log_marginal.copy_(lm_fwd)
         ps = ShardedPrefixSampler(sf)
-        traj = torch.zeros((T + 1, d), dtype=torch.float64, device=dev)
+        traj = self.traj
         rows, xT = ps.local(fr, _KeyNoise(it.value), traj)
         ps.finish(self.exchange(rows), self.exchange(xT), traj)
-        # the whole proposal path on every rank
-        mine = traj[sf.t_lo:min(sf.t_hi, T)].contiguous()
-        pad = torch.zeros((ps.max_blocks * ps.Lb, d), dtype=torch.float64, device=dev)
-        pad[:mine.shape[0]] = mine
-        parts = self.exchange(pad)
-        full = torch.empty((T + 1, d), dtype=torch.float64, device=dev)
-        for r, part in enumerate(parts):
-            _, _, a, b = sf.geom.owned(r, self.world)
-            b = min(b, T)
-            if b > a:
-                full[a:b] = part[:b - a]
-        full[T] = traj[T]
-        _lib.check(lib.auxmc_copy_device(prop.value, full.data_ptr(), full.numel() * 8,
-                                         _stream()), "copy")
-        st_fwd = self._max_status(torch.stack([sf.status[0], ps.status[0]]).to(torch.int32))
+        self._halo(traj)
+        if hi > lo:
+            h0, h1 = max(lo - 1, 0), min(hi + 1, T + 1)
+            _lib.check(lib.auxmc_copy_device(prop.value + h0 * d * 8, traj[h0:h1].data_ptr(),
+                                             (h1 - h0) * d * 8, _stream()), "copy")
+        part = torch.zeros((self.max_owned + 2, 5), dtype=torch.float64, device=dev)
+        flags = torch.zeros(8, dtype=torch.int32, device=dev)
+        flags[0] = sf.status[0]
+        flags[1] = ps.status[0]
         _lib.check(lib.auxmc_tshard_aux_middle(
             C.byref(self._tr), C.byref(ch), C.byref(self.opts), self.ws.data_ptr(),
-            self.ws_bytes, lm_fwd.data_ptr(), st_fwd.data_ptr(), _stream()), "tshard_aux_middle")
+            self.ws_bytes, lo, hi, part.data_ptr(), flags.data_ptr(), _stream()),
+            "tshard_aux_middle")
         # reverse filter on the surrogate at x'
         sr = ShardedScanFilter(rm, self.rank, self.world)
         _, llr = sr.finish(self.exchange(sr.local(z.value)))
         lm_rev = sr.log_marginal(self.exchange(llr))
-        st_rev = self._max_status(sr.status.to(torch.int32))
+        flags[5] = sr.status[0]
         _lib.check(lib.auxmc_tshard_aux_end(
             C.byref(self._tr), C.byref(ch), C.byref(self.opts), self.ws.data_ptr(),
-            self.ws_bytes, lm_rev.data_ptr(), st_rev.data_ptr(), _stream()), "tshard_aux_end")
+            self.ws_bytes, lo, hi, part.data_ptr(), flags.data_ptr(), _stream()),
+            "tshard_aux_end")
+        # one exchange: super-block partials (rows 0..owned) with the flags in the last row
+        part[self.max_owned + 1, :].zero_()
+        part[self.max_owned, :] = 0.0
+        part[self.max_owned, 0:5] = flags[0:5].to(torch.float64)
+        part[self.max_owned + 1, 0:2] = flags[5:7].to(torch.float64)
+        parts = self.exchange(part)
+        rows_all, fl = [], torch.zeros(8, dtype=torch.float64, device=dev)
+        for r, pr in enumerate(parts):
+            s_lo, s_hi, _, _ = self.geom.owned(r, self.world)
+            rows_all.append(pr[:s_hi - s_lo])
+            fl[0:5] = torch.maximum(fl[0:5], pr[self.max_owned, 0:5])
+            fl[5:7] = torch.maximum(fl[5:7], pr[self.max_owned + 1, 0:2])
+        parts_all = torch.cat(rows_all, 0).contiguous()
+        flags_all = fl.to(torch.int32).contiguous()
+        _lib.check(lib.auxmc_tshard_aux_decide(
+            C.byref(self._tr), C.byref(ch), self.ws.data_ptr(), self.ws_bytes, lo, hi,
+            parts_all.data_ptr(), parts_all.shape[0], lm_fwd.data_ptr(), lm_rev.data_ptr(),
+            flags_all.data_ptr(), _stream()), "tshard_aux_decide")
 
 
 class LocalShardedAux:
     """Runs `world` ShardedAuxChain ranks in one process (tests): each rank owns
     its own chain state copy; every exchange is served once all ranks posted."""
+
+    @staticmethod
+    def assemble(chains) -> torch.Tensor:
+        """The chain's full path from the ranks' own time ranges (a rank's state is
+        valid on its range and one halo row on each side only)."""
+        world = len(chains)
+        T, d = chains[0].target.T, chains[0].target.dx
+        geom = TShardGeom.of(T, d)
+        out = torch.empty((1, T + 1, d), dtype=torch.float64, device=chains[0].x.device)
+        for r, ch in enumerate(chains):
+            _, _, lo, hi = geom.owned(r, world)
+            out[0, lo:hi] = ch.x[0, lo:hi]
+        return out
 
     @staticmethod
     def run(make_chains, world: int, steps: int):
