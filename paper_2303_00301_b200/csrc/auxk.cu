@@ -580,14 +580,23 @@ __global__ void k_ts_aux_v(int d, const double* __restrict__ u, const double* __
     v[t] = -0.5 * (d * (kLog2Pi + log(var)) + sq / var);  // gauss.cpp:59-62
   }
 }
-// super-block partial sums (t order) of v over the rank's super-blocks
+// super-block partial sums of v over the rank's super-blocks: one warp per super-block,
+// lane l sums its contiguous 1/32 of the block in t order, then a fixed shuffle tree —
+// an association that depends on (T, SB) only, so every split gives the same bits
 __global__ void k_ts_sb_sum(const double* __restrict__ v, int T, int SB, int sup_lo, int sup_hi,
                             double* part, int col) {
-  for (int s = sup_lo + blockIdx.x * blockDim.x + threadIdx.x; s < sup_hi; s += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int s = sup_lo + wid; s < sup_hi; s += nw) {
     const int lo = s * SB, hi = min((s + 1) * SB, T + 1);
+    const int ch = (hi - lo + 31) / 32;
+    const int a = min(lo + lane * ch, hi), b = min(a + ch, hi);
     double acc = 0.0;
-    for (int t = lo; t < hi; ++t) acc += v[t];
-    part[(size_t)(s - sup_lo) * 5 + col] = acc;
+    for (int t = a; t < b; ++t) acc += v[t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (lane == 0) part[(size_t)(s - sup_lo) * 5 + col] = acc;
   }
 }
 // the MH inputs from every rank's partials (super-block order) and the reduced flags
@@ -835,7 +844,7 @@ static int ts_path_part(const TsAux& a, const double* traj, int t_lo, int t_hi, 
   if (t_hi > t_lo) {
     AUXMC_LAUNCH(k_ts_path_v, grid_t(t_hi - t_lo), 128, 0, s, dm, a.z, traj, Ls, logdet, t_lo, t_hi,
                  a.terms);
-    AUXMC_LAUNCH(k_ts_sb_sum, 1, 128, 0, s, a.terms, dm.T, SB, slo, shi, part, col);
+    AUXMC_LAUNCH(k_ts_sb_sum, std::max(1, (shi - slo + 3) / 4), 128, 0, s, a.terms, dm.T, SB, slo, shi, part, col);
   }
   cudaFreeAsync(Ls, s);
   cudaFreeAsync(logdet, s);
@@ -878,7 +887,7 @@ int auxmc_tshard_aux_middle(const auxmc_target* target, auxmc_chains* ch,
   if (t_hi > t_lo) {
     AUXMC_LAUNCH(k_ts_gamma_v, grid_t(t_hi - t_lo), 128, 0, s, tg, fl, a.prop, Ls, logdet, t_lo,
                  t_hi, a.terms);
-    AUXMC_LAUNCH(k_ts_sb_sum, 1, 128, 0, s, a.terms, T, SB, slo, shi, part_out, 1);
+    AUXMC_LAUNCH(k_ts_sb_sum, std::max(1, (shi - slo + 3) / 4), 128, 0, s, a.terms, T, SB, slo, shi, part_out, 1);
   }
   if (h1 > h0) {
     AUXMC_LAUNCH(k_ts_grads, grid_t(h1 - h0), 128, 0, s, tg, fl, a.prop, Ls, h0, h1, t_lo, t_hi,
@@ -911,10 +920,10 @@ int auxmc_tshard_aux_end(const auxmc_target* target, auxmc_chains* ch,
   if (t_hi > t_lo) {
     AUXMC_LAUNCH(k_ts_aux_v, grid_t(t_hi - t_lo), 128, 0, s, d, a.u, a.prop, ch->delta, t_lo, t_hi,
                  a.terms);
-    AUXMC_LAUNCH(k_ts_sb_sum, 1, 128, 0, s, a.terms, T, SB, slo, shi, part_out, 3);
+    AUXMC_LAUNCH(k_ts_sb_sum, std::max(1, (shi - slo + 3) / 4), 128, 0, s, a.terms, T, SB, slo, shi, part_out, 3);
     AUXMC_LAUNCH(k_ts_aux_v, grid_t(t_hi - t_lo), 128, 0, s, d, a.u, ch->x, ch->delta, t_lo, t_hi,
                  a.terms);
-    AUXMC_LAUNCH(k_ts_sb_sum, 1, 128, 0, s, a.terms, T, SB, slo, shi, part_out, 4);
+    AUXMC_LAUNCH(k_ts_sb_sum, std::max(1, (shi - slo + 3) / 4), 128, 0, s, a.terms, T, SB, slo, shi, part_out, 4);
   }
   return AUXMC_OK;
 }

@@ -86,48 +86,59 @@ __device__ __forceinline__ void frag2(const double* Me, const double* Mo, double
   for (int l = 0; l < 32; ++l) out[l] = (((l >> 2) & 1) ? Mo : Me)[4 * (l >> 3) + (l & 3)];
 }
 
-// Per (superchunk, warp group): the 8 step-pair records and Gw = G_lo ... G_{lo+15}.
-// Dead steps (t >= T) are G = I, off = 0, L = 0: they pass the state through.
+// The step-pair records, one thread per pair (dead steps t >= T: G = I, off = 0, L = 0, so
+// they pass the state through).
 __global__ void k_mma_pack(const double* __restrict__ elems, int T, double* tiles) {
   using G = MmaGeom;
-  constexpr int D = G::D;
+  const int n = ((T + G::S - 1) / G::S) * (G::S / 2);
+  const int ESg = elem_stride(G::D);
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int k = q / (G::S / 2), pr = q % (G::S / 2);  // pair pr = w * NP + j of superchunk k
+    double* rec = tiles + (size_t)k * G::TB + (size_t)pr * G::PR;
+    double Gs[2][16], Ls[2][16], off[2][4], GG[16], GL[16];
+    for (int h = 0; h < 2; ++h) {  // h = 0: lo step, h = 1: hi step
+      const int t = k * G::S + 2 * pr + h;
+      if (t >= T) {
+        for (int i = 0; i < 16; ++i) Gs[h][i] = (i / 4 == i % 4) ? 1.0 : 0.0;
+        for (int i = 0; i < 16; ++i) Ls[h][i] = 0.0;
+        for (int i = 0; i < 4; ++i) off[h][i] = 0.0;
+        continue;
+      }
+      const double* e = elems + (size_t)t * ESg;
+      for (int i = 0; i < 16; ++i) Gs[h][i] = e[i];
+      for (int i = 0; i < 4; ++i) off[h][i] = e[16 + i];
+      for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) Ls[h][r * 4 + c] = c <= r ? e[20 + r * 4 + c] : 0.0;
+    }
+    mm4(Gs[0], Gs[1], GG);
+    mm4(Gs[0], Ls[1], GL);
+    frag2(Gs[1], GG, rec);
+    frag2(Ls[1], GL, rec + 32);
+    for (int i = 0; i < 16; ++i) rec[64 + i] = Ls[0][i];
+    for (int d = 0; d < 4; ++d) {
+      double acc = 0.0;
+      for (int c = 0; c < 4; ++c) acc += Gs[0][d * 4 + c] * off[1][c];
+      rec[80 + 2 * d] = off[1][d];
+      rec[80 + 2 * d + 1] = acc + off[0][d];
+    }
+  }
+}
+
+// Gw = G_lo ... G_{lo+15} per (superchunk, warp group): GG_j (read back from the odd
+// fragment lanes) composed top-down, GG_7 first.
+__global__ void k_mma_spans(int T, double* tiles) {
+  using G = MmaGeom;
   const int n = ((T + G::S - 1) / G::S) * G::W;
-  const int ESg = elem_stride(D);
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
-    const int k = s / G::W, w = s % G::W;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int k = q / G::W, w = q % G::W;
     double* tile = tiles + (size_t)k * G::TB;
-    const int lo = k * G::S + w * G::GS;
-    double Gs[2][16], Ls[2][16], off[2][4];
-    double P[16], Q[16], GG[16], GL[16];
+    double P[16], Q[16], GG[16];
     for (int i = 0; i < 16; ++i) P[i] = (i / 4 == i % 4) ? 1.0 : 0.0;
     for (int j = G::NP - 1; j >= 0; --j) {
-      for (int h = 0; h < 2; ++h) {  // h = 0: lo step 2j, h = 1: hi step 2j + 1
-        const int t = lo + 2 * j + h;
-        if (t >= T) {
-          for (int i = 0; i < 16; ++i) Gs[h][i] = (i / 4 == i % 4) ? 1.0 : 0.0;
-          for (int i = 0; i < 16; ++i) Ls[h][i] = 0.0;
-          for (int i = 0; i < 4; ++i) off[h][i] = 0.0;
-          continue;
-        }
-        const double* e = elems + (size_t)t * ESg;
-        for (int i = 0; i < 16; ++i) Gs[h][i] = e[i];
-        for (int i = 0; i < 4; ++i) off[h][i] = e[16 + i];
-        for (int r = 0; r < 4; ++r)
-          for (int c = 0; c < 4; ++c) Ls[h][r * 4 + c] = c <= r ? e[20 + r * 4 + c] : 0.0;
-      }
-      double* rec = tile + (w * G::NP + j) * G::PR;
-      mm4(Gs[0], Gs[1], GG);
-      mm4(Gs[0], Ls[1], GL);
-      frag2(Gs[1], GG, rec);
-      frag2(Ls[1], GL, rec + 32);
-      for (int i = 0; i < 16; ++i) rec[64 + i] = Ls[0][i];
-      for (int d = 0; d < 4; ++d) {
-        double acc = 0.0;
-        for (int c = 0; c < 4; ++c) acc += Gs[0][d * 4 + c] * off[1][c];
-        rec[80 + 2 * d] = off[1][d];
-        rec[80 + 2 * d + 1] = acc + off[0][d];
-      }
-      mm4(GG, P, Q);  // group span: G_{2j} G_{2j+1} (G_{2j+2} ... G_15)
+      const double* fr = tile + (size_t)(w * G::NP + j) * G::PR;
+      for (int l = 0; l < 32; ++l)
+        if ((l >> 2) & 1) GG[4 * (l >> 3) + (l & 3)] = fr[l];
+      mm4(GG, P, Q);
       for (int i = 0; i < 16; ++i) P[i] = Q[i];
     }
     double* gw = tile + G::EB + w * 16;
@@ -372,8 +383,9 @@ int run_prefix_mma(int T, int B, const double* elems, const double* term, Arena&
   if (nz.kind == AUXMC_NOISE_PREDRAWN && (reinterpret_cast<uintptr_t>(nz.backward) & 15))
     return AUXMC_E_ARG;  // cp.async.bulk stages noise rows: 16-B aligned source required
   if (T > 0) {
-    const int n = K * G::W;
-    AUXMC_LAUNCH(k_mma_pack, std::min((n + 127) / 128, 148 * 16), 128, 0, stream, elems, T, tiles);
+    const int np = K * (G::S / 2), ng = K * G::W;
+    AUXMC_LAUNCH(k_mma_pack, std::min((np + 127) / 128, 148 * 32), 128, 0, stream, elems, T, tiles);
+    AUXMC_LAUNCH(k_mma_spans, std::min((ng + 127) / 128, 148 * 16), 128, 0, stream, T, tiles);
   }
   const int grid = std::max((B + G::ROWS - 1) / G::ROWS, std::min(B, num_sms()));
   if (nz.kind == AUXMC_NOISE_PREDRAWN) {
