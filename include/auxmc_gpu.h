@@ -222,6 +222,10 @@ size_t auxmc_affine_law_workspace(const auxmc_lgssm* model, int sampler);
 /* testhooks::flip_backward_gain (testhooks.hpp:11): negate every backward gain
  * (a deliberate bug the law checks must catch, runner.cpp:301-312). */
 int auxmc_test_flip_backward_gain(int on);
+/* Test hook: 1 routes the auxiliary step's sequential filter through the generic
+ * (d+q)-dimensional filter even where the fused direct-observation filter applies
+ * (auxmc_target::exact_sel); the parity tests compare the two.  Host-side switch. */
+int auxmc_test_force_generic_filter(int on);
 
 /* Host-buffer convenience entry for the reference-facing facade: copies the
  * model, filter result and noise keys to the device, draws B paths and copies
@@ -271,6 +275,13 @@ typedef struct {
   /* kind parameters (ModelSpec fields) */
   double lz_sigma, lz_rho, lz_beta, lz_h;
   double l96_F, l96_h;
+  /* 1: every exact row has one nonzero, a 1, in a distinct state column, R_e is diagonal
+   * positive and ne = 1 (the diffusion-smoothing models; any target with q = 0).  The
+   * auxiliary step then filters with the fused direct-observation filter (filter_direct.cu)
+   * and, for Lorenz-96, never materializes the dynamics Jacobian.  The kernel re-checks
+   * the structure and marks the chain's filter status 3 if it does not hold; 0 is always
+   * valid (generic filter). */
+  int exact_sel;
 } auxmc_target;
 
 /* ---- auxiliary Kalman MH kernel (auxk.hpp:15-79) ---- */

@@ -55,7 +55,7 @@ class Target(C.Structure):
                 ("gmask", C.c_void_p), ("gH", C.c_void_p), ("gc", C.c_void_p),
                 ("gR", C.c_void_p), ("lz_sigma", C.c_double), ("lz_rho", C.c_double),
                 ("lz_beta", C.c_double), ("lz_h", C.c_double), ("l96_F", C.c_double),
-                ("l96_h", C.c_double)]
+                ("l96_h", C.c_double), ("exact_sel", C.c_int)]
 
 
 class KernelOptions(C.Structure):
@@ -140,6 +140,7 @@ SIGNATURES = {
                                    VP, VP, C.c_size_t, VP]),
     "auxmc_affine_law_workspace": (C.c_size_t, [C.POINTER(Lgssm), C.c_int]),
     "auxmc_test_flip_backward_gain": (C.c_int, [C.c_int]),
+    "auxmc_test_force_generic_filter": (C.c_int, [C.c_int]),
     "auxmc_path_logpdf": (C.c_int, [C.POINTER(Lgssm), VP, C.c_int, VP, C.POINTER(FilterResult),
                                     C.c_int, C.c_int, VP, VP, VP]),
     "auxmc_init_chains": (C.c_int, [C.POINTER(Target), C.POINTER(Chains), VP, C.c_size_t, VP]),

@@ -30,6 +30,20 @@ def _t(a, device, dtype=torch.float64):
     return torch.from_numpy(host).to(device=device, dtype=dtype).contiguous()
 
 
+def _unit_selection(H, R) -> bool:
+    """Each exact row observes one state component with unit gain (distinct components)
+    under a diagonal positive R_e: the fused direct-observation filter applies."""
+    H = np.asarray(H, np.float64)
+    R = np.asarray(R, np.float64).reshape(H.shape[0], H.shape[0])
+    nz = H != 0.0
+    if not (nz.sum(axis=1) == 1).all() or not (H[nz] == 1.0).all():
+        return False
+    cols = nz.argmax(axis=1)
+    if len(set(cols.tolist())) != len(cols):
+        return False
+    return bool((R == np.diag(np.diag(R))).all() and (np.diag(R) > 0).all())
+
+
 class GenSSMTarget:
     """Device target: linear or tractable dynamics × exact / generic potentials."""
 
@@ -66,6 +80,7 @@ class GenSSMTarget:
         self.emask_host = em
         self.emask = _t(em, device, torch.uint8)
         self.exact_tv = int(self.q > 0 and (self.ne > 1 or (em.min() != em.max())))
+        self.exact_sel = int(self.q == 0 or (self.ne == 1 and _unit_selection(eHn[0], eR)))
         self.data = None if data is None else _t(data, device).reshape(T1, -1)
         self.ydim = 0 if data is None else self.data.shape[1]
         gm = np.zeros(T1, np.uint8) if gmask is None else np.asarray(gmask, np.uint8)
@@ -92,6 +107,7 @@ class GenSSMTarget:
         r.kind, r.T, r.dx, r.ydim, r.linear = self.kind, self.T, self.dx, self.ydim, int(self.linear)
         r.m0, r.P0, r.F, r.b, r.Q, r.nF = p(self.m0), p(self.P0), p(self.F), p(self.b), p(self.Q), self.nF
         r.q, r.ne, r.exact_tv = self.q, self.ne, self.exact_tv
+        r.exact_sel = self.exact_sel
         r.eH, r.ec, r.eR, r.ey = p(self.eH), p(self.ec), p(self.eR), p(self.ey)
         r.emask, r.data, r.gmask = p(self.emask), p(self.data), p(self.gmask)
         r.gH, r.gc, r.gR = p(self.gH), p(self.gc), p(self.gR)

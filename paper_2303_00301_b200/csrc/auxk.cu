@@ -33,6 +33,15 @@ int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int f
 int launch_path_logpdf(const DevModel& dm, const double* obs, long long obs_stride,
                        const double* traj, const double* log_marginal, int lm_shared, int B,
                        double* out, int* status, cudaStream_t s);
+bool filter_direct_ok(const DevTarget& tg, const DevModel& dm, bool stencil);
+int launch_filter_direct(const DevTarget& tg, const DevModel& dm, bool stencil,
+                         const double* xl, const double* delta, const double* z, int C,
+                         auxmc_filter_result* fr, int* status, int covs, cudaStream_t s);
+
+// auxmc_test_force_generic_filter: route the sequential aux filter through the generic
+// (d+q)-dimensional filter (k_filter_cta / k_filter_seq) even when the fused
+// direct-observation filter applies — the parity tests compare the two.
+static int g_force_generic_filter = 0;
 
 __global__ void k_target_factors(DevTarget tg, FactorLayout fl, double* Ls, double* logdet,
                                  int* status) {
@@ -156,14 +165,25 @@ __global__ void k_build_aux(DevTarget tg, int C, int zeroth, const double* __res
     for (int k = 0; k < tg.q; ++k) zt[d + k] = tg.emask[t] ? tg.ey[(size_t)t * tg.q + k] : 0.0;
     if (!tg.linear && t < T) {
       const double* xt = xs + (size_t)q * d;
-      double* F = Fa + ((size_t)c * T + t) * d * d;
       double* bb = ba + ((size_t)c * T + t) * d;
-      for (int i = 0; i < d; ++i)
-        for (int j = 0; j < d; ++j) F[i * d + j] = dyn_jac_ij(tg, t, xt, i, j);
-      for (int i = 0; i < d; ++i) {
-        double s = 0.0;
-        for (int j = 0; j < d; ++j) s += F[i * d + j] * xt[j];
-        bb[i] = dyn_mean_i(tg, t, xt, i) - s;
+      if (Fa) {
+        double* F = Fa + ((size_t)c * T + t) * d * d;
+        for (int i = 0; i < d; ++i)
+          for (int j = 0; j < d; ++j) F[i * d + j] = dyn_jac_ij(tg, t, xt, i, j);
+        for (int i = 0; i < d; ++i) {
+          double s = 0.0;
+          for (int j = 0; j < d; ++j) s += F[i * d + j] * xt[j];
+          bb[i] = dyn_mean_i(tg, t, xt, i) - s;
+        }
+      } else {  // Lorenz-96 stencil: F stays implicit; the row's nonzeros in column order
+        for (int i = 0; i < d; ++i) {
+          int cs[4];
+          double vs[4];
+          l96_row(xt, d, tg.l96_h, i, cs, vs);
+          double s = 0.0;
+          for (int a = 0; a < 4; ++a) s += vs[a] * xt[cs[a]];
+          bb[i] = dyn_mean_i(tg, t, xt, i) - s;
+        }
       }
     }
   }
@@ -349,12 +369,27 @@ static int aux_step(const DevTarget& tg, auxmc_chains* ch, const auxmc_kernel_op
   const int C = ch->C, T = tg.T, d = tg.dx, p = d + tg.q;
   const int nH = tg.exact_tv ? T + 1 : 1;
   const size_t nx = (size_t)C * (T + 1) * d;
+  // Structure-aware path: the fused direct-observation filter (filter_direct.cu) for the
+  // sequential filter; for Lorenz-96 (d > 4) also F_t as a stencil of the linearisation
+  // point in every consumer (filter, backward elements, path terms), never in HBM.
+  const bool stencil_ok = !tg.linear && tg.kind == AUXMC_KIND_LORENZ96 && d > 4;
+  bool direct = false;
+  {
+    DevModel probe{};
+    probe.T = T; probe.dx = d; probe.dy = p; probe.mask = nullptr;
+    probe.nF = tg.linear ? tg.nF : (T > 0 ? T : 1);  // as dm below
+    probe.nQ = tg.linear ? tg.nF : 1;
+    direct = !o.parallel_filter && !g_force_generic_filter &&
+             filter_direct_ok(tg, probe, stencil_ok);
+  }
+  const bool stencil = direct && stencil_ok;
   uint64_t* it = ws.take<uint64_t>(C);
   double* u = ws.take<double>(nx);
   double* prop = ws.take<double>(nx);
   double* gprop = ws.take<double>(nx);
   double* z = ws.take<double>((size_t)C * (T + 1) * p);
-  double* Fa = tg.linear ? nullptr : ws.take<double>((size_t)C * (T > 0 ? T : 1) * d * d);
+  double* Fa = (tg.linear || stencil) ? nullptr
+                                      : ws.take<double>((size_t)C * (T > 0 ? T : 1) * d * d);
   double* ba = tg.linear ? nullptr : ws.take<double>((size_t)C * (T > 0 ? T : 1) * d);
   double* H = ws.take<double>((size_t)nH * p * d);
   double* cv = ws.take<double>((size_t)nH * p);
@@ -388,6 +423,8 @@ static int aux_step(const DevTarget& tg, auxmc_chains* ch, const auxmc_kernel_op
   dm.c = cv; dm.nc = nH; dm.sc = 0;
   dm.R = R; dm.nR = nH; dm.sR = (long long)nH * p * p;
   dm.mask = nullptr;
+  dm.xl = nullptr; dm.sxl = (long long)(T + 1) * d; dm.fst = stencil ? 1 : 0; dm.fh = tg.l96_h;
+  if (stencil) dm.F = nullptr;
   const int sampler = o.backend;
   int rc;
   // sub-arenas for the sampler, log γ and gradients (sizing pass included)
@@ -403,7 +440,7 @@ static int aux_step(const DevTarget& tg, auxmc_chains* ch, const auxmc_kernel_op
     return launch_grads(tg, C, prop, gprop, nullptr, ws, s);
   }
   if (!it || !u || !prop || !gprop || !z || !H || !cv || !R || !fr.filt_cov || !ints || !terms ||
-      (!tg.linear && (!Fa || !ba)))
+      (!tg.linear && ((!stencil && !Fa) || !ba)))
     return AUXMC_E_WORKSPACE;
   sc.st_filt = ints; sc.st_samp = ints + C; sc.st_lqf = ints + 2 * C; sc.st_lg = ints + 3 * C;
   sc.bad = ints + 4 * C; sc.st_filt_r = ints + 5 * C; sc.st_lqr = ints + 6 * C;
@@ -418,14 +455,17 @@ static int aux_step(const DevTarget& tg, auxmc_chains* ch, const auxmc_kernel_op
   AUXMC_LAUNCH(k_build_aux, grid_for((long long)C * (T + 1), 128), 128, 0, s, tg, C,
                o.zeroth_order, ch->x, ch->grad_gen, u, ch->delta, z, Fa, ba);
   Arena pf_ws = ws;  // scan-filter scratch (sized in the sizing pass above)
-  auto filter = [&](int* st) {
+  // covs = 0: the reverse pass needs log p(z) only (launch_path_logpdf)
+  auto filter = [&](int* st, const double* xlin, int covs) {
     if (o.parallel_filter) {
       Arena sub = pf_ws;
       return launch_filter_pit(dm, z, C, &fr, st, sub, s);
     }
+    if (direct) return launch_filter_direct(tg, dm, stencil, xlin, ch->delta, z, C, &fr, st, covs, s);
     return launch_filter_seq(dm, z, C, &fr, st, s);
   };
-  rc = filter(sc.st_filt);
+  dm.xl = ch->x;
+  rc = filter(sc.st_filt, ch->x, 1);
   if (rc) return rc;
   rc = launch_sample_paths(dm, &fr, 0, &nz, C, sampler, prop, sc.st_samp, ws, s);
   if (rc) return rc;
@@ -444,7 +484,8 @@ static int aux_step(const DevTarget& tg, auxmc_chains* ch, const auxmc_kernel_op
   // reverse: surrogate at x', filter, log q(x|x')
   AUXMC_LAUNCH(k_build_aux, grid_for((long long)C * (T + 1), 128), 128, 0, s, tg, C,
                o.zeroth_order, prop, gprop, u, ch->delta, z, Fa, ba);
-  rc = filter(sc.st_filt_r);
+  dm.xl = prop;
+  rc = filter(sc.st_filt_r, prop, 0);
   if (rc) return rc;
   rc = launch_path_logpdf(dm, z, (long long)(T + 1) * p, ch->x, fr.log_marginal, 0, C,
                           sc.logq_rev, sc.st_lqr, s);
@@ -958,3 +999,8 @@ int auxmc_tshard_aux_decide(const auxmc_target* target, auxmc_chains* ch, void* 
 }
 
 }  // extern "C"
+
+extern "C" int auxmc_test_force_generic_filter(int on) {
+  auxmc_gpu::g_force_generic_filter = on ? 1 : 0;
+  return AUXMC_OK;
+}

@@ -81,6 +81,12 @@ struct DevModel {
   int nF, nb, nQ, nH, nc, nR;
   long long sF, sb, sQ, sH, sc, sR;
   const uint8_t* mask;
+  // F given as a stencil instead of a dense array (fst = 1: F_t = I + h J_L96(xl_t), the
+  // auxiliary model of Lorenz-96; F == nullptr): xl [B][T+1][dx] with stride sxl
+  const double* xl = nullptr;
+  long long sxl = 0;
+  int fst = 0;
+  double fh = 0.0;
   __device__ __forceinline__ const double* Ft(int t, int k = 0) const { return F + (size_t)k * sF + (size_t)(nF > 1 ? t : 0) * dx * dx; }
   __device__ __forceinline__ const double* bt(int t, int k = 0) const { return b + (size_t)k * sb + (size_t)(nb > 1 ? t : 0) * dx; }
   __device__ __forceinline__ const double* Qt(int t, int k = 0) const { return Q + (size_t)k * sQ + (size_t)(nQ > 1 ? t : 0) * dx * dx; }
@@ -97,7 +103,56 @@ inline DevModel to_dev(const auxmc_lgssm& m) {
   d.nF = m.nF; d.nb = m.nb; d.nQ = m.nQ; d.nH = m.nH; d.nc = m.nc; d.nR = m.nR;
   d.sF = d.sb = d.sQ = d.sH = d.sc = d.sR = 0;
   d.mask = m.mask;
+  d.xl = nullptr; d.sxl = 0; d.fst = 0; d.fh = 0.0;
   return d;
+}
+
+// Row i of F = I + h J_L96(x): columns ascending (dyn_jac_ij's entries, same rounding).
+__device__ __forceinline__ void l96_row(const double* x, int d, double h, int i, int* cols,
+                                        double* vals) {
+  const int ip1 = (i + 1) % d, im1 = (i + d - 1) % d, im2 = (i + d - 2) % d;
+  int c4[4] = {im2, im1, i, ip1};
+  double v4[4] = {h * (0.0 - x[im1]), h * (0.0 + (x[ip1] - x[im2])), 1.0 + h * (0.0 - 1.0),
+                  h * (0.0 + x[im1])};
+  // sort by column (wrap-around rows)
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 3 - a; ++b)
+      if (c4[b] > c4[b + 1]) {
+        const int tc = c4[b]; c4[b] = c4[b + 1]; c4[b + 1] = tc;
+        const double tv = v4[b]; v4[b] = v4[b + 1]; v4[b + 1] = tv;
+      }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    cols[a] = c4[a];
+    vals[a] = v4[a];
+  }
+}
+
+// Row i of the model's F_t for path k as (column, value) pairs; returns the count
+// (dense rows: every column).  cols/vals hold up to dx entries for dense F.
+__device__ __forceinline__ void stencil_row(const DevModel& m, int t, int k, int i, int* cols,
+                                            double* vals) {
+  l96_row(m.xl + (size_t)k * m.sxl + (size_t)t * m.dx, m.dx, m.fh, i, cols, vals);
+}
+
+// dense F_t of path k into dst (d*d), group-strided over `lane` / `size`
+__device__ __forceinline__ void fill_F(const DevModel& m, int t, int k, double* dst, int lane,
+                                      int size) {
+  const int d = m.dx;
+  if (!m.fst) {
+    const double* F = m.Ft(t, k);
+    for (int i = lane; i < d * d; i += size) dst[i] = F[i];
+    return;
+  }
+  for (int i = lane; i < d; i += size) {  // row i by one lane: zero, then the stencil
+    int cs[4];
+    double vs[4];
+    stencil_row(m, t, k, i, cs, vs);
+    for (int j = 0; j < d; ++j) dst[i * d + j] = 0.0;
+    for (int a = 0; a < 4; ++a) dst[i * d + cs[a]] = vs[a];
+  }
 }
 
 int check_model(const auxmc_lgssm* m);

@@ -43,9 +43,9 @@ __device__ __forceinline__ int backward_step_group(const Grp& g, const DevModel&
   double* B4 = B3 + dd;    // solve rhs/result; then products; then chol(Λ)
   double* v = B4 + (f_smem ? 2 : 1) * dd;
   double* red = v + 2 * d;
-  const double* F = m.Ft(t, k);
-  if (f_smem) {
-    g_copy(g, dd, F, B4 + dd);
+  const double* F = m.fst ? nullptr : m.Ft(t, k);
+  if (f_smem) {  // staged (stencil models: formed here, never read from HBM)
+    fill_F(m, t, k, B4 + dd, g.lane, g.size);
     F = B4 + dd;
   }
   double* P = B0;
@@ -136,7 +136,8 @@ __global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
   extern __shared__ double smem[];
   const int d = m.dx, dd = d * d;
   const int T = m.T;
-  const int per = bwd_buffers(!BLOCK) * dd + 4 * d + 4;
+  const bool f_smem = !BLOCK || m.fst;
+  const int per = bwd_buffers(f_smem) * dd + 4 * d + 4;
   Grp g = BLOCK ? block_group() : warp_group();
   const int gid = BLOCK ? 0 : (threadIdx.x >> 5);
   const int groups_per_block = BLOCK ? 1 : (blockDim.x >> 5);
@@ -165,7 +166,155 @@ __global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
       for (int i = g.lane; i < dd; i += g.size) out[d + i] = L[i];
     } else {
       st = backward_step_group(g, m, t, fm, fc, pc, sm, flag,
-                               elems + ((size_t)b * T + t) * elem_stride(d), b, store_cov, !BLOCK);
+                               elems + ((size_t)b * T + t) * elem_stride(d), b, store_cov, f_smem);
+    }
+    if (st && g.lane == 0) atomicMax(status + b, st);
+    g.sync();
+  }
+}
+
+// Lean backward elements for CTA-sized d (d > 16): the same conditional law
+// (lgssm.cpp:129-149) in the Schur form
+//   C = F P,  S = L L^T,  W = L^{-1} C,  Λ = P - W^T W,  G^T = L^{-T} W,
+//   off = m - G (F m + b),  L_Λ = chol_psd(Λ)
+// (Λ = P - P F^T S^{-1} F P, algebraically the reference's Joseph form; FP64
+// association differs, within the parity tolerance).  Three d×d buffers: the factor
+// of S is built in place from HBM and rebuilt from HBM for the jitter ladder, the
+// cross block is solved in place twice, Λ overwrites P.  Products, factors and solves
+// are the blocked DMMA routines of group.cuh; a stencil F (m.fst) forms C with four
+// FMAs per entry.  About 1/4 of the FLOPs and 3/5 of the shared memory of
+// backward_step_group, so five items run per SM.
+constexpr int kBwdLeanThreads = 128;
+__host__ __device__ inline int bwd_lean_doubles(int d) {
+  return 3 * d * d + dinv_doubles(d) + 8 * d + 4;
+}
+
+__global__ void __launch_bounds__(kBwdLeanThreads)
+k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __restrict__ filt_cov,
+           const double* __restrict__ pred_cov, int Bfr, double* elems, double* term,
+           int* status, int store_cov, int t_lo, int t_hi) {
+  extern __shared__ double smem[];
+  const int d = m.dx, dd = d * d, T = m.T;
+  const Grp g = block_group();
+  double* Lb = smem;                    // chol(S), then chol(Λ)
+  double* W = Lb + dd;                  // C = F P -> L^{-1} C -> G^T
+  double* P = W + dd;                   // P -> Λ
+  double* dinv = P + dd;                // inverted 8×8 diagonal blocks
+  double* v = dinv + dinv_doubles(d);   // F m + b
+  double* fvb = v + 2 * d;              // stencil values [d][4]
+  int* fcb = reinterpret_cast<int*>(fvb + 4 * d);  // stencil columns [d][4]
+  double* red = fvb + 6 * d;
+  int* flag = reinterpret_cast<int*>(red + 2);
+  const int span = t_hi - t_lo;
+  const long long n_items = (long long)Bfr * span;
+  for (long long item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int b = (int)(item / span);
+    const int t = t_lo + (int)(item % span);
+    const double* fm = filt_mean + (size_t)b * (T + 1) * d;
+    const double* fc = filt_cov + (size_t)b * (T + 1) * dd;
+    const double* pc = pred_cov + (size_t)b * (T + 1) * dd;
+    int st = 0;
+    if (t == T) {  // terminal law (pit.cpp:85-87)
+      double* out = term + (size_t)b * term_stride(d);
+      g_copy(g, dd, fc + (size_t)T * dd, P);
+      g.sync();
+      st = g_chol_psd(g, d, P, Lb, dinv, flag, red);
+      for (int i = g.lane; i < d; i += g.size) out[i] = fm[(size_t)T * d + i];
+      for (int i = g.lane; i < dd; i += g.size) out[d + i] = Lb[i];
+      if (st && g.lane == 0) atomicMax(status + b, st);
+      g.sync();
+      continue;
+    }
+    double* out = elems + ((size_t)b * T + t) * elem_stride(d);
+    const double* S = pc + (size_t)(t + 1) * dd;
+    g_copy(g, dd, fc + (size_t)t * dd, P);
+    for (int i = g.ty(); i < d; i += g.ny())
+      for (int j = g.tx(); j < d; j += 16) Lb[i * d + j] = j <= i ? S[i * d + j] : 0.0;
+    if (m.fst)
+      for (int i = g.lane; i < d; i += g.size) stencil_row(m, t, b, i, fcb + 4 * i, fvb + 4 * i);
+    g.sync();
+    // C = F P
+    if (m.fst) {
+      for (int e = g.lane; e < dd; e += g.size) {
+        const int a = e / d, c = e % d;
+        double x = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x += fvb[4 * a + k] * P[fcb[4 * a + k] * d + c];
+        W[e] = x;
+      }
+    } else {
+      g_dmma<false, false>(g, d, d, d, m.Ft(t, b), d, P, d, W, d, false, false);
+    }
+    g.sync();
+    if (!g_all_zero(g, dd, W, flag)) {
+      bool ok = g_llt_blocked(g, d, Lb, flag, dinv);
+      if (!ok) {  // factor_psd ladder (gauss.cpp:26-35) on S, rebuilt from HBM
+        if (g.lane == 0) {
+          double tr = 0.0;
+          for (int i = 0; i < d; ++i) tr += S[i * d + i];
+          double sc = tr / static_cast<double>(d);
+          if (sc <= 0.0) {
+            double mx = 0.0;
+            for (int i = 0; i < dd; ++i) mx = fabs(S[i]) > mx ? fabs(S[i]) : mx;
+            sc = mx;
+          }
+          *red = sc;
+        }
+        g.sync();
+        const double sc = *red;
+        for (int e = 0; e < 2 && !ok; ++e) {
+          const double eps = e == 0 ? 1e-10 : 1e-8;
+          for (int i = g.ty(); i < d; i += g.ny())
+            for (int j = g.tx(); j < d; j += 16)
+              Lb[i * d + j] = j <= i ? S[i * d + j] + (i == j ? (eps * sc) * 1.0 : 0.0) : 0.0;
+          g.sync();
+          ok = g_llt_blocked(g, d, Lb, flag, dinv);
+        }
+      }
+      if (!ok) {
+        if (g.lane == 0) atomicMax(status + b, 2);
+        g.sync();
+        continue;
+      }
+      g_trsm_lower_blocked(g, d, Lb, dinv, d, W, d);                    // W = L^{-1} C
+      g_dmma<true, false>(g, d, d, d, W, d, W, d, P, d, true, true);   // Λ (lower) = P - W^T W
+      g.sync();
+      g_trsm_lower_t_blocked(g, d, Lb, dinv, d, W, d);                  // W = S^{-1} C = G^T
+      for (int i = g.ty(); i < d; i += g.ny())
+        for (int j = g.tx(); j < d; j += 16)
+          if (j > i) P[i * d + j] = P[j * d + i];
+      g.sync();
+    }
+    if (g_flip_backward_gain) {
+      for (int i = g.lane; i < dd; i += g.size) W[i] = -W[i];
+      g.sync();
+    }
+    // offset = m_t - G (F m_t + b_t)
+    const double* mt = fm + (size_t)t * d;
+    const double* bt = m.bt(t, b);
+    for (int i = g.lane; i < d; i += g.size) {
+      double x = 0.0;
+      if (m.fst) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x += fvb[4 * i + k] * mt[fcb[4 * i + k]];
+      } else {
+        const double* F = m.Ft(t, b);
+        for (int k = 0; k < d; ++k) x += F[i * d + k] * mt[k];
+      }
+      v[i] = x + bt[i];
+    }
+    g.sync();
+    for (int i = g.lane; i < d; i += g.size) {
+      double x = 0.0;
+      for (int k = 0; k < d; ++k) x += W[k * d + i] * v[k];
+      out[dd + i] = mt[i] - x;
+    }
+    for (int e = g.lane; e < dd; e += g.size) out[e] = W[(e % d) * d + e / d];
+    if (store_cov) {
+      for (int e = g.lane; e < dd; e += g.size) out[dd + d + e] = P[e];
+    } else {
+      st = g_chol_psd(g, d, P, Lb, dinv, flag, red);
+      for (int e = g.lane; e < dd; e += g.size) out[dd + d + e] = Lb[e];
     }
     if (st && g.lane == 0) atomicMax(status + b, st);
     g.sync();
@@ -640,12 +789,13 @@ int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, 
                         int Bfr, double* elems, double* term, int* st_fr, int store_cov,
                         cudaStream_t stream, int t_lo = 0, int t_hi = -1) {
   const int d = dm.dx;
-  const int per_blk = bwd_buffers(false) * d * d + 4 * d + 4;  // CTA items: F from global
+  const int per_blk = bwd_buffers(dm.fst != 0) * d * d + 4 * d + 4;  // CTA items: F from global
   const int per = bwd_buffers(true) * d * d + 4 * d + 4;       // warp items: F staged
   if (t_hi < 0) t_hi = dm.T + 1;
   if (t_hi <= t_lo) return AUXMC_OK;
   const long long n_items = (long long)Bfr * (t_hi - t_lo);
   if (d <= 4) {
+    if (dm.fst) return AUXMC_E_CONFIG;  // the register path reads a dense F
     const int grid = (int)std::min<long long>((n_items + 127) / 128, 148LL * 16);
     switch (d) {
 #define CASE(D)                                                                                  \
@@ -657,12 +807,13 @@ int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, 
 #undef CASE
     }
   } else if (d > 16) {
-    const size_t smem = sizeof(double) * per_blk;
-    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_bwd_elements<true>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t smem = sizeof(double) * bwd_lean_doubles(d);
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_bwd_lean, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
     const int grid = (int)std::min<long long>(n_items, 148LL * 64);
-    AUXMC_LAUNCH(k_bwd_elements<true>, grid, 128, smem, stream, dm, fm, fc, pc, Bfr, elems, term,
+    AUXMC_LAUNCH(k_bwd_lean, grid, kBwdLeanThreads, smem, stream, dm, fm, fc, pc, Bfr, elems, term,
                  st_fr, store_cov, t_lo, t_hi);
+    (void)per_blk;
   } else {
     const int warps = 4;
     const size_t smem = sizeof(double) * per * warps;

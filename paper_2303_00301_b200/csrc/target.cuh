@@ -16,6 +16,7 @@ struct DevTarget {
   const uint8_t* gmask;
   const double *gH, *gc, *gR;
   double lz_sigma, lz_rho, lz_beta, lz_h, l96_F, l96_h;
+  int exact_sel;
   __device__ __forceinline__ const double* Ft(int t) const { return F + (size_t)(nF > 1 ? t : 0) * dx * dx; }
   __device__ __forceinline__ const double* bt(int t) const { return b + (size_t)(nF > 1 ? t : 0) * dx; }
   __device__ __forceinline__ const double* Qt(int t) const { return Q + (size_t)(nF > 1 ? t : 0) * dx * dx; }
@@ -36,6 +37,7 @@ static DevTarget to_dev_target(const auxmc_target& t) {
   d.data = t.data; d.gmask = t.gmask; d.gH = t.gH; d.gc = t.gc; d.gR = t.gR;
   d.lz_sigma = t.lz_sigma; d.lz_rho = t.lz_rho; d.lz_beta = t.lz_beta; d.lz_h = t.lz_h;
   d.l96_F = t.l96_F; d.l96_h = t.l96_h;
+  d.exact_sel = t.exact_sel;
   return d;
 }
 

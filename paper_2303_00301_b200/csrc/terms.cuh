@@ -31,12 +31,23 @@ __device__ __forceinline__ double path_term_k(const DevModel& m, const double* _
   } else if (k <= T) {
     const int t = k - 1;
     nn = dx;
-    const double* F = m.Ft(t, b);
     const double* bb = m.bt(t, b);
-    for (int i = 0; i < dx; ++i) {
-      double s = 0.0;
-      for (int j = 0; j < dx; ++j) s += F[i * dx + j] * x[(size_t)t * dx + j];
-      r[i] = x[(size_t)(t + 1) * dx + i] - (s + bb[i]);
+    if (m.fst) {  // stencil F (l96_row): the dense row's nonzeros in column order
+      for (int i = 0; i < dx; ++i) {
+        int cs[4];
+        double vs[4];
+        stencil_row(m, t, b, i, cs, vs);
+        double s = 0.0;
+        for (int a = 0; a < 4; ++a) s += vs[a] * x[(size_t)t * dx + cs[a]];
+        r[i] = x[(size_t)(t + 1) * dx + i] - (s + bb[i]);
+      }
+    } else {
+      const double* F = m.Ft(t, b);
+      for (int i = 0; i < dx; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < dx; ++j) s += F[i * dx + j] * x[(size_t)t * dx + j];
+        r[i] = x[(size_t)(t + 1) * dx + i] - (s + bb[i]);
+      }
     }
     const int j = 1 + (m.sQ ? b * m.nQ : 0) + (m.nQ > 1 ? t : 0);
     L = Ls + (size_t)j * W * W;

@@ -632,7 +632,30 @@ struct GenSSMTarget::Impl {
     t.lz_h = lz_h;
     t.l96_F = l96_F;
     t.l96_h = l96_h;
+    t.exact_sel = exact_selection() ? 1 : 0;
     uploaded = true;
+  }
+
+  // auxmc_target::exact_sel: unit selection rows, diagonal positive R_e, ne = 1
+  bool exact_selection() const {
+    if (q == 0) return true;
+    if (ne != 1) return false;
+    std::vector<int> used(dx, 0);
+    for (int k = 0; k < q; ++k) {
+      int nz = 0, col = -1;
+      for (int j = 0; j < dx; ++j)
+        if (eH[(size_t)k * dx + j] != 0.0) {
+          ++nz;
+          col = j;
+          if (eH[(size_t)k * dx + j] != 1.0) return false;
+        }
+      if (nz != 1 || used[col]++) return false;
+      for (int j = 0; j < q; ++j) {
+        const double v = eR[(size_t)k * q + j];
+        if (j == k ? !(v > 0.0) : v != 0.0) return false;
+      }
+    }
+    return true;
   }
 };
 
