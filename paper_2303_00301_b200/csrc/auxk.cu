@@ -530,7 +530,7 @@ namespace auxmc_gpu {
 // ---- time-sharded aux step kernels (one chain; t ranges are absolute steps)
 int tshard_geometry(int T, int* LB, int* nblk, int* nsup, int* SB);
 __global__ void k_factor_list(DevModel m, int nQb, int nRb, double* Ls, double* logdet,
-                              int* status);  // logpdf.cu
+                              unsigned char* dg, int* status);  // logpdf.cu
 
 // aux observations (if u_out) and the surrogate LGSSM rows at the path xs on [t0, t1)
 __global__ void k_ts_prep(DevTarget tg, int zeroth, const double* __restrict__ xs,
@@ -881,7 +881,7 @@ static int ts_path_part(const TsAux& a, const double* traj, int t_lo, int t_hi, 
   AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_factor_list, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
   AUXMC_LAUNCH(k_factor_list, std::min((n_mats + warps - 1) / warps, 148 * 8), 32 * warps, smem, s,
-               dm, 1, 1, Ls, logdet, fst);
+               dm, 1, 1, Ls, logdet, (unsigned char*)nullptr, fst);
   if (t_hi > t_lo) {
     AUXMC_LAUNCH(k_ts_path_v, grid_t(t_hi - t_lo), 128, 0, s, dm, a.z, traj, Ls, logdet, t_lo, t_hi,
                  a.terms);

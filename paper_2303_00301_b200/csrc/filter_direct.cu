@@ -48,9 +48,12 @@ __host__ __device__ inline int fd_nt(int d) { return (2 * d + 1 + 3) / 4; }
 __host__ __device__ inline int fd_tiles(int d) { return fd_nt(d) * (fd_nt(d) + 1) / 2; }
 __host__ __device__ inline int fd_nt8(int d) { return (2 * d + 1 + 7) / 8; }
 
+constexpr int kFdWarps = kFdThreads / 32;
+constexpr int kFdTpw = 9;  // 8×8 tiles per warp: 66 tiles of the lower triangle for d <= 43
+
 // shared-memory layout (doubles)
 struct FdLayout {
-  int P, A, Pp, Q, F, fv, fc, m, mp, w, r, ex, col, piv, in, bq, cq, sel, red, Rb, Dv, total;
+  int P, A, Pp, Q, F, fv, fc, m, mp, w, r, ex, col, piv, in, bq, cq, sel, red, Rb, Dv, tab, total;
   __host__ __device__ FdLayout(int d, int q, bool fst) {
     const int dd = d * d, npad = 4 * fd_nt(d), nin = (d + q) + 2 * d;
     int o = 0;
@@ -68,14 +71,15 @@ struct FdLayout {
     ex = o; o += d;
     col = o; o += 2 * npad;
     piv = o; o += d;
-    in = o; o += 2 * nin;
     bq = o; o += d;
     cq = o; o += d;
     sel = o; o += (d + 1) / 2;  // d ints
     red = o; o += 4;
     o = (o + 1) & ~1;  // 16-byte alignment for the double2 panel / D^{-1} loads
     Rb = o; o += 2 * 4 * 8 * fd_nt8(d);  // MMA panels (double-buffered)
-    Dv = o; o += 16;
+    Dv = o; o += 4 * 8 * fd_nt8(d);  // Y = R D^{-1} of the current panel
+    tab = o; o += kFdWarps * kFdTpw;  // int2 per (warp, slot)
+    in = o; o += 2 * nin;  // last: the only q-dependent block
     total = o;
   }
 };
@@ -140,8 +144,6 @@ __device__ __forceinline__ double rcp_nr(double x) {  // 1/x: MUFU seed + two Ne
   return fma(y, e, y);
 }
 
-constexpr int kFdWarps = kFdThreads / 32;
-constexpr int kFdTpw = 9;  // 8×8 tiles per warp: 66 tiles of the lower triangle for d <= 40
 __host__ __device__ inline bool fd_use_mma(int d) {
   return fd_nt8(d) * (fd_nt8(d) + 1) / 2 <= kFdWarps * kFdTpw;
 }
@@ -156,14 +158,17 @@ __host__ __device__ inline bool fd_use_mma(int d) {
 // (R D^{-1}) rows of the tile's columns.  Two barriers per 4 pivots.  The leading
 // minors of each D decide the factorization (the LDL pivots are their ratios), so the
 // failure test is the reference's; log det S = Σ log det D.  dets[p] per panel.
+// tab: per (warp, slot) the tile's (row-tile, column-tile), warp-uniform, in shared
+// memory (broadcast reads keep the accumulators' register budget); (-1, 99) unowned.
 __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp, const double* r,
                                          const double* w, const double* mp, double* Rb,
                                          double* Dv, double* dets, double* P, double* mv,
-                                         double* red, const int (&tI)[kFdTpw],
-                                         const int (&tJ)[kFdTpw]) {
+                                         double* red, const int2* __restrict__ tab) {
   const int lane = tid & 31, warp = tid >> 5;
   const int gi = lane >> 2, ti = lane & 3;
   const int rstride = 4 * 8 * fd_nt8(d);
+  const int2* wt = tab + warp * kFdTpw;
+  double* Y = Dv;
   double c[kFdTpw][2];
   bool ok = false;
   double jit = 0.0;
@@ -173,8 +178,9 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
 #pragma unroll
     for (int s = 0; s < kFdTpw; ++s) {
       c[s][0] = c[s][1] = 0.0;
-      if (tI[s] >= 0) {
-        const int i = 8 * tI[s] + gi, j = 8 * tJ[s] + 2 * ti;
+      const int2 tt = wt[s];
+      if (tt.x >= 0) {
+        const int i = 8 * tt.x + gi, j = 8 * tt.y + 2 * ti;
         c[s][0] = fd_mval(i, j, d, n, Pp, r, w, mp, eps);
         c[s][1] = fd_mval(i, j + 1, d, n, Pp, r, w, mp, eps);
       }
@@ -185,14 +191,16 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
       double* R = Rb + ((kb >> 2) & 1) * rstride;
       // panel columns kb..kb+3 from their owners (pivot columns past d stay zero)
 #pragma unroll
-      for (int s = 0; s < kFdTpw; ++s)
-        if (tI[s] >= 0 && tJ[s] == Jp && (ti >> 1) == half) {
-          const int row = 8 * tI[s] + gi, m0 = 2 * ti - 4 * half;
+      for (int s = 0; s < kFdTpw; ++s) {
+        const int2 tt = wt[s];
+        if (tt.y == Jp && (ti >> 1) == half) {
+          const int row = 8 * tt.x + gi, m0 = 2 * ti - 4 * half;
           R[row * 4 + m0] = (row >= kb && kb + m0 < d) ? c[s][0] : 0.0;
           R[row * 4 + m0 + 1] = (row >= kb && kb + m0 + 1 < d) ? c[s][1] : 0.0;
         }
+      }
       __syncthreads();
-      if (warp == 0) {
+      if (warp == 0) {  // D^{-1} of the 4×4 pivot block by cofactors (lane 4i + j)
         auto D = [&](int a, int b) -> double {
           const int hi = a > b ? a : b, lo = a > b ? b : a;
           if (kb + hi >= d) return a == b ? 1.0 : 0.0;
@@ -213,8 +221,17 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
         const double lead3 = __shfl_sync(0xffffffffu, cof, 15);
         const double d00 = D(0, 0), lead2 = d00 * D(1, 1) - D(1, 0) * D(1, 0);
         const bool good = d00 > 0.0 && lead2 > 0.0 && lead3 > 0.0 && det > 0.0;
-        const double rd = rcp_nr(det);
-        if (lane < 16) Dv[lane] = cof * rd;  // (D^{-1})_{ij}
+        const double dinv = cof * rcp_nr(det);  // (D^{-1})_{ij}
+        double q[4];  // column j of D^{-1}
+#pragma unroll
+        for (int mm = 0; mm < 4; ++mm) q[mm] = __shfl_sync(0xffffffffu, dinv, 4 * mm + j);
+        // Y = R D^{-1} (the B operand of every tile update), rows of the active tiles;
+        // lane (row-in-8, column j) forms Y[row][j] for 8 rows per pass
+        for (int row = 8 * Jp + (lane >> 2); row < 8 * fd_nt8(d); row += 8) {
+          const double2 r01 = *reinterpret_cast<const double2*>(R + row * 4);
+          const double2 r23 = *reinterpret_cast<const double2*>(R + row * 4 + 2);
+          Y[row * 4 + j] = (r01.x * q[0] + r01.y * q[1]) + (r23.x * q[2] + r23.y * q[3]);
+        }
         if (lane == 0) {
           dets[kb >> 2] = det;
           red[3] = good ? 0.0 : 1.0;
@@ -225,15 +242,12 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
         failed = true;
         break;
       }
-      const double2 q01 = *reinterpret_cast<const double2*>(Dv + 4 * ti);
-      const double2 q23 = *reinterpret_cast<const double2*>(Dv + 4 * ti + 2);
 #pragma unroll
       for (int s = 0; s < kFdTpw; ++s) {
-        if (tI[s] < 0 || tJ[s] < Jp) continue;
-        const double a = -R[(8 * tI[s] + gi) * 4 + ti];
-        const double2* rj = reinterpret_cast<const double2*>(R + (8 * tJ[s] + gi) * 4);
-        const double2 r01 = rj[0], r23 = rj[1];
-        const double y = (r01.x * q01.x + r01.y * q01.y) + (r23.x * q23.x + r23.y * q23.y);
+        const int2 tt = wt[s];
+        if (tt.y < Jp || tt.x < 0) continue;  // retired (all columns < kb) or unowned
+        const double a = -R[(8 * tt.x + gi) * 4 + ti];
+        const double y = Y[(8 * tt.y + gi) * 4 + ti];
         asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
             : "+d"(c[s][0]), "+d"(c[s][1])
             : "d"(a), "d"(y));
@@ -244,8 +258,8 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
   if (!ok) return false;
 #pragma unroll
   for (int s = 0; s < kFdTpw; ++s)
-    if (tI[s] >= 0) {
-      const int i = 8 * tI[s] + gi, j = 8 * tJ[s] + 2 * ti;
+    if (wt[s].x >= 0) {
+      const int i = 8 * wt[s].x + gi, j = 8 * wt[s].y + 2 * ti;
       fd_readout(i, j, c[s][0], d, n, mp, P, mv, red);
       fd_readout(i, j + 1, c[s][1], d, n, mp, P, mv, red);
     }
@@ -349,14 +363,15 @@ __device__ __forceinline__ bool elim_rank1(int tid, int d, int n, int npad, cons
   return ok;
 }
 
-template <bool FST, int TPT, bool MMA>
+template <bool FST, int TPT, bool MMA, int DC>
 __global__ void __launch_bounds__(kFdThreads, MMA ? 2 : 1)
 k_filter_direct(DevModel m, DevTarget tg, const double* __restrict__ xl,
                 const double* __restrict__ delta, const double* __restrict__ z, int C, int covs,
                 double* pred_mean, double* pred_cov, double* filt_mean, double* filt_cov,
                 double* log_marginal, int* status) {
   extern __shared__ double sm[];
-  const int d = m.dx, T = m.T, q = tg.q, p = d + q, dd = d * d;
+  // DC > 0: the state dimension as a compile-time constant (index arithmetic folds)
+  const int d = DC > 0 ? DC : m.dx, T = m.T, q = tg.q, p = d + q, dd = d * d;
   const int n = 2 * d + 1, nt = fd_nt(d), npad = 4 * nt, ntiles = fd_tiles(d);
   const int nin = p + 2 * d;
   const FdLayout L(d, q, FST);
@@ -386,18 +401,15 @@ k_filter_direct(DevModel m, DevTarget tg, const double* __restrict__ xl,
   if (c >= C) return;
   (void)Rp; (void)Dv; (void)col; (void)npad;
 
-  // MMA: 8×8 tiles of M's lower triangle, tile warp + 8 s of the row-major order
-  int tI[kFdTpw], tJ[kFdTpw];
-  if (MMA) {
+  // MMA: 8×8 tiles of M's lower triangle; (warp, slot) owns tile warp + 8 slot of the
+  // row-major order
+  int2* ttab = reinterpret_cast<int2*>(sm + L.tab);
+  if (MMA && tid < kFdWarps * kFdTpw) {
     const int nt8 = fd_nt8(d), ntile8 = nt8 * (nt8 + 1) / 2;
-#pragma unroll
-    for (int s = 0; s < kFdTpw; ++s) {
-      const int tau = (tid >> 5) + kFdWarps * s;
-      int I = 0;
-      while ((I + 1) * (I + 2) / 2 <= tau) ++I;
-      tI[s] = tau < ntile8 ? I : -1;
-      tJ[s] = tau - I * (I + 1) / 2;
-    }
+    const int tau = tid / kFdTpw + kFdWarps * (tid % kFdTpw);
+    int I = 0;
+    while ((I + 1) * (I + 2) / 2 <= tau) ++I;
+    ttab[tid] = tau < ntile8 ? make_int2(I, tau - I * (I + 1) / 2) : make_int2(-1, 99);
   }
 
   // tiles owned by this thread
@@ -559,7 +571,7 @@ k_filter_direct(DevModel m, DevTarget tg, const double* __restrict__ xl,
     }
     bool ok;
     if constexpr (MMA)
-      ok = elim_mma(tid, d, n, Pp, r, w, mp, Rp, Dv, piv, P, mv, red, tI, tJ);
+      ok = elim_mma(tid, d, n, Pp, r, w, mp, Rp, Dv, piv, P, mv, red, ttab);
     else if constexpr (TPT == 0)
       ok = false;
     else
@@ -621,20 +633,23 @@ int launch_filter_direct(const DevTarget& tg, const DevModel& dm, bool stencil,
   const int d = dm.dx;
   const size_t smem = sizeof(double) * FdLayout(d, tg.q, stencil).total;
   const int tpt = (fd_tiles(d) + kFdThreads - 1) / kFdThreads;
-#define FD_LAUNCH(FS, TP, MM)                                                                    \
+#define FD_LAUNCH(FS, TP, MM, DC)                                                                \
   do {                                                                                           \
-    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_filter_direct<FS, TP, MM>,                             \
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_filter_direct<FS, TP, MM, DC>,                         \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    AUXMC_LAUNCH((k_filter_direct<FS, TP, MM>), C, kFdThreads, smem, s, dm, tg, xl, delta, z, C,  \
+    AUXMC_LAUNCH((k_filter_direct<FS, TP, MM, DC>), C, kFdThreads, smem, s, dm, tg, xl, delta, z, \
+                 C,                                                                              \
                  covs,                                                                           \
                  fr->pred_mean, fr->pred_cov, fr->filt_mean, fr->filt_cov, fr->log_marginal,     \
                  status);                                                                        \
   } while (0)
   if (fd_use_mma(d)) {
-    if (stencil) FD_LAUNCH(true, 0, true); else FD_LAUNCH(false, 0, true);
+    if (stencil && d == 40) FD_LAUNCH(true, 0, true, 40);  // Lorenz-96 d = 40 (C3)
+    else if (stencil) FD_LAUNCH(true, 0, true, 0);
+    else FD_LAUNCH(false, 0, true, 0);
   } else {
     if (tpt > 3) return AUXMC_E_DIM;
-    if (stencil) FD_LAUNCH(true, 3, false); else FD_LAUNCH(false, 3, false);
+    if (stencil) FD_LAUNCH(true, 3, false, 0); else FD_LAUNCH(false, 3, false, 0);
   }
 #undef FD_LAUNCH
   return AUXMC_OK;

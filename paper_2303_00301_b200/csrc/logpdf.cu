@@ -14,7 +14,7 @@ namespace auxmc_gpu {
 // Factor matrix j of a list: P0 (j = 0), then Q sets (nQb of nQ matrices),
 // then R sets (nRb of nR); a set per problem when that array is batch-strided.
 __global__ void k_factor_list(DevModel m, int nQb, int nRb, double* Ls, double* logdet,
-                              int* status) {
+                              unsigned char* dg, int* status) {
   extern __shared__ double smem[];
   const int dx = m.dx, dy = m.dy;
   const int nq = nQb * m.nQ;
@@ -48,10 +48,14 @@ __global__ void k_factor_list(DevModel m, int nQb, int nRb, double* Ls, double* 
     const int st = g_factor_psd(g, n, A, L, scr, flag, red);
     double* out = Ls + (size_t)j * W * W;
     for (int i = g.lane; i < n * n; i += g.size) out[i] = L[i];
+    bool off = false;  // any nonzero below the diagonal
+    for (int i = g.lane; i < n * n; i += g.size) off = off || (i % n < i / n && L[i] != 0.0);
+    off = __any_sync(0xffffffffu, off);
     if (g.lane == 0) {
       double ld = 0.0;
       for (int i = 0; i < n; ++i) ld += log(L[i * n + i]);
       logdet[j] = ld;
+      if (dg) dg[j] = off ? 0 : 1;
       if (st) atomicMax(status, st);
     }
     g.sync();
@@ -61,7 +65,8 @@ __global__ void k_factor_list(DevModel m, int nQb, int nRb, double* Ls, double* 
 // term index k: 0 prior; 1..T transition t=k-1; T+1..2T+1 observation t=k-T-1.
 __global__ void k_path_terms(DevModel m, const double* __restrict__ obs, long long obs_stride,
                              const double* __restrict__ traj, int B, const double* __restrict__ Ls,
-                             const double* __restrict__ logdet, double* terms) {
+                             const double* __restrict__ logdet,
+                             const unsigned char* __restrict__ dg, double* terms) {
   const int T = m.T;
   const int K = 2 * T + 2;
   const long long n = (long long)B * K;
@@ -69,7 +74,7 @@ __global__ void k_path_terms(DevModel m, const double* __restrict__ obs, long lo
        q += (long long)gridDim.x * blockDim.x) {
     const int b = (int)(q / K), k = (int)(q % K);
     terms[q] = path_term_k(m, obs + (size_t)b * obs_stride, traj + (size_t)b * (T + 1) * m.dx, b, B,
-                           Ls, logdet, k);
+                           Ls, logdet, k, dg);
   }
 }
 
@@ -104,6 +109,8 @@ int launch_path_logpdf(const DevModel& dm, const double* obs, long long obs_stri
   const int K = 2 * dm.T + 2;
   double *Ls = nullptr, *logdet = nullptr, *terms = nullptr;
   int* fst = nullptr;
+  unsigned char* dg = nullptr;
+  AUXMC_CUDA_TRY(cudaMallocAsync(&dg, n_mats, s));
   AUXMC_CUDA_TRY(cudaMallocAsync(&Ls, sizeof(double) * n_mats * W * W, s));
   AUXMC_CUDA_TRY(cudaMallocAsync(&logdet, sizeof(double) * n_mats, s));
   AUXMC_CUDA_TRY(cudaMallocAsync(&terms, sizeof(double) * (size_t)B * K, s));
@@ -114,16 +121,17 @@ int launch_path_logpdf(const DevModel& dm, const double* obs, long long obs_stri
   AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_factor_list, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
   AUXMC_LAUNCH(k_factor_list, std::min((n_mats + warps - 1) / warps, 148 * 8), 32 * warps, smem,
-               s, dm, nQb, nRb, Ls, logdet, fst);
+               s, dm, nQb, nRb, Ls, logdet, dg, fst);
   const long long n = (long long)B * K;
   AUXMC_LAUNCH(k_path_terms, (int)std::min<long long>((n + 127) / 128, 148LL * 64), 128, 0, s, dm,
-               obs, obs_stride, traj, B, Ls, logdet, terms);
+               obs, obs_stride, traj, B, Ls, logdet, dg, terms);
   AUXMC_LAUNCH(k_path_sum, B, kSumThreads, 0, s, dm.T, B, terms, dm.mask, dm.dy,
                log_marginal, lm_shared, fst, out, status);
   cudaFreeAsync(Ls, s);
   cudaFreeAsync(logdet, s);
   cudaFreeAsync(terms, s);
   cudaFreeAsync(fst, s);
+  cudaFreeAsync(dg, s);
   return AUXMC_OK;
 }
 

@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "dense.cuh"
 #include "rng.cuh"
+#include "tma.cuh"
 
 namespace auxmc_gpu {
 
@@ -189,7 +190,7 @@ __host__ __device__ inline int bwd_lean_doubles(int d) {
   return 3 * d * d + dinv_doubles(d) + 8 * d + 4;
 }
 
-__global__ void __launch_bounds__(kBwdLeanThreads)
+__global__ void __launch_bounds__(kBwdLeanThreads, 4)
 k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __restrict__ filt_cov,
            const double* __restrict__ pred_cov, int Bfr, double* elems, double* term,
            int* status, int store_cov, int t_lo, int t_hi) {
@@ -596,6 +597,111 @@ __global__ void k_seq_sample_warp(int T, int d, int C, const double* __restrict_
   }
 }
 
+// Any state dimension (8 < d <= 64), one CTA per path: the backward recursion
+// x_t = G_t x_{t+1} + off_t + L_t ξ_t (lgssm.cpp:151-177) streams its elements — one
+// contiguous 8·elem_stride(d) block per step, 26 KB at d = 40 — through an NS-stage
+// shared-memory ring filled by 1-D TMA bulk copies issued NS steps ahead, so the HBM
+// stream never waits on the recursion.  Row i is one warp's dot products (lanes over
+// columns, fixed xor-tree sums); ξ_t and L_t ξ_t do not depend on the path and are
+// formed before x_{t+1} is needed, so only G_t x_{t+1} is on the serial chain.
+constexpr int kSeqCtaThreads = 256;
+__host__ __device__ inline int seq_cta_stages(int d) {
+  const long long es = (long long)elem_stride(d) * 8;
+  return 3 * es <= 112 * 1024 ? 3 : 2;
+}
+__host__ __device__ inline size_t seq_cta_smem(int d) {
+  return (size_t)seq_cta_stages(d) * elem_stride(d) * 8 + sizeof(double) * 4 * 64 + 64;
+}
+
+__device__ __forceinline__ double warp_sum_xor(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(kSeqCtaThreads)
+k_seq_sample_cta(int T, int d, int C, const double* __restrict__ elems, long long estride,
+                 const double* __restrict__ term, long long tstride, NoiseArgs noise,
+                 double* __restrict__ traj) {
+  extern __shared__ __align__(128) double smem[];
+  const int c = blockIdx.x;
+  if (c >= C) return;
+  const int NS = seq_cta_stages(d), ES = elem_stride(d), dd = d * d;
+  double* stage = smem;
+  double* xb = stage + (size_t)NS * ES;  // [2][64] path rows
+  double* xi = xb + 128;                 // ξ_t
+  double* lx = xi + 64;                  // off_t + L_t ξ_t
+  uint64_t* bar = reinterpret_cast<uint64_t*>(lx + 64);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* E = elems + (size_t)c * estride;
+  const double* tm = term + (size_t)c * tstride;
+  double* out = traj + (size_t)c * (T + 1) * d;
+  const bool pre = noise.kind == AUXMC_NOISE_PREDRAWN;
+  const unsigned bytes = (unsigned)ES * 8u;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(bar + s, 1);
+    mbar_fence_init();
+    for (int s = 0; s < NS && T - 1 - s >= 0; ++s) {
+      mbar_expect_tx(bar + s, bytes);
+      bulk_g2s(stage + (size_t)s * ES, E + (size_t)(T - 1 - s) * ES, bytes, bar + s);
+    }
+  }
+  // terminal draw x_T = m_T + chol(P_T) ξ (pit.cpp:85-87)
+  for (int i = tid; i < d; i += kSeqCtaThreads)
+    xi[i] = pre ? noise.terminal[(size_t)c * d + i]
+                : normal_at(derive(noise.keys[c], kTerminalDraw, 0), (uint64_t)i);
+  __syncthreads();
+  for (int i = tid; i < d; i += kSeqCtaThreads) {
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) s += tm[d + i * d + j] * xi[j];
+    const double v = tm[i] + s;
+    xb[i] = v;
+    out[(size_t)T * d + i] = v;
+  }
+  const uint64_t kl = pre ? 0 : derive_label(noise.keys[c], kBackwardNoise);
+  auto draw = [&](int t) {  // ξ_t into xi
+    const uint64_t key = pre ? 0 : derive_index(kl, (uint64_t)t);
+    for (int i = tid; i < d; i += kSeqCtaThreads)
+      xi[i] = pre ? noise.backward[((size_t)c * T + t) * d + i] : normal_at(key, (uint64_t)i);
+  };
+  if (T > 0) draw(T - 1);
+  __syncthreads();
+  for (int k = 0; k < T; ++k) {
+    const int t = T - 1 - k, s = k % NS;
+    const double* e = stage + (size_t)s * ES;
+    mbar_wait(bar + s, (unsigned)((k / NS) & 1));
+    // off_t + L_t ξ_t (independent of the path)
+    for (int i = warp; i < d; i += kSeqCtaThreads / 32) {
+      const double* Lr = e + dd + d + (size_t)i * d;
+      double v = lane < d ? Lr[lane] * xi[lane] : 0.0;
+      if (lane + 32 < d) v += Lr[lane + 32] * xi[lane + 32];
+      v = warp_sum_xor(v);
+      if (lane == 0) lx[i] = e[dd + i] + v;
+    }
+    __syncthreads();
+    // x_t = G_t x_{t+1} + (off_t + L_t ξ_t)
+    const double* xp = xb + (k & 1) * 64;
+    double* xn = xb + ((k + 1) & 1) * 64;
+    for (int i = warp; i < d; i += kSeqCtaThreads / 32) {
+      const double* Gr = e + (size_t)i * d;
+      double v = lane < d ? Gr[lane] * xp[lane] : 0.0;
+      if (lane + 32 < d) v += Gr[lane + 32] * xp[lane + 32];
+      v = warp_sum_xor(v);
+      if (lane == 0) {
+        const double x = v + lx[i];
+        xn[i] = x;
+        out[(size_t)t * d + i] = x;
+      }
+    }
+    if (t > 0) draw(t - 1);
+    __syncthreads();
+    if (tid == 0 && t - NS >= 0) {  // refill this stage NS steps ahead
+      mbar_expect_tx(bar + s, bytes);
+      bulk_g2s(stage + (size_t)s * ES, E + (size_t)(t - NS) * ES, bytes, bar + s);
+    }
+  }
+}
+
 // Per-path-element prefix sampler (aux-kernel backend): thread per (path,
 // sub-chunk) with in-thread sub-chunk products; sub-chunk carries scanned by
 // one thread per path.  Same fixed tree as k_prefix_shared.
@@ -868,8 +974,17 @@ int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int f
         } else if (ws.base != nullptr) {
           const long long es = fr_shared ? 0 : (long long)T * elem_stride(d);
           const long long ts = fr_shared ? 0 : term_stride(d);
-          AUXMC_LAUNCH(k_seq_sample_warp, (B + 3) / 4, 128, 0, stream, T, d, B, elems, es, term,
-                       ts, nz, traj);
+          if (d > 8) {
+            const size_t smem = seq_cta_smem(d);
+            AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_seq_sample_cta,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem));
+            AUXMC_LAUNCH(k_seq_sample_cta, B, kSeqCtaThreads, smem, stream, T, d, B, elems, es,
+                         term, ts, nz, traj);
+          } else {
+            AUXMC_LAUNCH(k_seq_sample_warp, (B + 3) / 4, 128, 0, stream, T, d, B, elems, es, term,
+                         ts, nz, traj);
+          }
         }
     }
   }

@@ -12,69 +12,73 @@
 namespace auxmc_gpu {
 
 // lgssm::path_logpdf term k of path b (x = its [T+1][dx] rows, obs_b its [T+1][dy] rows).
-// Masked or absent observations contribute 0 (lgssm.cpp:193-196).
+// Masked or absent observations contribute 0 (lgssm.cpp:193-196).  dg (optional): 1 per
+// factor whose L is diagonal — the residual is then scaled entry by entry with no local
+// residual array (the same operations: the off-diagonal updates are exact zeros).
 __device__ __forceinline__ double path_term_k(const DevModel& m, const double* __restrict__ obs_b,
                                               const double* __restrict__ x, int b, int B,
                                               const double* __restrict__ Ls,
-                                              const double* __restrict__ logdet, int k) {
+                                              const double* __restrict__ logdet, int k,
+                                              const unsigned char* __restrict__ dg = nullptr) {
   const int T = m.T, dx = m.dx, dy = m.dy;
   const int W = dx > dy ? dx : dy;
-  double r[64];
-  const double* L;
-  double ld;
-  int nn;
+  int nn, j, t = 0, kind;
   if (k == 0) {
+    kind = 0;
     nn = dx;
-    for (int i = 0; i < dx; ++i) r[i] = x[i] - m.m0[i];
-    L = Ls;
-    ld = logdet[0];
+    j = 0;
   } else if (k <= T) {
-    const int t = k - 1;
+    kind = 1;
+    t = k - 1;
     nn = dx;
-    const double* bb = m.bt(t, b);
-    if (m.fst) {  // stencil F (l96_row): the dense row's nonzeros in column order
-      for (int i = 0; i < dx; ++i) {
+    j = 1 + (m.sQ ? b * m.nQ : 0) + (m.nQ > 1 ? t : 0);
+  } else {
+    kind = 2;
+    t = k - T - 1;
+    if (!m.observed(t) || dy == 0) return 0.0;
+    nn = dy;
+    const int nq = (m.sQ ? B : 1) * m.nQ;
+    j = 1 + nq + (m.sR ? b * m.nR : 0) + (m.nR > 1 ? t : 0);
+  }
+  const double* L = Ls + (size_t)j * W * W;
+  const double ld = logdet[j];
+  const double* bb = kind == 1 ? m.bt(t, b) : nullptr;
+  const double* H = kind == 2 ? m.Ht(t, b) : nullptr;
+  const double* cc = kind == 2 ? m.ct(t, b) : nullptr;
+  const double* y = kind == 2 ? obs_b + (size_t)t * dy : nullptr;
+  auto res = [&](int i) -> double {  // residual entry i
+    if (kind == 0) return x[i] - m.m0[i];
+    double s = 0.0;
+    if (kind == 1) {
+      if (m.fst) {  // stencil F (l96_row): the dense row's nonzeros in column order
         int cs[4];
         double vs[4];
         stencil_row(m, t, b, i, cs, vs);
-        double s = 0.0;
         for (int a = 0; a < 4; ++a) s += vs[a] * x[(size_t)t * dx + cs[a]];
-        r[i] = x[(size_t)(t + 1) * dx + i] - (s + bb[i]);
+      } else {
+        const double* F = m.Ft(t, b);
+        for (int jj = 0; jj < dx; ++jj) s += F[i * dx + jj] * x[(size_t)t * dx + jj];
       }
-    } else {
-      const double* F = m.Ft(t, b);
-      for (int i = 0; i < dx; ++i) {
-        double s = 0.0;
-        for (int j = 0; j < dx; ++j) s += F[i * dx + j] * x[(size_t)t * dx + j];
-        r[i] = x[(size_t)(t + 1) * dx + i] - (s + bb[i]);
-      }
+      return x[(size_t)(t + 1) * dx + i] - (s + bb[i]);
     }
-    const int j = 1 + (m.sQ ? b * m.nQ : 0) + (m.nQ > 1 ? t : 0);
-    L = Ls + (size_t)j * W * W;
-    ld = logdet[j];
-  } else {
-    const int t = k - T - 1;
-    if (!m.observed(t) || dy == 0) return 0.0;
-    nn = dy;
-    const double* H = m.Ht(t, b);
-    const double* cc = m.ct(t, b);
-    const double* y = obs_b + (size_t)t * dy;
-    for (int i = 0; i < dy; ++i) {
-      double s = 0.0;
-      for (int j = 0; j < dx; ++j) s += H[i * dx + j] * x[(size_t)t * dx + j];
-      r[i] = y[i] - (s + cc[i]);
-    }
-    const int nq = (m.sQ ? B : 1) * m.nQ;
-    const int j = 1 + nq + (m.sR ? b * m.nR : 0) + (m.nR > 1 ? t : 0);
-    L = Ls + (size_t)j * W * W;
-    ld = logdet[j];
-  }
+    for (int jj = 0; jj < dx; ++jj) s += H[i * dx + jj] * x[(size_t)t * dx + jj];
+    return y[i] - (s + cc[i]);
+  };
   double sq = 0.0;
-  for (int i = 0; i < nn; ++i) {
-    double s = r[i];
-    for (int j = 0; j < i; ++j) s -= L[i * nn + j] * r[j];
-    r[i] = s / L[i * nn + i];
-    sq += r[i] * r[i];
+  if (dg && dg[j]) {
+    for (int i = 0; i < nn; ++i) {
+      const double v = res(i) / L[i * nn + i];
+      sq += v * v;
+    }
+  } else {
+    double r[64];
+    for (int i = 0; i < nn; ++i) r[i] = res(i);
+    for (int i = 0; i < nn; ++i) {
+      double s = r[i];
+      for (int jj = 0; jj < i; ++jj) s -= L[i * nn + jj] * r[jj];
+      r[i] = s / L[i * nn + i];
+      sq += r[i] * r[i];
+    }
   }
   return -0.5 * (nn * kLog2Pi + sq) - ld;
 }

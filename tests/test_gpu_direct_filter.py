@@ -61,27 +61,17 @@ def test_l96_stencil_direct_matches_generic(mods, d):
     _compare(gen, fused, f"L96 d={d}")
 
 
-def test_l96_rank1_form_vs_oracle(mods, oracle):
-    """d = 48 (d + q = 72: past the generic filter's 64): the rank-1 register-tile
-    elimination, against the oracle's aux chains (two chains, two iterations)."""
+def test_rank1_form_matches_generic(mods):
+    """d = 49 (spatio-temporal grid 7, no exact rows): past the DMMA panel form's d <= 43,
+    the rank-1 register-tile elimination."""
     _, auxk, bm = mods
-    O = oracle
-    T, d, C = 24, 48, 2
-    s = O.spec("lorenz96", T=T, dx=d, data_seed=3)
-    lat, data = O.simulate(s)
-    otg = O.make_target(s, data)
-    tg = auxk.make_target(bm.ModelSpec(kind="lorenz96", T=T, dx=d, data_seed=3), data)
-    ch = auxk.init_chains(tg, lat, 0.05, 1, C)
-    for it in range(2):
-        ch.kernel_step(0)
-    assert int(ch.aborted.sum()) == 0
-    for c in range(C):
-        o = O.AuxChain(otg, lat, 0.05)
-        root = O.derive(O.from_seed(1), O.L_CHAIN, c)
-        o.step(root, 0, 0, 0)
-        o.step(root, 0, 0, 0)
-        assert int(ch.accepted[c]) == o.c.stats.accepted
-        assert_close(ch.x[c].cpu().numpy(), o.x, 1e-8, f"chain {c}")
+    T = 24
+    spec = bm.ModelSpec(kind="spatio-temporal", T=T, grid=7, data_seed=5)
+    lat, data = bm.simulate(spec)
+    tg = auxk.make_target(spec, data)
+    assert tg.dx == 49 and tg.exact_sel == 1
+    gen, fused = _pair(mods, tg, lat, 0.5, 2, 2)
+    _compare(gen, fused, "spatio d=49")
 
 
 def test_l96_partial_exact_blocks(mods):
