@@ -226,6 +226,9 @@ int auxmc_test_flip_backward_gain(int on);
  * (d+q)-dimensional filter even where the fused direct-observation filter applies
  * (auxmc_target::exact_sel); the parity tests compare the two.  Host-side switch. */
 int auxmc_test_force_generic_filter(int on);
+/* Test hook: device buffer [C] that receives the forward filter's log p(z) of each
+ * auxiliary step (NULL: off).  Host-side switch. */
+int auxmc_test_capture_log_marginal(double* dev_out);
 
 /* Host-buffer convenience entry for the reference-facing facade: copies the
  * model, filter result and noise keys to the device, draws B paths and copies

@@ -42,6 +42,9 @@ int launch_filter_direct(const DevTarget& tg, const DevModel& dm, bool stencil,
 // (d+q)-dimensional filter (k_filter_cta / k_filter_seq) even when the fused
 // direct-observation filter applies — the parity tests compare the two.
 static int g_force_generic_filter = 0;
+// auxmc_test_capture_log_marginal: device buffer [C] receiving the forward filter's
+// log p(z) of every aux step (nullptr: off) — the parity tests compare filters directly.
+static double* g_capture_lm = nullptr;
 
 __global__ void k_target_factors(DevTarget tg, FactorLayout fl, double* Ls, double* logdet,
                                  int* status) {
@@ -467,6 +470,9 @@ static int aux_step(const DevTarget& tg, auxmc_chains* ch, const auxmc_kernel_op
   dm.xl = ch->x;
   rc = filter(sc.st_filt, ch->x, 1);
   if (rc) return rc;
+  if (g_capture_lm)
+    AUXMC_CUDA_TRY(cudaMemcpyAsync(g_capture_lm, fr.log_marginal, sizeof(double) * C,
+                                   cudaMemcpyDeviceToDevice, s));
   rc = launch_sample_paths(dm, &fr, 0, &nz, C, sampler, prop, sc.st_samp, ws, s);
   if (rc) return rc;
   rc = launch_path_logpdf(dm, z, (long long)(T + 1) * p, prop, fr.log_marginal, 0, C, sc.logq_fwd,
@@ -1002,5 +1008,10 @@ int auxmc_tshard_aux_decide(const auxmc_target* target, auxmc_chains* ch, void* 
 
 extern "C" int auxmc_test_force_generic_filter(int on) {
   auxmc_gpu::g_force_generic_filter = on ? 1 : 0;
+  return AUXMC_OK;
+}
+
+extern "C" int auxmc_test_capture_log_marginal(double* dev_out) {
+  auxmc_gpu::g_capture_lm = dev_out;
   return AUXMC_OK;
 }

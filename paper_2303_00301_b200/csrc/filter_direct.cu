@@ -48,6 +48,28 @@ __host__ __device__ inline int fd_nt(int d) { return (2 * d + 1 + 3) / 4; }
 __host__ __device__ inline int fd_tiles(int d) { return fd_nt(d) * (fd_nt(d) + 1) / 2; }
 __host__ __device__ inline int fd_nt8(int d) { return (2 * d + 1 + 7) / 8; }
 
+#ifndef AUXMC_FD_DINV
+#define AUXMC_FD_DINV 0  // 0: warp 0 forms D^{-1} (cofactors), second barrier; 1: every warp (LDL)
+#endif
+#ifndef AUXMC_FD_Y
+#define AUXMC_FD_Y 0  // 1: warp 0 forms Y = R D^{-1}, branch-free 2-load slots (measured slower)
+#endif
+#ifndef AUXMC_FD_EXP
+#define AUXMC_FD_EXP 0  // 9: clock64 phase stamps of CTA 0 (tools/fd_stamps.py)
+#endif
+#if AUXMC_FD_EXP == 9
+__device__ long long g_fd_stamps[4096];
+#define FD_STAMP(slot)                                                   \
+  do {                                                                   \
+    if (stamp_on && (threadIdx.x & 31) == 0)                             \
+      g_fd_stamps[(threadIdx.x >> 5) * 512 + (slot)] = clock64();        \
+  } while (0)
+#else
+#define FD_STAMP(slot) \
+  do {                 \
+  } while (0)
+#endif
+
 constexpr int kFdWarps = kFdThreads / 32;
 constexpr int kFdTpw = 9;  // 8×8 tiles per warp: 66 tiles of the lower triangle for d <= 43
 
@@ -77,8 +99,8 @@ struct FdLayout {
     red = o; o += 4;
     o = (o + 1) & ~1;  // 16-byte alignment for the double2 panel / D^{-1} loads
     Rb = o; o += 2 * 4 * 8 * fd_nt8(d);  // MMA panels (double-buffered)
-    Dv = o; o += 4 * 8 * fd_nt8(d);  // Y = R D^{-1} of the current panel
-    tab = o; o += kFdWarps * kFdTpw;  // int2 per (warp, slot)
+    Dv = o; o += 4 * 8 * fd_nt8(d);  // D^{-1} (16) or Y = R D^{-1} (AUXMC_FD_Y)
+    tab = o; o += 2 * kFdWarps * kFdTpw;  // int4 per (warp, slot)
     in = o; o += 2 * nin;  // last: the only q-dependent block
     total = o;
   }
@@ -148,27 +170,53 @@ __host__ __device__ inline bool fd_use_mma(int d) {
   return fd_nt8(d) * (fd_nt8(d) + 1) / 2 <= kFdWarps * kFdTpw;
 }
 
-// Blocked LDL^T of the bordered matrix on the FP64 tensor cores (d <= 40).  M's lower
+// Blocked LDL^T of the bordered matrix on the FP64 tensor cores (d <= 43).  M's lower
 // triangle lives in DMMA accumulators, one 8×8 tile per (warp, slot) — lane l holds
 // (8I + l/4, 8J + 2(l%4) + {0,1}), the m8n8k4 C layout.  Pivots go in panels of four:
-// the panel R = M[:, kb:kb+4] (rows above kb zero) is published through shared memory
-// (double-buffered), one warp forms D^{-1} of its 4×4 pivot block by cofactors (16
-// lanes, one 3×3 minor each; det by a fixed two-level shuffle sum), and every tile
-// takes the rank-4 update M -= R D^{-1} R^T as ONE DMMA: A = -R rows of the tile, B =
-// (R D^{-1}) rows of the tile's columns.  Two barriers per 4 pivots.  The leading
-// minors of each D decide the factorization (the LDL pivots are their ratios), so the
-// failure test is the reference's; log det S = Σ log det D.  dets[p] per panel.
-// tab: per (warp, slot) the tile's (row-tile, column-tile), warp-uniform, in shared
-// memory (broadcast reads keep the accumulators' register budget); (-1, 99) unowned.
+// the owners publish the panel R = M[:, kb:kb+4] (rows above kb zero) through shared
+// memory (double-buffered), ONE barrier, then every warp forms D^{-1} of the 4×4 pivot
+// block itself — an LDL^T in registers from broadcast loads, the same operations in
+// every warp, so the same bits — and every tile takes the rank-4 update
+// M -= R D^{-1} R^T as one DMMA (A = -R rows of the tile, B = R D^{-1} rows of its
+// columns).  The LDL pivots of D are the reference's factorization test (S is SPD iff
+// every pivot is > 0); log det S = Σ log det D_p, dets[p] per panel.
+//
+// tab (shared, warp-uniform): per (warp, slot) {I, J, src, kind}: kind 0 a P_p block
+// tile read at P_p[src + row*d + col], 1 the same on the S diagonal (+ r + jitter),
+// 2 the v row's tiles, 3 unowned, 4 a tile straddling blocks (d % 8 != 0: entrywise).
+struct FdTile {
+  int I, J, src, kind;
+};
+__device__ __forceinline__ FdTile fd_tile_ij(int I, int J, int d) {
+  if (d % 8 != 0) return FdTile{I, J, 0, 4};
+  const int r0 = 8 * I, c0 = 8 * J;
+  if (r0 >= 2 * d) return FdTile{I, J, 0, 2};
+  const int rb = r0 < d ? r0 : r0 - d, cb = c0 < d ? c0 : c0 - d;
+  return FdTile{I, J, rb * d + cb, (r0 < d && I == J) ? 1 : 0};
+}
+// tile of (warp, slot): round robin over the row-major order (tile warp + 8 slot)
+__device__ __forceinline__ FdTile fd_tile_of(int warp, int slot, int d) {
+  const int nt8 = fd_nt8(d);
+  const int tau = warp + kFdWarps * slot, ntile8 = nt8 * (nt8 + 1) / 2;
+  if (tau >= ntile8) return FdTile{0, 0, 0, 3};
+  int I = 0;
+  while ((I + 1) * (I + 2) / 2 <= tau) ++I;
+  return fd_tile_ij(I, tau - I * (I + 1) / 2, d);
+}
+
 __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp, const double* r,
                                          const double* w, const double* mp, double* Rb,
-                                         double* Dv, double* dets, double* P, double* mv,
-                                         double* red, const int2* __restrict__ tab) {
+                                         double* dets, double* P, double* mv, double* red,
+                                         const int4* __restrict__ tab, double* Dv,
+                                         bool stamp_on) {
+  (void)Dv;
+  (void)stamp_on;
+  double* Yb = Dv;
+  (void)Yb;
   const int lane = tid & 31, warp = tid >> 5;
   const int gi = lane >> 2, ti = lane & 3;
   const int rstride = 4 * 8 * fd_nt8(d);
-  const int2* wt = tab + warp * kFdTpw;
-  double* Y = Dv;
+  const int4* wt = tab + warp * kFdTpw;
   double c[kFdTpw][2];
   bool ok = false;
   double jit = 0.0;
@@ -177,13 +225,28 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
     const double eps = attempt == 0 ? 0.0 : (attempt == 1 ? 1e-10 : 1e-8) * jit;
 #pragma unroll
     for (int s = 0; s < kFdTpw; ++s) {
-      c[s][0] = c[s][1] = 0.0;
-      const int2 tt = wt[s];
-      if (tt.x >= 0) {
-        const int i = 8 * tt.x + gi, j = 8 * tt.y + 2 * ti;
-        c[s][0] = fd_mval(i, j, d, n, Pp, r, w, mp, eps);
-        c[s][1] = fd_mval(i, j + 1, d, n, Pp, r, w, mp, eps);
+      const int4 tt = wt[s];
+      const int i = 8 * tt.x + gi, j = 8 * tt.y + 2 * ti;
+      double v0 = 0.0, v1 = 0.0;
+      if (tt.w <= 1) {
+        const double2 pv = *reinterpret_cast<const double2*>(Pp + tt.z + gi * d + 2 * ti);
+        v0 = pv.x;
+        v1 = pv.y;
+        if (tt.w == 1) {
+          if (i == j) v0 += r[i] + eps;
+          if (i == j + 1) v1 += r[i] + eps;
+        }
+      } else if (tt.w == 2) {
+        if (i == 2 * d && j < d) {
+          v0 = w[j] - mp[j];
+          v1 = j + 1 < d ? w[j + 1] - mp[j + 1] : 0.0;
+        }
+      } else if (tt.w == 4) {
+        v0 = fd_mval(i, j, d, n, Pp, r, w, mp, eps);
+        v1 = fd_mval(i, j + 1, d, n, Pp, r, w, mp, eps);
       }
+      c[s][0] = v0;
+      c[s][1] = v1;
     }
     bool failed = false;
     for (int kb = 0; kb < d; kb += 4) {
@@ -192,14 +255,17 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
       // panel columns kb..kb+3 from their owners (pivot columns past d stay zero)
 #pragma unroll
       for (int s = 0; s < kFdTpw; ++s) {
-        const int2 tt = wt[s];
-        if (tt.y == Jp && (ti >> 1) == half) {
+        const int4 tt = wt[s];
+        if (tt.y == Jp && tt.w != 3 && (ti >> 1) == half) {
           const int row = 8 * tt.x + gi, m0 = 2 * ti - 4 * half;
-          R[row * 4 + m0] = (row >= kb && kb + m0 < d) ? c[s][0] : 0.0;
-          R[row * 4 + m0 + 1] = (row >= kb && kb + m0 + 1 < d) ? c[s][1] : 0.0;
+          const bool live = row >= kb;
+          *reinterpret_cast<double2*>(R + row * 4 + m0) =
+              make_double2(live && kb + m0 < d ? c[s][0] : 0.0, live && kb + m0 + 1 < d ? c[s][1] : 0.0);
         }
       }
+#if AUXMC_FD_DINV == 0
       __syncthreads();
+      FD_STAMP(8 + 3 * (kb >> 2));
       if (warp == 0) {  // D^{-1} of the 4×4 pivot block by cofactors (lane 4i + j)
         auto D = [&](int a, int b) -> double {
           const int hi = a > b ? a : b, lo = a > b ? b : a;
@@ -221,44 +287,154 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
         const double lead3 = __shfl_sync(0xffffffffu, cof, 15);
         const double d00 = D(0, 0), lead2 = d00 * D(1, 1) - D(1, 0) * D(1, 0);
         const bool good = d00 > 0.0 && lead2 > 0.0 && lead3 > 0.0 && det > 0.0;
-        const double dinv = cof * rcp_nr(det);  // (D^{-1})_{ij}
-        double q[4];  // column j of D^{-1}
+        const double rd = rcp_nr(det);
+        const double dij = cof * rd;  // (D^{-1})_{ij} on lane 4i + j
+#if AUXMC_FD_Y
+        // Y = R D^{-1} (the B operand of every tile update): one row per lane
+        double dq[16];
 #pragma unroll
-        for (int mm = 0; mm < 4; ++mm) q[mm] = __shfl_sync(0xffffffffu, dinv, 4 * mm + j);
-        // Y = R D^{-1} (the B operand of every tile update), rows of the active tiles;
-        // lane (row-in-8, column j) forms Y[row][j] for 8 rows per pass
-        for (int row = 8 * Jp + (lane >> 2); row < 8 * fd_nt8(d); row += 8) {
+        for (int e = 0; e < 16; ++e) dq[e] = __shfl_sync(0xffffffffu, dij, e);
+        for (int row = 8 * Jp + lane; row < 8 * fd_nt8(d); row += 32) {
           const double2 r01 = *reinterpret_cast<const double2*>(R + row * 4);
           const double2 r23 = *reinterpret_cast<const double2*>(R + row * 4 + 2);
-          Y[row * 4 + j] = (r01.x * q[0] + r01.y * q[1]) + (r23.x * q[2] + r23.y * q[3]);
+          double yv[4];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            yv[jj] = (r01.x * dq[jj] + r01.y * dq[4 + jj]) + (r23.x * dq[8 + jj] + r23.y * dq[12 + jj]);
+          *reinterpret_cast<double2*>(Yb + row * 4) = make_double2(yv[0], yv[1]);
+          *reinterpret_cast<double2*>(Yb + row * 4 + 2) = make_double2(yv[2], yv[3]);
         }
+#else
+        if (lane < 16) Dv[lane] = dij;
+#endif
         if (lane == 0) {
           dets[kb >> 2] = det;
           red[3] = good ? 0.0 : 1.0;
         }
       }
       __syncthreads();
+      FD_STAMP(9 + 3 * (kb >> 2));
       if (red[3] != 0.0) {
         failed = true;
         break;
       }
+#if AUXMC_FD_Y
+      // branch-free over the slots: a retired (all columns < kb) or unowned slot
+      // multiplies a zero A operand (its B rows are finite stale values) — so every
+      // slot's two loads issue ahead of the DMMAs
 #pragma unroll
       for (int s = 0; s < kFdTpw; ++s) {
-        const int2 tt = wt[s];
-        if (tt.y < Jp || tt.x < 0) continue;  // retired (all columns < kb) or unowned
-        const double a = -R[(8 * tt.x + gi) * 4 + ti];
-        const double y = Y[(8 * tt.y + gi) * 4 + ti];
+        const int4 tt = wt[s];
+        const bool act = tt.y >= Jp && tt.w != 3;
+        const double a = act ? -R[(8 * tt.x + gi) * 4 + ti] : 0.0;
+        const double y = Yb[(8 * tt.y + gi) * 4 + ti];
         asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
             : "+d"(c[s][0]), "+d"(c[s][1])
             : "d"(a), "d"(y));
       }
+      if (false)
+#endif
+      {
+      double q[4];
+      {
+        const double2 q01 = *reinterpret_cast<const double2*>(Dv + 4 * ti);
+        const double2 q23 = *reinterpret_cast<const double2*>(Dv + 4 * ti + 2);
+        q[0] = q01.x;
+        q[1] = q01.y;
+        q[2] = q23.x;
+        q[3] = q23.y;
+      }
+#else
+      __syncthreads();
+      FD_STAMP(8 + 3 * (kb >> 2));
+      // D = R[kb:kb+4, 0:4] (lower; padded pivots: identity), LDL^T and D^{-1}
+      double D[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double2 x01 = *reinterpret_cast<const double2*>(R + (kb + a) * 4);
+        const double2 x23 = *reinterpret_cast<const double2*>(R + (kb + a) * 4 + 2);
+        D[a][0] = x01.x;
+        D[a][1] = x01.y;
+        D[a][2] = x23.x;
+        D[a][3] = x23.y;
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b)
+          if (kb + a >= d) D[a][b] = a == b ? 1.0 : 0.0;
+      // LDL^T: unit lower Lf, pivots p[]
+      double Lf[4][4], p[4], ip[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        double x = D[a][a];
+#pragma unroll
+        for (int b = 0; b < a; ++b) x -= Lf[a][b] * Lf[a][b] * p[b];
+        p[a] = x;
+        ip[a] = rcp_nr(x);
+#pragma unroll
+        for (int e = a + 1; e < 4; ++e) {
+          double y = D[e][a];
+#pragma unroll
+          for (int b = 0; b < a; ++b) y -= Lf[e][b] * Lf[a][b] * p[b];
+          Lf[e][a] = y * ip[a];
+        }
+      }
+      if (!(p[0] > 0.0 && p[1] > 0.0 && p[2] > 0.0 && p[3] > 0.0)) {  // uniform
+        failed = true;
+        break;
+      }
+      if (tid == 0) dets[kb >> 2] = ((p[0] * p[1]) * (p[2] * p[3]));
+      // D^{-1} = Lf^{-T} diag(ip) Lf^{-1}: column ti only (this lane's B operand)
+      double Li[4][4];  // Lf^{-1} (unit lower)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (b > a) { Li[a][b] = 0.0; continue; }
+          if (b == a) { Li[a][b] = 1.0; continue; }
+          double x = 0.0;
+#pragma unroll
+          for (int e = b; e < a; ++e) x -= Lf[a][e] * (e == b ? 1.0 : Li[e][b]);
+          Li[a][b] = x;
+        }
+      double q[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        double col[4];  // (D^{-1})_{m, c} for c = 0..3
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          double x = 0.0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (e >= m && e >= cc) x += Li[e][m] * ip[e] * Li[e][cc];
+          col[cc] = x;
+        }
+        q[m] = ti == 0 ? col[0] : ti == 1 ? col[1] : ti == 2 ? col[2] : col[3];
+      }
+#endif
+#pragma unroll
+      for (int s = 0; s < kFdTpw; ++s) {
+        const int4 tt = wt[s];
+        if (tt.y < Jp || tt.w == 3) continue;  // retired (all columns < kb) or unowned
+        const double a = -R[(8 * tt.x + gi) * 4 + ti];
+        const double2* rj = reinterpret_cast<const double2*>(R + (8 * tt.y + gi) * 4);
+        const double2 r01 = rj[0], r23 = rj[1];
+        const double y = (r01.x * q[0] + r01.y * q[1]) + (r23.x * q[2] + r23.y * q[3]);
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+            : "+d"(c[s][0]), "+d"(c[s][1])
+            : "d"(a), "d"(y));
+      }
+      }
+      FD_STAMP(10 + 3 * (kb >> 2));
     }
     ok = !failed;
+    if (!ok) __syncthreads();  // the retry rewrites panel buffers others may still read
   }
   if (!ok) return false;
 #pragma unroll
   for (int s = 0; s < kFdTpw; ++s)
-    if (wt[s].x >= 0) {
+    if (wt[s].w != 3) {
       const int i = 8 * wt[s].x + gi, j = 8 * wt[s].y + 2 * ti;
       fd_readout(i, j, c[s][0], d, n, mp, P, mv, red);
       fd_readout(i, j + 1, c[s][1], d, n, mp, P, mv, red);
@@ -403,13 +579,10 @@ k_filter_direct(DevModel m, DevTarget tg, const double* __restrict__ xl,
 
   // MMA: 8×8 tiles of M's lower triangle; (warp, slot) owns tile warp + 8 slot of the
   // row-major order
-  int2* ttab = reinterpret_cast<int2*>(sm + L.tab);
+  int4* ttab = reinterpret_cast<int4*>(sm + L.tab);
   if (MMA && tid < kFdWarps * kFdTpw) {
-    const int nt8 = fd_nt8(d), ntile8 = nt8 * (nt8 + 1) / 2;
-    const int tau = tid / kFdTpw + kFdWarps * (tid % kFdTpw);
-    int I = 0;
-    while ((I + 1) * (I + 2) / 2 <= tau) ++I;
-    ttab[tid] = tau < ntile8 ? make_int2(I, tau - I * (I + 1) / 2) : make_int2(-1, 99);
+    const FdTile ft = fd_tile_of(tid / kFdTpw, tid % kFdTpw, d);
+    ttab[tid] = make_int4(ft.I, ft.J, ft.src, ft.kind);
   }
 
   // tiles owned by this thread
@@ -472,6 +645,9 @@ k_filter_direct(DevModel m, DevTarget tg, const double* __restrict__ xl,
   int st = 0;
 
   for (int t = 0; t <= T; ++t) {
+    const bool stamp_on = AUXMC_FD_EXP == 9 && blockIdx.x == 0 && t == 200;
+    (void)stamp_on;
+    FD_STAMP(0);
     const double* cur = inb + (t & 1) * nin;  // z_t | x_{t-1} | b_{t-1}
     // prefetch step t+1's inputs: z_{t+1}, x_t, b_t
     double nxt = 0.0;
@@ -484,35 +660,41 @@ k_filter_direct(DevModel m, DevTarget tg, const double* __restrict__ xl,
     if (t > 0) {
       const double* bp = cur + p + d;
       if (FST) {
-        for (int i = tid; i < d; i += kFdThreads) l96_row(cur + p, d, tg.l96_h, i, fc + 4 * i, fv + 4 * i);
-        __syncthreads();
-        for (int e = tid; e < dd; e += kFdThreads) {
-          const int a = e / d, b = e % d;
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) s += fv[4 * a + k] * P[fc[4 * a + k] * d + b];
-          A[e] = s;
-        }
-        for (int i = tid; i < d; i += kFdThreads) {
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) s += fv[4 * i + k] * mv[fc[4 * i + k]];
-          mp[i] = s + bp[i];
+        // row a of F: columns (a-2, a-1, a, a+1) mod d (target.cuh dyn_jac_ij's entries)
+        const double* xl0 = cur + p;
+        for (int a = tid; a < d; a += kFdThreads) {
+          const int ip1 = (a + 1) % d, im1 = (a + d - 1) % d, im2 = (a + d - 2) % d;
+          const double h = tg.l96_h;
+          *reinterpret_cast<double2*>(fv + 4 * a) =
+              make_double2(h * (0.0 - xl0[im1]), h * (0.0 + (xl0[ip1] - xl0[im2])));
+          *reinterpret_cast<double2*>(fv + 4 * a + 2) =
+              make_double2(1.0 + h * (0.0 - 1.0), h * (0.0 + xl0[im1]));
         }
         __syncthreads();
+        // A = F P and m_p = F m + b: rows of P are contiguous in b (no bank conflicts)
         for (int e = tid; e < dd; e += kFdThreads) {
           const int a = e / d, b = e % d;
-          if (b > a) continue;
-          double x1 = 0.0, x2 = 0.0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            x1 += A[a * d + fc[4 * b + k]] * fv[4 * b + k];
-            x2 += A[b * d + fc[4 * a + k]] * fv[4 * a + k];
-          }
-          const double qs = Qs[e];
-          const double v = 0.5 * ((x1 + qs) + (x2 + qs));
-          Pp[a * d + b] = v;
-          Pp[b * d + a] = v;
+          const double2 f01 = *reinterpret_cast<const double2*>(fv + 4 * a);
+          const double2 f23 = *reinterpret_cast<const double2*>(fv + 4 * a + 2);
+          A[e] = ((f01.x * P[((a + d - 2) % d) * d + b] + f01.y * P[((a + d - 1) % d) * d + b]) +
+                  f23.x * P[a * d + b]) + f23.y * P[((a + 1) % d) * d + b];
+        }
+        for (int a = tid; a < d; a += kFdThreads) {
+          const double2 f01 = *reinterpret_cast<const double2*>(fv + 4 * a);
+          const double2 f23 = *reinterpret_cast<const double2*>(fv + 4 * a + 2);
+          mp[a] = (((f01.x * mv[(a + d - 2) % d] + f01.y * mv[(a + d - 1) % d]) +
+                    f23.x * mv[a]) + f23.y * mv[(a + 1) % d]) + bp[a];
+        }
+        __syncthreads();
+        // P_p = A F^T + symm(Q), every entry by the same formula (symmetric up to
+        // rounding; the reference's extra symmetrization is within the FP64 tolerance)
+        for (int e = tid; e < dd; e += kFdThreads) {
+          const int a = e / d, b = e % d;
+          const double2 f01 = *reinterpret_cast<const double2*>(fv + 4 * b);
+          const double2 f23 = *reinterpret_cast<const double2*>(fv + 4 * b + 2);
+          const double* Ar = A + a * d;
+          Pp[e] = (((Ar[(b + d - 2) % d] * f01.x + Ar[(b + d - 1) % d] * f01.y) + Ar[b] * f23.x) +
+                   Ar[(b + 1) % d] * f23.y) + Qs[e];
         }
       } else {
         for (int e = tid; e < dd; e += kFdThreads) {
@@ -563,15 +745,17 @@ k_filter_direct(DevModel m, DevTarget tg, const double* __restrict__ xl,
       }
     }
     __syncthreads();
+    FD_STAMP(1);
     if (covs) {
       double* pmo = pred_mean + ((size_t)c * (T + 1) + t) * d;
       double* pco = pred_cov + ((size_t)c * (T + 1) + t) * dd;
       for (int i = tid; i < d; i += kFdThreads) pmo[i] = mp[i];
       for (int e = tid; e < dd; e += kFdThreads) pco[e] = Pp[e];
     }
+    FD_STAMP(2);
     bool ok;
     if constexpr (MMA)
-      ok = elim_mma(tid, d, n, Pp, r, w, mp, Rp, Dv, piv, P, mv, red, ttab);
+      ok = elim_mma(tid, d, n, Pp, r, w, mp, Rp, piv, P, mv, red, ttab, Dv, stamp_on);
     else if constexpr (TPT == 0)
       ok = false;
     else
@@ -580,13 +764,14 @@ k_filter_direct(DevModel m, DevTarget tg, const double* __restrict__ xl,
       st = 2;
       break;
     }
+    FD_STAMP(40);
     __syncthreads();
+    FD_STAMP(41);
     if (tid < 32) {  // log N(w; m_p, S) + fused-pair terms, fixed order
       double lg = 0.0, e2 = 0.0;
-      for (int i = tid; i < (MMA ? (d + 3) / 4 : d); i += 32) {
+      for (int i = tid; i < (MMA ? (d + 3) / 4 : d); i += 32)
         lg += log(piv[i]);  // LDL pivots (rank-1) or det of each 4×4 pivot block (MMA)
-        e2 += ex[i];
-      }
+      for (int i = tid; i < d; i += 32) e2 += ex[i];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         lg += __shfl_xor_sync(0xffffffffu, lg, o);
@@ -607,6 +792,7 @@ k_filter_direct(DevModel m, DevTarget tg, const double* __restrict__ xl,
     }
     if (t < T && tid < nin) inb[((t + 1) & 1) * nin + tid] = nxt;
     __syncthreads();
+    FD_STAMP(42);
   }
   if (tid == 0) {
     log_marginal[c] = st ? NAN : ll;
@@ -656,3 +842,11 @@ int launch_filter_direct(const DevTarget& tg, const DevModel& dm, bool stencil,
 }
 
 }  // namespace auxmc_gpu
+
+#if AUXMC_FD_EXP == 9
+extern "C" int auxmc_debug_fd_stamps(long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, auxmc_gpu::g_fd_stamps, sizeof(long long) * n) == cudaSuccess
+             ? 0
+             : 1;
+}
+#endif

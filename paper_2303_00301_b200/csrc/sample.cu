@@ -186,11 +186,14 @@ __global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
 // FMAs per entry.  About 1/4 of the FLOPs and 3/5 of the shared memory of
 // backward_step_group, so five items run per SM.
 constexpr int kBwdLeanThreads = 128;
+#ifndef BWD_LEAN_MINB
+#define BWD_LEAN_MINB 4  // CTAs per SM the register budget is cut for (smem allows 5 at d = 40)
+#endif
 __host__ __device__ inline int bwd_lean_doubles(int d) {
   return 3 * d * d + dinv_doubles(d) + 8 * d + 4;
 }
 
-__global__ void __launch_bounds__(kBwdLeanThreads, 4)
+__global__ void __launch_bounds__(kBwdLeanThreads, BWD_LEAN_MINB)
 k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __restrict__ filt_cov,
            const double* __restrict__ pred_cov, int Bfr, double* elems, double* term,
            int* status, int store_cov, int t_lo, int t_hi) {

@@ -26,22 +26,30 @@ def _pair(mods, tg, x0, delta, C, iters, backend=0):
     _lib, auxk, _ = mods
     lib = _lib.load()
     out = []
-    for force in (1, 0):
-        lib.auxmc_test_force_generic_filter(force)
-        ch = auxk.init_chains(tg, x0, delta, 5, C)
-        hist = []
-        for _ in range(iters):
-            ch.kernel_step(backend)
-            hist.append((ch.accepted.cpu().numpy().copy(), ch.last_log_alpha.cpu().numpy().copy(),
-                         ch.x.cpu().numpy().copy(), int(ch.aborted.sum())))
-        out.append(hist)
-    lib.auxmc_test_force_generic_filter(0)
+    lm = torch.zeros(C, dtype=torch.float64, device="cuda")
+    lib.auxmc_test_capture_log_marginal(lm.data_ptr())
+    try:
+        for force in (1, 0):
+            lib.auxmc_test_force_generic_filter(force)
+            ch = auxk.init_chains(tg, x0, delta, 5, C)
+            hist = []
+            for _ in range(iters):
+                ch.kernel_step(backend)
+                hist.append((ch.accepted.cpu().numpy().copy(),
+                             ch.last_log_alpha.cpu().numpy().copy(), ch.x.cpu().numpy().copy(),
+                             int(ch.aborted.sum()), lm.cpu().numpy().copy()))
+            out.append(hist)
+    finally:
+        lib.auxmc_test_force_generic_filter(0)
+        lib.auxmc_test_capture_log_marginal(None)
     return out
 
 
 def _compare(gen, fused, what):
-    for it, ((a0, l0, x0, ab0), (a1, l1, x1, ab1)) in enumerate(zip(gen, fused)):
+    for it, ((a0, l0, x0, ab0, m0), (a1, l1, x1, ab1, m1)) in enumerate(zip(gen, fused)):
         assert ab0 == ab1 == 0, f"{what} aborted at {it}"
+        # the filters' own output: log p(z) of the forward auxiliary model
+        assert_close(m1, m0, 1e-10, f"{what} log p(z) at {it}")
         assert np.array_equal(a0, a1), f"{what}: decisions differ at {it}"
         fin = np.isfinite(l0)
         assert np.allclose(l1[fin], l0[fin], rtol=0, atol=1e-7 * max(1.0, np.abs(l0[fin]).max()))
