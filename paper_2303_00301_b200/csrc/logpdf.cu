@@ -62,11 +62,26 @@ __global__ void k_factor_list(DevModel m, int nQb, int nRb, double* Ls, double* 
   }
 }
 
+// per row of every H_t: the single nonzero column, -1 for a zero row, -2 otherwise
+__global__ void k_row_sparsity(DevModel m, int* hsel) {
+  const long long n = (long long)m.nH * m.dy;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(q / m.dy), i = (int)(q % m.dy);
+    const double* H = m.H + (size_t)t * m.dy * m.dx + (size_t)i * m.dx;
+    int col = -1;
+    for (int j = 0; j < m.dx; ++j)
+      if (H[j] != 0.0) col = col == -1 ? j : -2;
+    hsel[q] = col;
+  }
+}
+
 // term index k: 0 prior; 1..T transition t=k-1; T+1..2T+1 observation t=k-T-1.
 __global__ void k_path_terms(DevModel m, const double* __restrict__ obs, long long obs_stride,
                              const double* __restrict__ traj, int B, const double* __restrict__ Ls,
                              const double* __restrict__ logdet,
-                             const unsigned char* __restrict__ dg, double* terms) {
+                             const unsigned char* __restrict__ dg,
+                             const int* __restrict__ hsel, double* terms) {
   const int T = m.T;
   const int K = 2 * T + 2;
   const long long n = (long long)B * K;
@@ -74,7 +89,7 @@ __global__ void k_path_terms(DevModel m, const double* __restrict__ obs, long lo
        q += (long long)gridDim.x * blockDim.x) {
     const int b = (int)(q / K), k = (int)(q % K);
     terms[q] = path_term_k(m, obs + (size_t)b * obs_stride, traj + (size_t)b * (T + 1) * m.dx, b, B,
-                           Ls, logdet, k, dg);
+                           Ls, logdet, k, dg, hsel);
   }
 }
 
@@ -110,7 +125,10 @@ int launch_path_logpdf(const DevModel& dm, const double* obs, long long obs_stri
   double *Ls = nullptr, *logdet = nullptr, *terms = nullptr;
   int* fst = nullptr;
   unsigned char* dg = nullptr;
+  int* hsel = nullptr;
+  const bool rows = dm.dy > 0 && dm.sH == 0;  // H shared by the batch
   AUXMC_CUDA_TRY(cudaMallocAsync(&dg, n_mats, s));
+  if (rows) AUXMC_CUDA_TRY(cudaMallocAsync(&hsel, sizeof(int) * (size_t)dm.nH * dm.dy, s));
   AUXMC_CUDA_TRY(cudaMallocAsync(&Ls, sizeof(double) * n_mats * W * W, s));
   AUXMC_CUDA_TRY(cudaMallocAsync(&logdet, sizeof(double) * n_mats, s));
   AUXMC_CUDA_TRY(cudaMallocAsync(&terms, sizeof(double) * (size_t)B * K, s));
@@ -122,9 +140,13 @@ int launch_path_logpdf(const DevModel& dm, const double* obs, long long obs_stri
                                       (int)smem));
   AUXMC_LAUNCH(k_factor_list, std::min((n_mats + warps - 1) / warps, 148 * 8), 32 * warps, smem,
                s, dm, nQb, nRb, Ls, logdet, dg, fst);
+  if (rows)
+    AUXMC_LAUNCH(k_row_sparsity, (int)std::min<long long>(((long long)dm.nH * dm.dy + 127) / 128,
+                                                         148LL * 16),
+                 128, 0, s, dm, hsel);
   const long long n = (long long)B * K;
   AUXMC_LAUNCH(k_path_terms, (int)std::min<long long>((n + 127) / 128, 148LL * 64), 128, 0, s, dm,
-               obs, obs_stride, traj, B, Ls, logdet, dg, terms);
+               obs, obs_stride, traj, B, Ls, logdet, dg, hsel, terms);
   AUXMC_LAUNCH(k_path_sum, B, kSumThreads, 0, s, dm.T, B, terms, dm.mask, dm.dy,
                log_marginal, lm_shared, fst, out, status);
   cudaFreeAsync(Ls, s);
@@ -132,6 +154,7 @@ int launch_path_logpdf(const DevModel& dm, const double* obs, long long obs_stri
   cudaFreeAsync(terms, s);
   cudaFreeAsync(fst, s);
   cudaFreeAsync(dg, s);
+  if (hsel) cudaFreeAsync(hsel, s);
   return AUXMC_OK;
 }
 

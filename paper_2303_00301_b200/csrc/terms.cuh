@@ -19,7 +19,8 @@ __device__ __forceinline__ double path_term_k(const DevModel& m, const double* _
                                               const double* __restrict__ x, int b, int B,
                                               const double* __restrict__ Ls,
                                               const double* __restrict__ logdet, int k,
-                                              const unsigned char* __restrict__ dg = nullptr) {
+                                              const unsigned char* __restrict__ dg = nullptr,
+                                              const int* __restrict__ hsel = nullptr) {
   const int T = m.T, dx = m.dx, dy = m.dy;
   const int W = dx > dy ? dx : dy;
   int nn, j, t = 0, kind;
@@ -61,7 +62,12 @@ __device__ __forceinline__ double path_term_k(const DevModel& m, const double* _
       }
       return x[(size_t)(t + 1) * dx + i] - (s + bb[i]);
     }
-    for (int jj = 0; jj < dx; ++jj) s += H[i * dx + jj] * x[(size_t)t * dx + jj];
+    // hsel: per H row, the one nonzero column (-1: none; -2: dense) — the dense sum's
+    // value exactly (its other products are zeros)
+    const int hs = hsel ? hsel[(size_t)(m.nH > 1 ? t : 0) * dy + i] : -2;
+    if (hs >= 0) s = H[i * dx + hs] * x[(size_t)t * dx + hs];
+    else if (hs == -2)
+      for (int jj = 0; jj < dx; ++jj) s += H[i * dx + jj] * x[(size_t)t * dx + jj];
     return y[i] - (s + cc[i]);
   };
   double sq = 0.0;
