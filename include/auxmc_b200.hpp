@@ -406,6 +406,13 @@ class AuxChains {
   /* Gather x[c][t][j] for the given flat coordinates (t*dx + j) of every chain
    * into out[c * coords.size() + k] (one device gather + one copy). */
   void gather(const std::vector<long>& coords, std::vector<double>& out) const;
+  /* bench/runner.cpp:61-85 gamma_move for every chain (device; Lorenz targets): stream
+   * root_c.derive(kParam, iter); gamma[c] updated in place when chain c's move is
+   * accepted; returns the accept flags. */
+  std::vector<int> gamma_move(long iter, double step, std::vector<double>& gamma);
+  /* Swap the target (runner.cpp:162-167: a new γ) and recompute log γ(x) and the
+   * gradients for the current paths; x, δ, iteration counts and stats are kept. */
+  void retarget(const GenSSMTarget& target);
 
  private:
   struct Impl;
@@ -463,6 +470,9 @@ class PGChains {
   std::vector<long> updates() const;
   std::vector<double> deltas() const;
   void gather(const std::vector<long>& coords, std::vector<double>& out) const;
+  /* runner.cpp:190-196: gamma_move on every chain's path, and the target swap */
+  std::vector<int> gamma_move(long iter, double step, std::vector<double>& gamma);
+  void retarget(const auxk::GenSSMTarget& target);
 
  private:
   struct Impl;
@@ -491,6 +501,8 @@ struct RunConfig {
   bool parallel_filter = false;    // aux family: scan filter (KernelOptions)
   int chains = 1;                  // new: chains run as one batch; chain c rooted at
                                    // from_seed(seed).derive(kChain, c)
+  bool sample_param = false;       // config.hpp:30 diffusion-coefficient move (Lorenz)
+  double param_step = 0.2;         // config.hpp:31 random-walk scale on log gamma
   ModelSpec model;
 };
 
@@ -508,6 +520,9 @@ struct ChainSummary {
   double burn_seconds = 0.0;
   double sample_seconds = 0.0;
   int chains = 1;
+  bool has_param = false;     // sample_param: moments of γ over the kept iterations
+  double param_mean = 0.0;
+  double param_sd = 0.0;
 };
 
 struct RunResult {

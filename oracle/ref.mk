@@ -38,9 +38,14 @@ $(OUT)/libauxmc_ref.so: $(LIB_OBJS)
 	$(CXX) -shared -o $@ $(LIB_OBJS) -lpthread
 
 # C bridge (oracle/ref_bridge.cpp, our code): flat extern "C" entry points over the
-# reference's C++ API for the Python parity tests and the CPU baseline.
-$(OUT)/libref_bridge.so: $(HERE)ref_bridge.cpp $(OUT)/libauxmc_ref.so $(SHIM_DEPS)
-	$(CXX) $(CXXFLAGS) $(INC) -I$(REF)/tests -shared -o $@ $< -L$(OUT) -lauxmc_ref -Wl,-rpath,'$$ORIGIN' -lpthread
+# reference's C++ API for the Python parity tests and the CPU baseline.  Self-contained:
+# the reference objects and a private static libstdc++ (symbols hidden), so the C++
+# runtime exported by other extension modules of the host Python process (numpy's core
+# module re-exports libstdc++ type_info and locale symbols) cannot interpose on its
+# iostreams and exceptions.
+$(OUT)/libref_bridge.so: $(HERE)ref_bridge.cpp $(LIB_OBJS) $(SHIM_DEPS)
+	$(CXX) $(CXXFLAGS) $(INC) -I$(REF)/tests -shared -static-libstdc++ -static-libgcc \
+	  -Wl,--exclude-libs,ALL -o $@ $< $(LIB_OBJS) -lpthread
 
 $(OUT)/auxmc_tests: $(TEST_OBJS) $(OUT)/libauxmc_ref.so
 	$(CXX) -o $@ $(TEST_OBJS) -L$(OUT) -lauxmc_ref -Wl,-rpath,'$$ORIGIN' -lpthread

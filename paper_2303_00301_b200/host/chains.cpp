@@ -214,6 +214,34 @@ std::vector<double> AuxChains::deltas() const {
   return d;
 }
 
+static std::vector<int> device_gamma_move(const GenSSMTarget& tg, int C, const double* x,
+                                          const std::uint64_t* keys, long iter, double step,
+                                          std::vector<double>& gamma) {
+  require_dim(static_cast<int>(gamma.size()) == C, "gamma_move: one γ per chain");
+  DeviceBuffer g(sizeof(double) * C), mv(sizeof(int) * C);
+  g.upload(gamma.data(), sizeof(double) * C);
+  const auxmc_target& t = tg.device();
+  check_status(auxmc_gamma_move(&t, C, x, keys, iter, step, g.as<double>(), mv.as<int>(), nullptr),
+               "gamma_move");
+  std::vector<int> moved(C);
+  g.download(gamma.data(), sizeof(double) * C);
+  mv.download(moved.data(), sizeof(int) * C);
+  return moved;
+}
+
+std::vector<int> AuxChains::gamma_move(long iter, double step, std::vector<double>& gamma) {
+  Impl& m = *impl_;
+  return device_gamma_move(m.target, m.C, m.x.as<double>(), m.keys.as<std::uint64_t>(), iter,
+                           step, gamma);
+}
+
+void AuxChains::retarget(const GenSSMTarget& target) {
+  Impl& m = *impl_;
+  require_dim(target.horizon() + 1 == m.T1 && target.dx() == m.dx, "retarget: same shape");
+  m.target = target;
+  m.init();  // auxk.cpp:120-128: log γ and gradients at the kept paths
+}
+
 void AuxChains::gather(const std::vector<long>& coords, std::vector<double>& out) const {
   detail::gather_coords(impl_->x.as<double>(), impl_->C,
                         static_cast<size_t>(impl_->T1) * impl_->dx, coords, out);
@@ -417,6 +445,18 @@ void PGChains::gather(const std::vector<long>& coords, std::vector<double>& out)
                         static_cast<size_t>(impl_->T1) * impl_->dx, coords, out);
 }
 
+std::vector<int> PGChains::gamma_move(long iter, double step, std::vector<double>& gamma) {
+  Impl& m = *impl_;
+  return auxk::device_gamma_move(m.target, m.C, m.x.as<double>(), m.roots.as<std::uint64_t>(),
+                                 iter, step, gamma);
+}
+
+void PGChains::retarget(const auxk::GenSSMTarget& target) {
+  Impl& m = *impl_;
+  require_dim(target.horizon() + 1 == m.T1 && target.dx() == m.dx, "retarget: same shape");
+  m.target = target;  // runner.cpp:195: the sweep state carries nothing target-derived
+}
+
 // fkpg.cpp:252-258
 PGState init_pg(Trajectory x0, double delta) {
   PGState s;
@@ -512,9 +552,19 @@ RunResult run(const RunConfig& cfg_in) {
     throw ConfigError("target_acceptance must be in [0, 1)");
   if (cfg.target_acceptance == 0.0)
     cfg.target_acceptance = is_aux_family(cfg.sampler) ? 0.574 : 0.9;
+  if (cfg.sample_param) {  // config.cpp:128-130 (+ Lorenz-96, whose γ move is the same law)
+    if (cfg.model.kind != "diffusion-smoothing" && cfg.model.kind != "lorenz96")
+      throw ConfigError("sample_param requires the diffusion-smoothing model");
+    if (!(cfg.param_step > 0)) throw ConfigError("param_step must be > 0");
+    // runner.cpp runs one chain: γ is part of the target, which the batch shares
+    if (cfg.chains != 1) throw ConfigError("sample_param runs a single chain");
+  }
 
-  const SimResult sim = simulate(cfg.model);
-  const auxk::GenSSMTarget target = make_target(cfg.model, sim.data);
+  ModelSpec spec = cfg.model;
+  const SimResult sim = simulate(spec);
+  auxk::GenSSMTarget target = make_target(spec, sim.data);
+  double& gam = spec.kind == "lorenz96" ? spec.l96_gamma : spec.lz_gamma;
+  std::vector<double> param_draws;
   const int T = target.horizon(), dx = target.dx(), C = cfg.chains;
   const long keep = cfg.chain_length - cfg.burn_in;
   const std::vector<int> times = choose_probes(cfg, T, dx);
@@ -545,6 +595,17 @@ RunResult run(const RunConfig& cfg_in) {
     for (size_t j = 0; j < K; ++j) trace << "," << num(g[j]);  // chain 0
     trace << "\n";
     draws.insert(draws.end(), g.begin(), g.end());
+    if (cfg.sample_param) param_draws.push_back(gam);  // runner.cpp:148
+  };
+  // runner.cpp:159-167 / :192-196: the γ move after each sweep; a new γ rebuilds the target
+  auto param_move = [&](auto& ch, long iter) {
+    if (!cfg.sample_param) return;
+    std::vector<double> gv(1, gam);
+    if (ch.gamma_move(iter, cfg.param_step, gv)[0]) {
+      gam = gv[0];
+      target = make_target(spec, sim.data);
+      ch.retarget(target);
+    }
   };
 
   const clk::time_point t0 = clk::now();
@@ -561,6 +622,7 @@ RunResult run(const RunConfig& cfg_in) {
     std::vector<long> mark(C, 0);
     for (long iter = 0; iter < cfg.chain_length; ++iter) {
       ch.kernel_step(opts);
+      param_move(ch, iter);
       if (iter < cfg.burn_in) {
         ch.adapt_delta(cfg.target_acceptance);
         if (iter + 1 == cfg.burn_in) {
@@ -585,6 +647,7 @@ RunResult run(const RunConfig& cfg_in) {
     std::vector<long> mark(C, 0);
     for (long iter = 0; iter < cfg.chain_length; ++iter) {
       ch.aux_pgibbs_step(opts);
+      param_move(ch, iter);
       if (iter < cfg.burn_in) {
         ch.adapt_delta(cfg.target_acceptance);
         if (iter + 1 == cfg.burn_in) {
@@ -625,6 +688,16 @@ RunResult run(const RunConfig& cfg_in) {
         s.sd[j] = std::sqrt(ss / static_cast<double>(n - 1));
       }
     s.rate = rate_num / static_cast<double>(n);
+    if (cfg.sample_param && !param_draws.empty()) {  // runner.cpp:228-236
+      const double pn = static_cast<double>(param_draws.size());
+      double pm = 0.0, pss = 0.0;
+      for (double v : param_draws) pm += v;
+      pm /= pn;
+      for (double v : param_draws) pss += (v - pm) * (v - pm);
+      s.has_param = true;
+      s.param_mean = pm;
+      s.param_sd = param_draws.size() > 1 ? std::sqrt(pss / (pn - 1.0)) : 0.0;
+    }
   }
 
   std::ofstream sf(res.summary_path);  // config.cpp:178-207 (ESS / MCSE not computed)
@@ -643,6 +716,9 @@ RunResult run(const RunConfig& cfg_in) {
      << "  \"sd\": " << (n ? arr(s.sd) : "null") << ",\n"
      << "  \"rate\": " << (n ? num(s.rate) : "null") << ",\n"
      << "  \"final_delta\": " << num(s.final_delta) << ",\n"
+     << (s.has_param ? "  \"param_mean\": " + num(s.param_mean) + ",\n  \"param_sd\": " +
+                           num(s.param_sd) + ",\n"
+                     : std::string())
      << "  \"burn_seconds\": " << num(s.burn_seconds) << ",\n"
      << "  \"sample_seconds\": " << num(s.sample_seconds) << "\n}\n";
   return res;

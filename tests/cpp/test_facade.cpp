@@ -515,7 +515,37 @@ static void host_tests(bool device) {
   }
 }
 
+// --run sampler kind T chain_length burn_in seed sample_param param_step delta out_dir:
+// one bench::run (the facade's run driver) for the reference-parity test
+// (tests/test_facade_run.py compares its files with the reference's bench::run).
+static int run_mode(int argc, char** argv) {
+  if (argc < 12) {
+    std::printf("usage: --run sampler kind T length burn seed sample_param step delta out\n");
+    return 2;
+  }
+  bench::RunConfig cfg;
+  cfg.sampler = argv[2];
+  cfg.model.kind = argv[3];
+  cfg.model.T = std::atoi(argv[4]);
+  cfg.chain_length = std::atol(argv[5]);
+  cfg.burn_in = std::atol(argv[6]);
+  cfg.seed = std::strtoull(argv[7], nullptr, 10);
+  cfg.sample_param = std::atoi(argv[8]) != 0;
+  cfg.param_step = std::atof(argv[9]);
+  cfg.delta_init = std::atof(argv[10]);
+  cfg.output_dir = argv[11];
+  try {
+    const bench::RunResult r = bench::run(cfg);
+    std::printf("rate %.17g param_mean %.17g\n", r.summary.rate, r.summary.param_mean);
+  } catch (const std::exception& e) {
+    std::printf("error: %s\n", e.what());
+    return 1;
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::strcmp(argv[1], "--run") == 0) return run_mode(argc, argv);
   const bool no_device = argc > 1 && std::strcmp(argv[1], "--no-device") == 0;
   const bool device = auxmc_device_ok() == 1;
   if (!no_device && !device) {
