@@ -838,41 +838,58 @@ __global__ void __launch_bounds__(1024, 1)
 // the GPU (CTA per (chain, t), thread per j; three passes over i: max, sequential sum,
 // sequential cumulative search).  The sequential chain is then an index chase through
 // the [T][N] table (k_pit_backward_chase).  -1 marks a degenerate row.
-__global__ void k_pit_backward_table(DevTarget tg, FactorRef f, PgArgs a, int* seltab) {
+// The backward index draws of every step at once (fkpg.cpp:112-152's backward pass,
+// tabulated): for step t and each particle j at t+1, the ancestor index the uniform
+// u_t selects from the normalized backward weights alpha_t(i) p(x_{t+1}^j | x_t^i).
+// The transition density comes from the forward pass's whitened operands (V: means,
+// X: particles, k_pit_whiten), so each weight is alpha_t(i) - |X_j - V_i|^2 / 2 (the
+// Gaussian's constant cancels in the normalization); one online max/sum pass, then
+// the cumulative pass to the first u <= acc.
+template <int DT>
+__global__ void k_pit_backward_table(DevTarget tg, PgArgs a, const double* __restrict__ V,
+                                     const double* __restrict__ X, int* seltab) {
   extern __shared__ double sm[];
-  const int N = a.N, T = tg.T, d = tg.dx;
+  const int N = a.N, T = tg.T;
   const int c = (int)(blockIdx.x / T), t = (int)(blockIdx.x % T);
   if (a.status[c] != AUXMC_OK) return;
-  double* mean = sm;           // N*d dynamics means of x_t^i
-  double* At = mean + (size_t)N * d;  // N
-  const double* P = a.part + (size_t)c * (T + 1) * N * d;
+  double* vs = sm;                          // N*DT whitened means of x_t^i
+  double* At = vs + (size_t)N * DT;         // N
   const double* A = a.Wt + (size_t)c * (T + 1) * N;
-  for (int q = threadIdx.x; q < N * d; q += blockDim.x)
-    mean[q] = dyn_mean_i(tg, t, P + ((size_t)t * N + q / d) * d, q % d);
+  const double* Vt = V + ((size_t)c * T + t) * N * DT;   // step t+1's operands
+  const double* Xt = X + ((size_t)c * T + t) * N * DT;
+  for (int q = threadIdx.x; q < N * DT; q += blockDim.x) vs[q] = Vt[q];
   for (int i = threadIdx.x; i < N; i += blockDim.x) At[i] = A[(size_t)t * N + i];
   __syncthreads();
-  const int jq = 1 + (f.fl.nQ > 1 ? t : 0);
-  const double* L = f.L(jq);
-  const double ld = f.logdet[jq];
   const double u = uniform_at(derive(a.it[c], kBackwardIndex, (uint64_t)t), 0);
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
-    const double* ch = P + ((size_t)(t + 1) * N + j) * d;
-    double chosen[8], r[8];
-    for (int k = 0; k < d; ++k) chosen[k] = ch[k];
+    double w[DT];
+#pragma unroll
+    for (int k = 0; k < DT; ++k) w[k] = Xt[(size_t)j * DT + k];
     auto logb = [&](int i) {
-      for (int k = 0; k < d; ++k) r[k] = chosen[k] - mean[i * d + k];
-      return At[i] + gauss_term(d, r, L, ld);
+      double sq = 0.0;
+#pragma unroll
+      for (int k = 0; k < DT; ++k) {
+        const double z = w[k] - vs[i * DT + k];
+        sq += z * z;
+      }
+      return At[i] - 0.5 * sq;
     };
-    double m = -INFINITY;
-    for (int i = 0; i < N; ++i) m = fmax(m, logb(i));
+    double m = -INFINITY, sum = 0.0;
+    for (int i = 0; i < N; ++i) {
+      const double v = logb(i);
+      if (v > m) {
+        sum = sum * exp(m - v) + 1.0;
+        m = v;
+      } else {
+        sum += exp(v - m);
+      }
+    }
     int sel = -1;
     if (isfinite(m)) {
-      double s = 0.0;
-      for (int i = 0; i < N; ++i) s += exp(logb(i) - m);
       double acc = 0.0;
       sel = N - 1;
       for (int i = 0; i < N; ++i) {
-        acc += exp(logb(i) - m) / s;
+        acc += exp(logb(i) - m) / sum;
         if (u <= acc) {
           sel = i;
           break;
@@ -1156,6 +1173,13 @@ __global__ void k_pg_adapt(int C, const long long* iter, const double* last_upda
   delta[c] = exp(log(delta[c]) + pow(n, -0.6) * (last_update[c] - target));
 }
 
+#ifndef AUXMC_PIT_CS
+#define AUXMC_PIT_CS 16  // CTAs per chain in the few-chain forward (16: non-portable cluster)
+#endif
+static int pit_cluster(int C) {
+  return (AUXMC_PIT_CS > 8 && C * AUXMC_PIT_CS <= num_sms()) ? AUXMC_PIT_CS : 8;
+}
+
 template <int DT>
 static int launch_pit_forward_dt(int C, int CS, int threads, size_t smem, cudaStream_t s,
                                  const DevTarget& tg, const FactorRef& f, const PgArgs& a,
@@ -1166,6 +1190,8 @@ static int launch_pit_forward_dt(int C, int CS, int threads, size_t smem, cudaSt
                  tg, f, a, V, X);
   auto kern = k_pit_forward_cluster<DT>;
   AUXMC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (CS > 8)
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C * CS);
   cfg.blockDim = dim3(threads);
@@ -1264,7 +1290,7 @@ static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int mode, int varia
                  tg, f, a, lw);
     if (d <= 8) {
       // cluster-parallel forward messages: 8 SMs per chain when the batch leaves SMs idle
-      const int CS = pit_few ? 8 : 1;
+      const int CS = pit_few ? pit_cluster(C) : 1;
       const int JLmax = (N + CS - 1) / CS;
       const int fthreads = 1024;
       const size_t fsmem = sizeof(double) * (2 * (size_t)N + 2 * (size_t)N * d + 2 * (size_t)JLmax * d +
@@ -1273,7 +1299,14 @@ static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int mode, int varia
       if (rc2) return rc2;
       if (pit_few && T > 0) {
         const size_t tsmem = sizeof(double) * ((size_t)N * d + N);
-        AUXMC_LAUNCH(k_pit_backward_table, C * T, threads, tsmem, s, tg, f, a, seltab);
+        switch (d) {
+#define TCASE(DT)                                                                            \
+  case DT:                                                                                   \
+    AUXMC_LAUNCH(k_pit_backward_table<DT>, C * T, threads, tsmem, s, tg, a, pV, pX, seltab); \
+    break;
+          TCASE(1) TCASE(2) TCASE(3) TCASE(4) TCASE(5) TCASE(6) TCASE(7) TCASE(8)
+#undef TCASE
+        }
         const size_t csmem = sizeof(double) * (3 * (size_t)N + 40) +
                              sizeof(int) * ((size_t)kChaseBlock * (N + 1) + 1);
         AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pit_backward_chase,

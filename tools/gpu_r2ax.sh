@@ -1,0 +1,4 @@
+python tools/c4_kernels.py 1 3
+python tools/c4_kernels.py 148 2 | head -2
+AUXMC_LIB_PATH=tools/_exp/p9.so python tools/pit_stamps.py
+timeout 900 python -m pytest tests/test_gpu_fkpg.py tests/test_gpu_shapes.py tests/test_gpu_pm.py tests/test_gpu_failures.py -q -m gpu 2>&1 | tail -2
