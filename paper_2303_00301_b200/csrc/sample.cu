@@ -186,6 +186,9 @@ __global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
 // FMAs per entry.  About 1/4 of the FLOPs and 3/5 of the shared memory of
 // backward_step_group, so five items run per SM.
 constexpr int kBwdLeanThreads = 128;
+#ifndef BWD_LEAN_MIN_D
+#define BWD_LEAN_MIN_D 17  // smallest d on the CTA Schur-form kernel (below: warp groups)
+#endif
 #ifndef BWD_LEAN_MINB
 #define BWD_LEAN_MINB 4  // CTAs per SM the register budget is cut for (smem allows 5 at d = 40)
 #endif
@@ -915,7 +918,7 @@ int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, 
       CASE(1) CASE(2) CASE(3) CASE(4)
 #undef CASE
     }
-  } else if (d > 16) {
+  } else if (d >= BWD_LEAN_MIN_D) {
     const size_t smem = sizeof(double) * bwd_lean_doubles(d);
     AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_bwd_lean, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
