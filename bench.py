@@ -115,23 +115,29 @@ class Clocks:
                 idx = int(vis.split(",")[self.index])
             self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(idx)
             self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self._sample()  # one at the region's start: short regions get >= 2 samples
             self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
         except Exception:
             self.h = None
         return self
 
-    def _poll(self):
+    def _sample(self):
         N = self.N
+        try:
+            self.samples.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
+                                 N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+        except Exception:
+            pass
+
+    def _poll(self):
         while not self.stop.is_set():
-            try:
-                self.samples.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
-                                     N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
-            except Exception:
-                pass
+            self._sample()
             time.sleep(0.002)
 
     def __exit__(self, *a):
+        if self.h is not None:
+            self._sample()  # and one at its end, before the device work drains
         self.stop.set()
         if self.h is not None:
             self.thread.join(timeout=1)
