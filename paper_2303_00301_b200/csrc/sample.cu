@@ -186,6 +186,20 @@ __global__ void k_bwd_elements(DevModel m, const double* __restrict__ filt_mean,
 // FMAs per entry.  About 1/4 of the FLOPs and 3/5 of the shared memory of
 // backward_step_group, so five items run per SM.
 constexpr int kBwdLeanThreads = 128;
+#ifndef AUXMC_BWD_EXP
+#define AUXMC_BWD_EXP 0  // 9: clock64 phase stamps of the first item of CTA 0 (tools/bwd_stamps.py)
+#endif
+#if AUXMC_BWD_EXP == 9
+__device__ long long g_bwd_stamps[64];
+#define BWD_STAMP(k)                                                       \
+  do {                                                                     \
+    if (stamp && threadIdx.x == 0) g_bwd_stamps[(k)] = clock64();          \
+  } while (0)
+#else
+#define BWD_STAMP(k) \
+  do {               \
+  } while (0)
+#endif
 #ifndef BWD_LEAN_MIN_D
 #define BWD_LEAN_MIN_D 17  // smallest d on the CTA Schur-form kernel (below: warp groups)
 #endif
@@ -212,6 +226,16 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
   int* fcb = reinterpret_cast<int*>(fvb + 4 * d);  // stencil columns [d][4]
   double* red = fvb + 6 * d;
   int* flag = reinterpret_cast<int*>(red + 2);
+  __shared__ __align__(8) uint64_t bar[1];
+  unsigned phase = 0;
+  // bulk copies need 16-B aligned sources and sizes
+  const bool tma = (dd % 2 == 0) && ((reinterpret_cast<uintptr_t>(filt_cov) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(pred_cov) & 15) == 0);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
   const int span = t_hi - t_lo;
   const long long n_items = (long long)Bfr * span;
   for (long long item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -234,11 +258,32 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
     }
     double* out = elems + ((size_t)b * T + t) * elem_stride(d);
     const double* S = pc + (size_t)(t + 1) * dd;
-    g_copy(g, dd, fc + (size_t)t * dd, P);
-    for (int i = g.ty(); i < d; i += g.ny())
-      for (int j = g.tx(); j < d; j += 16) Lb[i * d + j] = j <= i ? S[i * d + j] : 0.0;
+    const bool stamp = AUXMC_BWD_EXP == 9 && blockIdx.x == 0 && item == 0;
+    (void)stamp;
+    BWD_STAMP(0);
+    // P_t and S = P_{t+1|t} by two TMA bulk copies (one HBM round trip, not a load/store
+    // loop per element); S's upper triangle is zeroed once it lands
+    if (tma) {
+      if (g.lane == 0) {
+        mbar_expect_tx(bar, 2u * (unsigned)dd * 8u);
+        bulk_g2s(P, fc + (size_t)t * dd, (unsigned)dd * 8u, bar);
+        bulk_g2s(Lb, S, (unsigned)dd * 8u, bar);
+      }
+    } else {
+      g_copy(g, dd, fc + (size_t)t * dd, P);
+      g_copy(g, dd, S, Lb);
+    }
     if (m.fst)
       for (int i = g.lane; i < d; i += g.size) stencil_row(m, t, b, i, fcb + 4 * i, fvb + 4 * i);
+    if (tma) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+    } else {
+      g.sync();
+    }
+    for (int i = g.ty(); i < d; i += g.ny())
+      for (int j = g.tx(); j < d; j += 16)
+        if (j > i) Lb[i * d + j] = 0.0;
     g.sync();
     // C = F P
     if (m.fst) {
@@ -253,8 +298,11 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
       g_dmma<false, false>(g, d, d, d, m.Ft(t, b), d, P, d, W, d, false, false);
     }
     g.sync();
+    BWD_STAMP(1);
     if (!g_all_zero(g, dd, W, flag)) {
+      BWD_STAMP(2);
       bool ok = g_llt_blocked(g, d, Lb, flag, dinv);
+      BWD_STAMP(3);
       if (!ok) {  // factor_psd ladder (gauss.cpp:26-35) on S, rebuilt from HBM
         if (g.lane == 0) {
           double tr = 0.0;
@@ -284,9 +332,12 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
         continue;
       }
       g_trsm_lower_blocked(g, d, Lb, dinv, d, W, d);                    // W = L^{-1} C
+      BWD_STAMP(4);
       g_dmma<true, false>(g, d, d, d, W, d, W, d, P, d, true, true);   // Λ (lower) = P - W^T W
       g.sync();
+      BWD_STAMP(5);
       g_trsm_lower_t_blocked(g, d, Lb, dinv, d, W, d);                  // W = S^{-1} C = G^T
+      BWD_STAMP(6);
       for (int i = g.ty(); i < d; i += g.ny())
         for (int j = g.tx(); j < d; j += 16)
           if (j > i) P[i * d + j] = P[j * d + i];
@@ -296,6 +347,7 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
       for (int i = g.lane; i < dd; i += g.size) W[i] = -W[i];
       g.sync();
     }
+    BWD_STAMP(7);
     // offset = m_t - G (F m_t + b_t)
     const double* mt = fm + (size_t)t * d;
     const double* bt = m.bt(t, b);
@@ -320,11 +372,14 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
     if (store_cov) {
       for (int e = g.lane; e < dd; e += g.size) out[dd + d + e] = P[e];
     } else {
+      BWD_STAMP(8);
       st = g_chol_psd(g, d, P, Lb, dinv, flag, red);
+      BWD_STAMP(9);
       for (int e = g.lane; e < dd; e += g.size) out[dd + d + e] = Lb[e];
     }
     if (st && g.lane == 0) atomicMax(status + b, st);
     g.sync();
+    BWD_STAMP(10);
   }
 }
 
@@ -1010,3 +1065,11 @@ extern "C" int auxmc_test_flip_backward_gain(int on) {
              ? AUXMC_OK
              : AUXMC_E_CUDA;
 }
+
+#if AUXMC_BWD_EXP == 9
+extern "C" int auxmc_debug_bwd_stamps(long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, auxmc_gpu::g_bwd_stamps, sizeof(long long) * n) == cudaSuccess
+             ? 0
+             : 1;
+}
+#endif
