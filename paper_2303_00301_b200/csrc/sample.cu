@@ -201,7 +201,7 @@ __device__ long long g_bwd_stamps[64];
   } while (0)
 #endif
 #ifndef BWD_LEAN_MIN_D
-#define BWD_LEAN_MIN_D 17  // smallest d on the CTA Schur-form kernel (below: warp groups)
+#define BWD_LEAN_MIN_D 16  // smallest d on the CTA Schur-form kernel (below: warp groups)
 #endif
 #ifndef BWD_LEAN_MINB
 #define BWD_LEAN_MINB 4  // CTAs per SM the register budget is cut for (smem allows 5 at d = 40)
