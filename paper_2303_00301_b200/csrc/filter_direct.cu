@@ -48,12 +48,6 @@ __host__ __device__ inline int fd_nt(int d) { return (2 * d + 1 + 3) / 4; }
 __host__ __device__ inline int fd_tiles(int d) { return fd_nt(d) * (fd_nt(d) + 1) / 2; }
 __host__ __device__ inline int fd_nt8(int d) { return (2 * d + 1 + 7) / 8; }
 
-#ifndef AUXMC_FD_DINV
-#define AUXMC_FD_DINV 0  // 0: warp 0 forms D^{-1} (cofactors), second barrier; 1: every warp (LDL)
-#endif
-#ifndef AUXMC_FD_Y
-#define AUXMC_FD_Y 0  // 1: warp 0 forms Y = R D^{-1}, branch-free 2-load slots (measured slower)
-#endif
 #ifndef AUXMC_FD_EXP
 #define AUXMC_FD_EXP 0  // 9: clock64 phase stamps of CTA 0 (tools/fd_stamps.py)
 #endif
@@ -99,7 +93,7 @@ struct FdLayout {
     red = o; o += 4;
     o = (o + 1) & ~1;  // 16-byte alignment for the double2 panel / D^{-1} loads
     Rb = o; o += 2 * 4 * 8 * fd_nt8(d);  // MMA panels (double-buffered)
-    Dv = o; o += 4 * 8 * fd_nt8(d);  // D^{-1} (16) or Y = R D^{-1} (AUXMC_FD_Y)
+    Dv = o; o += 16;  // D^{-1} of the current pivot block
     tab = o; o += 2 * kFdWarps * kFdTpw;  // int4 per (warp, slot)
     in = o; o += 2 * nin;  // last: the only q-dependent block
     total = o;
@@ -174,12 +168,13 @@ __host__ __device__ inline bool fd_use_mma(int d) {
 // triangle lives in DMMA accumulators, one 8×8 tile per (warp, slot) — lane l holds
 // (8I + l/4, 8J + 2(l%4) + {0,1}), the m8n8k4 C layout.  Pivots go in panels of four:
 // the owners publish the panel R = M[:, kb:kb+4] (rows above kb zero) through shared
-// memory (double-buffered), ONE barrier, then every warp forms D^{-1} of the 4×4 pivot
-// block itself — an LDL^T in registers from broadcast loads, the same operations in
-// every warp, so the same bits — and every tile takes the rank-4 update
-// M -= R D^{-1} R^T as one DMMA (A = -R rows of the tile, B = R D^{-1} rows of its
-// columns).  The LDL pivots of D are the reference's factorization test (S is SPD iff
-// every pivot is > 0); log det S = Σ log det D_p, dets[p] per panel.
+// memory (double-buffered); after a barrier warp 0 forms D^{-1} of the 4×4 pivot block
+// by cofactors (lane 4i + j one 3×3 minor; det by a fixed two-level shuffle sum) and
+// tests the leading minors — S is SPD iff all are > 0, the reference's LLT criterion;
+// after a second barrier every tile takes the rank-4 update M -= R D^{-1} R^T as one
+// DMMA (A = -R rows of the tile, B = R D^{-1} rows of its columns, formed per slot from
+// the tile's R row and the lane's column of D^{-1}).  log det S = Σ log det D_p,
+// dets[p] per panel.  (Variants measured slower: DESIGN.md §5.2.)
 //
 // tab (shared, warp-uniform): per (warp, slot) {I, J, src, kind}: kind 0 a P_p block
 // tile read at P_p[src + row*d + col], 1 the same on the S diagonal (+ r + jitter),
@@ -209,10 +204,7 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
                                          double* dets, double* P, double* mv, double* red,
                                          const int4* __restrict__ tab, double* Dv,
                                          bool stamp_on) {
-  (void)Dv;
   (void)stamp_on;
-  double* Yb = Dv;
-  (void)Yb;
   const int lane = tid & 31, warp = tid >> 5;
   const int gi = lane >> 2, ti = lane & 3;
   const int rstride = 4 * 8 * fd_nt8(d);
@@ -263,7 +255,6 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
               make_double2(live && kb + m0 < d ? c[s][0] : 0.0, live && kb + m0 + 1 < d ? c[s][1] : 0.0);
         }
       }
-#if AUXMC_FD_DINV == 0
       __syncthreads();
       FD_STAMP(8 + 3 * (kb >> 2));
       if (warp == 0) {  // D^{-1} of the 4×4 pivot block by cofactors (lane 4i + j)
@@ -289,24 +280,7 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
         const bool good = d00 > 0.0 && lead2 > 0.0 && lead3 > 0.0 && det > 0.0;
         const double rd = rcp_nr(det);
         const double dij = cof * rd;  // (D^{-1})_{ij} on lane 4i + j
-#if AUXMC_FD_Y
-        // Y = R D^{-1} (the B operand of every tile update): one row per lane
-        double dq[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) dq[e] = __shfl_sync(0xffffffffu, dij, e);
-        for (int row = 8 * Jp + lane; row < 8 * fd_nt8(d); row += 32) {
-          const double2 r01 = *reinterpret_cast<const double2*>(R + row * 4);
-          const double2 r23 = *reinterpret_cast<const double2*>(R + row * 4 + 2);
-          double yv[4];
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj)
-            yv[jj] = (r01.x * dq[jj] + r01.y * dq[4 + jj]) + (r23.x * dq[8 + jj] + r23.y * dq[12 + jj]);
-          *reinterpret_cast<double2*>(Yb + row * 4) = make_double2(yv[0], yv[1]);
-          *reinterpret_cast<double2*>(Yb + row * 4 + 2) = make_double2(yv[2], yv[3]);
-        }
-#else
         if (lane < 16) Dv[lane] = dij;
-#endif
         if (lane == 0) {
           dets[kb >> 2] = det;
           red[3] = good ? 0.0 : 1.0;
@@ -318,24 +292,7 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
         failed = true;
         break;
       }
-#if AUXMC_FD_Y
-      // branch-free over the slots: a retired (all columns < kb) or unowned slot
-      // multiplies a zero A operand (its B rows are finite stale values) — so every
-      // slot's two loads issue ahead of the DMMAs
-#pragma unroll
-      for (int s = 0; s < kFdTpw; ++s) {
-        const int4 tt = wt[s];
-        const bool act = tt.y >= Jp && tt.w != 3;
-        const double a = act ? -R[(8 * tt.x + gi) * 4 + ti] : 0.0;
-        const double y = Yb[(8 * tt.y + gi) * 4 + ti];
-        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-            : "+d"(c[s][0]), "+d"(c[s][1])
-            : "d"(a), "d"(y));
-      }
-      if (false)
-#endif
-      {
-      double q[4];
+      double q[4];  // column ti of D^{-1}: this lane's B-operand weights
       {
         const double2 q01 = *reinterpret_cast<const double2*>(Dv + 4 * ti);
         const double2 q23 = *reinterpret_cast<const double2*>(Dv + 4 * ti + 2);
@@ -344,75 +301,6 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
         q[2] = q23.x;
         q[3] = q23.y;
       }
-#else
-      __syncthreads();
-      FD_STAMP(8 + 3 * (kb >> 2));
-      // D = R[kb:kb+4, 0:4] (lower; padded pivots: identity), LDL^T and D^{-1}
-      double D[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const double2 x01 = *reinterpret_cast<const double2*>(R + (kb + a) * 4);
-        const double2 x23 = *reinterpret_cast<const double2*>(R + (kb + a) * 4 + 2);
-        D[a][0] = x01.x;
-        D[a][1] = x01.y;
-        D[a][2] = x23.x;
-        D[a][3] = x23.y;
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b <= a; ++b)
-          if (kb + a >= d) D[a][b] = a == b ? 1.0 : 0.0;
-      // LDL^T: unit lower Lf, pivots p[]
-      double Lf[4][4], p[4], ip[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        double x = D[a][a];
-#pragma unroll
-        for (int b = 0; b < a; ++b) x -= Lf[a][b] * Lf[a][b] * p[b];
-        p[a] = x;
-        ip[a] = rcp_nr(x);
-#pragma unroll
-        for (int e = a + 1; e < 4; ++e) {
-          double y = D[e][a];
-#pragma unroll
-          for (int b = 0; b < a; ++b) y -= Lf[e][b] * Lf[a][b] * p[b];
-          Lf[e][a] = y * ip[a];
-        }
-      }
-      if (!(p[0] > 0.0 && p[1] > 0.0 && p[2] > 0.0 && p[3] > 0.0)) {  // uniform
-        failed = true;
-        break;
-      }
-      if (tid == 0) dets[kb >> 2] = ((p[0] * p[1]) * (p[2] * p[3]));
-      // D^{-1} = Lf^{-T} diag(ip) Lf^{-1}: column ti only (this lane's B operand)
-      double Li[4][4];  // Lf^{-1} (unit lower)
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          if (b > a) { Li[a][b] = 0.0; continue; }
-          if (b == a) { Li[a][b] = 1.0; continue; }
-          double x = 0.0;
-#pragma unroll
-          for (int e = b; e < a; ++e) x -= Lf[a][e] * (e == b ? 1.0 : Li[e][b]);
-          Li[a][b] = x;
-        }
-      double q[4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        double col[4];  // (D^{-1})_{m, c} for c = 0..3
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          double x = 0.0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (e >= m && e >= cc) x += Li[e][m] * ip[e] * Li[e][cc];
-          col[cc] = x;
-        }
-        q[m] = ti == 0 ? col[0] : ti == 1 ? col[1] : ti == 2 ? col[2] : col[3];
-      }
-#endif
 #pragma unroll
       for (int s = 0; s < kFdTpw; ++s) {
         const int4 tt = wt[s];
@@ -424,7 +312,6 @@ __device__ __forceinline__ bool elim_mma(int tid, int d, int n, const double* Pp
         asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
             : "+d"(c[s][0]), "+d"(c[s][1])
             : "d"(a), "d"(y));
-      }
       }
       FD_STAMP(10 + 3 * (kb >> 2));
     }
