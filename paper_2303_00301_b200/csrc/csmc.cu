@@ -1292,7 +1292,11 @@ static int pg_step(const DevTarget& tg, auxmc_pg_chains* ch, int mode, int varia
       // cluster-parallel forward messages: 8 SMs per chain when the batch leaves SMs idle
       const int CS = pit_few ? pit_cluster(C) : 1;
       const int JLmax = (N + CS - 1) / CS;
-      const int fthreads = 1024;
+#ifndef AUXMC_PIT_FT16
+#define AUXMC_PIT_FT16 512
+#endif
+      // threads per CTA: the pair items are JL x 32 parts (512 at CS = 16, N = 256)
+      const int fthreads = CS >= 16 ? AUXMC_PIT_FT16 : 1024;
       const size_t fsmem = sizeof(double) * (2 * (size_t)N + 2 * (size_t)N * d + 2 * (size_t)JLmax * d +
                                              N + kPitParts * JLmax + 2 * CS + 40);
       int rc2 = launch_pit_forward(d, C, CS, fthreads, fsmem, s, tg, f, a, lw, pV, pX);
