@@ -460,7 +460,14 @@ def main():
                     configs["c2_rng"] = run_c2(args, rank, world, local, "rng", args.min_time,
                                                headline=False)
                 for name in ("c1", "c3", "c4", "c4_1chain", "c5"):
-                    configs[name] = bench_aux.record(name, args, rank, world, local)
+                    if world == 1:  # one failing sub-record must not cost the headline line
+                        try:
+                            configs[name] = bench_aux.record(name, args, rank, world, local)
+                        except Exception as e:  # noqa: BLE001 - reported in the line
+                            configs[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+                            torch.cuda.synchronize()
+                    else:  # ranks fail together (torchrun tears the job down): no hang
+                        configs[name] = bench_aux.record(name, args, rank, world, local)
                 line["configs"] = configs
                 # launches of every config's timed region count as ours too
                 line["gpu_launches_all_configs"] = line["gpu_launches"] + sum(
