@@ -465,7 +465,10 @@ def main():
                             configs[name] = bench_aux.record(name, args, rank, world, local)
                         except Exception as e:  # noqa: BLE001 - reported in the line
                             configs[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
-                            torch.cuda.synchronize()
+                            try:
+                                torch.cuda.synchronize()
+                            except Exception:  # noqa: BLE001 - a sticky context error
+                                pass
                     else:  # ranks fail together (torchrun tears the job down): no hang
                         configs[name] = bench_aux.record(name, args, rank, world, local)
                 line["configs"] = configs
