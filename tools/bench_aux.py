@@ -197,21 +197,21 @@ def cpu_record(name, c):
         allw = CR.aux_baseline(s, 20, 1, 1, 1, True, 1.0, workers=P, label="workers=nproc: ")
         one["workers_nproc"] = {k: allw[k] for k in ("value", "cores", "sample")}
         return one
-    if name == "c3":
-        s = O.spec("lorenz96", T=128, dx=40, data_seed=3)
-        return CR.aux_baseline(s, 1, P, P, 0, False, 0.05, label="reduced T: ")
+    if name == "c3":  # the full horizon: one kernel_step per host thread (~10 s)
+        s = O.spec("lorenz96", T=c["T"], dx=40, data_seed=3)
+        return CR.aux_baseline(s, 1, P, P, 0, False, 0.05, label="full T: ")
     if name == "c5":
-        s = O.spec("spatio-temporal", T=2048, grid=4, data_seed=7)
+        s = O.spec("spatio-temporal", T=16384, grid=4, data_seed=7)
         one = CR.aux_baseline(s, 1, 1, 1, 1, True, C5_DELTA, label="reduced T, 1 core: ")
         allw = CR.aux_baseline(s, 1, 1, 1, 1, True, C5_DELTA, workers=P,
                                label="reduced T, workers=nproc: ")
         one["workers_nproc"] = {k: allw[k] for k in ("value", "cores", "sample")}
         return one
     if name == "c4":
-        s = O.spec("stochvol", T=512, dx=3, data_seed=11)
+        s = O.spec("stochvol", T=4096, dx=3, data_seed=11)
         return CR.pg_baseline(s, 256, 1, P, P, label="reduced T, reference sequential cSMC: ")
     if name == "c4_1chain":
-        s = O.spec("stochvol", T=512, dx=3, data_seed=11)
+        s = O.spec("stochvol", T=4096, dx=3, data_seed=11)
         return CR.pg_baseline(s, 256, 1, 1, 1, label="reduced T, 1 chain, 1 core: ")
     return None
 
