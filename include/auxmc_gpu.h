@@ -229,6 +229,17 @@ int auxmc_test_force_generic_filter(int on);
 /* Test hook: device buffer [C] that receives the forward filter's log p(z) of each
  * auxiliary step (NULL: off).  Host-side switch. */
 int auxmc_test_capture_log_marginal(double* dev_out);
+/* Test hook: 0 makes every step of the scan filter's prefix chains a full combine
+ * and every backward element a full build; 1 (default) lets a chain whose element
+ * matrices repeat (time-invariant model) continue with vector-only steps once the
+ * filtered covariance reaches a fixed point, and lets the recovery and the
+ * backward elements (dense shared F) keep the matrices of a step whose covariance
+ * inputs repeat the previous step's bits (same results either way; pfilter_gen.cu,
+ * sample.cu).  Host-side switch. */
+int auxmc_test_pfg_fixed_point(int on);
+/* Test hook: vector-only scan-filter steps taken since the last reset (reset != 0
+ * zeroes the device counter afterwards); -1 without a device. */
+long long auxmc_test_pfg_fixed_point_steps(int reset);
 
 /* Host-buffer convenience entry for the reference-facing facade: copies the
  * model, filter result and noise keys to the device, draws B paths and copies

@@ -142,6 +142,8 @@ SIGNATURES = {
     "auxmc_test_flip_backward_gain": (C.c_int, [C.c_int]),
     "auxmc_test_force_generic_filter": (C.c_int, [C.c_int]),
     "auxmc_test_capture_log_marginal": (C.c_int, [C.c_void_p]),
+    "auxmc_test_pfg_fixed_point": (C.c_int, [C.c_int]),
+    "auxmc_test_pfg_fixed_point_steps": (C.c_longlong, [C.c_int]),
     "auxmc_path_logpdf": (C.c_int, [C.POINTER(Lgssm), VP, C.c_int, VP, C.POINTER(FilterResult),
                                     C.c_int, C.c_int, VP, VP, VP]),
     "auxmc_init_chains": (C.c_int, [C.POINTER(Target), C.POINTER(Chains), VP, C.c_size_t, VP]),

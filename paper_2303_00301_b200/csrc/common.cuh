@@ -195,4 +195,13 @@ __device__ __forceinline__ double cta_sum_fixed(long long n, Get get, double* re
 }
 constexpr int kSumThreads = 256;
 
+// block length of the generic prefix sampler (prefix_gen.cu): a power of two near
+// sqrt(T); the scan filter's super-blocks are multiples of it (pfilter_gen.cu), so
+// a time-sharded rank's range holds whole sampler blocks
+inline int prefix_block_len(int T) {
+  int lb = 16;
+  while ((long long)lb * lb < T && lb < 4096) lb <<= 1;
+  return lb;
+}
+
 }  // namespace auxmc_gpu

@@ -213,6 +213,19 @@ __device__ __forceinline__ bool g_all_zero(const Grp& g, int n, const double* A,
   return r;
 }
 
+// group-wide boolean "A and B hold the same bits" (n doubles); flag in shared memory
+__device__ __forceinline__ bool g_all_same(const Grp& g, int n, const double* A, const double* B,
+                                           int* flag) {
+  if (g.lane == 0) *flag = 1;
+  g.sync();
+  for (int i = g.lane; i < n; i += g.size)
+    if (__double_as_longlong(A[i]) != __double_as_longlong(B[i])) *flag = 0;
+  g.sync();
+  const bool r = *flag != 0;
+  g.sync();
+  return r;
+}
+
 // ---------------------------------------------------------------- blocked (CTA, n >= 16)
 // Blocked factor/solves with 8-wide panels.  The diagonal 8×8 blocks are
 // factored and inverted by one warp; every other step (panel solve, trailing

@@ -265,7 +265,7 @@ __device__ __noinline__ void g_combine(const Grp& g, int d, const double* u, con
 template <int DC>
 __device__ __forceinline__ void g_combine_bc_t(const Grp& g, int d_rt, const double* u,
                                                const double* v, double* o,
-                                               const CombScratch& s) {
+                                               const CombScratch& s, bool keep_minv) {
   const int d = DC ? DC : d_rt;
   const int dd = d * d;
   const double *ub = u + dd, *uC = u + dd + d, *ueta = u + 2 * dd + d, *uJ = u + 2 * dd + 2 * d;
@@ -291,6 +291,8 @@ __device__ __forceinline__ void g_combine_bc_t(const Grp& g, int d_rt, const dou
     s.t[i] = acc + ub[i];
   }
   g.sync();
+  if (keep_minv)  // Minv^T into s.S, free in this form (g_bc_vec_t reads it by columns)
+    for (int e = g.lane; e < dd; e += g.size) s.S[e] = Minv[(e % d) * d + e / d];
   g_mm(g, d, d, d, Minv, uC, s.T1);
   double* mt = M1;
   for (int i = g.lane; i < d; i += g.size) {
@@ -322,9 +324,86 @@ __device__ __forceinline__ void g_combine_bc_t(const Grp& g, int d_rt, const dou
 }
 
 __device__ __noinline__ void g_combine_bc(const Grp& g, int d, const double* u, const double* v,
-                                          double* o, const CombScratch& s) {
-  if (d == 16) g_combine_bc_t<16>(g, d, u, v, o, s);
-  else g_combine_bc_t<0>(g, d, u, v, o, s);
+                                          double* o, const CombScratch& s,
+                                          bool keep_minv = false) {
+  if (d == 16) g_combine_bc_t<16>(g, d, u, v, o, s, keep_minv);
+  else g_combine_bc_t<0>(g, d, u, v, o, s, keep_minv);
+}
+
+// ---------------------------------------------------------------- covariance fixed point
+// A chain of prefix combines u <- (u then v) whose v all carry the same matrices
+// (A, C, J) — the steps t >= 1 of a time-invariant model, or the aggregates of its
+// full blocks — maps u.C through the same function at every step: the Riccati
+// recursion of the filtered covariance.  Once one combine returns u.C unchanged
+// (same bits), every later combine of the chain receives the same C and the same
+// v matrices, so it forms the same inverse and returns the same C, A = 0 and J:
+// only (b, eta) still move.  g_bc_vec_t advances them in place with the inverse
+// the last full combine kept (keep_minv: its transpose in s.S) and v's A (its
+// transpose in s.T1, written when the fixed point is found), by the vector
+// operations of g_combine_bc_t in their order — the bits of the full combine,
+// without its d^3 products.  Every operand is read by columns (u.C by symmetry:
+// a combine output's C is symmetric to the bit), so the lanes' shared-memory
+// reads are conflict-free.  (A rounding 2-cycle never triggers the test and keeps
+// the full combines; the result is identical either way.)
+template <int DC>
+__device__ __forceinline__ void g_bc_vec_t(const Grp& g, int d_rt, double* u, const double* v,
+                                           const CombScratch& s) {
+  const int d = DC ? DC : d_rt;
+  const int dd = d * d;
+  double *ub = u + dd, *ueta = u + 2 * dd + d;
+  const double* uC = u + dd + d;  // symmetric: uC[k][i] = uC[i][k]
+  const double* vAt = s.T1;       // v's A, transposed
+  const double *vb = v + dd, *veta = v + 2 * dd + d;
+  const double* MinvT = s.S;
+  for (int i = g.lane; i < d; i += g.size) {
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) acc += uC[k * d + i] * veta[k];
+    s.t[i] = acc + ub[i];
+  }
+  g.sync();
+  for (int i = g.lane; i < d; i += g.size) {
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) acc += MinvT[k * d + i] * s.t[k];
+    s.w[i] = acc;
+  }
+  g.sync();
+  for (int i = g.lane; i < d; i += g.size) {
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) acc += vAt[k * d + i] * s.w[k];
+    ub[i] = acc + vb[i];
+    ueta[i] = 0.0 + ueta[i];
+  }
+  g.sync();
+}
+
+__device__ __noinline__ void g_bc_vec(const Grp& g, int d, double* u, const double* v,
+                                      const CombScratch& s) {
+  if (d == 16) g_bc_vec_t<16>(g, d, u, v, s);
+  else g_bc_vec_t<0>(g, d, u, v, s);
+}
+
+// vector-only steps taken (auxmc_test_fixed_point_steps)
+__device__ unsigned long long g_fp_steps = 0;
+
+// one step u <- (u then v) of a prefix chain; `same`: v's matrices are the
+// chain's shared ones.  fixed: the chain sits at a covariance fixed point (its A
+// transposed into s.T1, the kept inverse's transpose in s.S: g_bc_vec_t); o is the
+// full combine's output buffer.
+__device__ __forceinline__ void bc_chain_step(const Grp& g, int d, double* u, const double* v,
+                                              bool same, double* o, const CombScratch& s,
+                                              bool& fixed, int& nvec) {
+  const int dd = d * d;
+  if (fixed && same) {
+    g_bc_vec(g, d, u, v, s);
+    ++nvec;
+    return;
+  }
+  g_combine_bc(g, d, u, v, o, s, same);
+  fixed = same && g_all_same(g, dd, o + dd + d, u + dd + d, s.idx);
+  if (fixed)
+    for (int e = g.lane; e < dd; e += g.size) s.T1[e] = v[(e % d) * d + e / d];
+  g_copy(g, fe_size_g(d), o, u);
+  g.sync();
 }
 
 __host__ __device__ inline int comb_doubles(int d) { return 3 * d * d + 2 * d; }
@@ -500,6 +579,33 @@ inline bool pfg_time_invariant(const DevModel& m) {
          m.nb <= 1 && m.nQ <= 1 && m.nH <= 1 && m.nc <= 1 && m.nR <= 1;
 }
 
+// Every step t >= 1 builds its element matrices (A, C, J) from the same F, Q, H, R
+// by the same operations (b, c and the data only reach the vectors): the
+// covariance fixed point of the prefix chains applies (bc_chain_step).
+inline bool pfg_shared_mats(const DevModel& m) {
+  return m.T >= 2 && m.mask == nullptr && m.nF <= 1 && m.nQ <= 1 && m.nH <= 1 && m.nR <= 1;
+}
+// auxmc_test_pfg_fixed_point(0): every prefix step a full combine (the parity
+// tests compare both forms bit for bit)
+int g_pfg_fixed_on = 1;
+struct SameRanges {
+  int el_lo, el_hi;    // element indices t with the shared matrices
+  int agg_lo, agg_hi;  // block aggregates (full blocks past the first)
+  int sup_lo, sup_hi;  // super-block aggregates (made of such blocks only)
+};
+inline SameRanges same_ranges(const DevModel& m, int LB, int LB2) {
+  SameRanges r{0, 0, 0, 0, 0, 0};
+  if (!g_pfg_fixed_on || !pfg_shared_mats(m)) return r;
+  const int nfull = (m.T + 1) / LB;
+  r.el_lo = 1;
+  r.el_hi = m.T + 1;
+  r.agg_lo = 1;
+  r.agg_hi = nfull;
+  r.sup_lo = 1;
+  r.sup_hi = LB2 > 0 ? nfull / LB2 : 0;
+  return r;
+}
+
 constexpr int kFillWarps = 8;
 // warp w of a CTA: 32 consecutive steps of sequence b, lane = step
 __global__ void __launch_bounds__(kFillWarps * 32)
@@ -620,10 +726,11 @@ __global__ void k_pfg_reduce(int T, int d, int B, int LB, const double* __restri
 // combines elements whose matrix parts are those of t = 1, so the running
 // aggregate's matrices after p combines, and the inverse each combine forms, are
 // the same in every block.  k_pfg_reduce_proto runs that matrix sequence once
-// (on el[1] alone) and keeps, per position p, [A_p | C_p | J_p | Minv_{p+1}];
+// (on el[1] alone) and keeps, per position p, [A_p | C_p | J_p | Minv_{p+1} | its
+// transpose] (the transpose lets the fill read every operand column-wise);
 // k_pfg_reduce_fill then carries each block's (b, eta) through the combine's
 // vector formulas, in g_combine's loop order — identical bits to k_pfg_reduce.
-__host__ __device__ inline int rproto_doubles(int d, int LB) { return 4 * d * d * LB; }
+__host__ __device__ inline int rproto_doubles(int d, int LB) { return 5 * d * d * LB; }
 
 template <bool BLOCK>
 __global__ void k_pfg_reduce_proto(int T, int d, int B, int LB, const double* __restrict__ el,
@@ -641,13 +748,14 @@ __global__ void k_pfg_reduce_proto(int T, int d, int B, int LB, const double* __
     g_copy(g, ES, e1, acc);
     g.sync();
     for (int p = 0; p < LB; ++p) {
-      double* Mp = M + (size_t)p * 4 * dd;
+      double* Mp = M + (size_t)p * 5 * dd;
       g_copy(g, dd, acc, Mp);
       g_copy(g, dd, acc + dd + d, Mp + dd);
       g_copy(g, dd, acc + 2 * dd + 2 * d, Mp + 2 * dd);
       g.sync();
       if (p + 1 < LB) {
         g_combine(g, d, acc, e1, o, cs, Mp + 3 * dd);
+        for (int e = g.lane; e < dd; e += g.size) Mp[4 * dd + e] = Mp[3 * dd + (e % d) * d + e / d];
         g_copy(g, ES, o, acc);
         g.sync();
       }
@@ -655,94 +763,136 @@ __global__ void k_pfg_reduce_proto(int T, int d, int B, int LB, const double* __
   }
 }
 
-// thread per (sequence, block), blocks [max(k_lo, 1), k_hi)
-__global__ void k_pfg_reduce_fill(int T, int d, int B, int LB, const double* __restrict__ el,
-                                  const double* __restrict__ mats, double* agg, int k_lo,
-                                  int k_hi) {
-  constexpr int MX = 16;
+// warp per (sequence, block), blocks [max(k_lo, 1), k_hi): lane i of the low half
+// carries b_i, lane i of the high half eta_i; each length-d sum is one lane's, over
+// the other half's entries gathered by shuffles, in g_combine's order — identical bits
+constexpr int kFillWarpsR = 8;
+__global__ void __launch_bounds__(kFillWarpsR * 32)
+    k_pfg_reduce_fill(int T, int d, int B, int LB, const double* __restrict__ el,
+                      const double* __restrict__ mats, double* agg, int k_lo, int k_hi) {
+  __shared__ double s_vt[kFillWarpsR][2][256];  // per warp: vA^T, vJ^T of its sequence
   const int ES = fe_size_g(d), dd = d * d;
   const int nblk = (T + 1 + LB - 1) / LB;
   const int k0 = max(k_lo, 1), span = k_hi - k0;
   const long long n = (long long)B * span;
-  for (long long qq = (long long)blockIdx.x * blockDim.x + threadIdx.x; qq < n;
-       qq += (long long)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, hi = lane >> 4, i = lane & 15;
+  const int src = lane & 16;  // this half's first lane
+  const bool row = i < d;
+  for (long long qq = (long long)blockIdx.x * kFillWarpsR + (threadIdx.x >> 5); qq < n;
+       qq += (long long)gridDim.x * kFillWarpsR) {
     const int b = (int)(qq / span), k = k0 + (int)(qq % span);
-    const int lo = k * LB, hi = min(lo + LB, T + 1);
+    const int lo = k * LB, hb = min(lo + LB, T + 1);
     const double* base = el + (size_t)b * (T + 1) * ES;
     const double* M = mats + (size_t)b * rproto_doubles(d, LB);
     const double* e1 = base + ES;  // v matrices (shared by every t >= 1)
-    const double *vA = e1, *vJ = e1 + 2 * dd + 2 * d;
-    double ub[MX], ueta[MX];
     const double* e = base + (size_t)lo * ES;
-#pragma unroll
-    for (int i = 0; i < MX; ++i)
-      if (i < d) {
-        ub[i] = e[dd + i];
-        ueta[i] = e[2 * dd + d + i];
-      }
-    for (int t = lo + 1; t < hi; ++t) {
+    // the constant operands transposed in shared memory: the lane's row of vJ (high
+    // half) / vA (low half) is read as a column, conflict-free
+    double* vt = s_vt[threadIdx.x >> 5][0];
+    for (int e2 = lane; e2 < dd; e2 += 32) {
+      const int r2 = e2 / d, c2 = e2 % d;
+      vt[c2 * d + r2] = e1[e2];
+      vt[256 + c2 * d + r2] = e1[2 * dd + 2 * d + e2];
+    }
+    __syncwarp();
+    const double* vr = vt + (hi ? 256 : 0);
+    // x: b_i (low half) / eta_i (high half)
+    double x = row ? (hi ? e[2 * dd + d + i] : e[dd + i]) : 0.0;
+    for (int t = lo + 1; t < hb; ++t) {
       const int p = t - lo - 1;  // u = aggregate after p combines
-      const double* Mp = M + (size_t)p * 4 * dd;
-      const double *uA = Mp, *uC = Mp + dd, *Minv = Mp + 3 * dd;
+      const double* Mp = M + (size_t)p * 5 * dd;
+      // column-wise reads (coalesced across the half): uC is symmetric (bits), uA^T's
+      // column i is uA[:, i]; Minv's row i is column i of its stored transpose.  All of
+      // the step's operands are loaded up front (one memory latency per step).
+      const double* Pa = Mp + (hi ? 0 : dd);           // high: uA[q][i]; low: uC[q][i] = uC[i][q]
+      const double* Pm = Mp + (hi ? 3 * dd : 4 * dd);  // high: Minv[q][i]; low: Minv^T[q][i]
       const double* ev = base + (size_t)t * ES;
-      const double *vb = ev + dd, *veta = ev + 2 * dd + d;
-      double tt[MX], w[MX], mt[MX], mt2[MX];
+      double pa[16], pm[16];
 #pragma unroll
-      for (int i = 0; i < MX; ++i)
-        if (i < d) {
-          double acc = 0.0, acc2 = 0.0;
-          for (int q = 0; q < d; ++q) {
-            acc += uC[i * d + q] * veta[q];
-            acc2 += vJ[i * d + q] * ub[q];
-          }
-          tt[i] = acc + ub[i];
-          w[i] = veta[i] - acc2;
-        }
-#pragma unroll
-      for (int i = 0; i < MX; ++i)
-        if (i < d) {
-          double acc = 0.0, acc2 = 0.0;
-#pragma unroll
-          for (int q = 0; q < MX; ++q)
-            if (q < d) {
-              acc += Minv[i * d + q] * tt[q];
-              acc2 += Minv[q * d + i] * w[q];
-            }
-          mt[i] = acc;
-          mt2[i] = acc2;
-        }
-#pragma unroll
-      for (int i = 0; i < MX; ++i)
-        if (i < d) {
-          double acc = 0.0, acc2 = 0.0;
-#pragma unroll
-          for (int q = 0; q < MX; ++q)
-            if (q < d) {
-              acc += vA[i * d + q] * mt[q];
-              acc2 += uA[q * d + i] * mt2[q];
-            }
-          ub[i] = acc + vb[i];
-          ueta[i] = acc2 + ueta[i];
-        }
-    }
-    const double* Mf = M + (size_t)(hi - lo - 1) * 4 * dd;
-    double* out = agg + ((size_t)b * nblk + k) * ES;
-    for (int i = 0; i < dd; ++i) {
-      out[i] = Mf[i];
-      out[dd + d + i] = Mf[dd + i];
-      out[2 * dd + 2 * d + i] = Mf[2 * dd + i];
-    }
-#pragma unroll
-    for (int i = 0; i < MX; ++i)
-      if (i < d) {
-        out[dd + i] = ub[i];
-        out[2 * dd + d + i] = ueta[i];
+      for (int q = 0; q < 16; ++q) {
+        pa[q] = (row && q < d) ? Pa[q * d + i] : 0.0;
+        pm[q] = (row && q < d) ? Pm[q * d + i] : 0.0;
       }
+      const double veta_i = row ? ev[2 * dd + d + i] : 0.0;
+      const double vb_i = (row && !hi) ? ev[dd + i] : 0.0;
+      // low: tt_i = uC[i,:] veta + ub_i ; high: w_i = veta_i - vJ[i,:] ub
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (q < d) {
+          const double ubq = __shfl_sync(0xffffffffu, x, q);
+          const double veq = __shfl_sync(0xffffffffu, veta_i, q);
+          if (row) acc += (hi ? vr[q * d + i] : pa[q]) * (hi ? ubq : veq);
+        }
+      }
+      const double z = row ? (hi ? veta_i - acc : acc + x) : 0.0;
+      // low: mt_i = Minv[i,:] tt ; high: mt2_i = Minv[:,i] . w
+      acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (q < d) {
+          const double zq = __shfl_sync(0xffffffffu, z, src + q);
+          if (row) acc += pm[q] * zq;
+        }
+      }
+      const double mz = acc;
+      // low: ub_i = vA[i,:] mt + vb_i ; high: ueta_i = uA[:,i] . mt2 + ueta_i
+      acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (q < d) {
+          const double mq = __shfl_sync(0xffffffffu, mz, src + q);
+          if (row) acc += (hi ? pa[q] : vr[q * d + i]) * mq;
+        }
+      }
+      if (row) x = hi ? acc + x : acc + vb_i;
+    }
+    const double* Mf = M + (size_t)(hb - lo - 1) * 5 * dd;
+    double* out = agg + ((size_t)b * nblk + k) * ES;
+    for (int e2 = lane; e2 < dd; e2 += 32) {
+      out[e2] = Mf[e2];
+      out[dd + d + e2] = Mf[dd + e2];
+      out[2 * dd + 2 * d + e2] = Mf[2 * dd + e2];
+    }
+    if (row) out[hi ? 2 * dd + d + i : dd + i] = x;
+    __syncwarp();  // s_vt is rewritten for the warp's next block
+  }
+}
+
+// Block 0 of a model with shared step matrices: its first element (t = 0) has
+// A = 0, so the block is a prefix chain (bc_chain_step, the carries' form and
+// fixed point) — the aggregate g_combine's chain would give, at 4 d^3 products
+// per step or none once the covariance is fixed.
+template <bool BLOCK>
+__global__ void k_pfg_reduce0_bc(int T, int d, int B, int LB, const double* __restrict__ el,
+                                 double* agg, int same_lo, int same_hi) {
+  extern __shared__ double smem[];
+  const int ES = fe_size_g(d);
+  const Grp g = BLOCK ? block_group() : warp_group();
+  const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
+  double* sm = smem + (size_t)gid * scan_smem(d, 2);
+  double *acc = sm, *o = acc + ES;
+  const CombScratch cs = comb_scratch(d, o + ES, reinterpret_cast<int*>(o + ES + comb_doubles(d)));
+  const int nblk = (T + 1 + LB - 1) / LB;
+  const int hb = min(LB, T + 1);
+  for (int b = blockIdx.x * gpb + gid; b < B; b += gridDim.x * gpb) {
+    const double* base = el + (size_t)b * (T + 1) * ES;
+    g_copy(g, ES, base, acc);
+    g.sync();
+    bool fixed = false;
+    int nvec = 0;
+    for (int t = 1; t < hb; ++t)
+      bc_chain_step(g, d, acc, base + (size_t)t * ES, t >= same_lo && t < same_hi, o, cs, fixed,
+                    nvec);
+    g_copy(g, ES, acc, agg + (size_t)b * nblk * ES);
+    if (g.lane == 0 && nvec) atomicAdd(&g_fp_steps, (unsigned long long)nvec);
+    g.sync();
   }
 }
 
 template <bool BLOCK>
-__global__ void k_pfg_carry(int T, int d, int B, int LB, const double* __restrict__ agg, double* carry) {
+__global__ void k_pfg_carry(int T, int d, int B, int LB, const double* __restrict__ agg, double* carry,
+                            int same_lo, int same_hi) {
   extern __shared__ double smem[];
   const int ES = fe_size_g(d);
   const Grp g = BLOCK ? block_group() : warp_group();
@@ -752,14 +902,18 @@ __global__ void k_pfg_carry(int T, int d, int B, int LB, const double* __restric
   const CombScratch cs = comb_scratch(d, o + ES, reinterpret_cast<int*>(o + ES + comb_doubles(d)));
   const int nblk = (T + 1 + LB - 1) / LB;
   for (int b = blockIdx.x * gpb + gid; b < B; b += gridDim.x * gpb) {
-    g_copy(g, ES, agg + (size_t)b * nblk * ES, acc);
+    const double* ab = agg + (size_t)b * nblk * ES;
+    g_copy(g, ES, ab, acc);
     g.sync();
+    bool fixed = false;
+    int nvec = 0;
     for (int k = 1; k < nblk; ++k) {
       g_copy(g, ES, acc, carry + ((size_t)b * nblk + k) * ES);
-      g_combine_bc(g, d, acc, agg + ((size_t)b * nblk + k) * ES, o, cs);  // prefixes
-      g_copy(g, ES, o, acc);
       g.sync();
+      bc_chain_step(g, d, acc, ab + (size_t)k * ES, k >= same_lo && k < same_hi, o, cs, fixed,
+                    nvec);  // prefixes
     }
+    if (g.lane == 0 && nvec) atomicAdd(&g_fp_steps, (unsigned long long)nvec);
   }
 }
 
@@ -769,7 +923,7 @@ __global__ void k_pfg_carry(int T, int d, int B, int LB, const double* __restric
 template <bool BLOCK>
 __global__ void k_pfg_carry_seg(int nblk, int d, int B, int LB2, const double* __restrict__ agg,
                                 const double* __restrict__ carry2, double* carry, int j_lo,
-                                int j_hi) {
+                                int j_hi, int same_lo, int same_hi) {
   extern __shared__ double smem[];
   const int ES = fe_size_g(d);
   const Grp g = BLOCK ? block_group() : warp_group();
@@ -794,21 +948,23 @@ __global__ void k_pfg_carry_seg(int nblk, int d, int B, int LB2, const double* _
       g_copy(g, ES, carry2 + (size_t)q * ES, acc);
     }
     g.sync();
+    bool fixed = false;
+    int nvec = 0;
     for (; k < hi; ++k) {
       g_copy(g, ES, acc, Cy + (size_t)k * ES);
-      if (k + 1 < hi) {
-        g_combine_bc(g, d, acc, A + (size_t)k * ES, o, cs);  // prefixes
-        g_copy(g, ES, o, acc);
-      }
       g.sync();
+      if (k + 1 < hi)
+        bc_chain_step(g, d, acc, A + (size_t)k * ES, k >= same_lo && k < same_hi, o, cs, fixed,
+                      nvec);  // prefixes
     }
+    if (g.lane == 0 && nvec) atomicAdd(&g_fp_steps, (unsigned long long)nvec);
   }
 }
 
 template <bool BLOCK>
 __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restrict__ el,
                             const double* __restrict__ carry, double* filt_mean, double* filt_cov,
-                            int k_lo, int k_hi) {
+                            int k_lo, int k_hi, int same_lo, int same_hi) {
   extern __shared__ double smem[];
   const int ES = fe_size_g(d), dd = d * d;
   const Grp g = BLOCK ? block_group() : warp_group();
@@ -824,13 +980,22 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
     const long long q = (long long)b * nblk + k;
     const int lo = k * LB, hi = min(lo + LB, T + 1);
     const double* base = el + (size_t)b * (T + 1) * ES;
+    bool fixed = false;
+    int nvec = 0;
     if (k == 0) {
       g_copy(g, ES, base + (size_t)lo * ES, acc);
       g.sync();
     } else {
       g_copy(g, ES, carry + (size_t)q * ES, cy);
       g.sync();
-      g_combine_bc(g, d, cy, base + (size_t)lo * ES, acc, cs);  // carries are prefixes
+      const bool same = lo >= same_lo && lo < same_hi;
+      g_combine_bc(g, d, cy, base + (size_t)lo * ES, acc, cs, same);  // carries are prefixes
+      fixed = same && g_all_same(g, dd, acc + dd + d, cy + dd + d, cs.idx);
+      if (fixed) {
+        const double* v = base + (size_t)lo * ES;
+        for (int e = g.lane; e < dd; e += g.size) cs.T1[e] = v[(e % d) * d + e / d];
+        g.sync();
+      }
     }
     for (int t = lo;; ++t) {
       for (int i = g.lane; i < d; i += g.size)
@@ -838,10 +1003,11 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
       for (int i = g.lane; i < dd; i += g.size)
         filt_cov[((size_t)b * (T + 1) + t) * dd + i] = acc[dd + d + i];
       if (t + 1 >= hi) break;
-      g_combine_bc(g, d, acc, base + (size_t)(t + 1) * ES, o, cs);
-      g_copy(g, ES, o, acc);
       g.sync();
+      bc_chain_step(g, d, acc, base + (size_t)(t + 1) * ES, t + 1 >= same_lo && t + 1 < same_hi, o,
+                    cs, fixed, nvec);
     }
+    if (g.lane == 0 && nvec) atomicAdd(&g_fp_steps, (unsigned long long)nvec);
     g.sync();
   }
 }
@@ -849,8 +1015,11 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
 // ---------------------------------------------------------------- recovery
 __host__ __device__ inline int rec_smem(int d, int dy) {
   const int W = d > dy ? d : dy;
-  return 3 * d * d + dy * d + 3 * dy * dy + 2 * W + 8;
+  return 4 * d * d + dy * d + 3 * dy * dy + 2 * W + 8;
 }
+// steps per group in the recovery: consecutive steps, so a group can keep the
+// predictive covariance and the innovation factor of the previous step
+constexpr int kRecChunk = 32;
 
 // warp groups per CTA, per kernel: as many as its per-group shared-memory
 // footprint and its register count allow (<= 16; 12 -> 16 took the C5 iteration
@@ -918,7 +1087,8 @@ int launch_elements(const DevModel& dm, const double* obs, int B, double* el, do
 // S1 over blocks [k_lo, k_hi): the proto + fill path for time-invariant models
 template <bool BLOCK>
 int launch_reduce(const DevModel& dm, int B, int LB, const double* el, double* mats, double* agg,
-                  int k_lo, int k_hi, const KCfg& c2, const KCfg& cp, cudaStream_t s) {
+                  int k_lo, int k_hi, const KCfg& c2, const KCfg& cp, cudaStream_t s,
+                  int same_lo = 0, int same_hi = 0) {
   const int T = dm.T, d = dm.dx;
   if (k_hi <= k_lo) return AUXMC_OK;
   if (!mats || BLOCK || !pfg_time_invariant(dm) || LB < 2) {
@@ -928,14 +1098,23 @@ int launch_reduce(const DevModel& dm, int B, int LB, const double* el, double* m
   }
   AUXMC_LAUNCH(k_pfg_reduce_proto<BLOCK>, kgrid(cp, B), cp.threads, cp.smem, s, T, d, B, LB, el,
                mats);
-  if (k_lo == 0)
-    AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, B), c2.threads, c2.smem, s, T, d, B, LB, el, agg,
-                 0, 1);
+  if (k_lo == 0) {
+    if (same_hi > same_lo) {
+      const KCfg c0 = kcfg(k_pfg_reduce0_bc<BLOCK>, d, dm.dy, scan_smem(d, 2));
+      PFG_TRY(set_smem(k_pfg_reduce0_bc<BLOCK>, c0));
+      AUXMC_LAUNCH(k_pfg_reduce0_bc<BLOCK>, kgrid(c0, B), c0.threads, c0.smem, s, T, d, B, LB, el,
+                   agg, same_lo, same_hi);
+    } else {
+      AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, B), c2.threads, c2.smem, s, T, d, B, LB, el, agg,
+                   0, 1);
+    }
+  }
   const int k0 = std::max(k_lo, 1);
   if (k_hi > k0) {
     const long long n = (long long)B * (k_hi - k0);
-    AUXMC_LAUNCH(k_pfg_reduce_fill, (int)std::min<long long>((n + 127) / 128, 148LL * 16), 128, 0,
-                 s, T, d, B, LB, el, mats, agg, k_lo, k_hi);
+    AUXMC_LAUNCH(k_pfg_reduce_fill,
+                 (int)std::min<long long>((n + kFillWarpsR - 1) / kFillWarpsR, 148LL * 32),
+                 32 * kFillWarpsR, 0, s, T, d, B, LB, el, mats, agg, k_lo, k_hi);
   }
   return AUXMC_OK;
 }
@@ -944,7 +1123,7 @@ template <bool BLOCK>
 __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
                               const double* __restrict__ fm, const double* __restrict__ fc,
                               double* pm, double* pc, double* terms, int* status, int t_lo,
-                              int t_hi, int sb = 0, const double* bnd = nullptr) {
+                              int t_hi, int sb, const double* bnd, int reuse) {
   extern __shared__ double smem[];
   const int T = m.T, d = m.dx, dy = m.dy, dd = d * d;
   const int W = d > dy ? d : dy;
@@ -955,12 +1134,24 @@ __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
          *scr = L + dy * dy;
   double *mp = scr + dy * dy, *r = mp + W, *red = r + W;
   int* flag = reinterpret_cast<int*>(red + 2);
+  double* Cprev = red + 4;  // the filtered covariance P, L and scr were formed from
   const int span = t_hi - t_lo;
-  const long long n = (long long)B * span;
+  const int nch = (span + kRecChunk - 1) / kRecChunk;
+  const long long n = (long long)B * nch;
   for (long long qq = (long long)blockIdx.x * gpb + gid; qq < n; qq += (long long)gridDim.x * gpb) {
-    const int b = (int)(qq / span), t = t_lo + (int)(qq % span);
+    const int b = (int)(qq / nch), c0 = t_lo + (int)(qq % nch) * kRecChunk;
+    const int c1 = min(c0 + kRecChunk, t_hi);
+    // reuse (shared F, Q, H, R; pfg_shared_mats): a step whose previous filtered
+    // covariance has the bits of the one P, L were formed from has the same
+    // predictive covariance and innovation factor — the time-invariant filter's
+    // steady state, where only the means move
+    bool have = false;
+    int st_keep = 0;
+    for (int t = c0; t < c1; ++t) {
     const long long q = (long long)b * (T + 1) + t;
+    bool hit = false;
     if (t == 0) {
+      have = false;
       for (int i = g.lane; i < d; i += g.size) mp[i] = m.m0[i];
       for (int i = g.ty(); i < d; i += g.ny())
         for (int j = g.tx(); j < d; j += 16) P[i * d + j] = 0.5 * (m.P0[i * d + j] + m.P0[j * d + i]);
@@ -979,14 +1170,19 @@ __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
         for (int k = 0; k < d; ++k) acc += F[i * d + k] * x[k];
         mp[i] = acc + bb[i];
       }
-      g_mm(g, d, d, d, F, C, t1);
-      for (int i = g.ty(); i < d; i += g.ny())
-        for (int j = g.tx(); j < d; j += 16) qs[i * d + j] = 0.5 * (Q[i * d + j] + Q[j * d + i]);
-      g.sync();
-      g_mm_nt(g, d, d, d, t1, F, P, qs);
-      g.sync();
-      g_symm(g, d, P);
-      g.sync();
+      hit = reuse && have && g_all_same(g, dd, C, Cprev, flag);
+      if (!hit) {
+        g_mm(g, d, d, d, F, C, t1);
+        for (int i = g.ty(); i < d; i += g.ny())
+          for (int j = g.tx(); j < d; j += 16) qs[i * d + j] = 0.5 * (Q[i * d + j] + Q[j * d + i]);
+        if (reuse) g_copy(g, dd, C, Cprev);
+        g.sync();
+        g_mm_nt(g, d, d, d, t1, F, P, qs);
+        g.sync();
+        g_symm(g, d, P);
+        g.sync();
+        have = reuse != 0;
+      }
     }
     for (int i = g.lane; i < d; i += g.size) pm[(size_t)q * d + i] = mp[i];
     for (int i = g.lane; i < dd; i += g.size) pc[(size_t)q * dd + i] = P[i];
@@ -1001,13 +1197,18 @@ __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
         for (int k = 0; k < d; ++k) acc += h[i * d + k] * mp[k];
         r[i] = acc + c[i];  // mean H m + c
       }
-      g_mm(g, dy, d, d, h, P, hp);
-      g.sync();
-      g_mm_nt(g, dy, d, dy, hp, h, s, R);
-      g.sync();
-      g_symm(g, dy, s);
-      g.sync();
-      const int st = g_factor_psd(g, dy, s, L, scr, flag, red);
+      int st = st_keep;
+      if (!hit) {
+        g_mm(g, dy, d, d, h, P, hp);
+        g.sync();
+        g_mm_nt(g, dy, d, dy, hp, h, s, R);
+        g.sync();
+        g_symm(g, dy, s);
+        g.sync();
+        st = st_keep = g_factor_psd(g, dy, s, L, scr, flag, red);
+      } else {
+        g.sync();
+      }
       if (st) {
         if (g.lane == 0 && status) atomicMax(status + b, st);
       } else {
@@ -1016,6 +1217,7 @@ __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
     }
     if (g.lane == 0) terms[q] = term;
     g.sync();
+    }
   }
 }
 
@@ -1029,6 +1231,12 @@ __global__ void k_pfg_sum(int T, int B, const double* terms, double* out) {
 
 // block length ~ (T+1)^(1/3): S1 and S3 run LB sequential combines, S2 runs two
 // levels of ~LB when there are many blocks.
+// super-blocks of LB / 4 blocks (the super-level reduction's full combines are the
+// serial depth the carries' fixed point cannot shorten), at least one prefix-sampler
+// block long (both powers of two: the super-block is a multiple of it)
+int pf_sup_g(int T, int LB) {
+  return std::max({2, LB / 4, prefix_block_len(T > 0 ? T : 1) / LB});
+}
 int pf_block_g(int T) {
   int lb = 4;
   while ((long long)lb * lb * lb < T + 1) lb <<= 1;
@@ -1049,7 +1257,7 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   double* proto = ws.take<double>((size_t)B * proto_doubles(d, dy));
   double* mats = ws.take<double>((size_t)B * rproto_doubles(d, LB));
   const bool two = nblk > kPfTwoLevel;
-  const int LB2 = LB, nsup = (nblk + LB2 - 1) / LB2;
+  const int LB2 = pf_sup_g(T, LB), nsup = (nblk + LB2 - 1) / LB2;
   double* agg2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
   double* carry2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
   if (ws.base == nullptr) return AUXMC_OK;
@@ -1072,24 +1280,27 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   if (status) AUXMC_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int) * B, s));
   const long long n = (long long)B * (T + 1);
   const long long nb = (long long)B * nblk;
+  const SameRanges sr = same_ranges(dm, LB, LB2);
   PFG_TRY(launch_elements<BLOCK>(dm, obs, B, el, proto, status, 0, T + 1, ce, s));
-  PFG_TRY(launch_reduce<BLOCK>(dm, B, LB, el, mats, agg, 0, nblk, c2, cp, s));
+  PFG_TRY(launch_reduce<BLOCK>(dm, B, LB, el, mats, agg, 0, nblk, c2, cp, s, sr.el_lo, sr.el_hi));
   if (two) {
     const long long ns = (long long)B * nsup;
     AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, ns), c2.threads, c2.smem, s, nblk - 1, d, B, LB2,
                  agg, agg2, 0, nsup);
     AUXMC_LAUNCH(k_pfg_carry<BLOCK>, kgrid(cc, B), cc.threads, cc.smem, s, nsup - 1, d, B, 1, agg2,
-                 carry2);
+                 carry2, sr.sup_lo, sr.sup_hi);
     AUXMC_LAUNCH(k_pfg_carry_seg<BLOCK>, kgrid(cg, ns), cg.threads, cg.smem, s, nblk, d, B, LB2,
-                 agg, carry2, carry, 0, nsup);
+                 agg, carry2, carry, 0, nsup, sr.agg_lo, sr.agg_hi);
   } else {
-    AUXMC_LAUNCH(k_pfg_carry<BLOCK>, kgrid(cc, B), cc.threads, cc.smem, s, T, d, B, LB, agg, carry);
+    AUXMC_LAUNCH(k_pfg_carry<BLOCK>, kgrid(cc, B), cc.threads, cc.smem, s, T, d, B, LB, agg, carry,
+                 sr.agg_lo, sr.agg_hi);
   }
   AUXMC_LAUNCH(k_pfg_apply<BLOCK>, kgrid(c3, nb), c3.threads, c3.smem, s, T, d, B, LB, el, carry,
-               out->filt_mean, out->filt_cov, 0, nblk);
-  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, kgrid(cr, n), cr.threads, cr.smem, s, dm, obs, B,
-               out->filt_mean, out->filt_cov, out->pred_mean, out->pred_cov, terms, status, 0,
-               T + 1);
+               out->filt_mean, out->filt_cov, 0, nblk, sr.el_lo, sr.el_hi);
+  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, kgrid(cr, (long long)B * ((T + kRecChunk) / kRecChunk)),
+               cr.threads, cr.smem, s, dm, obs, B, out->filt_mean, out->filt_cov, out->pred_mean,
+               out->pred_cov, terms, status, 0, T + 1, 0, (const double*)nullptr,
+               sr.el_hi > 0 ? 1 : 0);
   AUXMC_LAUNCH(k_pfg_sum, B, kSumThreads, 0, s, T, B, terms, out->log_marginal);
   return AUXMC_OK;
 }
@@ -1108,7 +1319,7 @@ TsGeom ts_geom(int T) {
   TsGeom g;
   g.LB = pf_block_g(T);
   g.nblk = (T + 1 + g.LB - 1) / g.LB;
-  g.LB2 = g.LB;
+  g.LB2 = pf_sup_g(T, g.LB);
   g.nsup = (g.nblk + g.LB2 - 1) / g.LB2;
   g.SB = g.LB * g.LB2;
   return g;
@@ -1175,7 +1386,9 @@ int ts_filter_local(const DevModel& dm, const double* obs, int j_lo, int j_hi, A
   const int t_lo = j_lo * G.SB, t_hi = std::min(j_hi * G.SB, T + 1);
   const int k_lo = j_lo * G.LB2, k_hi = std::min(j_hi * G.LB2, G.nblk);
   PFG_TRY(launch_elements<BLOCK>(dm, obs, 1, b.el, b.proto, status, t_lo, t_hi, ce, s));
-  PFG_TRY(launch_reduce<BLOCK>(dm, 1, G.LB, b.el, b.mats, b.agg, k_lo, k_hi, c2, cp, s));
+  const SameRanges sr = same_ranges(dm, G.LB, G.LB2);
+  PFG_TRY(launch_reduce<BLOCK>(dm, 1, G.LB, b.el, b.mats, b.agg, k_lo, k_hi, c2, cp, s, sr.el_lo,
+                               sr.el_hi));
   AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, j_hi - j_lo), c2.threads, c2.smem, s, G.nblk - 1, d,
                1, G.LB2, b.agg, b.agg2, j_lo, j_hi);
   AUXMC_CUDA_TRY(cudaMemcpyAsync(sup_out, b.agg2 + (size_t)j_lo * ES,
@@ -1207,21 +1420,23 @@ int ts_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_hi, 
   AUXMC_CUDA_TRY(cudaMemcpyAsync(b.agg2, sup_all, sizeof(double) * (size_t)G.nsup * ES,
                                  cudaMemcpyDeviceToDevice, s));
   // every rank runs the same serial carry over all super-block aggregates
+  const SameRanges sr = same_ranges(dm, G.LB, G.LB2);
   AUXMC_LAUNCH(k_pfg_carry<BLOCK>, 1, cc.threads, cc.smem, s, G.nsup - 1, d, 1, 1, b.agg2,
-               b.carry2);
+               b.carry2, sr.sup_lo, sr.sup_hi);
   AUXMC_LAUNCH(k_pfg_carry_seg<BLOCK>, kgrid(cg, j_hi - j_lo), cg.threads, cg.smem, s, G.nblk, d,
-               1, G.LB2, b.agg, b.carry2, b.carry, j_lo, j_hi);
+               1, G.LB2, b.agg, b.carry2, b.carry, j_lo, j_hi, sr.agg_lo, sr.agg_hi);
   AUXMC_LAUNCH(k_pfg_apply<BLOCK>, kgrid(c3, k_hi - k_lo), c3.threads, c3.smem, s, T, d, 1, G.LB,
-               b.el, b.carry, out->filt_mean, out->filt_cov, k_lo, k_hi);
+               b.el, b.carry, out->filt_mean, out->filt_cov, k_lo, k_hi, sr.el_lo, sr.el_hi);
   const int jb_hi = std::min(j_hi + 1, G.nsup);  // owned super-blocks and the next one's start
   AUXMC_LAUNCH(k_ts_boundary, std::max(1, jb_hi - j_lo), 128, 0, s, d, j_lo, jb_hi, b.carry2,
                b.bnd);
   // + the predictive moments at t_hi (the next range's first step, from the
   // carry of super-block j_hi: identical bits on both ranks) for the sampler
   const int r_hi = std::min(t_hi + 1, T + 1);
-  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, kgrid(cr, r_hi - t_lo), cr.threads, cr.smem, s, dm, obs, 1,
+  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, kgrid(cr, (r_hi - t_lo + kRecChunk - 1) / kRecChunk),
+               cr.threads, cr.smem, s, dm, obs, 1,
                out->filt_mean, out->filt_cov, out->pred_mean, out->pred_cov, b.terms, status, t_lo,
-               r_hi, G.SB, b.bnd);
+               r_hi, G.SB, b.bnd, sr.el_hi > 0 ? 1 : 0);
   AUXMC_LAUNCH(k_ts_partials, (j_hi - j_lo + 127) / 128, 128, 0, s, T, G.SB, j_lo, j_hi, b.terms,
                ll_out);
   return AUXMC_OK;
@@ -1253,6 +1468,17 @@ int tshard_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_
 }
 int tshard_elem_doubles(int dx) { return fe_size_g(dx); }
 
+void pfg_set_fixed_point(int on) { g_pfg_fixed_on = on ? 1 : 0; }
+unsigned long long pfg_fixed_point_steps(int reset) {
+  unsigned long long v = 0;
+  cudaMemcpyFromSymbol(&v, g_fp_steps, sizeof(v));
+  if (reset) {
+    const unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_fp_steps, &z, sizeof(z));
+  }
+  return v;
+}
+
 int dispatch_pf_generic(const DevModel& dm, const double* obs, int B, auxmc_filter_result* out,
                         int* status, Arena& ws, cudaStream_t s) {
   if (dm.dx > 32 || dm.dy > 64) return AUXMC_E_DIM;
@@ -1261,3 +1487,18 @@ int dispatch_pf_generic(const DevModel& dm, const double* obs, int B, auxmc_filt
 }
 
 }  // namespace auxmc_gpu
+
+namespace auxmc_gpu {
+extern int g_bwd_reuse;
+}
+
+extern "C" int auxmc_test_pfg_fixed_point(int on) {
+  auxmc_gpu::pfg_set_fixed_point(on);
+  auxmc_gpu::g_bwd_reuse = on ? 1 : 0;
+  return AUXMC_OK;
+}
+
+extern "C" long long auxmc_test_pfg_fixed_point_steps(int reset) {
+  if (!auxmc_gpu::device_ok()) return -1;
+  return (long long)auxmc_gpu::pfg_fixed_point_steps(reset);
+}

@@ -195,11 +195,7 @@ __global__ void k_pg_apply(int T, int d, int B, int fr_shared, int Lb, int P,
   }
 }
 
-int block_len(int T) {
-  int lb = 16;
-  while ((long long)lb * lb < T && lb < 4096) lb <<= 1;
-  return lb;
-}
+int block_len(int T) { return prefix_block_len(T); }
 
 }  // namespace
 

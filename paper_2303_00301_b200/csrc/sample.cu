@@ -22,6 +22,9 @@ namespace auxmc_gpu {
 
 
 __device__ int g_flip_backward_gain = 0;  // testhooks::flip_backward_gain (testhooks.hpp:11)
+// k_bwd_lean's steady-state reuse (auxmc_test_pfg_fixed_point switches it with the
+// scan filter's fixed point); host-side
+int g_bwd_reuse = 1;
 
 // ---------------------------------------------------------------- elements
 // smem per group: bwd_buffers(f_smem) d*d matrices + 4 d doubles + 2 ints.  Five
@@ -213,9 +216,10 @@ __host__ __device__ inline int bwd_lean_doubles(int d) {
 __global__ void __launch_bounds__(kBwdLeanThreads, BWD_LEAN_MINB)
 k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __restrict__ filt_cov,
            const double* __restrict__ pred_cov, int Bfr, double* elems, double* term,
-           int* status, int store_cov, int t_lo, int t_hi) {
+           int* status, int store_cov, int t_lo, int t_hi, int reuse) {
   extern __shared__ double smem[];
   const int d = m.dx, dd = d * d, T = m.T;
+  const bool flip = g_flip_backward_gain != 0;
   const Grp g = block_group();
   double* Lb = smem;                    // chol(S), then chol(Λ)
   double* W = Lb + dd;                  // C = F P -> L^{-1} C -> G^T
@@ -238,13 +242,38 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
   __syncthreads();
   const int span = t_hi - t_lo;
   const long long n_items = (long long)Bfr * span;
-  for (long long item = blockIdx.x; item < n_items; item += gridDim.x) {
+  // reuse (dense F shared by every step, no stencil): each CTA takes a contiguous
+  // run of items, and an item whose P_t and P_{t+1|t} have the bits of the previous
+  // item's keeps that item's G, Λ and factor (the time-invariant filter's steady
+  // state: only the offset moves).  Otherwise the items are strided over the grid.
+  const long long per = reuse ? (n_items + gridDim.x - 1) / gridDim.x : 1;
+  const long long i_lo = reuse ? blockIdx.x * per : blockIdx.x;
+  const long long i_hi = reuse ? min(n_items, i_lo + per) : n_items;
+  const long long i_step = reuse ? 1 : gridDim.x;
+  bool have = false;  // smem holds W, P (Λ), Lb of item (b, t - 1)
+  int st_keep = 0, b_prev = -1, t_prev = -1;
+  for (long long item = i_lo; item < i_hi; item += i_step) {
     const int b = (int)(item / span);
     const int t = t_lo + (int)(item % span);
     const double* fm = filt_mean + (size_t)b * (T + 1) * d;
     const double* fc = filt_cov + (size_t)b * (T + 1) * dd;
     const double* pc = pred_cov + (size_t)b * (T + 1) * dd;
     int st = 0;
+    bool hit = false;
+    if (have && b == b_prev && t == t_prev + 1 && t < T) {
+      if (g.lane == 0) *flag = 1;
+      g.sync();
+      const long long* x0 = reinterpret_cast<const long long*>(fc + (size_t)t * dd);
+      const long long* x1 = reinterpret_cast<const long long*>(pc + (size_t)(t + 1) * dd);
+      for (int i = g.lane; i < dd; i += g.size)
+        if (x0[i] != x0[i - dd] || x1[i] != x1[i - dd]) *flag = 0;
+      g.sync();
+      hit = *flag != 0;
+      g.sync();
+    }
+    have = false;
+    b_prev = b;
+    t_prev = t;
     if (t == T) {  // terminal law (pit.cpp:85-87)
       double* out = term + (size_t)b * term_stride(d);
       g_copy(g, dd, fc + (size_t)T * dd, P);
@@ -261,6 +290,7 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
     const bool stamp = AUXMC_BWD_EXP == 9 && blockIdx.x == 0 && item == 0;
     (void)stamp;
     BWD_STAMP(0);
+    if (!hit) {
     // P_t and S = P_{t+1|t} by two TMA bulk copies (one HBM round trip, not a load/store
     // loop per element); S's upper triangle is zeroed once it lands
     if (tma) {
@@ -329,7 +359,7 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
       if (!ok) {
         if (g.lane == 0) atomicMax(status + b, 2);
         g.sync();
-        continue;
+        continue;  // have stays false
       }
       g_trsm_lower_blocked(g, d, Lb, dinv, d, W, d);                    // W = L^{-1} C
       BWD_STAMP(4);
@@ -343,10 +373,7 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
           if (j > i) P[i * d + j] = P[j * d + i];
       g.sync();
     }
-    if (g_flip_backward_gain) {
-      for (int i = g.lane; i < dd; i += g.size) W[i] = -W[i];
-      g.sync();
-    }
+    }  // !hit
     BWD_STAMP(7);
     // offset = m_t - G (F m_t + b_t)
     const double* mt = fm + (size_t)t * d;
@@ -363,22 +390,28 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
       v[i] = x + bt[i];
     }
     g.sync();
+    // flip (testhooks::flip_backward_gain): the gain enters negated; W itself is kept
     for (int i = g.lane; i < d; i += g.size) {
       double x = 0.0;
-      for (int k = 0; k < d; ++k) x += W[k * d + i] * v[k];
+      for (int k = 0; k < d; ++k) x += (flip ? -W[k * d + i] : W[k * d + i]) * v[k];
       out[dd + i] = mt[i] - x;
     }
-    for (int e = g.lane; e < dd; e += g.size) out[e] = W[(e % d) * d + e / d];
+    for (int e = g.lane; e < dd; e += g.size) {
+      const double w = W[(e % d) * d + e / d];
+      out[e] = flip ? -w : w;
+    }
     if (store_cov) {
       for (int e = g.lane; e < dd; e += g.size) out[dd + d + e] = P[e];
     } else {
       BWD_STAMP(8);
-      st = g_chol_psd(g, d, P, Lb, dinv, flag, red);
+      if (!hit) st_keep = g_chol_psd(g, d, P, Lb, dinv, flag, red);
+      st = st_keep;
       BWD_STAMP(9);
       for (int e = g.lane; e < dd; e += g.size) out[dd + d + e] = Lb[e];
     }
     if (st && g.lane == 0) atomicMax(status + b, st);
     g.sync();
+    have = reuse != 0;
     BWD_STAMP(10);
   }
 }
@@ -978,8 +1011,9 @@ int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, 
     AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_bwd_lean, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
     const int grid = (int)std::min<long long>(n_items, 148LL * 64);
+    const int reuse = g_bwd_reuse && !dm.fst && dm.nF <= 1;
     AUXMC_LAUNCH(k_bwd_lean, grid, kBwdLeanThreads, smem, stream, dm, fm, fc, pc, Bfr, elems, term,
-                 st_fr, store_cov, t_lo, t_hi);
+                 st_fr, store_cov, t_lo, t_hi, reuse);
     (void)per_blk;
   } else {
     const int warps = 4;

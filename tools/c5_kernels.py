@@ -23,7 +23,9 @@ for _ in range(iters):
     ch.kernel_step(auxk.Backend.kPrefix, parallel_filter=True)
 torch.cuda.synchronize()
 tot, cnt = ctypes.c_double(0.0), ctypes.c_longlong(0)
-names = ["k_pfg", "k_bwd", "k_prefix", "k_path_terms", "k_gamma_terms", "k_build_aux", "k_grads"]
+names = ["k_pfg_elements", "k_pfg_elem_fill", "k_pfg_reduce_proto", "k_pfg_reduce_fill", "k_pfg_reduce<",
+         "k_pfg_carry", "k_pfg_apply", "k_pfg_recover", "k_pfg_sum", "k_bwd", "k_pg_", "k_mma", "k_prefix",
+         "k_path_terms", "k_gamma_terms", "k_build_aux", "k_grads", "k_aux"]
 out = {}
 for nm in names:
     lib.auxmc_profile_end(nm.encode(), ctypes.byref(tot), ctypes.byref(cnt)) if False else None
@@ -35,6 +37,10 @@ for _ in range(iters):
 e1.record()
 torch.cuda.synchronize()
 print(f"C5 T={T}: iteration {e0.elapsed_time(e1) / iters:.2f} ms (all kernels {tot.value / iters:.2f} ms)")
+lib.auxmc_test_pfg_fixed_point_steps(1)
+ch.kernel_step(auxk.Backend.kPrefix, parallel_filter=True)
+torch.cuda.synchronize()
+print(f"  vector-only scan-filter steps per iteration: {lib.auxmc_test_pfg_fixed_point_steps(1)}")
 for nm in names:
     lib.auxmc_profile_begin()
     ch.kernel_step(auxk.Backend.kPrefix, parallel_filter=True)
