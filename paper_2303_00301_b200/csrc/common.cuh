@@ -195,6 +195,13 @@ __device__ __forceinline__ double cta_sum_fixed(long long n, Get get, double* re
 }
 constexpr int kSumThreads = 256;
 
+// k_bwd_lean's items per chunk in its reuse mode, and the chunk records
+// (uniform flag, status) k_bwd_lanes reads
+constexpr int kBwdChunk = 128;
+inline size_t bwd_recs_doubles(int Bfr, int span) {
+  return 2 * (size_t)Bfr * ((span + kBwdChunk - 1) / kBwdChunk);
+}
+
 // block length of the generic prefix sampler (prefix_gen.cu): a power of two near
 // sqrt(T); the scan filter's super-blocks are multiples of it (pfilter_gen.cu), so
 // a time-sharded rank's range holds whole sampler blocks

@@ -1019,7 +1019,10 @@ __host__ __device__ inline int rec_smem(int d, int dy) {
 }
 // steps per group in the recovery: consecutive steps, so a group can keep the
 // predictive covariance and the innovation factor of the previous step
-constexpr int kRecChunk = 32;
+#ifndef AUXMC_REC_CHUNK
+#define AUXMC_REC_CHUNK 128
+#endif
+constexpr int kRecChunk = AUXMC_REC_CHUNK;
 
 // warp groups per CTA, per kernel: as many as its per-group shared-memory
 // footprint and its register count allow (<= 16; 12 -> 16 took the C5 iteration
@@ -1119,11 +1122,111 @@ int launch_reduce(const DevModel& dm, int B, int LB, const double* el, double* m
   return AUXMC_OK;
 }
 
+// per recovery chunk (kRecChunk steps): [uniform flag, status, log det, L (dy^2)]
+__host__ __device__ inline int rec_rec_doubles(int dy) { return 3 + dy * dy; }
+
+// The steps (c0, c1) of every chunk k_pfg_recover marked uniform — each previous
+// filtered covariance has the bits of step c0's, so every step has step c0's
+// predictive covariance (pc row c0) and innovation factor (the chunk record):
+// one lane per step forms its predictive mean and innovation term by the per-step
+// code's operations in its order (the warp log-density's forward substitution and
+// square sum element by element; the log-diagonal sum is the record's) — the same
+// bits, as independent lanes of a light kernel instead of the step-serial chain of
+// the warp group.  d, dy <= 16.
+constexpr int kRecLaneWarps = 8;
+__global__ void __launch_bounds__(kRecLaneWarps * 32)
+    k_pfg_recover_lanes(DevModel m, const double* __restrict__ obs, int B,
+                        const double* __restrict__ fm, double* pm, double* pc, double* terms,
+                        int* status, int t_lo, int t_hi, const double* __restrict__ recs) {
+  constexpr int MX = 16;
+  const int T = m.T, d = m.dx, dy = m.dy, dd = d * d;
+  const int lane = threadIdx.x & 31;
+  const int span = t_hi - t_lo;
+  const int nch = (span + kRecChunk - 1) / kRecChunk;
+  const long long n = (long long)B * nch;
+  for (long long qq = (long long)blockIdx.x * kRecLaneWarps + (threadIdx.x >> 5); qq < n;
+       qq += (long long)gridDim.x * kRecLaneWarps) {
+    const double* rc = recs + (size_t)qq * rec_rec_doubles(dy);
+    if (rc[0] == 0.0) continue;  // not uniform: k_pfg_recover took every step
+    const int b = (int)(qq / nch), c0 = t_lo + (int)(qq % nch) * kRecChunk;
+    const int c1 = min(c0 + kRecChunk, t_hi);
+    const int st = (int)rc[1];
+    const double ld = rc[2];
+    const double* L = rc + 3;
+    const double* P = pc + ((size_t)b * (T + 1) + c0) * dd;
+    for (int u = c0 + 1; u < c1; ++u) {
+      double* row = pc + ((size_t)b * (T + 1) + u) * dd;
+      for (int e = lane; e < dd; e += 32) row[e] = P[e];
+    }
+    for (int t = c0 + 1 + lane; t < c1; t += 32) {
+      const long long q = (long long)b * (T + 1) + t;
+      const double* F = m.Ft(t - 1, b);
+      const double* bb = m.bt(t - 1, b);
+      const double* x = fm + (size_t)(q - 1) * d;
+      double xv[MX], mv[MX];
+#pragma unroll
+      for (int k = 0; k < MX; ++k) xv[k] = k < d ? x[k] : 0.0;
+#pragma unroll
+      for (int i = 0; i < MX; ++i) {
+        if (i < d) {
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < MX; ++k)
+            if (k < d) acc += F[i * d + k] * xv[k];
+          mv[i] = acc + bb[i];
+          pm[(size_t)q * d + i] = mv[i];
+        }
+      }
+      double term = 0.0;
+      if (dy > 0 && m.observed(t)) {
+        if (st) {
+          atomicMax(status + b, st);
+        } else {
+          const double* h = m.Ht(t, b);
+          const double* c = m.ct(t, b);
+          const double* y = obs + (size_t)q * dy;
+          const int nn = dy;
+          double w[MX];
+#pragma unroll
+          for (int i = 0; i < MX; ++i) {
+            if (i < nn) {
+              double acc = 0.0;
+#pragma unroll
+              for (int k = 0; k < MX; ++k)
+                if (k < d) acc += h[i * d + k] * mv[k];
+              w[i] = y[i] - (acc + c[i]);  // x - mean, mean = H m + c
+            }
+          }
+          w[0] = w[0] / L[0];
+#pragma unroll
+          for (int i = 0; i < MX; ++i) {
+            if (i < nn) {
+#pragma unroll
+              for (int j = i + 1; j < MX; ++j) {
+                if (j < nn) {
+                  if (j == i + 1) w[j] = (w[j] - L[j * nn + i] * w[i]) / L[j * nn + j];
+                  else w[j] -= L[j * nn + i] * w[i];
+                }
+              }
+            }
+          }
+          double sq = 0.0;
+#pragma unroll
+          for (int i = 0; i < MX; ++i)
+            if (i < nn) sq += w[i] * w[i];
+          term = -0.5 * (nn * kLog2Pi + sq) - ld;
+        }
+      }
+      terms[q] = term;
+    }
+  }
+}
+
 template <bool BLOCK>
 __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
                               const double* __restrict__ fm, const double* __restrict__ fc,
                               double* pm, double* pc, double* terms, int* status, int t_lo,
-                              int t_hi, int sb, const double* bnd, int reuse) {
+                              int t_hi, int sb, const double* bnd, int reuse, double* recs) {
   extern __shared__ double smem[];
   const int T = m.T, d = m.dx, dy = m.dy, dd = d * d;
   const int W = d > dy ? d : dy;
@@ -1150,6 +1253,40 @@ __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
     for (int t = c0; t < c1; ++t) {
     const long long q = (long long)b * (T + 1) + t;
     bool hit = false;
+    if constexpr (!BLOCK) {
+      // every later step of the chunk repeats step c0's covariance: leave them to
+      // k_pfg_recover_lanes with the chunk's record
+      if (t == c0 + 1 && recs) {
+        double* rc = recs + (size_t)qq * rec_rec_doubles(dy);
+        bool all = have && !(sb > 0 && c0 / sb != (c1 - 1) / sb);
+        if (all) {
+          if (g.lane == 0) *flag = 1;
+          __syncwarp();
+          const long long* cc = reinterpret_cast<const long long*>(fc + (size_t)(q - 1) * dd);
+          const long long* cp = reinterpret_cast<const long long*>(Cprev);
+          for (int u = 0; u < c1 - t; ++u)
+            for (int e = g.lane; e < dd; e += 32)
+              if (cc[(size_t)u * dd + e] != cp[e]) *flag = 0;
+          __syncwarp();
+          all = *flag != 0;
+          __syncwarp();
+        }
+        if (g.lane == 0) {
+          rc[0] = all ? 1.0 : 0.0;
+          rc[1] = (double)st_keep;
+          double ld = 0.0;  // the warp log-density's sum of the logs of L's diagonal
+          if (all && st_keep == 0 && dy > 0)
+            for (int i = 0; i < dy; ++i) ld += log(L[i * dy + i]);
+          rc[2] = ld;
+        }
+        if (all) {
+          for (int e = g.lane; e < dy * dy; e += 32) rc[3 + e] = L[e];
+          __syncwarp();
+          break;
+        }
+        __syncwarp();
+      }
+    }
     if (t == 0) {
       have = false;
       for (int i = g.lane; i < d; i += g.size) mp[i] = m.m0[i];
@@ -1256,12 +1393,13 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   double* terms = ws.take<double>((size_t)B * (T + 1));
   double* proto = ws.take<double>((size_t)B * proto_doubles(d, dy));
   double* mats = ws.take<double>((size_t)B * rproto_doubles(d, LB));
+  double* recs = ws.take<double>((size_t)B * ((T + kRecChunk) / kRecChunk) * rec_rec_doubles(dy));
   const bool two = nblk > kPfTwoLevel;
   const int LB2 = pf_sup_g(T, LB), nsup = (nblk + LB2 - 1) / LB2;
   double* agg2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
   double* carry2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!el || !agg || !carry || !terms || !proto || !mats || (two && (!agg2 || !carry2)))
+  if (!el || !agg || !carry || !terms || !proto || !mats || !recs || (two && (!agg2 || !carry2)))
     return AUXMC_E_WORKSPACE;
   const KCfg ce = kcfg(k_pfg_elements<BLOCK>, d, dy, elem_smem(d, dy));
   const KCfg c2 = kcfg(k_pfg_reduce<BLOCK>, d, dy, scan_smem(d, 2));
@@ -1297,10 +1435,16 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   }
   AUXMC_LAUNCH(k_pfg_apply<BLOCK>, kgrid(c3, nb), c3.threads, c3.smem, s, T, d, B, LB, el, carry,
                out->filt_mean, out->filt_cov, 0, nblk, sr.el_lo, sr.el_hi);
-  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, kgrid(cr, (long long)B * ((T + kRecChunk) / kRecChunk)),
-               cr.threads, cr.smem, s, dm, obs, B, out->filt_mean, out->filt_cov, out->pred_mean,
-               out->pred_cov, terms, status, 0, T + 1, 0, (const double*)nullptr,
-               sr.el_hi > 0 ? 1 : 0);
+  const long long nrc = (long long)B * ((T + kRecChunk) / kRecChunk);
+  double* recs_on = (!BLOCK && sr.el_hi > 0) ? recs : nullptr;
+  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, kgrid(cr, nrc), cr.threads, cr.smem, s, dm, obs, B,
+               out->filt_mean, out->filt_cov, out->pred_mean, out->pred_cov, terms, status, 0, T + 1,
+               0, (const double*)nullptr, sr.el_hi > 0 ? 1 : 0, recs_on);
+  if (recs_on)
+    AUXMC_LAUNCH(k_pfg_recover_lanes,
+                 (int)std::min<long long>((nrc + kRecLaneWarps - 1) / kRecLaneWarps, 148LL * 32),
+                 32 * kRecLaneWarps, 0, s, dm, obs, B, out->filt_mean, out->pred_mean,
+                 out->pred_cov, terms, status, 0, T + 1, recs_on);
   AUXMC_LAUNCH(k_pfg_sum, B, kSumThreads, 0, s, T, B, terms, out->log_marginal);
   return AUXMC_OK;
 }
@@ -1326,7 +1470,7 @@ TsGeom ts_geom(int T) {
 }
 
 struct TsBufs {
-  double *el, *agg, *carry, *terms, *agg2, *carry2, *bnd, *proto, *mats;
+  double *el, *agg, *carry, *terms, *agg2, *carry2, *bnd, *proto, *mats, *recs;
 };
 TsBufs ts_take(const DevModel& dm, Arena& ws) {
   const TsGeom G = ts_geom(dm.T);
@@ -1341,6 +1485,7 @@ TsBufs ts_take(const DevModel& dm, Arena& ws) {
   b.bnd = ws.take<double>((size_t)G.nsup * (dm.dx + dm.dx * dm.dx));
   b.proto = ws.take<double>((size_t)proto_doubles(dm.dx, dm.dy));
   b.mats = ws.take<double>((size_t)rproto_doubles(dm.dx, G.LB));
+  b.recs = ws.take<double>((size_t)((T + kRecChunk) / kRecChunk + 1) * rec_rec_doubles(dm.dy));
   return b;
 }
 
@@ -1433,10 +1578,16 @@ int ts_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_hi, 
   // + the predictive moments at t_hi (the next range's first step, from the
   // carry of super-block j_hi: identical bits on both ranks) for the sampler
   const int r_hi = std::min(t_hi + 1, T + 1);
-  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, kgrid(cr, (r_hi - t_lo + kRecChunk - 1) / kRecChunk),
-               cr.threads, cr.smem, s, dm, obs, 1,
+  const long long nrc = (r_hi - t_lo + kRecChunk - 1) / kRecChunk;
+  double* recs_on = (!BLOCK && sr.el_hi > 0) ? b.recs : nullptr;
+  AUXMC_LAUNCH(k_pfg_recover<BLOCK>, kgrid(cr, nrc), cr.threads, cr.smem, s, dm, obs, 1,
                out->filt_mean, out->filt_cov, out->pred_mean, out->pred_cov, b.terms, status, t_lo,
-               r_hi, G.SB, b.bnd, sr.el_hi > 0 ? 1 : 0);
+               r_hi, G.SB, b.bnd, sr.el_hi > 0 ? 1 : 0, recs_on);
+  if (recs_on)
+    AUXMC_LAUNCH(k_pfg_recover_lanes,
+                 (int)std::min<long long>((nrc + kRecLaneWarps - 1) / kRecLaneWarps, 148LL * 32),
+                 32 * kRecLaneWarps, 0, s, dm, obs, 1, out->filt_mean, out->pred_mean,
+                 out->pred_cov, b.terms, status, t_lo, r_hi, recs_on);
   AUXMC_LAUNCH(k_ts_partials, (j_hi - j_lo + 127) / 128, 128, 0, s, T, G.SB, j_lo, j_hi, b.terms,
                ll_out);
   return AUXMC_OK;

@@ -245,11 +245,11 @@ int launch_prefix_generic(int T, int d, int B, int fr_shared, const double* elem
 // blocks (every rank, same bits) and expands the rank's blocks.
 int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, const double* pc,
                         int Bfr, double* elems, double* term, int* st_fr, int store_cov,
-                        cudaStream_t stream, int t_lo, int t_hi);
+                        cudaStream_t stream, int t_lo, int t_hi, double* recs);
 
 namespace {
 struct TsPrefixBufs {
-  double *elems, *term, *ops, *offs, *xin;
+  double *elems, *term, *ops, *offs, *xin, *recs;
   int* st;
 };
 TsPrefixBufs tsp_take(const DevModel& dm, Arena& ws) {
@@ -262,6 +262,7 @@ TsPrefixBufs tsp_take(const DevModel& dm, Arena& ws) {
   b.offs = ws.take<double>((size_t)P * d);
   b.xin = ws.take<double>((size_t)P * d);
   b.st = ws.take<int>(1);
+  b.recs = ws.take<double>(bwd_recs_doubles(1, T + 1));
   return b;
 }
 
@@ -303,11 +304,12 @@ int tshard_prefix_local(const DevModel& dm, const double* fm, const double* fc, 
   if (d < 1 || d > 64) return AUXMC_E_DIM;
   const TsPrefixBufs b = tsp_take(dm, ws);
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!b.elems || !b.st) return AUXMC_E_WORKSPACE;
+  if (!b.elems || !b.st || !b.recs) return AUXMC_E_WORKSPACE;
   if (t_lo < 0 || t_hi > T + 1 || t_lo >= t_hi || t_lo % Lb != 0) return AUXMC_E_ARG;
   AUXMC_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), stream));
   // elements for steps [t_lo, min(t_hi, T)) and the terminal law when T is owned
-  int rc = launch_bwd_elements(dm, fm, fc, pc, 1, b.elems, b.term, status, 0, stream, t_lo, t_hi);
+  int rc = launch_bwd_elements(dm, fm, fc, pc, 1, b.elems, b.term, status, 0, stream, t_lo, t_hi,
+                               b.recs);
   if (rc) return rc;
   const int s_hi = std::min(t_hi, T);
   if (s_hi > t_lo) {
@@ -338,7 +340,7 @@ int tshard_prefix_finish(const DevModel& dm, const NoiseArgs& nz, int t_lo, int 
   const int T = dm.T, d = dm.dx, Lb = block_len(T > 0 ? T : 1);
   const TsPrefixBufs b = tsp_take(dm, ws);
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!b.elems || !b.st) return AUXMC_E_WORKSPACE;
+  if (!b.elems || !b.st || !b.recs) return AUXMC_E_WORKSPACE;
   if (T == 0) return AUXMC_OK;
   const int P = (T + Lb - 1) / Lb;
   AUXMC_LAUNCH(k_tsp_unpack, 64, 256, 0, stream, d, P, blk_all, b.ops, b.offs);

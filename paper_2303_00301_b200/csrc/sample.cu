@@ -216,7 +216,7 @@ __host__ __device__ inline int bwd_lean_doubles(int d) {
 __global__ void __launch_bounds__(kBwdLeanThreads, BWD_LEAN_MINB)
 k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __restrict__ filt_cov,
            const double* __restrict__ pred_cov, int Bfr, double* elems, double* term,
-           int* status, int store_cov, int t_lo, int t_hi, int reuse) {
+           int* status, int store_cov, int t_lo, int t_hi, int reuse, double* recs) {
   extern __shared__ double smem[];
   const int d = m.dx, dd = d * d, T = m.T;
   const bool flip = g_flip_backward_gain != 0;
@@ -242,19 +242,49 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
   __syncthreads();
   const int span = t_hi - t_lo;
   const long long n_items = (long long)Bfr * span;
-  // reuse (dense F shared by every step, no stencil): each CTA takes a contiguous
-  // run of items, and an item whose P_t and P_{t+1|t} have the bits of the previous
-  // item's keeps that item's G, Λ and factor (the time-invariant filter's steady
-  // state: only the offset moves).  Otherwise the items are strided over the grid.
-  const long long per = reuse ? (n_items + gridDim.x - 1) / gridDim.x : 1;
-  const long long i_lo = reuse ? blockIdx.x * per : blockIdx.x;
-  const long long i_hi = reuse ? min(n_items, i_lo + per) : n_items;
-  const long long i_step = reuse ? 1 : gridDim.x;
+  // reuse (dense F shared by every step, no stencil): each CTA takes chunks of
+  // kBwdChunk consecutive items, and an item whose P_t and P_{t+1|t} have the bits of
+  // the previous item's keeps that item's G, Λ and factor (the time-invariant
+  // filter's steady state: only the offset moves).  recs (d <= 16): when every
+  // later item of a chunk repeats its first item's inputs, the chunk is recorded
+  // and left to k_bwd_lanes.  Otherwise the items are strided over the grid.
+  const int nchk = reuse ? (span + kBwdChunk - 1) / kBwdChunk : 0;
+  const long long n_units = reuse ? (long long)Bfr * nchk : n_items;
   bool have = false;  // smem holds W, P (Λ), Lb of item (b, t - 1)
   int st_keep = 0, b_prev = -1, t_prev = -1;
-  for (long long item = i_lo; item < i_hi; item += i_step) {
+  for (long long unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+  long long i0 = unit, i1 = unit + 1;
+  if (reuse) {
+    const long long bu = unit / nchk, cu = unit % nchk;
+    i0 = bu * span + cu * kBwdChunk;
+    i1 = bu * span + min((long long)span, (cu + 1) * kBwdChunk);
+  }
+  for (long long item = i0; item < i1; ++item) {
     const int b = (int)(item / span);
     const int t = t_lo + (int)(item % span);
+    if (recs && item == i0 + 1) {
+      const int t_last = t_lo + (int)((i1 - 1) % span);
+      bool all = have && b == b_prev && t == t_prev + 1 && t_last < T;
+      if (all) {
+        const long long* f0 = reinterpret_cast<const long long*>(filt_cov + ((size_t)b * (T + 1) + t - 1) * dd);
+        const long long* p0 = reinterpret_cast<const long long*>(pred_cov + ((size_t)b * (T + 1) + t) * dd);
+        if (g.lane == 0) *flag = 1;
+        g.sync();
+        const int nrest = t_last - t + 1;
+        for (long long e = g.lane; e < (long long)nrest * dd; e += g.size) {
+          const int e0 = (int)(e % dd);
+          if (f0[dd + e] != f0[e0] || p0[dd + e] != p0[e0]) *flag = 0;
+        }
+        g.sync();
+        all = *flag != 0;
+        g.sync();
+      }
+      if (g.lane == 0) {
+        recs[2 * unit] = all ? 1.0 : 0.0;
+        recs[2 * unit + 1] = (double)st_keep;
+      }
+      if (all) break;
+    }
     const double* fm = filt_mean + (size_t)b * (T + 1) * d;
     const double* fc = filt_cov + (size_t)b * (T + 1) * dd;
     const double* pc = pred_cov + (size_t)b * (T + 1) * dd;
@@ -413,6 +443,69 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
     g.sync();
     have = reuse != 0;
     BWD_STAMP(10);
+  }
+  }
+}
+
+// The items (c0, c1) of every chunk k_bwd_lean recorded uniform (each repeats item
+// c0's P_t and P_{t+1|t}): their G and factor are item c0's, copied row by row, and
+// lane j forms item c0 + 1 + j's offset m_t - G (F m_t + b_t) by k_bwd_lean's
+// operations in its order (G read from item c0's element: the bits k_bwd_lean
+// wrote, gain flip included).  Dense shared F, d <= 16.
+constexpr int kBwdLaneWarps = 8;
+__global__ void __launch_bounds__(kBwdLaneWarps * 32)
+    k_bwd_lanes(DevModel m, const double* __restrict__ filt_mean, int Bfr, double* elems,
+                int* status, int t_lo, int t_hi, const double* __restrict__ recs) {
+  constexpr int MX = 16;
+  const int d = m.dx, dd = d * d, T = m.T, es = elem_stride(d);
+  const int lane = threadIdx.x & 31;
+  const int span = t_hi - t_lo;
+  const int nchk = (span + kBwdChunk - 1) / kBwdChunk;
+  const long long n_units = (long long)Bfr * nchk;
+  for (long long unit = (long long)blockIdx.x * kBwdLaneWarps + (threadIdx.x >> 5); unit < n_units;
+       unit += (long long)gridDim.x * kBwdLaneWarps) {
+    if (recs[2 * unit] == 0.0) continue;
+    const int b = (int)(unit / nchk), cu = (int)(unit % nchk);
+    const int c0 = t_lo + cu * kBwdChunk, c1 = t_lo + min(span, (cu + 1) * kBwdChunk);
+    const int st = (int)recs[2 * unit + 1];
+    if (st && lane == 0) atomicMax(status + b, st);
+    const double* src = elems + ((size_t)b * T + c0) * es;
+    for (int u = c0 + 1; u < c1; ++u) {
+      double* o = elems + ((size_t)b * T + u) * es;
+      for (int e = lane; e < dd; e += 32) {
+        o[e] = src[e];
+        o[dd + d + e] = src[dd + d + e];
+      }
+    }
+    const double* F = m.Ft(0, b);
+    for (int t = c0 + 1 + lane; t < c1; t += 32) {
+      const double* mt = filt_mean + ((size_t)b * (T + 1) + t) * d;
+      const double* bt = m.bt(t, b);
+      double mv[MX], v[MX];
+#pragma unroll
+      for (int k = 0; k < MX; ++k) mv[k] = k < d ? mt[k] : 0.0;
+#pragma unroll
+      for (int i = 0; i < MX; ++i) {
+        if (i < d) {
+          double x = 0.0;
+#pragma unroll
+          for (int k = 0; k < MX; ++k)
+            if (k < d) x += F[i * d + k] * mv[k];
+          v[i] = x + bt[i];
+        }
+      }
+      double* o = elems + ((size_t)b * T + t) * es;
+#pragma unroll
+      for (int i = 0; i < MX; ++i) {
+        if (i < d) {
+          double x = 0.0;
+#pragma unroll
+          for (int k = 0; k < MX; ++k)
+            if (k < d) x += src[i * d + k] * v[k];
+          o[dd + i] = mv[i] - x;
+        }
+      }
+    }
   }
 }
 
@@ -987,7 +1080,8 @@ int run_sampler(int sampler, int T, int B, int fr_shared, const double* elems,
 // terminal law)
 int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, const double* pc,
                         int Bfr, double* elems, double* term, int* st_fr, int store_cov,
-                        cudaStream_t stream, int t_lo = 0, int t_hi = -1) {
+                        cudaStream_t stream, int t_lo = 0, int t_hi = -1,
+                        double* recs = nullptr) {
   const int d = dm.dx;
   const int per_blk = bwd_buffers(dm.fst != 0) * d * d + 4 * d + 4;  // CTA items: F from global
   const int per = bwd_buffers(true) * d * d + 4 * d + 4;       // warp items: F staged
@@ -1012,8 +1106,15 @@ int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, 
                                         (int)smem));
     const int grid = (int)std::min<long long>(n_items, 148LL * 64);
     const int reuse = g_bwd_reuse && !dm.fst && dm.nF <= 1;
+    double* recs_on = (reuse && d <= 16) ? recs : nullptr;  // k_bwd_lanes: d <= 16
     AUXMC_LAUNCH(k_bwd_lean, grid, kBwdLeanThreads, smem, stream, dm, fm, fc, pc, Bfr, elems, term,
-                 st_fr, store_cov, t_lo, t_hi, reuse);
+                 st_fr, store_cov, t_lo, t_hi, reuse, recs_on);
+    if (recs_on) {
+      const long long nu = (long long)Bfr * ((t_hi - t_lo + kBwdChunk - 1) / kBwdChunk);
+      AUXMC_LAUNCH(k_bwd_lanes,
+                   (int)std::min<long long>((nu + kBwdLaneWarps - 1) / kBwdLaneWarps, 148LL * 32),
+                   32 * kBwdLaneWarps, 0, stream, dm, fm, Bfr, elems, st_fr, t_lo, t_hi, recs_on);
+    }
     (void)per_blk;
   } else {
     const int warps = 4;
@@ -1036,6 +1137,7 @@ int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int f
   double* elems = ws.take<double>((size_t)Bfr * (T > 0 ? T : 1) * elem_stride(d));
   double* term = ws.take<double>((size_t)Bfr * term_stride(d));
   int* st_fr = ws.take<int>((size_t)Bfr);
+  double* recs = ws.take<double>(bwd_recs_doubles(Bfr, T + 1));
   NoiseArgs nz{};
   if (noise) {
     nz.kind = noise->kind;
@@ -1046,10 +1148,10 @@ int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int f
     nz.n_bridge = noise->n_bridge;
   }
   if (ws.base != nullptr) {
-    if (!elems || !term || !st_fr) return AUXMC_E_WORKSPACE;
+    if (!elems || !term || !st_fr || !recs) return AUXMC_E_WORKSPACE;
     AUXMC_CUDA_TRY(cudaMemsetAsync(st_fr, 0, sizeof(int) * Bfr, stream));
     int rc = launch_bwd_elements(dm, fr->filt_mean, fr->filt_cov, fr->pred_cov, Bfr, elems, term,
-                                 st_fr, sampler == AUXMC_SAMPLER_DNC ? 1 : 0, stream);
+                                 st_fr, sampler == AUXMC_SAMPLER_DNC ? 1 : 0, stream, 0, -1, recs);
     if (rc) return rc;
   }
   int rc = AUXMC_OK;
