@@ -226,6 +226,30 @@ __device__ __forceinline__ bool g_all_same(const Grp& g, int n, const double* A,
   return r;
 }
 
+// this thread's share of "every row r < nrows of rows (row length n) has the bits of
+// ref": threads tid, tid + nth, ... of each row, eight rows' loads in flight per
+// round (a streaming compare: the rows are read once, at memory bandwidth)
+__device__ __forceinline__ bool rows_match_part(const double* __restrict__ rows,
+                                                const double* __restrict__ ref, int nrows, int n,
+                                                int tid, int nth) {
+  const long long* a = reinterpret_cast<const long long*>(rows);
+  const long long* z = reinterpret_cast<const long long*>(ref);
+  bool ok = true;
+  for (int e = tid; e < n; e += nth) {
+    const long long z0 = z[e];
+    int r = 0;
+    for (; r + 8 <= nrows; r += 8) {
+      long long v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = a[(size_t)(r + k) * n + e];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ok &= v[k] == z0;
+    }
+    for (; r < nrows; ++r) ok &= a[(size_t)r * n + e] == z0;
+  }
+  return ok;
+}
+
 // ---------------------------------------------------------------- blocked (CTA, n >= 16)
 // Blocked factor/solves with 8-wide panels.  The diagonal 8×8 blocks are
 // factored and inverted by one warp; every other step (panel solve, trailing

@@ -1260,16 +1260,8 @@ __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
         double* rc = recs + (size_t)qq * rec_rec_doubles(dy);
         bool all = have && !(sb > 0 && c0 / sb != (c1 - 1) / sb);
         if (all) {
-          if (g.lane == 0) *flag = 1;
-          __syncwarp();
-          const long long* cc = reinterpret_cast<const long long*>(fc + (size_t)(q - 1) * dd);
-          const long long* cp = reinterpret_cast<const long long*>(Cprev);
-          for (int u = 0; u < c1 - t; ++u)
-            for (int e = g.lane; e < dd; e += 32)
-              if (cc[(size_t)u * dd + e] != cp[e]) *flag = 0;
-          __syncwarp();
-          all = *flag != 0;
-          __syncwarp();
+          all = __all_sync(0xffffffffu, rows_match_part(fc + (size_t)(q - 1) * dd, Cprev, c1 - t,
+                                                        dd, g.lane, 32));
         }
         if (g.lane == 0) {
           rc[0] = all ? 1.0 : 0.0;

@@ -266,18 +266,12 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
       const int t_last = t_lo + (int)((i1 - 1) % span);
       bool all = have && b == b_prev && t == t_prev + 1 && t_last < T;
       if (all) {
-        const long long* f0 = reinterpret_cast<const long long*>(filt_cov + ((size_t)b * (T + 1) + t - 1) * dd);
-        const long long* p0 = reinterpret_cast<const long long*>(pred_cov + ((size_t)b * (T + 1) + t) * dd);
-        if (g.lane == 0) *flag = 1;
-        g.sync();
+        const double* f0 = filt_cov + ((size_t)b * (T + 1) + t - 1) * dd;
+        const double* p0 = pred_cov + ((size_t)b * (T + 1) + t) * dd;
         const int nrest = t_last - t + 1;
-        for (long long e = g.lane; e < (long long)nrest * dd; e += g.size) {
-          const int e0 = (int)(e % dd);
-          if (f0[dd + e] != f0[e0] || p0[dd + e] != p0[e0]) *flag = 0;
-        }
-        g.sync();
-        all = *flag != 0;
-        g.sync();
+        const bool mine = rows_match_part(f0 + dd, f0, nrest, dd, g.lane, g.size) &&
+                          rows_match_part(p0 + dd, p0, nrest, dd, g.lane, g.size);
+        all = __syncthreads_and(mine) != 0;
       }
       if (g.lane == 0) {
         recs[2 * unit] = all ? 1.0 : 0.0;
