@@ -203,12 +203,14 @@ inline size_t bwd_recs_doubles(int Bfr, int span) {
 }
 
 // block length of the generic prefix sampler (prefix_gen.cu): a power of two near
-// sqrt(T); the scan filter's super-blocks are multiples of it (pfilter_gen.cu), so
-// a time-sharded rank's range holds whole sampler blocks
+// sqrt(T) / 4 — short block passes for one long chain, the serial block carry
+// streamed (k_pg_carry); the scan filter's super-blocks are multiples of it
+// (pfilter_gen.cu), so a time-sharded rank's range holds whole sampler blocks
 inline int prefix_block_len(int T) {
-  int lb = 16;
-  while ((long long)lb * lb < T && lb < 4096) lb <<= 1;
-  return lb;
+  int lb = 16, lr = 16;  // ~sqrt(T) / 4; ~sqrt(T), kept up to 64 (block rows stay
+  while ((long long)lb * lb * 16 < T && lb < 4096) lb <<= 1;  // well below a path's
+  while ((long long)lr * lr < T && lr < 64) lr <<= 1;         // size for d < 16)
+  return lb > lr ? lb : lr;
 }
 
 }  // namespace auxmc_gpu

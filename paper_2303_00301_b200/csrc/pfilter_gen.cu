@@ -739,13 +739,14 @@ __global__ void k_pfg_reduce_proto(int T, int d, int B, int LB, const double* __
   const int ES = fe_size_g(d), dd = d * d;
   const Grp g = BLOCK ? block_group() : warp_group();
   const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
-  double* sm = smem + (size_t)gid * scan_smem(d, 2);
-  double *acc = sm, *o = acc + ES;
-  const CombScratch cs = comb_scratch(d, o + ES, reinterpret_cast<int*>(o + ES + comb_doubles(d)));
+  double* sm = smem + (size_t)gid * scan_smem(d, 3);
+  double *acc = sm, *o = acc + ES, *e1 = o + ES;  // e1: the shared element, staged
+  const CombScratch cs = comb_scratch(d, e1 + ES, reinterpret_cast<int*>(e1 + ES + comb_doubles(d)));
   for (int b = blockIdx.x * gpb + gid; b < B; b += gridDim.x * gpb) {
-    const double* e1 = el + ((size_t)b * (T + 1) + 1) * ES;
+    const double* e1g = el + ((size_t)b * (T + 1) + 1) * ES;
     double* M = mats + (size_t)b * rproto_doubles(d, LB);
-    g_copy(g, ES, e1, acc);
+    g_copy(g, ES, e1g, acc);
+    g_copy(g, ES, e1g, e1);
     g.sync();
     for (int p = 0; p < LB; ++p) {
       double* Mp = M + (size_t)p * 5 * dd;
@@ -1064,11 +1065,37 @@ int set_smem(K kernel, const KCfg& c) {
     if (rc_) return rc_;    \
   } while (0)
 
+// The block-matrix sequence (k_pfg_reduce_proto, one warp, LB serial combines)
+// needs only the shared element el[1]: it is forked onto a side stream once that
+// element is built and runs beside the element fill and block 0's chain; the block
+// fill waits for it.
+struct ProtoJob {
+  int LB;
+  double* mats;
+  KCfg cp;
+  bool forked;
+};
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+inline int side_stream(SideStream** out) {
+  static SideStream sd;
+  if (!sd.s) {
+    AUXMC_CUDA_TRY(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking));
+    AUXMC_CUDA_TRY(cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming));
+    AUXMC_CUDA_TRY(cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming));
+  }
+  *out = &sd;
+  return AUXMC_OK;
+}
+
 // elements of [t_lo, t_hi): the fill path when the model is time-invariant
 // (t = 1 always built in full for its factors), the full build otherwise
 template <bool BLOCK>
 int launch_elements(const DevModel& dm, const double* obs, int B, double* el, double* proto,
-                    int* status, int t_lo, int t_hi, const KCfg& ce, cudaStream_t s) {
+                    int* status, int t_lo, int t_hi, const KCfg& ce, cudaStream_t s,
+                    ProtoJob* pj = nullptr) {
   if (t_hi <= t_lo) return AUXMC_OK;
   if (!proto || !pfg_time_invariant(dm) || BLOCK) {
     AUXMC_LAUNCH(k_pfg_elements<BLOCK>, kgrid(ce, (long long)B * (t_hi - t_lo)), ce.threads,
@@ -1078,6 +1105,16 @@ int launch_elements(const DevModel& dm, const double* obs, int B, double* el, do
   const int f_lo = t_lo == 0 ? 0 : 1;  // full build of t = 1 (and t = 0 when owned)
   AUXMC_LAUNCH(k_pfg_elements<BLOCK>, kgrid(ce, (long long)B * (2 - f_lo)), ce.threads, ce.smem,
                s, dm, obs, B, el, status, f_lo, 2, proto);
+  if (pj && pj->mats && pj->LB >= 2) {
+    SideStream* sd = nullptr;
+    PFG_TRY(side_stream(&sd));
+    AUXMC_CUDA_TRY(cudaEventRecord(sd->fork, s));
+    AUXMC_CUDA_TRY(cudaStreamWaitEvent(sd->s, sd->fork, 0));
+    AUXMC_LAUNCH(k_pfg_reduce_proto<BLOCK>, kgrid(pj->cp, B), pj->cp.threads, pj->cp.smem, sd->s,
+                 dm.T, dm.dx, B, pj->LB, el, pj->mats);
+    AUXMC_CUDA_TRY(cudaEventRecord(sd->join, sd->s));
+    pj->forked = true;
+  }
   const int g_lo = std::max(t_lo, 2);
   if (t_hi > g_lo) {
     const int per_b = (t_hi - g_lo + 32 * kFillWarps - 1) / (32 * kFillWarps);
@@ -1091,7 +1128,7 @@ int launch_elements(const DevModel& dm, const double* obs, int B, double* el, do
 template <bool BLOCK>
 int launch_reduce(const DevModel& dm, int B, int LB, const double* el, double* mats, double* agg,
                   int k_lo, int k_hi, const KCfg& c2, const KCfg& cp, cudaStream_t s,
-                  int same_lo = 0, int same_hi = 0) {
+                  int same_lo = 0, int same_hi = 0, const ProtoJob* pj = nullptr) {
   const int T = dm.T, d = dm.dx;
   if (k_hi <= k_lo) return AUXMC_OK;
   if (!mats || BLOCK || !pfg_time_invariant(dm) || LB < 2) {
@@ -1099,8 +1136,10 @@ int launch_reduce(const DevModel& dm, int B, int LB, const double* el, double* m
                  c2.smem, s, T, d, B, LB, el, agg, k_lo, k_hi);
     return AUXMC_OK;
   }
-  AUXMC_LAUNCH(k_pfg_reduce_proto<BLOCK>, kgrid(cp, B), cp.threads, cp.smem, s, T, d, B, LB, el,
-               mats);
+  const bool forked = pj && pj->forked;
+  if (!forked)
+    AUXMC_LAUNCH(k_pfg_reduce_proto<BLOCK>, kgrid(cp, B), cp.threads, cp.smem, s, T, d, B, LB, el,
+                 mats);
   if (k_lo == 0) {
     if (same_hi > same_lo) {
       const KCfg c0 = kcfg(k_pfg_reduce0_bc<BLOCK>, d, dm.dy, scan_smem(d, 2));
@@ -1111,6 +1150,11 @@ int launch_reduce(const DevModel& dm, int B, int LB, const double* el, double* m
       AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, B), c2.threads, c2.smem, s, T, d, B, LB, el, agg,
                    0, 1);
     }
+  }
+  if (forked) {
+    SideStream* sd = nullptr;
+    PFG_TRY(side_stream(&sd));
+    AUXMC_CUDA_TRY(cudaStreamWaitEvent(s, sd->join, 0));
   }
   const int k0 = std::max(k_lo, 1);
   if (k_hi > k0) {
@@ -1395,7 +1439,7 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
     return AUXMC_E_WORKSPACE;
   const KCfg ce = kcfg(k_pfg_elements<BLOCK>, d, dy, elem_smem(d, dy));
   const KCfg c2 = kcfg(k_pfg_reduce<BLOCK>, d, dy, scan_smem(d, 2));
-  const KCfg cp = kcfg(k_pfg_reduce_proto<BLOCK>, d, dy, scan_smem(d, 2));
+  const KCfg cp = kcfg(k_pfg_reduce_proto<BLOCK>, d, dy, scan_smem(d, 3));
   const KCfg cc = kcfg(k_pfg_carry<BLOCK>, d, dy, scan_smem(d, 2));
   const KCfg cg = kcfg(k_pfg_carry_seg<BLOCK>, d, dy, scan_smem(d, 2));
   const KCfg c3 = kcfg(k_pfg_apply<BLOCK>, d, dy, scan_smem(d, 3));
@@ -1411,8 +1455,10 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   const long long n = (long long)B * (T + 1);
   const long long nb = (long long)B * nblk;
   const SameRanges sr = same_ranges(dm, LB, LB2);
-  PFG_TRY(launch_elements<BLOCK>(dm, obs, B, el, proto, status, 0, T + 1, ce, s));
-  PFG_TRY(launch_reduce<BLOCK>(dm, B, LB, el, mats, agg, 0, nblk, c2, cp, s, sr.el_lo, sr.el_hi));
+  ProtoJob pj{LB, mats, cp, false};
+  PFG_TRY(launch_elements<BLOCK>(dm, obs, B, el, proto, status, 0, T + 1, ce, s, &pj));
+  PFG_TRY(launch_reduce<BLOCK>(dm, B, LB, el, mats, agg, 0, nblk, c2, cp, s, sr.el_lo, sr.el_hi,
+                               &pj));
   if (two) {
     const long long ns = (long long)B * nsup;
     AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, ns), c2.threads, c2.smem, s, nblk - 1, d, B, LB2,
@@ -1516,16 +1562,17 @@ int ts_filter_local(const DevModel& dm, const double* obs, int j_lo, int j_hi, A
   if (j_lo < 0 || j_hi > G.nsup || j_lo >= j_hi) return AUXMC_E_ARG;
   const KCfg ce = kcfg(k_pfg_elements<BLOCK>, d, dy, elem_smem(d, dy));
   const KCfg c2 = kcfg(k_pfg_reduce<BLOCK>, d, dy, scan_smem(d, 2));
-  const KCfg cp = kcfg(k_pfg_reduce_proto<BLOCK>, d, dy, scan_smem(d, 2));
+  const KCfg cp = kcfg(k_pfg_reduce_proto<BLOCK>, d, dy, scan_smem(d, 3));
   PFG_TRY(set_smem(k_pfg_elements<BLOCK>, ce));
   PFG_TRY(set_smem(k_pfg_reduce<BLOCK>, c2));
   PFG_TRY(set_smem(k_pfg_reduce_proto<BLOCK>, cp));
   const int t_lo = j_lo * G.SB, t_hi = std::min(j_hi * G.SB, T + 1);
   const int k_lo = j_lo * G.LB2, k_hi = std::min(j_hi * G.LB2, G.nblk);
-  PFG_TRY(launch_elements<BLOCK>(dm, obs, 1, b.el, b.proto, status, t_lo, t_hi, ce, s));
+  ProtoJob pj{G.LB, b.mats, cp, false};
+  PFG_TRY(launch_elements<BLOCK>(dm, obs, 1, b.el, b.proto, status, t_lo, t_hi, ce, s, &pj));
   const SameRanges sr = same_ranges(dm, G.LB, G.LB2);
   PFG_TRY(launch_reduce<BLOCK>(dm, 1, G.LB, b.el, b.mats, b.agg, k_lo, k_hi, c2, cp, s, sr.el_lo,
-                               sr.el_hi));
+                               sr.el_hi, &pj));
   AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, j_hi - j_lo), c2.threads, c2.smem, s, G.nblk - 1, d,
                1, G.LB2, b.agg, b.agg2, j_lo, j_hi);
   AUXMC_CUDA_TRY(cudaMemcpyAsync(sup_out, b.agg2 + (size_t)j_lo * ES,

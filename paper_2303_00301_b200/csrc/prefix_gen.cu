@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "dense.cuh"
 #include "rng.cuh"
+#include "tma.cuh"
 
 namespace auxmc_gpu {
 
@@ -63,8 +64,9 @@ __global__ void k_pg_block_ops(int T, int d, int Bfr, int Lb, int P, const doubl
     A = Bm;
     Bm = tmp;
   }
+  // stored transposed: the carry's lanes read row i of A_k as a column (conflict-free)
   double* out = ops + ((size_t)f * P + k) * dd;
-  for (int i = lane; i < dd; i += 32) out[i] = A[i];
+  for (int i = lane; i < dd; i += 32) out[(i % d) * d + i / d] = A[i];
 }
 
 // pass 2: c~_t into traj[t] and a_k; smem per warp: 2 * 64 (xi, a)
@@ -110,19 +112,30 @@ __global__ void k_pg_block_offsets(int T, int d, int B, int fr_shared, int Lb, i
   for (int i = lane; i < d; i += 32) o[i] = a[i];
 }
 
-// pass 3: terminal draw and the serial block carry (one warp per chain)
-__global__ void k_pg_carry(int T, int d, int B, int fr_shared, int P, const double* __restrict__ term,
-                           const double* __restrict__ ops, const double* __restrict__ offs,
-                           NoiseArgs nz, double* __restrict__ traj, double* __restrict__ xin,
-                           const double* __restrict__ xT_in) {
-  __shared__ double sv[kWarpsPG][2][64];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * kWarpsPG + w;
+// pass 3: terminal draw and the serial block carry (one warp per chain, one chain
+// per CTA).  The block operators (stored transposed) and offsets stream through a
+// kCarryStages ring of bulk copies issued kCarryStages blocks ahead, so a step is
+// the d-long dot products alone; without 16-B alignment (odd d) they are read
+// from global memory directly.  Same operations in the same order either way.
+constexpr int kCarryStages = 4;
+__host__ __device__ inline int carry_slot(int d) { return (d * d + d + 1) & ~1; }
+__host__ __device__ inline size_t carry_smem(int d) {
+  return sizeof(double) * ((size_t)kCarryStages * carry_slot(d) + 128);
+}
+__global__ void __launch_bounds__(32)
+    k_pg_carry(int T, int d, int B, int fr_shared, int P, const double* __restrict__ term,
+               const double* __restrict__ ops, const double* __restrict__ offs, NoiseArgs nz,
+               double* __restrict__ traj, double* __restrict__ xin,
+               const double* __restrict__ xT_in) {
+  extern __shared__ __align__(16) double csm[];
+  __shared__ __align__(8) uint64_t bars[kCarryStages];
+  const int lane = threadIdx.x;
+  const int c = blockIdx.x;
   if (c >= B) return;
-  const int dd = d * d;
+  const int dd = d * d, slot = carry_slot(d);
   const double* tm = term + (size_t)(fr_shared ? 0 : c) * term_stride(d);
-  double* x = sv[w][0];
-  double* xn = sv[w][1];
+  double* x = csm + (size_t)kCarryStages * slot;
+  double* xn = x + 64;
   double* out = traj + (size_t)c * (T + 1) * d;
   const bool pre = nz.kind == AUXMC_NOISE_PREDRAWN;
   if (xT_in) {  // time-sharded: x_T drawn by the rank that owns T
@@ -144,20 +157,54 @@ __global__ void k_pg_carry(int T, int d, int B, int fr_shared, int P, const doub
   }
   __syncwarp();
   const double* O = ops + (size_t)(fr_shared ? 0 : c) * P * dd;
-  for (int k = P - 1; k >= 0; --k) {
+  const double* OF = offs + (size_t)c * P * d;
+  const bool tma = (d % 2 == 0) && ((reinterpret_cast<uintptr_t>(O) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(OF) & 15) == 0);
+  if (tma && lane == 0) {
+    for (int st = 0; st < kCarryStages; ++st) mbar_init(&bars[st], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  auto issue = [&](int k, int st) {  // block k's (A_k^T | a_k) into ring slot st
+    mbar_expect_tx(&bars[st], (unsigned)(dd + d) * 8u);
+    bulk_g2s(csm + (size_t)st * slot, O + (size_t)k * dd, (unsigned)dd * 8u, &bars[st]);
+    bulk_g2s(csm + (size_t)st * slot + dd, OF + (size_t)k * d, (unsigned)d * 8u, &bars[st]);
+  };
+  if (tma && lane == 0)
+    for (int st = 0; st < kCarryStages && P - 1 - st >= 0; ++st) issue(P - 1 - st, st);
+  for (int k = P - 1, it = 0; k >= 0; --k, ++it) {
     double* xe = xin + ((size_t)c * P + k) * d;
     for (int i = lane; i < d; i += 32) xe[i] = x[i];
-    const double* A = O + (size_t)k * dd;
-    const double* a = offs + ((size_t)c * P + k) * d;
+    const double *At, *a;
+    const int st = it % kCarryStages;
+    if (tma) {
+      mbar_wait(&bars[st], (unsigned)(it / kCarryStages) & 1u);
+      At = csm + (size_t)st * slot;
+      a = At + dd;
+    } else {
+      At = O + (size_t)k * dd;
+      a = OF + (size_t)k * d;
+    }
     for (int i = lane; i < d; i += 32) {
       double s = 0.0;
-      for (int j = 0; j < d; ++j) s += A[i * d + j] * x[j];
+      for (int j = 0; j < d; ++j) s += At[j * d + i] * x[j];
       xn[i] = s + a[i];
     }
     __syncwarp();
+    if (tma && lane == 0 && k - kCarryStages >= 0) issue(k - kCarryStages, st);
     for (int i = lane; i < d; i += 32) x[i] = xn[i];
     __syncwarp();
   }
+}
+
+int launch_pg_carry(int T, int d, int B, int fr_shared, int P, const double* term,
+                    const double* ops, const double* offs, const NoiseArgs& nz, double* traj,
+                    double* xin, const double* xT_in, cudaStream_t stream) {
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pg_carry, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)carry_smem(d)));
+  AUXMC_LAUNCH(k_pg_carry, B, 32, carry_smem(d), stream, T, d, B, fr_shared, P, term, ops, offs,
+               nz, traj, xin, xT_in);
+  return AUXMC_OK;
 }
 
 // pass 4: x_t = G_t x_{t+1} + c~_t inside each block
@@ -224,8 +271,11 @@ int launch_prefix_generic(int T, int d, int B, int fr_shared, const double* elem
     AUXMC_LAUNCH(k_pg_block_offsets, (int)((nvec + kWarpsPG - 1) / kWarpsPG), 32 * kWarpsPG, 0,
                  stream, T, d, B, fr_shared, Lb, P, elems, nz, traj, offs, 0, P);
   }
-  AUXMC_LAUNCH(k_pg_carry, (B + kWarpsPG - 1) / kWarpsPG, 32 * kWarpsPG, 0, stream, T, d, B,
-               fr_shared, P, term, ops, offs, nz, traj, xin, nullptr);
+  {
+    const int rc = launch_pg_carry(T, d, B, fr_shared, P, term, ops, offs, nz, traj, xin, nullptr,
+                                   stream);
+    if (rc) return rc;
+  }
   if (T > 0) {
     const long long nvec = (long long)B * P;
     AUXMC_LAUNCH(k_pg_apply, (int)((nvec + kWarpsPG - 1) / kWarpsPG), 32 * kWarpsPG, 0, stream, T,
@@ -326,8 +376,9 @@ int tshard_prefix_local(const DevModel& dm, const double* fm, const double* fc, 
     AUXMC_LAUNCH(k_tsp_pack, 64, 256, 0, stream, d, k_lo, k_hi, b.ops, b.offs, blk_out);
   }
   if (t_hi == T + 1) {  // x_T = m_T + L_T xi on the rank that owns T
-    AUXMC_LAUNCH(k_pg_carry, 1, 32 * kWarpsPG, 0, stream, T, d, 1, 1, 0, b.term, b.ops, b.offs, nz,
-                 traj, b.xin, nullptr);
+    const int rc2 = launch_pg_carry(T, d, 1, 1, 0, b.term, b.ops, b.offs, nz, traj, b.xin, nullptr,
+                                    stream);
+    if (rc2) return rc2;
     AUXMC_CUDA_TRY(cudaMemcpyAsync(xT_out, traj + (size_t)T * d, sizeof(double) * d,
                                    cudaMemcpyDeviceToDevice, stream));
   }
@@ -344,8 +395,11 @@ int tshard_prefix_finish(const DevModel& dm, const NoiseArgs& nz, int t_lo, int 
   if (T == 0) return AUXMC_OK;
   const int P = (T + Lb - 1) / Lb;
   AUXMC_LAUNCH(k_tsp_unpack, 64, 256, 0, stream, d, P, blk_all, b.ops, b.offs);
-  AUXMC_LAUNCH(k_pg_carry, 1, 32 * kWarpsPG, 0, stream, T, d, 1, 1, P, b.term, b.ops, b.offs, nz,
-               traj, b.xin, xT);
+  {
+    const int rc = launch_pg_carry(T, d, 1, 1, P, b.term, b.ops, b.offs, nz, traj, b.xin, xT,
+                                   stream);
+    if (rc) return rc;
+  }
   const int s_hi = std::min(t_hi, T);
   if (s_hi > t_lo) {
     const int k_lo = t_lo / Lb, k_hi = (s_hi + Lb - 1) / Lb;
