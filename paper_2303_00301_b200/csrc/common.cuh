@@ -182,7 +182,15 @@ __device__ __forceinline__ double cta_sum_fixed(long long n, Get get, double* re
   const long long lo = tid * chunk;
   const long long hi = lo + chunk < n ? lo + chunk : n;
   double s = 0.0;
-  for (long long i = lo; i < hi; ++i) s += get(i);
+  long long i = lo;
+  for (; i + 8 <= hi; i += 8) {  // eight loads in flight, added in index order
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = get(i + k);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+  }
+  for (; i < hi; ++i) s += get(i);
   red[tid] = s;
   __syncthreads();
   for (int w = nt >> 1; w > 0; w >>= 1) {

@@ -262,15 +262,18 @@ __device__ __noinline__ void g_combine(const Grp& g, int d, const double* u, con
 // g_combine_t uses for them; with u.A = 0 the full combine's other outputs reduce
 // to A = 0, eta = 0 + u.eta, J = symm(0 + u.J), written directly.  The output is
 // bit-identical to g_combine_t's, at 4 instead of 9 d^3 products.
+// vm: where v's matrices (A, C, J) are read — v itself, or an element with the same
+// matrices (the shared element of a time-invariant model, whose per-step copies the
+// element fill then need not write)
 template <int DC>
 __device__ __forceinline__ void g_combine_bc_t(const Grp& g, int d_rt, const double* u,
-                                               const double* v, double* o,
+                                               const double* v, const double* vm, double* o,
                                                const CombScratch& s, bool keep_minv) {
   const int d = DC ? DC : d_rt;
   const int dd = d * d;
   const double *ub = u + dd, *uC = u + dd + d, *ueta = u + 2 * dd + d, *uJ = u + 2 * dd + 2 * d;
-  const double *vA = v, *vb = v + dd, *vC = v + dd + d, *veta = v + 2 * dd + d,
-               *vJ = v + 2 * dd + 2 * d;
+  const double *vA = vm, *vb = v + dd, *vC = vm + dd + d, *veta = v + 2 * dd + d,
+               *vJ = vm + 2 * dd + 2 * d;
   double *oA = o, *ob = o + dd, *oC = o + dd + d, *oeta = o + 2 * dd + d, *oJ = o + 2 * dd + 2 * d;
   double* const M1 = oC;
   double* Minv = oJ;
@@ -325,9 +328,10 @@ __device__ __forceinline__ void g_combine_bc_t(const Grp& g, int d_rt, const dou
 
 __device__ __noinline__ void g_combine_bc(const Grp& g, int d, const double* u, const double* v,
                                           double* o, const CombScratch& s,
-                                          bool keep_minv = false) {
-  if (d == 16) g_combine_bc_t<16>(g, d, u, v, o, s, keep_minv);
-  else g_combine_bc_t<0>(g, d, u, v, o, s, keep_minv);
+                                          bool keep_minv = false, const double* vm = nullptr) {
+  if (!vm) vm = v;
+  if (d == 16) g_combine_bc_t<16>(g, d, u, v, vm, o, s, keep_minv);
+  else g_combine_bc_t<0>(g, d, u, v, vm, o, s, keep_minv);
 }
 
 // ---------------------------------------------------------------- covariance fixed point
@@ -386,22 +390,24 @@ __device__ __noinline__ void g_bc_vec(const Grp& g, int d, double* u, const doub
 __device__ unsigned long long g_fp_steps = 0;
 
 // one step u <- (u then v) of a prefix chain; `same`: v's matrices are the
-// chain's shared ones.  fixed: the chain sits at a covariance fixed point (its A
-// transposed into s.T1, the kept inverse's transpose in s.S: g_bc_vec_t); o is the
-// full combine's output buffer.
+// chain's shared ones (read from vsh when given).  fixed: the chain sits at a
+// covariance fixed point (its A transposed into s.T1, the kept inverse's transpose
+// in s.S: g_bc_vec_t); o is the full combine's output buffer.
 __device__ __forceinline__ void bc_chain_step(const Grp& g, int d, double* u, const double* v,
                                               bool same, double* o, const CombScratch& s,
-                                              bool& fixed, int& nvec) {
+                                              bool& fixed, int& nvec,
+                                              const double* vsh = nullptr) {
   const int dd = d * d;
   if (fixed && same) {
     g_bc_vec(g, d, u, v, s);
     ++nvec;
     return;
   }
-  g_combine_bc(g, d, u, v, o, s, same);
+  const double* vm = same && vsh ? vsh : v;
+  g_combine_bc(g, d, u, v, o, s, same, vm);
   fixed = same && g_all_same(g, dd, o + dd + d, u + dd + d, s.idx);
   if (fixed)
-    for (int e = g.lane; e < dd; e += g.size) s.T1[e] = v[(e % d) * d + e / d];
+    for (int e = g.lane; e < dd; e += g.size) s.T1[e] = vm[(e % d) * d + e / d];
   g_copy(g, fe_size_g(d), o, u);
   g.sync();
 }
@@ -588,6 +594,11 @@ inline bool pfg_shared_mats(const DevModel& m) {
 // auxmc_test_pfg_fixed_point(0): every prefix step a full combine (the parity
 // tests compare both forms bit for bit)
 int g_pfg_fixed_on = 1;
+// the prefix chains over the elements read the matrices of every step t >= 1 from
+// el[1] (the fill path's shared element), so the fill writes only the vectors
+inline bool shared_el_reads(const DevModel& m, bool block) {
+  return g_pfg_fixed_on && !block && pfg_time_invariant(m);
+}
 struct SameRanges {
   int el_lo, el_hi;    // element indices t with the shared matrices
   int agg_lo, agg_hi;  // block aggregates (full blocks past the first)
@@ -610,7 +621,7 @@ constexpr int kFillWarps = 8;
 // warp w of a CTA: 32 consecutive steps of sequence b, lane = step
 __global__ void __launch_bounds__(kFillWarps * 32)
     k_pfg_elem_fill(DevModel m, const double* __restrict__ obs, int B, double* el,
-                    const double* __restrict__ proto, int t_lo, int t_hi) {
+                    const double* __restrict__ proto, int t_lo, int t_hi, int write_mats) {
   __shared__ double s_mat[3 * 256], s_x1[256], s_x2[256], s_h[256], s_f[256], s_c[16], s_bd[16];
   const int T = m.T, d = m.dx, dy = m.dy, dd = d * d, ES = fe_size_g(d);
   const int span = t_hi - t_lo;
@@ -674,7 +685,9 @@ __global__ void __launch_bounds__(kFillWarps * 32)
       }
     }
   }
-  // A, C, J of the warp's 32 steps, coalesced
+  // A, C, J of the warp's 32 steps, coalesced — unless every reader takes them from
+  // the shared element el[1] (write_mats = 0: the prefix chains' vsh)
+  if (!write_mats) return;
   const int nt = min(32, t_hi - t0);
   for (int u = 0; u < nt; ++u) {
     double* e = el + ((size_t)b * (T + 1) + t0 + u) * ES;
@@ -866,7 +879,7 @@ __global__ void __launch_bounds__(kFillWarpsR * 32)
 // per step or none once the covariance is fixed.
 template <bool BLOCK>
 __global__ void k_pfg_reduce0_bc(int T, int d, int B, int LB, const double* __restrict__ el,
-                                 double* agg, int same_lo, int same_hi) {
+                                 double* agg, int same_lo, int same_hi, int shared_el) {
   extern __shared__ double smem[];
   const int ES = fe_size_g(d);
   const Grp g = BLOCK ? block_group() : warp_group();
@@ -882,9 +895,10 @@ __global__ void k_pfg_reduce0_bc(int T, int d, int B, int LB, const double* __re
     g.sync();
     bool fixed = false;
     int nvec = 0;
+    const double* vsh = shared_el ? base + (size_t)same_lo * ES : nullptr;
     for (int t = 1; t < hb; ++t)
       bc_chain_step(g, d, acc, base + (size_t)t * ES, t >= same_lo && t < same_hi, o, cs, fixed,
-                    nvec);
+                    nvec, vsh);
     g_copy(g, ES, acc, agg + (size_t)b * nblk * ES);
     if (g.lane == 0 && nvec) atomicAdd(&g_fp_steps, (unsigned long long)nvec);
     g.sync();
@@ -965,7 +979,7 @@ __global__ void k_pfg_carry_seg(int nblk, int d, int B, int LB2, const double* _
 template <bool BLOCK>
 __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restrict__ el,
                             const double* __restrict__ carry, double* filt_mean, double* filt_cov,
-                            int k_lo, int k_hi, int same_lo, int same_hi) {
+                            int k_lo, int k_hi, int same_lo, int same_hi, int shared_el) {
   extern __shared__ double smem[];
   const int ES = fe_size_g(d), dd = d * d;
   const Grp g = BLOCK ? block_group() : warp_group();
@@ -981,6 +995,7 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
     const long long q = (long long)b * nblk + k;
     const int lo = k * LB, hi = min(lo + LB, T + 1);
     const double* base = el + (size_t)b * (T + 1) * ES;
+    const double* vsh = shared_el ? base + (size_t)same_lo * ES : nullptr;
     bool fixed = false;
     int nvec = 0;
     if (k == 0) {
@@ -990,11 +1005,11 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
       g_copy(g, ES, carry + (size_t)q * ES, cy);
       g.sync();
       const bool same = lo >= same_lo && lo < same_hi;
-      g_combine_bc(g, d, cy, base + (size_t)lo * ES, acc, cs, same);  // carries are prefixes
+      const double* vm = same && vsh ? vsh : base + (size_t)lo * ES;
+      g_combine_bc(g, d, cy, base + (size_t)lo * ES, acc, cs, same, vm);  // carries are prefixes
       fixed = same && g_all_same(g, dd, acc + dd + d, cy + dd + d, cs.idx);
       if (fixed) {
-        const double* v = base + (size_t)lo * ES;
-        for (int e = g.lane; e < dd; e += g.size) cs.T1[e] = v[(e % d) * d + e / d];
+        for (int e = g.lane; e < dd; e += g.size) cs.T1[e] = vm[(e % d) * d + e / d];
         g.sync();
       }
     }
@@ -1006,7 +1021,7 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
       if (t + 1 >= hi) break;
       g.sync();
       bc_chain_step(g, d, acc, base + (size_t)(t + 1) * ES, t + 1 >= same_lo && t + 1 < same_hi, o,
-                    cs, fixed, nvec);
+                    cs, fixed, nvec, vsh);
     }
     if (g.lane == 0 && nvec) atomicAdd(&g_fp_steps, (unsigned long long)nvec);
     g.sync();
@@ -1119,7 +1134,7 @@ int launch_elements(const DevModel& dm, const double* obs, int B, double* el, do
   if (t_hi > g_lo) {
     const int per_b = (t_hi - g_lo + 32 * kFillWarps - 1) / (32 * kFillWarps);
     AUXMC_LAUNCH(k_pfg_elem_fill, B * per_b, 32 * kFillWarps, 0, s, dm, obs, B, el, proto, g_lo,
-                 t_hi);
+                 t_hi, shared_el_reads(dm, BLOCK) ? 0 : 1);
   }
   return AUXMC_OK;
 }
@@ -1145,7 +1160,7 @@ int launch_reduce(const DevModel& dm, int B, int LB, const double* el, double* m
       const KCfg c0 = kcfg(k_pfg_reduce0_bc<BLOCK>, d, dm.dy, scan_smem(d, 2));
       PFG_TRY(set_smem(k_pfg_reduce0_bc<BLOCK>, c0));
       AUXMC_LAUNCH(k_pfg_reduce0_bc<BLOCK>, kgrid(c0, B), c0.threads, c0.smem, s, T, d, B, LB, el,
-                   agg, same_lo, same_hi);
+                   agg, same_lo, same_hi, shared_el_reads(dm, BLOCK) ? 1 : 0);
     } else {
       AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, B), c2.threads, c2.smem, s, T, d, B, LB, el, agg,
                    0, 1);
@@ -1472,7 +1487,8 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
                  sr.agg_lo, sr.agg_hi);
   }
   AUXMC_LAUNCH(k_pfg_apply<BLOCK>, kgrid(c3, nb), c3.threads, c3.smem, s, T, d, B, LB, el, carry,
-               out->filt_mean, out->filt_cov, 0, nblk, sr.el_lo, sr.el_hi);
+               out->filt_mean, out->filt_cov, 0, nblk, sr.el_lo, sr.el_hi,
+               shared_el_reads(dm, BLOCK) ? 1 : 0);
   const long long nrc = (long long)B * ((T + kRecChunk) / kRecChunk);
   double* recs_on = (!BLOCK && sr.el_hi > 0) ? recs : nullptr;
   AUXMC_LAUNCH(k_pfg_recover<BLOCK>, kgrid(cr, nrc), cr.threads, cr.smem, s, dm, obs, B,
@@ -1610,7 +1626,8 @@ int ts_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_hi, 
   AUXMC_LAUNCH(k_pfg_carry_seg<BLOCK>, kgrid(cg, j_hi - j_lo), cg.threads, cg.smem, s, G.nblk, d,
                1, G.LB2, b.agg, b.carry2, b.carry, j_lo, j_hi, sr.agg_lo, sr.agg_hi);
   AUXMC_LAUNCH(k_pfg_apply<BLOCK>, kgrid(c3, k_hi - k_lo), c3.threads, c3.smem, s, T, d, 1, G.LB,
-               b.el, b.carry, out->filt_mean, out->filt_cov, k_lo, k_hi, sr.el_lo, sr.el_hi);
+               b.el, b.carry, out->filt_mean, out->filt_cov, k_lo, k_hi, sr.el_lo, sr.el_hi,
+               shared_el_reads(dm, BLOCK) ? 1 : 0);
   const int jb_hi = std::min(j_hi + 1, G.nsup);  // owned super-blocks and the next one's start
   AUXMC_LAUNCH(k_ts_boundary, std::max(1, jb_hi - j_lo), 128, 0, s, d, j_lo, jb_hi, b.carry2,
                b.bnd);
