@@ -777,6 +777,147 @@ __global__ void k_pfg_reduce_proto(int T, int d, int B, int LB, const double* __
   }
 }
 
+// g_combine_t (warp groups, d <= 16) spread over four warps of a CTA: every product
+// and vector loop is the same warp-level routine on the same operands as in the
+// one-warp combine (identical bits); the independent ones run side by side, so the
+// chain of dependent products is four long instead of nine.  X: one extra d×d buffer
+// (uA^T T2 while S is still being read).  Minv (and its transpose) saved for the fill.
+template <int DC>
+__device__ __forceinline__ void combine4_t(int d_rt, const double* u, const double* v, double* o,
+                                           const CombScratch& s, double* X, double* save_minv,
+                                           double* save_minv_t) {
+  const int d = DC ? DC : d_rt;
+  const int dd = d * d;
+  const Grp g = warp_group();
+  const int warp = threadIdx.x >> 5;
+  const double *uA = u, *ub = u + dd, *uC = u + dd + d, *ueta = u + 2 * dd + d,
+               *uJ = u + 2 * dd + 2 * d;
+  const double *vA = v, *vb = v + dd, *vC = v + dd + d, *veta = v + 2 * dd + d,
+               *vJ = v + 2 * dd + 2 * d;
+  double *oA = o, *ob = o + dd, *oC = o + dd + d, *oeta = o + 2 * dd + d, *oJ = o + 2 * dd + 2 * d;
+  double* const M1 = oC;
+  double* Minv = oJ;
+  double* mt = M1;
+  double* mt2 = M1 + d;
+  // A: Minv = (I + uC vJ)^{-1} (warp 0) | t, w (warp 1)
+  if (warp == 0) {
+    g_mm(g, d, d, d, uC, vJ, M1);
+    g.sync();
+    for (int i = g.lane; i < d; i += g.size) M1[i * d + i] += 1.0;
+    g.sync();
+    w_inverse_gj_t<DC>(g.lane, d, M1, Minv);
+  } else if (warp == 1) {
+    for (int i = g.lane; i < d; i += g.size) {
+      double acc = 0.0, acc2 = 0.0;
+      for (int k = 0; k < d; ++k) {
+        acc += uC[i * d + k] * veta[k];
+        acc2 += vJ[i * d + k] * ub[k];
+      }
+      s.t[i] = acc + ub[i];
+      s.w[i] = veta[i] - acc2;
+    }
+  }
+  __syncthreads();
+  // B: S = Minv uA | T1 = Minv uC | T2 = Minv^T vJ | mt, mt2 and the saved inverse
+  if (warp == 0) {
+    g_mm(g, d, d, d, Minv, uA, s.S);
+  } else if (warp == 1) {
+    g_mm(g, d, d, d, Minv, uC, s.T1);
+  } else if (warp == 2) {
+    g_mm_tn(g, d, d, d, Minv, vJ, s.T2);
+  } else {
+    for (int i = g.lane; i < d; i += g.size) {
+      double acc = 0.0, acc2 = 0.0;
+      for (int k = 0; k < d; ++k) {
+        acc += Minv[i * d + k] * s.t[k];
+        acc2 += Minv[k * d + i] * s.w[k];
+      }
+      mt[i] = acc;
+      mt2[i] = acc2;
+    }
+    for (int e = g.lane; e < dd; e += 32) {
+      save_minv[e] = Minv[e];
+      save_minv_t[e] = Minv[(e % d) * d + e / d];
+    }
+  }
+  __syncthreads();
+  // C: A = vA S | Minv' = vA T1 | X = uA^T T2 | b, eta
+  if (warp == 0) {
+    g_mm(g, d, d, d, vA, s.S, oA);
+  } else if (warp == 1) {
+    g_mm(g, d, d, d, vA, s.T1, Minv);
+  } else if (warp == 2) {
+    g_mm_tn(g, d, d, d, uA, s.T2, X);
+  } else {
+    for (int i = g.lane; i < d; i += g.size) {
+      double acc = 0.0, acc2 = 0.0;
+      for (int k = 0; k < d; ++k) {
+        acc += vA[i * d + k] * mt[k];
+        acc2 += uA[k * d + i] * mt2[k];
+      }
+      ob[i] = acc + vb[i];
+      oeta[i] = acc2 + ueta[i];
+    }
+  }
+  __syncthreads();
+  // D: T1 = Minv' vA^T + vC | T2 = X uA + uJ
+  if (warp == 0) g_mm_nt(g, d, d, d, Minv, vA, s.T1, vC);
+  else if (warp == 1) g_mm(g, d, d, d, X, uA, s.T2, uJ);
+  __syncthreads();
+  for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+    const int i = e / d, j = e % d;
+    oC[e] = 0.5 * (s.T1[i * d + j] + s.T1[j * d + i]);
+    oJ[e] = 0.5 * (s.T2[i * d + j] + s.T2[j * d + i]);
+  }
+  __syncthreads();
+}
+
+__device__ __noinline__ void combine4(int d, const double* u, const double* v, double* o,
+                                      const CombScratch& s, double* X, double* save_minv,
+                                      double* save_minv_t) {
+  if (d == 16) combine4_t<16>(d, u, v, o, s, X, save_minv, save_minv_t);
+  else combine4_t<0>(d, u, v, o, s, X, save_minv, save_minv_t);
+}
+
+// k_pfg_reduce_proto for warp-group models on four warps (combine4): a CTA per
+// sequence, the same matrices bit for bit
+constexpr int kProto4Threads = 128;
+__host__ __device__ inline int proto4_smem(int d) {
+  return 3 * fe_size_g(d) + comb_doubles(d) + comb_ints(d) + d * d;
+}
+__global__ void __launch_bounds__(kProto4Threads)
+    k_pfg_reduce_proto4(int T, int d, int B, int LB, const double* __restrict__ el,
+                        double* mats) {
+  extern __shared__ double smem[];
+  const int ES = fe_size_g(d), dd = d * d;
+  double *acc = smem, *o = acc + ES, *e1 = o + ES;
+  const CombScratch cs = comb_scratch(d, e1 + ES, reinterpret_cast<int*>(e1 + ES + comb_doubles(d)));
+  double* X = e1 + ES + comb_doubles(d) + comb_ints(d);
+  for (int b = blockIdx.x; b < B; b += gridDim.x) {
+    const double* e1g = el + ((size_t)b * (T + 1) + 1) * ES;
+    double* M = mats + (size_t)b * rproto_doubles(d, LB);
+    for (int e = threadIdx.x; e < ES; e += blockDim.x) {
+      acc[e] = e1g[e];
+      e1[e] = e1g[e];
+    }
+    __syncthreads();
+    for (int p = 0; p < LB; ++p) {
+      double* Mp = M + (size_t)p * 5 * dd;
+      for (int e = threadIdx.x; e < dd; e += blockDim.x) {
+        Mp[e] = acc[e];
+        Mp[dd + e] = acc[dd + d + e];
+        Mp[2 * dd + e] = acc[2 * dd + 2 * d + e];
+      }
+      __syncthreads();
+      if (p + 1 < LB) {
+        combine4(d, acc, e1, o, cs, X, Mp + 3 * dd, Mp + 4 * dd);
+        for (int e = threadIdx.x; e < ES; e += blockDim.x) acc[e] = o[e];
+        __syncthreads();
+      }
+    }
+  }
+}
+
 // warp per (sequence, block), blocks [max(k_lo, 1), k_hi): lane i of the low half
 // carries b_i, lane i of the high half eta_i; each length-d sum is one lane's, over
 // the other half's entries gathered by shuffles, in g_combine's order — identical bits
@@ -984,9 +1125,11 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
   const int ES = fe_size_g(d), dd = d * d;
   const Grp g = BLOCK ? block_group() : warp_group();
   const int gid = BLOCK ? 0 : (threadIdx.x >> 5), gpb = BLOCK ? 1 : (blockDim.x >> 5);
-  double* sm = smem + (size_t)gid * scan_smem(d, 3);
-  double *acc = sm, *o = acc + ES, *cy = o + ES;
-  const CombScratch cs = comb_scratch(d, cy + ES, reinterpret_cast<int*>(cy + ES + comb_doubles(d)));
+  double* sm = smem + (size_t)gid * scan_smem(d, 2);
+  // the block's carry is read only by the first combine, whose output is acc: it
+  // shares the combine output buffer o (two element buffers per group, not three)
+  double *acc = sm, *o = acc + ES, *cy = o;
+  const CombScratch cs = comb_scratch(d, o + ES, reinterpret_cast<int*>(o + ES + comb_doubles(d)));
   const int nblk = (T + 1 + LB - 1) / LB;
   const int span = k_hi - k_lo;
   const long long n = (long long)B * span;
@@ -1080,6 +1223,23 @@ int set_smem(K kernel, const KCfg& c) {
     if (rc_) return rc_;    \
   } while (0)
 
+// the block-matrix sequence: four warps per sequence for warp-group models (the
+// one-warp combine's bits), the group kernel otherwise
+template <bool BLOCK>
+int launch_proto(int T, int d, int B, int LB, const double* el, double* mats, const KCfg& cp,
+                 cudaStream_t s) {
+  if (!BLOCK) {
+    const size_t sm = sizeof(double) * proto4_smem(d);
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_reduce_proto4,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    AUXMC_LAUNCH(k_pfg_reduce_proto4, B, kProto4Threads, sm, s, T, d, B, LB, el, mats);
+  } else {
+    AUXMC_LAUNCH(k_pfg_reduce_proto<BLOCK>, kgrid(cp, B), cp.threads, cp.smem, s, T, d, B, LB, el,
+                 mats);
+  }
+  return AUXMC_OK;
+}
+
 // The block-matrix sequence (k_pfg_reduce_proto, one warp, LB serial combines)
 // needs only the shared element el[1]: it is forked onto a side stream once that
 // element is built and runs beside the element fill and block 0's chain; the block
@@ -1125,8 +1285,7 @@ int launch_elements(const DevModel& dm, const double* obs, int B, double* el, do
     PFG_TRY(side_stream(&sd));
     AUXMC_CUDA_TRY(cudaEventRecord(sd->fork, s));
     AUXMC_CUDA_TRY(cudaStreamWaitEvent(sd->s, sd->fork, 0));
-    AUXMC_LAUNCH(k_pfg_reduce_proto<BLOCK>, kgrid(pj->cp, B), pj->cp.threads, pj->cp.smem, sd->s,
-                 dm.T, dm.dx, B, pj->LB, el, pj->mats);
+    PFG_TRY(launch_proto<BLOCK>(dm.T, dm.dx, B, pj->LB, el, pj->mats, pj->cp, sd->s));
     AUXMC_CUDA_TRY(cudaEventRecord(sd->join, sd->s));
     pj->forked = true;
   }
@@ -1152,9 +1311,7 @@ int launch_reduce(const DevModel& dm, int B, int LB, const double* el, double* m
     return AUXMC_OK;
   }
   const bool forked = pj && pj->forked;
-  if (!forked)
-    AUXMC_LAUNCH(k_pfg_reduce_proto<BLOCK>, kgrid(cp, B), cp.threads, cp.smem, s, T, d, B, LB, el,
-                 mats);
+  if (!forked) PFG_TRY(launch_proto<BLOCK>(T, d, B, LB, el, mats, cp, s));
   if (k_lo == 0) {
     if (same_hi > same_lo) {
       const KCfg c0 = kcfg(k_pfg_reduce0_bc<BLOCK>, d, dm.dy, scan_smem(d, 2));
@@ -1457,7 +1614,7 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   const KCfg cp = kcfg(k_pfg_reduce_proto<BLOCK>, d, dy, scan_smem(d, 3));
   const KCfg cc = kcfg(k_pfg_carry<BLOCK>, d, dy, scan_smem(d, 2));
   const KCfg cg = kcfg(k_pfg_carry_seg<BLOCK>, d, dy, scan_smem(d, 2));
-  const KCfg c3 = kcfg(k_pfg_apply<BLOCK>, d, dy, scan_smem(d, 3));
+  const KCfg c3 = kcfg(k_pfg_apply<BLOCK>, d, dy, scan_smem(d, 2));
   const KCfg cr = kcfg(k_pfg_recover<BLOCK>, d, dy, rec_smem(d, dy));
   PFG_TRY(set_smem(k_pfg_elements<BLOCK>, ce));
   PFG_TRY(set_smem(k_pfg_reduce<BLOCK>, c2));
@@ -1609,7 +1766,7 @@ int ts_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_hi, 
   if (j_lo < 0 || j_hi > G.nsup || j_lo >= j_hi) return AUXMC_E_ARG;
   const KCfg cc = kcfg(k_pfg_carry<BLOCK>, d, dy, scan_smem(d, 2));
   const KCfg cg = kcfg(k_pfg_carry_seg<BLOCK>, d, dy, scan_smem(d, 2));
-  const KCfg c3 = kcfg(k_pfg_apply<BLOCK>, d, dy, scan_smem(d, 3));
+  const KCfg c3 = kcfg(k_pfg_apply<BLOCK>, d, dy, scan_smem(d, 2));
   const KCfg cr = kcfg(k_pfg_recover<BLOCK>, d, dy, rec_smem(d, dy));
   PFG_TRY(set_smem(k_pfg_carry<BLOCK>, cc));
   PFG_TRY(set_smem(k_pfg_carry_seg<BLOCK>, cg));
