@@ -835,10 +835,11 @@ __device__ __forceinline__ void combine4_t(int d_rt, const double* u, const doub
       mt[i] = acc;
       mt2[i] = acc2;
     }
-    for (int e = g.lane; e < dd; e += 32) {
-      save_minv[e] = Minv[e];
-      save_minv_t[e] = Minv[(e % d) * d + e / d];
-    }
+    if (save_minv)
+      for (int e = g.lane; e < dd; e += 32) {
+        save_minv[e] = Minv[e];
+        save_minv_t[e] = Minv[(e % d) * d + e / d];
+      }
   }
   __syncthreads();
   // C: A = vA S | Minv' = vA T1 | X = uA^T T2 | b, eta
@@ -877,6 +878,39 @@ __device__ __noinline__ void combine4(int d, const double* u, const double* v, d
                                       double* save_minv_t) {
   if (d == 16) combine4_t<16>(d, u, v, o, s, X, save_minv, save_minv_t);
   else combine4_t<0>(d, u, v, o, s, X, save_minv, save_minv_t);
+}
+
+// k_pfg_reduce for warp-group models on four warps (combine4), a CTA per item: the
+// super-block reduction of the two-level scan, whose LB2-long chains of full
+// combines are its serial depth
+__global__ void __launch_bounds__(128)
+    k_pfg_reduce4(int T, int d, int B, int LB, const double* __restrict__ el, double* agg,
+                  int k_lo, int k_hi) {
+  extern __shared__ double smem[];
+  const int ES = fe_size_g(d);
+  double *acc = smem, *o = acc + ES, *vs = o + ES;
+  const CombScratch cs = comb_scratch(d, vs + ES, reinterpret_cast<int*>(vs + ES + comb_doubles(d)));
+  double* X = vs + ES + comb_doubles(d) + comb_ints(d);
+  const int nblk = (T + 1 + LB - 1) / LB;
+  const int span = k_hi - k_lo;
+  const long long n = (long long)B * span;
+  for (long long qq = blockIdx.x; qq < n; qq += gridDim.x) {
+    const int b = (int)(qq / span), k = k_lo + (int)(qq % span);
+    const long long q = (long long)b * nblk + k;
+    const int lo = k * LB, hi = min(lo + LB, T + 1);
+    const double* base = el + (size_t)b * (T + 1) * ES;
+    for (int e = threadIdx.x; e < ES; e += blockDim.x) acc[e] = base[(size_t)lo * ES + e];
+    __syncthreads();
+    for (int t = lo + 1; t < hi; ++t) {
+      for (int e = threadIdx.x; e < ES; e += blockDim.x) vs[e] = base[(size_t)t * ES + e];
+      __syncthreads();
+      combine4(d, acc, vs, o, cs, X, nullptr, nullptr);
+      for (int e = threadIdx.x; e < ES; e += blockDim.x) acc[e] = o[e];
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < ES; e += blockDim.x) agg[(size_t)q * ES + e] = acc[e];
+    __syncthreads();
+  }
 }
 
 // k_pfg_reduce_proto for warp-group models on four warps (combine4): a CTA per
@@ -1222,6 +1256,25 @@ int set_smem(K kernel, const KCfg& c) {
     const int rc_ = (x);    \
     if (rc_) return rc_;    \
   } while (0)
+
+// the super-block reduction: combine4 CTAs for warp-group models (the one-warp
+// combine's bits), the group kernel otherwise
+template <bool BLOCK>
+int launch_sup_reduce(int T, int d, int B, int LB, const double* agg, double* agg2, int k_lo,
+                      int k_hi, const KCfg& c2, cudaStream_t s) {
+  if (!BLOCK) {
+    const size_t sm = sizeof(double) * proto4_smem(d);
+    AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_reduce4,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const long long n = (long long)B * (k_hi - k_lo);
+    AUXMC_LAUNCH(k_pfg_reduce4, (int)std::min<long long>(n, 148LL * 16), 128, sm, s, T, d, B, LB,
+                 agg, agg2, k_lo, k_hi);
+  } else {
+    AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, (long long)B * (k_hi - k_lo)), c2.threads,
+                 c2.smem, s, T, d, B, LB, agg, agg2, k_lo, k_hi);
+  }
+  return AUXMC_OK;
+}
 
 // the block-matrix sequence: four warps per sequence for warp-group models (the
 // one-warp combine's bits), the group kernel otherwise
@@ -1633,8 +1686,7 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
                                &pj));
   if (two) {
     const long long ns = (long long)B * nsup;
-    AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, ns), c2.threads, c2.smem, s, nblk - 1, d, B, LB2,
-                 agg, agg2, 0, nsup);
+    PFG_TRY(launch_sup_reduce<BLOCK>(nblk - 1, d, B, LB2, agg, agg2, 0, nsup, c2, s));
     AUXMC_LAUNCH(k_pfg_carry<BLOCK>, kgrid(cc, B), cc.threads, cc.smem, s, nsup - 1, d, B, 1, agg2,
                  carry2, sr.sup_lo, sr.sup_hi);
     AUXMC_LAUNCH(k_pfg_carry_seg<BLOCK>, kgrid(cg, ns), cg.threads, cg.smem, s, nblk, d, B, LB2,
@@ -1746,8 +1798,7 @@ int ts_filter_local(const DevModel& dm, const double* obs, int j_lo, int j_hi, A
   const SameRanges sr = same_ranges(dm, G.LB, G.LB2);
   PFG_TRY(launch_reduce<BLOCK>(dm, 1, G.LB, b.el, b.mats, b.agg, k_lo, k_hi, c2, cp, s, sr.el_lo,
                                sr.el_hi, &pj));
-  AUXMC_LAUNCH(k_pfg_reduce<BLOCK>, kgrid(c2, j_hi - j_lo), c2.threads, c2.smem, s, G.nblk - 1, d,
-               1, G.LB2, b.agg, b.agg2, j_lo, j_hi);
+  PFG_TRY(launch_sup_reduce<BLOCK>(G.nblk - 1, d, 1, G.LB2, b.agg, b.agg2, j_lo, j_hi, c2, s));
   AUXMC_CUDA_TRY(cudaMemcpyAsync(sup_out, b.agg2 + (size_t)j_lo * ES,
                                  sizeof(double) * (size_t)(j_hi - j_lo) * ES,
                                  cudaMemcpyDeviceToDevice, s));
