@@ -97,12 +97,13 @@ __global__ void k_gamma_terms(DevTarget tg, FactorLayout fl, int C, const double
 }
 
 __global__ void k_gamma_sum(int T, int C, const double* terms, const int* fst, double* out,
-                            int* status) {
+                            int* status, const double* parts) {
   __shared__ double red[kSumThreads];
   const int c = blockIdx.x;
   const long long K = 2LL * T + 2;
   const double* tm = terms + (size_t)c * K;
-  const double lg = cta_sum_fixed(K, [&](long long i) { return tm[i]; }, red);
+  const double lg = cta_sum_fixed(K, [&](long long i) { return tm[i]; }, red,
+                                  parts ? parts + (size_t)c * kSumThreads : nullptr);
   if (threadIdx.x == 0) {
     out[c] = lg;
     if (status) status[c] = *fst;
@@ -236,11 +237,12 @@ __global__ void k_aux_lik_terms(int C, int T, int d, const double* __restrict__ 
   }
 }
 
-__global__ void k_row_sum(int C, int n, const double* terms, double* out) {
+__global__ void k_row_sum(int C, int n, const double* terms, double* out, const double* parts) {
   __shared__ double red[kSumThreads];
   const int c = blockIdx.x;
   const double* tm = terms + (size_t)c * n;
-  const double s = cta_sum_fixed(n, [&](long long i) { return tm[i]; }, red);
+  const double s = cta_sum_fixed(n, [&](long long i) { return tm[i]; }, red,
+                                 parts ? parts + (size_t)c * kSumThreads : nullptr);
   if (threadIdx.x == 0) out[c] = s;
 }
 
@@ -340,7 +342,9 @@ static int launch_log_gamma(const DevTarget& tg, int C, const double* traj, doub
                logdet, fst);
   AUXMC_LAUNCH(k_gamma_terms, grid_for((long long)C * (2 * tg.T + 2), 128), 128, 0, s, tg, fl, C,
                traj, Ls, logdet, terms);
-  AUXMC_LAUNCH(k_gamma_sum, C, kSumThreads, 0, s, tg.T, C, terms, fst, out, status);
+  PFG_SUM_PARTS(C, 2LL * tg.T + 2, terms);
+  AUXMC_LAUNCH(k_gamma_sum, C, kSumThreads, 0, s, tg.T, C, terms, fst, out, status, parts);
+  if (parts) cudaFreeAsync(parts, s);
   return AUXMC_OK;
 }
 
@@ -499,10 +503,18 @@ static int aux_step(const DevTarget& tg, auxmc_chains* ch, const auxmc_kernel_op
   // aux log-likelihoods Σ_t log N(u_t; ·, δ/2 I)
   AUXMC_LAUNCH(k_aux_lik_terms, grid_for((long long)C * (T + 1)), 256, 0, s, C, T, d, u, prop,
                ch->delta, terms);
-  AUXMC_LAUNCH(k_row_sum, C, kSumThreads, 0, s, C, T + 1, terms, sc.aux_prop);
+  {
+    PFG_SUM_PARTS(C, (long long)T + 1, terms);
+    AUXMC_LAUNCH(k_row_sum, C, kSumThreads, 0, s, C, T + 1, terms, sc.aux_prop, parts);
+    if (parts) cudaFreeAsync(parts, s);
+  }
   AUXMC_LAUNCH(k_aux_lik_terms, grid_for((long long)C * (T + 1)), 256, 0, s, C, T, d, u, ch->x,
                ch->delta, terms);
-  AUXMC_LAUNCH(k_row_sum, C, kSumThreads, 0, s, C, T + 1, terms, sc.aux_x);
+  {
+    PFG_SUM_PARTS(C, (long long)T + 1, terms);
+    AUXMC_LAUNCH(k_row_sum, C, kSumThreads, 0, s, C, T + 1, terms, sc.aux_x, parts);
+    if (parts) cudaFreeAsync(parts, s);
+  }
   AUXMC_LAUNCH(k_mh, cb, 128, 0, s, C, sc, it, ch->log_gamma, ch->iter, ch->stats);
   AUXMC_LAUNCH(k_accept_copy, grid_for((long long)nx), 256, 0, s, C, (long long)(T + 1) * d,
                sc.accept, prop, gprop, ch->x, ch->grad_gen);

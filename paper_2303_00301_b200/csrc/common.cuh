@@ -176,12 +176,13 @@ struct NoiseArgs {
 // (same terms, different association: within the FP64 parity tolerance).
 // red: blockDim.x doubles of shared memory.  Returns the sum on all threads.
 template <class Get>
-__device__ __forceinline__ double cta_sum_fixed(long long n, Get get, double* red) {
+__device__ __forceinline__ double cta_sum_fixed(long long n, Get get, double* red,
+                                              const double* parts = nullptr) {
   const int nt = blockDim.x, tid = threadIdx.x;
   const long long chunk = (n + nt - 1) / nt;
   const long long lo = tid * chunk;
-  const long long hi = lo + chunk < n ? lo + chunk : n;
-  double s = 0.0;
+  const long long hi = parts ? lo : (lo + chunk < n ? lo + chunk : n);
+  double s = parts ? parts[tid] : 0.0;  // parts: the chunk sums, from k_sum_parts
   long long i = lo;
   for (; i + 8 <= hi; i += 8) {  // eight loads in flight, added in index order
     double v[8];
@@ -202,6 +203,49 @@ __device__ __forceinline__ double cta_sum_fixed(long long n, Get get, double* re
   return r;
 }
 constexpr int kSumThreads = 256;
+
+// cta_sum_fixed's chunk sums of a few long rows, spread over warps of many CTAs (one
+// SM alone cannot stream a 2^20-term row): warp (row, c) loads chunk c 32 terms at a
+// time, coalesced, and adds them in index order from 0.0 — the thread loop's sum,
+// bit for bit; cta_sum_fixed(..., parts) then runs the same tree.
+template <typename Get>
+__global__ void __launch_bounds__(256) k_sum_parts(int rows, long long n, Get get, double* parts) {
+  const long long w = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (w >= (long long)rows * kSumThreads) return;
+  const int r = (int)(w / kSumThreads), c = (int)(w % kSumThreads);
+  const long long chunk = (n + kSumThreads - 1) / kSumThreads;
+  const long long lo = c * chunk, hi = lo + chunk < n ? lo + chunk : n;
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (long long base = lo; base < hi; base += 32) {
+    const long long i = base + lane;
+    const double v = i < hi ? get(r, i) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const double vk = __shfl_sync(0xffffffffu, v, k);
+      if (base + k < hi) s += vk;
+    }
+  }
+  if (lane == 0) parts[(size_t)r * kSumThreads + c] = s;
+}
+// rows of a terms array
+struct RowTerms {
+  const double* t;
+  long long stride;
+  __device__ double operator()(int r, long long i) const { return t[(size_t)r * stride + i]; }
+};
+// the two-kernel form pays off for few, long rows
+inline bool sum_parts_pay(int rows, long long n) { return rows <= 16 && n >= 65536; }
+// declares `double* parts` (stream-ordered allocation, freed by the caller after the
+// sum kernel) and fills it with k_sum_parts over `rows` rows of n terms, or leaves it
+// null when one CTA per row is enough
+#define PFG_SUM_PARTS(rows, n, terms)                                                        \
+  double* parts = nullptr;                                                                   \
+  if (::auxmc_gpu::sum_parts_pay((rows), (n))) {                                             \
+    AUXMC_CUDA_TRY(cudaMallocAsync(&parts, sizeof(double) * (rows) * kSumThreads, s));       \
+    AUXMC_LAUNCH(k_sum_parts<RowTerms>, ((rows) * kSumThreads + 7) / 8, 256, 0, s, (rows),   \
+                 (long long)(n), (RowTerms{(terms), (long long)(n)}), parts);                \
+  }
 
 // k_bwd_lean's items per chunk in its reuse mode, and the chunk records
 // (uniform flag, status) k_bwd_lanes reads

@@ -93,18 +93,29 @@ __global__ void k_path_terms(DevModel m, const double* __restrict__ obs, long lo
   }
 }
 
-__global__ void k_path_sum(int T, int B, const double* terms, const uint8_t* mask, int dy,
-                           const double* log_marginal, int fr_shared, const int* fst,
-                           double* out, int* status) {
-  __shared__ double red[kSumThreads];
-  const int b = blockIdx.x;
-  const long long K = 2LL * T + 2;
-  const double* tm = terms + (size_t)b * K;
-  const double lp = cta_sum_fixed(K, [&](long long i) {
+// the path density's terms: T + 1 transition terms, then the observation terms of
+// the observed steps
+struct PathTerms {
+  const double* terms;
+  int T, dy;
+  const uint8_t* mask;
+  __device__ double operator()(int b, long long i) const {
+    const double* tm = terms + (size_t)b * (2LL * T + 2);
     if (i <= T) return tm[i];
     const long long t = i - T - 1;
     return (dy > 0 && (mask == nullptr || mask[t])) ? tm[i] : 0.0;
-  }, red);
+  }
+};
+
+__global__ void k_path_sum(int T, int B, const double* terms, const uint8_t* mask, int dy,
+                           const double* log_marginal, int fr_shared, const int* fst,
+                           double* out, int* status, const double* parts) {
+  __shared__ double red[kSumThreads];
+  const int b = blockIdx.x;
+  const long long K = 2LL * T + 2;
+  const PathTerms pt{terms, T, dy, mask};
+  const double lp = cta_sum_fixed(K, [&](long long i) { return pt(b, i); }, red,
+                                  parts ? parts + (size_t)b * kSumThreads : nullptr);
   if (threadIdx.x == 0) {
     out[b] = lp - log_marginal[fr_shared ? 0 : b];
     status[b] = *fst;
@@ -147,8 +158,15 @@ int launch_path_logpdf(const DevModel& dm, const double* obs, long long obs_stri
   const long long n = (long long)B * K;
   AUXMC_LAUNCH(k_path_terms, (int)std::min<long long>((n + 127) / 128, 148LL * 64), 128, 0, s, dm,
                obs, obs_stride, traj, B, Ls, logdet, dg, hsel, terms);
+  double* parts = nullptr;
+  if (sum_parts_pay(B, 2LL * dm.T + 2)) {
+    AUXMC_CUDA_TRY(cudaMallocAsync(&parts, sizeof(double) * B * kSumThreads, s));
+    AUXMC_LAUNCH(k_sum_parts<PathTerms>, (B * kSumThreads + 7) / 8, 256, 0, s, B,
+                 2LL * dm.T + 2, (PathTerms{terms, dm.T, dm.dy, dm.mask}), parts);
+  }
   AUXMC_LAUNCH(k_path_sum, B, kSumThreads, 0, s, dm.T, B, terms, dm.mask, dm.dy,
-               log_marginal, lm_shared, fst, out, status);
+               log_marginal, lm_shared, fst, out, status, parts);
+  if (parts) cudaFreeAsync(parts, s);
   cudaFreeAsync(Ls, s);
   cudaFreeAsync(logdet, s);
   cudaFreeAsync(terms, s);

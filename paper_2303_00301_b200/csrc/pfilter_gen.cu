@@ -1619,11 +1619,12 @@ __global__ void k_pfg_recover(DevModel m, const double* __restrict__ obs, int B,
   }
 }
 
-__global__ void k_pfg_sum(int T, int B, const double* terms, double* out) {
+__global__ void k_pfg_sum(int T, int B, const double* terms, double* out, const double* parts) {
   __shared__ double red[kSumThreads];
   const int b = blockIdx.x;
   const double* tm = terms + (size_t)b * (T + 1);
-  const double s = cta_sum_fixed((long long)T + 1, [&](long long i) { return tm[i]; }, red);
+  const double s = cta_sum_fixed((long long)T + 1, [&](long long i) { return tm[i]; }, red,
+                                 parts ? parts + (size_t)b * kSumThreads : nullptr);
   if (threadIdx.x == 0) out[b] = s;
 }
 
@@ -1708,7 +1709,14 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
                  (int)std::min<long long>((nrc + kRecLaneWarps - 1) / kRecLaneWarps, 148LL * 32),
                  32 * kRecLaneWarps, 0, s, dm, obs, B, out->filt_mean, out->pred_mean,
                  out->pred_cov, terms, status, 0, T + 1, recs_on);
-  AUXMC_LAUNCH(k_pfg_sum, B, kSumThreads, 0, s, T, B, terms, out->log_marginal);
+  double* parts = nullptr;
+  if (sum_parts_pay(B, (long long)T + 1)) {
+    AUXMC_CUDA_TRY(cudaMallocAsync(&parts, sizeof(double) * B * kSumThreads, s));
+    AUXMC_LAUNCH(k_sum_parts<RowTerms>, (B * kSumThreads + 7) / 8, 256, 0, s, B, (long long)T + 1,
+                 RowTerms{terms, (long long)T + 1}, parts);
+  }
+  AUXMC_LAUNCH(k_pfg_sum, B, kSumThreads, 0, s, T, B, terms, out->log_marginal, parts);
+  if (parts) cudaFreeAsync(parts, s);
   return AUXMC_OK;
 }
 

@@ -123,3 +123,21 @@ def test_c5_shape_aux_step_bit_identical(mods):
     assert n_fixed > 0
     for (a0, l0, x0), (a1, l1, x1) in zip(full, fixed):
         assert torch.equal(a0, a1) and torch.equal(l0, l1) and torch.equal(x0, x1)
+
+
+def test_long_row_sums_keep_their_order(mods, oracle):
+    """Few long rows are summed in two kernels (k_sum_parts: chunk sums by warps of many
+    CTAs, then cta_sum_fixed's tree): the bits of the one-CTA-per-row form, which runs
+    for 17 rows.  Scan-filter log p(y) (d = 7) and the path density, T = 70000."""
+    lib, lgssm, _, _ = mods
+    T, d, dy = 70000, 7, 2
+    m, obs = _strong_model(oracle, T, d, dy, 0.1, seed=5)
+    gm = to_gpu_model(m)
+    one = lgssm.parallel_filter(gm, obs)
+    many = lgssm.parallel_filter(gm, np.stack([obs] * 17))
+    assert torch.equal(one.log_marginal[0], many.log_marginal[0])
+    assert torch.equal(many.log_marginal, many.log_marginal[:1].expand(17))
+    traj = one.filt_mean[0]
+    lp1 = lgssm.path_logpdf(gm, obs, traj, one)
+    lp17 = lgssm.path_logpdf(gm, obs, traj.expand(17, -1, -1).contiguous(), one)
+    assert torch.equal(lp1[0], lp17[0]) and torch.equal(lp17, lp17[:1].expand(17))
