@@ -350,14 +350,13 @@ __device__ __noinline__ void g_combine_bc(const Grp& g, int d, const double* u, 
 // reads are conflict-free.  (A rounding 2-cycle never triggers the test and keeps
 // the full combines; the result is identical either way.)
 template <int DC>
-__device__ __forceinline__ void g_bc_vec_t(const Grp& g, int d_rt, double* u, const double* v,
-                                           const CombScratch& s) {
+__device__ __forceinline__ void g_bc_vec_t(const Grp& g, int d_rt, double* u, const double* vb,
+                                           const double* veta, const CombScratch& s) {
   const int d = DC ? DC : d_rt;
   const int dd = d * d;
   double *ub = u + dd, *ueta = u + 2 * dd + d;
   const double* uC = u + dd + d;  // symmetric: uC[k][i] = uC[i][k]
   const double* vAt = s.T1;       // v's A, transposed
-  const double *vb = v + dd, *veta = v + 2 * dd + d;
   const double* MinvT = s.S;
   for (int i = g.lane; i < d; i += g.size) {
     double acc = 0.0;
@@ -380,10 +379,15 @@ __device__ __forceinline__ void g_bc_vec_t(const Grp& g, int d_rt, double* u, co
   g.sync();
 }
 
-__device__ __noinline__ void g_bc_vec(const Grp& g, int d, double* u, const double* v,
-                                      const CombScratch& s) {
-  if (d == 16) g_bc_vec_t<16>(g, d, u, v, s);
-  else g_bc_vec_t<0>(g, d, u, v, s);
+// v's vectors (b, eta) at vb, veta: in the element, or staged by the caller
+__device__ __noinline__ void g_bc_vec2(const Grp& g, int d, double* u, const double* vb,
+                                       const double* veta, const CombScratch& s) {
+  if (d == 16) g_bc_vec_t<16>(g, d, u, vb, veta, s);
+  else g_bc_vec_t<0>(g, d, u, vb, veta, s);
+}
+__device__ __forceinline__ void g_bc_vec(const Grp& g, int d, double* u, const double* v,
+                                         const CombScratch& s) {
+  g_bc_vec2(g, d, u, v + d * d, v + 2 * d * d + d, s);
 }
 
 // vector-only steps taken (auxmc_test_fixed_point_steps)
@@ -1190,6 +1194,10 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
         g.sync();
       }
     }
+    // at the fixed point the next step's (b, eta) are loaded one step ahead into
+    // registers (lane i < d: its entries) and staged in cs.T2 (free in this form)
+    double pvb = 0.0, pve = 0.0;
+    bool pre = false;
     for (int t = lo;; ++t) {
       for (int i = g.lane; i < d; i += g.size)
         filt_mean[((size_t)b * (T + 1) + t) * d + i] = acc[dd + i];
@@ -1197,8 +1205,30 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
         filt_cov[((size_t)b * (T + 1) + t) * dd + i] = acc[dd + d + i];
       if (t + 1 >= hi) break;
       g.sync();
-      bc_chain_step(g, d, acc, base + (size_t)(t + 1) * ES, t + 1 >= same_lo && t + 1 < same_hi, o,
-                    cs, fixed, nvec, vsh);
+      const bool same1 = t + 1 >= same_lo && t + 1 < same_hi;
+      if (fixed && same1) {
+        const double* v1 = base + (size_t)(t + 1) * ES;
+        if (!pre && g.lane < d) {
+          pvb = v1[dd + g.lane];
+          pve = v1[2 * dd + d + g.lane];
+        }
+        if (g.lane < d) {
+          cs.T2[g.lane] = pvb;
+          cs.T2[d + g.lane] = pve;
+        }
+        pre = t + 2 < hi && t + 2 >= same_lo && t + 2 < same_hi;
+        if (pre && g.lane < d) {
+          const double* v2 = v1 + ES;
+          pvb = v2[dd + g.lane];
+          pve = v2[2 * dd + d + g.lane];
+        }
+        g.sync();
+        g_bc_vec2(g, d, acc, cs.T2, cs.T2 + d, cs);
+        ++nvec;
+      } else {
+        bc_chain_step(g, d, acc, base + (size_t)(t + 1) * ES, same1, o, cs, fixed, nvec, vsh);
+        pre = false;
+      }
     }
     if (g.lane == 0 && nvec) atomicAdd(&g_fp_steps, (unsigned long long)nvec);
     g.sync();
