@@ -1155,10 +1155,16 @@ __global__ void k_pfg_carry_seg(int nblk, int d, int B, int LB2, const double* _
   }
 }
 
+// per applied block: [flag, next step, b (d), C, Minv^T, vA^T (d*d each)] — a block
+// that reached the covariance fixed point hands its remaining steps to
+// k_pfg_apply_lanes
+__host__ __device__ inline int apply_rec_doubles(int d) { return 2 + d + 3 * d * d; }
+
 template <bool BLOCK>
 __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restrict__ el,
                             const double* __restrict__ carry, double* filt_mean, double* filt_cov,
-                            int k_lo, int k_hi, int same_lo, int same_hi, int shared_el) {
+                            int k_lo, int k_hi, int same_lo, int same_hi, int shared_el,
+                            double* recs) {
   extern __shared__ double smem[];
   const int ES = fe_size_g(d), dd = d * d;
   const Grp g = BLOCK ? block_group() : warp_group();
@@ -1179,6 +1185,7 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
     const double* vsh = shared_el ? base + (size_t)same_lo * ES : nullptr;
     bool fixed = false;
     int nvec = 0;
+    if (recs && g.lane == 0) recs[(size_t)qq * apply_rec_doubles(d)] = 0.0;
     if (k == 0) {
       g_copy(g, ES, base + (size_t)lo * ES, acc);
       g.sync();
@@ -1206,6 +1213,21 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
       if (t + 1 >= hi) break;
       g.sync();
       const bool same1 = t + 1 >= same_lo && t + 1 < same_hi;
+      if (recs && fixed && same1 && hi - 1 < same_hi) {
+        // every remaining step is a vector step: record the state and stop here
+        double* rc = recs + (size_t)qq * apply_rec_doubles(d);
+        for (int i = g.lane; i < d; i += g.size) rc[2 + i] = acc[dd + i];
+        for (int e = g.lane; e < dd; e += g.size) {
+          rc[2 + d + e] = acc[dd + d + e];
+          rc[2 + d + dd + e] = cs.S[e];
+          rc[2 + d + 2 * dd + e] = cs.T1[e];
+        }
+        if (g.lane == 0) {
+          rc[0] = 1.0;
+          rc[1] = (double)(t + 1);
+        }
+        break;
+      }
       if (fixed && same1) {
         const double* v1 = base + (size_t)(t + 1) * ES;
         if (!pre && g.lane < d) {
@@ -1223,7 +1245,8 @@ __global__ void k_pfg_apply(int T, int d, int B, int LB, const double* __restric
           pve = v2[2 * dd + d + g.lane];
         }
         g.sync();
-        g_bc_vec2(g, d, acc, cs.T2, cs.T2 + d, cs);
+        if (d == 16) g_bc_vec_t<16>(g, d, acc, cs.T2, cs.T2 + d, cs);  // inlined: no call frame
+        else g_bc_vec2(g, d, acc, cs.T2, cs.T2 + d, cs);
         ++nvec;
       } else {
         bc_chain_step(g, d, acc, base + (size_t)(t + 1) * ES, same1, o, cs, fixed, nvec, vsh);
@@ -1418,6 +1441,80 @@ int launch_reduce(const DevModel& dm, int B, int LB, const double* el, double* m
                  (int)std::min<long long>((n + kFillWarpsR - 1) / kFillWarpsR, 148LL * 32),
                  32 * kFillWarpsR, 0, s, T, d, B, LB, el, mats, agg, k_lo, k_hi);
   }
+  return AUXMC_OK;
+}
+
+// The remaining steps of every block k_pfg_apply recorded at the fixed point: a warp
+// per block advances b by g_bc_vec_t's three products in its order (same bits) from
+// shared-memory copies of the record, and writes the block's filtered moments — a
+// light kernel at full occupancy instead of the combine kernel's.  d <= 16.
+constexpr int kApplyLaneWarps = 8;
+__global__ void __launch_bounds__(kApplyLaneWarps * 32)
+    k_pfg_apply_lanes(int T, int d, int B, int LB, const double* __restrict__ el,
+                      const double* __restrict__ recs, double* filt_mean, double* filt_cov,
+                      int k_lo, int k_hi) {
+  extern __shared__ double asm_[];
+  const int ES = fe_size_g(d), dd = d * d;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* sm = asm_ + (size_t)w * (3 * dd + 4 * 16);
+  double *uC = sm, *MinvT = uC + dd, *vAt = MinvT + dd, *ub = vAt + dd, *tt = ub + 16,
+         *ww = tt + 16;
+  const int span = k_hi - k_lo;
+  const long long n = (long long)B * span;
+  for (long long qq = (long long)blockIdx.x * kApplyLaneWarps + w; qq < n;
+       qq += (long long)gridDim.x * kApplyLaneWarps) {
+    const double* rc = recs + (size_t)qq * apply_rec_doubles(d);
+    if (rc[0] == 0.0) continue;
+    const int b = (int)(qq / span), k = k_lo + (int)(qq % span);
+    const int lo = k * LB, hi = min(lo + LB, T + 1);
+    const int t0 = (int)rc[1];
+    if (lane == 0) atomicAdd(&g_fp_steps, (unsigned long long)(hi - t0));
+    for (int i = lane; i < d; i += 32) ub[i] = rc[2 + i];
+    for (int e = lane; e < dd; e += 32) {
+      uC[e] = rc[2 + d + e];
+      MinvT[e] = rc[2 + d + dd + e];
+      vAt[e] = rc[2 + d + 2 * dd + e];
+    }
+    __syncwarp();
+    const double* base = el + (size_t)b * (T + 1) * ES;
+    for (int t = t0; t < hi; ++t) {
+      const double* v = base + (size_t)t * ES;
+      const double *vb = v + dd, *veta = v + 2 * dd + d;
+      if (lane < d) {
+        double acc = 0.0;
+        for (int kk = 0; kk < d; ++kk) acc += uC[kk * d + lane] * veta[kk];
+        tt[lane] = acc + ub[lane];
+      }
+      __syncwarp();
+      if (lane < d) {
+        double acc = 0.0;
+        for (int kk = 0; kk < d; ++kk) acc += MinvT[kk * d + lane] * tt[kk];
+        ww[lane] = acc;
+      }
+      __syncwarp();
+      if (lane < d) {
+        double acc = 0.0;
+        for (int kk = 0; kk < d; ++kk) acc += vAt[kk * d + lane] * ww[kk];
+        ub[lane] = acc + vb[lane];
+        filt_mean[((size_t)b * (T + 1) + t) * d + lane] = ub[lane];
+      }
+      double* fc = filt_cov + ((size_t)b * (T + 1) + t) * dd;
+      for (int e = lane; e < dd; e += 32) fc[e] = uC[e];
+      __syncwarp();
+    }
+  }
+}
+
+int launch_apply_lanes(int T, int d, int B, int LB, const double* el, const double* recs,
+                       auxmc_filter_result* out, int k_lo, int k_hi, cudaStream_t s) {
+  const size_t sm = sizeof(double) * (size_t)kApplyLaneWarps * (3 * d * d + 64);
+  AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_pfg_apply_lanes,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  const long long n = (long long)B * (k_hi - k_lo);
+  AUXMC_LAUNCH(k_pfg_apply_lanes,
+               (int)std::min<long long>((n + kApplyLaneWarps - 1) / kApplyLaneWarps, 148LL * 16),
+               32 * kApplyLaneWarps, sm, s, T, d, B, LB, el, recs, out->filt_mean, out->filt_cov,
+               k_lo, k_hi);
   return AUXMC_OK;
 }
 
@@ -1686,12 +1783,14 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   double* proto = ws.take<double>((size_t)B * proto_doubles(d, dy));
   double* mats = ws.take<double>((size_t)B * rproto_doubles(d, LB));
   double* recs = ws.take<double>((size_t)B * ((T + kRecChunk) / kRecChunk) * rec_rec_doubles(dy));
+  double* arecs = ws.take<double>((size_t)B * nblk * apply_rec_doubles(d));
   const bool two = nblk > kPfTwoLevel;
   const int LB2 = pf_sup_g(T, LB), nsup = (nblk + LB2 - 1) / LB2;
   double* agg2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
   double* carry2 = two ? ws.take<double>((size_t)B * nsup * ES) : nullptr;
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!el || !agg || !carry || !terms || !proto || !mats || !recs || (two && (!agg2 || !carry2)))
+  if (!el || !agg || !carry || !terms || !proto || !mats || !recs || !arecs ||
+      (two && (!agg2 || !carry2)))
     return AUXMC_E_WORKSPACE;
   const KCfg ce = kcfg(k_pfg_elements<BLOCK>, d, dy, elem_smem(d, dy));
   const KCfg c2 = kcfg(k_pfg_reduce<BLOCK>, d, dy, scan_smem(d, 2));
@@ -1726,9 +1825,11 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
     AUXMC_LAUNCH(k_pfg_carry<BLOCK>, kgrid(cc, B), cc.threads, cc.smem, s, T, d, B, LB, agg, carry,
                  sr.agg_lo, sr.agg_hi);
   }
+  double* arecs_on = (!BLOCK && sr.el_hi > 0) ? arecs : nullptr;
   AUXMC_LAUNCH(k_pfg_apply<BLOCK>, kgrid(c3, nb), c3.threads, c3.smem, s, T, d, B, LB, el, carry,
                out->filt_mean, out->filt_cov, 0, nblk, sr.el_lo, sr.el_hi,
-               shared_el_reads(dm, BLOCK) ? 1 : 0);
+               shared_el_reads(dm, BLOCK) ? 1 : 0, arecs_on);
+  if (arecs_on) PFG_TRY(launch_apply_lanes(T, d, B, LB, el, arecs_on, out, 0, nblk, s));
   const long long nrc = (long long)B * ((T + kRecChunk) / kRecChunk);
   double* recs_on = (!BLOCK && sr.el_hi > 0) ? recs : nullptr;
   AUXMC_LAUNCH(k_pfg_recover<BLOCK>, kgrid(cr, nrc), cr.threads, cr.smem, s, dm, obs, B,
@@ -1771,7 +1872,7 @@ TsGeom ts_geom(int T) {
 }
 
 struct TsBufs {
-  double *el, *agg, *carry, *terms, *agg2, *carry2, *bnd, *proto, *mats, *recs;
+  double *el, *agg, *carry, *terms, *agg2, *carry2, *bnd, *proto, *mats, *recs, *arecs;
 };
 TsBufs ts_take(const DevModel& dm, Arena& ws) {
   const TsGeom G = ts_geom(dm.T);
@@ -1787,6 +1888,7 @@ TsBufs ts_take(const DevModel& dm, Arena& ws) {
   b.proto = ws.take<double>((size_t)proto_doubles(dm.dx, dm.dy));
   b.mats = ws.take<double>((size_t)rproto_doubles(dm.dx, G.LB));
   b.recs = ws.take<double>((size_t)((T + kRecChunk) / kRecChunk + 1) * rec_rec_doubles(dm.dy));
+  b.arecs = ws.take<double>((size_t)G.nblk * apply_rec_doubles(dm.dx));
   return b;
 }
 
@@ -1871,9 +1973,11 @@ int ts_filter_finish(const DevModel& dm, const double* obs, int j_lo, int j_hi, 
                b.carry2, sr.sup_lo, sr.sup_hi);
   AUXMC_LAUNCH(k_pfg_carry_seg<BLOCK>, kgrid(cg, j_hi - j_lo), cg.threads, cg.smem, s, G.nblk, d,
                1, G.LB2, b.agg, b.carry2, b.carry, j_lo, j_hi, sr.agg_lo, sr.agg_hi);
+  double* arecs_on = (!BLOCK && sr.el_hi > 0) ? b.arecs : nullptr;
   AUXMC_LAUNCH(k_pfg_apply<BLOCK>, kgrid(c3, k_hi - k_lo), c3.threads, c3.smem, s, T, d, 1, G.LB,
                b.el, b.carry, out->filt_mean, out->filt_cov, k_lo, k_hi, sr.el_lo, sr.el_hi,
-               shared_el_reads(dm, BLOCK) ? 1 : 0);
+               shared_el_reads(dm, BLOCK) ? 1 : 0, arecs_on);
+  if (arecs_on) PFG_TRY(launch_apply_lanes(T, d, 1, G.LB, b.el, arecs_on, out, k_lo, k_hi, s));
   const int jb_hi = std::min(j_hi + 1, G.nsup);  // owned super-blocks and the next one's start
   AUXMC_LAUNCH(k_ts_boundary, std::max(1, jb_hi - j_lo), 128, 0, s, d, j_lo, jb_hi, b.carry2,
                b.bnd);

@@ -24,7 +24,7 @@ for _ in range(iters):
 torch.cuda.synchronize()
 tot, cnt = ctypes.c_double(0.0), ctypes.c_longlong(0)
 names = ["k_pfg_elements", "k_pfg_elem_fill", "k_pfg_reduce_proto", "k_pfg_reduce_fill", "k_pfg_reduce<",
-         "k_pfg_carry", "k_pfg_apply", "k_pfg_recover<", "k_pfg_recover_lanes", "k_pfg_sum", "k_bwd_lean", "k_bwd_lanes", "k_pg_block_ops", "k_pg_block_offsets", "k_pg_carry", "k_pg_apply", "k_mma", "k_prefix",
+         "k_pfg_carry", "k_pfg_apply<", "k_pfg_apply_lanes", "k_pfg_recover<", "k_pfg_recover_lanes", "k_pfg_sum", "k_bwd_lean", "k_bwd_lanes", "k_pg_block_ops", "k_pg_block_offsets", "k_pg_carry", "k_pg_apply", "k_mma", "k_prefix",
          "k_path_terms", "k_gamma_terms", "k_build_aux", "k_grads", "k_aux"]
 out = {}
 for nm in names:
