@@ -185,10 +185,25 @@ __global__ void __launch_bounds__(32)
       At = O + (size_t)k * dd;
       a = OF + (size_t)k * d;
     }
-    for (int i = lane; i < d; i += 32) {
-      double s = 0.0;
-      for (int j = 0; j < d; ++j) s += At[j * d + i] * x[j];
-      xn[i] = s + a[i];
+    if (d == 16) {  // static bounds: the 16 operand pairs load before the FMA chain
+      if (lane < 16) {
+        double av[16], xv[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          av[j] = At[j * 16 + lane];
+          xv[j] = x[j];
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) s += av[j] * xv[j];
+        xn[lane] = s + a[lane];
+      }
+    } else {
+      for (int i = lane; i < d; i += 32) {
+        double s = 0.0;
+        for (int j = 0; j < d; ++j) s += At[j * d + i] * x[j];
+        xn[i] = s + a[i];
+      }
     }
     __syncwarp();
     if (tma && lane == 0 && k - kCarryStages >= 0) issue(k - kCarryStages, st);
