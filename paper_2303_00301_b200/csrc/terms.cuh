@@ -71,6 +71,38 @@ __device__ __forceinline__ double path_term_k(const DevModel& m, const double* _
     return y[i] - (s + cc[i]);
   };
   double sq = 0.0;
+  if (kind == 1 && !m.fst && dx == 16) {
+    // dense transition at d = 16: the row x_t loaded once into registers, the same
+    // products and solve in the same order (static bounds)
+    const double* F = m.Ft(t, b);
+    double xv[16], r[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) xv[jj] = x[(size_t)t * 16 + jj];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) s += F[i * 16 + jj] * xv[jj];
+      r[i] = x[(size_t)(t + 1) * 16 + i] - (s + bb[i]);
+    }
+    if (dg && dg[j]) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const double v = r[i] / L[i * 16 + i];
+        sq += v * v;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        double s = r[i];
+#pragma unroll
+        for (int jj = 0; jj < i; ++jj) s -= L[i * 16 + jj] * r[jj];
+        r[i] = s / L[i * 16 + i];
+        sq += r[i] * r[i];
+      }
+    }
+    return -0.5 * (nn * kLog2Pi + sq) - ld;
+  }
   if (dg && dg[j]) {
     for (int i = 0; i < nn; ++i) {
       const double v = res(i) / L[i * nn + i];
