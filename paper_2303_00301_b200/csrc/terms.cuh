@@ -134,8 +134,35 @@ __device__ __forceinline__ double gamma_term_k(const DevTarget& tg, const Factor
   }
   if (k <= T) {
     const int t = k - 1;
-    for (int i = 0; i < d; ++i) r[i] = x[(size_t)(t + 1) * d + i] - dyn_mean_i(tg, t, x + (size_t)t * d, i);
     const int jq = 1 + (fl.nQ > 1 ? t : 0);
+    if (tg.linear && d == 16) {
+      // d = 16 linear dynamics: dyn_mean_i and gauss_term's operations in their order,
+      // with the state row in registers and static bounds
+      const double* F = tg.Ft(t);
+      const double* bt = tg.bt(t);
+      const double* L = Ls + (size_t)jq * W * W;
+      double xv[16], rr[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) xv[j] = x[(size_t)t * 16 + j];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) s += F[i * 16 + j] * xv[j];
+        rr[i] = x[(size_t)(t + 1) * 16 + i] - (s + bt[i]);
+      }
+      double sq = 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        double s = rr[i];
+#pragma unroll
+        for (int j = 0; j < i; ++j) s -= L[i * 16 + j] * rr[j];
+        rr[i] = s / L[i * 16 + i];
+        sq += rr[i] * rr[i];
+      }
+      return -0.5 * (16 * kLog2Pi + sq) - logdet[jq];
+    }
+    for (int i = 0; i < d; ++i) r[i] = x[(size_t)(t + 1) * d + i] - dyn_mean_i(tg, t, x + (size_t)t * d, i);
     return gauss_term(d, r, Ls + (size_t)jq * W * W, logdet[jq]);
   }
   const int t = k - T - 1;
