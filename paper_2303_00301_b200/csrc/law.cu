@@ -16,7 +16,7 @@ namespace auxmc_gpu {
 int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, const double* pc,
                         int Bfr, double* elems, double* term, int* st_fr, int store_cov,
                         cudaStream_t stream, int t_lo = 0, int t_hi = -1,
-                        double* recs = nullptr);
+                        double* recs = nullptr, int* rep = nullptr);
 int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int fr_shared,
                         const auxmc_noise* noise, int B, int sampler, double* traj, int* status,
                         Arena& ws, cudaStream_t stream);

@@ -40,8 +40,16 @@ __device__ __forceinline__ void noise_vec(const NoiseArgs& nz, int c, int T, int
 }
 
 // pass 1: A_k for (fr, block k); smem per warp: 2 d*d
+// rep (nullable): rep[f T + t] = the element whose matrices (G, L) step t shares —
+// k_bwd_lanes writes only the offsets of a uniform chunk's later steps
+__device__ __forceinline__ const double* el_mat(const double* E, const int* rep, int T, int f, int t,
+                                                int ES) {
+  return E + (size_t)(rep ? rep[(size_t)f * T + t] : t) * ES;
+}
+
 __global__ void k_pg_block_ops(int T, int d, int Bfr, int Lb, int P, const double* __restrict__ elems,
-                               double* __restrict__ ops, int k_lo, int k_hi) {
+                               double* __restrict__ ops, int k_lo, int k_hi,
+                               const int* __restrict__ rep) {
   extern __shared__ double sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const long long item = (long long)blockIdx.x * nw + w;
@@ -55,10 +63,13 @@ __global__ void k_pg_block_ops(int T, int d, int Bfr, int Lb, int P, const doubl
   const double* E = elems + (size_t)f * T * ES;
   const Grp g = warp_group();
   // A = G_{e-1}
-  for (int i = lane; i < dd; i += 32) A[i] = E[(size_t)(e - 1) * ES + i];
+  {
+    const double* G = el_mat(E, rep, T, f, e - 1, ES);
+    for (int i = lane; i < dd; i += 32) A[i] = G[i];
+  }
   __syncwarp();
   for (int t = e - 2; t >= s; --t) {  // A := G_t A
-    g_dmma<false, false>(g, d, d, d, E + (size_t)t * ES, d, A, d, Bm, d, false, false);
+    g_dmma<false, false>(g, d, d, d, el_mat(E, rep, T, f, t, ES), d, A, d, Bm, d, false, false);
     __syncwarp();
     double* tmp = A;
     A = Bm;
@@ -73,7 +84,7 @@ __global__ void k_pg_block_ops(int T, int d, int Bfr, int Lb, int P, const doubl
 __global__ void k_pg_block_offsets(int T, int d, int B, int fr_shared, int Lb, int P,
                                    const double* __restrict__ elems, NoiseArgs nz,
                                    double* __restrict__ traj, double* __restrict__ offs, int k_lo,
-                                   int k_hi) {
+                                   int k_hi, const int* __restrict__ rep) {
   __shared__ double sv[kWarpsPG][3][64];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long item = (long long)blockIdx.x * kWarpsPG + w;
@@ -87,20 +98,22 @@ __global__ void k_pg_block_offsets(int T, int d, int B, int fr_shared, int Lb, i
   double* a = sv[w][1];
   double* an = sv[w][2];
   const int s = k * Lb, e = min(T, s + Lb);
+  const int f = fr_shared ? 0 : c;
   for (int t = e - 1; t >= s; --t) {
     const double* el = E + (size_t)t * ES;
+    const double* em = el_mat(E, rep, T, f, t, ES);
     noise_vec(nz, c, T, t, d, lane, xi);
     __syncwarp();
     for (int i = lane; i < d; i += 32) {
       double cv = 0.0;
-      for (int j = 0; j < d; ++j) cv += el[dd + d + i * d + j] * xi[j];
+      for (int j = 0; j < d; ++j) cv += em[dd + d + i * d + j] * xi[j];
       const double ct = el[dd + i] + cv;  // c~_t
       out[(size_t)t * d + i] = ct;
       if (t == e - 1) {
         an[i] = ct;
       } else {
         double ga = 0.0;
-        for (int j = 0; j < d; ++j) ga += el[i * d + j] * a[j];
+        for (int j = 0; j < d; ++j) ga += em[i * d + j] * a[j];
         an[i] = ga + ct;
       }
     }
@@ -225,7 +238,8 @@ int launch_pg_carry(int T, int d, int B, int fr_shared, int P, const double* ter
 // pass 4: x_t = G_t x_{t+1} + c~_t inside each block
 __global__ void k_pg_apply(int T, int d, int B, int fr_shared, int Lb, int P,
                            const double* __restrict__ elems, const double* __restrict__ xin,
-                           double* __restrict__ traj, int k_lo, int k_hi) {
+                           double* __restrict__ traj, int k_lo, int k_hi,
+                           const int* __restrict__ rep) {
   __shared__ double sv[kWarpsPG][2][64];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long item = (long long)blockIdx.x * kWarpsPG + w;
@@ -242,7 +256,7 @@ __global__ void k_pg_apply(int T, int d, int B, int fr_shared, int Lb, int P,
   __syncwarp();
   const int s = k * Lb, e = min(T, s + Lb);
   for (int t = e - 1; t >= s; --t) {
-    const double* el = E + (size_t)t * ES;
+    const double* el = el_mat(E, rep, T, fr_shared ? 0 : c, t, ES);
     for (int i = lane; i < d; i += 32) {
       double gx = 0.0;
       for (int j = 0; j < d; ++j) gx += el[i * d + j] * x[j];
@@ -264,7 +278,7 @@ int block_len(int T) { return prefix_block_len(T); }
 // elems/term from launch_bwd_elements (store_cov = 0: element holds chol(Λ)).
 int launch_prefix_generic(int T, int d, int B, int fr_shared, const double* elems,
                           const double* term, const NoiseArgs& nz, double* traj, Arena& ws,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, const int* rep) {
   if (d < 1 || d > 64) return AUXMC_E_DIM;
   const int Bfr = fr_shared ? 1 : B;
   const int Lb = block_len(T > 0 ? T : 1);
@@ -282,9 +296,9 @@ int launch_prefix_generic(int T, int d, int B, int fr_shared, const double* elem
         cudaFuncSetAttribute(k_pg_block_ops, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const long long nops = (long long)Bfr * P, nvec = (long long)B * P;
     AUXMC_LAUNCH(k_pg_block_ops, (int)((nops + wo - 1) / wo), 32 * wo, smem, stream, T, d, Bfr,
-                 Lb, P, elems, ops, 0, P);
+                 Lb, P, elems, ops, 0, P, rep);
     AUXMC_LAUNCH(k_pg_block_offsets, (int)((nvec + kWarpsPG - 1) / kWarpsPG), 32 * kWarpsPG, 0,
-                 stream, T, d, B, fr_shared, Lb, P, elems, nz, traj, offs, 0, P);
+                 stream, T, d, B, fr_shared, Lb, P, elems, nz, traj, offs, 0, P, rep);
   }
   {
     const int rc = launch_pg_carry(T, d, B, fr_shared, P, term, ops, offs, nz, traj, xin, nullptr,
@@ -294,7 +308,7 @@ int launch_prefix_generic(int T, int d, int B, int fr_shared, const double* elem
   if (T > 0) {
     const long long nvec = (long long)B * P;
     AUXMC_LAUNCH(k_pg_apply, (int)((nvec + kWarpsPG - 1) / kWarpsPG), 32 * kWarpsPG, 0, stream, T,
-                 d, B, fr_shared, Lb, P, elems, xin, traj, 0, P);
+                 d, B, fr_shared, Lb, P, elems, xin, traj, 0, P, rep);
   }
   return AUXMC_OK;
 }
@@ -310,7 +324,7 @@ int launch_prefix_generic(int T, int d, int B, int fr_shared, const double* elem
 // blocks (every rank, same bits) and expands the rank's blocks.
 int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, const double* pc,
                         int Bfr, double* elems, double* term, int* st_fr, int store_cov,
-                        cudaStream_t stream, int t_lo, int t_hi, double* recs);
+                        cudaStream_t stream, int t_lo, int t_hi, double* recs, int* rep);
 
 namespace {
 struct TsPrefixBufs {
@@ -374,7 +388,7 @@ int tshard_prefix_local(const DevModel& dm, const double* fm, const double* fc, 
   AUXMC_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), stream));
   // elements for steps [t_lo, min(t_hi, T)) and the terminal law when T is owned
   int rc = launch_bwd_elements(dm, fm, fc, pc, 1, b.elems, b.term, status, 0, stream, t_lo, t_hi,
-                               b.recs);
+                               b.recs, nullptr);
   if (rc) return rc;
   const int s_hi = std::min(t_hi, T);
   if (s_hi > t_lo) {
@@ -385,9 +399,9 @@ int tshard_prefix_local(const DevModel& dm, const double* fm, const double* fc, 
         cudaFuncSetAttribute(k_pg_block_ops, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int nk = k_hi - k_lo;
     AUXMC_LAUNCH(k_pg_block_ops, (nk + wo - 1) / wo, 32 * wo, smem, stream, T, d, 1, Lb, P,
-                 b.elems, b.ops, k_lo, k_hi);
+                 b.elems, b.ops, k_lo, k_hi, (const int*)nullptr);
     AUXMC_LAUNCH(k_pg_block_offsets, (nk + kWarpsPG - 1) / kWarpsPG, 32 * kWarpsPG, 0, stream, T, d,
-                 1, 1, Lb, P, b.elems, nz, traj, b.offs, k_lo, k_hi);
+                 1, 1, Lb, P, b.elems, nz, traj, b.offs, k_lo, k_hi, (const int*)nullptr);
     AUXMC_LAUNCH(k_tsp_pack, 64, 256, 0, stream, d, k_lo, k_hi, b.ops, b.offs, blk_out);
   }
   if (t_hi == T + 1) {  // x_T = m_T + L_T xi on the rank that owns T
@@ -419,7 +433,7 @@ int tshard_prefix_finish(const DevModel& dm, const NoiseArgs& nz, int t_lo, int 
   if (s_hi > t_lo) {
     const int k_lo = t_lo / Lb, k_hi = (s_hi + Lb - 1) / Lb;
     AUXMC_LAUNCH(k_pg_apply, (k_hi - k_lo + kWarpsPG - 1) / kWarpsPG, 32 * kWarpsPG, 0, stream, T,
-                 d, 1, 1, Lb, P, b.elems, b.xin, traj, k_lo, k_hi);
+                 d, 1, 1, Lb, P, b.elems, b.xin, traj, k_lo, k_hi, (const int*)nullptr);
   }
   return AUXMC_OK;
 }

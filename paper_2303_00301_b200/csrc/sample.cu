@@ -216,7 +216,7 @@ __host__ __device__ inline int bwd_lean_doubles(int d) {
 __global__ void __launch_bounds__(kBwdLeanThreads, BWD_LEAN_MINB)
 k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __restrict__ filt_cov,
            const double* __restrict__ pred_cov, int Bfr, double* elems, double* term,
-           int* status, int store_cov, int t_lo, int t_hi, int reuse, double* recs) {
+           int* status, int store_cov, int t_lo, int t_hi, int reuse, double* recs, int* rep) {
   extern __shared__ double smem[];
   const int d = m.dx, dd = d * d, T = m.T;
   const bool flip = g_flip_backward_gain != 0;
@@ -310,6 +310,7 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
       continue;
     }
     double* out = elems + ((size_t)b * T + t) * elem_stride(d);
+    if (rep && g.lane == 0) rep[(size_t)b * T + t] = t;  // this element holds its own matrices
     const double* S = pc + (size_t)(t + 1) * dd;
     const bool stamp = AUXMC_BWD_EXP == 9 && blockIdx.x == 0 && item == 0;
     (void)stamp;
@@ -449,7 +450,7 @@ k_bwd_lean(DevModel m, const double* __restrict__ filt_mean, const double* __res
 constexpr int kBwdLaneWarps = 8;
 __global__ void __launch_bounds__(kBwdLaneWarps * 32)
     k_bwd_lanes(DevModel m, const double* __restrict__ filt_mean, int Bfr, double* elems,
-                int* status, int t_lo, int t_hi, const double* __restrict__ recs) {
+                int* status, int t_lo, int t_hi, const double* __restrict__ recs, int* rep) {
   constexpr int MX = 16;
   const int d = m.dx, dd = d * d, T = m.T, es = elem_stride(d);
   const int lane = threadIdx.x & 31;
@@ -464,11 +465,15 @@ __global__ void __launch_bounds__(kBwdLaneWarps * 32)
     const int st = (int)recs[2 * unit + 1];
     if (st && lane == 0) atomicMax(status + b, st);
     const double* src = elems + ((size_t)b * T + c0) * es;
-    for (int u = c0 + 1; u < c1; ++u) {
-      double* o = elems + ((size_t)b * T + u) * es;
-      for (int e = lane; e < dd; e += 32) {
-        o[e] = src[e];
-        o[dd + d + e] = src[dd + d + e];
+    if (rep) {  // the sampler reads these steps' matrices from item c0's element
+      for (int u = c0 + 1 + lane; u < c1; u += 32) rep[(size_t)b * T + u] = c0;
+    } else {
+      for (int u = c0 + 1; u < c1; ++u) {
+        double* o = elems + ((size_t)b * T + u) * es;
+        for (int e = lane; e < dd; e += 32) {
+          o[e] = src[e];
+          o[dd + d + e] = src[dd + d + e];
+        }
       }
     }
     const double* F = m.Ft(0, b);
@@ -1015,7 +1020,7 @@ int launch_dnc(const DevModel& dm, int Bfr, int fr_shared, const double* elems,
                int* st_fr, cudaStream_t stream);
 int launch_prefix_generic(int T, int d, int B, int fr_shared, const double* elems,
                           const double* term, const NoiseArgs& nz, double* traj, Arena& ws,
-                          cudaStream_t stream);
+                          cudaStream_t stream, const int* rep);
 
 namespace {
 
@@ -1075,7 +1080,7 @@ int run_sampler(int sampler, int T, int B, int fr_shared, const double* elems,
 int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, const double* pc,
                         int Bfr, double* elems, double* term, int* st_fr, int store_cov,
                         cudaStream_t stream, int t_lo = 0, int t_hi = -1,
-                        double* recs = nullptr) {
+                        double* recs = nullptr, int* rep = nullptr) {
   const int d = dm.dx;
   const int per_blk = bwd_buffers(dm.fst != 0) * d * d + 4 * d + 4;  // CTA items: F from global
   const int per = bwd_buffers(true) * d * d + 4 * d + 4;       // warp items: F staged
@@ -1101,13 +1106,15 @@ int launch_bwd_elements(const DevModel& dm, const double* fm, const double* fc, 
     const int grid = (int)std::min<long long>(n_items, 148LL * 64);
     const int reuse = g_bwd_reuse && !dm.fst && dm.nF <= 1;
     double* recs_on = (reuse && d <= 16) ? recs : nullptr;  // k_bwd_lanes: d <= 16
+    int* rep_on = rep;  // every item k_bwd_lean takes points at itself
     AUXMC_LAUNCH(k_bwd_lean, grid, kBwdLeanThreads, smem, stream, dm, fm, fc, pc, Bfr, elems, term,
-                 st_fr, store_cov, t_lo, t_hi, reuse, recs_on);
+                 st_fr, store_cov, t_lo, t_hi, reuse, recs_on, rep_on);
     if (recs_on) {
       const long long nu = (long long)Bfr * ((t_hi - t_lo + kBwdChunk - 1) / kBwdChunk);
       AUXMC_LAUNCH(k_bwd_lanes,
                    (int)std::min<long long>((nu + kBwdLaneWarps - 1) / kBwdLaneWarps, 148LL * 32),
-                   32 * kBwdLaneWarps, 0, stream, dm, fm, Bfr, elems, st_fr, t_lo, t_hi, recs_on);
+                   32 * kBwdLaneWarps, 0, stream, dm, fm, Bfr, elems, st_fr, t_lo, t_hi, recs_on,
+                   rep_on);
     }
     (void)per_blk;
   } else {
@@ -1132,6 +1139,10 @@ int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int f
   double* term = ws.take<double>((size_t)Bfr * term_stride(d));
   int* st_fr = ws.take<int>((size_t)Bfr);
   double* recs = ws.take<double>(bwd_recs_doubles(Bfr, T + 1));
+  // the generic prefix sampler reads each step's matrices through rep (filled by the
+  // CTA Schur-form elements, d >= BWD_LEAN_MIN_D), so uniform chunks skip the copies
+  const bool use_rep = sampler == AUXMC_SAMPLER_PREFIX && d > 8 && d >= BWD_LEAN_MIN_D && d <= 64;
+  int* rep = use_rep ? ws.take<int>((size_t)Bfr * (T > 0 ? T : 1)) : nullptr;
   NoiseArgs nz{};
   if (noise) {
     nz.kind = noise->kind;
@@ -1142,10 +1153,11 @@ int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int f
     nz.n_bridge = noise->n_bridge;
   }
   if (ws.base != nullptr) {
-    if (!elems || !term || !st_fr || !recs) return AUXMC_E_WORKSPACE;
+    if (!elems || !term || !st_fr || !recs || (use_rep && !rep)) return AUXMC_E_WORKSPACE;
     AUXMC_CUDA_TRY(cudaMemsetAsync(st_fr, 0, sizeof(int) * Bfr, stream));
     int rc = launch_bwd_elements(dm, fr->filt_mean, fr->filt_cov, fr->pred_cov, Bfr, elems, term,
-                                 st_fr, sampler == AUXMC_SAMPLER_DNC ? 1 : 0, stream, 0, -1, recs);
+                                 st_fr, sampler == AUXMC_SAMPLER_DNC ? 1 : 0, stream, 0, -1, recs,
+                                 rep);
     if (rc) return rc;
   }
   int rc = AUXMC_OK;
@@ -1161,7 +1173,7 @@ int launch_sample_paths(const DevModel& dm, const auxmc_filter_result* fr, int f
         if (d > 64) {
           rc = AUXMC_E_DIM;
         } else if (sampler == AUXMC_SAMPLER_PREFIX) {
-          rc = launch_prefix_generic(T, d, B, fr_shared, elems, term, nz, traj, ws, stream);
+          rc = launch_prefix_generic(T, d, B, fr_shared, elems, term, nz, traj, ws, stream, rep);
         } else if (ws.base != nullptr) {
           const long long es = fr_shared ? 0 : (long long)T * elem_stride(d);
           const long long ts = fr_shared ? 0 : term_stride(d);
