@@ -1807,7 +1807,6 @@ int run_pfg(const DevModel& dm, const double* obs, int B, auxmc_filter_result* o
   PFG_TRY(set_smem(k_pfg_apply<BLOCK>, c3));
   PFG_TRY(set_smem(k_pfg_recover<BLOCK>, cr));
   if (status) AUXMC_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int) * B, s));
-  const long long n = (long long)B * (T + 1);
   const long long nb = (long long)B * nblk;
   const SameRanges sr = same_ranges(dm, LB, LB2);
   ProtoJob pj{LB, mats, cp, false};
