@@ -53,3 +53,18 @@ def test_sizes_are_host_computable(lib):
         assert n > 0
     assert lib.auxmc_dnc_bridge_count(65536) == 65536
     assert lib.auxmc_dnc_bridge_count(5) == 8
+
+
+@pytest.mark.parametrize("T", [1, 7, 300, 3000, 4095, 65536, 1 << 20, (1 << 20) + 5])
+def test_time_shard_geometry_nests_sampler_blocks(lib, T):
+    """The scan filter's super-blocks hold whole prefix-sampler blocks (a time-sharded
+    rank's range is a run of super-blocks, tshard.ShardedPrefixSampler), and the
+    block tree covers the horizon.  Host-computable, no device."""
+    LB, nblk, nsup, SB, ed = (ctypes.c_int() for _ in range(5))
+    assert lib.auxmc_tshard_geometry(T, 16, *(ctypes.byref(x) for x in (LB, nblk, nsup, SB, ed))) == 0
+    Lb, P = ctypes.c_int(), ctypes.c_int()
+    assert lib.auxmc_tshard_prefix_geometry(T, ctypes.byref(Lb), ctypes.byref(P)) == 0
+    assert SB.value % Lb.value == 0, (SB.value, Lb.value)
+    assert nblk.value * LB.value >= T + 1 > (nblk.value - 1) * LB.value
+    assert nsup.value * SB.value >= T + 1
+    assert P.value * Lb.value >= T
