@@ -46,8 +46,10 @@ static int g_force_generic_filter = 0;
 // log p(z) of every aux step (nullptr: off) — the parity tests compare filters directly.
 static double* g_capture_lm = nullptr;
 
+// dgf (nullable): per factor, 1 when it is diagonal to the bit (gauss_term's dense
+// solve then reduces to its diagonal terms, gamma_term_k)
 __global__ void k_target_factors(DevTarget tg, FactorLayout fl, double* Ls, double* logdet,
-                                 int* status) {
+                                 int* status, unsigned char* dgf = nullptr) {
   extern __shared__ double smem[];
   const int W = fl.W;
   Grp g = warp_group();
@@ -71,7 +73,13 @@ __global__ void k_target_factors(DevTarget tg, FactorLayout fl, double* Ls, doub
     g.sync();
     const int st = g_factor_psd(g, n, A, L, scr, flag, red);
     double* out = Ls + (size_t)j * W * W;
-    for (int i = g.lane; i < n * n; i += g.size) out[i] = L[i];
+    bool offz = true;
+    for (int i = g.lane; i < n * n; i += g.size) {
+      out[i] = L[i];
+      if (i / n != i % n && L[i] != 0.0) offz = false;
+    }
+    offz = __all_sync(0xffffffffu, offz);
+    if (dgf && g.lane == 0) dgf[j] = offz ? 1 : 0;
     if (g.lane == 0) {
       double ld = 0.0;
       for (int i = 0; i < n; ++i) ld += log(L[i * n + i]);
@@ -85,14 +93,14 @@ __global__ void k_target_factors(DevTarget tg, FactorLayout fl, double* Ls, doub
 // log γ terms (target.cpp:100-108): k = 0 prior, 1..T dynamics, T+1.. potentials
 __global__ void k_gamma_terms(DevTarget tg, FactorLayout fl, int C, const double* __restrict__ traj,
                               const double* __restrict__ Ls, const double* __restrict__ logdet,
-                              double* terms) {
+                              double* terms, const unsigned char* __restrict__ dgf) {
   const int T = tg.T, d = tg.dx;
   const int K = 2 * T + 2;
   const long long n = (long long)C * K;
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
        q += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(q / K), k = (int)(q % K);
-    terms[q] = gamma_term_k(tg, fl, traj + (size_t)c * (T + 1) * d, Ls, logdet, k);
+    terms[q] = gamma_term_k(tg, fl, traj + (size_t)c * (T + 1) * d, Ls, logdet, k, dgf);
   }
 }
 
@@ -331,17 +339,18 @@ static int launch_log_gamma(const DevTarget& tg, int C, const double* traj, doub
   double* logdet = ws.take<double>(fl.total());
   double* terms = ws.take<double>((size_t)C * (2 * tg.T + 2));
   int* fst = ws.take<int>(1);
+  unsigned char* dgf = ws.take<unsigned char>(fl.total());
   if (ws.base == nullptr) return AUXMC_OK;
-  if (!Ls || !logdet || !terms || !fst) return AUXMC_E_WORKSPACE;
+  if (!Ls || !logdet || !terms || !fst || !dgf) return AUXMC_E_WORKSPACE;
   AUXMC_CUDA_TRY(cudaMemsetAsync(fst, 0, sizeof(int), s));
   const int warps = factor_warps(fl.W);
   const size_t smem = sizeof(double) * (3 * fl.W * fl.W + 4) * warps;
   AUXMC_CUDA_TRY(cudaFuncSetAttribute(k_target_factors,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   AUXMC_LAUNCH(k_target_factors, (fl.total() + warps - 1) / warps, 32 * warps, smem, s, tg, fl, Ls,
-               logdet, fst);
+               logdet, fst, dgf);
   AUXMC_LAUNCH(k_gamma_terms, grid_for((long long)C * (2 * tg.T + 2), 128), 128, 0, s, tg, fl, C,
-               traj, Ls, logdet, terms);
+               traj, Ls, logdet, terms, dgf);
   PFG_SUM_PARTS(C, 2LL * tg.T + 2, terms);
   AUXMC_LAUNCH(k_gamma_sum, C, kSumThreads, 0, s, tg.T, C, terms, fst, out, status, parts);
   if (parts) cudaFreeAsync(parts, s);

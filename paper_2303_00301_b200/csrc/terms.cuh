@@ -125,12 +125,27 @@ __device__ __forceinline__ double path_term_k(const DevModel& m, const double* _
 __device__ __forceinline__ double gamma_term_k(const DevTarget& tg, const FactorLayout& fl,
                                                const double* __restrict__ x,
                                                const double* __restrict__ Ls,
-                                               const double* __restrict__ logdet, int k) {
+                                               const double* __restrict__ logdet, int k,
+                                               const unsigned char* __restrict__ dgf = nullptr) {
   const int T = tg.T, d = tg.dx, W = fl.W;
+  // a factor diagonal to the bit: gauss_term's dense solve subtracts only exact zeros
+  // (each s - 0 r_j is s, r_j finite), so its value is the diagonal terms' own
+  auto gterm = [&](int n, double* r, int jf) -> double {
+    const double* L = Ls + (size_t)jf * W * W;
+    if (dgf && dgf[jf]) {
+      double sq = 0.0;
+      for (int i = 0; i < n; ++i) {
+        r[i] = r[i] / L[i * n + i];
+        sq += r[i] * r[i];
+      }
+      return -0.5 * (n * kLog2Pi + sq) - logdet[jf];
+    }
+    return gauss_term(n, r, L, logdet[jf]);
+  };
   double r[64];
   if (k == 0) {
     for (int i = 0; i < d; ++i) r[i] = x[i] - tg.m0[i];
-    return gauss_term(d, r, Ls, logdet[0]);
+    return gterm(d, r, 0);
   }
   if (k <= T) {
     const int t = k - 1;
@@ -163,7 +178,7 @@ __device__ __forceinline__ double gamma_term_k(const DevTarget& tg, const Factor
       return -0.5 * (16 * kLog2Pi + sq) - logdet[jq];
     }
     for (int i = 0; i < d; ++i) r[i] = x[(size_t)(t + 1) * d + i] - dyn_mean_i(tg, t, x + (size_t)t * d, i);
-    return gauss_term(d, r, Ls + (size_t)jq * W * W, logdet[jq]);
+    return gterm(d, r, jq);
   }
   const int t = k - T - 1;
   const double* xt = x + (size_t)t * d;
@@ -178,7 +193,7 @@ __device__ __forceinline__ double gamma_term_k(const DevTarget& tg, const Factor
       r[i] = y[i] - (s + cc[i]);
     }
     const int je = 1 + fl.nQ + (tg.ne > 1 ? t : 0);
-    lp += gauss_term(tg.q, r, Ls + (size_t)je * W * W, logdet[je]);
+    lp += gterm(tg.q, r, je);
   }
   if (tg.gmask[t]) {
     const int jg = 1 + fl.nQ + fl.nE + (tg.ne > 1 ? t : 0);
