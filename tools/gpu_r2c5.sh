@@ -1,3 +1,5 @@
-timeout 300 python tools/c3_kernels.py 4096 256 3 2>&1 | head -8
-timeout 300 python tools/c5_kernels.py 1048576 3 2>&1 | grep -E "iteration|k_gamma"
-timeout 2400 python -m pytest tests -q -m gpu -x 2>&1 | tail -2
+mkdir -p gpurun_out/rc
+python tools/c5_kernels.py 65536 1 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_pfg_recover" -s 2 -c 1 -o gpurun_out/rc/rec python tools/c5_kernels.py 65536 1 > gpurun_out/rc/ncu.log 2>&1
+ncu -i gpurun_out/rc/rec.ncu-rep --page source --csv --print-source sass > gpurun_out/rc/src.csv 2>&1
+ncu -i gpurun_out/rc/rec.ncu-rep --page raw --csv > gpurun_out/rc/raw.csv 2>&1
+rm -f gpurun_out/rc/rec.ncu-rep; ls -la gpurun_out/rc
